@@ -1,0 +1,186 @@
+/* rotavote_b200 -- C-ABI of the B200-native spatial-voting path (arXiv 2502.06337).
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no CUDA/torch types. Each entry
+ * point replaces one function of the reference library "rotavote" (C++20, CPU only,
+ * /root/reference/proj); the reference signature it replaces is cited next to it
+ * (file:line under proj/). Arrays follow the reference's memory layout:
+ *   - correspondences: n x 6 doubles, row i = (x0 x1 x2 y0 y1 y2)  == span<const Correspondence>
+ *     (Correspondence = {Eigen::Vector3d x, y}, angles.hpp:11-14: 48 B, no padding)
+ *   - constraints:     n x 3 doubles                             == span<const Vec3>
+ *   - vote grid:       grid*grid uint32, row-major counts[iy*grid + ix]  (voting.hpp:14-39)
+ *   - matrices:        3x3 row-major doubles
+ * Errors: every call returns rv_status. The reference throws typed exceptions
+ * (errors.hpp:8-55); the C++ drop-in headers (include/rotavote/) rethrow the same types.
+ *
+ * Host-buffer entry points copy inputs to the device (H2D) and results back (D2H) inside
+ * the call; *_device variants take device pointers already resident in HBM.
+ * A context is not thread-safe: use one context per host thread (the reference estimator is
+ * stateless; contexts keep that property per thread).
+ */
+#ifndef ROTAVOTE_B200_H
+#define ROTAVOTE_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RV_ABI_VERSION 1
+
+typedef enum rv_status {
+  RV_OK = 0,
+  RV_ERR_EMPTY_INPUT = 1,           /* rotavote::EmptyInput */
+  RV_ERR_NO_PEAK = 2,               /* rotavote::NoPeak */
+  RV_ERR_DEGENERATE_PROJECTION = 3, /* rotavote::DegenerateProjection */
+  RV_ERR_NO_VOTES = 4,              /* rotavote::NoVotes */
+  RV_ERR_ALL_DEGENERATE = 5,        /* rotavote::AllDegenerate */
+  RV_ERR_RANK_DEFICIENT = 6,        /* rotavote::RankDeficient */
+  RV_ERR_NO_CONSENSUS = 7,          /* rotavote::NoConsensus */
+  RV_ERR_INVALID_CONFIG = 8,        /* rotavote::InvalidConfig */
+  RV_ERR_POLE_PROXIMITY = 9,        /* rotavote::PoleProximity */
+  RV_ERR_OUT_OF_MEMORY = 10,
+  RV_ERR_CUDA = 11,                 /* CUDA runtime failure (message in rv_context_last_error) */
+  RV_ERR_NCCL = 12,
+  RV_ERR_INVALID_ARGUMENT = 13,
+  RV_ERR_NO_DEVICE = 14
+} rv_status;
+
+/* EstimatorConfig, estimator.hpp:13-29 -- same fields, same defaults (rv_config_default). */
+typedef struct rv_config {
+  int32_t grid;                /* accumulator resolution G (512) */
+  double extent;               /* accumulator half-width E (1.05) */
+  int32_t theta_samples;       /* circle samples J (2048) */
+  double epsilon;              /* inlier threshold on |axis . z| (0.015) */
+  int32_t angle_bins;          /* 1024 */
+  int32_t max_models;          /* 1 */
+  double min_votes_frac;       /* 0.02 */
+  double consensus_floor_mult; /* 1.5 */
+  double dedupe_overlap;       /* 0.5 */
+  double tau_z;                /* 1e-9 */
+  double tau_deg;              /* 1e-6 */
+  int32_t suppression_radius;  /* 8 */
+  int32_t refine;              /* 1 */
+  int32_t normalize_inputs;    /* 1 */
+  int32_t threads;             /* accepted for API parity; the device path ignores it */
+} rv_config;
+
+/* Peak, voting.hpp:41-46 (center = cell center (A, B)). */
+typedef struct rv_peak {
+  int32_t ix, iy;
+  double A, B;
+  uint32_t votes;
+} rv_peak;
+
+/* RotationEstimate, estimator.hpp:31-38. Inliers are fetched with rv_result_inliers. */
+typedef struct rv_estimate {
+  double axis[3];
+  double angle;
+  double rotation[9];
+  uint32_t axis_votes;
+  int64_t n_inliers;
+  double elapsed_s;
+} rv_estimate;
+
+/* Device time of each stage of the last call (CUDA events on the context stream; only
+ * filled when timing is enabled). Used by bench.py for the roofline. */
+typedef struct rv_stage_times {
+  double preprocess_ms; /* K1: preprocess + basis + band plan */
+  double vote_ms;       /* K2: band-tiled vote (+ tile reduction) */
+  double peaks_ms;      /* K3: argmax / NMS / blur */
+  double refine_ms;     /* K4: classify + scatter + eigen loop */
+  double angles_ms;     /* K4: angle histogram + circular mean + model support */
+  double total_ms;
+  int64_t vote_pairs;       /* sample pairs evaluated by the vote kernel (work incl. padding) */
+  int64_t vote_samples;     /* algorithmic samples N_kept * J of all vote launches */
+  int32_t vote_launches;    /* vote kernel launches in the call */
+  int32_t kernel_launches;  /* all kernels launched by the call */
+} rv_stage_times;
+
+typedef struct rv_context rv_context;
+
+/* ---- context ---------------------------------------------------------------------- */
+void rv_config_default(rv_config* cfg);
+const char* rv_status_string(rv_status st);
+int32_t rv_abi_version(void);
+rv_status rv_context_create(int32_t device, rv_context** out);
+void rv_context_destroy(rv_context* ctx);
+/* Run on an external CUDA stream (cudaStream_t as void*); NULL = the context's own stream. */
+rv_status rv_context_set_stream(rv_context* ctx, void* cuda_stream);
+const char* rv_context_last_error(const rv_context* ctx);
+rv_status rv_context_enable_timing(rv_context* ctx, int32_t enable);
+rv_status rv_context_stage_times(const rv_context* ctx, rv_stage_times* out);
+
+/* ---- solver API (the drop-in for estimate_single / estimate_multi) ------------------ */
+/* RotationEstimate estimate_single(span<const Correspondence>, const EstimatorConfig&)
+ * -- estimator.hpp:63-64, estimator.cpp:320-371 */
+rv_status rv_estimate_single(rv_context* ctx, const double* corrs, int64_t n, const rv_config* cfg,
+                             rv_estimate* out);
+rv_status rv_estimate_single_device(rv_context* ctx, const double* d_corrs, int64_t n,
+                                    const rv_config* cfg, rv_estimate* out);
+/* vector<RotationEstimate> estimate_multi(span<const Correspondence>, const EstimatorConfig&)
+ * -- estimator.hpp:69-70, estimator.cpp:373-493 (sequential extraction, sorted by votes) */
+rv_status rv_estimate_multi(rv_context* ctx, const double* corrs, int64_t n, const rv_config* cfg,
+                            rv_estimate* out, int32_t capacity, int32_t* n_models);
+rv_status rv_estimate_multi_device(rv_context* ctx, const double* d_corrs, int64_t n,
+                                   const rv_config* cfg, rv_estimate* out, int32_t capacity,
+                                   int32_t* n_models);
+/* Inliers (ascending input indices) of model `model` of the last estimate call. */
+rv_status rv_result_inliers(rv_context* ctx, int32_t model, int32_t* dst, int64_t capacity);
+
+/* ---- path functions (voting.hpp / estimator.hpp / angles.hpp) ----------------------- */
+/* PreprocessResult preprocess(span<const Correspondence>, double tau_z, bool normalize)
+ * -- estimator.hpp:47-48, estimator.cpp:259-285. Outputs sized >= n. */
+rv_status rv_preprocess(rv_context* ctx, const double* corrs, int64_t n, double tau_z,
+                        int32_t normalize, double* constraints_out, int32_t* kept_out,
+                        int32_t* dropped_out, int64_t* n_kept, int64_t* n_dropped);
+/* Accumulator2D accumulate(span<const Vec3>, int grid, double extent, int samples, int threads)
+ * -- voting.hpp:64-65, voting.cpp:88-118. Bit-exact with the reference for every config. */
+rv_status rv_accumulate(rv_context* ctx, const double* constraints, int64_t n, int32_t grid,
+                        double extent, int32_t samples, uint32_t* counts_out);
+rv_status rv_accumulate_device(rv_context* ctx, const double* d_constraints, int64_t n,
+                               int32_t grid, double extent, int32_t samples, uint32_t* d_counts);
+/* void deposit_circle_votes(const Vec3& z, Accumulator2D& acc, int samples)
+ * -- voting.hpp:60, voting.cpp:83-86. counts is read, incremented, written back. */
+rv_status rv_deposit_circle_votes(rv_context* ctx, const double z[3], uint32_t* counts,
+                                  int32_t grid, double extent, int32_t samples);
+/* PeakSet find_peaks(const Accumulator2D&, int max_peaks, int radius, uint32_t min_votes)
+ * -- voting.hpp:70-71, voting.cpp:120-170. out sized >= max_peaks. */
+rv_status rv_find_peaks(rv_context* ctx, const uint32_t* counts, int32_t grid, double extent,
+                        int32_t max_peaks, int32_t radius, uint32_t min_votes, rv_peak* out,
+                        int32_t* n_out);
+/* Peak blurred_argmax(const Accumulator2D&, int radius) -- voting.hpp:80, voting.cpp:176-216 */
+rv_status rv_blurred_argmax(rv_context* ctx, const uint32_t* counts, int32_t grid, double extent,
+                            int32_t radius, rv_peak* out);
+/* vector<int> classify_inliers(const Vec3&, span<const Vec3>, double) -- estimator.hpp:51-52 */
+rv_status rv_classify_inliers(rv_context* ctx, const double axis[3], const double* constraints,
+                              int64_t n, double epsilon, int32_t* out, int64_t* n_out);
+/* Vec3 refine_axis(span<const Vec3>) -- estimator.hpp:57, estimator.cpp:299-309 */
+rv_status rv_refine_axis(rv_context* ctx, const double* constraints, int64_t n, double axis_out[3]);
+/* AngleHistogram vote_angles(axis, span<const Correspondence>, span<const int>, bins, tau)
+ * -- angles.hpp:37-40, angles.cpp:46-68. raw_angles_out sized >= n_idx (insertion order). */
+rv_status rv_vote_angles(rv_context* ctx, const double axis[3], const double* corrs, int64_t n_corrs,
+                         const int32_t* indices, int64_t n_idx, int32_t bin_count, double tau,
+                         uint32_t* bins_out, uint64_t* contributing, uint64_t* degenerate,
+                         double* raw_angles_out);
+/* double peak_angle(const AngleHistogram&, bool refine, span<const double>) -- angles.hpp:44-45 */
+rv_status rv_peak_angle(rv_context* ctx, const uint32_t* bins, int32_t bin_count,
+                        uint64_t contributing, int32_t refine, const double* raw_angles,
+                        int64_t n_raw, double* angle_out);
+/* uint32_t peak_vote_floor(const EstimatorConfig&, size_t) -- estimator.hpp:61 (host arithmetic) */
+uint32_t rv_peak_vote_floor(const rv_config* cfg, int64_t n_constraints);
+
+/* ---- geometry (geom.hpp:25-43; host arithmetic, identical formulas) ----------------- */
+void rv_rodrigues(const double axis[3], double angle, double r_out[9]);
+double rv_rotation_error(const double r_gt[9], const double r_opt[9]);
+rv_status rv_project(const double p[3], double* A, double* B);
+void rv_unproject(double A, double B, double out[3]);
+void rv_canonicalize(const double p[3], double out[3]);
+void rv_orthonormal_basis(const double z[3], double a1[3], double a2[3]);
+rv_status rv_correspondence_angle(const double axis[3], const double x[3], const double y[3],
+                                  double tau, double* angle_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ROTAVOTE_B200_H */

@@ -1,0 +1,371 @@
+"""rotavote-b200: B200-native spatial-voting rotation estimation (arXiv 2502.06337).
+
+Python view of the C-ABI (include/rotavote_b200.h). The host solver is C++ inside
+librotavote_b200.so; this module only marshals numpy arrays through ctypes, mirroring the
+reference's public API (proj/include/rotavote/{estimator,voting,angles,geom}.hpp):
+names, argument meaning, defaults and exception types are the reference's.
+
+Arrays: correspondences (n, 6) float64 rows (x0 x1 x2 y0 y1 y2); constraints (n, 3) float64;
+vote grid (G, G) uint32 indexed [iy, ix]; rotations (3, 3) float64.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field, fields
+
+import numpy as np
+
+from . import errors
+from ._native import check, lib, rv_config, rv_estimate, rv_peak, rv_stage_times
+from .errors import (AllDegenerate, DegenerateProjection, EmptyInput, Error, InvalidConfig, NoConsensus,  # noqa: F401
+                     NoPeak, NoVotes, PoleProximity, RankDeficient)
+
+__all__ = [
+    "EstimatorConfig", "RotationEstimate", "Peak", "Context", "default_context", "errors",
+    "estimate_single", "estimate_multi", "preprocess", "accumulate", "find_peaks", "blurred_argmax",
+    "classify_inliers", "refine_axis", "vote_angles", "peak_angle", "peak_vote_floor", "deposit_circle_votes",
+    "rodrigues", "rotation_error", "project", "unproject", "canonicalize", "orthonormal_basis",
+    "correspondence_angle",
+]
+
+
+@dataclass
+class EstimatorConfig:
+    """EstimatorConfig, estimator.hpp:13-29 (same fields and defaults)."""
+    grid: int = 512
+    extent: float = 1.05
+    theta_samples: int = 2048
+    epsilon: float = 0.015
+    angle_bins: int = 1024
+    max_models: int = 1
+    min_votes_frac: float = 0.02
+    consensus_floor_mult: float = 1.5
+    dedupe_overlap: float = 0.5
+    tau_z: float = 1e-9
+    tau_deg: float = 1e-6
+    suppression_radius: int = 8
+    refine: bool = True
+    normalize_inputs: bool = True
+    threads: int = 1
+
+    def to_c(self) -> rv_config:
+        c = rv_config()
+        for f in fields(self):
+            v = getattr(self, f.name)
+            setattr(c, f.name, int(v) if isinstance(v, bool) else v)
+        return c
+
+
+@dataclass
+class RotationEstimate:
+    """RotationEstimate, estimator.hpp:31-38."""
+    axis: np.ndarray = field(default_factory=lambda: np.array([0.0, 0.0, -1.0]))
+    angle: float = 0.0
+    rotation: np.ndarray = field(default_factory=lambda: np.eye(3))
+    inliers: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
+    axis_votes: int = 0
+    elapsed_s: float = 0.0
+
+
+@dataclass
+class Peak:
+    """Peak, voting.hpp:41-46."""
+    ix: int
+    iy: int
+    A: float
+    B: float
+    votes: int
+
+
+def _f64(a, shape_tail) -> np.ndarray:
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if arr.ndim == 1 and shape_tail and arr.size % shape_tail == 0:
+        arr = arr.reshape(-1, shape_tail)
+    return arr
+
+
+def _ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+class Context:
+    """One device context (stream + buffers) of the C-ABI; not thread-safe, one per thread."""
+
+    def __init__(self, device: int = 0):
+        self._lib = lib()
+        h = C.c_void_p()
+        check(self._lib.rv_context_create(device, C.byref(h)))
+        self.handle = h
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self._lib.rv_context_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st: int) -> None:
+        check(st, self.handle)
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        self._check(self._lib.rv_context_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
+
+    def enable_timing(self, on: bool = True) -> None:
+        self._check(self._lib.rv_context_enable_timing(self.handle, int(on)))
+
+    def stage_times(self) -> dict:
+        t = rv_stage_times()
+        self._check(self._lib.rv_context_stage_times(self.handle, C.byref(t)))
+        return {f: getattr(t, f) for f, _ in rv_stage_times._fields_}
+
+    # ---- solver API -------------------------------------------------------------------
+    def _estimate(self, e: rv_estimate, model: int) -> RotationEstimate:
+        inl = np.empty(int(e.n_inliers), np.int32)
+        self._check(self._lib.rv_result_inliers(self.handle, model, _ptr(inl, C.c_int32), inl.size))
+        return RotationEstimate(axis=np.array(e.axis[:]), angle=e.angle,
+                                rotation=np.array(e.rotation[:]).reshape(3, 3), inliers=inl,
+                                axis_votes=int(e.axis_votes), elapsed_s=e.elapsed_s)
+
+    def estimate_single(self, corrs, cfg: EstimatorConfig | None = None) -> RotationEstimate:
+        """estimate_single, estimator.hpp:63-64 (host buffers: H2D + D2H inside the call)."""
+        cfg = cfg or EstimatorConfig()
+        a = _f64(corrs, 6)
+        e = rv_estimate()
+        c = cfg.to_c()
+        self._check(self._lib.rv_estimate_single(self.handle, _ptr(a, C.c_double), a.shape[0] if a.size else 0,
+                                                 C.byref(c), C.byref(e)))
+        return self._estimate(e, 0)
+
+    def estimate_single_device(self, dptr: int, n: int, cfg: EstimatorConfig | None = None) -> RotationEstimate:
+        """Same solve on correspondences already resident in HBM (device pointer, n x 6 f64)."""
+        cfg = cfg or EstimatorConfig()
+        e = rv_estimate()
+        c = cfg.to_c()
+        self._check(self._lib.rv_estimate_single_device(self.handle, C.c_void_p(dptr), n, C.byref(c), C.byref(e)))
+        return self._estimate(e, 0)
+
+    def estimate_multi(self, corrs, cfg: EstimatorConfig | None = None) -> list[RotationEstimate]:
+        """estimate_multi, estimator.hpp:69-70 (sequential extraction, sorted by axis_votes)."""
+        cfg = cfg or EstimatorConfig()
+        a = _f64(corrs, 6)
+        cap = max(1, cfg.max_models)
+        out = (rv_estimate * cap)()
+        nm = C.c_int32()
+        c = cfg.to_c()
+        self._check(self._lib.rv_estimate_multi(self.handle, _ptr(a, C.c_double), a.shape[0] if a.size else 0,
+                                                C.byref(c), out, cap, C.byref(nm)))
+        return [self._estimate(out[k], k) for k in range(nm.value)]
+
+    def estimate_multi_device(self, dptr: int, n: int, cfg: EstimatorConfig | None = None) -> list[RotationEstimate]:
+        cfg = cfg or EstimatorConfig()
+        cap = max(1, cfg.max_models)
+        out = (rv_estimate * cap)()
+        nm = C.c_int32()
+        c = cfg.to_c()
+        self._check(self._lib.rv_estimate_multi_device(self.handle, C.c_void_p(dptr), n, C.byref(c), out, cap,
+                                                       C.byref(nm)))
+        return [self._estimate(out[k], k) for k in range(nm.value)]
+
+    # ---- path functions -----------------------------------------------------------------
+    def preprocess(self, corrs, tau_z: float = 1e-9, normalize: bool = True):
+        """preprocess, estimator.hpp:47-48 -> (constraints (k,3), kept (k,), dropped (d,))."""
+        a = _f64(corrs, 6)
+        n = a.shape[0] if a.size else 0
+        z = np.empty((max(n, 1), 3))
+        kept = np.empty(max(n, 1), np.int32)
+        dropped = np.empty(max(n, 1), np.int32)
+        nk, nd = C.c_int64(), C.c_int64()
+        self._check(self._lib.rv_preprocess(self.handle, _ptr(a, C.c_double), n, tau_z, int(normalize),
+                                            _ptr(z, C.c_double), _ptr(kept, C.c_int32), _ptr(dropped, C.c_int32),
+                                            C.byref(nk), C.byref(nd)))
+        return z[:nk.value].copy(), kept[:nk.value].copy(), dropped[:nd.value].copy()
+
+    def accumulate(self, constraints, grid: int = 512, extent: float = 1.05, samples: int = 2048,
+                   threads: int = 1) -> np.ndarray:
+        """accumulate, voting.hpp:64-65 -> (grid, grid) uint32 counts[iy, ix]."""
+        z = _f64(constraints, 3)
+        n = z.shape[0] if z.size else 0
+        out = np.empty((max(grid, 1), max(grid, 1)), np.uint32)
+        self._check(self._lib.rv_accumulate(self.handle, _ptr(z, C.c_double), n, grid, extent, samples,
+                                            _ptr(out, C.c_uint32)))
+        return out
+
+    def deposit_circle_votes(self, z, counts: np.ndarray, extent: float = 1.05, samples: int = 2048) -> None:
+        """deposit_circle_votes, voting.hpp:60 (in-place on a (G, G) uint32 grid)."""
+        zz = _f64(z, 0).reshape(3)
+        assert counts.dtype == np.uint32 and counts.flags.c_contiguous
+        self._check(self._lib.rv_deposit_circle_votes(self.handle, _ptr(zz, C.c_double), _ptr(counts, C.c_uint32),
+                                                      counts.shape[0], extent, samples))
+
+    def find_peaks(self, counts: np.ndarray, max_peaks: int, suppression_radius: int, min_votes: int,
+                   extent: float = 1.05) -> list[Peak]:
+        """find_peaks, voting.hpp:70-71."""
+        g = np.ascontiguousarray(counts, dtype=np.uint32)
+        out = (rv_peak * max(1, max_peaks))()
+        n = C.c_int32()
+        self._check(self._lib.rv_find_peaks(self.handle, _ptr(g, C.c_uint32), g.shape[0], extent, max_peaks,
+                                            suppression_radius, min_votes, out, C.byref(n)))
+        return [Peak(out[k].ix, out[k].iy, out[k].A, out[k].B, out[k].votes) for k in range(n.value)]
+
+    def blurred_argmax(self, counts: np.ndarray, radius: int, extent: float = 1.05) -> Peak:
+        """blurred_argmax, voting.hpp:80."""
+        g = np.ascontiguousarray(counts, dtype=np.uint32)
+        p = rv_peak()
+        self._check(self._lib.rv_blurred_argmax(self.handle, _ptr(g, C.c_uint32), g.shape[0], extent, radius,
+                                                C.byref(p)))
+        return Peak(p.ix, p.iy, p.A, p.B, p.votes)
+
+    def classify_inliers(self, axis, constraints, epsilon: float) -> np.ndarray:
+        """classify_inliers, estimator.hpp:51-52."""
+        ax = _f64(axis, 0).reshape(3)
+        z = _f64(constraints, 3)
+        n = z.shape[0] if z.size else 0
+        out = np.empty(max(n, 1), np.int32)
+        m = C.c_int64()
+        self._check(self._lib.rv_classify_inliers(self.handle, _ptr(ax, C.c_double), _ptr(z, C.c_double), n, epsilon,
+                                                  _ptr(out, C.c_int32), C.byref(m)))
+        return out[:m.value].copy()
+
+    def refine_axis(self, constraints) -> np.ndarray:
+        """refine_axis, estimator.hpp:57."""
+        z = _f64(constraints, 3)
+        n = z.shape[0] if z.size else 0
+        out = np.empty(3)
+        self._check(self._lib.rv_refine_axis(self.handle, _ptr(z, C.c_double), n, _ptr(out, C.c_double)))
+        return out
+
+    def vote_angles(self, axis, corrs, indices, bin_count: int, tau: float = 1e-6):
+        """vote_angles, angles.hpp:37-40 -> dict(bins, contributing, degenerate, raw_angles)."""
+        ax = _f64(axis, 0).reshape(3)
+        a = _f64(corrs, 6)
+        idx = np.ascontiguousarray(np.asarray(indices, dtype=np.int32))
+        bins = np.empty(max(bin_count, 1), np.uint32)
+        raw = np.empty(max(idx.size, 1))
+        contrib, degen = C.c_uint64(), C.c_uint64()
+        self._check(self._lib.rv_vote_angles(self.handle, _ptr(ax, C.c_double), _ptr(a, C.c_double),
+                                             a.shape[0] if a.size else 0, _ptr(idx, C.c_int32), idx.size, bin_count,
+                                             tau, _ptr(bins, C.c_uint32), C.byref(contrib), C.byref(degen),
+                                             _ptr(raw, C.c_double)))
+        return {"bins": bins[:bin_count], "contributing": contrib.value, "degenerate": degen.value,
+                "raw_angles": raw[:contrib.value].copy()}
+
+    def peak_angle(self, hist: dict, refine: bool, raw_angles=None) -> float:
+        """peak_angle, angles.hpp:44-49."""
+        bins = np.ascontiguousarray(hist["bins"], dtype=np.uint32)
+        raw = _f64(hist["raw_angles"] if raw_angles is None else raw_angles, 0).reshape(-1)
+        out = C.c_double()
+        self._check(self._lib.rv_peak_angle(self.handle, _ptr(bins, C.c_uint32), bins.size, hist["contributing"],
+                                            int(refine), _ptr(raw, C.c_double), raw.size, C.byref(out)))
+        return out.value
+
+
+_default: Context | None = None
+
+
+def default_context() -> Context:
+    global _default
+    if _default is None:
+        _default = Context(0)
+    return _default
+
+
+def estimate_single(corrs, cfg: EstimatorConfig | None = None) -> RotationEstimate:
+    return default_context().estimate_single(corrs, cfg)
+
+
+def estimate_multi(corrs, cfg: EstimatorConfig | None = None) -> list[RotationEstimate]:
+    return default_context().estimate_multi(corrs, cfg)
+
+
+def preprocess(corrs, tau_z: float = 1e-9, normalize: bool = True):
+    return default_context().preprocess(corrs, tau_z, normalize)
+
+
+def accumulate(constraints, grid: int = 512, extent: float = 1.05, samples: int = 2048, threads: int = 1):
+    return default_context().accumulate(constraints, grid, extent, samples, threads)
+
+
+def deposit_circle_votes(z, counts, extent: float = 1.05, samples: int = 2048):
+    return default_context().deposit_circle_votes(z, counts, extent, samples)
+
+
+def find_peaks(counts, max_peaks, suppression_radius, min_votes, extent: float = 1.05):
+    return default_context().find_peaks(counts, max_peaks, suppression_radius, min_votes, extent)
+
+
+def blurred_argmax(counts, radius, extent: float = 1.05):
+    return default_context().blurred_argmax(counts, radius, extent)
+
+
+def classify_inliers(axis, constraints, epsilon):
+    return default_context().classify_inliers(axis, constraints, epsilon)
+
+
+def refine_axis(constraints):
+    return default_context().refine_axis(constraints)
+
+
+def vote_angles(axis, corrs, indices, bin_count, tau: float = 1e-6):
+    return default_context().vote_angles(axis, corrs, indices, bin_count, tau)
+
+
+def peak_angle(hist, refine, raw_angles=None):
+    return default_context().peak_angle(hist, refine, raw_angles)
+
+
+def peak_vote_floor(cfg: EstimatorConfig, n_constraints: int) -> int:
+    c = cfg.to_c()
+    return int(lib().rv_peak_vote_floor(C.byref(c), n_constraints))
+
+
+# ---- geometry (geom.hpp:25-43; host arithmetic in the library) -----------------------------
+def rodrigues(axis, angle: float) -> np.ndarray:
+    ax = _f64(axis, 0).reshape(3)
+    r = np.empty(9)
+    lib().rv_rodrigues(_ptr(ax, C.c_double), angle, _ptr(r, C.c_double))
+    return r.reshape(3, 3)
+
+
+def rotation_error(r_gt, r_opt) -> float:
+    a = np.ascontiguousarray(r_gt, dtype=np.float64).reshape(9)
+    b = np.ascontiguousarray(r_opt, dtype=np.float64).reshape(9)
+    return float(lib().rv_rotation_error(_ptr(a, C.c_double), _ptr(b, C.c_double)))
+
+
+def project(p):
+    pp = _f64(p, 0).reshape(3)
+    A, B = C.c_double(), C.c_double()
+    check(lib().rv_project(_ptr(pp, C.c_double), C.byref(A), C.byref(B)))
+    return A.value, B.value
+
+
+def unproject(A: float, B: float) -> np.ndarray:
+    o = np.empty(3)
+    lib().rv_unproject(A, B, _ptr(o, C.c_double))
+    return o
+
+
+def canonicalize(p) -> np.ndarray:
+    pp = _f64(p, 0).reshape(3)
+    o = np.empty(3)
+    lib().rv_canonicalize(_ptr(pp, C.c_double), _ptr(o, C.c_double))
+    return o
+
+
+def orthonormal_basis(z):
+    zz = _f64(z, 0).reshape(3)
+    a1, a2 = np.empty(3), np.empty(3)
+    lib().rv_orthonormal_basis(_ptr(zz, C.c_double), _ptr(a1, C.c_double), _ptr(a2, C.c_double))
+    return a1, a2
+
+
+def correspondence_angle(axis, x, y, tau: float = 1e-6) -> float:
+    a, xx, yy = (_f64(v, 0).reshape(3) for v in (axis, x, y))
+    out = C.c_double()
+    check(lib().rv_correspondence_angle(_ptr(a, C.c_double), _ptr(xx, C.c_double), _ptr(yy, C.c_double), tau,
+                                        C.byref(out)))
+    return out.value

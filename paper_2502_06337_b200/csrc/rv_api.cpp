@@ -1,0 +1,1373 @@
+// Host side of the B200 path: the C-ABI (include/rotavote_b200.h), the device context, and
+// the estimator control flow (estimate_single / estimate_multi, refine_loop, rescue,
+// sequential multi-model extraction) driving the sm_100a kernels. Every O(N) and O(N*J) step
+// runs on the GPU; the host keeps the reference's O(1) decisions and 3x3 solves.
+// Compiled with -ffp-contract=off: host arithmetic follows the reference op order.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <iterator>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <numbers>
+#include <string>
+#include <vector>
+
+#include "../../include/rotavote_b200.h"
+#include "rv_internal.h"
+#include "rv_linalg.hpp"
+
+using namespace rvb;
+
+namespace {
+
+struct RvError {
+  rv_status st;
+  std::string msg;
+};
+
+[[noreturn]] void fail(rv_status st, const std::string& msg) { throw RvError{st, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(RV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <typename T>
+  T* get(size_t count) {
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    if (bytes > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      cap = 0;
+      const size_t want = bytes + bytes / 4;
+      if (cudaMalloc(&p, want) != cudaSuccess) {
+        cudaGetLastError();
+        fail(RV_ERR_OUT_OF_MEMORY, "cudaMalloc failed");
+      }
+      cap = want;
+    }
+    return static_cast<T*>(p);
+  }
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct StageEvent {
+  int stage;
+  cudaEvent_t a, b;
+};
+
+enum Stage { kPrep = 0, kVote = 1, kPeaks = 2, kRefine = 3, kAngles = 4 };
+
+struct Peak {
+  int ix, iy;
+  double A, B;
+  uint32_t votes;
+};
+
+struct Estimate {
+  double axis[3] = {0, 0, -1};
+  double angle = 0;
+  double R[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  uint32_t votes = 0;
+  std::vector<int32_t> inliers;
+  double elapsed = 0;
+};
+
+// Constraint set on the device (SoA) with its kept map (constraint -> input index).
+struct ConstraintSet {
+  const double* zx = nullptr;
+  const double* zy = nullptr;
+  const double* zz = nullptr;
+  const int32_t* kept = nullptr;
+  int64_t n = 0;
+};
+
+}  // namespace
+
+struct rv_context {
+  int device = 0;
+  int sms = 148;
+  int max_smem = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t st = nullptr;
+  std::string last_error;
+  bool timing = false;
+  rv_stage_times times{};
+  std::vector<StageEvent> events;
+  std::vector<cudaEvent_t> event_pool;
+  size_t event_used = 0;
+  std::chrono::steady_clock::time_point t0;
+
+  // preprocess
+  DBuf corrs, zx, zy, zz, kept, dropped, status, misc32;
+  // residual (estimate_multi)
+  DBuf rzx, rzy, rzz, rkept, removed;
+  // vote
+  DBuf basis_a, basis_b, ranges, band_work, table32, table64, grid, partials, slot_band, counters, stats;
+  int table_J = -1;
+  // peaks
+  DBuf arg_keys, arg_out, sat, blur_best, blur_out, done;
+  // classify / refine
+  DBuf flagsA, flagsB, bcount, bscatter, bdiff, boffA, boffB, cls_result, compact_out;
+  // angles / support
+  DBuf bins, raw, angle_counts, angle_sums, angle_result, sup_counts, sup_result, band_flagsA, band_flagsB,
+      band_idx, band_vals, near_h, near_result;
+  DBuf user_z;  // scratch copy of a constraint span (path functions)
+  // pinned host scalars
+  void* pinned = nullptr;
+  std::vector<std::vector<int32_t>> results;
+
+  unsigned int* done_ptr() { return done.get<unsigned int>(8); }
+};
+
+namespace {
+
+double* pin_d(rv_context* c) { return static_cast<double*>(c->pinned); }
+
+void sync(rv_context* c) { ck(cudaStreamSynchronize(c->st), "cudaStreamSynchronize"); }
+
+cudaEvent_t take_event(rv_context* c) {
+  if (c->event_used == c->event_pool.size()) {
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    c->event_pool.push_back(e);
+  }
+  return c->event_pool[c->event_used++];
+}
+
+struct StageScope {
+  rv_context* c;
+  int stage;
+  cudaEvent_t a = nullptr;
+  StageScope(rv_context* cc, int s) : c(cc), stage(s) {
+    if (c->timing) {
+      a = take_event(c);
+      cudaEventRecord(a, c->st);
+    }
+  }
+  ~StageScope() {
+    if (c->timing) {
+      cudaEvent_t b = take_event(c);
+      cudaEventRecord(b, c->st);
+      c->events.push_back({stage, a, b});
+    }
+  }
+};
+
+void begin_call(rv_context* c) {
+  c->times = rv_stage_times{};
+  c->events.clear();
+  c->event_used = 0;
+  c->t0 = std::chrono::steady_clock::now();
+  c->last_error.clear();
+}
+
+void end_call(rv_context* c) {
+  if (!c->timing) return;
+  sync(c);
+  for (const auto& e : c->events) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    switch (e.stage) {
+      case kPrep: c->times.preprocess_ms += ms; break;
+      case kVote: c->times.vote_ms += ms; break;
+      case kPeaks: c->times.peaks_ms += ms; break;
+      case kRefine: c->times.refine_ms += ms; break;
+      default: c->times.angles_ms += ms; break;
+    }
+  }
+  c->times.total_ms = c->times.preprocess_ms + c->times.vote_ms + c->times.peaks_ms + c->times.refine_ms +
+                      c->times.angles_ms;
+}
+
+void count_launch(rv_context* c, int k = 1) { c->times.kernel_launches += k; }
+
+// ---------------------------------------------------------------------------------------
+// Vote plan (geometry of the band-tiled kernel) for (grid, extent, samples).
+VotePlan make_plan(rv_context* c, int G, double E, int J) {
+  VotePlan p;
+  p.G = G;
+  p.J = J;
+  p.E = E;
+  p.inv_cell = G / (2.0 * E);  // voting.cpp:30
+  p.cs = 2.0 * E / G;          // voting.hpp:23
+  p.halfJ = J / 2;
+  p.step_f = (float)(2.0 * std::numbers::pi / J);
+  p.banded = 0;
+  const bool twins_ok = (J % 2 == 0) && J >= 2 && p.halfJ <= 32768;
+  const bool magic_ok = G <= 4000;  // t + 1.5*2^13 must stay in [8192, 16384)
+  if (!twins_ok || !magic_ok) return p;
+  p.Kf = (float)p.inv_cell;
+  p.CMf = 12288.0f + (float)(0.5 * G);  // E*inv_cell == G/2 exactly in real arithmetic
+  p.clamp = E <= 1.0 + 1e-6 ? 1 : 0;
+  const double lo_t = (E - 1.0) * p.inv_cell, hi_t = (E + 1.0) * p.inv_cell;
+  if (p.clamp) {
+    p.r_min = 0;
+    p.r_max = G - 1;
+  } else {
+    p.r_min = std::max(0, (int)std::floor(lo_t) - 2);
+    p.r_max = std::min(G - 1, (int)std::ceil(hi_t) + 1);
+  }
+  p.c_min = p.r_min;
+  p.c_max = p.r_max;
+  p.W = p.c_max - p.c_min + 1;
+  const size_t table_bytes = ((size_t)((p.halfJ + 1) & ~1)) * sizeof(float2);
+  const size_t fbq_bytes = (size_t)(kVoteThreads / 32) * kFbqCap * 8;
+  const size_t reserve = table_bytes + fbq_bytes + 1024;
+  if ((size_t)c->max_smem <= reserve) return p;
+  const size_t budget_words = ((size_t)c->max_smem - reserve) / 4;
+  const int h_allowed = (int)(budget_words / p.W);
+  if (h_allowed < 1) return p;
+  const int rows = p.r_max - p.r_min + 1;
+  const int nb = (rows + h_allowed - 1) / h_allowed;
+  if (nb > kMaxBands) return p;
+  const int H = (rows + nb - 1) / nb;
+  p.n_bands = nb;
+  p.H_max = H;
+  for (int b = 0; b <= nb; ++b) p.band_r0[b] = std::min(p.r_min + b * H, p.r_max + 1);
+  const double dy = 1e-5;  // culling margin (plane units) >> f32 error of the interval math
+  for (int b = 0; b < nb; ++b) {
+    p.band_ylo[b] = b == 0 ? -INFINITY : (float)(-E + p.band_r0[b] * p.cs - dy);
+    p.band_yhi[b] = b == nb - 1 ? INFINITY : (float)(-E + p.band_r0[b + 1] * p.cs + dy);
+  }
+  p.tile_words = (size_t)H * p.W;
+  p.smem_bytes = ((p.tile_words * 4 + 15) & ~size_t(15)) + table_bytes + fbq_bytes;
+  p.banded = p.smem_bytes <= (size_t)c->max_smem ? 1 : 0;
+  return p;
+}
+
+// Sample table exactly as the reference (voting.cpp:72-81), on the host libm.
+void ensure_tables(rv_context* c, int J) {
+  if (c->table_J == J) return;
+  std::vector<double2> t64(J);
+  const double step = 2.0 * std::numbers::pi / J;
+  for (int j = 0; j < J; ++j) {
+    const double theta = -std::numbers::pi + j * step;
+    t64[j] = make_double2(std::cos(theta), std::sin(theta));
+  }
+  const int M = J / 2;
+  std::vector<float2> t32(std::max(M, 1));
+  for (int j = 0; j < M; ++j) t32[j] = make_float2((float)t64[j].x, (float)t64[j].y);
+  ck(cudaMemcpyAsync(c->table64.get<double2>(J), t64.data(), sizeof(double2) * J, cudaMemcpyHostToDevice, c->st),
+     "table64");
+  ck(cudaMemcpyAsync(c->table32.get<float2>(std::max(M, 1)), t32.data(), sizeof(float2) * std::max(M, 1),
+                     cudaMemcpyHostToDevice, c->st),
+     "table32");
+  sync(c);
+  c->table_J = J;
+}
+
+// accumulate (voting.cpp:88-118) over device SoA constraints into the context grid.
+uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* zz, int64_t n, int G, double E,
+               int J) {
+  if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no constraints to accumulate");
+  if (G < 1 || !(E > 0.0)) fail(RV_ERR_INVALID_CONFIG, "accumulator needs grid >= 1, extent > 0");
+  if (J < 1) fail(RV_ERR_INVALID_CONFIG, "theta_samples must be >= 1");
+  ensure_tables(c, J);
+  const VotePlan p = make_plan(c, G, E, J);
+  uint32_t* grid = c->grid.get<uint32_t>((size_t)G * G);
+  StageScope sc(c, kVote);
+  ck(cudaMemsetAsync(grid, 0, sizeof(uint32_t) * (size_t)G * G, c->st), "memset grid");
+  VoteBuffers b;
+  b.zx = zx;
+  b.zy = zy;
+  b.zz = zz;
+  b.grid = grid;
+  b.table64 = c->table64.get<double2>(J);
+  b.table32 = c->table32.get<float2>(std::max(J / 2, 1));
+  c->times.vote_samples += n * (int64_t)J;
+  c->times.vote_launches += 1;
+  if (!p.banded) {
+    launch_vote_generic(p, b, n, c->st);
+    count_launch(c);
+    ck(cudaGetLastError(), "vote_generic");
+    return grid;
+  }
+  b.basis_a = c->basis_a.get<float4>(n);
+  b.basis_b = c->basis_b.get<float2>(n);
+  b.ranges = c->ranges.get<uint32_t>((size_t)n * p.n_bands * 2);
+  b.band_work = c->band_work.get<unsigned long long>(kMaxBands);
+  b.counters = c->counters.get<int32_t>(kMaxBands + 1);
+  b.stats = c->stats.get<unsigned long long>(2);
+  const int n_ctas = c->sms;
+  b.max_slots = n_ctas * p.n_bands;
+  b.partials = c->partials.get<uint32_t>((size_t)b.max_slots * p.tile_words);
+  b.slot_band = c->slot_band.get<int32_t>(b.max_slots);
+  ck(cudaMemsetAsync(b.band_work, 0, sizeof(unsigned long long) * kMaxBands, c->st), "memset band_work");
+  ck(cudaMemsetAsync(b.counters, 0, sizeof(int32_t) * (kMaxBands + 1), c->st), "memset counters");
+  ck(cudaMemsetAsync(b.stats, 0, sizeof(unsigned long long) * 2, c->st), "memset stats");
+  launch_plan(p, b, n, c->st);
+  const int64_t per_cta = std::max<int64_t>(1, (n * p.n_bands) / ((int64_t)n_ctas * 8));
+  const int chunk = (int)std::min<int64_t>(512, std::max<int64_t>(32, per_cta));
+  launch_vote_banded(p, b, n, n_ctas, chunk, c->st);
+  launch_vote_reduce(p, b, c->st);
+  count_launch(c, 3);
+  ck(cudaGetLastError(), "vote_banded");
+  if (c->timing) {
+    unsigned long long st[2];
+    ck(cudaMemcpyAsync(st, b.stats, sizeof st, cudaMemcpyDeviceToHost, c->st), "stats");
+    sync(c);
+    c->times.vote_pairs += (int64_t)st[0];
+  }
+  return grid;
+}
+
+// ---------------------------------------------------------------------------------------
+// Peaks
+double cell_center(int i, int G, double E) { return -E + (i + 0.5) * (2.0 * E / G); }
+int coord_to_cell(double v, int G, double E) {  // voting.cpp:17-23, :55-57
+  const double inv_cell = G / (2.0 * E);
+  const double t = (v + E) * inv_cell;
+  const double f = std::floor(t);
+  int i = (int)f;
+  if (f == t && i > 0) --i;
+  return std::clamp(i, 0, G - 1);
+}
+
+// find_peaks (voting.cpp:120-170): greedy; device argmax per round, host NMS bookkeeping.
+std::vector<Peak> find_peaks_dev(rv_context* c, const uint32_t* grid, int G, double E, int max_peaks, int radius,
+                                 uint32_t min_votes) {
+  StageScope sc(c, kPeaks);
+  std::vector<Peak> out;
+  std::vector<Disk> disks;
+  const double cs = 2.0 * E / G;
+  unsigned long long* keys = c->arg_keys.get<unsigned long long>(argmax_block_count());
+  unsigned long long* okey = c->arg_out.get<unsigned long long>(1);
+  for (int k = 0; k < max_peaks; ++k) {
+    if (disks.size() > 16) fail(RV_ERR_INVALID_CONFIG, "find_peaks: more than 8 peaks with mirrors unsupported");
+    launch_argmax(grid, G, disks.data(), (int)disks.size(), radius, keys, okey, c->done_ptr(), c->st);
+    count_launch(c);
+    unsigned long long* hk = reinterpret_cast<unsigned long long*>(c->pinned);
+    ck(cudaMemcpyAsync(hk, okey, 8, cudaMemcpyDeviceToHost, c->st), "argmax D2H");
+    sync(c);
+    const unsigned long long key = *hk;
+    if (key == 0) break;
+    const uint32_t best = (uint32_t)(key >> 32);
+    const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu);
+    if (best < min_votes) break;
+    Peak pk;
+    pk.iy = (int)idx / G;
+    pk.ix = (int)idx % G;
+    pk.A = cell_center(pk.ix, G, E);
+    pk.B = cell_center(pk.iy, G, E);
+    pk.votes = best;
+    out.push_back(pk);
+    disks.push_back({pk.ix, pk.iy});
+    const double norm = std::hypot(pk.A, pk.B);
+    if (std::abs(norm - 1.0) <= 1.5 * cs && norm > 0.0) {
+      const double mx = -pk.A / norm, my = -pk.B / norm;
+      disks.push_back({coord_to_cell(mx, G, E), coord_to_cell(my, G, E)});
+    }
+  }
+  if (out.empty()) fail(RV_ERR_NO_PEAK, "no accumulator cell reaches min_votes");
+  return out;
+}
+
+// blurred_argmax for a list of radii (voting.cpp:176-216)
+std::vector<Peak> blurred_argmax_dev(rv_context* c, const uint32_t* grid, int G, double E, const std::vector<int>& radii) {
+  StageScope sc(c, kPeaks);
+  std::vector<Peak> out;
+  if (radii.empty()) return out;
+  unsigned long long* sat = c->sat.get<unsigned long long>((size_t)(G + 1) * (G + 1));
+  unsigned long long* bb = c->blur_best.get<unsigned long long>((size_t)blur_block_count() * 16);
+  unsigned long long* ob = c->blur_out.get<unsigned long long>(16);
+  for (size_t off = 0; off < radii.size(); off += 8) {
+    const int nr = (int)std::min<size_t>(8, radii.size() - off);
+    launch_blur_argmax(grid, G, radii.data() + off, nr, sat, bb, ob, c->done_ptr(), c->st);
+    count_launch(c, 3);
+    unsigned long long* h = reinterpret_cast<unsigned long long*>(c->pinned);
+    ck(cudaMemcpyAsync(h, ob, sizeof(unsigned long long) * 2 * nr, cudaMemcpyDeviceToHost, c->st), "blur D2H");
+    sync(c);
+    for (int k = 0; k < nr; ++k) {
+      const unsigned long long sum = h[2 * k], idx = h[2 * k + 1];
+      Peak pk;
+      pk.iy = (int)(idx / G);
+      pk.ix = (int)(idx % G);
+      pk.A = cell_center(pk.ix, G, E);
+      pk.B = cell_center(pk.iy, G, E);
+      pk.votes = (uint32_t)std::min<unsigned long long>(sum, 0xFFFFFFFFull);
+      out.push_back(pk);
+    }
+  }
+  return out;
+}
+
+// interpolate_peak (estimator.cpp:32-47): 3x3 vote-weighted centroid from the device grid.
+void interpolate_peak_dev(rv_context* c, const uint32_t* grid, int G, double E, const Peak& pk, double* A, double* B) {
+  const int x0 = std::max(0, pk.ix - 1), x1 = std::min(G - 1, pk.ix + 1);
+  const int y0 = std::max(0, pk.iy - 1), y1 = std::min(G - 1, pk.iy + 1);
+  uint32_t* h = reinterpret_cast<uint32_t*>(c->pinned);
+  const int w = x1 - x0 + 1, hgt = y1 - y0 + 1;
+  ck(cudaMemcpy2DAsync(h, sizeof(uint32_t) * 3, grid + (size_t)y0 * G + x0, sizeof(uint32_t) * G,
+                       sizeof(uint32_t) * w, hgt, cudaMemcpyDeviceToHost, c->st),
+     "interp D2H");
+  sync(c);
+  double wsum = 0.0, asum = 0.0, bsum = 0.0;
+  for (int dy = -1; dy <= 1; ++dy) {
+    for (int dx = -1; dx <= 1; ++dx) {
+      const int ix = pk.ix + dx, iy = pk.iy + dy;
+      if (ix < 0 || ix >= G || iy < 0 || iy >= G) continue;
+      const double wv = h[(iy - y0) * 3 + (ix - x0)];
+      const double cA = cell_center(ix, G, E), cB = cell_center(iy, G, E);
+      wsum += wv;
+      asum += wv * cA;
+      bsum += wv * cB;
+    }
+  }
+  if (wsum <= 0.0) {
+    *A = pk.A;
+    *B = pk.B;
+    return;
+  }
+  *A = asum / wsum;
+  *B = bsum / wsum;
+}
+
+uint32_t grid_cell(rv_context* c, const uint32_t* grid, int G, int ix, int iy) {
+  uint32_t* h = reinterpret_cast<uint32_t*>(c->pinned);
+  ck(cudaMemcpyAsync(h, grid + (size_t)iy * G + ix, 4, cudaMemcpyDeviceToHost, c->st), "cell D2H");
+  sync(c);
+  return *h;
+}
+
+// ---------------------------------------------------------------------------------------
+// Classification state: a bitmask over a constraint set + its block offsets and count.
+struct Cls {
+  uint32_t* flags;
+  int32_t* offsets;
+  int64_t count;
+  bool differs;
+  double scatter[6];
+};
+
+// classify (estimator.cpp:287-297) fused with the scatter of the same inliers.
+Cls classify_dev(rv_context* c, const ConstraintSet& cs, const double axis[3], double eps, int slot,
+                 const uint32_t* prev, int mode = 0) {
+  StageScope sc(c, kRefine);
+  const int nb = classify_blocks(cs.n);
+  const size_t words = (size_t)(cs.n + 31) / 32 + 32;
+  Cls r;
+  r.flags = slot == 0 ? c->flagsA.get<uint32_t>(words) : c->flagsB.get<uint32_t>(words);
+  r.offsets = slot == 0 ? c->boffA.get<int32_t>(nb) : c->boffB.get<int32_t>(nb);
+  ClassifyOut o;
+  o.flags = r.flags;
+  o.prev = prev;
+  o.block_count = c->bcount.get<int32_t>(nb);
+  o.block_scatter = c->bscatter.get<double>((size_t)nb * 6);
+  o.block_diff = c->bdiff.get<int32_t>(nb);
+  o.result = c->cls_result.get<double>(8);
+  launch_classify_mode(cs.zx, cs.zy, cs.zz, cs.n, axis, eps, mode, o, r.offsets, c->done_ptr(), c->st);
+  count_launch(c);
+  double* h = pin_d(c);
+  ck(cudaMemcpyAsync(h, o.result, sizeof(double) * 8, cudaMemcpyDeviceToHost, c->st), "classify D2H");
+  sync(c);
+  r.count = (int64_t)h[0];
+  r.differs = h[1] != 0.0;
+  for (int k = 0; k < 6; ++k) r.scatter[k] = h[2 + k];
+  return r;
+}
+
+// refine_loop (estimator.cpp:51-69). Returns the final classification (in flags slot A or B).
+Cls refine_loop_dev(rv_context* c, const ConstraintSet& cs, double axis[3], const rv_config& cfg, int* passes = nullptr) {
+  int slot = 0;
+  Cls inl = classify_dev(c, cs, axis, cfg.epsilon, slot, nullptr);
+  if (passes) *passes = 0;
+  if (!cfg.refine) return inl;
+  for (int pass = 0; pass < 10 && inl.count >= 2; ++pass) {
+    double next[3];
+    if (!axis_from_scatter(inl.scatter, next)) break;  // RankDeficient: keep the current axis
+    if (passes) ++*passes;
+    slot ^= 1;
+    Cls nx = classify_dev(c, cs, next, cfg.epsilon, slot, inl.flags);
+    axis[0] = next[0];
+    axis[1] = next[1];
+    axis[2] = next[2];
+    const bool stable = !nx.differs;
+    inl = nx;
+    if (stable) break;
+  }
+  return inl;
+}
+
+// Compact a classification into input indices (through the kept map).
+int32_t* compact_dev(rv_context* c, const ConstraintSet& cs, const Cls& cl) {
+  int32_t* out = c->compact_out.get<int32_t>((size_t)std::max<int64_t>(cl.count, 1));
+  if (cl.count > 0) {
+    launch_compact_flags(cl.flags, cs.n, cs.kept, cl.offsets, out, c->st);
+    count_launch(c);
+  }
+  return out;
+}
+
+// vote_angles + peak_angle (angles.cpp:46-90) over device input indices. Throws NoVotes.
+double angle_dev(rv_context* c, const double axis[3], const double* corrs, const int32_t* idx, int64_t m,
+                 const rv_config& cfg) {
+  StageScope sc(c, kAngles);
+  if (cfg.angle_bins < 8) fail(RV_ERR_INVALID_CONFIG, "angle histogram needs bin_count >= 8");
+  uint32_t* bins = c->bins.get<uint32_t>(cfg.angle_bins);
+  double* raw = c->raw.get<double>((size_t)std::max<int64_t>(m, 1));
+  unsigned long long* cnt = c->angle_counts.get<unsigned long long>(2);
+  ck(cudaMemsetAsync(bins, 0, sizeof(uint32_t) * cfg.angle_bins, c->st), "memset bins");
+  ck(cudaMemsetAsync(cnt, 0, 16, c->st), "memset counts");
+  if (m > 0) {
+    launch_vote_angles_k(axis, corrs, idx, m, cfg.angle_bins, cfg.tau_deg, bins, raw, cnt, c->st);
+    count_launch(c);
+  }
+  double* res = c->angle_result.get<double>(4);
+  if (m > 0) {
+    launch_peak_angle_k(bins, cfg.angle_bins, raw, m, c->angle_sums.get<double>(2 * 296), res, c->done_ptr(), c->st);
+    count_launch(c);
+  }
+  double* h = pin_d(c);
+  ck(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, c->st), "angle counts D2H");
+  if (m > 0) ck(cudaMemcpyAsync(h + 2, res, 32, cudaMemcpyDeviceToHost, c->st), "angle sums D2H");
+  sync(c);
+  const unsigned long long contributing = reinterpret_cast<unsigned long long*>(h)[0];
+  if (contributing == 0) fail(RV_ERR_NO_VOTES, "no correspondence produced an angle vote");
+  const double s = h[2], co = h[3], center = h[5];
+  if (!cfg.refine) return center;
+  if (s == 0.0 && co == 0.0) return center;
+  double mean = std::atan2(s, co);
+  if (mean <= -kPiD) mean += 2.0 * kPiD;
+  return mean;
+}
+
+// build_estimate (estimator.cpp:73-92)
+Estimate build_estimate_dev(rv_context* c, const ConstraintSet& cs, const double axis[3], const Cls& cl,
+                            uint32_t votes, const double* corrs, const rv_config& cfg, bool want_inliers = true) {
+  int32_t* idx = compact_dev(c, cs, cl);
+  Estimate est;
+  est.angle = angle_dev(c, axis, corrs, idx, cl.count, cfg);
+  std::memcpy(est.axis, axis, sizeof est.axis);
+  rodrigues3(axis, est.angle, est.R);
+  est.votes = votes;
+  if (want_inliers) {
+    est.inliers.resize(cl.count);
+    if (cl.count > 0) {
+      ck(cudaMemcpyAsync(est.inliers.data(), idx, sizeof(int32_t) * cl.count, cudaMemcpyDeviceToHost, c->st),
+         "inliers D2H");
+      sync(c);
+    }
+  }
+  return est;
+}
+
+struct Support {
+  int64_t coherent = 0;
+  int64_t band = 0;
+};
+
+// model_support (estimator.cpp:117-137); band flags to `band_flags` if given.
+Support model_support_dev(rv_context* c, const ConstraintSet& cs, const double* corrs, const Estimate& est,
+                          const rv_config& cfg, uint32_t* band_flags) {
+  StageScope sc(c, kAngles);
+  const int nb = classify_blocks(cs.n);
+  int32_t* bc = c->sup_counts.get<int32_t>((size_t)nb * 2);
+  int32_t* res = c->sup_result.get<int32_t>(2);
+  launch_model_support_k(cs.zx, cs.zy, cs.zz, cs.kept, corrs, cs.n, est.axis, est.angle, cfg.epsilon, cfg.tau_deg,
+                         band_flags, bc, res, c->done_ptr(), c->st);
+  count_launch(c);
+  int32_t* h = reinterpret_cast<int32_t*>(c->pinned);
+  ck(cudaMemcpyAsync(h, res, 8, cudaMemcpyDeviceToHost, c->st), "support D2H");
+  sync(c);
+  return Support{h[0], h[1]};
+}
+
+// anneal_axis (estimator.cpp:145-160)
+void anneal_axis_dev(rv_context* c, const ConstraintSet& cs, double axis[3], double eps0, const rv_config& cfg) {
+  double e = std::max(eps0, cfg.epsilon);
+  while (true) {
+    const Cls cl = classify_dev(c, cs, axis, e, 0, nullptr);
+    if (cl.count >= 2) {
+      double next[3];
+      if (axis_from_scatter(cl.scatter, next)) std::memcpy(axis, next, sizeof next);
+    }
+    if (e <= cfg.epsilon) break;
+    e = std::max(cfg.epsilon, 0.5 * e);
+  }
+}
+
+// rescue_axes (estimator.cpp:162-179)
+std::vector<std::array<double, 3>> rescue_axes_dev(rv_context* c, const uint32_t* grid, const ConstraintSet& cs,
+                                                   const rv_config& cfg) {
+  std::vector<std::array<double, 3>> out;
+  std::vector<int> radii;
+  for (int w : {4, 8, 16, 32, 64}) {
+    if (2 * w + 1 > cfg.grid) break;
+    radii.push_back(w);
+  }
+  const std::vector<Peak> ps = blurred_argmax_dev(c, grid, cfg.grid, cfg.extent, radii);
+  const double cs_ = 2.0 * cfg.extent / cfg.grid;
+  for (size_t k = 0; k < ps.size(); ++k) {
+    double b[3], start[3];
+    backproject(ps[k].A, ps[k].B, b);
+    canonicalize3(b, start);
+    anneal_axis_dev(c, cs, start, radii[k] * cs_, cfg);
+    out.push_back({start[0], start[1], start[2]});
+  }
+  // least squares over all constraints (refine_axis(constraints))
+  if (cs.n >= 2) {
+    const Cls all = classify_dev(c, cs, nullptr, 0.0, 0, nullptr, 1);
+    double ls[3];
+    if (axis_from_scatter(all.scatter, ls)) {
+      anneal_axis_dev(c, cs, ls, 0.25, cfg);
+      out.push_back({ls[0], ls[1], ls[2]});
+    }
+  }
+  return out;
+}
+
+// build_candidate (estimator.cpp:183-194). Throws NoVotes.
+Estimate build_candidate_dev(rv_context* c, const double start[3], const uint32_t* grid, const ConstraintSet& cs,
+                             const double* corrs, const rv_config& cfg) {
+  double axis[3] = {start[0], start[1], start[2]};
+  const Cls cl = refine_loop_dev(c, cs, axis, cfg);
+  uint32_t votes = 0;
+  double A, B;
+  if (project3(axis, &A, &B))
+    votes = grid_cell(c, grid, cfg.grid, coord_to_cell(A, cfg.grid, cfg.extent), coord_to_cell(B, cfg.grid, cfg.extent));
+  return build_estimate_dev(c, cs, axis, cl, votes, corrs, cfg);
+}
+
+// ---------------------------------------------------------------------------------------
+struct PreResult {
+  ConstraintSet cs;
+  int64_t n_dropped = 0;
+};
+
+PreResult preprocess_dev(rv_context* c, const double* d_corrs, int64_t n, double tau_z, int normalize) {
+  StageScope sc(c, kPrep);
+  PrepBuffers b;
+  b.corrs = d_corrs;
+  b.zx = c->zx.get<double>(n);
+  b.zy = c->zy.get<double>(n);
+  b.zz = c->zz.get<double>(n);
+  b.kept = c->kept.get<int32_t>(n);
+  b.dropped = c->dropped.get<int32_t>(n);
+  const int nb = prep_blocks(n);
+  b.status = c->status.get<unsigned long long>(nb);
+  int32_t* misc = c->misc32.get<int32_t>(8);
+  b.block_counter = misc;
+  b.totals = misc + 2;
+  ck(cudaMemsetAsync(b.status, 0, sizeof(unsigned long long) * nb, c->st), "memset status");
+  ck(cudaMemsetAsync(misc, 0, sizeof(int32_t) * 8, c->st), "memset misc");
+  launch_preprocess(b, n, tau_z, normalize, c->st);
+  count_launch(c);
+  ck(cudaGetLastError(), "preprocess");
+  int32_t* h = reinterpret_cast<int32_t*>(c->pinned);
+  ck(cudaMemcpyAsync(h, b.totals, 8, cudaMemcpyDeviceToHost, c->st), "totals D2H");
+  sync(c);
+  PreResult r;
+  r.cs.zx = b.zx;
+  r.cs.zy = b.zy;
+  r.cs.zz = b.zz;
+  r.cs.kept = b.kept;
+  r.cs.n = h[0];
+  r.n_dropped = h[1];
+  return r;
+}
+
+const double* upload_corrs(rv_context* c, const double* corrs, int64_t n) {
+  double* d = c->corrs.get<double>((size_t)n * 6);
+  StageScope sc(c, kPrep);
+  ck(cudaMemcpyAsync(d, corrs, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, c->st), "H2D corrs");
+  return d;
+}
+
+std::vector<int32_t> dropped_list(rv_context* c, int64_t nd) {
+  std::vector<int32_t> v(nd);
+  if (nd > 0) {
+    ck(cudaMemcpyAsync(v.data(), c->dropped.get<int32_t>(1), sizeof(int32_t) * nd, cudaMemcpyDeviceToHost, c->st),
+       "dropped D2H");
+    sync(c);
+  }
+  return v;
+}
+
+Estimate identity_estimate(std::vector<int32_t> idx) {
+  Estimate e;
+  e.inliers = std::move(idx);
+  return e;
+}
+
+// estimate_single (estimator.cpp:320-371) over device-resident correspondences.
+Estimate estimate_single_dev(rv_context* c, const double* d_corrs, int64_t n, const rv_config& cfg) {
+  if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
+  const PreResult pre = preprocess_dev(c, d_corrs, n, cfg.tau_z, cfg.normalize_inputs);
+  if (pre.cs.n == 0) {
+    std::vector<int32_t> all(n);
+    for (int64_t i = 0; i < n; ++i) all[i] = (int32_t)i;
+    return identity_estimate(std::move(all));
+  }
+  if (pre.n_dropped * 10 >= n * 9) return identity_estimate(dropped_list(c, pre.n_dropped));
+  const uint32_t* grid = vote(c, pre.cs.zx, pre.cs.zy, pre.cs.zz, pre.cs.n, cfg.grid, cfg.extent, cfg.theta_samples);
+  const std::vector<Peak> peaks = find_peaks_dev(c, grid, cfg.grid, cfg.extent, 1, cfg.suppression_radius, 1);
+  Estimate est;
+  {  // estimate_from_peak (estimator.cpp:94-101)
+    double A, B, b[3], axis[3];
+    interpolate_peak_dev(c, grid, cfg.grid, cfg.extent, peaks[0], &A, &B);
+    backproject(A, B, b);
+    canonicalize3(b, axis);
+    const Cls cl = refine_loop_dev(c, pre.cs, axis, cfg);
+    est = build_estimate_dev(c, pre.cs, axis, cl, peaks[0].votes, d_corrs, cfg);
+  }
+  const double chance = cfg.epsilon * (double)pre.cs.n;
+  if (cfg.refine && (double)est.inliers.size() < 3.0 * chance) {  // estimator.cpp:352-368
+    int64_t best = model_support_dev(c, pre.cs, d_corrs, est, cfg, nullptr).coherent;
+    for (const auto& ax : rescue_axes_dev(c, grid, pre.cs, cfg)) {
+      Estimate cand;
+      try {
+        cand = build_candidate_dev(c, ax.data(), grid, pre.cs, d_corrs, cfg);
+      } catch (const RvError& e) {
+        if (e.st == RV_ERR_NO_VOTES) continue;
+        throw;
+      }
+      const int64_t coh = model_support_dev(c, pre.cs, d_corrs, cand, cfg, nullptr).coherent;
+      if (coh > best) {
+        best = coh;
+        est = std::move(cand);
+      }
+    }
+  }
+  return est;
+}
+
+// near_identity_model (estimator.cpp:224-249) over the residual set.
+bool near_identity_dev(rv_context* c, const double* d_corrs, const ConstraintSet& sub, const rv_config& cfg,
+                       int64_t min_cluster, Estimate* out) {
+  StageScope sc(c, kAngles);
+  const int nb = classify_blocks(sub.n);
+  uint32_t* flags = c->flagsA.get<uint32_t>((size_t)(sub.n + 31) / 32 + 32);
+  int32_t* offs = c->boffA.get<int32_t>(nb);
+  double* res = c->near_result.get<double>(10);
+  launch_near_identity_k(d_corrs, sub.kept, sub.n, cfg.normalize_inputs, flags, c->bcount.get<int32_t>(nb),
+                         c->near_h.get<double>((size_t)nb * 9), offs, res, c->done_ptr(), c->st);
+  count_launch(c);
+  double* h = pin_d(c);
+  ck(cudaMemcpyAsync(h, res, sizeof(double) * 10, cudaMemcpyDeviceToHost, c->st), "near D2H");
+  sync(c);
+  const int64_t nc = (int64_t)h[0];
+  if (nc < std::max<int64_t>(min_cluster, 3)) return false;
+  double hm[9];
+  std::memcpy(hm, h + 1, sizeof hm);
+  int32_t* idx = c->compact_out.get<int32_t>((size_t)nc);
+  launch_compact_flags(flags, sub.n, sub.kept, offs, idx, c->st);
+  count_launch(c);
+  Estimate e;
+  e.inliers.resize(nc);
+  ck(cudaMemcpyAsync(e.inliers.data(), idx, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, c->st), "cluster D2H");
+  sync(c);
+  kabsch(hm, e.R);
+  angle_axis_canonical(e.R, e.axis, &e.angle);
+  e.votes = (uint32_t)nc;
+  *out = std::move(e);
+  return true;
+}
+
+// estimate_multi (estimator.cpp:373-493)
+std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, int64_t n, const rv_config& cfg) {
+  if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
+  const PreResult pre = preprocess_dev(c, d_corrs, n, cfg.tau_z, cfg.normalize_inputs);
+  if (pre.cs.n == 0) fail(RV_ERR_ALL_DEGENERATE, "every correspondence pair is degenerate (x ~ y)");
+  const double chance = cfg.epsilon * (double)pre.cs.n;
+  const int64_t consensus_floor = (int64_t)std::max(2.0, cfg.consensus_floor_mult * chance);
+  uint8_t* removed = c->removed.get<uint8_t>(pre.cs.n);
+  ck(cudaMemsetAsync(removed, 0, pre.cs.n, c->st), "memset removed");
+  std::vector<Estimate> out;
+  while ((int)out.size() < cfg.max_models) {
+    // residual (estimator.cpp:392-398)
+    ConstraintSet sub;
+    {
+      StageScope sc(c, kPrep);
+      const int nb = (int)((pre.cs.n + 255) / 256);
+      unsigned long long* stt = c->status.get<unsigned long long>(nb);
+      int32_t* misc = c->misc32.get<int32_t>(8);
+      ck(cudaMemsetAsync(stt, 0, sizeof(unsigned long long) * nb, c->st), "memset status");
+      ck(cudaMemsetAsync(misc, 0, sizeof(int32_t) * 8, c->st), "memset misc");
+      double* ozx = c->rzx.get<double>(pre.cs.n);
+      double* ozy = c->rzy.get<double>(pre.cs.n);
+      double* ozz = c->rzz.get<double>(pre.cs.n);
+      int32_t* okept = c->rkept.get<int32_t>(pre.cs.n);
+      launch_gather_residual(pre.cs.zx, pre.cs.zy, pre.cs.zz, pre.cs.kept, removed, pre.cs.n, stt, misc, ozx, ozy,
+                             ozz, okept, misc + 4, c->st);
+      count_launch(c);
+      int32_t* h = reinterpret_cast<int32_t*>(c->pinned);
+      ck(cudaMemcpyAsync(h, misc + 4, 4, cudaMemcpyDeviceToHost, c->st), "residual D2H");
+      sync(c);
+      sub.zx = ozx;
+      sub.zy = ozy;
+      sub.zz = ozz;
+      sub.kept = okept;
+      sub.n = h[0];
+    }
+    if (sub.n < std::max<int64_t>(2, consensus_floor)) break;
+    const uint32_t* grid = vote(c, sub.zx, sub.zy, sub.zz, sub.n, cfg.grid, cfg.extent, cfg.theta_samples);
+    std::vector<Peak> peaks;
+    bool have_peak = true;
+    try {
+      peaks = find_peaks_dev(c, grid, cfg.grid, cfg.extent, 1, cfg.suppression_radius, rv_peak_vote_floor(&cfg, sub.n));
+    } catch (const RvError& e) {
+      if (e.st != RV_ERR_NO_PEAK) throw;
+      have_peak = false;
+    }
+    Estimate est;
+    Support sup;
+    bool have = false;
+    uint32_t* best_band = c->band_flagsA.get<uint32_t>((size_t)(pre.cs.n + 31) / 32 + 32);
+    uint32_t* cand_band = c->band_flagsB.get<uint32_t>((size_t)(pre.cs.n + 31) / 32 + 32);
+    if (have_peak) {
+      std::vector<std::array<double, 3>> starts;
+      double A, B, b[3], s0[3];
+      interpolate_peak_dev(c, grid, cfg.grid, cfg.extent, peaks[0], &A, &B);
+      backproject(A, B, b);
+      canonicalize3(b, s0);
+      starts.push_back({s0[0], s0[1], s0[2]});
+      for (const auto& a : rescue_axes_dev(c, grid, sub, cfg)) starts.push_back(a);
+      for (size_t s = 0; s < starts.size(); ++s) {
+        Estimate cand;
+        try {
+          cand = build_candidate_dev(c, starts[s].data(), grid, pre.cs, d_corrs, cfg);
+        } catch (const RvError& e) {
+          if (e.st == RV_ERR_NO_VOTES) continue;
+          throw;
+        }
+        if (s == 0) cand.votes = peaks[0].votes;
+        const Support cs = model_support_dev(c, pre.cs, d_corrs, cand, cfg, cand_band);
+        if (!have || cs.coherent > sup.coherent) {
+          est = std::move(cand);
+          sup = cs;
+          std::swap(best_band, cand_band);
+          have = true;
+        }
+      }
+    }
+    bool identity_model = false;
+    const bool valid = have && (int64_t)est.inliers.size() >= consensus_floor &&
+                       sup.coherent >= std::max<int64_t>(8, (int64_t)est.inliers.size() / 5);
+    if (!valid) {
+      Estimate ident;
+      if (!near_identity_dev(c, d_corrs, sub, cfg, consensus_floor, &ident)) break;
+      est = std::move(ident);
+      identity_model = true;
+    }
+    bool duplicate = false;
+    for (const auto& e : out) {
+      std::vector<int32_t> common;
+      std::set_intersection(e.inliers.begin(), e.inliers.end(), est.inliers.begin(), est.inliers.end(),
+                            std::back_inserter(common));
+      if ((double)common.size() > cfg.dedupe_overlap * (double)est.inliers.size()) {
+        duplicate = true;
+        break;
+      }
+    }
+    if (duplicate) break;
+    if (identity_model) {
+      launch_strip_identity_k(d_corrs, pre.cs.kept, pre.cs.n, cfg.normalize_inputs, removed, c->st);
+      count_launch(c);
+    } else {
+      double strip = 2.0 * cfg.epsilon;
+      if (sup.band > 0) {
+        // 95th-percentile band value (nth_element) over the band members
+        const int nb = classify_blocks(pre.cs.n);
+        int32_t* offs = c->boffB.get<int32_t>(nb);
+        std::vector<uint32_t> hf((size_t)(pre.cs.n + 31) / 32);
+        ck(cudaMemcpyAsync(hf.data(), best_band, sizeof(uint32_t) * hf.size(), cudaMemcpyDeviceToHost, c->st),
+           "band flags D2H");
+        sync(c);
+        std::vector<int32_t> hoffs(nb);
+        int64_t acc = 0;
+        for (int bk = 0; bk < nb; ++bk) {
+          hoffs[bk] = (int32_t)acc;
+          for (int w = 0; w < 32; ++w) {
+            const size_t wi = (size_t)bk * 32 + w;
+            if (wi < hf.size()) acc += __builtin_popcount(hf[wi]);
+          }
+        }
+        ck(cudaMemcpyAsync(offs, hoffs.data(), sizeof(int32_t) * nb, cudaMemcpyHostToDevice, c->st), "offs H2D");
+        int32_t* bidx = c->band_idx.get<int32_t>((size_t)std::max<int64_t>(acc, 1));
+        launch_compact_flags(best_band, pre.cs.n, nullptr, offs, bidx, c->st);
+        double* bv = c->band_vals.get<double>((size_t)std::max<int64_t>(acc, 1));
+        launch_gather_dot_k(pre.cs.zx, pre.cs.zy, pre.cs.zz, bidx, acc, est.axis, bv, c->st);
+        count_launch(c, 2);
+        std::vector<double> band(acc);
+        ck(cudaMemcpyAsync(band.data(), bv, sizeof(double) * acc, cudaMemcpyDeviceToHost, c->st), "band D2H");
+        sync(c);
+        if (!band.empty()) {
+          const size_t q = std::min(band.size() - 1, (band.size() * 95) / 100);
+          std::nth_element(band.begin(), band.begin() + (std::ptrdiff_t)q, band.end());
+          strip = std::max(strip, 1.25 * band[q]);
+        }
+      }
+      launch_strip_k(pre.cs.zx, pre.cs.zy, pre.cs.zz, pre.cs.n, est.axis, strip, removed, c->st);
+      count_launch(c);
+    }
+    out.push_back(std::move(est));
+  }
+  if (out.empty()) fail(RV_ERR_NO_PEAK, "no peak produced a usable model");
+  std::stable_sort(out.begin(), out.end(), [](const Estimate& a, const Estimate& b) { return a.votes > b.votes; });
+  return out;
+}
+
+void to_c(const Estimate& e, rv_estimate* o, double elapsed) {
+  std::memcpy(o->axis, e.axis, sizeof o->axis);
+  o->angle = e.angle;
+  std::memcpy(o->rotation, e.R, sizeof o->rotation);
+  o->axis_votes = e.votes;
+  o->n_inliers = (int64_t)e.inliers.size();
+  o->elapsed_s = elapsed;
+}
+
+template <typename F>
+rv_status guarded(rv_context* c, F&& f) {
+  try {
+    if (c) begin_call(c);
+    f();
+    if (c) end_call(c);
+    return RV_OK;
+  } catch (const RvError& e) {
+    if (c) {
+      c->last_error = e.msg;
+      if (e.st == RV_ERR_CUDA) cudaGetLastError();
+    }
+    return e.st;
+  } catch (const std::bad_alloc&) {
+    if (c) c->last_error = "host allocation failed";
+    return RV_ERR_OUT_OF_MEMORY;
+  } catch (...) {
+    if (c) c->last_error = "unexpected exception";
+    return RV_ERR_INVALID_ARGUMENT;
+  }
+}
+
+double seconds_since(const rv_context* c) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - c->t0).count();
+}
+
+// Constraint span (host, n x 3 AoS) -> device SoA in the context's preprocess buffers.
+ConstraintSet upload_constraints(rv_context* c, const double* z, int64_t n) {
+  std::vector<double> sx(n), sy(n), szz(n);
+  for (int64_t i = 0; i < n; ++i) {
+    sx[i] = z[3 * i];
+    sy[i] = z[3 * i + 1];
+    szz[i] = z[3 * i + 2];
+  }
+  ConstraintSet cs;
+  double* dx = c->zx.get<double>(n);
+  double* dy = c->zy.get<double>(n);
+  double* dz = c->zz.get<double>(n);
+  ck(cudaMemcpyAsync(dx, sx.data(), 8 * n, cudaMemcpyHostToDevice, c->st), "H2D zx");
+  ck(cudaMemcpyAsync(dy, sy.data(), 8 * n, cudaMemcpyHostToDevice, c->st), "H2D zy");
+  ck(cudaMemcpyAsync(dz, szz.data(), 8 * n, cudaMemcpyHostToDevice, c->st), "H2D zz");
+  sync(c);
+  cs.zx = dx;
+  cs.zy = dy;
+  cs.zz = dz;
+  cs.kept = nullptr;
+  cs.n = n;
+  return cs;
+}
+
+}  // namespace
+
+// =========================================================================================
+extern "C" {
+
+int32_t rv_abi_version(void) { return RV_ABI_VERSION; }
+
+void rv_config_default(rv_config* c) {  // estimator.hpp:13-29
+  c->grid = 512;
+  c->extent = 1.05;
+  c->theta_samples = 2048;
+  c->epsilon = 0.015;
+  c->angle_bins = 1024;
+  c->max_models = 1;
+  c->min_votes_frac = 0.02;
+  c->consensus_floor_mult = 1.5;
+  c->dedupe_overlap = 0.5;
+  c->tau_z = 1e-9;
+  c->tau_deg = 1e-6;
+  c->suppression_radius = 8;
+  c->refine = 1;
+  c->normalize_inputs = 1;
+  c->threads = 1;
+}
+
+const char* rv_status_string(rv_status st) {
+  switch (st) {
+    case RV_OK: return "ok";
+    case RV_ERR_EMPTY_INPUT: return "EmptyInput";
+    case RV_ERR_NO_PEAK: return "NoPeak";
+    case RV_ERR_DEGENERATE_PROJECTION: return "DegenerateProjection";
+    case RV_ERR_NO_VOTES: return "NoVotes";
+    case RV_ERR_ALL_DEGENERATE: return "AllDegenerate";
+    case RV_ERR_RANK_DEFICIENT: return "RankDeficient";
+    case RV_ERR_NO_CONSENSUS: return "NoConsensus";
+    case RV_ERR_INVALID_CONFIG: return "InvalidConfig";
+    case RV_ERR_POLE_PROXIMITY: return "PoleProximity";
+    case RV_ERR_OUT_OF_MEMORY: return "OutOfMemory";
+    case RV_ERR_CUDA: return "CudaError";
+    case RV_ERR_NCCL: return "NcclError";
+    case RV_ERR_INVALID_ARGUMENT: return "InvalidArgument";
+    case RV_ERR_NO_DEVICE: return "NoDevice";
+  }
+  return "unknown";
+}
+
+rv_status rv_context_create(int32_t device, rv_context** out) {
+  if (!out) return RV_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return RV_ERR_NO_DEVICE;
+  }
+  if (device < 0 || device >= count) return RV_ERR_INVALID_ARGUMENT;
+  auto* c = new (std::nothrow) rv_context();
+  if (!c) return RV_ERR_OUT_OF_MEMORY;
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMallocHost(&c->pinned, 4096) != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return RV_ERR_CUDA;
+  }
+  c->st = c->own;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&c->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  *out = c;
+  return RV_OK;
+}
+
+void rv_context_destroy(rv_context* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->st);
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+}
+
+rv_status rv_context_set_stream(rv_context* c, void* stream) {
+  if (!c) return RV_ERR_INVALID_ARGUMENT;
+  c->st = stream ? static_cast<cudaStream_t>(stream) : c->own;
+  return RV_OK;
+}
+
+const char* rv_context_last_error(const rv_context* c) { return c ? c->last_error.c_str() : "null context"; }
+
+rv_status rv_context_enable_timing(rv_context* c, int32_t enable) {
+  if (!c) return RV_ERR_INVALID_ARGUMENT;
+  c->timing = enable != 0;
+  return RV_OK;
+}
+
+rv_status rv_context_stage_times(const rv_context* c, rv_stage_times* out) {
+  if (!c || !out) return RV_ERR_INVALID_ARGUMENT;
+  *out = c->times;
+  return RV_OK;
+}
+
+rv_status rv_estimate_single_device(rv_context* c, const double* d_corrs, int64_t n, const rv_config* cfg,
+                                    rv_estimate* out) {
+  if (!c || !cfg || !out || (n > 0 && !d_corrs)) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    c->results.clear();
+    Estimate e = estimate_single_dev(c, d_corrs, n, *cfg);
+    to_c(e, out, seconds_since(c));
+    c->results.push_back(std::move(e.inliers));
+  });
+}
+
+rv_status rv_estimate_single(rv_context* c, const double* corrs, int64_t n, const rv_config* cfg, rv_estimate* out) {
+  if (!c || !cfg || !out || (n > 0 && !corrs)) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    c->results.clear();
+    if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
+    const double* d = upload_corrs(c, corrs, n);
+    Estimate e = estimate_single_dev(c, d, n, *cfg);
+    to_c(e, out, seconds_since(c));
+    c->results.push_back(std::move(e.inliers));
+  });
+}
+
+static rv_status multi_impl(rv_context* c, const double* d, int64_t n, const rv_config* cfg, rv_estimate* out,
+                            int32_t capacity, int32_t* n_models, bool host) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    c->results.clear();
+    *n_models = 0;
+    if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
+    const double* dd = host ? upload_corrs(c, d, n) : d;
+    std::vector<Estimate> v = estimate_multi_dev(c, dd, n, *cfg);
+    const double el = seconds_since(c);
+    for (size_t k = 0; k < v.size(); ++k) {
+      if ((int32_t)k < capacity) to_c(v[k], out + k, el);
+      c->results.push_back(std::move(v[k].inliers));
+    }
+    *n_models = (int32_t)v.size();
+  });
+}
+
+rv_status rv_estimate_multi(rv_context* c, const double* corrs, int64_t n, const rv_config* cfg, rv_estimate* out,
+                            int32_t capacity, int32_t* n_models) {
+  if (!c || !cfg || !out || !n_models || (n > 0 && !corrs)) return RV_ERR_INVALID_ARGUMENT;
+  return multi_impl(c, corrs, n, cfg, out, capacity, n_models, true);
+}
+
+rv_status rv_estimate_multi_device(rv_context* c, const double* d_corrs, int64_t n, const rv_config* cfg,
+                                   rv_estimate* out, int32_t capacity, int32_t* n_models) {
+  if (!c || !cfg || !out || !n_models || (n > 0 && !d_corrs)) return RV_ERR_INVALID_ARGUMENT;
+  return multi_impl(c, d_corrs, n, cfg, out, capacity, n_models, false);
+}
+
+rv_status rv_result_inliers(rv_context* c, int32_t model, int32_t* dst, int64_t capacity) {
+  if (!c || model < 0 || model >= (int32_t)c->results.size()) return RV_ERR_INVALID_ARGUMENT;
+  const auto& v = c->results[model];
+  if ((int64_t)v.size() > capacity || (!dst && !v.empty())) return RV_ERR_INVALID_ARGUMENT;
+  if (!v.empty()) std::memcpy(dst, v.data(), sizeof(int32_t) * v.size());
+  return RV_OK;
+}
+
+rv_status rv_preprocess(rv_context* c, const double* corrs, int64_t n, double tau_z, int32_t normalize,
+                        double* constraints_out, int32_t* kept_out, int32_t* dropped_out, int64_t* n_kept,
+                        int64_t* n_dropped) {
+  if (!c || !n_kept || !n_dropped || (n > 0 && (!corrs || !constraints_out || !kept_out || !dropped_out)))
+    return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    *n_kept = 0;
+    *n_dropped = 0;
+    if (n == 0) return;
+    const double* d = upload_corrs(c, corrs, n);
+    const PreResult r = preprocess_dev(c, d, n, tau_z, normalize);
+    std::vector<double> sx(r.cs.n), sy(r.cs.n), sz(r.cs.n);
+    if (r.cs.n) {
+      ck(cudaMemcpyAsync(sx.data(), r.cs.zx, 8 * r.cs.n, cudaMemcpyDeviceToHost, c->st), "D2H");
+      ck(cudaMemcpyAsync(sy.data(), r.cs.zy, 8 * r.cs.n, cudaMemcpyDeviceToHost, c->st), "D2H");
+      ck(cudaMemcpyAsync(sz.data(), r.cs.zz, 8 * r.cs.n, cudaMemcpyDeviceToHost, c->st), "D2H");
+      ck(cudaMemcpyAsync(kept_out, r.cs.kept, 4 * r.cs.n, cudaMemcpyDeviceToHost, c->st), "D2H");
+    }
+    if (r.n_dropped)
+      ck(cudaMemcpyAsync(dropped_out, c->dropped.get<int32_t>(1), 4 * r.n_dropped, cudaMemcpyDeviceToHost, c->st),
+         "D2H");
+    sync(c);
+    for (int64_t i = 0; i < r.cs.n; ++i) {
+      constraints_out[3 * i] = sx[i];
+      constraints_out[3 * i + 1] = sy[i];
+      constraints_out[3 * i + 2] = sz[i];
+    }
+    *n_kept = r.cs.n;
+    *n_dropped = r.n_dropped;
+    if (r.cs.n == 0) fail(RV_ERR_ALL_DEGENERATE, "every correspondence pair is degenerate (x ~ y)");
+  });
+}
+
+rv_status rv_accumulate(rv_context* c, const double* z, int64_t n, int32_t grid, double extent, int32_t samples,
+                        uint32_t* counts_out) {
+  if (!c || (n > 0 && !z) || !counts_out) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no constraints to accumulate");
+    if (grid < 1 || !(extent > 0.0)) fail(RV_ERR_INVALID_CONFIG, "accumulator needs grid >= 1, extent > 0");
+    const ConstraintSet cs = upload_constraints(c, z, n);
+    const uint32_t* g = vote(c, cs.zx, cs.zy, cs.zz, n, grid, extent, samples);
+    ck(cudaMemcpyAsync(counts_out, g, sizeof(uint32_t) * (size_t)grid * grid, cudaMemcpyDeviceToHost, c->st), "D2H grid");
+    sync(c);
+  });
+}
+
+rv_status rv_accumulate_device(rv_context* c, const double* d_z, int64_t n, int32_t grid, double extent,
+                               int32_t samples, uint32_t* d_counts) {
+  if (!c || (n > 0 && !d_z) || !d_counts) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    // d_z: n x 3 AoS on the device -> SoA copies (strided device-to-device)
+    double* dx = c->zx.get<double>(n);
+    double* dy = c->zy.get<double>(n);
+    double* dz = c->zz.get<double>(n);
+    ck(cudaMemcpy2DAsync(dx, 8, d_z, 24, 8, n, cudaMemcpyDeviceToDevice, c->st), "soa x");
+    ck(cudaMemcpy2DAsync(dy, 8, d_z + 1, 24, 8, n, cudaMemcpyDeviceToDevice, c->st), "soa y");
+    ck(cudaMemcpy2DAsync(dz, 8, d_z + 2, 24, 8, n, cudaMemcpyDeviceToDevice, c->st), "soa z");
+    const uint32_t* g = vote(c, dx, dy, dz, n, grid, extent, samples);
+    ck(cudaMemcpyAsync(d_counts, g, sizeof(uint32_t) * (size_t)grid * grid, cudaMemcpyDeviceToDevice, c->st), "D2D");
+  });
+}
+
+rv_status rv_deposit_circle_votes(rv_context* c, const double z[3], uint32_t* counts, int32_t grid, double extent,
+                                  int32_t samples) {
+  if (!c || !z || !counts) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (grid < 1 || !(extent > 0.0)) fail(RV_ERR_INVALID_CONFIG, "accumulator needs grid >= 1, extent > 0");
+    ensure_tables(c, samples);
+    const VotePlan p = make_plan(c, grid, extent, samples);
+    uint32_t* g = c->grid.get<uint32_t>((size_t)grid * grid);
+    double* dz = c->user_z.get<double>(3);
+    ck(cudaMemcpyAsync(g, counts, sizeof(uint32_t) * (size_t)grid * grid, cudaMemcpyHostToDevice, c->st), "H2D");
+    ck(cudaMemcpyAsync(dz, z, 24, cudaMemcpyHostToDevice, c->st), "H2D");
+    launch_deposit_one(p, dz, c->table64.get<double2>(samples), g, c->st);
+    count_launch(c);
+    ck(cudaMemcpyAsync(counts, g, sizeof(uint32_t) * (size_t)grid * grid, cudaMemcpyDeviceToHost, c->st), "D2H");
+    sync(c);
+  });
+}
+
+rv_status rv_find_peaks(rv_context* c, const uint32_t* counts, int32_t grid, double extent, int32_t max_peaks,
+                        int32_t radius, uint32_t min_votes, rv_peak* out, int32_t* n_out) {
+  if (!c || !counts || !n_out || (max_peaks > 0 && !out)) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    *n_out = 0;
+    if (grid < 1 || !(extent > 0.0)) fail(RV_ERR_INVALID_CONFIG, "accumulator needs grid >= 1, extent > 0");
+    uint32_t* g = c->grid.get<uint32_t>((size_t)grid * grid);
+    ck(cudaMemcpyAsync(g, counts, sizeof(uint32_t) * (size_t)grid * grid, cudaMemcpyHostToDevice, c->st), "H2D");
+    const auto ps = find_peaks_dev(c, g, grid, extent, max_peaks, radius, min_votes);
+    for (size_t k = 0; k < ps.size(); ++k) out[k] = {ps[k].ix, ps[k].iy, ps[k].A, ps[k].B, ps[k].votes};
+    *n_out = (int32_t)ps.size();
+  });
+}
+
+rv_status rv_blurred_argmax(rv_context* c, const uint32_t* counts, int32_t grid, double extent, int32_t radius,
+                            rv_peak* out) {
+  if (!c || !counts || !out) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (radius < 0) fail(RV_ERR_INVALID_CONFIG, "blur radius must be non-negative");
+    if (grid < 1 || !(extent > 0.0)) fail(RV_ERR_INVALID_CONFIG, "accumulator needs grid >= 1, extent > 0");
+    uint32_t* g = c->grid.get<uint32_t>((size_t)grid * grid);
+    ck(cudaMemcpyAsync(g, counts, sizeof(uint32_t) * (size_t)grid * grid, cudaMemcpyHostToDevice, c->st), "H2D");
+    const auto ps = blurred_argmax_dev(c, g, grid, extent, {radius});
+    *out = {ps[0].ix, ps[0].iy, ps[0].A, ps[0].B, ps[0].votes};
+  });
+}
+
+rv_status rv_classify_inliers(rv_context* c, const double axis[3], const double* z, int64_t n, double eps, int32_t* out,
+                              int64_t* n_out) {
+  if (!c || !axis || !n_out || (n > 0 && (!z || !out))) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    *n_out = 0;
+    if (n == 0) return;
+    const ConstraintSet cs = upload_constraints(c, z, n);
+    const Cls cl = classify_dev(c, cs, axis, eps, 0, nullptr, 2);
+    int32_t* idx = compact_dev(c, cs, cl);
+    if (cl.count) ck(cudaMemcpyAsync(out, idx, 4 * cl.count, cudaMemcpyDeviceToHost, c->st), "D2H");
+    sync(c);
+    *n_out = cl.count;
+  });
+}
+
+rv_status rv_refine_axis(rv_context* c, const double* z, int64_t n, double axis_out[3]) {
+  if (!c || !axis_out || (n > 0 && !z)) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (n < 2) fail(RV_ERR_RANK_DEFICIENT, "need at least two constraints");
+    const ConstraintSet cs = upload_constraints(c, z, n);
+    const Cls all = classify_dev(c, cs, nullptr, 0.0, 0, nullptr, 1);
+    if (!axis_from_scatter(all.scatter, axis_out)) fail(RV_ERR_RANK_DEFICIENT, "constraints span fewer than two directions");
+  });
+}
+
+rv_status rv_vote_angles(rv_context* c, const double axis[3], const double* corrs, int64_t n_corrs,
+                         const int32_t* indices, int64_t n_idx, int32_t bin_count, double tau, uint32_t* bins_out,
+                         uint64_t* contributing, uint64_t* degenerate, double* raw_out) {
+  if (!c || !axis || !bins_out || !contributing || !degenerate || (n_idx > 0 && (!indices || !corrs || !raw_out)))
+    return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (bin_count < 8) fail(RV_ERR_INVALID_CONFIG, "angle histogram needs bin_count >= 8");
+    for (int64_t k = 0; k < n_idx; ++k)
+      if (indices[k] < 0 || indices[k] >= n_corrs) fail(RV_ERR_INVALID_ARGUMENT, "index out of range");
+    const double* d = n_corrs > 0 ? upload_corrs(c, corrs, n_corrs) : c->corrs.get<double>(6);
+    int32_t* di = c->compact_out.get<int32_t>((size_t)std::max<int64_t>(n_idx, 1));
+    if (n_idx) ck(cudaMemcpyAsync(di, indices, 4 * n_idx, cudaMemcpyHostToDevice, c->st), "H2D idx");
+    uint32_t* bins = c->bins.get<uint32_t>(bin_count);
+    double* raw = c->raw.get<double>((size_t)std::max<int64_t>(n_idx, 1));
+    unsigned long long* cnt = c->angle_counts.get<unsigned long long>(2);
+    ck(cudaMemsetAsync(bins, 0, 4 * bin_count, c->st), "memset");
+    ck(cudaMemsetAsync(cnt, 0, 16, c->st), "memset");
+    if (n_idx) {
+      launch_vote_angles_k(axis, d, di, n_idx, bin_count, tau, bins, raw, cnt, c->st);
+      count_launch(c);
+    }
+    std::vector<double> hraw(n_idx);
+    unsigned long long hc[2];
+    ck(cudaMemcpyAsync(bins_out, bins, 4 * bin_count, cudaMemcpyDeviceToHost, c->st), "D2H");
+    ck(cudaMemcpyAsync(hc, cnt, 16, cudaMemcpyDeviceToHost, c->st), "D2H");
+    if (n_idx) ck(cudaMemcpyAsync(hraw.data(), raw, 8 * n_idx, cudaMemcpyDeviceToHost, c->st), "D2H");
+    sync(c);
+    int64_t m = 0;  // raw_angles keeps contributing votes only, in insertion order
+    for (int64_t k = 0; k < n_idx; ++k)
+      if (hraw[k] == hraw[k]) raw_out[m++] = hraw[k];
+    *contributing = hc[0];
+    *degenerate = hc[1];
+    if (hc[0] == 0) fail(RV_ERR_NO_VOTES, "no correspondence produced an angle vote");
+  });
+}
+
+rv_status rv_peak_angle(rv_context* c, const uint32_t* bins, int32_t bin_count, uint64_t contributing, int32_t refine,
+                        const double* raw, int64_t n_raw, double* angle_out) {
+  if (!c || !bins || !angle_out || bin_count < 1 || (n_raw > 0 && !raw)) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (contributing == 0) fail(RV_ERR_NO_VOTES, "empty angle histogram");
+    uint32_t* db = c->bins.get<uint32_t>(bin_count);
+    double* dr = c->raw.get<double>((size_t)std::max<int64_t>(n_raw, 1));
+    ck(cudaMemcpyAsync(db, bins, 4 * bin_count, cudaMemcpyHostToDevice, c->st), "H2D");
+    if (n_raw) ck(cudaMemcpyAsync(dr, raw, 8 * n_raw, cudaMemcpyHostToDevice, c->st), "H2D");
+    double* res = c->angle_result.get<double>(4);
+    launch_peak_angle_k(db, bin_count, dr, n_raw, c->angle_sums.get<double>(2 * 296), res, c->done_ptr(), c->st);
+    count_launch(c);
+    double* h = pin_d(c);
+    ck(cudaMemcpyAsync(h, res, 32, cudaMemcpyDeviceToHost, c->st), "D2H");
+    sync(c);
+    const double s = h[0], co = h[1], center = h[3];
+    if (!refine || (s == 0.0 && co == 0.0)) {
+      *angle_out = center;
+      return;
+    }
+    double mean = std::atan2(s, co);
+    if (mean <= -kPiD) mean += 2.0 * kPiD;
+    *angle_out = mean;
+  });
+}
+
+uint32_t rv_peak_vote_floor(const rv_config* cfg, int64_t n) {  // estimator.cpp:311-318
+  const double cell = 2.0 * cfg->extent / cfg->grid;
+  const double per_crossing = cfg->theta_samples * cell / (2.0 * std::numbers::pi);
+  const double floor_votes = cfg->min_votes_frac * static_cast<double>(n) * per_crossing;
+  return static_cast<uint32_t>(std::max(16.0, floor_votes));
+}
+
+void rv_rodrigues(const double axis[3], double angle, double r[9]) { rodrigues3(axis, angle, r); }
+double rv_rotation_error(const double g[9], const double o[9]) { return rotation_error3(g, o); }
+rv_status rv_project(const double p[3], double* A, double* B) {
+  return project3(p, A, B) ? RV_OK : RV_ERR_POLE_PROXIMITY;
+}
+void rv_unproject(double A, double B, double out[3]) { unproject2(A, B, out); }
+void rv_canonicalize(const double p[3], double out[3]) { canonicalize3(p, out); }
+void rv_orthonormal_basis(const double z[3], double a1[3], double a2[3]) { orthonormal_basis3(z, a1, a2); }
+rv_status rv_correspondence_angle(const double axis[3], const double x[3], const double y[3], double tau,
+                                  double* angle_out) {  // angles.cpp:36-44 (host formula; libm atan2)
+  double beta[3], gamma[3], bg[3];
+  cross3(axis, x, beta);
+  cross3(axis, y, gamma);
+  if (norm3(beta) <= tau || norm3(gamma) <= tau) return RV_ERR_DEGENERATE_PROJECTION;
+  cross3(beta, gamma, bg);
+  *angle_out = std::atan2(dot3(bg, axis), dot3(beta, gamma));
+  return RV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,142 @@
+// Internal interfaces between the host orchestration (rv_api.cpp) and the sm_100a kernels
+// (rv_kernels.cu). Not part of the public C-ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace rvb {
+
+constexpr int kMaxBands = 64;        // row bands of the smem-tiled vote kernel
+constexpr int kVoteThreads = 1024;   // threads per vote CTA (32 warps)
+constexpr int kPad = 2;              // pair-index padding of each band range (culling slack)
+constexpr int kFbqCap = 64;          // per-warp exact-fallback queue entries
+constexpr int kReduceThreads = 256;
+
+// Geometry of one accumulate call, computed on the host from (grid, extent, samples).
+struct VotePlan {
+  int G = 0;         // grid
+  int J = 0;         // theta samples
+  int halfJ = 0;     // J/2 sample pairs (twins j, j+J/2)
+  double E = 0;      // extent
+  double inv_cell = 0;  // grid / (2*extent)   (voting.cpp:30)
+  double cs = 0;        // 2*extent / grid     (voting.hpp:23)
+  float Kf = 0;      // (float) inv_cell
+  float CMf = 0;     // (float)(extent*inv_cell) + 1.5*2^13 (folds the 2^-10 rounding magic)
+  int clamp = 0;     // 1 if votes can fall outside the unit-disk rows/cols (extent <= 1)
+  int r_min = 0, r_max = 0;  // stored rows [r_min, r_max]
+  int c_min = 0, c_max = 0;  // stored cols
+  int W = 0;                 // c_max - c_min + 1
+  int n_bands = 0;
+  int H_max = 0;             // rows of the tallest band
+  int band_r0[kMaxBands + 1];   // band b stores rows [band_r0[b], band_r0[b+1])
+  float band_ylo[kMaxBands];    // plane-coordinate band limits with culling margin (+-inf at ends)
+  float band_yhi[kMaxBands];
+  float step_f = 0;             // (float)(2*pi/J)
+  int banded = 0;               // 1: smem-tiled kernel; 0: exact generic global-atomic kernel
+  size_t tile_words = 0;        // H_max * W
+  size_t smem_bytes = 0;        // dynamic smem of the vote kernel
+};
+
+// Device workspace for one accumulate (sizes grow-only, owned by the context).
+struct VoteBuffers {
+  const double* zx = nullptr;  // constraints SoA (f64)
+  const double* zy = nullptr;
+  const double* zz = nullptr;
+  float4* basis_a = nullptr;   // (a1x a1y a1z a2x) rounded to f32
+  float2* basis_b = nullptr;   // (a2y a2z)
+  uint32_t* ranges = nullptr;  // [n_bands][n][2]: (start | len<<16) x 2
+  unsigned long long* band_work = nullptr;  // [kMaxBands] pairs per band (incl. padding)
+  float2* table32 = nullptr;   // [halfJ] (cos, sin) of theta_p, rounded to f32
+  double2* table64 = nullptr;  // [J] (cos, sin) exactly as the reference (host libm)
+  uint32_t* grid = nullptr;    // [G*G] output
+  uint32_t* partials = nullptr;        // [max_slots][tile_words]
+  int32_t* slot_band = nullptr;        // [max_slots]
+  int32_t* counters = nullptr;         // [0]=slot counter, [1..kMaxBands]=chunk counters per band
+  unsigned long long* stats = nullptr; // [0]=pairs evaluated, [1]=fallback pairs
+  int max_slots = 0;
+};
+
+// K1: constraint basis (exact f64 -> f32) and band culling plan per constraint.
+void launch_plan(const VotePlan& p, const VoteBuffers& b, int64_t n, cudaStream_t s);
+// K2: band-tiled vote into smem tiles, flushed to partial slots; then tile reduction.
+void launch_vote_banded(const VotePlan& p, const VoteBuffers& b, int64_t n, int n_ctas,
+                        int chunk, cudaStream_t s);
+void launch_vote_reduce(const VotePlan& p, const VoteBuffers& b, cudaStream_t s);
+// Exact generic vote (any config): one thread per (constraint, sample), global atomics.
+void launch_vote_generic(const VotePlan& p, const VoteBuffers& b, int64_t n, cudaStream_t s);
+// Single-constraint deposit on top of an existing grid (deposit_circle_votes).
+void launch_deposit_one(const VotePlan& p, const double* z3, const double2* table64,
+                        uint32_t* grid, cudaStream_t s);
+
+// Preprocess (estimator.cpp:259-285): AoS correspondences -> SoA constraints, order-kept.
+struct PrepBuffers {
+  const double* corrs = nullptr;  // n x 6
+  double* zx = nullptr;
+  double* zy = nullptr;
+  double* zz = nullptr;
+  int32_t* kept = nullptr;
+  int32_t* dropped = nullptr;
+  unsigned long long* status = nullptr;  // [nblocks] look-back status (zeroed before launch)
+  int32_t* block_counter = nullptr;      // dynamic block id (zeroed before launch)
+  int32_t* totals = nullptr;             // [0]=n_kept [1]=n_dropped
+};
+int prep_blocks(int64_t n);
+void launch_preprocess(const PrepBuffers& b, int64_t n, double tau_z, int normalize, cudaStream_t s);
+
+// K3: peak search over a device grid (rv_peaks.cu).
+struct Disk {
+  int cx, cy;
+};
+int argmax_block_count();
+// Argmax over cells not inside any disk (radius r): key = (count << 32) | (~index), count > 0.
+void launch_argmax(const uint32_t* grid, int G, const Disk* disks, int n_disks, int r,
+                   unsigned long long* block_keys, unsigned long long* out_key, unsigned int* done,
+                   cudaStream_t s);
+int blur_block_count();
+// Box-blurred argmax for up to 8 radii at once (voting.cpp:176-216). sat: (G+1)^2 u64 scratch;
+// block_best: [blur_block_count()][8][2]; out_best: [n_radii][2] = (sum, index).
+void launch_blur_argmax(const uint32_t* grid, int G, const int* radii, int n_radii, unsigned long long* sat,
+                        unsigned long long* block_best, unsigned long long* out_best, unsigned int* done,
+                        cudaStream_t s);
+
+// K4: consensus / angle kernels (rv_refine.cu).
+struct ClassifyOut {
+  uint32_t* flags = nullptr;       // bitmask [ceil(n/32)]
+  const uint32_t* prev = nullptr;  // previous bitmask (or null)
+  int32_t* block_count = nullptr;  // [nblocks]
+  double* block_scatter = nullptr; // [nblocks][6] (xx xy xz yy yz zz) over inliers
+  int32_t* block_diff = nullptr;   // [nblocks] any flag word differs from prev
+  double* result = nullptr;        // [8]: count, differs, scatter[6]
+};
+int classify_blocks(int64_t n);
+// mode 0: classify + scatter over inliers; 1: scatter over all constraints; 2: classify only.
+void launch_classify_mode(const double* zx, const double* zy, const double* zz, int64_t n, const double axis[3],
+                          double eps, int mode, const ClassifyOut& o, int32_t* block_offsets, unsigned int* done,
+                          cudaStream_t s);
+void launch_compact_flags(const uint32_t* flags, int64_t n, const int32_t* map, const int32_t* block_offsets,
+                          int32_t* out, cudaStream_t s);
+void launch_vote_angles_k(const double axis[3], const double* corrs, const int32_t* idx, int64_t n_idx, int bin_count,
+                          double tau, uint32_t* bins, double* raw, unsigned long long* counts, cudaStream_t s);
+void launch_peak_angle_k(const uint32_t* bins, int bin_count, const double* raw, int64_t n_raw, double* block_sums,
+                         double* result, unsigned int* done, cudaStream_t s);
+void launch_model_support_k(const double* zx, const double* zy, const double* zz, const int32_t* kept,
+                            const double* corrs, int64_t n, const double axis[3], double angle, double eps, double tau,
+                            uint32_t* band_flags, int32_t* block_counts, int32_t* result, unsigned int* done,
+                            cudaStream_t s);
+void launch_strip_k(const double* zx, const double* zy, const double* zz, int64_t n, const double axis[3], double strip,
+                    uint8_t* removed, cudaStream_t s);
+void launch_strip_identity_k(const double* corrs, const int32_t* kept, int64_t n, int normalize, uint8_t* removed,
+                             cudaStream_t s);
+void launch_gather_dot_k(const double* zx, const double* zy, const double* zz, const int32_t* idx, int64_t n,
+                         const double axis[3], double* out, cudaStream_t s);
+void launch_near_identity_k(const double* corrs, const int32_t* sub_kept, int64_t n, int normalize, uint32_t* flags,
+                            int32_t* block_count, double* block_h, int32_t* block_offsets, double* result,
+                            unsigned int* done, cudaStream_t s);
+void launch_gather_residual(const double* zx, const double* zy, const double* zz, const int32_t* kept,
+                            const uint8_t* removed, int64_t n, unsigned long long* status,
+                            int32_t* block_counter, double* ozx, double* ozy, double* ozz, int32_t* okept,
+                            int32_t* total, cudaStream_t s);
+
+}  // namespace rvb

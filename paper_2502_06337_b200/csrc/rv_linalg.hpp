@@ -1,0 +1,402 @@
+// Host 3x3 linear algebra of the estimator (run on the host, as the reference does):
+//  * eigen_sym3: the smallest-eigenvector solve of refine_axis (estimator.cpp:303-308).
+//    Eigen is not vendored by the reference (version unpinned); this restates Eigen 3.4's
+//    SelfAdjointEigenSolver path for a real 3x3 matrix: scale by max |lower coefficient|,
+//    closed-form 3x3 Householder tridiagonalization, implicit symmetric QR with Wilkinson
+//    shift, ascending selection sort.
+//  * svd3: two-sided Jacobi SVD for the Kabsch fallback (estimator.cpp:198-215).
+//  * geometry of geom.cpp:10-43 with the reference's evaluation order.
+// This translation unit must be compiled without FMA contraction (-ffp-contract=off).
+#pragma once
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstring>
+
+namespace rvb {
+
+constexpr double kPiD = 3.14159265358979323846;
+
+inline double dot3(const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+inline double norm3(const double* a) { return std::sqrt(dot3(a, a)); }
+inline void normalized3(const double* a, double* o) {
+  const double n2 = dot3(a, a);
+  if (n2 > 0.0) {
+    const double s = std::sqrt(n2);
+    o[0] = a[0] / s;
+    o[1] = a[1] / s;
+    o[2] = a[2] / s;
+  } else {
+    o[0] = a[0];
+    o[1] = a[1];
+    o[2] = a[2];
+  }
+}
+inline void cross3(const double* a, const double* b, double* o) {
+  const double t0 = a[1] * b[2] - a[2] * b[1];
+  const double t1 = a[2] * b[0] - a[0] * b[2];
+  const double t2 = a[0] * b[1] - a[1] * b[0];
+  o[0] = t0;
+  o[1] = t1;
+  o[2] = t2;
+}
+inline void canonicalize3(const double* p, double* o) {  // geom.cpp:34
+  if (p[2] > 0.0) {
+    o[0] = -p[0];
+    o[1] = -p[1];
+    o[2] = -p[2];
+  } else {
+    o[0] = p[0];
+    o[1] = p[1];
+    o[2] = p[2];
+  }
+}
+inline void unproject2(double A, double B, double* o) {  // geom.cpp:29-32
+  const double s = 1.0 + A * A + B * B;
+  o[0] = 2.0 * A / s;
+  o[1] = 2.0 * B / s;
+  o[2] = (A * A + B * B - 1.0) / s;
+}
+inline bool project3(const double* p, double* A, double* B) {  // geom.cpp:21-27
+  if (p[2] >= 1.0 - 1e-9) return false;
+  const double inv = 1.0 / (1.0 - p[2]);
+  *A = p[0] * inv;
+  *B = p[1] * inv;
+  return true;
+}
+inline void backproject(double A, double B, double* o) {  // voting.cpp:172-174
+  double u[3];
+  unproject2(A, B, u);
+  normalized3(u, o);
+}
+inline void rodrigues3(const double* a, double angle, double* r) {  // geom.cpp:10-14
+  const double k[9] = {0, -a[2], a[1], a[2], 0, -a[0], -a[1], a[0], 0};
+  const double s = std::sin(angle), c1 = 1.0 - std::cos(angle);
+  double sk[9];
+  for (int i = 0; i < 9; ++i) sk[i] = c1 * k[i];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      const double p = sk[i * 3 + 0] * k[0 * 3 + j] + sk[i * 3 + 1] * k[1 * 3 + j] + sk[i * 3 + 2] * k[2 * 3 + j];
+      const double id = (i == j) ? 1.0 : 0.0;
+      r[i * 3 + j] = (id + s * k[i * 3 + j]) + p;
+    }
+}
+inline double rotation_error3(const double* g, const double* o) {  // geom.cpp:16-19
+  double tr = 0.0;
+  for (int i = 0; i < 3; ++i) {
+    const double d = g[0 * 3 + i] * o[0 * 3 + i] + g[1 * 3 + i] * o[1 * 3 + i] + g[2 * 3 + i] * o[2 * 3 + i];
+    tr = (i == 0) ? d : tr + d;
+  }
+  double c = 0.5 * (tr - 1.0);
+  c = std::min(1.0, std::max(-1.0, c));
+  return std::acos(c);
+}
+inline void orthonormal_basis3(const double* z, double* a1, double* a2) {  // geom.cpp:36-43
+  int least = 0;
+  const double az[3] = {std::fabs(z[0]), std::fabs(z[1]), std::fabs(z[2])};
+  for (int i = 1; i < 3; ++i)
+    if (az[i] < az[least]) least = i;
+  double seed[3] = {0, 0, 0};
+  seed[least] = 1.0;
+  const double s = dot3(seed, z);
+  double v[3];
+  for (int i = 0; i < 3; ++i) v[i] = seed[i] - s * z[i];
+  normalized3(v, a1);
+  cross3(z, a1, a2);
+}
+
+inline void givens(double p, double q, double* c, double* s) {
+  if (q == 0.0) {
+    *c = p < 0.0 ? -1.0 : 1.0;
+    *s = 0.0;
+  } else if (p == 0.0) {
+    *c = 0.0;
+    *s = q < 0.0 ? 1.0 : -1.0;
+  } else if (std::fabs(p) > std::fabs(q)) {
+    const double t = q / p;
+    double u = std::sqrt(1.0 + t * t);
+    if (p < 0.0) u = -u;
+    *c = 1.0 / u;
+    *s = -t * *c;
+  } else {
+    const double t = p / q;
+    double u = std::sqrt(1.0 + t * t);
+    if (q < 0.0) u = -u;
+    *s = -1.0 / u;
+    *c = -t * *s;
+  }
+}
+
+// Symmetric 3x3 eigen-decomposition; sm row-major (lower triangle read). evecs row-major,
+// eigenvector k = column k; eigenvalues ascending.
+inline void eigen_sym3(const double sm[9], double evals[3], double ev[9]) {
+  double m[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  for (int j = 0; j < 3; ++j)
+    for (int i = j; i < 3; ++i) m[i][j] = sm[i * 3 + j];
+  double scale = 0.0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) scale = std::fabs(m[i][j]) > scale ? std::fabs(m[i][j]) : scale;
+  if (scale == 0.0) scale = 1.0;
+  for (int j = 0; j < 3; ++j)
+    for (int i = j; i < 3; ++i) m[i][j] /= scale;
+  double diag[3], sub[2], q[3][3];
+  diag[0] = m[0][0];
+  const double v1norm2 = m[2][0] * m[2][0];
+  if (v1norm2 <= DBL_MIN) {
+    diag[1] = m[1][1];
+    diag[2] = m[2][2];
+    sub[0] = m[1][0];
+    sub[1] = m[2][1];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) q[i][j] = (i == j) ? 1.0 : 0.0;
+  } else {
+    const double beta = std::sqrt(m[1][0] * m[1][0] + v1norm2);
+    const double inv_beta = 1.0 / beta;
+    const double m01 = m[1][0] * inv_beta;
+    const double m02 = m[2][0] * inv_beta;
+    const double qq = 2.0 * m01 * m[2][1] + m02 * (m[2][2] - m[1][1]);
+    diag[1] = m[1][1] + m02 * qq;
+    diag[2] = m[2][2] - m02 * qq;
+    sub[0] = beta;
+    sub[1] = m[2][1] - m01 * qq;
+    const double qi[3][3] = {{1, 0, 0}, {0, m01, m02}, {0, m02, -m01}};
+    std::memcpy(q, qi, sizeof q);
+  }
+  int end = 2, start = 0, iter = 0;
+  const double precision_inv = 1.0 / DBL_EPSILON;
+  while (end > 0) {
+    for (int i = start; i < end; ++i) {
+      if (std::fabs(sub[i]) < DBL_MIN) {
+        sub[i] = 0.0;
+      } else {
+        const double scaled = precision_inv * sub[i];
+        if (scaled * scaled <= (std::fabs(diag[i]) + std::fabs(diag[i + 1]))) sub[i] = 0.0;
+      }
+    }
+    while (end > 0 && sub[end - 1] == 0.0) end--;
+    if (end <= 0) break;
+    if (++iter > 30 * 3) break;
+    start = end - 1;
+    while (start > 0 && sub[start - 1] != 0.0) start--;
+    const double td = (diag[end - 1] - diag[end]) * 0.5;
+    const double e = sub[end - 1];
+    double mu = diag[end];
+    if (td == 0.0) {
+      mu -= std::fabs(e);
+    } else if (e != 0.0) {
+      const double e2 = e * e;
+      const double h = std::hypot(td, e);
+      if (e2 == 0.0)
+        mu -= e / ((td + (td > 0.0 ? h : -h)) / e);
+      else
+        mu -= e2 / (td + (td > 0.0 ? h : -h));
+    }
+    double x = diag[start] - mu;
+    double z = sub[start];
+    for (int k = start; k < end && z != 0.0; ++k) {
+      double c, s;
+      givens(x, z, &c, &s);
+      const double sdk = s * diag[k] + c * sub[k];
+      const double dkp1 = s * sub[k] + c * diag[k + 1];
+      diag[k] = c * (c * diag[k] - s * sub[k]) - s * (c * sub[k] - s * diag[k + 1]);
+      diag[k + 1] = s * sdk + c * dkp1;
+      sub[k] = c * sdk - s * dkp1;
+      if (k > start) sub[k - 1] = c * sub[k - 1] - s * z;
+      x = sub[k];
+      if (k < end - 1) {
+        z = -s * sub[k + 1];
+        sub[k + 1] = c * sub[k + 1];
+      }
+      for (int i = 0; i < 3; ++i) {
+        const double qa = q[i][k], qb = q[i][k + 1];
+        q[i][k] = c * qa - s * qb;
+        q[i][k + 1] = s * qa + c * qb;
+      }
+    }
+  }
+  for (int i = 0; i < 2; ++i) {
+    int k = i;
+    for (int j = i + 1; j < 3; ++j)
+      if (diag[j] < diag[k]) k = j;
+    if (k != i) {
+      std::swap(diag[i], diag[k]);
+      for (int r = 0; r < 3; ++r) std::swap(q[r][i], q[r][k]);
+    }
+  }
+  for (int i = 0; i < 3; ++i) evals[i] = diag[i] * scale;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) ev[i * 3 + j] = q[i][j];
+}
+
+// refine_axis from scatter sums (xx xy xz yy yz zz), estimator.cpp:303-308. false = RankDeficient.
+inline bool axis_from_scatter(const double s6[6], double axis[3]) {
+  const double sm[9] = {s6[0], s6[1], s6[2], s6[1], s6[3], s6[4], s6[2], s6[4], s6[5]};
+  double evals[3], ev[9];
+  eigen_sym3(sm, evals, ev);
+  if (evals[1] <= 1e-10 * std::max(evals[2], 1e-300)) return false;
+  const double v0[3] = {ev[0], ev[3], ev[6]};
+  double nv[3];
+  normalized3(v0, nv);
+  canonicalize3(nv, axis);
+  return true;
+}
+
+// Two-sided Jacobi SVD of a 3x3 (row-major); u, v row-major, singular values descending.
+inline void svd3(const double a[9], double u[9], double v[9]) {
+  double w[3][3], U[3][3], V[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      w[i][j] = a[i * 3 + j];
+      U[i][j] = V[i][j] = (i == j) ? 1.0 : 0.0;
+    }
+  const double prec = 2.0 * DBL_EPSILON;
+  double max_diag = 0;
+  for (int i = 0; i < 3; ++i) max_diag = std::max(max_diag, std::fabs(w[i][i]));
+  bool finished = false;
+  for (int sweeps = 0; !finished && sweeps < 100; ++sweeps) {
+    finished = true;
+    for (int p = 1; p < 3; ++p)
+      for (int qi = 0; qi < p; ++qi) {
+        const double thr = std::max(4.9e-324, prec * max_diag);
+        if (std::fabs(w[p][qi]) > thr || std::fabs(w[qi][p]) > thr) {
+          finished = false;
+          const double m00 = w[qi][qi], m01 = w[qi][p], m10 = w[p][qi], m11 = w[p][p];
+          double c1 = 1, s1 = 0;
+          const double t = m00 + m11, d = m10 - m01;
+          if (std::fabs(d) >= DBL_MIN) {
+            const double uu = t / d;
+            const double tmp = std::sqrt(1.0 + uu * uu);
+            s1 = 1.0 / tmp;
+            c1 = uu / tmp;
+          }
+          const double n00 = c1 * m00 + s1 * m10, n01 = c1 * m01 + s1 * m11;
+          const double n11 = -s1 * m01 + c1 * m11;
+          double jc = 1, js = 0;
+          const double deno = 2.0 * std::fabs(n01);
+          if (deno >= DBL_MIN) {
+            const double tau = (n00 - n11) / deno;
+            const double ww = std::sqrt(tau * tau + 1.0);
+            const double tt = tau > 0.0 ? 1.0 / (tau + ww) : 1.0 / (tau - ww);
+            const double sign_t = tt > 0.0 ? 1.0 : -1.0;
+            const double nn = 1.0 / std::sqrt(tt * tt + 1.0);
+            js = -sign_t * (n01 / std::fabs(n01)) * std::fabs(tt) * nn;
+            jc = nn;
+          }
+          const double lc = c1 * jc - s1 * (-js), ls = c1 * (-js) + s1 * jc;
+          for (int k = 0; k < 3; ++k) {
+            const double x = w[qi][k], y = w[p][k];
+            w[qi][k] = lc * x + ls * y;
+            w[p][k] = -ls * x + lc * y;
+          }
+          for (int k = 0; k < 3; ++k) {
+            const double x = U[k][qi], y = U[k][p];
+            U[k][qi] = lc * x + ls * y;
+            U[k][p] = -ls * x + lc * y;
+          }
+          for (int k = 0; k < 3; ++k) {
+            double x = w[k][qi], y = w[k][p];
+            w[k][qi] = jc * x - js * y;
+            w[k][p] = js * x + jc * y;
+            x = V[k][qi];
+            y = V[k][p];
+            V[k][qi] = jc * x - js * y;
+            V[k][p] = js * x + jc * y;
+          }
+          max_diag = std::max(max_diag, std::max(std::fabs(w[p][p]), std::fabs(w[qi][qi])));
+        }
+      }
+  }
+  double sv[3];
+  for (int i = 0; i < 3; ++i) {
+    sv[i] = std::fabs(w[i][i]);
+    if (w[i][i] < 0.0)
+      for (int k = 0; k < 3; ++k) U[k][i] = -U[k][i];
+  }
+  for (int i = 0; i < 3; ++i) {
+    int best = i;
+    for (int j = i + 1; j < 3; ++j)
+      if (sv[j] > sv[best]) best = j;
+    if (best != i) {
+      std::swap(sv[i], sv[best]);
+      for (int k = 0; k < 3; ++k) {
+        std::swap(U[k][i], U[k][best]);
+        std::swap(V[k][i], V[k][best]);
+      }
+    }
+  }
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      u[i * 3 + j] = U[i][j];
+      v[i * 3 + j] = V[i][j];
+    }
+}
+
+inline void mat3_mul(const double* a, const double* b, double* o) {
+  double t[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) t[i * 3 + j] = a[i * 3 + 0] * b[0 * 3 + j] + a[i * 3 + 1] * b[1 * 3 + j] + a[i * 3 + 2] * b[2 * 3 + j];
+  std::memcpy(o, t, sizeof t);
+}
+inline void mat3_t(const double* a, double* o) {
+  double t[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) t[j * 3 + i] = a[i * 3 + j];
+  std::memcpy(o, t, sizeof t);
+}
+inline double det3(const double* m) {
+  return m[0] * (m[4] * m[8] - m[7] * m[5]) - m[3] * (m[1] * m[8] - m[7] * m[2]) + m[6] * (m[1] * m[5] - m[4] * m[2]);
+}
+
+// Kabsch from a cross-covariance h (estimator.cpp:211-214).
+inline void kabsch(const double h[9], double r[9]) {
+  double u[9], v[9], vt[9], uvt[9], d[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  svd3(h, u, v);
+  mat3_t(v, vt);
+  mat3_mul(u, vt, uvt);
+  d[8] = det3(uvt) < 0.0 ? -1.0 : 1.0;
+  double ud[9];
+  mat3_mul(u, d, ud);
+  mat3_mul(ud, vt, r);
+}
+
+// AngleAxisd(r) via Quaternion(r) (Eigen), then the canonical axis/angle of estimator.cpp:242-244.
+inline void angle_axis_canonical(const double r[9], double axis[3], double* angle) {
+  double qw, qv[3];
+  double t = r[0] + r[4] + r[8];
+  if (t > 0.0) {
+    t = std::sqrt(t + 1.0);
+    qw = 0.5 * t;
+    t = 0.5 / t;
+    qv[0] = (r[7] - r[5]) * t;
+    qv[1] = (r[2] - r[6]) * t;
+    qv[2] = (r[3] - r[1]) * t;
+  } else {
+    int i = 0;
+    if (r[4] > r[0]) i = 1;
+    if (r[8] > r[i * 4]) i = 2;
+    const int j = (i + 1) % 3, k = (j + 1) % 3;
+    t = std::sqrt(r[i * 4] - r[j * 4] - r[k * 4] + 1.0);
+    qv[i] = 0.5 * t;
+    t = 0.5 / t;
+    qw = (r[k * 3 + j] - r[j * 3 + k]) * t;
+    qv[j] = (r[j * 3 + i] + r[i * 3 + j]) * t;
+    qv[k] = (r[k * 3 + i] + r[i * 3 + k]) * t;
+  }
+  double n = norm3(qv), aa_angle, aa_axis[3];
+  if (n != 0.0) {
+    aa_angle = 2.0 * std::atan2(n, std::fabs(qw));
+    if (qw < 0.0) n = -n;
+    aa_axis[0] = qv[0] / n;
+    aa_axis[1] = qv[1] / n;
+    aa_axis[2] = qv[2] / n;
+  } else {
+    aa_angle = 0.0;
+    aa_axis[0] = 1.0;
+    aa_axis[1] = 0.0;
+    aa_axis[2] = 0.0;
+  }
+  canonicalize3(aa_axis, axis);
+  *angle = dot3(axis, aa_axis) < 0.0 ? -aa_angle : aa_angle;
+}
+
+}  // namespace rvb

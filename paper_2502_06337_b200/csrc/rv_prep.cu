@@ -1,0 +1,145 @@
+// K1a: preprocess (estimator.cpp:259-285) in one HBM pass.
+//
+// Reads the reference's AoS correspondence layout (48 B/pair, 3 x 16 B vector loads per
+// thread), normalises x and y, forms z = (y-x)/|y-x| with the reference's exact f64 op order,
+// and writes kept constraints as SoA f64 in input order (order-preserving compaction by a
+// single-pass decoupled look-back scan), the kept index map and the dropped index list.
+// Algorithmic bytes: 48 B read + 24 B (z) + 4 B (kept) written per kept pair = 76 B.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "rv_exact.cuh"
+#include "rv_internal.h"
+#include "rv_scan.cuh"
+
+namespace rvb {
+namespace {
+
+constexpr int kPrepThreads = 256;
+
+template <bool kVec>
+__global__ void __launch_bounds__(kPrepThreads) preprocess_kernel(PrepBuffers b, int64_t n, double tau_z,
+                                                                  int normalize) {
+  __shared__ int s_bid;
+  __shared__ int s_warp_kept[kPrepThreads / 32];
+  __shared__ long long s_excl;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_bid = atomicAdd(b.block_counter, 1);
+  __syncthreads();
+  const int bid = s_bid;
+  const int64_t i = (int64_t)bid * kPrepThreads + tid;
+  double x0 = 0, x1 = 0, x2 = 0, y0 = 0, y1 = 0, y2 = 0;
+  bool valid = i < n;
+  if (valid) {
+    if (kVec) {
+      const double2* p = reinterpret_cast<const double2*>(b.corrs + 6 * i);
+      const double2 u = p[0], v = p[1], w = p[2];
+      x0 = u.x; x1 = u.y; x2 = v.x; y0 = v.y; y1 = w.x; y2 = w.y;
+    } else {
+      const double* p = b.corrs + 6 * i;
+      x0 = p[0]; x1 = p[1]; x2 = p[2]; y0 = p[3]; y1 = p[4]; y2 = p[5];
+    }
+  }
+  if (normalize) {
+    const double nx = __dsqrt_rn(xdot(x0, x1, x2, x0, x1, x2));
+    const double ny = __dsqrt_rn(xdot(y0, y1, y2, y0, y1, y2));
+    if (nx > 0.0) { x0 = xd(x0, nx); x1 = xd(x1, nx); x2 = xd(x2, nx); }
+    if (ny > 0.0) { y0 = xd(y0, ny); y1 = xd(y1, ny); y2 = xd(y2, ny); }
+  }
+  const double d0 = xs(y0, x0), d1 = xs(y1, x1), d2 = xs(y2, x2);
+  const double len = __dsqrt_rn(xdot(d0, d1, d2, d0, d1, d2));
+  const bool drop = valid && (len < tau_z);
+  const bool keep = valid && !drop;
+  const unsigned km = __ballot_sync(0xFFFFFFFFu, keep);
+  if (lane == 0) s_warp_kept[warp] = __popc(km);
+  __syncthreads();
+  int before = 0, total = 0;
+  for (int w = 0; w < kPrepThreads / 32; ++w) {
+    const int c = s_warp_kept[w];
+    if (w < warp) before += c;
+    total += c;
+  }
+  if (warp == 0) {
+    const long long e = lookback_exclusive(reinterpret_cast<unsigned long long*>(b.status), bid, total);
+    if (lane == 0) s_excl = e;
+  }
+  __syncthreads();
+  const long long excl = s_excl;
+  const long long rank = excl + before + __popc(km & ((1u << lane) - 1u));
+  if (keep) {
+    b.zx[rank] = xd(d0, len);
+    b.zy[rank] = xd(d1, len);
+    b.zz[rank] = xd(d2, len);
+    b.kept[rank] = (int32_t)i;
+  } else if (drop) {
+    b.dropped[i - rank] = (int32_t)i;
+  }
+  const int64_t block_end = (int64_t)(bid + 1) * kPrepThreads;
+  if (tid == 0 && block_end >= n) {  // the last block publishes the totals
+    b.totals[0] = (int32_t)(excl + total);
+    b.totals[1] = (int32_t)(n - (excl + total));
+  }
+}
+
+constexpr int kGatherThreads = 256;
+
+__global__ void __launch_bounds__(kGatherThreads)
+    gather_residual_kernel(const double* zx, const double* zy, const double* zz, const int32_t* kept,
+                           const uint8_t* removed, int64_t n, unsigned long long* status, int32_t* block_counter,
+                           double* ozx, double* ozy, double* ozz, int32_t* okept, int32_t* total_out) {
+  __shared__ int s_bid;
+  __shared__ int s_warp[kGatherThreads / 32];
+  __shared__ long long s_excl;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_bid = atomicAdd(block_counter, 1);
+  __syncthreads();
+  const int bid = s_bid;
+  const int64_t i = (int64_t)bid * kGatherThreads + tid;
+  const bool keep = i < n && !removed[i];
+  const unsigned km = __ballot_sync(0xFFFFFFFFu, keep);
+  if (lane == 0) s_warp[warp] = __popc(km);
+  __syncthreads();
+  int before = 0, total = 0;
+  for (int w = 0; w < kGatherThreads / 32; ++w) {
+    const int c = s_warp[w];
+    if (w < warp) before += c;
+    total += c;
+  }
+  if (warp == 0) {
+    const long long e = lookback_exclusive(status, bid, total);
+    if (lane == 0) s_excl = e;
+  }
+  __syncthreads();
+  const long long rank = s_excl + before + __popc(km & ((1u << lane) - 1u));
+  if (keep) {
+    ozx[rank] = zx[i];
+    ozy[rank] = zy[i];
+    ozz[rank] = zz[i];
+    okept[rank] = kept[i];
+  }
+  if (tid == 0 && (int64_t)(bid + 1) * kGatherThreads >= n) *total_out = (int32_t)(s_excl + total);
+}
+
+}  // namespace
+
+int prep_blocks(int64_t n) { return (int)((n + kPrepThreads - 1) / kPrepThreads); }
+
+void launch_preprocess(const PrepBuffers& b, int64_t n, double tau_z, int normalize, cudaStream_t s) {
+  const int blocks = prep_blocks(n);
+  const bool vec = (reinterpret_cast<uintptr_t>(b.corrs) & 15u) == 0;
+  if (vec)
+    preprocess_kernel<true><<<blocks, kPrepThreads, 0, s>>>(b, n, tau_z, normalize);
+  else
+    preprocess_kernel<false><<<blocks, kPrepThreads, 0, s>>>(b, n, tau_z, normalize);
+}
+
+void launch_gather_residual(const double* zx, const double* zy, const double* zz, const int32_t* kept,
+                            const uint8_t* removed, int64_t n, unsigned long long* status, int32_t* block_counter,
+                            double* ozx, double* ozy, double* ozz, int32_t* okept, int32_t* total, cudaStream_t s) {
+  const int blocks = (int)((n + kGatherThreads - 1) / kGatherThreads);
+  gather_residual_kernel<<<blocks, kGatherThreads, 0, s>>>(zx, zy, zz, kept, removed, n, status, block_counter,
+                                                           ozx, ozy, ozz, okept, total);
+}
+
+}  // namespace rvb

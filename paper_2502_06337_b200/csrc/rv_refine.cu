@@ -1,0 +1,653 @@
+// K4: consensus and angle kernels.
+//  * classify (estimator.cpp:287-297): |ax*zx + ay*zy + az*zz| < eps, strict, exact f64
+//    op order -> inlier bitmask; fused with the scatter partial sums of refine_axis
+//    (estimator.cpp:299-302) over the same inliers and a "set changed" test against the
+//    previous bitmask (refine_loop's next_inl == inl, estimator.cpp:64).
+//  * compaction of a bitmask into ascending (optionally kept-mapped) indices.
+//  * vote_angles / peak_angle sums (angles.cpp:36-90) and model_support (estimator.cpp:117-137).
+// Floating-point partial sums are reduced in a fixed tree order (deterministic run to run).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "rv_exact.cuh"
+#include "rv_internal.h"
+
+namespace rvb {
+namespace {
+
+constexpr int kClsThreads = 256;
+constexpr int kClsPerThread = 4;
+constexpr int kClsPerBlock = kClsThreads * kClsPerThread;  // 1024 elements = 32 flag words
+constexpr double kPi = 3.14159265358979323846;
+
+template <int K>
+__device__ __forceinline__ void block_sum(double (&v)[K], double (*s)[kClsThreads / 32]) {
+  // fixed-shape tree: warp xor-shuffle, then warp 0 over warp partials
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    for (int o = 16; o > 0; o >>= 1) v[k] = __dadd_rn(v[k], __shfl_xor_sync(0xFFFFFFFFu, v[k], o));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) s[k][warp] = v[k];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double t = lane < kClsThreads / 32 ? s[k][lane] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) t = __dadd_rn(t, __shfl_xor_sync(0xFFFFFFFFu, t, o));
+      v[k] = t;
+    }
+  }
+  __syncthreads();
+}
+
+struct ClsArgs {
+  const double* zx;
+  const double* zy;
+  const double* zz;
+  int64_t n;
+  double ax, ay, az, eps;
+  int mode;  // 0 classify, 1 all constraints (refine_axis(constraints)), 2 classify w/o scatter
+  uint32_t* flags;
+  const uint32_t* prev;
+  int32_t* block_count;
+  double* block_scatter;
+  int32_t* block_diff;
+  int32_t* block_offsets;  // exclusive scan of block_count (written by the last block)
+  double* result;          // [0]=count [1]=differs [2..7]=scatter
+  unsigned int* done;
+};
+
+__global__ void __launch_bounds__(kClsThreads) classify_kernel(ClsArgs a) {
+  __shared__ double s_red[6][kClsThreads / 32];
+  __shared__ int s_cnt[kClsThreads / 32], s_diff[kClsThreads / 32];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kClsPerBlock;
+  double sc[6] = {0, 0, 0, 0, 0, 0};
+  int cnt = 0, diff = 0;
+#pragma unroll
+  for (int r = 0; r < kClsPerThread; ++r) {
+    const int64_t i = base + r * kClsThreads + tid;
+    bool in = false;
+    double z0 = 0, z1 = 0, z2 = 0;
+    if (i < a.n) {
+      z0 = a.zx[i];
+      z1 = a.zy[i];
+      z2 = a.zz[i];
+      if (a.mode == 1) {
+        in = true;
+      } else {
+        const double d = xa(xa(xm(a.ax, z0), xm(a.ay, z1)), xm(a.az, z2));
+        in = fabs(d) < a.eps;
+      }
+    }
+    const unsigned word = __ballot_sync(0xFFFFFFFFu, in);
+    const int64_t wi = (base + r * kClsThreads + warp * 32) >> 5;
+    if (lane == 0 && a.mode != 1 && (base + r * kClsThreads + warp * 32) < a.n) {
+      a.flags[wi] = word;
+      if (a.prev && a.prev[wi] != word) diff = 1;
+    }
+    if (in) {
+      ++cnt;
+      if (a.mode != 2) {
+        sc[0] = xa(sc[0], xm(z0, z0));
+        sc[1] = xa(sc[1], xm(z0, z1));
+        sc[2] = xa(sc[2], xm(z0, z2));
+        sc[3] = xa(sc[3], xm(z1, z1));
+        sc[4] = xa(sc[4], xm(z1, z2));
+        sc[5] = xa(sc[5], xm(z2, z2));
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
+  diff = __any_sync(0xFFFFFFFFu, diff);
+  if (lane == 0) {
+    s_cnt[warp] = cnt;
+    s_diff[warp] = diff;
+  }
+  if (a.mode != 2) block_sum<6>(sc, s_red);
+  else __syncthreads();
+  if (tid == 0) {
+    int c = 0, d = 0;
+    for (int w = 0; w < kClsThreads / 32; ++w) {
+      c += s_cnt[w];
+      d |= s_diff[w];
+    }
+    a.block_count[blockIdx.x] = c;
+    a.block_diff[blockIdx.x] = d;
+    if (a.mode != 2)
+      for (int k = 0; k < 6; ++k) a.block_scatter[(size_t)blockIdx.x * 6 + k] = sc[k];
+    __threadfence();
+    s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // last block: fixed-order reduction over blocks + exclusive scan of block counts
+  const int nb = gridDim.x;
+  volatile int32_t* bc = a.block_count;
+  volatile int32_t* bd = a.block_diff;
+  volatile double* bs = a.block_scatter;
+  double v[6] = {0, 0, 0, 0, 0, 0};
+  long long tc = 0;
+  int td = 0;
+  // each thread owns a contiguous run of blocks (sequential), then a fixed tree across threads
+  const int per = (nb + kClsThreads - 1) / kClsThreads;
+  const int b0 = tid * per, b1 = min(nb, b0 + per);
+  for (int b = b0; b < b1; ++b) {
+    tc += bc[b];
+    td |= bd[b];
+    if (a.mode != 2)
+      for (int k = 0; k < 6; ++k) v[k] = xa(v[k], bs[(size_t)b * 6 + k]);
+  }
+  // exclusive scan of per-thread run totals
+  __shared__ long long s_run[kClsThreads];
+  s_run[tid] = tc;
+  __syncthreads();
+  if (tid == 0) {
+    long long acc = 0;
+    for (int t = 0; t < kClsThreads; ++t) {
+      const long long x = s_run[t];
+      s_run[t] = acc;
+      acc += x;
+    }
+  }
+  __syncthreads();
+  long long off = s_run[tid];
+  for (int b = b0; b < b1; ++b) {
+    a.block_offsets[b] = (int32_t)off;
+    off += bc[b];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    tc += __shfl_xor_sync(0xFFFFFFFFu, tc, o);
+    td |= __shfl_xor_sync(0xFFFFFFFFu, td, o);
+  }
+  __shared__ long long s_tc[kClsThreads / 32];
+  __shared__ int s_td[kClsThreads / 32];
+  if (lane == 0) {
+    s_tc[warp] = tc;
+    s_td[warp] = td;
+  }
+  if (a.mode != 2) block_sum<6>(v, s_red);
+  else __syncthreads();
+  if (tid == 0) {
+    long long c = 0;
+    int d = 0;
+    for (int w = 0; w < kClsThreads / 32; ++w) {
+      c += s_tc[w];
+      d |= s_td[w];
+    }
+    a.result[0] = (double)c;
+    a.result[1] = (double)d;
+    for (int k = 0; k < 6; ++k) a.result[2 + k] = a.mode != 2 ? v[k] : 0.0;
+    *a.done = 0u;
+  }
+}
+
+// bitmask -> ascending indices (through map if given). Uses block_offsets from classify.
+__global__ void __launch_bounds__(kClsThreads) compact_kernel(const uint32_t* flags, int64_t n, const int32_t* map,
+                                                             const int32_t* block_offsets, int32_t* out) {
+  __shared__ int s_pref[kClsPerBlock / 32 + 1];
+  const int tid = threadIdx.x;
+  const int64_t wbase = (int64_t)blockIdx.x * (kClsPerBlock / 32);
+  const int64_t nwords = (n + 31) / 32;
+  if (tid == 0) {
+    int acc = 0;
+    for (int w = 0; w < kClsPerBlock / 32; ++w) {
+      s_pref[w] = acc;
+      if (wbase + w < nwords) acc += __popc(flags[wbase + w]);
+    }
+    s_pref[kClsPerBlock / 32] = acc;
+  }
+  __syncthreads();
+  const int lane = tid & 31, warp = tid >> 5;
+  const int off = block_offsets[blockIdx.x];
+  for (int w = warp; w < kClsPerBlock / 32; w += kClsThreads / 32) {
+    if (wbase + w >= nwords) break;
+    const uint32_t word = flags[wbase + w];
+    if ((word >> lane) & 1u) {
+      const int64_t i = (wbase + w) * 32 + lane;
+      const int pos = off + s_pref[w] + __popc(word & ((1u << lane) - 1u));
+      out[pos] = map ? map[i] : (int32_t)i;
+    }
+  }
+}
+
+// correspondence_angle, angles.cpp:36-44, exact op order (atan2 is CUDA's, <= 2 ulp).
+__device__ __forceinline__ bool corr_angle(double a0, double a1, double a2, const double* c, double tau,
+                                           double* out) {
+  const double x0 = c[0], x1 = c[1], x2 = c[2], y0 = c[3], y1 = c[4], y2 = c[5];
+  const double b0 = xs(xm(a1, x2), xm(a2, x1)), b1 = xs(xm(a2, x0), xm(a0, x2)), b2 = xs(xm(a0, x1), xm(a1, x0));
+  const double g0 = xs(xm(a1, y2), xm(a2, y1)), g1 = xs(xm(a2, y0), xm(a0, y2)), g2 = xs(xm(a0, y1), xm(a1, y0));
+  if (__dsqrt_rn(xdot(b0, b1, b2, b0, b1, b2)) <= tau || __dsqrt_rn(xdot(g0, g1, g2, g0, g1, g2)) <= tau) return false;
+  const double c0 = xs(xm(b1, g2), xm(b2, g1)), c1 = xs(xm(b2, g0), xm(b0, g2)), c2 = xs(xm(b0, g1), xm(b1, g0));
+  *out = atan2(xdot(c0, c1, c2, a0, a1, a2), xdot(b0, b1, b2, g0, g1, g2));
+  return true;
+}
+
+__device__ __forceinline__ int bin_of(double angle, int n) {  // angles.cpp:25-30
+  const double w = xd(2.0 * kPi, (double)n);
+  const int k = __double2int_rz(ceil(xd(xa(angle, kPi), w))) - 1;
+  return min(max(k, 0), n - 1);
+}
+
+struct AngArgs {
+  double a0, a1, a2, tau;
+  const double* corrs;
+  const int32_t* idx;
+  int64_t n;
+  int bins_n;
+  uint32_t* bins;
+  double* raw;
+  unsigned long long* counts;
+};
+
+__global__ void __launch_bounds__(256) vote_angles_kernel(AngArgs a) {
+  extern __shared__ uint32_t s_bins[];
+  const bool use_smem = a.bins_n <= 8192;
+  if (use_smem)
+    for (int k = threadIdx.x; k < a.bins_n; k += blockDim.x) s_bins[k] = 0;
+  __syncthreads();
+  unsigned long long contrib = 0, degen = 0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.n; k += (int64_t)gridDim.x * blockDim.x) {
+    const double* c = a.corrs + 6 * (int64_t)a.idx[k];
+    double ang;
+    if (corr_angle(a.a0, a.a1, a.a2, c, a.tau, &ang)) {
+      a.raw[k] = ang;
+      const int b = bin_of(ang, a.bins_n);
+      if (use_smem) atomicAdd(&s_bins[b], 1u);
+      else atomicAdd(&a.bins[b], 1u);
+      ++contrib;
+    } else {
+      a.raw[k] = __longlong_as_double(0x7ff8000000000000ll);  // NaN marks a degenerate pair
+      ++degen;
+    }
+  }
+  __syncthreads();
+  if (use_smem)
+    for (int k = threadIdx.x; k < a.bins_n; k += blockDim.x)
+      if (s_bins[k]) atomicAdd(&a.bins[k], s_bins[k]);
+  for (int o = 16; o > 0; o >>= 1) {
+    contrib += __shfl_xor_sync(0xFFFFFFFFu, contrib, o);
+    degen += __shfl_xor_sync(0xFFFFFFFFu, degen, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (contrib) atomicAdd(&a.counts[0], contrib);
+    if (degen) atomicAdd(&a.counts[1], degen);
+  }
+}
+
+// peak_angle sums (angles.cpp:70-90): first max bin, then sin/cos sums of raw angles within
+// 1.5 bin widths (wrapped difference) of the bin center. result: [0]=s [1]=c [2]=k [3]=center.
+__global__ void __launch_bounds__(256) peak_angle_kernel(const uint32_t* bins, int bins_n, const double* raw,
+                                                        int64_t n, double* block_sums, double* result,
+                                                        unsigned int* done) {
+  __shared__ unsigned long long s_key[8];
+  __shared__ double s_red[2][8];
+  __shared__ bool s_last;
+  // every block finds the peak bin redundantly (bins are tiny)
+  unsigned long long key = 0;
+  for (int k = threadIdx.x; k < bins_n; k += blockDim.x) {
+    const unsigned long long kk = ((unsigned long long)bins[k] << 32) | (0xFFFFFFFFu - (uint32_t)k);
+    key = key > kk ? key : kk;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xFFFFFFFFu, key, o);
+    key = key > t ? key : t;
+  }
+  if ((threadIdx.x & 31) == 0) s_key[threadIdx.x >> 5] = key;
+  __syncthreads();
+  key = 0;
+  for (int w = 0; w < 8; ++w) key = key > s_key[w] ? key : s_key[w];
+  const int kpk = (int)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu));
+  const double w = xd(2.0 * kPi, (double)bins_n);
+  const double center = xa(-kPi, xm(kpk + 0.5, w));
+  const double window = xm(1.5, w);
+  double v[2] = {0.0, 0.0};
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const double a = raw[k];
+    if (a != a) continue;  // degenerate
+    double d = fmod(xs(a, center), 2.0 * kPi);
+    if (d <= -kPi) d = xa(d, 2.0 * kPi);
+    if (d > kPi) d = xs(d, 2.0 * kPi);
+    if (fabs(d) <= window) {
+      v[0] = xa(v[0], sin(a));
+      v[1] = xa(v[1], cos(a));
+    }
+  }
+  for (int k = 0; k < 2; ++k)
+    for (int o = 16; o > 0; o >>= 1) v[k] = xa(v[k], __shfl_xor_sync(0xFFFFFFFFu, v[k], o));
+  if ((threadIdx.x & 31) == 0) {
+    s_red[0][threadIdx.x >> 5] = v[0];
+    s_red[1][threadIdx.x >> 5] = v[1];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0, c = 0;
+    for (int ww = 0; ww < 8; ++ww) {
+      s = xa(s, s_red[0][ww]);
+      c = xa(c, s_red[1][ww]);
+    }
+    block_sums[2 * blockIdx.x] = s;
+    block_sums[2 * blockIdx.x + 1] = c;
+    __threadfence();
+    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    volatile double* bsum = block_sums;
+    double s = 0, c = 0;
+    for (unsigned b = 0; b < gridDim.x; ++b) {
+      s = xa(s, bsum[2 * b]);
+      c = xa(c, bsum[2 * b + 1]);
+    }
+    result[0] = s;
+    result[1] = c;
+    result[2] = (double)kpk;
+    result[3] = center;
+    *done = 0u;
+  }
+}
+
+struct SupArgs {
+  const double* zx;
+  const double* zy;
+  const double* zz;
+  const int32_t* kept;
+  const double* corrs;
+  int64_t n;
+  double a0, a1, a2, angle, eps, tau;
+  uint32_t* band_flags;  // nullable
+  int32_t* block_counts; // [nblocks][2]
+  int32_t* result;       // [0]=coherent [1]=band size
+  unsigned int* done;
+};
+
+__global__ void __launch_bounds__(kClsThreads) model_support_kernel(SupArgs a) {
+  __shared__ int s_c[kClsThreads / 32][2];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kClsPerBlock;
+  int coh = 0, band = 0;
+  for (int r = 0; r < kClsPerThread; ++r) {
+    const int64_t i = base + r * kClsThreads + tid;
+    bool inb = false;
+    if (i < a.n) {
+      const double d = fabs(xdot(a.a0, a.a1, a.a2, a.zx[i], a.zy[i], a.zz[i]));
+      if (d < 4.0 * a.eps) {
+        double ang;
+        if (corr_angle(a.a0, a.a1, a.a2, a.corrs + 6 * (int64_t)a.kept[i], a.tau, &ang)) {
+          if (fabs(remainder(xs(ang, a.angle), 2.0 * kPi)) < 0.1) {
+            inb = true;
+            if (d < a.eps) ++coh;
+          }
+        }
+      }
+    }
+    const unsigned word = __ballot_sync(0xFFFFFFFFu, inb);
+    band += inb ? 1 : 0;
+    if (a.band_flags && lane == 0 && (base + r * kClsThreads + warp * 32) < a.n)
+      a.band_flags[(base + r * kClsThreads + warp * 32) >> 5] = word;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    coh += __shfl_xor_sync(0xFFFFFFFFu, coh, o);
+    band += __shfl_xor_sync(0xFFFFFFFFu, band, o);
+  }
+  if (lane == 0) {
+    s_c[warp][0] = coh;
+    s_c[warp][1] = band;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int c = 0, b = 0;
+    for (int w = 0; w < kClsThreads / 32; ++w) {
+      c += s_c[w][0];
+      b += s_c[w][1];
+    }
+    a.block_counts[2 * blockIdx.x] = c;
+    a.block_counts[2 * blockIdx.x + 1] = b;
+    __threadfence();
+    s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && tid == 0) {
+    volatile int32_t* bc = a.block_counts;
+    long long c = 0, b = 0;
+    for (unsigned k = 0; k < gridDim.x; ++k) {
+      c += bc[2 * k];
+      b += bc[2 * k + 1];
+    }
+    a.result[0] = (int32_t)c;
+    a.result[1] = (int32_t)b;
+    *a.done = 0u;
+  }
+}
+
+__global__ void strip_kernel(const double* zx, const double* zy, const double* zz, int64_t n, double a0, double a1,
+                             double a2, double strip, uint8_t* removed) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (fabs(xdot(a0, a1, a2, zx[i], zy[i], zz[i])) < strip) removed[i] = 1;
+}
+
+// |axis.z| of listed constraints (band values for the strip percentile).
+__global__ void gather_dot_kernel(const double* zx, const double* zy, const double* zz, const int32_t* idx,
+                                  int64_t n, double a0, double a1, double a2, double* out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int32_t i = idx[k];
+  out[k] = fabs(xdot(a0, a1, a2, zx[i], zy[i], zz[i]));
+}
+
+// near_identity_model cluster test + Kabsch cross-covariance (estimator.cpp:198-249).
+struct NearArgs {
+  const double* corrs;
+  const int32_t* sub_kept;
+  int64_t n;
+  int normalize;
+  uint32_t* flags;
+  int32_t* block_count;
+  double* block_h;  // [nblocks][9]
+  int32_t* block_offsets;
+  double* result;   // [0]=count [1..9]=H row-major
+  unsigned int* done;
+};
+
+__device__ __forceinline__ void load_norm(const double* c, int normalize, double* x, double* y) {
+  x[0] = c[0]; x[1] = c[1]; x[2] = c[2]; y[0] = c[3]; y[1] = c[4]; y[2] = c[5];
+  if (normalize) {
+    const double nx = __dsqrt_rn(xdot(x[0], x[1], x[2], x[0], x[1], x[2]));
+    const double ny = __dsqrt_rn(xdot(y[0], y[1], y[2], y[0], y[1], y[2]));
+    if (nx > 0.0) { x[0] = xd(x[0], nx); x[1] = xd(x[1], nx); x[2] = xd(x[2], nx); }
+    if (ny > 0.0) { y[0] = xd(y[0], ny); y[1] = xd(y[1], ny); y[2] = xd(y[2], ny); }
+  }
+}
+
+__global__ void __launch_bounds__(kClsThreads) near_identity_kernel(NearArgs a) {
+  __shared__ double s_red[9][kClsThreads / 32];
+  __shared__ int s_cnt[kClsThreads / 32];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kClsPerBlock;
+  double h[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int cnt = 0;
+  for (int r = 0; r < kClsPerThread; ++r) {
+    const int64_t i = base + r * kClsThreads + tid;
+    bool in = false;
+    double x[3], y[3];
+    if (i < a.n) {
+      load_norm(a.corrs + 6 * (int64_t)a.sub_kept[i], a.normalize, x, y);
+      const double d0 = xs(y[0], x[0]), d1 = xs(y[1], x[1]), d2 = xs(y[2], x[2]);
+      in = __dsqrt_rn(xdot(d0, d1, d2, d0, d1, d2)) < 0.1;
+    }
+    const unsigned word = __ballot_sync(0xFFFFFFFFu, in);
+    if (lane == 0 && (base + r * kClsThreads + warp * 32) < a.n) a.flags[(base + r * kClsThreads + warp * 32) >> 5] = word;
+    if (in) {
+      ++cnt;
+      for (int p = 0; p < 3; ++p)
+        for (int q = 0; q < 3; ++q) h[p * 3 + q] = xa(h[p * 3 + q], xm(y[p], x[q]));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
+  if (lane == 0) s_cnt[warp] = cnt;
+  block_sum<9>(h, s_red);
+  if (tid == 0) {
+    int c = 0;
+    for (int w = 0; w < kClsThreads / 32; ++w) c += s_cnt[w];
+    a.block_count[blockIdx.x] = c;
+    for (int k = 0; k < 9; ++k) a.block_h[(size_t)blockIdx.x * 9 + k] = h[k];
+    __threadfence();
+    s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && tid == 0) {
+    volatile int32_t* bc = a.block_count;
+    volatile double* bh = a.block_h;
+    long long c = 0;
+    double hh[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (unsigned b = 0; b < gridDim.x; ++b) {
+      a.block_offsets[b] = (int32_t)c;
+      c += bc[b];
+      for (int k = 0; k < 9; ++k) hh[k] = xa(hh[k], bh[(size_t)b * 9 + k]);
+    }
+    a.result[0] = (double)c;
+    for (int k = 0; k < 9; ++k) a.result[1 + k] = hh[k];
+    *a.done = 0u;
+  }
+}
+
+}  // namespace
+
+int classify_blocks(int64_t n) { return (int)((n + kClsPerBlock - 1) / kClsPerBlock); }
+
+void launch_classify_mode(const double* zx, const double* zy, const double* zz, int64_t n, const double axis[3],
+                          double eps, int mode, const ClassifyOut& o, int32_t* block_offsets, unsigned int* done,
+                          cudaStream_t s) {
+  ClsArgs a;
+  a.zx = zx;
+  a.zy = zy;
+  a.zz = zz;
+  a.n = n;
+  a.ax = axis ? axis[0] : 0;
+  a.ay = axis ? axis[1] : 0;
+  a.az = axis ? axis[2] : 0;
+  a.eps = eps;
+  a.mode = mode;
+  a.flags = o.flags;
+  a.prev = o.prev;
+  a.block_count = o.block_count;
+  a.block_scatter = o.block_scatter;
+  a.block_diff = o.block_diff;
+  a.block_offsets = block_offsets;
+  a.result = o.result;
+  a.done = done;
+  classify_kernel<<<classify_blocks(n), kClsThreads, 0, s>>>(a);
+}
+
+void launch_compact_flags(const uint32_t* flags, int64_t n, const int32_t* map, const int32_t* block_offsets,
+                          int32_t* out, cudaStream_t s) {
+  compact_kernel<<<classify_blocks(n), kClsThreads, 0, s>>>(flags, n, map, block_offsets, out);
+}
+
+void launch_vote_angles_k(const double axis[3], const double* corrs, const int32_t* idx, int64_t n_idx, int bin_count,
+                          double tau, uint32_t* bins, double* raw, unsigned long long* counts, cudaStream_t s) {
+  AngArgs a;
+  a.a0 = axis[0];
+  a.a1 = axis[1];
+  a.a2 = axis[2];
+  a.tau = tau;
+  a.corrs = corrs;
+  a.idx = idx;
+  a.n = n_idx;
+  a.bins_n = bin_count;
+  a.bins = bins;
+  a.raw = raw;
+  a.counts = counts;
+  const int64_t want = (n_idx + 255) / 256;
+  const int blocks = (int)(want < 1 ? 1 : (want > 592 ? 592 : want));
+  const size_t smem = bin_count <= 8192 ? (size_t)bin_count * 4 : 0;
+  vote_angles_kernel<<<blocks, 256, smem, s>>>(a);
+}
+
+void launch_peak_angle_k(const uint32_t* bins, int bin_count, const double* raw, int64_t n_raw, double* block_sums,
+                         double* result, unsigned int* done, cudaStream_t s) {
+  const int64_t want = (n_raw + 255) / 256;
+  const int blocks = (int)(want < 1 ? 1 : (want > 296 ? 296 : want));
+  peak_angle_kernel<<<blocks, 256, 0, s>>>(bins, bin_count, raw, n_raw, block_sums, result, done);
+}
+
+void launch_model_support_k(const double* zx, const double* zy, const double* zz, const int32_t* kept,
+                            const double* corrs, int64_t n, const double axis[3], double angle, double eps, double tau,
+                            uint32_t* band_flags, int32_t* block_counts, int32_t* result, unsigned int* done,
+                            cudaStream_t s) {
+  SupArgs a;
+  a.zx = zx;
+  a.zy = zy;
+  a.zz = zz;
+  a.kept = kept;
+  a.corrs = corrs;
+  a.n = n;
+  a.a0 = axis[0];
+  a.a1 = axis[1];
+  a.a2 = axis[2];
+  a.angle = angle;
+  a.eps = eps;
+  a.tau = tau;
+  a.band_flags = band_flags;
+  a.block_counts = block_counts;
+  a.result = result;
+  a.done = done;
+  model_support_kernel<<<classify_blocks(n), kClsThreads, 0, s>>>(a);
+}
+
+void launch_strip_k(const double* zx, const double* zy, const double* zz, int64_t n, const double axis[3], double strip,
+                    uint8_t* removed, cudaStream_t s) {
+  strip_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(zx, zy, zz, n, axis[0], axis[1], axis[2], strip, removed);
+}
+
+void launch_gather_dot_k(const double* zx, const double* zy, const double* zz, const int32_t* idx, int64_t n,
+                         const double axis[3], double* out, cudaStream_t s) {
+  if (n <= 0) return;
+  gather_dot_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(zx, zy, zz, idx, n, axis[0], axis[1], axis[2], out);
+}
+
+void launch_near_identity_k(const double* corrs, const int32_t* sub_kept, int64_t n, int normalize, uint32_t* flags,
+                            int32_t* block_count, double* block_h, int32_t* block_offsets, double* result,
+                            unsigned int* done, cudaStream_t s) {
+  NearArgs a;
+  a.corrs = corrs;
+  a.sub_kept = sub_kept;
+  a.n = n;
+  a.normalize = normalize;
+  a.flags = flags;
+  a.block_count = block_count;
+  a.block_h = block_h;
+  a.block_offsets = block_offsets;
+  a.result = result;
+  a.done = done;
+  near_identity_kernel<<<classify_blocks(n), kClsThreads, 0, s>>>(a);
+}
+
+}  // namespace rvb
+
+namespace rvb {
+namespace {
+// Identity-model removal (estimator.cpp:461-467): the residual members with small motion.
+__global__ void strip_identity_kernel(const double* corrs, const int32_t* kept, int64_t n, int normalize,
+                                      uint8_t* removed) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n || removed[k]) return;
+  double x[3], y[3];
+  load_norm(corrs + 6 * (int64_t)kept[k], normalize, x, y);
+  const double d0 = xs(y[0], x[0]), d1 = xs(y[1], x[1]), d2 = xs(y[2], x[2]);
+  if (__dsqrt_rn(xdot(d0, d1, d2, d0, d1, d2)) < 0.1) removed[k] = 1;
+}
+}  // namespace
+void launch_strip_identity_k(const double* corrs, const int32_t* kept, int64_t n, int normalize, uint8_t* removed,
+                             cudaStream_t s) {
+  if (n <= 0) return;
+  strip_identity_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(corrs, kept, n, normalize, removed);
+}
+}  // namespace rvb

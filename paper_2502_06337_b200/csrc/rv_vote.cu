@@ -1,0 +1,533 @@
+// K1 (band plan) and K2 (band-tiled vote) of the spatial-voting path.
+//
+// Reference semantics (voting.cpp:25-45, :88-118): every constraint z deposits exactly J
+// votes, one per sample theta_j = -pi + j*2pi/J of the great circle {v : z.v = 0}; each
+// sample is flipped to the southern hemisphere, stereographically projected and counted in
+// its cell of a G x G uint32 grid. The device result is BIT-EXACT with that definition:
+//
+//  * Twins. Samples j and j+J/2 are antipodal, so after the hemisphere flip they land on
+//    the same plane point (up to ~1e-15). K2 evaluates one "pair" per twin and deposits 2.
+//  * f32 filter + exact f64 fallback. The pair is evaluated in f32 from an f64 basis; the
+//    cell coordinate t is produced on a 2^-10 grid by one FFMA against a magic constant.
+//    Worst-case |t32 - t64| <= 2.1e-4 cell (derivation in DESIGN.md), so whenever the
+//    fractional part of t32 is >= 1.46e-3 from an integer (and |c| >= 2e-6, no hemisphere
+//    ambiguity) the f32 cell IS the reference cell. Otherwise the pair is queued and both
+//    twins are recomputed exactly in f64 (same op order, no FMA) -- ~0.6% of pairs.
+//  * Band tiling. The grid's reachable rows are split into bands that fit one CTA's shared
+//    memory (u32 counters, 1 CTA/SM). K1 computes per (constraint, band) the pair-index
+//    ranges whose projected points can fall in the band (analytic circle/line intersection,
+//    padded), so K2 only evaluates pairs near its band; an exact ownership test on the row
+//    decides the deposit, so a sample is counted by exactly one band.
+//  * Tiles are flushed once per (CTA, band) to partial slots; a reduction kernel sums the
+//    slots of each band (integer sums: order-free, deterministic).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "rv_exact.cuh"
+#include "rv_internal.h"
+
+namespace rvb {
+
+namespace {
+
+constexpr float kPiF = 3.14159265358979323846f;
+constexpr float kTwoPiF = 6.28318530717958647692f;
+constexpr float kRcMin = 1e-3f;     // |c| amplitude below which a circle is treated as all-band
+constexpr float kDc = 2e-6f;        // |c| below this: hemisphere flip ambiguous -> exact path
+constexpr int kMagicBits = 0x46400000;  // bits of 1.5 * 2^13 (2^-10 ulp in [8192, 16384))
+
+struct Iv {
+  float a, b;
+};
+
+// Intervals of s in [0, pi] where A cos(theta_a + s) + B sin(theta_a + s) >= y0.
+__device__ int arc_ge(float A, float B, float y0, float theta_a, Iv* out) {
+  const float R = hypotf(A, B);
+  if (!(R > 0.f)) {
+    if (0.f >= y0) {
+      out[0] = {0.f, kPiF};
+      return 1;
+    }
+    return 0;
+  }
+  const float ratio = y0 / R;
+  if (ratio <= -1.f) {
+    out[0] = {0.f, kPiF};
+    return 1;
+  }
+  if (!(ratio < 1.f)) return 0;
+  const float alpha = acosf(ratio);
+  float sig = atan2f(B, A) - theta_a;
+  sig = sig - kTwoPiF * floorf((sig + kPiF) / kTwoPiF);
+  int k = 0;
+  for (int m = -1; m <= 1; ++m) {
+    const float lo = fmaxf(sig - alpha + m * kTwoPiF, 0.f);
+    const float hi = fminf(sig + alpha + m * kTwoPiF, kPiF);
+    if (lo <= hi && k < 3) out[k++] = {lo, hi};
+  }
+  return k;
+}
+
+struct Seg {
+  int s, e;  // [s, e) on [0, M)
+};
+
+// Plans the pair ranges of one constraint for one band. Returns the two encoded ranges.
+__device__ void plan_band(const VotePlan& p, int band, const float a1[3], const float a2[3], float theta_a,
+                          float pa, uint32_t* r_out, unsigned long long* work) {
+  const int M = p.halfJ;
+  Iv lo[3], hi[3];
+  int nlo, nhi;
+  const float ylo = p.band_ylo[band], yhi = p.band_yhi[band];
+  if (ylo == -INFINITY) {
+    lo[0] = {0.f, kPiF};
+    nlo = 1;
+  } else {
+    nlo = arc_ge(a1[1] + ylo * a1[2], a2[1] + ylo * a2[2], ylo, theta_a, lo);
+  }
+  if (yhi == INFINITY) {
+    nhi = 0;
+  } else {
+    nhi = arc_ge(a1[1] + yhi * a1[2], a2[1] + yhi * a2[2], yhi, theta_a, hi);
+  }
+  // complement of hi within [0, pi]
+  if (nhi == 2 && hi[1].a < hi[0].a) {
+    const Iv t = hi[0];
+    hi[0] = hi[1];
+    hi[1] = t;
+  }
+  Iv comp[4];
+  int nc = 0;
+  float cur = 0.f;
+  for (int k = 0; k < nhi; ++k) {
+    if (hi[k].a > cur) comp[nc++] = {cur, hi[k].a};
+    cur = fmaxf(cur, hi[k].b);
+  }
+  if (cur < kPiF || nhi == 0) comp[nc++] = {cur, kPiF};
+  // pieces = lo intersect comp, converted to padded pair-index arcs, then unioned.
+  Seg seg[16];
+  int ns = 0;
+  bool full = false;
+  const float inv_step = 1.f / p.step_f;
+  for (int i = 0; i < nlo && !full; ++i) {
+    for (int j = 0; j < nc && !full; ++j) {
+      const float s1 = fmaxf(lo[i].a, comp[j].a), s2 = fminf(lo[i].b, comp[j].b);
+      if (!(s1 <= s2)) continue;
+      const int u1 = __float2int_rd(pa + s1 * inv_step) - kPad;
+      const int u2 = __float2int_ru(pa + s2 * inv_step) + kPad;
+      const int len = u2 - u1 + 1;
+      if (len >= M) {
+        full = true;
+        break;
+      }
+      int st = u1 % M;
+      if (st < 0) st += M;
+      if (st + len <= M) {
+        seg[ns++] = {st, st + len};
+      } else {
+        seg[ns++] = {st, M};
+        seg[ns++] = {0, st + len - M};
+      }
+    }
+  }
+  uint32_t r0 = 0, r1 = 0;
+  if (full) {
+    r0 = (uint32_t)M << 16;
+    *work += (unsigned long long)M;
+  } else if (ns > 0) {
+    for (int i = 1; i < ns; ++i) {  // insertion sort by start
+      const Seg t = seg[i];
+      int j = i - 1;
+      while (j >= 0 && seg[j].s > t.s) {
+        seg[j + 1] = seg[j];
+        --j;
+      }
+      seg[j + 1] = t;
+    }
+    int nm = 0;
+    for (int i = 0; i < ns; ++i) {
+      if (nm > 0 && seg[i].s <= seg[nm - 1].e) {
+        seg[nm - 1].e = max(seg[nm - 1].e, seg[i].e);
+      } else {
+        seg[nm++] = seg[i];
+      }
+    }
+    int starts[2], lens[2], nr = 0;
+    if (nm >= 2 && seg[0].s == 0 && seg[nm - 1].e == M) {  // join across the wrap
+      starts[0] = seg[nm - 1].s;
+      lens[0] = seg[nm - 1].e - seg[nm - 1].s + seg[0].e;
+      nr = 1;
+      for (int i = 1; i < nm - 1; ++i) {
+        if (nr < 2) {
+          starts[nr] = seg[i].s;
+          lens[nr] = seg[i].e - seg[i].s;
+        }
+        ++nr;
+      }
+    } else {
+      for (int i = 0; i < nm; ++i) {
+        if (nr < 2) {
+          starts[nr] = seg[i].s;
+          lens[nr] = seg[i].e - seg[i].s;
+        }
+        ++nr;
+      }
+    }
+    if (nr > 2) {  // cannot happen for a minor arc; stay conservative
+      r0 = (uint32_t)M << 16;
+      *work += (unsigned long long)M;
+    } else {
+      r0 = (uint32_t)starts[0] | ((uint32_t)lens[0] << 16);
+      *work += (unsigned long long)lens[0];
+      if (nr == 2) {
+        r1 = (uint32_t)starts[1] | ((uint32_t)lens[1] << 16);
+        *work += (unsigned long long)lens[1];
+      }
+    }
+  }
+  r_out[0] = r0;
+  r_out[1] = r1;
+}
+
+__global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, int64_t n) {
+  __shared__ unsigned long long s_work[kMaxBands];
+  for (int t = threadIdx.x; t < p.n_bands; t += blockDim.x) s_work[t] = 0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    double a1[3], a2[3];
+    exact_basis(b.zx[i], b.zy[i], b.zz[i], a1, a2);
+    float f1[3], f2[3];
+    for (int k = 0; k < 3; ++k) {
+      f1[k] = __double2float_rn(a1[k]);
+      f2[k] = __double2float_rn(a2[k]);
+    }
+    b.basis_a[i] = make_float4(f1[0], f1[1], f1[2], f2[0]);
+    b.basis_b[i] = make_float2(f2[1], f2[2]);
+    const float rc = hypotf(f1[2], f2[2]);
+    const int M = p.halfJ;
+    if (!(rc >= kRcMin)) {  // near-polar constraint: c ~ 0 everywhere, every band sees all pairs
+      for (int band = 0; band < p.n_bands; ++band) {
+        uint2* rp = reinterpret_cast<uint2*>(b.ranges) + (int64_t)band * n + i;
+        *rp = make_uint2((uint32_t)M << 16, 0u);
+        atomicAdd(&s_work[band], (unsigned long long)M);
+      }
+    } else {
+      const float theta_c = atan2f(f2[2], f1[2]);
+      const float theta_a = theta_c + 0.5f * kPiF;  // c(theta_a + s) = -rc sin(s) <= 0 on s in [0, pi]
+      const float pa = (theta_a + kPiF) / p.step_f;
+      for (int band = 0; band < p.n_bands; ++band) {
+        uint32_t r[2];
+        unsigned long long w = 0;
+        plan_band(p, band, f1, f2, theta_a, pa, r, &w);
+        uint2* rp = reinterpret_cast<uint2*>(b.ranges) + (int64_t)band * n + i;
+        *rp = make_uint2(r[0], r[1]);
+        if (w) atomicAdd(&s_work[band], w);
+      }
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < p.n_bands; t += blockDim.x)
+    if (s_work[t]) atomicAdd(&b.band_work[t], s_work[t]);
+}
+
+// ---- K2 ------------------------------------------------------------------------------
+
+struct FbEntry {
+  uint32_t circle, pair;
+};
+
+// Exact f64 evaluation of both twins of a queued pair; deposits the ones this band owns.
+__device__ __forceinline__ void fallback_pair(const VotePlan& p, const VoteBuffers& b, FbEntry e, int band,
+                                              uint32_t* tile, int r0, int hb) {
+  double a1[3], a2[3];
+  exact_basis(b.zx[e.circle], b.zy[e.circle], b.zz[e.circle], a1, a2);
+  const int own_lo = band == 0 ? 0 : p.band_r0[band];
+  const int own_hi = band == p.n_bands - 1 ? p.G : p.band_r0[band + 1];
+#pragma unroll
+  for (int tw = 0; tw < 2; ++tw) {
+    const double2 cs = b.table64[e.pair + tw * p.halfJ];
+    int row, col;
+    exact_sample(a1, a2, cs.x, cs.y, p, &row, &col);
+    if (row < own_lo || row >= own_hi) continue;
+    const int lr = row - r0, lc = col - p.c_min;
+    if ((unsigned)lr < (unsigned)hb && (unsigned)lc < (unsigned)p.W)
+      atomicAdd(&tile[lr * p.W + lc], 1u);
+    else
+      atomicAdd(&b.grid[(size_t)row * p.G + col], 1u);
+  }
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+template <bool kClamp>
+__global__ void __launch_bounds__(kVoteThreads, 1)
+    vote_banded_kernel(VotePlan p, VoteBuffers b, int64_t n, int chunk, int n_chunks) {
+  extern __shared__ uint4 smem_raw[];
+  uint32_t* tile = reinterpret_cast<uint32_t*>(smem_raw);
+  float2* tab = reinterpret_cast<float2*>(tile + ((p.tile_words + 3) & ~size_t(3)));
+  FbEntry* fbq_all = reinterpret_cast<FbEntry*>(tab + ((p.halfJ + 1) & ~1));
+  __shared__ int s_item, s_band, s_slot;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  FbEntry* fbq = fbq_all + warp * kFbqCap;
+  const int M = p.halfJ;
+  for (int k = tid; k < M; k += blockDim.x) tab[k] = b.table32[k];
+
+  if (tid == 0) {  // initial band: CTAs split across bands in proportion to planned work
+    unsigned long long total = 0;
+    for (int q = 0; q < p.n_bands; ++q) total += b.band_work[q];
+    int band = p.n_bands - 1;
+    if (total > 0) {
+      const double pos = ((double)blockIdx.x + 0.5) / gridDim.x * (double)total;
+      double acc = 0;
+      for (int q = 0; q < p.n_bands; ++q) {
+        acc += (double)b.band_work[q];
+        if (pos < acc) {
+          band = q;
+          break;
+        }
+      }
+    }
+    s_band = band;
+  }
+  for (size_t k = tid; k < p.tile_words; k += blockDim.x) tile[k] = 0u;
+  __syncthreads();
+  int band = s_band;
+  int r0 = p.band_r0[band], hb = p.band_r0[band + 1] - r0;
+  int own_lo = band == 0 ? 0 : r0, own_hi = band == p.n_bands - 1 ? p.G : r0 + hb;
+  int qn = 0;  // per-warp fallback queue length (warp-uniform)
+  unsigned long long my_pairs = 0, my_fb = 0;
+  const unsigned lt_mask = (1u << lane) - 1u;
+
+  auto drain = [&](int count) {
+    if (lane < count) fallback_pair(p, b, fbq[lane], band, tile, r0, hb);
+    __syncwarp();
+  };
+
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) {
+      int item = atomicAdd(&b.counters[1 + band], 1);
+      int nb = band;
+      if (item >= n_chunks) {
+        item = -1;
+        for (int d = 1; d < p.n_bands; ++d) {
+          const int q = (band + d) % p.n_bands;
+          if (*((volatile int*)&b.counters[1 + q]) >= n_chunks) continue;
+          const int it = atomicAdd(&b.counters[1 + q], 1);
+          if (it < n_chunks) {
+            item = it;
+            nb = q;
+            break;
+          }
+        }
+      }
+      s_item = item;
+      s_band = nb;
+    }
+    __syncthreads();
+    const int item = s_item;
+    const int nb = s_band;
+    if (item < 0 || nb != band) {
+      // finish the current band: drain the exact queue, flush the tile to a partial slot
+      if (qn > 0) drain(qn);
+      qn = 0;
+      __syncthreads();
+      if (tid == 0) {
+        const int slot = atomicAdd(&b.counters[0], 1);
+        s_slot = slot;
+        if (slot < b.max_slots) b.slot_band[slot] = band;
+      }
+      __syncthreads();
+      const int slot = s_slot;
+      const size_t words = (size_t)hb * p.W;
+      if (slot < b.max_slots) {
+        uint32_t* dst = b.partials + (size_t)slot * p.tile_words;
+        for (size_t k = tid; k < words; k += blockDim.x) dst[k] = tile[k];
+      } else {  // cannot happen (each CTA visits each band at most once); stay exact anyway
+        for (size_t k = tid; k < words; k += blockDim.x)
+          if (tile[k]) atomicAdd(&b.grid[(size_t)(r0 + k / p.W) * p.G + p.c_min + k % p.W], tile[k]);
+      }
+      if (item < 0) break;
+      __syncthreads();
+      for (size_t k = tid; k < p.tile_words; k += blockDim.x) tile[k] = 0u;
+      band = nb;
+      r0 = p.band_r0[band];
+      hb = p.band_r0[band + 1] - r0;
+      own_lo = band == 0 ? 0 : r0;
+      own_hi = band == p.n_bands - 1 ? p.G : r0 + hb;
+      __syncthreads();
+    }
+    const int64_t c_begin = (int64_t)item * chunk;
+    const int64_t c_end = (n < c_begin + chunk) ? n : c_begin + chunk;
+    const uint2* rbase = reinterpret_cast<const uint2*>(b.ranges) + (int64_t)band * n;
+    for (int64_t ci = c_begin + warp; ci < c_end; ci += kVoteThreads / 32) {
+      const uint2 rr = rbase[ci];
+      if ((rr.x >> 16) == 0 && (rr.y >> 16) == 0) continue;
+      const float4 ba = b.basis_a[ci];
+      const float2 bb = b.basis_b[ci];
+#pragma unroll 1
+      for (int rk = 0; rk < 2; ++rk) {
+        const uint32_t enc = rk == 0 ? rr.x : rr.y;
+        const int start = enc & 0xFFFF, len = enc >> 16;
+        for (int k0 = 0; k0 < len; k0 += 32) {
+          const int k = k0 + lane;
+          const bool active = k < len;
+          int pidx = start + k;
+          if (pidx >= M) pidx -= M;
+          const float2 t = tab[active ? pidx : 0];
+          const float x = fmaf(ba.w, t.y, ba.x * t.x);
+          const float y = fmaf(bb.x, t.y, ba.y * t.x);
+          const float c = fmaf(bb.y, t.y, ba.z * t.x);
+          const float r = rcp_approx(1.f + fabsf(c));
+          const float rs = __int_as_float(__float_as_int(r) | (~__float_as_int(c) & 0x80000000));
+          const float rkf = rs * p.Kf;
+          const int tx = __float_as_int(fmaf(x, rkf, p.CMf)) - kMagicBits;
+          const int ty = __float_as_int(fmaf(y, rkf, p.CMf)) - kMagicBits;
+          const bool bad = (fabsf(c) < kDc) | ((((unsigned)tx + 1u) & 1023u) <= 2u) |
+                           ((((unsigned)ty + 1u) & 1023u) <= 2u);
+          int col = tx >> 10, row = ty >> 10;
+          if (kClamp) {
+            col = min(max(col, 0), p.G - 1);
+            row = min(max(row, 0), p.G - 1);
+          }
+          if (active && !bad && row >= own_lo && row < own_hi) {
+            const int lr = row - r0, lc = col - p.c_min;
+            if ((unsigned)lr < (unsigned)hb && (unsigned)lc < (unsigned)p.W)
+              atomicAdd(&tile[lr * p.W + lc], 2u);
+            else
+              atomicAdd(&b.grid[(size_t)row * p.G + col], 2u);
+          }
+          const unsigned fm = __ballot_sync(0xFFFFFFFFu, active && bad);
+          if (fm) {
+            if (active && bad) fbq[qn + __popc(fm & lt_mask)] = FbEntry{(uint32_t)ci, (uint32_t)pidx};
+            qn += __popc(fm);
+            my_fb += __popc(fm);
+            __syncwarp();
+            if (qn >= 32) {
+              drain(32);
+              qn -= 32;
+              if (lane < qn) fbq[lane] = fbq[32 + lane];
+              __syncwarp();
+            }
+          }
+        }
+        my_pairs += (unsigned long long)len;
+      }
+    }
+  }
+  if (lane == 0) {
+    atomicAdd(&b.stats[0], my_pairs);
+    atomicAdd(&b.stats[1], my_fb);
+  }
+}
+
+// Sum the partial tiles of every band into the output grid.
+__global__ void __launch_bounds__(kReduceThreads) vote_reduce_kernel(VotePlan p, VoteBuffers b) {
+  __shared__ int s_slots[1024];
+  __shared__ int s_n;
+  const int band = blockIdx.y;
+  const int r0 = p.band_r0[band], hb = p.band_r0[band + 1] - r0;
+  const int words = hb * p.W;
+  int used = min(b.counters[0], b.max_slots);
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  // slot list of this band (order irrelevant: integer sums)
+  for (int s = threadIdx.x; s < used; s += blockDim.x) {
+    if (b.slot_band[s] == band) {
+      const int k = atomicAdd(&s_n, 1);
+      if (k < 1024) s_slots[k] = s;
+    }
+  }
+  __syncthreads();
+  const int ns = s_n;
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
+    uint32_t acc = 0;
+    if (ns <= 1024) {
+      for (int k = 0; k < ns; ++k) acc += b.partials[(size_t)s_slots[k] * p.tile_words + w];
+    } else {
+      for (int s = 0; s < used; ++s)
+        if (b.slot_band[s] == band) acc += b.partials[(size_t)s * p.tile_words + w];
+    }
+    if (acc) {
+      const int row = r0 + w / p.W, col = p.c_min + w % p.W;
+      b.grid[(size_t)row * p.G + col] += acc;
+    }
+  }
+}
+
+// Exact generic vote: one warp per constraint, lanes over samples, global atomics.
+__global__ void __launch_bounds__(256) vote_generic_kernel(VotePlan p, const double* zx, const double* zy,
+                                                           const double* zz, const double2* table64,
+                                                           uint32_t* grid, int64_t n) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n) return;
+  double a1[3], a2[3];
+  exact_basis(zx[w], zy[w], zz[w], a1, a2);
+  for (int j = lane; j < p.J; j += 32) {
+    const double2 cs = table64[j];
+    int row, col;
+    exact_sample(a1, a2, cs.x, cs.y, p, &row, &col);
+    atomicAdd(&grid[(size_t)row * p.G + col], 1u);
+  }
+}
+
+__global__ void deposit_one_kernel(VotePlan p, const double* z3, const double2* table64, uint32_t* grid) {
+  double a1[3], a2[3];
+  exact_basis(z3[0], z3[1], z3[2], a1, a2);
+  for (int j = threadIdx.x; j < p.J; j += blockDim.x) {
+    const double2 cs = table64[j];
+    int row, col;
+    exact_sample(a1, a2, cs.x, cs.y, p, &row, &col);
+    atomicAdd(&grid[(size_t)row * p.G + col], 1u);
+  }
+}
+
+}  // namespace
+
+void launch_plan(const VotePlan& p, const VoteBuffers& b, int64_t n, cudaStream_t s) {
+  const int threads = 256;
+  const int64_t blocks = (n + threads - 1) / threads;
+  plan_kernel<<<(unsigned)blocks, threads, 0, s>>>(p, b, n);
+}
+
+void launch_vote_banded(const VotePlan& p, const VoteBuffers& b, int64_t n, int n_ctas, int chunk,
+                        cudaStream_t s) {
+  const int n_chunks = (int)((n + chunk - 1) / chunk);
+  if (p.clamp) {
+    cudaFuncSetAttribute(vote_banded_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)p.smem_bytes);
+    vote_banded_kernel<true><<<n_ctas, kVoteThreads, p.smem_bytes, s>>>(p, b, n, chunk, n_chunks);
+  } else {
+    cudaFuncSetAttribute(vote_banded_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)p.smem_bytes);
+    vote_banded_kernel<false><<<n_ctas, kVoteThreads, p.smem_bytes, s>>>(p, b, n, chunk, n_chunks);
+  }
+}
+
+void launch_vote_reduce(const VotePlan& p, const VoteBuffers& b, cudaStream_t s) {
+  const int words = p.H_max * p.W;
+  const int bx = (words + kReduceThreads - 1) / kReduceThreads;
+  dim3 grid((unsigned)min(bx, 64), (unsigned)p.n_bands);
+  vote_reduce_kernel<<<grid, kReduceThreads, 0, s>>>(p, b);
+}
+
+void launch_vote_generic(const VotePlan& p, const VoteBuffers& b, int64_t n, cudaStream_t s) {
+  const int threads = 256;
+  const int64_t blocks = (n * 32 + threads - 1) / threads;
+  vote_generic_kernel<<<(unsigned)blocks, threads, 0, s>>>(p, b.zx, b.zy, b.zz, b.table64, b.grid, n);
+}
+
+void launch_deposit_one(const VotePlan& p, const double* z3, const double2* table64, uint32_t* grid,
+                        cudaStream_t s) {
+  deposit_one_kernel<<<1, 256, 0, s>>>(p, z3, table64, grid);
+}
+
+}  // namespace rvb
