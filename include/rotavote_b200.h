@@ -92,6 +92,7 @@ typedef struct rv_stage_times {
   double angles_ms;     /* K4: angle histogram + circular mean + model support */
   double total_ms;
   int64_t vote_pairs;       /* sample pairs evaluated by the vote kernel (work incl. padding) */
+  int64_t vote_fallback_pairs; /* pairs re-evaluated on the exact f64 path */
   int64_t vote_samples;     /* algorithmic samples N_kept * J of all vote launches */
   int32_t vote_launches;    /* vote kernel launches in the call */
   int32_t kernel_launches;  /* all kernels launched by the call */

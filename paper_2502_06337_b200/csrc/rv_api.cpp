@@ -9,6 +9,7 @@
 #include <array>
 #include <iterator>
 #include <chrono>
+#include <deque>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -122,6 +123,7 @@ struct rv_context {
   DBuf bins, raw, angle_counts, angle_sums, angle_result, sup_counts, sup_result, band_flagsA, band_flagsB,
       band_idx, band_vals, near_h, near_result;
   DBuf user_z;  // scratch copy of a constraint span (path functions)
+  std::deque<std::pair<VotePlan, int>> plans;  // vote plans by (G, E, J)
   // pinned host scalars
   void* pinned = nullptr;
   std::vector<std::vector<int32_t>> results;
@@ -203,11 +205,22 @@ VotePlan make_plan(rv_context* c, int G, double E, int J) {
   p.halfJ = J / 2;
   p.step_f = (float)(2.0 * std::numbers::pi / J);
   p.banded = 0;
-  const bool twins_ok = (J % 2 == 0) && J >= 2 && p.halfJ <= 32768;
-  const bool magic_ok = G <= 4000;  // t + 1.5*2^13 must stay in [8192, 16384)
-  if (!twins_ok || !magic_ok) return p;
+  // twins j, j+J/2 and 64-aligned pair ranges; queue entries hold the pair in 16 bits
+  const bool twins_ok = (J % 128 == 0) && p.halfJ <= 32768;
+  // t + 1.5*2^(23-S) must stay inside [2^(22-S)... 2^(24-S)): t in [-2^(22-S), 2^(22-S))
+  int S = 12;
+  while (S >= 8 && G + 8 >= (1 << (22 - S))) --S;
+  if (!twins_ok || S < 8) return p;
+  p.frac_shift = S;
+  p.frac_mask = ((1u << S) - 1u) & ~7u;
+  const double magic = 1.5 * std::ldexp(1.0, 23 - S);
+  const float magic_f = (float)magic;
+  uint32_t magic_bits;
+  std::memcpy(&magic_bits, &magic_f, 4);
+  p.magic_hi = (int)(magic_bits >> S);
   p.Kf = (float)p.inv_cell;
-  p.CMf = 12288.0f + (float)(0.5 * G);  // E*inv_cell == G/2 exactly in real arithmetic
+  // E*inv_cell == G/2 exactly in real arithmetic; +3 units of 2^-S bias the frac window to [-3, 4]
+  p.CMf = (float)(magic + 0.5 * G + 3.0 * std::ldexp(1.0, -S));
   p.clamp = E <= 1.0 + 1e-6 ? 1 : 0;
   const double lo_t = (E - 1.0) * p.inv_cell, hi_t = (E + 1.0) * p.inv_cell;
   if (p.clamp) {
@@ -220,8 +233,8 @@ VotePlan make_plan(rv_context* c, int G, double E, int J) {
   p.c_min = p.r_min;
   p.c_max = p.r_max;
   p.W = p.c_max - p.c_min + 1;
-  const size_t table_bytes = ((size_t)((p.halfJ + 1) & ~1)) * sizeof(float2);
-  const size_t fbq_bytes = (size_t)(kVoteThreads / 32) * kFbqCap * 8;
+  const size_t table_bytes = (size_t)(2 * p.halfJ + 64) * sizeof(float2);  // doubled: ranges never wrap
+  const size_t fbq_bytes = (size_t)(kVoteThreads / 32) * kFbqCap * 4 + 32 * 4;  // + lane sink words
   const size_t reserve = table_bytes + fbq_bytes + 1024;
   if ((size_t)c->max_smem <= reserve) return p;
   const size_t budget_words = ((size_t)c->max_smem - reserve) / 4;
@@ -243,6 +256,17 @@ VotePlan make_plan(rv_context* c, int G, double E, int J) {
   p.smem_bytes = ((p.tile_words * 4 + 15) & ~size_t(15)) + table_bytes + fbq_bytes;
   p.banded = p.smem_bytes <= (size_t)c->max_smem ? 1 : 0;
   return p;
+}
+
+const VotePlan& cached_plan(rv_context* c, int G, double E, int J) {
+  for (const auto& e : c->plans)
+    if (e.first.G == G && e.first.E == E && e.first.J == J) return e.first;
+  VotePlan p = make_plan(c, G, E, J);
+  if (p.banded) {  // opt-in shared memory once per plan
+    ck(set_vote_smem(p), "cudaFuncSetAttribute");
+  }
+  c->plans.emplace_back(p, 0);
+  return c->plans.back().first;
 }
 
 // Sample table exactly as the reference (voting.cpp:72-81), on the host libm.
@@ -273,7 +297,7 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   if (G < 1 || !(E > 0.0)) fail(RV_ERR_INVALID_CONFIG, "accumulator needs grid >= 1, extent > 0");
   if (J < 1) fail(RV_ERR_INVALID_CONFIG, "theta_samples must be >= 1");
   ensure_tables(c, J);
-  const VotePlan p = make_plan(c, G, E, J);
+  const VotePlan& p = cached_plan(c, G, E, J);
   uint32_t* grid = c->grid.get<uint32_t>((size_t)G * G);
   StageScope sc(c, kVote);
   ck(cudaMemsetAsync(grid, 0, sizeof(uint32_t) * (size_t)G * G, c->st), "memset grid");
@@ -298,7 +322,9 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   b.band_work = c->band_work.get<unsigned long long>(kMaxBands);
   b.counters = c->counters.get<int32_t>(kMaxBands + 1);
   b.stats = c->stats.get<unsigned long long>(2);
-  const int n_ctas = c->sms;
+  // enough CTAs to keep every SM busy, but not more than the work can feed (~1M pairs per CTA)
+  const int64_t est_pairs = n * (int64_t)p.halfJ;
+  const int n_ctas = (int)std::clamp<int64_t>(est_pairs >> 20, std::min(p.n_bands, c->sms), c->sms);
   b.max_slots = n_ctas * p.n_bands;
   b.partials = c->partials.get<uint32_t>((size_t)b.max_slots * p.tile_words);
   b.slot_band = c->slot_band.get<int32_t>(b.max_slots);
@@ -306,17 +332,18 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   ck(cudaMemsetAsync(b.counters, 0, sizeof(int32_t) * (kMaxBands + 1), c->st), "memset counters");
   ck(cudaMemsetAsync(b.stats, 0, sizeof(unsigned long long) * 2, c->st), "memset stats");
   launch_plan(p, b, n, c->st);
-  const int64_t per_cta = std::max<int64_t>(1, (n * p.n_bands) / ((int64_t)n_ctas * 8));
-  const int chunk = (int)std::min<int64_t>(512, std::max<int64_t>(32, per_cta));
-  launch_vote_banded(p, b, n, n_ctas, chunk, c->st);
+  launch_vote_banded(p, b, n, n_ctas, c->st);
   launch_vote_reduce(p, b, c->st);
   count_launch(c, 3);
   ck(cudaGetLastError(), "vote_banded");
   if (c->timing) {
-    unsigned long long st[2];
+    unsigned long long st[2], work[kMaxBands];
     ck(cudaMemcpyAsync(st, b.stats, sizeof st, cudaMemcpyDeviceToHost, c->st), "stats");
+    ck(cudaMemcpyAsync(work, b.band_work, sizeof(unsigned long long) * p.n_bands, cudaMemcpyDeviceToHost, c->st),
+       "band work");
     sync(c);
-    c->times.vote_pairs += (int64_t)st[0];
+    for (int q = 0; q < p.n_bands; ++q) c->times.vote_pairs += (int64_t)work[q];
+    c->times.vote_fallback_pairs += (int64_t)st[1];
   }
   return grid;
 }

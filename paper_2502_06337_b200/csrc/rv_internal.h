@@ -9,7 +9,7 @@
 namespace rvb {
 
 constexpr int kMaxBands = 64;        // row bands of the smem-tiled vote kernel
-constexpr int kVoteThreads = 1024;   // threads per vote CTA (32 warps)
+constexpr int kVoteThreads = 512;    // threads per vote CTA (16 warps, 128 regs each)
 constexpr int kPad = 2;              // pair-index padding of each band range (culling slack)
 constexpr int kFbqCap = 64;          // per-warp exact-fallback queue entries
 constexpr int kReduceThreads = 256;
@@ -23,7 +23,10 @@ struct VotePlan {
   double inv_cell = 0;  // grid / (2*extent)   (voting.cpp:30)
   double cs = 0;        // 2*extent / grid     (voting.hpp:23)
   float Kf = 0;      // (float) inv_cell
-  float CMf = 0;     // (float)(extent*inv_cell) + 1.5*2^13 (folds the 2^-10 rounding magic)
+  float CMf = 0;     // G/2 + 1.5*2^(23-S) + 3*2^-S: one FFMA yields t on a 2^-S grid, biased +3 units
+  int frac_shift = 0;     // S: fixed-point resolution 2^-S of the cell coordinate t
+  uint32_t frac_mask = 0; // ((1<<S)-1) & ~7: bits & mask == 0 <=> round(t*2^S) mod 2^S in [-3, 4]
+  int magic_hi = 0;       // bits(1.5*2^(23-S)) >> S
   int clamp = 0;     // 1 if votes can fall outside the unit-disk rows/cols (extent <= 1)
   int r_min = 0, r_max = 0;  // stored rows [r_min, r_max]
   int c_min = 0, c_max = 0;  // stored cols
@@ -53,7 +56,7 @@ struct VoteBuffers {
   uint32_t* grid = nullptr;    // [G*G] output
   uint32_t* partials = nullptr;        // [max_slots][tile_words]
   int32_t* slot_band = nullptr;        // [max_slots]
-  int32_t* counters = nullptr;         // [0]=slot counter, [1..kMaxBands]=chunk counters per band
+  int32_t* counters = nullptr;         // [0]=slot counter, [1..kMaxBands]=constraint counters per band
   unsigned long long* stats = nullptr; // [0]=pairs evaluated, [1]=fallback pairs
   int max_slots = 0;
 };
@@ -61,8 +64,8 @@ struct VoteBuffers {
 // K1: constraint basis (exact f64 -> f32) and band culling plan per constraint.
 void launch_plan(const VotePlan& p, const VoteBuffers& b, int64_t n, cudaStream_t s);
 // K2: band-tiled vote into smem tiles, flushed to partial slots; then tile reduction.
-void launch_vote_banded(const VotePlan& p, const VoteBuffers& b, int64_t n, int n_ctas,
-                        int chunk, cudaStream_t s);
+void launch_vote_banded(const VotePlan& p, const VoteBuffers& b, int64_t n, int n_ctas, cudaStream_t s);
+cudaError_t set_vote_smem(const VotePlan& p);  // opt-in dynamic smem (once per size)
 void launch_vote_reduce(const VotePlan& p, const VoteBuffers& b, cudaStream_t s);
 // Exact generic vote (any config): one thread per (constraint, sample), global atomics.
 void launch_vote_generic(const VotePlan& p, const VoteBuffers& b, int64_t n, cudaStream_t s);

@@ -35,7 +35,6 @@ constexpr float kPiF = 3.14159265358979323846f;
 constexpr float kTwoPiF = 6.28318530717958647692f;
 constexpr float kRcMin = 1e-3f;     // |c| amplitude below which a circle is treated as all-band
 constexpr float kDc = 2e-6f;        // |c| below this: hemisphere flip ambiguous -> exact path
-constexpr int kMagicBits = 0x46400000;  // bits of 1.5 * 2^13 (2^-10 ulp in [8192, 16384))
 
 struct Iv {
   float a, b;
@@ -178,11 +177,32 @@ __device__ void plan_band(const VotePlan& p, int band, const float a1[3], const 
       r0 = (uint32_t)M << 16;
       *work += (unsigned long long)M;
     } else {
-      r0 = (uint32_t)starts[0] | ((uint32_t)lens[0] << 16);
-      *work += (unsigned long long)lens[0];
+      // K2 walks ranges 64 pairs per warp iteration: round each range up to a multiple of 64
+      // (the extra pairs are real samples; ownership still decides) and merge overlaps so a
+      // pair is never visited twice by the same band.
+      int s0 = starts[0], l0 = (lens[0] + 63) & ~63;
+      int s1 = nr == 2 ? starts[1] : 0, l1 = nr == 2 ? (lens[1] + 63) & ~63 : 0;
       if (nr == 2) {
-        r1 = (uint32_t)starts[1] | ((uint32_t)lens[1] << 16);
-        *work += (unsigned long long)lens[1];
+        const int d01 = ((s1 - s0) % M + M) % M, d10 = ((s0 - s1) % M + M) % M;
+        if (d01 < l0) {
+          l0 = (max(l0, d01 + l1) + 63) & ~63;
+          nr = 1;
+        } else if (d10 < l1) {
+          s0 = s1;
+          l0 = (max(l1, d10 + l0) + 63) & ~63;
+          nr = 1;
+        }
+      }
+      if (l0 >= M || (nr == 2 && l0 + l1 >= M)) {
+        r0 = (uint32_t)M << 16;
+        *work += (unsigned long long)M;
+      } else {
+        r0 = (uint32_t)s0 | ((uint32_t)l0 << 16);
+        *work += (unsigned long long)l0;
+        if (nr == 2) {
+          r1 = (uint32_t)s1 | ((uint32_t)l1 << 16);
+          *work += (unsigned long long)l1;
+        }
       }
     }
   }
@@ -234,29 +254,45 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
 
 // ---- K2 ------------------------------------------------------------------------------
 
-struct FbEntry {
-  uint32_t circle, pair;
+// Exact f64 evaluation of both twins of a queued pair; deposits the ones this band owns.
+// Cold path (~0.6% of pairs), kept out of line so the hot loop keeps its registers.
+struct FbCtx {  // the few scalars the exact path needs (keeps the kernel-param struct in cbank)
+  const double* zx;
+  const double* zy;
+  const double* zz;
+  const double2* table64;
+  uint32_t* grid;
+  double E, inv_cell;
+  int G, halfJ, c_min, W, own_lo, own_hi;
 };
 
-// Exact f64 evaluation of both twins of a queued pair; deposits the ones this band owns.
-__device__ __forceinline__ void fallback_pair(const VotePlan& p, const VoteBuffers& b, FbEntry e, int band,
-                                              uint32_t* tile, int r0, int hb) {
-  double a1[3], a2[3];
-  exact_basis(b.zx[e.circle], b.zy[e.circle], b.zz[e.circle], a1, a2);
-  const int own_lo = band == 0 ? 0 : p.band_r0[band];
-  const int own_hi = band == p.n_bands - 1 ? p.G : p.band_r0[band + 1];
+__device__ __noinline__ void fallback_pairs(FbCtx f, const uint32_t* q, int count, int64_t c_begin, uint32_t* tile,
+                                            int r0, int hb) {
+  const int lane = threadIdx.x & 31;
+  if (lane < count) {
+    const uint32_t e = q[lane];
+    const int64_t ci = c_begin + (e >> 16);
+    const int pair = (int)(e & 0xFFFFu);
+    double a1[3], a2[3];
+    exact_basis(f.zx[ci], f.zy[ci], f.zz[ci], a1, a2);
+    VotePlan p1;
+    p1.E = f.E;
+    p1.inv_cell = f.inv_cell;
+    p1.G = f.G;
 #pragma unroll
-  for (int tw = 0; tw < 2; ++tw) {
-    const double2 cs = b.table64[e.pair + tw * p.halfJ];
-    int row, col;
-    exact_sample(a1, a2, cs.x, cs.y, p, &row, &col);
-    if (row < own_lo || row >= own_hi) continue;
-    const int lr = row - r0, lc = col - p.c_min;
-    if ((unsigned)lr < (unsigned)hb && (unsigned)lc < (unsigned)p.W)
-      atomicAdd(&tile[lr * p.W + lc], 1u);
-    else
-      atomicAdd(&b.grid[(size_t)row * p.G + col], 1u);
+    for (int tw = 0; tw < 2; ++tw) {
+      const double2 cs = f.table64[pair + tw * f.halfJ];
+      int row, col;
+      exact_sample(a1, a2, cs.x, cs.y, p1, &row, &col);
+      if (row < f.own_lo || row >= f.own_hi) continue;
+      const int lr = row - r0, lc = col - f.c_min;
+      if ((unsigned)lr < (unsigned)hb && (unsigned)lc < (unsigned)f.W)
+        atomicAdd(&tile[lr * f.W + lc], 1u);
+      else
+        atomicAdd(&f.grid[(size_t)row * f.G + col], 1u);
+    }
   }
+  __syncwarp();
 }
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -265,19 +301,38 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
+__device__ __forceinline__ void red_shared(uint32_t saddr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v));
+}
+
+__device__ __forceinline__ void red_shared_if(uint32_t saddr, uint32_t v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.add.u32 [%0], %1;\n\t}" ::"r"(saddr), "r"(v),
+      "r"((uint32_t)pred));
+}
+
+// K2: persistent, one CTA per SM, 16 warps. A CTA owns one row band's u32 tile in shared
+// memory at a time. Warps grab kWarpGrab constraints at a time from the band's global work
+// counter (no CTA barrier per chunk); when the band is exhausted the CTA flushes its tile to a
+// partial slot and steals the band with the most remaining work. Warp = one constraint; lanes
+// walk 64 consecutive sample pairs per iteration of the constraint's planned ranges (64-aligned,
+// table doubled so ranges never wrap). Pairs whose f32 cell is not provably the reference cell
+// are queued per warp and recomputed exactly in f64.
+constexpr int kWarpGrab = 16;
+
 template <bool kClamp>
-__global__ void __launch_bounds__(kVoteThreads, 1)
-    vote_banded_kernel(VotePlan p, VoteBuffers b, int64_t n, int chunk, int n_chunks) {
+__global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p, VoteBuffers b, int64_t n) {
   extern __shared__ uint4 smem_raw[];
   uint32_t* tile = reinterpret_cast<uint32_t*>(smem_raw);
   float2* tab = reinterpret_cast<float2*>(tile + ((p.tile_words + 3) & ~size_t(3)));
-  FbEntry* fbq_all = reinterpret_cast<FbEntry*>(tab + ((p.halfJ + 1) & ~1));
-  __shared__ int s_item, s_band, s_slot;
+  const int M = p.halfJ;
+  uint32_t* fbq_all = reinterpret_cast<uint32_t*>(tab + 2 * M + 64);
+  uint32_t* dummy = fbq_all + (kVoteThreads / 32) * kFbqCap;  // [32] sink words for masked lanes
+  __shared__ int s_band, s_slot;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  FbEntry* fbq = fbq_all + warp * kFbqCap;
-  const int M = p.halfJ;
-  for (int k = tid; k < M; k += blockDim.x) tab[k] = b.table32[k];
+  uint32_t* fbq = fbq_all + warp * kFbqCap;
+  for (int k = tid; k < 2 * M + 64; k += blockDim.x) tab[k] = b.table32[k % M];
 
   if (tid == 0) {  // initial band: CTAs split across bands in proportion to planned work
     unsigned long long total = 0;
@@ -298,134 +353,150 @@ __global__ void __launch_bounds__(kVoteThreads, 1)
   }
   for (size_t k = tid; k < p.tile_words; k += blockDim.x) tile[k] = 0u;
   __syncthreads();
-  int band = s_band;
-  int r0 = p.band_r0[band], hb = p.band_r0[band + 1] - r0;
-  int own_lo = band == 0 ? 0 : r0, own_hi = band == p.n_bands - 1 ? p.G : r0 + hb;
-  int qn = 0;  // per-warp fallback queue length (warp-uniform)
-  unsigned long long my_pairs = 0, my_fb = 0;
+  unsigned int my_fb = 0;
   const unsigned lt_mask = (1u << lane) - 1u;
-
-  auto drain = [&](int count) {
-    if (lane < count) fallback_pair(p, b, fbq[lane], band, tile, r0, hb);
-    __syncwarp();
-  };
+  const uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(tile);
+  const uint32_t dummy_s = (uint32_t)__cvta_generic_to_shared(dummy + lane);
+  const float Kf = p.Kf, CMf = p.CMf;
+  const int W = p.W, G = p.G;
+  const int S = p.frac_shift;
+  const uint32_t fmask = p.frac_mask;
+  FbCtx fc;
+  fc.zx = b.zx;
+  fc.zy = b.zy;
+  fc.zz = b.zz;
+  fc.table64 = b.table64;
+  fc.grid = b.grid;
+  fc.E = p.E;
+  fc.inv_cell = p.inv_cell;
+  fc.G = G;
+  fc.halfJ = M;
+  fc.c_min = p.c_min;
+  fc.W = W;
 
   for (;;) {
-    __syncthreads();
-    if (tid == 0) {
-      int item = atomicAdd(&b.counters[1 + band], 1);
-      int nb = band;
-      if (item >= n_chunks) {
-        item = -1;
-        for (int d = 1; d < p.n_bands; ++d) {
-          const int q = (band + d) % p.n_bands;
-          if (*((volatile int*)&b.counters[1 + q]) >= n_chunks) continue;
-          const int it = atomicAdd(&b.counters[1 + q], 1);
-          if (it < n_chunks) {
-            item = it;
-            nb = q;
-            break;
-          }
-        }
-      }
-      s_item = item;
-      s_band = nb;
-    }
-    __syncthreads();
-    const int item = s_item;
-    const int nb = s_band;
-    if (item < 0 || nb != band) {
-      // finish the current band: drain the exact queue, flush the tile to a partial slot
-      if (qn > 0) drain(qn);
-      qn = 0;
-      __syncthreads();
-      if (tid == 0) {
-        const int slot = atomicAdd(&b.counters[0], 1);
-        s_slot = slot;
-        if (slot < b.max_slots) b.slot_band[slot] = band;
-      }
-      __syncthreads();
-      const int slot = s_slot;
-      const size_t words = (size_t)hb * p.W;
-      if (slot < b.max_slots) {
-        uint32_t* dst = b.partials + (size_t)slot * p.tile_words;
-        for (size_t k = tid; k < words; k += blockDim.x) dst[k] = tile[k];
-      } else {  // cannot happen (each CTA visits each band at most once); stay exact anyway
-        for (size_t k = tid; k < words; k += blockDim.x)
-          if (tile[k]) atomicAdd(&b.grid[(size_t)(r0 + k / p.W) * p.G + p.c_min + k % p.W], tile[k]);
-      }
-      if (item < 0) break;
-      __syncthreads();
-      for (size_t k = tid; k < p.tile_words; k += blockDim.x) tile[k] = 0u;
-      band = nb;
-      r0 = p.band_r0[band];
-      hb = p.band_r0[band + 1] - r0;
-      own_lo = band == 0 ? 0 : r0;
-      own_hi = band == p.n_bands - 1 ? p.G : r0 + hb;
-      __syncthreads();
-    }
-    const int64_t c_begin = (int64_t)item * chunk;
-    const int64_t c_end = (n < c_begin + chunk) ? n : c_begin + chunk;
+    const int band = s_band;
+    if (band < 0) break;
+    const int r0 = p.band_r0[band], hb = p.band_r0[band + 1] - r0;
+    fc.own_lo = band == 0 ? 0 : r0;
+    fc.own_hi = band == p.n_bands - 1 ? G : r0 + hb;
+    const int row_off = p.magic_hi + r0;      // row_local = (bits_y >> S) - row_off
+    const int col_off = p.magic_hi + p.c_min; // col_local = (bits_x >> S) - col_off
     const uint2* rbase = reinterpret_cast<const uint2*>(b.ranges) + (int64_t)band * n;
-    for (int64_t ci = c_begin + warp; ci < c_end; ci += kVoteThreads / 32) {
-      const uint2 rr = rbase[ci];
-      if ((rr.x >> 16) == 0 && (rr.y >> 16) == 0) continue;
-      const float4 ba = b.basis_a[ci];
-      const float2 bb = b.basis_b[ci];
+    int* counter = &b.counters[1 + band];
+    for (;;) {  // per-warp dynamic grabs of kWarpGrab constraints
+      int64_t g0 = 0;
+      if (lane == 0) g0 = atomicAdd(counter, kWarpGrab);
+      g0 = __shfl_sync(0xFFFFFFFFu, g0, 0);
+      if (g0 >= n) break;
+      const int64_t g1 = (g0 + kWarpGrab < n) ? g0 + kWarpGrab : n;
+      int qn = 0;
+      uint2 rr = rbase[g0];
+      float4 ba = b.basis_a[g0];
+      float2 bb = b.basis_b[g0];
+      for (int64_t ci = g0; ci < g1; ++ci) {
+        uint2 rr_n = rr;
+        float4 ba_n = ba;
+        float2 bb_n = bb;
+        if (ci + 1 < g1) {  // prefetch the next constraint
+          rr_n = rbase[ci + 1];
+          ba_n = b.basis_a[ci + 1];
+          bb_n = b.basis_b[ci + 1];
+        }
+        const uint32_t local_ci = (uint32_t)(ci - g0) << 16;
 #pragma unroll 1
-      for (int rk = 0; rk < 2; ++rk) {
-        const uint32_t enc = rk == 0 ? rr.x : rr.y;
-        const int start = enc & 0xFFFF, len = enc >> 16;
-        for (int k0 = 0; k0 < len; k0 += 32) {
-          const int k = k0 + lane;
-          const bool active = k < len;
-          int pidx = start + k;
-          if (pidx >= M) pidx -= M;
-          const float2 t = tab[active ? pidx : 0];
-          const float x = fmaf(ba.w, t.y, ba.x * t.x);
-          const float y = fmaf(bb.x, t.y, ba.y * t.x);
-          const float c = fmaf(bb.y, t.y, ba.z * t.x);
-          const float r = rcp_approx(1.f + fabsf(c));
-          const float rs = __int_as_float(__float_as_int(r) | (~__float_as_int(c) & 0x80000000));
-          const float rkf = rs * p.Kf;
-          const int tx = __float_as_int(fmaf(x, rkf, p.CMf)) - kMagicBits;
-          const int ty = __float_as_int(fmaf(y, rkf, p.CMf)) - kMagicBits;
-          const bool bad = (fabsf(c) < kDc) | ((((unsigned)tx + 1u) & 1023u) <= 2u) |
-                           ((((unsigned)ty + 1u) & 1023u) <= 2u);
-          int col = tx >> 10, row = ty >> 10;
-          if (kClamp) {
-            col = min(max(col, 0), p.G - 1);
-            row = min(max(row, 0), p.G - 1);
-          }
-          if (active && !bad && row >= own_lo && row < own_hi) {
-            const int lr = row - r0, lc = col - p.c_min;
-            if ((unsigned)lr < (unsigned)hb && (unsigned)lc < (unsigned)p.W)
-              atomicAdd(&tile[lr * p.W + lc], 2u);
-            else
-              atomicAdd(&b.grid[(size_t)row * p.G + col], 2u);
-          }
-          const unsigned fm = __ballot_sync(0xFFFFFFFFu, active && bad);
-          if (fm) {
-            if (active && bad) fbq[qn + __popc(fm & lt_mask)] = FbEntry{(uint32_t)ci, (uint32_t)pidx};
-            qn += __popc(fm);
-            my_fb += __popc(fm);
-            __syncwarp();
-            if (qn >= 32) {
-              drain(32);
-              qn -= 32;
-              if (lane < qn) fbq[lane] = fbq[32 + lane];
-              __syncwarp();
+        for (int rk = 0; rk < 2; ++rk) {
+          const uint32_t enc = rk == 0 ? rr.x : rr.y;
+          const int start = (int)(enc & 0xFFFFu), len = (int)(enc >> 16);
+          const float2* tp = tab + start + lane;
+#pragma unroll 1
+          for (int k0 = 0; k0 < len; k0 += 64) {
+            bool flag[2];
+            uint32_t addr[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const float2 t = tp[k0 + 32 * h];
+              const float x = fmaf(ba.w, t.y, ba.x * t.x);
+              const float y = fmaf(bb.x, t.y, ba.y * t.x);
+              const float c = fmaf(bb.y, t.y, ba.z * t.x);
+              const float r = rcp_approx(1.f + fabsf(c));
+              const float rs = __int_as_float(__float_as_int(r) | (~__float_as_int(c) & 0x80000000));
+              const float rkf = rs * Kf;
+              const uint32_t bx = (uint32_t)__float_as_int(fmaf(x, rkf, CMf));
+              const uint32_t by = (uint32_t)__float_as_int(fmaf(y, rkf, CMf));
+              flag[h] = (fabsf(c) < kDc) | ((bx & fmask) == 0u) | ((by & fmask) == 0u);
+              int row = (int)(by >> S) - row_off;
+              int col = (int)(bx >> S) - col_off;
+              if (kClamp) {
+                row = min(max(row + r0, 0), G - 1) - r0;
+                col = min(max(col + p.c_min, 0), G - 1) - p.c_min;
+              }
+              const bool dep = !flag[h] && (unsigned)row < (unsigned)hb;
+              addr[h] = dep ? tile_s + 4u * (uint32_t)(row * W + col) : dummy_s;
+            }
+            red_shared(addr[0], 2u);
+            red_shared(addr[1], 2u);
+            if (__any_sync(0xFFFFFFFFu, flag[0] | flag[1])) {  // cold: queue for the exact f64 path
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const unsigned fm = __ballot_sync(0xFFFFFFFFu, flag[h]);
+                if (flag[h]) {
+                  int pair = start + k0 + 32 * h + lane;
+                  if (pair >= M) pair -= M;
+                  fbq[qn + __popc(fm & lt_mask)] = local_ci | (uint32_t)pair;
+                }
+                qn += __popc(fm);
+                my_fb += __popc(fm);
+                __syncwarp();
+                if (qn >= 32) {
+                  fallback_pairs(fc, fbq, 32, g0, tile, r0, hb);
+                  qn -= 32;
+                  if (lane < qn) fbq[lane] = fbq[32 + lane];
+                  __syncwarp();
+                }
+              }
             }
           }
         }
-        my_pairs += (unsigned long long)len;
+        rr = rr_n;
+        ba = ba_n;
+        bb = bb_n;
       }
+      if (qn > 0) fallback_pairs(fc, fbq, qn, g0, tile, r0, hb);
     }
+    // band exhausted for this CTA: flush the tile to a partial slot, steal the next band
+    __syncthreads();
+    if (tid == 0) {
+      const int slot = atomicAdd(&b.counters[0], 1);
+      s_slot = slot;
+      if (slot < b.max_slots) b.slot_band[slot] = band;
+      int best = -1;
+      long long best_rem = 0;
+      for (int q = 0; q < p.n_bands; ++q) {
+        const long long rem = (long long)n - *((volatile int*)&b.counters[1 + q]);
+        if (rem > best_rem) {
+          best_rem = rem;
+          best = q;
+        }
+      }
+      s_band = best;
+    }
+    __syncthreads();
+    const int slot = s_slot;
+    const size_t words = (size_t)hb * W;
+    if (slot < b.max_slots) {
+      uint32_t* dst = b.partials + (size_t)slot * p.tile_words;
+      for (size_t k = tid; k < words; k += blockDim.x) dst[k] = tile[k];
+    } else {  // cannot happen (a CTA visits each band at most once); stay exact anyway
+      for (size_t k = tid; k < words; k += blockDim.x)
+        if (tile[k]) atomicAdd(&b.grid[(size_t)(r0 + k / W) * G + p.c_min + k % W], tile[k]);
+    }
+    __syncthreads();
+    if (s_band >= 0)
+      for (size_t k = tid; k < p.tile_words; k += blockDim.x) tile[k] = 0u;
+    __syncthreads();
   }
-  if (lane == 0) {
-    atomicAdd(&b.stats[0], my_pairs);
-    atomicAdd(&b.stats[1], my_fb);
-  }
+  if (lane == 0 && my_fb) atomicAdd(&b.stats[1], (unsigned long long)my_fb);
 }
 
 // Sum the partial tiles of every band into the output grid.
@@ -498,18 +569,23 @@ void launch_plan(const VotePlan& p, const VoteBuffers& b, int64_t n, cudaStream_
   plan_kernel<<<(unsigned)blocks, threads, 0, s>>>(p, b, n);
 }
 
-void launch_vote_banded(const VotePlan& p, const VoteBuffers& b, int64_t n, int n_ctas, int chunk,
-                        cudaStream_t s) {
-  const int n_chunks = (int)((n + chunk - 1) / chunk);
-  if (p.clamp) {
-    cudaFuncSetAttribute(vote_banded_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)p.smem_bytes);
-    vote_banded_kernel<true><<<n_ctas, kVoteThreads, p.smem_bytes, s>>>(p, b, n, chunk, n_chunks);
-  } else {
-    cudaFuncSetAttribute(vote_banded_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)p.smem_bytes);
-    vote_banded_kernel<false><<<n_ctas, kVoteThreads, p.smem_bytes, s>>>(p, b, n, chunk, n_chunks);
-  }
+cudaError_t set_vote_smem(const VotePlan& p) {
+  static int configured[2] = {0, 0};  // largest dynamic smem opted in per instantiation
+  const int k = p.clamp ? 1 : 0;
+  if ((int)p.smem_bytes <= configured[k]) return cudaSuccess;
+  const cudaError_t e = p.clamp ? cudaFuncSetAttribute(vote_banded_kernel<true>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes)
+                                : cudaFuncSetAttribute(vote_banded_kernel<false>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  if (e == cudaSuccess) configured[k] = (int)p.smem_bytes;
+  return e;
+}
+
+void launch_vote_banded(const VotePlan& p, const VoteBuffers& b, int64_t n, int n_ctas, cudaStream_t s) {
+  if (p.clamp)
+    vote_banded_kernel<true><<<n_ctas, kVoteThreads, p.smem_bytes, s>>>(p, b, n);
+  else
+    vote_banded_kernel<false><<<n_ctas, kVoteThreads, p.smem_bytes, s>>>(p, b, n);
 }
 
 void launch_vote_reduce(const VotePlan& p, const VoteBuffers& b, cudaStream_t s) {
