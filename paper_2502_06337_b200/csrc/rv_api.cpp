@@ -128,7 +128,15 @@ struct rv_context {
   void* pinned = nullptr;
   std::vector<std::vector<int32_t>> results;
 
-  unsigned int* done_ptr() { return done.get<unsigned int>(8); }
+  // "last block done" counters of the single-pass reductions: must start at zero; every kernel
+  // that uses one resets it before exiting.
+  unsigned int* done_ptr() {
+    if (!done.p) {
+      done.get<unsigned int>(8);
+      if (cudaMemset(done.p, 0, done.cap) != cudaSuccess) fail(RV_ERR_CUDA, "memset done counter");
+    }
+    return static_cast<unsigned int*>(done.p);
+  }
 };
 
 namespace {
