@@ -1,0 +1,142 @@
+// Drop-in for proj/include/rotavote/voting.hpp (voting.hpp:14-85): Accumulator2D, Peak,
+// PeakSet and the voting functions, with accumulate / find_peaks / blurred_argmax /
+// deposit_circle_votes executed by the sm_100a kernels of librotavote_b200 (bit-exact with the
+// reference's sampled-deposit semantics, voting.cpp:17-216).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <algorithm>
+#include <ostream>
+#include <numbers>
+#include <numeric>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "device.hpp"
+#include "geom.hpp"
+
+namespace rotavote {
+
+class Accumulator2D {
+ public:
+  Accumulator2D(int grid, double extent)
+      : grid_(grid), extent_(extent), counts_(static_cast<std::size_t>(grid > 0 ? grid : 0) * (grid > 0 ? grid : 0), 0u) {
+    if (grid < 1 || extent <= 0.0) throw InvalidConfig("accumulator needs grid >= 1, extent > 0");
+  }
+  int grid() const { return grid_; }
+  double extent() const { return extent_; }
+  double cell_size() const { return 2.0 * extent_ / grid_; }
+  int coord_to_cell(double v) const {  // voting.cpp:17-23
+    const double t = (v + extent_) * (grid_ / (2.0 * extent_));
+    const double f = std::floor(t);
+    int i = static_cast<int>(f);
+    if (f == t && i > 0) --i;
+    return i < 0 ? 0 : (i > grid_ - 1 ? grid_ - 1 : i);
+  }
+  PlanePoint cell_center(int ix, int iy) const {
+    const double cs = cell_size();
+    return {-extent_ + (ix + 0.5) * cs, -extent_ + (iy + 0.5) * cs};
+  }
+  std::uint32_t& at(int ix, int iy) { return counts_[static_cast<std::size_t>(iy) * grid_ + ix]; }
+  std::uint32_t at(int ix, int iy) const { return counts_[static_cast<std::size_t>(iy) * grid_ + ix]; }
+  std::span<const std::uint32_t> counts() const { return counts_; }
+  std::span<std::uint32_t> counts() { return counts_; }
+  std::uint64_t total() const { return std::accumulate(counts_.begin(), counts_.end(), std::uint64_t{0}); }
+  void add(const Accumulator2D& other) {
+    for (std::size_t i = 0; i < counts_.size(); ++i) counts_[i] += other.counts_[i];
+  }
+
+ private:
+  int grid_;
+  double extent_;
+  std::vector<std::uint32_t> counts_;
+};
+
+struct Peak {
+  int ix = 0;
+  int iy = 0;
+  PlanePoint center;
+  std::uint32_t votes = 0;
+};
+
+struct PeakSet {
+  std::vector<Peak> peaks;
+  int suppression_radius = 0;
+};
+
+inline std::vector<double> circle_sample_table(int samples) {  // voting.cpp:72-81
+  std::vector<double> table(2 * static_cast<std::size_t>(samples));
+  const double step = 2.0 * std::numbers::pi / samples;
+  for (int j = 0; j < samples; ++j) {
+    const double theta = -std::numbers::pi + j * step;
+    table[2 * j] = std::cos(theta);
+    table[2 * j + 1] = std::sin(theta);
+  }
+  return table;
+}
+
+inline void deposit_circle_votes(const Vec3& z, Accumulator2D& acc, int samples) {
+  double zz[3];
+  detail::to3(z, zz);
+  detail::check(rv_deposit_circle_votes(detail::context(), zz, acc.counts().data(), acc.grid(), acc.extent(), samples));
+}
+
+inline Accumulator2D accumulate(std::span<const Vec3> constraints, int grid, double extent, int samples,
+                                int threads = 1) {
+  (void)threads;  // the device result is independent of host threads, like the reference's
+  if (constraints.empty()) throw EmptyInput("no constraints to accumulate");
+  Accumulator2D acc(grid, extent);
+  std::vector<double> z(3 * constraints.size());
+  for (std::size_t i = 0; i < constraints.size(); ++i) detail::to3(constraints[i], z.data() + 3 * i);
+  detail::check(rv_accumulate(detail::context(), z.data(), static_cast<int64_t>(constraints.size()), grid, extent,
+                              samples, acc.counts().data()));
+  return acc;
+}
+
+inline PeakSet find_peaks(const Accumulator2D& acc, int max_peaks, int suppression_radius, std::uint32_t min_votes) {
+  PeakSet out;
+  out.suppression_radius = suppression_radius;
+  if (max_peaks < 1) throw NoPeak("no accumulator cell reaches min_votes");
+  std::vector<rv_peak> ps(static_cast<std::size_t>(max_peaks));
+  int32_t n = 0;
+  detail::check(rv_find_peaks(detail::context(), acc.counts().data(), acc.grid(), acc.extent(), max_peaks,
+                              suppression_radius, min_votes, ps.data(), &n));
+  for (int k = 0; k < n; ++k) out.peaks.push_back(Peak{ps[k].ix, ps[k].iy, {ps[k].A, ps[k].B}, ps[k].votes});
+  return out;
+}
+
+inline Vec3 backproject_peak(const PlanePoint& center) { return unproject(center).normalized(); }
+
+inline Peak blurred_argmax(const Accumulator2D& acc, int radius) {
+  rv_peak p;
+  detail::check(rv_blurred_argmax(detail::context(), acc.counts().data(), acc.grid(), acc.extent(), radius, &p));
+  return Peak{p.ix, p.iy, {p.A, p.B}, p.votes};
+}
+
+// Dump formats (voting.hpp:83-84; plot-ready host formatting, voting.cpp:218-239).
+inline void dump_accumulator_text(const Accumulator2D& acc, std::ostream& out) {
+  const int g = acc.grid();
+  for (int iy = 0; iy < g; ++iy) {
+    for (int ix = 0; ix < g; ++ix) {
+      if (ix) out << ' ';
+      out << acc.at(ix, iy);
+    }
+    out << '\n';
+  }
+}
+
+inline void dump_accumulator_pgm(const Accumulator2D& acc, std::ostream& out) {
+  const int g = acc.grid();
+  const auto counts = acc.counts();
+  const std::uint32_t peak = counts.empty() ? 0 : *std::max_element(counts.begin(), counts.end());
+  out << "P5\n" << g << ' ' << g << "\n255\n";
+  for (std::uint32_t c : counts) {
+    const unsigned char v =
+        peak == 0 ? 0 : static_cast<unsigned char>((static_cast<std::uint64_t>(c) * 255) / peak);
+    out.put(static_cast<char>(v));
+  }
+}
+
+}  // namespace rotavote
