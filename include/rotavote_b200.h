@@ -93,6 +93,7 @@ typedef struct rv_stage_times {
   double total_ms;
   int64_t vote_pairs;       /* sample pairs evaluated by the vote kernel (work incl. padding) */
   int64_t vote_fallback_pairs; /* pairs re-evaluated on the exact f64 path */
+  int64_t vote_guard_reruns;   /* votes redone by the generic exact kernel (grid sum != N*J) */
   int64_t vote_samples;     /* algorithmic samples N_kept * J of all vote launches */
   int32_t vote_launches;    /* vote kernel launches in the call */
   int32_t kernel_launches;  /* all kernels launched by the call */

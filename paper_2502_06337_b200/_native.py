@@ -64,6 +64,7 @@ class rv_stage_times(C.Structure):
         ("total_ms", C.c_double),
         ("vote_pairs", C.c_int64),
         ("vote_fallback_pairs", C.c_int64),
+        ("vote_guard_reruns", C.c_int64),
         ("vote_samples", C.c_int64),
         ("vote_launches", C.c_int32),
         ("kernel_launches", C.c_int32),

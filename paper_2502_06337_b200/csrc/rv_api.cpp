@@ -300,7 +300,7 @@ void ensure_tables(rv_context* c, int J) {
 
 // accumulate (voting.cpp:88-118) over device SoA constraints into the context grid.
 uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* zz, int64_t n, int G, double E,
-               int J) {
+               int J, bool force_generic = false) {
   if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no constraints to accumulate");
   if (G < 1 || !(E > 0.0)) fail(RV_ERR_INVALID_CONFIG, "accumulator needs grid >= 1, extent > 0");
   if (J < 1) fail(RV_ERR_INVALID_CONFIG, "theta_samples must be >= 1");
@@ -318,7 +318,7 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   b.table32 = c->table32.get<float2>(std::max(J / 2, 1));
   c->times.vote_samples += n * (int64_t)J;
   c->times.vote_launches += 1;
-  if (!p.banded) {
+  if (!p.banded || force_generic) {
     launch_vote_generic(p, b, n, c->st);
     count_launch(c);
     ck(cudaGetLastError(), "vote_generic");
@@ -370,21 +370,22 @@ int coord_to_cell(double v, int G, double E) {  // voting.cpp:17-23, :55-57
 
 // find_peaks (voting.cpp:120-170): greedy; device argmax per round, host NMS bookkeeping.
 std::vector<Peak> find_peaks_dev(rv_context* c, const uint32_t* grid, int G, double E, int max_peaks, int radius,
-                                 uint32_t min_votes) {
+                                 uint32_t min_votes, unsigned long long* grid_total = nullptr) {
   StageScope sc(c, kPeaks);
   std::vector<Peak> out;
   std::vector<Disk> disks;
   const double cs = 2.0 * E / G;
-  unsigned long long* keys = c->arg_keys.get<unsigned long long>(argmax_block_count());
-  unsigned long long* okey = c->arg_out.get<unsigned long long>(1);
+  unsigned long long* keys = c->arg_keys.get<unsigned long long>(2 * argmax_block_count());
+  unsigned long long* okey = c->arg_out.get<unsigned long long>(2);
   for (int k = 0; k < max_peaks; ++k) {
     if (disks.size() > 16) fail(RV_ERR_INVALID_CONFIG, "find_peaks: more than 8 peaks with mirrors unsupported");
     launch_argmax(grid, G, disks.data(), (int)disks.size(), radius, keys, okey, c->done_ptr(), c->st);
     count_launch(c);
     unsigned long long* hk = reinterpret_cast<unsigned long long*>(c->pinned);
-    ck(cudaMemcpyAsync(hk, okey, 8, cudaMemcpyDeviceToHost, c->st), "argmax D2H");
+    ck(cudaMemcpyAsync(hk, okey, 16, cudaMemcpyDeviceToHost, c->st), "argmax D2H");
     sync(c);
-    const unsigned long long key = *hk;
+    const unsigned long long key = hk[0];
+    if (k == 0 && grid_total) *grid_total = hk[1];
     if (key == 0) break;
     const uint32_t best = (uint32_t)(key >> 32);
     const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu);
@@ -405,6 +406,36 @@ std::vector<Peak> find_peaks_dev(rv_context* c, const uint32_t* grid, int G, dou
   }
   if (out.empty()) fail(RV_ERR_NO_PEAK, "no accumulator cell reaches min_votes");
   return out;
+}
+
+// accumulate + find_peaks(K=1) with the exactness guard: every constraint deposits exactly J
+// votes (voting.cpp:33-44), so the grid must sum to n*J. If the band planner ever under-covered a
+// sample the sum would be short: the vote is then redone with the generic exact kernel.
+std::pair<const uint32_t*, std::vector<Peak>> vote_and_peak(rv_context* c, const double* zx, const double* zy,
+                                                            const double* zz, int64_t n, const rv_config& cfg,
+                                                            uint32_t min_votes, bool allow_no_peak) {
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const uint32_t* grid = vote(c, zx, zy, zz, n, cfg.grid, cfg.extent, cfg.theta_samples, attempt == 1);
+    unsigned long long total = 0;
+    std::vector<Peak> peaks;
+    try {
+      peaks = find_peaks_dev(c, grid, cfg.grid, cfg.extent, 1, cfg.suppression_radius, min_votes, &total);
+    } catch (const RvError& e) {
+      if (e.st != RV_ERR_NO_PEAK || !allow_no_peak) throw;
+      if (total == 0) {  // NoPeak: re-read the total for the guard
+        unsigned long long* keys = c->arg_keys.get<unsigned long long>(2 * argmax_block_count());
+        unsigned long long* okey = c->arg_out.get<unsigned long long>(2);
+        launch_argmax(grid, cfg.grid, nullptr, 0, cfg.suppression_radius, keys, okey, c->done_ptr(), c->st);
+        unsigned long long* hk = reinterpret_cast<unsigned long long*>(c->pinned);
+        ck(cudaMemcpyAsync(hk, okey, 16, cudaMemcpyDeviceToHost, c->st), "argmax D2H");
+        sync(c);
+        total = hk[1];
+      }
+    }
+    if (total == (unsigned long long)n * (unsigned long long)cfg.theta_samples) return {grid, peaks};
+    c->times.vote_guard_reruns += 1;
+  }
+  fail(RV_ERR_CUDA, "vote grid total mismatch after exact rerun");
 }
 
 // blurred_argmax for a list of radii (voting.cpp:176-216)
@@ -744,8 +775,7 @@ Estimate estimate_single_dev(rv_context* c, const double* d_corrs, int64_t n, co
     return identity_estimate(std::move(all));
   }
   if (pre.n_dropped * 10 >= n * 9) return identity_estimate(dropped_list(c, pre.n_dropped));
-  const uint32_t* grid = vote(c, pre.cs.zx, pre.cs.zy, pre.cs.zz, pre.cs.n, cfg.grid, cfg.extent, cfg.theta_samples);
-  const std::vector<Peak> peaks = find_peaks_dev(c, grid, cfg.grid, cfg.extent, 1, cfg.suppression_radius, 1);
+  const auto [grid, peaks] = vote_and_peak(c, pre.cs.zx, pre.cs.zy, pre.cs.zz, pre.cs.n, cfg, 1, false);
   Estimate est;
   {  // estimate_from_peak (estimator.cpp:94-101)
     double A, B, b[3], axis[3];
@@ -845,15 +875,8 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
       sub.n = h[0];
     }
     if (sub.n < std::max<int64_t>(2, consensus_floor)) break;
-    const uint32_t* grid = vote(c, sub.zx, sub.zy, sub.zz, sub.n, cfg.grid, cfg.extent, cfg.theta_samples);
-    std::vector<Peak> peaks;
-    bool have_peak = true;
-    try {
-      peaks = find_peaks_dev(c, grid, cfg.grid, cfg.extent, 1, cfg.suppression_radius, rv_peak_vote_floor(&cfg, sub.n));
-    } catch (const RvError& e) {
-      if (e.st != RV_ERR_NO_PEAK) throw;
-      have_peak = false;
-    }
+    const auto [grid, peaks] = vote_and_peak(c, sub.zx, sub.zy, sub.zz, sub.n, cfg, rv_peak_vote_floor(&cfg, sub.n), true);
+    const bool have_peak = !peaks.empty();
     Estimate est;
     Support sup;
     bool have = false;
@@ -1217,8 +1240,14 @@ rv_status rv_accumulate(rv_context* c, const double* z, int64_t n, int32_t grid,
     if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no constraints to accumulate");
     if (grid < 1 || !(extent > 0.0)) fail(RV_ERR_INVALID_CONFIG, "accumulator needs grid >= 1, extent > 0");
     const ConstraintSet cs = upload_constraints(c, z, n);
-    const uint32_t* g = vote(c, cs.zx, cs.zy, cs.zz, n, grid, extent, samples);
-    ck(cudaMemcpyAsync(counts_out, g, sizeof(uint32_t) * (size_t)grid * grid, cudaMemcpyDeviceToHost, c->st), "D2H grid");
+    rv_config cfg;
+    rv_config_default(&cfg);
+    cfg.grid = grid;
+    cfg.extent = extent;
+    cfg.theta_samples = samples;
+    const auto gp = vote_and_peak(c, cs.zx, cs.zy, cs.zz, n, cfg, 1, true);
+    ck(cudaMemcpyAsync(counts_out, gp.first, sizeof(uint32_t) * (size_t)grid * grid, cudaMemcpyDeviceToHost, c->st),
+       "D2H grid");
     sync(c);
   });
 }

@@ -35,19 +35,22 @@ __device__ __forceinline__ bool masked(const DiskSet& d, int x, int y) {
   return false;
 }
 
+// Also sums every cell (u64) into out_key[1]: the vote's exactness guard (sum == N*J).
 __global__ void __launch_bounds__(kArgThreads) argmax_kernel(const uint32_t* grid, int G, DiskSet disks,
                                                              unsigned long long* block_keys,
                                                              unsigned long long* out_key, unsigned int* done) {
   __shared__ unsigned long long s_red[kArgThreads / 32];
+  __shared__ unsigned long long s_sum[kArgThreads / 32];
   __shared__ bool s_last;
   const int64_t total = (int64_t)G * G;
-  unsigned long long best = 0;
+  unsigned long long best = 0, sum = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   if ((total & 3) == 0) {
     const uint4* g4 = reinterpret_cast<const uint4*>(grid);
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total / 4; q += stride) {
       const uint4 v = g4[q];
       const uint32_t c[4] = {v.x, v.y, v.z, v.w};
+      sum += (unsigned long long)v.x + v.y + v.z + v.w;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         if (c[k] == 0) continue;
@@ -59,32 +62,56 @@ __global__ void __launch_bounds__(kArgThreads) argmax_kernel(const uint32_t* gri
   } else {
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += stride) {
       const uint32_t c = grid[idx];
+      sum += c;
       if (c == 0) continue;
       if (disks.n && masked(disks, (int)(idx % G), (int)(idx / G))) continue;
       best = umax64(best, ((unsigned long long)c << 32) | (0xFFFFFFFFu - (uint32_t)idx));
     }
   }
-  for (int o = 16; o > 0; o >>= 1) best = umax64(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
-  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = best;
+  for (int o = 16; o > 0; o >>= 1) {
+    best = umax64(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
+    sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_red[threadIdx.x >> 5] = best;
+    s_sum[threadIdx.x >> 5] = sum;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned long long b = 0;
-    for (int w = 0; w < kArgThreads / 32; ++w) b = umax64(b, s_red[w]);
+    unsigned long long b = 0, sm = 0;
+    for (int w = 0; w < kArgThreads / 32; ++w) {
+      b = umax64(b, s_red[w]);
+      sm += s_sum[w];
+    }
     block_keys[blockIdx.x] = b;
+    block_keys[gridDim.x + blockIdx.x] = sm;
     __threadfence();
     s_last = atomicAdd(done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (s_last) {
-    unsigned long long b = 0;
-    for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) b = umax64(b, ((volatile unsigned long long*)block_keys)[k]);
-    for (int o = 16; o > 0; o >>= 1) b = umax64(b, __shfl_xor_sync(0xFFFFFFFFu, b, o));
-    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = b;
+    unsigned long long b = 0, sm = 0;
+    for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) {
+      b = umax64(b, ((volatile unsigned long long*)block_keys)[k]);
+      sm += ((volatile unsigned long long*)block_keys)[gridDim.x + k];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      b = umax64(b, __shfl_xor_sync(0xFFFFFFFFu, b, o));
+      sm += __shfl_xor_sync(0xFFFFFFFFu, sm, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s_red[threadIdx.x >> 5] = b;
+      s_sum[threadIdx.x >> 5] = sm;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-      unsigned long long bb = 0;
-      for (int w = 0; w < kArgThreads / 32; ++w) bb = umax64(bb, s_red[w]);
-      *out_key = bb;
+      unsigned long long bb = 0, ss = 0;
+      for (int w = 0; w < kArgThreads / 32; ++w) {
+        bb = umax64(bb, s_red[w]);
+        ss += s_sum[w];
+      }
+      out_key[0] = bb;
+      out_key[1] = ss;
       *done = 0u;
     }
   }

@@ -36,178 +36,197 @@ constexpr float kTwoPiF = 6.28318530717958647692f;
 constexpr float kRcMin = 1e-3f;     // |c| amplitude below which a circle is treated as all-band
 constexpr float kDc = 2e-6f;        // |c| below this: hemisphere flip ambiguous -> exact path
 
-struct Iv {
-  float a, b;
-};
-
-// Intervals of s in [0, pi] where A cos(theta_a + s) + B sin(theta_a + s) >= y0.
-__device__ int arc_ge(float A, float B, float y0, float theta_a, Iv* out) {
-  const float R = hypotf(A, B);
-  if (!(R > 0.f)) {
-    if (0.f >= y0) {
-      out[0] = {0.f, kPiF};
-      return 1;
-    }
-    return 0;
-  }
-  const float ratio = y0 / R;
-  if (ratio <= -1.f) {
-    out[0] = {0.f, kPiF};
-    return 1;
-  }
-  if (!(ratio < 1.f)) return 0;
-  const float alpha = acosf(ratio);
-  float sig = atan2f(B, A) - theta_a;
-  sig = sig - kTwoPiF * floorf((sig + kPiF) / kTwoPiF);
-  int k = 0;
-  for (int m = -1; m <= 1; ++m) {
-    const float lo = fmaxf(sig - alpha + m * kTwoPiF, 0.f);
-    const float hi = fminf(sig + alpha + m * kTwoPiF, kPiF);
-    if (lo <= hi && k < 3) out[k++] = {lo, hi};
-  }
-  return k;
+// ---- K1b: band plan --------------------------------------------------------------------
+// Cheap trig for the planner: errors (~1e-5 rad) are far below the 2-pair padding (6e-3 rad at
+// J=2048); coverage only has to be a superset, ownership is decided exactly per sample.
+__device__ __forceinline__ float atan2_fast(float y, float x) {
+  const float ax = fabsf(x), ay = fabsf(y);
+  const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+  const float a = mx > 0.f ? __fdividef(mn, mx) : 0.f;
+  const float s = a * a;
+  float r = fmaf(fmaf(fmaf(-0.0464964749f, s, 0.15931422f), s, -0.327622764f), s * a, a);
+  if (ay > ax) r = 1.57079637f - r;
+  if (x < 0.f) r = 3.14159274f - r;
+  return y < 0.f ? -r : r;
+}
+__device__ __forceinline__ float acos_fast(float x) {  // Abramowitz-Stegun 4.4.46, |err| <= 2e-8 (+f32)
+  const float ax = fminf(fabsf(x), 1.f);
+  float p = -0.0012624911f;
+  p = fmaf(p, ax, 0.0066700901f);
+  p = fmaf(p, ax, -0.0170881256f);
+  p = fmaf(p, ax, 0.0308918810f);
+  p = fmaf(p, ax, -0.0501743046f);
+  p = fmaf(p, ax, 0.0889789874f);
+  p = fmaf(p, ax, -0.2145988016f);
+  p = fmaf(p, ax, 1.5707963050f);
+  const float r = sqrtf(1.f - ax) * p;
+  return x < 0.f ? kPiF - r : r;
 }
 
-struct Seg {
-  int s, e;  // [s, e) on [0, M)
+// Up to two disjoint, sorted intervals of s in [0, pi] (register-resident, no dynamic indexing).
+struct Arc2 {
+  float a0, b0, a1, b1;
+  int n;
 };
 
-// Plans the pair ranges of one constraint for one band. Returns the two encoded ranges.
-__device__ void plan_band(const VotePlan& p, int band, const float a1[3], const float a2[3], float theta_a,
-                          float pa, uint32_t* r_out, unsigned long long* work) {
-  const int M = p.halfJ;
-  Iv lo[3], hi[3];
-  int nlo, nhi;
-  const float ylo = p.band_ylo[band], yhi = p.band_yhi[band];
-  if (ylo == -INFINITY) {
-    lo[0] = {0.f, kPiF};
-    nlo = 1;
+// { s in [0, pi] : A cos(theta_a + s) + B sin(theta_a + s) >= y0 } -- on the canonical arc this is
+// { Y(s) >= y0 } because 1 - c > 0 there. `dil` widens (>0) or narrows (<0) the interval by ~10x the
+// trig approximation error (atan2_fast <= 2.1e-4 rad), so a nearly-empty interval is never lost.
+constexpr float kArcDilate = 2e-3f;
+__device__ __forceinline__ Arc2 arc_ge(float A, float B, float y0, float theta_a, float dil) {
+  Arc2 r{0.f, 0.f, 0.f, 0.f, 0};
+  const float R = sqrtf(fmaf(A, A, B * B));
+  if (!(R > 0.f)) {
+    if (y0 <= 0.f) r = Arc2{0.f, kPiF, 0.f, 0.f, 1};
+    return r;
+  }
+  const float ratio = __fdividef(y0, R);
+  if (ratio <= -1.f) return Arc2{0.f, kPiF, 0.f, 0.f, 1};
+  if (!(ratio < 1.f)) return r;
+  const float alpha = acos_fast(ratio);
+  float sig = atan2_fast(B, A) - theta_a;
+  sig -= kTwoPiF * floorf((sig + kPiF) * (1.f / kTwoPiF));
+  const float half = alpha + dil;
+  const float lo0 = fmaxf(sig - half, 0.f), hi0 = fminf(sig + half, kPiF);
+  const float lo1 = fmaxf(sig - half + kTwoPiF, 0.f), hi1 = fminf(sig + half + kTwoPiF, kPiF);
+  if (lo0 <= hi0) {
+    r.a0 = lo0;
+    r.b0 = hi0;
+    r.n = 1;
+    if (lo1 <= hi1) {
+      r.a1 = lo1;
+      r.b1 = hi1;
+      r.n = 2;
+    }
+  } else if (lo1 <= hi1) {
+    r.a0 = lo1;
+    r.b0 = hi1;
+    r.n = 1;
+  }
+  return r;
+}
+
+// Appends an integer pair interval [lo, hi] (u coordinates, increasing starts) to a running
+// merge of at most 3 output intervals held in registers.
+struct Runs {
+  int l0, h0, l1, h1, l2, h2, n;
+};
+__device__ __forceinline__ void runs_push(Runs& r, int lo, int hi) {
+  if (r.n == 0) {
+    r.l0 = lo;
+    r.h0 = hi;
+    r.n = 1;
+  } else if (r.n == 1) {
+    if (lo <= r.h0 + 1) r.h0 = max(r.h0, hi);
+    else {
+      r.l1 = lo;
+      r.h1 = hi;
+      r.n = 2;
+    }
+  } else if (r.n == 2) {
+    if (lo <= r.h1 + 1) r.h1 = max(r.h1, hi);
+    else {
+      r.l2 = lo;
+      r.h2 = hi;
+      r.n = 3;
+    }
   } else {
-    nlo = arc_ge(a1[1] + ylo * a1[2], a2[1] + ylo * a2[2], ylo, theta_a, lo);
+    if (lo <= r.h2 + 1) r.h2 = max(r.h2, hi);
+    else r.n = 4;  // overflow: caller goes conservative
   }
-  if (yhi == INFINITY) {
-    nhi = 0;
+}
+
+// Ranges of one band from its lower/upper arc sets: S = U_lo \ U_hi, padded, merged, wrapped.
+__device__ __forceinline__ uint2 plan_from_sets(const Arc2& ulo, const Arc2& uhi, float pa, float inv_step, int M,
+                                                unsigned long long* work) {
+  // gaps of uhi inside [0, pi] (sorted): [0, a0], [b0, a1], [b_last, pi]
+  float g[6];
+  int ng;
+  if (uhi.n == 0) {
+    g[0] = 0.f;
+    g[1] = kPiF;
+    ng = 1;
+  } else if (uhi.n == 1) {
+    g[0] = 0.f;
+    g[1] = uhi.a0;
+    g[2] = uhi.b0;
+    g[3] = kPiF;
+    ng = 2;
   } else {
-    nhi = arc_ge(a1[1] + yhi * a1[2], a2[1] + yhi * a2[2], yhi, theta_a, hi);
+    g[0] = 0.f;
+    g[1] = uhi.a0;
+    g[2] = uhi.b0;
+    g[3] = uhi.a1;
+    g[4] = uhi.b1;
+    g[5] = kPiF;
+    ng = 3;
   }
-  // complement of hi within [0, pi]
-  if (nhi == 2 && hi[1].a < hi[0].a) {
-    const Iv t = hi[0];
-    hi[0] = hi[1];
-    hi[1] = t;
-  }
-  Iv comp[4];
-  int nc = 0;
-  float cur = 0.f;
-  for (int k = 0; k < nhi; ++k) {
-    if (hi[k].a > cur) comp[nc++] = {cur, hi[k].a};
-    cur = fmaxf(cur, hi[k].b);
-  }
-  if (cur < kPiF || nhi == 0) comp[nc++] = {cur, kPiF};
-  // pieces = lo intersect comp, converted to padded pair-index arcs, then unioned.
-  Seg seg[16];
-  int ns = 0;
-  bool full = false;
-  const float inv_step = 1.f / p.step_f;
-  for (int i = 0; i < nlo && !full; ++i) {
-    for (int j = 0; j < nc && !full; ++j) {
-      const float s1 = fmaxf(lo[i].a, comp[j].a), s2 = fminf(lo[i].b, comp[j].b);
-      if (!(s1 <= s2)) continue;
-      const int u1 = __float2int_rd(pa + s1 * inv_step) - kPad;
-      const int u2 = __float2int_ru(pa + s2 * inv_step) + kPad;
-      const int len = u2 - u1 + 1;
-      if (len >= M) {
-        full = true;
-        break;
-      }
-      int st = u1 % M;
-      if (st < 0) st += M;
-      if (st + len <= M) {
-        seg[ns++] = {st, st + len};
-      } else {
-        seg[ns++] = {st, M};
-        seg[ns++] = {0, st + len - M};
+  const float lo_a[2] = {ulo.a0, ulo.a1}, lo_b[2] = {ulo.b0, ulo.b1};
+  Runs runs{0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      if (i < ulo.n && j < ng) {
+        // strict: a zero-length gap/piece only arises where U_hi (eroded) robustly covers an arc
+        // end, so it holds no sample of this band
+        const float s1 = fmaxf(lo_a[i], g[2 * j]), s2 = fminf(lo_b[i], g[2 * j + 1]);
+        if (s1 < s2)
+          runs_push(runs, __float2int_rd(fmaf(s1, inv_step, pa)) - kPad, __float2int_ru(fmaf(s2, inv_step, pa)) + kPad);
       }
     }
   }
-  uint32_t r0 = 0, r1 = 0;
-  if (full) {
-    r0 = (uint32_t)M << 16;
+  const uint2 full = make_uint2((uint32_t)M << 16, 0u);
+  if (runs.n == 0) return make_uint2(0u, 0u);
+  if (runs.n > 3) {
     *work += (unsigned long long)M;
-  } else if (ns > 0) {
-    for (int i = 1; i < ns; ++i) {  // insertion sort by start
-      const Seg t = seg[i];
-      int j = i - 1;
-      while (j >= 0 && seg[j].s > t.s) {
-        seg[j + 1] = seg[j];
-        --j;
-      }
-      seg[j + 1] = t;
-    }
-    int nm = 0;
-    for (int i = 0; i < ns; ++i) {
-      if (nm > 0 && seg[i].s <= seg[nm - 1].e) {
-        seg[nm - 1].e = max(seg[nm - 1].e, seg[i].e);
-      } else {
-        seg[nm++] = seg[i];
-      }
-    }
-    int starts[2], lens[2], nr = 0;
-    if (nm >= 2 && seg[0].s == 0 && seg[nm - 1].e == M) {  // join across the wrap
-      starts[0] = seg[nm - 1].s;
-      lens[0] = seg[nm - 1].e - seg[nm - 1].s + seg[0].e;
-      nr = 1;
-      for (int i = 1; i < nm - 1; ++i) {
-        if (nr < 2) {
-          starts[nr] = seg[i].s;
-          lens[nr] = seg[i].e - seg[i].s;
-        }
-        ++nr;
-      }
+    return full;
+  }
+  // u spans [pa - pad, pa + M + pad]: the last run may wrap onto the first
+  int nl = runs.n;
+  int L0 = runs.l0, H0 = runs.h0, L1 = runs.l1, H1 = runs.h1;
+  if (nl == 3) {
+    if (runs.h2 - M >= runs.l0 - 1) {  // join last with first across the wrap
+      L0 = runs.l2;
+      H0 = runs.h0 + M;
+      nl = 2;  // (L0,H0) and (l1,h1)
     } else {
-      for (int i = 0; i < nm; ++i) {
-        if (nr < 2) {
-          starts[nr] = seg[i].s;
-          lens[nr] = seg[i].e - seg[i].s;
-        }
-        ++nr;
-      }
-    }
-    if (nr > 2) {  // cannot happen for a minor arc; stay conservative
-      r0 = (uint32_t)M << 16;
       *work += (unsigned long long)M;
-    } else {
-      // K2 walks ranges 64 pairs per warp iteration: round each range up to a multiple of 64
-      // (the extra pairs are real samples; ownership still decides) and merge overlaps so a
-      // pair is never visited twice by the same band.
-      int s0 = starts[0], l0 = (lens[0] + 63) & ~63;
-      int s1 = nr == 2 ? starts[1] : 0, l1 = nr == 2 ? (lens[1] + 63) & ~63 : 0;
-      if (nr == 2) {
-        const int d01 = ((s1 - s0) % M + M) % M, d10 = ((s0 - s1) % M + M) % M;
-        if (d01 < l0) {
-          l0 = (max(l0, d01 + l1) + 63) & ~63;
-          nr = 1;
-        } else if (d10 < l1) {
-          s0 = s1;
-          l0 = (max(l1, d10 + l0) + 63) & ~63;
-          nr = 1;
-        }
-      }
-      if (l0 >= M || (nr == 2 && l0 + l1 >= M)) {
-        r0 = (uint32_t)M << 16;
-        *work += (unsigned long long)M;
-      } else {
-        r0 = (uint32_t)s0 | ((uint32_t)l0 << 16);
-        *work += (unsigned long long)l0;
-        if (nr == 2) {
-          r1 = (uint32_t)s1 | ((uint32_t)l1 << 16);
-          *work += (unsigned long long)l1;
-        }
-      }
+      return full;
+    }
+  } else if (nl == 2) {
+    if (H1 - M >= L0 - 1) {
+      L0 = L1;
+      H0 = runs.h0 + M;
+      nl = 1;
     }
   }
-  r_out[0] = r0;
-  r_out[1] = r1;
+  int s0 = ((L0 % M) + M) % M, l0 = H0 - L0 + 1;
+  int s1 = ((L1 % M) + M) % M, l1 = nl == 2 ? H1 - L1 + 1 : 0;
+  if (l0 >= M || l1 >= M) {
+    *work += (unsigned long long)M;
+    return full;
+  }
+  // 64-pair alignment (K2 walks 64 pairs per warp iteration) and a final overlap merge
+  l0 = (l0 + 63) & ~63;
+  if (nl == 2) {
+    l1 = (l1 + 63) & ~63;
+    const int d01 = ((s1 - s0) % M + M) % M, d10 = ((s0 - s1) % M + M) % M;
+    if (d01 < l0) {
+      l0 = (max(l0, d01 + l1) + 63) & ~63;
+      nl = 1;
+    } else if (d10 < l1) {
+      s0 = s1;
+      l0 = (max(l1, d10 + l0) + 63) & ~63;
+      nl = 1;
+    }
+  }
+  if (l0 >= M || (nl == 2 && l0 + l1 >= M)) {
+    *work += (unsigned long long)M;
+    return full;
+  }
+  *work += (unsigned long long)(l0 + (nl == 2 ? l1 : 0));
+  return make_uint2((uint32_t)s0 | ((uint32_t)l0 << 16), nl == 2 ? ((uint32_t)s1 | ((uint32_t)l1 << 16)) : 0u);
 }
 
 __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, int64_t n) {
@@ -215,37 +234,50 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
   for (int t = threadIdx.x; t < p.n_bands; t += blockDim.x) s_work[t] = 0;
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
+  const bool valid = i < n;
+  const int M = p.halfJ;
+  float f1[3] = {0.f, 0.f, 0.f}, f2[3] = {0.f, 0.f, 0.f};
+  if (valid) {
     double a1[3], a2[3];
     exact_basis(b.zx[i], b.zy[i], b.zz[i], a1, a2);
-    float f1[3], f2[3];
+#pragma unroll
     for (int k = 0; k < 3; ++k) {
       f1[k] = __double2float_rn(a1[k]);
       f2[k] = __double2float_rn(a2[k]);
     }
     b.basis_a[i] = make_float4(f1[0], f1[1], f1[2], f2[0]);
     b.basis_b[i] = make_float2(f2[1], f2[2]);
-    const float rc = hypotf(f1[2], f2[2]);
-    const int M = p.halfJ;
-    if (!(rc >= kRcMin)) {  // near-polar constraint: c ~ 0 everywhere, every band sees all pairs
-      for (int band = 0; band < p.n_bands; ++band) {
-        uint2* rp = reinterpret_cast<uint2*>(b.ranges) + (int64_t)band * n + i;
-        *rp = make_uint2((uint32_t)M << 16, 0u);
-        atomicAdd(&s_work[band], (unsigned long long)M);
+  }
+  // near-polar constraint: c ~ 0 everywhere, every band sees all pairs
+  const bool polar = !(sqrtf(fmaf(f1[2], f1[2], f2[2] * f2[2])) >= kRcMin);
+  const float theta_a = atan2_fast(f2[2], f1[2]) + 0.5f * kPiF;  // c(theta_a + s) = -rc sin(s)
+  const float inv_step = 1.f / p.step_f;
+  const float pa = (theta_a + kPiF) * inv_step;
+  uint2* rp = reinterpret_cast<uint2*>(b.ranges) + i;
+  Arc2 ulo{0.f, kPiF, 0.f, 0.f, 1};  // band 0: Y >= -inf
+  for (int band = 0; band < p.n_bands; ++band) {  // uniform trip count: warp reductions below
+    unsigned long long w = 0;
+    if (valid) {
+      uint2 r;
+      if (polar) {
+        r = make_uint2((uint32_t)M << 16, 0u);
+        w = (unsigned long long)M;
+      } else {
+        if (band > 0) {
+          const float y0 = p.band_ylo[band];
+          ulo = arc_ge(fmaf(y0, f1[2], f1[1]), fmaf(y0, f2[2], f2[1]), y0, theta_a, kArcDilate);
+        }
+        Arc2 uhi{0.f, 0.f, 0.f, 0.f, 0};  // last band: Y >= +inf is empty
+        if (band < p.n_bands - 1) {
+          const float y1 = p.band_yhi[band];
+          uhi = arc_ge(fmaf(y1, f1[2], f1[1]), fmaf(y1, f2[2], f2[1]), y1, theta_a, -kArcDilate);
+        }
+        r = plan_from_sets(ulo, uhi, pa, inv_step, M, &w);
       }
-    } else {
-      const float theta_c = atan2f(f2[2], f1[2]);
-      const float theta_a = theta_c + 0.5f * kPiF;  // c(theta_a + s) = -rc sin(s) <= 0 on s in [0, pi]
-      const float pa = (theta_a + kPiF) / p.step_f;
-      for (int band = 0; band < p.n_bands; ++band) {
-        uint32_t r[2];
-        unsigned long long w = 0;
-        plan_band(p, band, f1, f2, theta_a, pa, r, &w);
-        uint2* rp = reinterpret_cast<uint2*>(b.ranges) + (int64_t)band * n + i;
-        *rp = make_uint2(r[0], r[1]);
-        if (w) atomicAdd(&s_work[band], w);
-      }
+      rp[(int64_t)band * n] = r;
     }
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xFFFFFFFFu, w, o);
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(&s_work[band], w);
   }
   __syncthreads();
   for (int t = threadIdx.x; t < p.n_bands; t += blockDim.x)
@@ -382,6 +414,8 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     fc.own_hi = band == p.n_bands - 1 ? G : r0 + hb;
     const int row_off = p.magic_hi + r0;      // row_local = (bits_y >> S) - row_off
     const int col_off = p.magic_hi + p.c_min; // col_local = (bits_x >> S) - col_off
+    const uint32_t lin_off = (uint32_t)row_off * (uint32_t)W + (uint32_t)col_off;
+    const uint32_t tile_cells = (uint32_t)hb * (uint32_t)W;
     const uint2* rbase = reinterpret_cast<const uint2*>(b.ranges) + (int64_t)band * n;
     int* counter = &b.counters[1 + band];
     for (;;) {  // per-warp dynamic grabs of kWarpGrab constraints
@@ -425,14 +459,19 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
               const uint32_t bx = (uint32_t)__float_as_int(fmaf(x, rkf, CMf));
               const uint32_t by = (uint32_t)__float_as_int(fmaf(y, rkf, CMf));
               flag[h] = (fabsf(c) < kDc) | ((bx & fmask) == 0u) | ((by & fmask) == 0u);
-              int row = (int)(by >> S) - row_off;
-              int col = (int)(bx >> S) - col_off;
+              // cell index relative to the tile; the column is always inside [c_min, c_min+W) for
+              // an unflagged pair (|X| <= 1 < extent, or clamped), so one unsigned range test on
+              // the linear index is the band-ownership test
+              uint32_t rel;
               if (kClamp) {
-                row = min(max(row + r0, 0), G - 1) - r0;
-                col = min(max(col + p.c_min, 0), G - 1) - p.c_min;
+                const int row = min(max((int)(by >> S) - p.magic_hi, 0), G - 1) - r0;
+                const int col = min(max((int)(bx >> S) - p.magic_hi, 0), G - 1) - p.c_min;
+                rel = (uint32_t)(row * W + col);
+              } else {
+                rel = (by >> S) * (uint32_t)W + (bx >> S) - lin_off;
               }
-              const bool dep = !flag[h] && (unsigned)row < (unsigned)hb;
-              addr[h] = dep ? tile_s + 4u * (uint32_t)(row * W + col) : dummy_s;
+              const bool dep = !flag[h] && rel < tile_cells;
+              addr[h] = dep ? tile_s + 4u * rel : dummy_s;
             }
             red_shared(addr[0], 2u);
             red_shared(addr[1], 2u);
