@@ -83,10 +83,14 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.05)
+            time.sleep(0.005)
 
     def __enter__(self):
         if self.nv:
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            except Exception:
+                pass
             self._thread = threading.Thread(target=self._run, daemon=True)
             self._thread.start()
         return self

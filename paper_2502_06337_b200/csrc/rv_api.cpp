@@ -123,6 +123,9 @@ struct rv_context {
   DBuf bins, raw, angle_counts, angle_sums, angle_result, sup_counts, sup_result, band_flagsA, band_flagsB,
       band_idx, band_vals, near_h, near_result;
   DBuf user_z;  // scratch copy of a constraint span (path functions)
+  DBuf chunk_hi;                          // pipelined vote: kept count at each chunk end
+  cudaStream_t copy_st = nullptr;         // H2D copies of the pipelined host path
+  std::vector<cudaEvent_t> chunk_events;
   std::deque<std::pair<VotePlan, int>> plans;  // vote plans by (G, E, J)
   // pinned host scalars
   void* pinned = nullptr;
@@ -314,6 +317,7 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   b.zy = zy;
   b.zz = zz;
   b.grid = grid;
+  b.layout_n = n;
   b.table64 = c->table64.get<double2>(J);
   b.table32 = c->table32.get<float2>(std::max(J / 2, 1));
   c->times.vote_samples += n * (int64_t)J;
@@ -413,9 +417,12 @@ std::vector<Peak> find_peaks_dev(rv_context* c, const uint32_t* grid, int G, dou
 // sample the sum would be short: the vote is then redone with the generic exact kernel.
 std::pair<const uint32_t*, std::vector<Peak>> vote_and_peak(rv_context* c, const double* zx, const double* zy,
                                                             const double* zz, int64_t n, const rv_config& cfg,
-                                                            uint32_t min_votes, bool allow_no_peak) {
+                                                            uint32_t min_votes, bool allow_no_peak,
+                                                            const uint32_t* prevoted = nullptr) {
   for (int attempt = 0; attempt < 2; ++attempt) {
-    const uint32_t* grid = vote(c, zx, zy, zz, n, cfg.grid, cfg.extent, cfg.theta_samples, attempt == 1);
+    const uint32_t* grid = (attempt == 0 && prevoted)
+                               ? prevoted
+                               : vote(c, zx, zy, zz, n, cfg.grid, cfg.extent, cfg.theta_samples, attempt == 1);
     unsigned long long total = 0;
     std::vector<Peak> peaks;
     try {
@@ -765,6 +772,137 @@ Estimate identity_estimate(std::vector<int32_t> idx) {
   return e;
 }
 
+// Host-buffer input, pipelined: the H2D copy of chunk k+1 (copy stream) overlaps preprocess +
+// band plan + vote of chunk k (compute stream). Chunk boundaries are multiples of the preprocess
+// block so the single-pass compaction continues across launches; each chunk's kept-constraint
+// range [lo, hi) stays on the device (chunk_hi[]) and bounds the plan/vote launches of that
+// chunk. Vote tiles flush to partial slots that the final reduction sums once (integer: the grid
+// is identical to the one-shot vote). Returns the preprocess result and the voted grid.
+struct PipelinedVote {
+  PreResult pre;
+  const uint32_t* grid = nullptr;
+  const double* d_corrs = nullptr;
+};
+
+PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n, const rv_config& cfg) {
+  PipelinedVote out;
+  double* d = c->corrs.get<double>((size_t)n * 6);
+  out.d_corrs = d;
+  const int G = cfg.grid, J = cfg.theta_samples;
+  if (G < 1 || !(cfg.extent > 0.0)) fail(RV_ERR_INVALID_CONFIG, "accumulator needs grid >= 1, extent > 0");
+  if (J < 1) fail(RV_ERR_INVALID_CONFIG, "theta_samples must be >= 1");
+  ensure_tables(c, J);
+  const VotePlan& p = cached_plan(c, G, cfg.extent, J);
+  const int C = (p.banded && n >= (int64_t)1 << 18) ? 4 : 1;
+  if (!c->copy_st) ck(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking), "copy stream");
+  while ((int)c->chunk_events.size() < C) {
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    c->chunk_events.push_back(e);
+  }
+  std::vector<int64_t> bounds(C + 1);
+  for (int k = 0; k <= C; ++k) bounds[k] = k == C ? n : std::min<int64_t>(n, ((n * k / C) + 255) / 256 * 256);
+  StageScope sc(c, kVote);
+  // order the copy stream after everything already queued on the compute stream (buffer reuse)
+  cudaEvent_t start = take_event(c);
+  ck(cudaEventRecord(start, c->st), "record");
+  ck(cudaStreamWaitEvent(c->copy_st, start, 0), "wait");
+  auto issue_copy = [&](int k) {
+    ck(cudaMemcpyAsync(d + 6 * bounds[k], h_corrs + 6 * bounds[k], sizeof(double) * 6 * (bounds[k + 1] - bounds[k]),
+                       cudaMemcpyHostToDevice, c->copy_st),
+       "H2D chunk");
+    ck(cudaEventRecord(c->chunk_events[k], c->copy_st), "record chunk");
+  };
+  issue_copy(0);
+  // preprocess state
+  PrepBuffers pb;
+  pb.corrs = d;
+  pb.zx = c->zx.get<double>(n);
+  pb.zy = c->zy.get<double>(n);
+  pb.zz = c->zz.get<double>(n);
+  pb.kept = c->kept.get<int32_t>(n);
+  pb.dropped = c->dropped.get<int32_t>(n);
+  const int nb_prep = prep_blocks(n);
+  pb.status = c->status.get<unsigned long long>(nb_prep);
+  int32_t* misc = c->misc32.get<int32_t>(8);
+  pb.block_counter = misc;
+  pb.totals = misc + 2;
+  int32_t* chunk_hi = c->chunk_hi.get<int32_t>(C + 1);
+  ck(cudaMemsetAsync(pb.status, 0, sizeof(unsigned long long) * nb_prep, c->st), "memset status");
+  ck(cudaMemsetAsync(misc, 0, sizeof(int32_t) * 8, c->st), "memset misc");
+  ck(cudaMemsetAsync(chunk_hi, 0, sizeof(int32_t) * (C + 1), c->st), "memset chunk_hi");
+  // vote state
+  uint32_t* grid = c->grid.get<uint32_t>((size_t)G * G);
+  VoteBuffers b;
+  b.zx = pb.zx;
+  b.zy = pb.zy;
+  b.zz = pb.zz;
+  b.grid = grid;
+  b.layout_n = n;
+  b.table64 = c->table64.get<double2>(J);
+  b.table32 = c->table32.get<float2>(std::max(J / 2, 1));
+  int n_ctas = c->sms;
+  if (p.banded) {
+    b.basis_a = c->basis_a.get<float4>(n);
+    b.basis_b = c->basis_b.get<float2>(n);
+    b.ranges = c->ranges.get<uint32_t>((size_t)n * p.n_bands * 2);
+    b.band_work = c->band_work.get<unsigned long long>(kMaxBands);
+    b.counters = c->counters.get<int32_t>(kMaxBands + 1);
+    b.stats = c->stats.get<unsigned long long>(2);
+    const int64_t est_pairs = (n / C) * (int64_t)p.halfJ;
+    n_ctas = (int)std::clamp<int64_t>(est_pairs >> 20, std::min(p.n_bands, c->sms), c->sms);
+    b.max_slots = C * n_ctas * p.n_bands;
+    b.partials = c->partials.get<uint32_t>((size_t)b.max_slots * p.tile_words);
+    b.slot_band = c->slot_band.get<int32_t>(b.max_slots);
+    ck(cudaMemsetAsync(b.band_work, 0, sizeof(unsigned long long) * kMaxBands, c->st), "memset band_work");
+    ck(cudaMemsetAsync(b.counters, 0, sizeof(int32_t) * (kMaxBands + 1), c->st), "memset counters");
+    ck(cudaMemsetAsync(b.stats, 0, sizeof(unsigned long long) * 2, c->st), "memset stats");
+  }
+  ck(cudaMemsetAsync(grid, 0, sizeof(uint32_t) * (size_t)G * G, c->st), "memset grid");
+  for (int k = 0; k < C; ++k) {
+    ck(cudaStreamWaitEvent(c->st, c->chunk_events[k], 0), "wait chunk");
+    pb.chunk_hi = chunk_hi + k + 1;
+    launch_preprocess_range(pb, n, bounds[k], bounds[k + 1], cfg.tau_z, cfg.normalize_inputs, c->st);
+    count_launch(c);
+    if (p.banded) {
+      b.bounds = chunk_hi + k;
+      const int64_t cap = bounds[k + 1] - bounds[k];
+      launch_plan(p, b, cap, c->st);
+      ck(cudaMemsetAsync(b.counters + 1, 0, sizeof(int32_t) * kMaxBands, c->st), "memset band counters");
+      launch_vote_banded(p, b, cap, n_ctas, c->st);
+      count_launch(c, 2);
+    }
+    // copy k+1 is issued after compute k is queued: with pinned input both run concurrently;
+    // with pageable input the host stages copy k+1 while the device computes chunk k
+    if (k + 1 < C) issue_copy(k + 1);
+  }
+  int32_t* h = reinterpret_cast<int32_t*>(c->pinned);
+  if (p.banded) {
+    launch_vote_reduce(p, b, c->st);
+    count_launch(c);
+  }
+  ck(cudaGetLastError(), "pipelined vote");
+  ck(cudaMemcpyAsync(h, pb.totals, 8, cudaMemcpyDeviceToHost, c->st), "totals D2H");
+  sync(c);
+  out.pre.cs.zx = pb.zx;
+  out.pre.cs.zy = pb.zy;
+  out.pre.cs.zz = pb.zz;
+  out.pre.cs.kept = pb.kept;
+  out.pre.cs.n = h[0];
+  out.pre.n_dropped = h[1];
+  if (!p.banded && out.pre.cs.n > 0)  // generic path: vote once all constraints are in
+    out.grid = vote(c, pb.zx, pb.zy, pb.zz, out.pre.cs.n, G, cfg.extent, J);
+  else
+    out.grid = grid;
+  c->times.vote_samples += out.pre.cs.n * (int64_t)J;
+  c->times.vote_launches += 1;
+  return out;
+}
+
+// estimate_single from a preprocessed constraint set (identity shortcuts already handled).
+Estimate finish_single(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
+                       const uint32_t* prevoted);
+
 // estimate_single (estimator.cpp:320-371) over device-resident correspondences.
 Estimate estimate_single_dev(rv_context* c, const double* d_corrs, int64_t n, const rv_config& cfg) {
   if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
@@ -775,7 +913,25 @@ Estimate estimate_single_dev(rv_context* c, const double* d_corrs, int64_t n, co
     return identity_estimate(std::move(all));
   }
   if (pre.n_dropped * 10 >= n * 9) return identity_estimate(dropped_list(c, pre.n_dropped));
-  const auto [grid, peaks] = vote_and_peak(c, pre.cs.zx, pre.cs.zy, pre.cs.zz, pre.cs.n, cfg, 1, false);
+  return finish_single(c, pre, d_corrs, cfg, nullptr);
+}
+
+// estimate_single with host input: pipelined H2D + preprocess + vote, then the same solve.
+Estimate estimate_single_host(rv_context* c, const double* h_corrs, int64_t n, const rv_config& cfg) {
+  if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
+  const PipelinedVote pv = prep_and_vote_host(c, h_corrs, n, cfg);
+  if (pv.pre.cs.n == 0) {
+    std::vector<int32_t> all(n);
+    for (int64_t i = 0; i < n; ++i) all[i] = (int32_t)i;
+    return identity_estimate(std::move(all));
+  }
+  if (pv.pre.n_dropped * 10 >= n * 9) return identity_estimate(dropped_list(c, pv.pre.n_dropped));
+  return finish_single(c, pv.pre, pv.d_corrs, cfg, pv.grid);
+}
+
+Estimate finish_single(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
+                       const uint32_t* prevoted) {
+  const auto [grid, peaks] = vote_and_peak(c, pre.cs.zx, pre.cs.zy, pre.cs.zz, pre.cs.n, cfg, 1, false, prevoted);
   Estimate est;
   {  // estimate_from_peak (estimator.cpp:94-101)
     double A, B, b[3], axis[3];
@@ -1110,6 +1266,8 @@ void rv_context_destroy(rv_context* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
   for (auto e : c->event_pool) cudaEventDestroy(e);
+  for (auto e : c->chunk_events) cudaEventDestroy(e);
+  if (c->copy_st) cudaStreamDestroy(c->copy_st);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
@@ -1153,8 +1311,7 @@ rv_status rv_estimate_single(rv_context* c, const double* corrs, int64_t n, cons
     cudaSetDevice(c->device);
     c->results.clear();
     if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
-    const double* d = upload_corrs(c, corrs, n);
-    Estimate e = estimate_single_dev(c, d, n, *cfg);
+    Estimate e = estimate_single_host(c, corrs, n, *cfg);
     to_c(e, out, seconds_since(c));
     c->results.push_back(std::move(e.inliers));
   });

@@ -59,6 +59,8 @@ struct VoteBuffers {
   int32_t* counters = nullptr;         // [0]=slot counter, [1..kMaxBands]=constraint counters per band
   unsigned long long* stats = nullptr; // [0]=pairs evaluated, [1]=fallback pairs
   int max_slots = 0;
+  int64_t layout_n = 0;                // ranges stride per band (capacity)
+  const int32_t* bounds = nullptr;     // device [lo, hi) of constraints for this launch (null: [0, n))
 };
 
 // K1: constraint basis (exact f64 -> f32) and band culling plan per constraint.
@@ -84,9 +86,13 @@ struct PrepBuffers {
   unsigned long long* status = nullptr;  // [nblocks] look-back status (zeroed before launch)
   int32_t* block_counter = nullptr;      // dynamic block id (zeroed before launch)
   int32_t* totals = nullptr;             // [0]=n_kept [1]=n_dropped
+  int32_t* chunk_hi = nullptr;           // optional: kept count through the end of this launch's range
 };
 int prep_blocks(int64_t n);
 void launch_preprocess(const PrepBuffers& b, int64_t n, double tau_z, int normalize, cudaStream_t s);
+// One chunk [elem_lo, elem_hi) of a pipelined preprocess (elem_lo multiple of 256; chunks in order).
+void launch_preprocess_range(const PrepBuffers& b, int64_t n, int64_t elem_lo, int64_t elem_hi, double tau_z,
+                             int normalize, cudaStream_t s);
 
 // K3: peak search over a device grid (rv_peaks.cu).
 struct Disk {

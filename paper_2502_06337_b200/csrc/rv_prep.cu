@@ -19,8 +19,8 @@ namespace {
 constexpr int kPrepThreads = 256;
 
 template <bool kVec>
-__global__ void __launch_bounds__(kPrepThreads) preprocess_kernel(PrepBuffers b, int64_t n, double tau_z,
-                                                                  int normalize) {
+__global__ void __launch_bounds__(kPrepThreads) preprocess_kernel(PrepBuffers b, int64_t n, int64_t elem_hi,
+                                                                  double tau_z, int normalize) {
   __shared__ int s_bid;
   __shared__ int s_warp_kept[kPrepThreads / 32];
   __shared__ long long s_excl;
@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(kPrepThreads) preprocess_kernel(PrepBuffers b,
     b.totals[0] = (int32_t)(excl + total);
     b.totals[1] = (int32_t)(n - (excl + total));
   }
+  if (tid == 0 && b.chunk_hi && block_end >= elem_hi) *b.chunk_hi = (int32_t)(excl + total);
 }
 
 constexpr int kGatherThreads = 256;
@@ -129,9 +130,20 @@ void launch_preprocess(const PrepBuffers& b, int64_t n, double tau_z, int normal
   const int blocks = prep_blocks(n);
   const bool vec = (reinterpret_cast<uintptr_t>(b.corrs) & 15u) == 0;
   if (vec)
-    preprocess_kernel<true><<<blocks, kPrepThreads, 0, s>>>(b, n, tau_z, normalize);
+    preprocess_kernel<true><<<blocks, kPrepThreads, 0, s>>>(b, n, n, tau_z, normalize);
   else
-    preprocess_kernel<false><<<blocks, kPrepThreads, 0, s>>>(b, n, tau_z, normalize);
+    preprocess_kernel<false><<<blocks, kPrepThreads, 0, s>>>(b, n, n, tau_z, normalize);
+}
+
+void launch_preprocess_range(const PrepBuffers& b, int64_t n, int64_t elem_lo, int64_t elem_hi, double tau_z,
+                             int normalize, cudaStream_t s) {
+  const int blocks = (int)((elem_hi - elem_lo + kPrepThreads - 1) / kPrepThreads);
+  if (blocks <= 0) return;
+  const bool vec = (reinterpret_cast<uintptr_t>(b.corrs) & 15u) == 0;
+  if (vec)
+    preprocess_kernel<true><<<blocks, kPrepThreads, 0, s>>>(b, n, elem_hi, tau_z, normalize);
+  else
+    preprocess_kernel<false><<<blocks, kPrepThreads, 0, s>>>(b, n, elem_hi, tau_z, normalize);
 }
 
 void launch_gather_residual(const double* zx, const double* zy, const double* zz, const int32_t* kept,

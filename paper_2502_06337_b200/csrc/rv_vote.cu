@@ -233,8 +233,10 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
   __shared__ unsigned long long s_work[kMaxBands];
   for (int t = threadIdx.x; t < p.n_bands; t += blockDim.x) s_work[t] = 0;
   __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = i < n;
+  const int64_t lo = b.bounds ? b.bounds[0] : 0, hi = b.bounds ? b.bounds[1] : n;
+  const int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = i < hi;
+  const int64_t stride = b.layout_n;
   const int M = p.halfJ;
   float f1[3] = {0.f, 0.f, 0.f}, f2[3] = {0.f, 0.f, 0.f};
   if (valid) {
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
         }
         r = plan_from_sets(ulo, uhi, pa, inv_step, M, &w);
       }
-      rp[(int64_t)band * n] = r;
+      rp[(int64_t)band * stride] = r;
     }
     for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xFFFFFFFFu, w, o);
     if ((threadIdx.x & 31) == 0 && w) atomicAdd(&s_work[band], w);
@@ -364,6 +366,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t* fbq = fbq_all + warp * kFbqCap;
+  const int64_t c_lo = b.bounds ? b.bounds[0] : 0, c_hi = b.bounds ? b.bounds[1] : n;
   for (int k = tid; k < 2 * M + 64; k += blockDim.x) tab[k] = b.table32[k % M];
 
   if (tid == 0) {  // initial band: CTAs split across bands in proportion to planned work
@@ -416,14 +419,14 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     const int col_off = p.magic_hi + p.c_min; // col_local = (bits_x >> S) - col_off
     const uint32_t lin_off = (uint32_t)row_off * (uint32_t)W + (uint32_t)col_off;
     const uint32_t tile_cells = (uint32_t)hb * (uint32_t)W;
-    const uint2* rbase = reinterpret_cast<const uint2*>(b.ranges) + (int64_t)band * n;
+    const uint2* rbase = reinterpret_cast<const uint2*>(b.ranges) + (int64_t)band * b.layout_n;
     int* counter = &b.counters[1 + band];
     for (;;) {  // per-warp dynamic grabs of kWarpGrab constraints
       int64_t g0 = 0;
       if (lane == 0) g0 = atomicAdd(counter, kWarpGrab);
-      g0 = __shfl_sync(0xFFFFFFFFu, g0, 0);
-      if (g0 >= n) break;
-      const int64_t g1 = (g0 + kWarpGrab < n) ? g0 + kWarpGrab : n;
+      g0 = __shfl_sync(0xFFFFFFFFu, g0, 0) + c_lo;
+      if (g0 >= c_hi) break;
+      const int64_t g1 = (g0 + kWarpGrab < c_hi) ? g0 + kWarpGrab : c_hi;
       int qn = 0;
       uint2 rr = rbase[g0];
       float4 ba = b.basis_a[g0];
@@ -512,7 +515,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
       int best = -1;
       long long best_rem = 0;
       for (int q = 0; q < p.n_bands; ++q) {
-        const long long rem = (long long)n - *((volatile int*)&b.counters[1 + q]);
+        const long long rem = (long long)(c_hi - c_lo) - *((volatile int*)&b.counters[1 + q]);
         if (rem > best_rem) {
           best_rem = rem;
           best = q;

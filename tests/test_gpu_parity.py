@@ -225,6 +225,20 @@ def test_full_size_properties(ctx, key):
     assert orc.rotation_error_deg(rots[0], e1.rotation) < (0.05 if key == "c3" else 1.0)
 
 
+def test_pipelined_host_path_matches_device_path(ctx):
+    # estimate_single with host input overlaps chunked H2D with preprocess/plan/vote; the result
+    # must be identical to the device-resident solve (same grid => same peak, inliers, rotation)
+    import torch
+    corrs, _, _ = synth.make_config("c3")
+    e_host = ctx.estimate_single(corrs)
+    d = torch.from_numpy(corrs).cuda()
+    e_dev = ctx.estimate_single_device(d.data_ptr(), corrs.shape[0])
+    assert np.array_equal(e_host.inliers, e_dev.inliers) and np.array_equal(e_host.rotation, e_dev.rotation)
+    assert e_host.axis_votes == e_dev.axis_votes
+    st = ctx.stage_times()
+    assert st["vote_guard_reruns"] == 0
+
+
 def test_full_size_multi_recovers_three(ctx):
     corrs, rots, _ = synth.make_config("c5")
     ms = ctx.estimate_multi(corrs, rv.EstimatorConfig(max_models=3))
