@@ -12,8 +12,10 @@ One step = one full solve (preprocess, vote, peak, refine, angle vote, rotation)
   cpu_baseline: the reference (oracle/_ref, unmodified sources, reference flags) on the host
            cores, bounded sample, rank 0 at N=1 only
 
-Multi-GPU (torchrun): every rank solves its own independent C3 problem (batches of independent
-problems split across GPUs, "scaling": "weak"); device time = max over ranks.
+Multi-GPU (torchrun, --mode sharded, default): one C3 problem, correspondences sharded across
+ranks, per-rank vote, NCCL all-reduce of the uint32 grid, all-gather of the input, replicated
+finish ("scaling": "strong"); --mode replicas: one independent problem per rank ("weak").
+Device time = max over ranks.
 `--impl reference` runs the reference CPU implementation instead (rank 0 only).
 """
 from __future__ import annotations
@@ -177,31 +179,50 @@ def run_device(args):
         dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
     import paper_2502_06337_b200 as rv
+    from paper_2502_06337_b200 import distributed as rvd
     from paper_2502_06337_b200 import synth
 
     ctx = rv.Context(local)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     cfg = rv.EstimatorConfig()
-    # independent problem per rank (replicas); rank 0 solves the canonical C3 scene
+    sharded = world > 1 and args.mode == "sharded"
     c = synth.CONFIGS[WORKLOAD]
-    corrs, rots, _ = synth.make_scene(c.n, c.outlier_frac, c.sigma, seed=c.seed + 1000 * rank)
-    n = corrs.shape[0]
-    d_corrs = torch.from_numpy(corrs).to(f"cuda:{local}")
-    host = torch.empty((n, 6), dtype=torch.float64, pin_memory=True)
-    host.numpy()[:] = corrs
+    if sharded:  # one C3 problem, correspondences sharded across ranks (strong scaling)
+        corrs, rots, _ = synth.make_config(WORKLOAD)
+        lo, hi = rvd.shard_bounds(corrs.shape[0], world, rank)
+        mine = np.ascontiguousarray(corrs[lo:hi])
+    else:  # independent problem per rank (replicas); rank 0 solves the canonical C3 scene
+        corrs, rots, _ = synth.make_scene(c.n, c.outlier_frac, c.sigma, seed=c.seed + 1000 * rank)
+        mine = corrs
+    n_total = corrs.shape[0]
+    n_mine = mine.shape[0]
+    d_mine = torch.from_numpy(mine).to(f"cuda:{local}")
+    host = torch.empty((n_mine, 6), dtype=torch.float64, pin_memory=True)
+    host.numpy()[:] = mine
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MiB > L2
+    backend = rvd.DeviceBackend(ctx)
+
+    def solve_device():
+        if sharded:
+            return rvd.sharded_estimate_single(d_mine, n_total, cfg, backend)
+        return ctx.estimate_single_device(d_mine.data_ptr(), n_mine, cfg)
+
+    def solve_e2e():
+        if sharded:  # H2D of this rank's shard inside the step, then the sharded solve
+            d_mine.copy_(host, non_blocking=True)
+            return rvd.sharded_estimate_single(d_mine, n_total, cfg, backend)
+        return ctx.estimate_single(host.numpy(), cfg)
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up (W >= 3 enforced)
     warm = max(3, args.warmup)
     for _ in range(warm):
-        ctx.estimate_single_device(d_corrs.data_ptr(), n, cfg)
-        ctx.estimate_single(host.numpy(), cfg)
+        solve_device()
+        solve_e2e()
     ctx.enable_timing(True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     vote_ms, launches, stage = [], 0, []
@@ -209,9 +230,10 @@ def run_device(args):
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             flush.zero_()
+            barrier()
             a, b = ev[k]
             a.record(stream)
-            est = ctx.estimate_single_device(d_corrs.data_ptr(), n, cfg)
+            est = solve_device()
             b.record(stream)
             st = ctx.stage_times()
             vote_ms.append(st["vote_ms"])
@@ -219,20 +241,18 @@ def run_device(args):
             stage.append(st)
         barrier()
     dev_ms = [a.elapsed_time(b) for a, b in ev]
-    # timing breakdown: events bracket the solve including its host round trips
     ctx.enable_timing(False)
-    # end-to-end through the public C-ABI with host (pinned) buffers
     ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     e2e_wall = []
     d2h_bytes = 0
     barrier()
     for k in range(args.steps):
         flush.zero_()
+        barrier()
         a, b = ev2[k]
-        torch.cuda.synchronize()
         t0 = time.perf_counter()
         a.record(stream)
-        est_h = ctx.estimate_single(host.numpy(), cfg)
+        est_h = solve_e2e()
         b.record(stream)
         torch.cuda.synchronize()
         e2e_wall.append(time.perf_counter() - t0)
@@ -246,7 +266,7 @@ def run_device(args):
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     t_dev, t_e2e, t_vote = vals.tolist()
-    total_corrs = n * world * args.steps
+    total_corrs = (n_total if sharded else n_total * world) * args.steps
     value = total_corrs / t_dev
     e2e_value = total_corrs / t_e2e
     if rank != 0:
@@ -255,7 +275,7 @@ def run_device(args):
         return
     err_deg = float(np.degrees(np.arccos(np.clip(0.5 * (np.trace(rots[0].T @ est.rotation) - 1), -1, 1))))
     # roofline of the dominant kernel (vote): algorithmic sample-votes per launch / launch time
-    votes_per_launch = n * cfg.theta_samples
+    votes_per_launch = n_mine * cfg.theta_samples
     vote_avg_s = t_vote / args.steps
     achieved = votes_per_launch / vote_avg_s
     peak = smem_atomic_peak(local)
@@ -263,11 +283,11 @@ def run_device(args):
             "achieved": achieved / 1e9, "peak": (peak / 1e9) if peak else None, "unit": "Gvotes/s",
             "frac": (achieved / peak) if peak else None, "traffic": None,
             "peak_source": "conflict-free u32 smem atomicAdd, measured live (tools/microbench)",
-            "work_per_launch": f"{votes_per_launch} sample-votes (N*J)",
+            "work_per_launch": f"{votes_per_launch} sample-votes (N*J of this rank)",
             "vote_ms_per_solve": 1e3 * vote_avg_s, "vote_share_of_solve": t_vote / t_dev}
     pre_ms = statistics.mean(s["preprocess_ms"] for s in stage)
     hbm = measured_peaks().get("hbm_gbs")
-    k1_gbs = (76.0 * n) / (pre_ms * 1e-3) / 1e9
+    k1_gbs = (76.0 * n_mine) / (pre_ms * 1e-3) / 1e9 if pre_ms > 0 else None
     cpu = None
     if world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
@@ -277,15 +297,21 @@ def run_device(args):
                "kind": "reference" if kind.startswith("ref") else "port",
                "sample": f"reference estimate_single on the first {args.cpu_sample} C3 correspondences, median of "
                          f"3, cfg.threads={threads}"}
+    extra = {"parallelism": (f"sharded{world} (contiguous shards, NCCL all-reduce of the uint32 grid, "
+                             f"all-gather of the input)") if sharded else
+             (f"replicas{world}" if world > 1 else "single"),
+             "solves_per_step": 1 if sharded else world}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": warm, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": warm, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
+            "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic (seeded BASELINE generator, sigma=0.01)",
-            "config": config_block(n, world),
+            "config": config_block(n_total, world, extra),
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": 1e3 * t_e2e / args.steps,
-                    "h2d_bytes_per_step": int(n * 48 * world), "d2h_bytes_per_step": int(d2h_bytes * world)},
+                    "h2d_bytes_per_step": int(n_total * 48 * (1 if sharded else world)),
+                    "d2h_bytes_per_step": int(d2h_bytes * (1 if sharded else world))},
             "roofline": roof,
             "roofline_k1": {"bound": "hbm", "kernel": "preprocess_kernel", "achieved": k1_gbs, "peak": hbm,
-                            "unit": "GB/s", "frac": k1_gbs / hbm if hbm else None,
+                            "unit": "GB/s", "frac": (k1_gbs / hbm) if (hbm and k1_gbs) else None,
                             "traffic": None, "bytes_per_corr": 76},
             "stage_ms": {k: statistics.mean(s[k] for s in stage) for k in
                          ("preprocess_ms", "vote_ms", "peaks_ms", "refine_ms", "angles_ms")},
@@ -302,9 +328,11 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=200_000)
-    ap.add_argument("--ref-sample", type=int, default=200_000)
+    ap.add_argument("--cpu-sample", type=int, default=1_000_000)
+    ap.add_argument("--ref-sample", type=int, default=1_000_000)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
+                    help="N>1: shard one C3 problem across ranks (strong) or one problem per rank (weak)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

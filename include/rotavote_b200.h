@@ -127,6 +127,18 @@ rv_status rv_estimate_multi(rv_context* ctx, const double* corrs, int64_t n, con
 rv_status rv_estimate_multi_device(rv_context* ctx, const double* d_corrs, int64_t n,
                                    const rv_config* cfg, rv_estimate* out, int32_t capacity,
                                    int32_t* n_models);
+/* ---- sharded solve (one process per GPU; the caller runs the collectives) ------------- */
+/* Vote of one contiguous shard of the correspondences: preprocess the shard and deposit its
+ * constraints' samples into d_grid (grid*grid uint32, device, overwritten). Integer grids of all
+ * shards sum (e.g. ncclAllReduce, ncclUint32, ncclSum) to exactly the grid of
+ * accumulate(preprocess(all)) -- voting.cpp:88-118 is order-independent. */
+rv_status rv_vote_shard(rv_context* ctx, const double* d_corrs_shard, int64_t n_shard, const rv_config* cfg,
+                        uint32_t* d_grid, int64_t* n_kept_shard);
+/* estimate_single (estimator.cpp:320-371) on all correspondences with the vote grid supplied
+ * (the summed shard grids): preprocess, then peak / refine / angle / rescue as usual. */
+rv_status rv_estimate_single_prevoted(rv_context* ctx, const double* d_corrs, int64_t n, const rv_config* cfg,
+                                      const uint32_t* d_grid, rv_estimate* out);
+
 /* Inliers (ascending input indices) of model `model` of the last estimate call. */
 rv_status rv_result_inliers(rv_context* ctx, int32_t model, int32_t* dst, int64_t capacity);
 

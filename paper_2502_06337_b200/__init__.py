@@ -170,6 +170,25 @@ class Context:
                                                        C.byref(nm)))
         return [self._estimate(out[k], k) for k in range(nm.value)]
 
+    # ---- sharded solve (device pointers; collectives are the caller's) ----------------------
+    def vote_shard(self, dptr: int, n: int, grid_dptr: int, cfg: EstimatorConfig | None = None) -> int:
+        """Preprocess + vote one shard into the device grid at grid_dptr; returns kept count."""
+        cfg = cfg or EstimatorConfig()
+        c = cfg.to_c()
+        nk = C.c_int64()
+        self._check(self._lib.rv_vote_shard(self.handle, C.c_void_p(dptr), n, C.byref(c), C.c_void_p(grid_dptr),
+                                            C.byref(nk)))
+        return nk.value
+
+    def estimate_single_prevoted(self, dptr: int, n: int, grid_dptr: int,
+                                 cfg: EstimatorConfig | None = None) -> RotationEstimate:
+        cfg = cfg or EstimatorConfig()
+        c = cfg.to_c()
+        e = rv_estimate()
+        self._check(self._lib.rv_estimate_single_prevoted(self.handle, C.c_void_p(dptr), n, C.byref(c),
+                                                          C.c_void_p(grid_dptr), C.byref(e)))
+        return self._estimate(e, 0)
+
     # ---- path functions -----------------------------------------------------------------
     def preprocess(self, corrs, tau_z: float = 1e-9, normalize: bool = True):
         """preprocess, estimator.hpp:47-48 -> (constraints (k,3), kept (k,), dropped (d,))."""

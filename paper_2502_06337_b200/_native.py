@@ -92,6 +92,10 @@ _SIGS = [
     ("rv_estimate_multi_device", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(rv_config), C.POINTER(rv_estimate), C.c_int32, c_int32_p]),
     ("rv_result_inliers", C.c_int, [C.c_void_p, C.c_int32, c_int32_p, C.c_int64]),
+    ("rv_vote_shard", C.c_int,
+     [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(rv_config), C.c_void_p, c_int64_p]),
+    ("rv_estimate_single_prevoted", C.c_int,
+     [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(rv_config), C.c_void_p, C.POINTER(rv_estimate)]),
     ("rv_preprocess", C.c_int,
      [C.c_void_p, c_double_p, C.c_int64, C.c_double, C.c_int32, c_double_p, c_int32_p, c_int32_p, c_int64_p, c_int64_p]),
     ("rv_accumulate", C.c_int, [C.c_void_p, c_double_p, C.c_int64, C.c_int32, C.c_double, C.c_int32, c_uint32_p]),

@@ -1347,6 +1347,59 @@ rv_status rv_estimate_multi_device(rv_context* c, const double* d_corrs, int64_t
   return multi_impl(c, d_corrs, n, cfg, out, capacity, n_models, false);
 }
 
+rv_status rv_vote_shard(rv_context* c, const double* d_corrs, int64_t n, const rv_config* cfg, uint32_t* d_grid,
+                        int64_t* n_kept) {
+  if (!c || !cfg || !d_grid || !n_kept || (n > 0 && !d_corrs)) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    const size_t cells = (size_t)cfg->grid * cfg->grid;
+    *n_kept = 0;
+    if (n <= 0) {
+      ck(cudaMemsetAsync(d_grid, 0, sizeof(uint32_t) * cells, c->st), "memset");
+      sync(c);
+      return;
+    }
+    const PreResult pre = preprocess_dev(c, d_corrs, n, cfg->tau_z, cfg->normalize_inputs);
+    *n_kept = pre.cs.n;
+    if (pre.cs.n == 0) {  // an all-degenerate shard votes nothing
+      ck(cudaMemsetAsync(d_grid, 0, sizeof(uint32_t) * cells, c->st), "memset");
+      sync(c);
+      return;
+    }
+    const auto gp = vote_and_peak(c, pre.cs.zx, pre.cs.zy, pre.cs.zz, pre.cs.n, *cfg, 1, true);
+    ck(cudaMemcpyAsync(d_grid, gp.first, sizeof(uint32_t) * cells, cudaMemcpyDeviceToDevice, c->st), "D2D grid");
+    sync(c);
+  });
+}
+
+rv_status rv_estimate_single_prevoted(rv_context* c, const double* d_corrs, int64_t n, const rv_config* cfg,
+                                      const uint32_t* d_grid, rv_estimate* out) {
+  if (!c || !cfg || !out || !d_grid || (n > 0 && !d_corrs)) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    c->results.clear();
+    if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
+    const PreResult pre = preprocess_dev(c, d_corrs, n, cfg->tau_z, cfg->normalize_inputs);
+    Estimate e;
+    if (pre.cs.n == 0) {
+      std::vector<int32_t> all(n);
+      for (int64_t i = 0; i < n; ++i) all[i] = (int32_t)i;
+      e = identity_estimate(std::move(all));
+    } else if (pre.n_dropped * 10 >= n * 9) {
+      e = identity_estimate(dropped_list(c, pre.n_dropped));
+    } else {
+      // the supplied grid is copied into the context grid (the guard may re-vote into it)
+      uint32_t* g = c->grid.get<uint32_t>((size_t)cfg->grid * cfg->grid);
+      ck(cudaMemcpyAsync(g, d_grid, sizeof(uint32_t) * (size_t)cfg->grid * cfg->grid, cudaMemcpyDeviceToDevice,
+                         c->st),
+         "D2D grid");
+      e = finish_single(c, pre, d_corrs, *cfg, g);
+    }
+    to_c(e, out, seconds_since(c));
+    c->results.push_back(std::move(e.inliers));
+  });
+}
+
 rv_status rv_result_inliers(rv_context* c, int32_t model, int32_t* dst, int64_t capacity) {
   if (!c || model < 0 || model >= (int32_t)c->results.size()) return RV_ERR_INVALID_ARGUMENT;
   const auto& v = c->results[model];

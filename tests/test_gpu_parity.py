@@ -239,6 +239,29 @@ def test_pipelined_host_path_matches_device_path(ctx):
     assert st["vote_guard_reruns"] == 0
 
 
+@pytest.mark.parametrize("world", [2, 8])
+def test_sharded_vote_protocol_single_gpu(ctx, world):
+    # the multi-GPU protocol emulated sequentially on one GPU (no cross-kernel waits): per-shard
+    # votes summed (what the NCCL all-reduce does) + finish on the gathered input must equal the
+    # single solve bit-for-bit
+    import torch
+    from paper_2502_06337_b200 import distributed as rvd
+    corrs, _, _ = synth.make_config("c3", 300_000)
+    d = torch.from_numpy(corrs).cuda()
+    total = torch.zeros((512, 512), dtype=torch.int32, device="cuda")
+    for r in range(world):
+        lo, hi = rvd.shard_bounds(corrs.shape[0], world, r)
+        g = torch.empty((512, 512), dtype=torch.int32, device="cuda")
+        ctx.vote_shard(d[lo:hi].data_ptr(), hi - lo, g.data_ptr())
+        total += g
+    e = ctx.estimate_single_prevoted(d.data_ptr(), corrs.shape[0], total.data_ptr())
+    z, _, _ = ctx.preprocess(corrs)
+    ref_grid = ctx.accumulate(z)
+    assert np.array_equal(total.cpu().numpy().view(np.uint32), ref_grid)
+    e1 = ctx.estimate_single_device(d.data_ptr(), corrs.shape[0])
+    assert np.array_equal(e.inliers, e1.inliers) and np.array_equal(e.rotation, e1.rotation)
+
+
 def test_full_size_multi_recovers_three(ctx):
     corrs, rots, _ = synth.make_config("c5")
     ms = ctx.estimate_multi(corrs, rv.EstimatorConfig(max_models=3))
