@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "rv_exact.cuh"
 #include "rv_internal.h"
@@ -207,17 +208,17 @@ __device__ __forceinline__ uint2 plan_from_sets(const Arc2& ulo, const Arc2& uhi
     *work += (unsigned long long)M;
     return full;
   }
-  // 64-pair alignment (K2 walks 64 pairs per warp iteration) and a final overlap merge
-  l0 = (l0 + 63) & ~63;
+  // 32-pair alignment (K2 walks 32 consecutive pairs per lane-step) and a final overlap merge
+  l0 = (l0 + 31) & ~31;
   if (nl == 2) {
-    l1 = (l1 + 63) & ~63;
+    l1 = (l1 + 31) & ~31;
     const int d01 = ((s1 - s0) % M + M) % M, d10 = ((s0 - s1) % M + M) % M;
     if (d01 < l0) {
-      l0 = (max(l0, d01 + l1) + 63) & ~63;
+      l0 = (max(l0, d01 + l1) + 31) & ~31;
       nl = 1;
     } else if (d10 < l1) {
       s0 = s1;
-      l0 = (max(l1, d10 + l0) + 63) & ~63;
+      l0 = (max(l1, d10 + l0) + 31) & ~31;
       nl = 1;
     }
   }
@@ -247,8 +248,11 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
       f1[k] = __double2float_rn(a1[k]);
       f2[k] = __double2float_rn(a2[k]);
     }
-    b.basis_a[i] = make_float4(f1[0], f1[1], f1[2], f2[0]);
-    b.basis_b[i] = make_float2(f2[1], f2[2]);
+    // the vote reads fl32(K * a_xy) (one rounding, like fl32(a_xy)): saves a multiply per pair
+    const double K = p.inv_cell;
+    b.basis_a[i] = make_float4(__double2float_rn(a1[0] * K), __double2float_rn(a1[1] * K), f1[2],
+                               __double2float_rn(a2[0] * K));
+    b.basis_b[i] = make_float2(__double2float_rn(a2[1] * K), f2[2]);
   }
   // near-polar constraint: c ~ 0 everywhere, every band sees all pairs
   const bool polar = !(sqrtf(fmaf(f1[2], f1[2], f2[2] * f2[2])) >= kRcMin);
@@ -392,7 +396,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
   const unsigned lt_mask = (1u << lane) - 1u;
   const uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(tile);
   const uint32_t dummy_s = (uint32_t)__cvta_generic_to_shared(dummy + lane);
-  const float Kf = p.Kf, CMf = p.CMf;
+  const float CMf = p.CMf;
   const int W = p.W, G = p.G;
   const int S = p.frac_shift;
   const uint32_t fmask = p.frac_mask;
@@ -421,46 +425,52 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     const uint32_t tile_cells = (uint32_t)hb * (uint32_t)W;
     const uint2* rbase = reinterpret_cast<const uint2*>(b.ranges) + (int64_t)band * b.layout_n;
     int* counter = &b.counters[1 + band];
+    const float4* basis_a = b.basis_a;
+    const float2* basis_b = b.basis_b;
+    const int ci_lo = (int)c_lo, ci_hi = (int)c_hi;  // constraint counts fit in 31 bits
     for (;;) {  // per-warp dynamic grabs of kWarpGrab constraints
-      int64_t g0 = 0;
+      int g0 = 0;
       if (lane == 0) g0 = atomicAdd(counter, kWarpGrab);
-      g0 = __shfl_sync(0xFFFFFFFFu, g0, 0) + c_lo;
-      if (g0 >= c_hi) break;
-      const int64_t g1 = (g0 + kWarpGrab < c_hi) ? g0 + kWarpGrab : c_hi;
+      g0 = __shfl_sync(0xFFFFFFFFu, g0, 0) + ci_lo;
+      if (g0 >= ci_hi) break;
+      const int g1 = min(g0 + kWarpGrab, ci_hi);
       int qn = 0;
       uint2 rr = rbase[g0];
-      float4 ba = b.basis_a[g0];
-      float2 bb = b.basis_b[g0];
-      for (int64_t ci = g0; ci < g1; ++ci) {
+      float4 ba = basis_a[g0];
+      float2 bb = basis_b[g0];
+      for (int ci = g0; ci < g1; ++ci) {
         uint2 rr_n = rr;
         float4 ba_n = ba;
         float2 bb_n = bb;
         if (ci + 1 < g1) {  // prefetch the next constraint
           rr_n = rbase[ci + 1];
-          ba_n = b.basis_a[ci + 1];
-          bb_n = b.basis_b[ci + 1];
+          ba_n = basis_a[ci + 1];
+          bb_n = basis_b[ci + 1];
         }
         const uint32_t local_ci = (uint32_t)(ci - g0) << 16;
 #pragma unroll 1
         for (int rk = 0; rk < 2; ++rk) {
           const uint32_t enc = rk == 0 ? rr.x : rr.y;
+          if (enc < 0x10000u) continue;  // empty range (len == 0)
           const int start = (int)(enc & 0xFFFFu), len = (int)(enc >> 16);
           const float2* tp = tab + start + lane;
-#pragma unroll 1
-          for (int k0 = 0; k0 < len; k0 += 64) {
-            bool flag[2];
-            uint32_t addr[2];
+          // NP pairs per lane per step (32*NP consecutive pairs per warp); ranges are 32-aligned:
+          // 64-pair steps while they fit, then one 32-pair tail step
+          auto step = [&](int k0, auto np_tag) {
+            constexpr int NP = decltype(np_tag)::value;
+            bool flag[NP];
+            uint32_t addr[NP];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < NP; ++h) {
               const float2 t = tp[k0 + 32 * h];
-              const float x = fmaf(ba.w, t.y, ba.x * t.x);
-              const float y = fmaf(bb.x, t.y, ba.y * t.x);
+              // x, y carry the cell scale K = G/(2E) (folded into the f32 basis by the planner)
+              const float xk = fmaf(ba.w, t.y, ba.x * t.x);
+              const float yk = fmaf(bb.x, t.y, ba.y * t.x);
               const float c = fmaf(bb.y, t.y, ba.z * t.x);
               const float r = rcp_approx(1.f + fabsf(c));
               const float rs = __int_as_float(__float_as_int(r) | (~__float_as_int(c) & 0x80000000));
-              const float rkf = rs * Kf;
-              const uint32_t bx = (uint32_t)__float_as_int(fmaf(x, rkf, CMf));
-              const uint32_t by = (uint32_t)__float_as_int(fmaf(y, rkf, CMf));
+              const uint32_t bx = (uint32_t)__float_as_int(fmaf(xk, rs, CMf));
+              const uint32_t by = (uint32_t)__float_as_int(fmaf(yk, rs, CMf));
               flag[h] = (fabsf(c) < kDc) | ((bx & fmask) == 0u) | ((by & fmask) == 0u);
               // cell index relative to the tile; the column is always inside [c_min, c_min+W) for
               // an unflagged pair (|X| <= 1 < extent, or clamped), so one unsigned range test on
@@ -476,11 +486,14 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
               const bool dep = !flag[h] && rel < tile_cells;
               addr[h] = dep ? tile_s + 4u * rel : dummy_s;
             }
-            red_shared(addr[0], 2u);
-            red_shared(addr[1], 2u);
-            if (__any_sync(0xFFFFFFFFu, flag[0] | flag[1])) {  // cold: queue for the exact f64 path
 #pragma unroll
-              for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < NP; ++h) red_shared(addr[h], 2u);
+            bool any = false;
+#pragma unroll
+            for (int h = 0; h < NP; ++h) any |= flag[h];
+            if (__any_sync(0xFFFFFFFFu, any)) {  // cold: queue for the exact f64 path
+#pragma unroll
+              for (int h = 0; h < NP; ++h) {
                 const unsigned fm = __ballot_sync(0xFFFFFFFFu, flag[h]);
                 if (flag[h]) {
                   int pair = start + k0 + 32 * h + lane;
@@ -498,7 +511,11 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
                 }
               }
             }
-          }
+          };
+          int k0 = 0;
+#pragma unroll 1
+          for (; k0 + 64 <= len; k0 += 64) step(k0, std::integral_constant<int, 2>{});
+          if (k0 < len) step(k0, std::integral_constant<int, 1>{});
         }
         rr = rr_n;
         ba = ba_n;
