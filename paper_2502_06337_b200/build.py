@@ -15,7 +15,9 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "librotavote_b200.so"
 INCLUDE = PKG.parent / "include"
-SOURCES = ["rv_prep.cu", "rv_vote.cu", "rv_peaks.cu", "rv_refine.cu", "rv_api.cpp"]
+SOURCES = ["rv_prep.cu", "rv_vote.cu", "rv_peaks.cu", "rv_refine.cu", "rv_coop.cu", "rv_api.cpp"]
+# translation units whose device arithmetic must follow the host op order exactly
+NO_FMAD = {"rv_coop.cu"}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -46,7 +48,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs = []
     for src in SOURCES:
         obj = obj_dir / (Path(src).stem + ".o")
-        cmd = [nvcc(), *ARCH, *common, *(["-Xptxas", "-v"] if verbose else []), "-x",
+        cmd = [nvcc(), *ARCH, *common, *(["-fmad=false"] if src in NO_FMAD else []),
+               *(["-Xptxas", "-v"] if verbose else []), "-x",
                "cu" if src.endswith(".cu") else "c++", "-c", str(CSRC / src), "-o", str(obj)]
         if src.endswith(".cpp"):
             cmd = [nvcc(), *ARCH, *[a for a in common if a != "--expt-relaxed-constexpr"], "-x", "c++", "-c",

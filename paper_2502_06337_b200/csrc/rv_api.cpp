@@ -119,6 +119,8 @@ struct rv_context {
   DBuf arg_keys, arg_out, sat, blur_best, blur_out, done;
   // classify / refine
   DBuf flagsA, flagsB, bcount, bscatter, bdiff, boffA, boffB, cls_result, compact_out;
+  DBuf coop_part, coop_state;  // device-resident refine_loop / anneal_axis (rv_coop.cu)
+  int coop_grid = 0;
   // angles / support
   DBuf bins, raw, angle_counts, angle_sums, angle_result, sup_counts, sup_result, band_flagsA, band_flagsB,
       band_idx, band_vals, near_h, near_result;
@@ -549,26 +551,43 @@ Cls classify_dev(rv_context* c, const ConstraintSet& cs, const double axis[3], d
   return r;
 }
 
-// refine_loop (estimator.cpp:51-69). Returns the final classification (in flags slot A or B).
+// refine_loop (estimator.cpp:51-69) / anneal_axis (estimator.cpp:145-160) as one cooperative
+// launch (rv_coop.cu): every classify pass, scatter reduction and 3x3 eigen-solve stays on the
+// device; the host reads the final state once. mode 0 returns the final classification with its
+// tile offsets ready for compaction; mode 1 returns the annealed axis in `axis`.
+Cls coop_refine_dev(rv_context* c, const ConstraintSet& cs, double axis[3], int mode, double e0, const rv_config& cfg,
+                    int* passes = nullptr) {
+  StageScope sc(c, kRefine);
+  if (c->coop_grid == 0) c->coop_grid = coop_refine_grid(c->sms);
+  const int nt = std::max(1, coop_tiles(cs.n));
+  const size_t words = (size_t)(cs.n + 31) / 32 + 32;
+  Cls r;
+  uint32_t* fa = c->flagsA.get<uint32_t>(words);
+  uint32_t* fb = c->flagsB.get<uint32_t>(words);
+  int32_t* tcount = c->bcount.get<int32_t>(nt);
+  int32_t* toff = c->boffA.get<int32_t>(nt);
+  double* part = c->coop_part.get<double>((size_t)c->coop_grid * 8);
+  CoopState* dst = c->coop_state.get<CoopState>(1);
+  ck(launch_coop_refine(cs.zx, cs.zy, cs.zz, cs.n, mode, cfg.refine ? 1 : 0, cfg.epsilon, e0, axis, fa, fb, tcount,
+                        toff, part, dst, c->coop_grid, c->st),
+     "coop refine launch");
+  count_launch(c);
+  static_assert(sizeof(CoopState) <= 4096, "pinned scratch");
+  CoopState* h = reinterpret_cast<CoopState*>(c->pinned);
+  ck(cudaMemcpyAsync(h, dst, sizeof(CoopState), cudaMemcpyDeviceToHost, c->st), "coop state D2H");
+  sync(c);
+  std::memcpy(axis, h->axis, sizeof(double) * 3);
+  r.flags = h->slot == 0 ? fa : fb;
+  r.offsets = toff;
+  r.count = h->count;
+  r.differs = false;
+  std::memcpy(r.scatter, h->scatter, sizeof r.scatter);
+  if (passes) *passes = h->refits;
+  return r;
+}
+
 Cls refine_loop_dev(rv_context* c, const ConstraintSet& cs, double axis[3], const rv_config& cfg, int* passes = nullptr) {
-  int slot = 0;
-  Cls inl = classify_dev(c, cs, axis, cfg.epsilon, slot, nullptr);
-  if (passes) *passes = 0;
-  if (!cfg.refine) return inl;
-  for (int pass = 0; pass < 10 && inl.count >= 2; ++pass) {
-    double next[3];
-    if (!axis_from_scatter(inl.scatter, next)) break;  // RankDeficient: keep the current axis
-    if (passes) ++*passes;
-    slot ^= 1;
-    Cls nx = classify_dev(c, cs, next, cfg.epsilon, slot, inl.flags);
-    axis[0] = next[0];
-    axis[1] = next[1];
-    axis[2] = next[2];
-    const bool stable = !nx.differs;
-    inl = nx;
-    if (stable) break;
-  }
-  return inl;
+  return coop_refine_dev(c, cs, axis, 0, 0.0, cfg, passes);
 }
 
 // Compact a classification into input indices (through the kept map).
@@ -657,16 +676,7 @@ Support model_support_dev(rv_context* c, const ConstraintSet& cs, const double* 
 
 // anneal_axis (estimator.cpp:145-160)
 void anneal_axis_dev(rv_context* c, const ConstraintSet& cs, double axis[3], double eps0, const rv_config& cfg) {
-  double e = std::max(eps0, cfg.epsilon);
-  while (true) {
-    const Cls cl = classify_dev(c, cs, axis, e, 0, nullptr);
-    if (cl.count >= 2) {
-      double next[3];
-      if (axis_from_scatter(cl.scatter, next)) std::memcpy(axis, next, sizeof next);
-    }
-    if (e <= cfg.epsilon) break;
-    e = std::max(cfg.epsilon, 0.5 * e);
-  }
+  coop_refine_dev(c, cs, axis, 1, eps0, cfg);
 }
 
 // rescue_axes (estimator.cpp:162-179)

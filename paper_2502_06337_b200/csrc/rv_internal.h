@@ -148,4 +148,25 @@ void launch_gather_residual(const double* zx, const double* zy, const double* zz
                             int32_t* block_counter, double* ozx, double* ozy, double* ozz, int32_t* okept,
                             int32_t* total, cudaStream_t s);
 
+// Device-resident refine_loop / anneal_axis (rv_coop.cu): one cooperative launch per call.
+struct CoopState {  // published by the kernel after each pass; read by the host at the end
+  double axis[3];   // axis of the last classify (refine_loop) / current axis (anneal)
+  double next[3];
+  double e;
+  double scatter[6];
+  long long count;  // inliers of the last classify
+  int slot;         // flags slot (0/1) holding the final inlier bitmask
+  int done;
+  int refits;
+  int rank_deficient;
+};
+int coop_refine_grid(int sms);
+int coop_tiles(int64_t n);
+size_t coop_state_bytes();
+// mode 0: refine_loop (estimator.cpp:51-69); mode 1: anneal_axis (estimator.cpp:145-160).
+cudaError_t launch_coop_refine(const double* zx, const double* zy, const double* zz, int64_t n, int mode, int refine,
+                               double eps, double e0, const double axis0[3], uint32_t* flags0, uint32_t* flags1,
+                               int32_t* tile_count, int32_t* tile_offset, double* block_part, void* state, int grid,
+                               cudaStream_t s);
+
 }  // namespace rvb

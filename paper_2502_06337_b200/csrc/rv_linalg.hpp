@@ -6,23 +6,68 @@
 //    shift, ascending selection sort.
 //  * svd3: two-sided Jacobi SVD for the Kabsch fallback (estimator.cpp:198-215).
 //  * geometry of geom.cpp:10-43 with the reference's evaluation order.
-// This translation unit must be compiled without FMA contraction (-ffp-contract=off).
+// Compiled without FMA contraction (host: -ffp-contract=off; device: nvcc -fmad=false), the
+// host and device instantiations are bit-identical to each other and to the reference.
 #pragma once
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstring>
 
+#if defined(__CUDACC__)
+#define RV_HD __host__ __device__ __forceinline__
+#else
+#define RV_HD inline
+#endif
+
 namespace rvb {
+
+// std::hypot of glibc 2.39 (sysdeps/ieee754/dbl-64/e_hypot.c, non-FMA kernel + scaling), which
+// Eigen's SelfAdjointEigenSolver calls through numext::hypot; restated so device code matches the
+// host bit-for-bit (glibc's hypot is not correctly rounded; verified equal on 3e7 random pairs).
+RV_HD double hypot_kernel(double ax, double ay) {
+  double t1, t2;
+  double h = sqrt(ax * ax + ay * ay);
+  if (h <= 2.0 * ay) {
+    const double delta = h - ay;
+    t1 = ax * (2.0 * delta - ax);
+    t2 = (delta - 2.0 * (ax - ay)) * delta;
+  } else {
+    const double delta = h - ax;
+    t1 = 2.0 * delta * (ax - 2.0 * ay);
+    t2 = (4.0 * delta - ay) * ay + delta * delta;
+  }
+  h -= (t1 + t2) / (2.0 * h);
+  return h;
+}
+RV_HD double hypot_glibc(double x, double y) {
+  using std::isfinite;
+  using std::isinf;
+  if (!isfinite(x) || !isfinite(y)) return (isinf(x) || isinf(y)) ? INFINITY : x + y;
+  x = fabs(x);
+  y = fabs(y);
+  const double ax = x < y ? y : x, ay = x < y ? x : y;
+  const double SCALE = 0x1p-600, LARGE_VAL = 0x1p+511, TINY_VAL = 0x1p-511, EPS = 0x1p-54;
+  if (ax > LARGE_VAL) {
+    if (ay <= ax * EPS) return ax + ay;
+    return hypot_kernel(ax * SCALE, ay * SCALE) / SCALE;
+  }
+  if (ay < TINY_VAL) {
+    if (ax >= ay / EPS) return ax + ay;
+    return hypot_kernel(ax / SCALE, ay / SCALE) * SCALE;
+  }
+  if (ay <= ax * EPS) return ax + ay;
+  return hypot_kernel(ax, ay);
+}
 
 constexpr double kPiD = 3.14159265358979323846;
 
-inline double dot3(const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
-inline double norm3(const double* a) { return std::sqrt(dot3(a, a)); }
-inline void normalized3(const double* a, double* o) {
+RV_HD double dot3(const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+RV_HD double norm3(const double* a) { return sqrt(dot3(a, a)); }
+RV_HD void normalized3(const double* a, double* o) {
   const double n2 = dot3(a, a);
   if (n2 > 0.0) {
-    const double s = std::sqrt(n2);
+    const double s = sqrt(n2);
     o[0] = a[0] / s;
     o[1] = a[1] / s;
     o[2] = a[2] / s;
@@ -32,7 +77,7 @@ inline void normalized3(const double* a, double* o) {
     o[2] = a[2];
   }
 }
-inline void cross3(const double* a, const double* b, double* o) {
+RV_HD void cross3(const double* a, const double* b, double* o) {
   const double t0 = a[1] * b[2] - a[2] * b[1];
   const double t1 = a[2] * b[0] - a[0] * b[2];
   const double t2 = a[0] * b[1] - a[1] * b[0];
@@ -40,7 +85,7 @@ inline void cross3(const double* a, const double* b, double* o) {
   o[1] = t1;
   o[2] = t2;
 }
-inline void canonicalize3(const double* p, double* o) {  // geom.cpp:34
+RV_HD void canonicalize3(const double* p, double* o) {  // geom.cpp:34
   if (p[2] > 0.0) {
     o[0] = -p[0];
     o[1] = -p[1];
@@ -93,7 +138,7 @@ inline double rotation_error3(const double* g, const double* o) {  // geom.cpp:1
 }
 inline void orthonormal_basis3(const double* z, double* a1, double* a2) {  // geom.cpp:36-43
   int least = 0;
-  const double az[3] = {std::fabs(z[0]), std::fabs(z[1]), std::fabs(z[2])};
+  const double az[3] = {fabs(z[0]), fabs(z[1]), fabs(z[2])};
   for (int i = 1; i < 3; ++i)
     if (az[i] < az[least]) least = i;
   double seed[3] = {0, 0, 0};
@@ -105,22 +150,22 @@ inline void orthonormal_basis3(const double* z, double* a1, double* a2) {  // ge
   cross3(z, a1, a2);
 }
 
-inline void givens(double p, double q, double* c, double* s) {
+RV_HD void givens(double p, double q, double* c, double* s) {
   if (q == 0.0) {
     *c = p < 0.0 ? -1.0 : 1.0;
     *s = 0.0;
   } else if (p == 0.0) {
     *c = 0.0;
     *s = q < 0.0 ? 1.0 : -1.0;
-  } else if (std::fabs(p) > std::fabs(q)) {
+  } else if (fabs(p) > fabs(q)) {
     const double t = q / p;
-    double u = std::sqrt(1.0 + t * t);
+    double u = sqrt(1.0 + t * t);
     if (p < 0.0) u = -u;
     *c = 1.0 / u;
     *s = -t * *c;
   } else {
     const double t = p / q;
-    double u = std::sqrt(1.0 + t * t);
+    double u = sqrt(1.0 + t * t);
     if (q < 0.0) u = -u;
     *s = -1.0 / u;
     *c = -t * *s;
@@ -129,13 +174,13 @@ inline void givens(double p, double q, double* c, double* s) {
 
 // Symmetric 3x3 eigen-decomposition; sm row-major (lower triangle read). evecs row-major,
 // eigenvector k = column k; eigenvalues ascending.
-inline void eigen_sym3(const double sm[9], double evals[3], double ev[9]) {
+RV_HD void eigen_sym3(const double sm[9], double evals[3], double ev[9]) {
   double m[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
   for (int j = 0; j < 3; ++j)
     for (int i = j; i < 3; ++i) m[i][j] = sm[i * 3 + j];
   double scale = 0.0;
   for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) scale = std::fabs(m[i][j]) > scale ? std::fabs(m[i][j]) : scale;
+    for (int j = 0; j < 3; ++j) scale = fabs(m[i][j]) > scale ? fabs(m[i][j]) : scale;
   if (scale == 0.0) scale = 1.0;
   for (int j = 0; j < 3; ++j)
     for (int i = j; i < 3; ++i) m[i][j] /= scale;
@@ -150,7 +195,7 @@ inline void eigen_sym3(const double sm[9], double evals[3], double ev[9]) {
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j) q[i][j] = (i == j) ? 1.0 : 0.0;
   } else {
-    const double beta = std::sqrt(m[1][0] * m[1][0] + v1norm2);
+    const double beta = sqrt(m[1][0] * m[1][0] + v1norm2);
     const double inv_beta = 1.0 / beta;
     const double m01 = m[1][0] * inv_beta;
     const double m02 = m[2][0] * inv_beta;
@@ -159,18 +204,25 @@ inline void eigen_sym3(const double sm[9], double evals[3], double ev[9]) {
     diag[2] = m[2][2] - m02 * qq;
     sub[0] = beta;
     sub[1] = m[2][1] - m01 * qq;
-    const double qi[3][3] = {{1, 0, 0}, {0, m01, m02}, {0, m02, -m01}};
-    std::memcpy(q, qi, sizeof q);
+    q[0][0] = 1;
+    q[0][1] = 0;
+    q[0][2] = 0;
+    q[1][0] = 0;
+    q[1][1] = m01;
+    q[1][2] = m02;
+    q[2][0] = 0;
+    q[2][1] = m02;
+    q[2][2] = -m01;
   }
   int end = 2, start = 0, iter = 0;
   const double precision_inv = 1.0 / DBL_EPSILON;
   while (end > 0) {
     for (int i = start; i < end; ++i) {
-      if (std::fabs(sub[i]) < DBL_MIN) {
+      if (fabs(sub[i]) < DBL_MIN) {
         sub[i] = 0.0;
       } else {
         const double scaled = precision_inv * sub[i];
-        if (scaled * scaled <= (std::fabs(diag[i]) + std::fabs(diag[i + 1]))) sub[i] = 0.0;
+        if (scaled * scaled <= (fabs(diag[i]) + fabs(diag[i + 1]))) sub[i] = 0.0;
       }
     }
     while (end > 0 && sub[end - 1] == 0.0) end--;
@@ -182,10 +234,10 @@ inline void eigen_sym3(const double sm[9], double evals[3], double ev[9]) {
     const double e = sub[end - 1];
     double mu = diag[end];
     if (td == 0.0) {
-      mu -= std::fabs(e);
+      mu -= fabs(e);
     } else if (e != 0.0) {
       const double e2 = e * e;
-      const double h = std::hypot(td, e);
+      const double h = hypot_glibc(td, e);
       if (e2 == 0.0)
         mu -= e / ((td + (td > 0.0 ? h : -h)) / e);
       else
@@ -219,8 +271,14 @@ inline void eigen_sym3(const double sm[9], double evals[3], double ev[9]) {
     for (int j = i + 1; j < 3; ++j)
       if (diag[j] < diag[k]) k = j;
     if (k != i) {
-      std::swap(diag[i], diag[k]);
-      for (int r = 0; r < 3; ++r) std::swap(q[r][i], q[r][k]);
+      const double t = diag[i];
+      diag[i] = diag[k];
+      diag[k] = t;
+      for (int r = 0; r < 3; ++r) {
+        const double u = q[r][i];
+        q[r][i] = q[r][k];
+        q[r][k] = u;
+      }
     }
   }
   for (int i = 0; i < 3; ++i) evals[i] = diag[i] * scale;
@@ -229,11 +287,11 @@ inline void eigen_sym3(const double sm[9], double evals[3], double ev[9]) {
 }
 
 // refine_axis from scatter sums (xx xy xz yy yz zz), estimator.cpp:303-308. false = RankDeficient.
-inline bool axis_from_scatter(const double s6[6], double axis[3]) {
+RV_HD bool axis_from_scatter(const double s6[6], double axis[3]) {
   const double sm[9] = {s6[0], s6[1], s6[2], s6[1], s6[3], s6[4], s6[2], s6[4], s6[5]};
   double evals[3], ev[9];
   eigen_sym3(sm, evals, ev);
-  if (evals[1] <= 1e-10 * std::max(evals[2], 1e-300)) return false;
+  if (evals[1] <= 1e-10 * (evals[2] > 1e-300 ? evals[2] : 1e-300)) return false;
   const double v0[3] = {ev[0], ev[3], ev[6]};
   double nv[3];
   normalized3(v0, nv);
@@ -251,35 +309,35 @@ inline void svd3(const double a[9], double u[9], double v[9]) {
     }
   const double prec = 2.0 * DBL_EPSILON;
   double max_diag = 0;
-  for (int i = 0; i < 3; ++i) max_diag = std::max(max_diag, std::fabs(w[i][i]));
+  for (int i = 0; i < 3; ++i) max_diag = std::max(max_diag, fabs(w[i][i]));
   bool finished = false;
   for (int sweeps = 0; !finished && sweeps < 100; ++sweeps) {
     finished = true;
     for (int p = 1; p < 3; ++p)
       for (int qi = 0; qi < p; ++qi) {
         const double thr = std::max(4.9e-324, prec * max_diag);
-        if (std::fabs(w[p][qi]) > thr || std::fabs(w[qi][p]) > thr) {
+        if (fabs(w[p][qi]) > thr || fabs(w[qi][p]) > thr) {
           finished = false;
           const double m00 = w[qi][qi], m01 = w[qi][p], m10 = w[p][qi], m11 = w[p][p];
           double c1 = 1, s1 = 0;
           const double t = m00 + m11, d = m10 - m01;
-          if (std::fabs(d) >= DBL_MIN) {
+          if (fabs(d) >= DBL_MIN) {
             const double uu = t / d;
-            const double tmp = std::sqrt(1.0 + uu * uu);
+            const double tmp = sqrt(1.0 + uu * uu);
             s1 = 1.0 / tmp;
             c1 = uu / tmp;
           }
           const double n00 = c1 * m00 + s1 * m10, n01 = c1 * m01 + s1 * m11;
           const double n11 = -s1 * m01 + c1 * m11;
           double jc = 1, js = 0;
-          const double deno = 2.0 * std::fabs(n01);
+          const double deno = 2.0 * fabs(n01);
           if (deno >= DBL_MIN) {
             const double tau = (n00 - n11) / deno;
-            const double ww = std::sqrt(tau * tau + 1.0);
+            const double ww = sqrt(tau * tau + 1.0);
             const double tt = tau > 0.0 ? 1.0 / (tau + ww) : 1.0 / (tau - ww);
             const double sign_t = tt > 0.0 ? 1.0 : -1.0;
-            const double nn = 1.0 / std::sqrt(tt * tt + 1.0);
-            js = -sign_t * (n01 / std::fabs(n01)) * std::fabs(tt) * nn;
+            const double nn = 1.0 / sqrt(tt * tt + 1.0);
+            js = -sign_t * (n01 / fabs(n01)) * fabs(tt) * nn;
             jc = nn;
           }
           const double lc = c1 * jc - s1 * (-js), ls = c1 * (-js) + s1 * jc;
@@ -302,13 +360,13 @@ inline void svd3(const double a[9], double u[9], double v[9]) {
             V[k][qi] = jc * x - js * y;
             V[k][p] = js * x + jc * y;
           }
-          max_diag = std::max(max_diag, std::max(std::fabs(w[p][p]), std::fabs(w[qi][qi])));
+          max_diag = std::max(max_diag, std::max(fabs(w[p][p]), fabs(w[qi][qi])));
         }
       }
   }
   double sv[3];
   for (int i = 0; i < 3; ++i) {
-    sv[i] = std::fabs(w[i][i]);
+    sv[i] = fabs(w[i][i]);
     if (w[i][i] < 0.0)
       for (int k = 0; k < 3; ++k) U[k][i] = -U[k][i];
   }
@@ -364,7 +422,7 @@ inline void angle_axis_canonical(const double r[9], double axis[3], double* angl
   double qw, qv[3];
   double t = r[0] + r[4] + r[8];
   if (t > 0.0) {
-    t = std::sqrt(t + 1.0);
+    t = sqrt(t + 1.0);
     qw = 0.5 * t;
     t = 0.5 / t;
     qv[0] = (r[7] - r[5]) * t;
@@ -375,7 +433,7 @@ inline void angle_axis_canonical(const double r[9], double axis[3], double* angl
     if (r[4] > r[0]) i = 1;
     if (r[8] > r[i * 4]) i = 2;
     const int j = (i + 1) % 3, k = (j + 1) % 3;
-    t = std::sqrt(r[i * 4] - r[j * 4] - r[k * 4] + 1.0);
+    t = sqrt(r[i * 4] - r[j * 4] - r[k * 4] + 1.0);
     qv[i] = 0.5 * t;
     t = 0.5 / t;
     qw = (r[k * 3 + j] - r[j * 3 + k]) * t;
@@ -384,7 +442,7 @@ inline void angle_axis_canonical(const double r[9], double axis[3], double* angl
   }
   double n = norm3(qv), aa_angle, aa_axis[3];
   if (n != 0.0) {
-    aa_angle = 2.0 * std::atan2(n, std::fabs(qw));
+    aa_angle = 2.0 * std::atan2(n, fabs(qw));
     if (qw < 0.0) n = -n;
     aa_axis[0] = qv[0] / n;
     aa_axis[1] = qv[1] / n;
