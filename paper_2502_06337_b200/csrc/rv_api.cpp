@@ -225,15 +225,15 @@ VotePlan make_plan(rv_context* c, int G, double E, int J) {
   while (S >= 8 && G + 8 >= (1 << (22 - S))) --S;
   if (!twins_ok || S < 8) return p;
   p.frac_shift = S;
-  p.frac_mask = ((1u << S) - 1u) & ~7u;
+  p.frac_mask = ((1u << S) - 1u) & ~3u;
   const double magic = 1.5 * std::ldexp(1.0, 23 - S);
   const float magic_f = (float)magic;
   uint32_t magic_bits;
   std::memcpy(&magic_bits, &magic_f, 4);
   p.magic_hi = (int)(magic_bits >> S);
   p.Kf = (float)p.inv_cell;
-  // E*inv_cell == G/2 exactly in real arithmetic; +3 units of 2^-S bias the frac window to [-3, 4]
-  p.CMf = (float)(magic + 0.5 * G + 3.0 * std::ldexp(1.0, -S));
+  // E*inv_cell == G/2 exactly in real arithmetic; +2 units of 2^-S bias the frac window to [-2, 1]
+  p.CMf = (float)(magic + 0.5 * G + 2.0 * std::ldexp(1.0, -S));
   p.clamp = E <= 1.0 + 1e-6 ? 1 : 0;
   const double lo_t = (E - 1.0) * p.inv_cell, hi_t = (E + 1.0) * p.inv_cell;
   if (p.clamp) {
@@ -319,7 +319,6 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   b.zy = zy;
   b.zz = zz;
   b.grid = grid;
-  b.layout_n = n;
   b.table64 = c->table64.get<double2>(J);
   b.table32 = c->table32.get<float2>(std::max(J / 2, 1));
   c->times.vote_samples += n * (int64_t)J;
@@ -332,9 +331,11 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   }
   b.basis_a = c->basis_a.get<float4>(n);
   b.basis_b = c->basis_b.get<float2>(n);
-  b.ranges = c->ranges.get<uint32_t>((size_t)n * p.n_bands * 2);
+  b.entry_cap = 2 * n;
+  b.entries = c->ranges.get<unsigned long long>((size_t)b.entry_cap * p.n_bands);
   b.band_work = c->band_work.get<unsigned long long>(kMaxBands);
-  b.counters = c->counters.get<int32_t>(kMaxBands + 1);
+  b.counters = c->counters.get<int32_t>(2 * kMaxBands + 1);
+  b.entry_count = b.counters + kMaxBands + 1;
   b.stats = c->stats.get<unsigned long long>(2);
   // enough CTAs to keep every SM busy, but not more than the work can feed (~1M pairs per CTA)
   const int64_t est_pairs = n * (int64_t)p.halfJ;
@@ -343,7 +344,7 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   b.partials = c->partials.get<uint32_t>((size_t)b.max_slots * p.tile_words);
   b.slot_band = c->slot_band.get<int32_t>(b.max_slots);
   ck(cudaMemsetAsync(b.band_work, 0, sizeof(unsigned long long) * kMaxBands, c->st), "memset band_work");
-  ck(cudaMemsetAsync(b.counters, 0, sizeof(int32_t) * (kMaxBands + 1), c->st), "memset counters");
+  ck(cudaMemsetAsync(b.counters, 0, sizeof(int32_t) * (2 * kMaxBands + 1), c->st), "memset counters");
   ck(cudaMemsetAsync(b.stats, 0, sizeof(unsigned long long) * 2, c->st), "memset stats");
   launch_plan(p, b, n, c->st);
   launch_vote_banded(p, b, n, n_ctas, c->st);
@@ -848,16 +849,17 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
   b.zy = pb.zy;
   b.zz = pb.zz;
   b.grid = grid;
-  b.layout_n = n;
   b.table64 = c->table64.get<double2>(J);
   b.table32 = c->table32.get<float2>(std::max(J / 2, 1));
   int n_ctas = c->sms;
   if (p.banded) {
     b.basis_a = c->basis_a.get<float4>(n);
     b.basis_b = c->basis_b.get<float2>(n);
-    b.ranges = c->ranges.get<uint32_t>((size_t)n * p.n_bands * 2);
+    b.entry_cap = 2 * n;
+    b.entries = c->ranges.get<unsigned long long>((size_t)b.entry_cap * p.n_bands);
     b.band_work = c->band_work.get<unsigned long long>(kMaxBands);
-    b.counters = c->counters.get<int32_t>(kMaxBands + 1);
+    b.counters = c->counters.get<int32_t>(2 * kMaxBands + 1);
+    b.entry_count = b.counters + kMaxBands + 1;
     b.stats = c->stats.get<unsigned long long>(2);
     const int64_t est_pairs = (n / C) * (int64_t)p.halfJ;
     n_ctas = (int)std::clamp<int64_t>(est_pairs >> 20, std::min(p.n_bands, c->sms), c->sms);
@@ -865,7 +867,7 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
     b.partials = c->partials.get<uint32_t>((size_t)b.max_slots * p.tile_words);
     b.slot_band = c->slot_band.get<int32_t>(b.max_slots);
     ck(cudaMemsetAsync(b.band_work, 0, sizeof(unsigned long long) * kMaxBands, c->st), "memset band_work");
-    ck(cudaMemsetAsync(b.counters, 0, sizeof(int32_t) * (kMaxBands + 1), c->st), "memset counters");
+    ck(cudaMemsetAsync(b.counters, 0, sizeof(int32_t) * (2 * kMaxBands + 1), c->st), "memset counters");
     ck(cudaMemsetAsync(b.stats, 0, sizeof(unsigned long long) * 2, c->st), "memset stats");
   }
   ck(cudaMemsetAsync(grid, 0, sizeof(uint32_t) * (size_t)G * G, c->st), "memset grid");
@@ -877,8 +879,11 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
     if (p.banded) {
       b.bounds = chunk_hi + k;
       const int64_t cap = bounds[k + 1] - bounds[k];
+      // entry lists and their counters are per chunk (reused: the stream orders chunk k's vote
+      // before chunk k+1's plan)
+      if (k > 0)
+        ck(cudaMemsetAsync(b.counters + 1, 0, sizeof(int32_t) * 2 * kMaxBands, c->st), "memset band counters");
       launch_plan(p, b, cap, c->st);
-      ck(cudaMemsetAsync(b.counters + 1, 0, sizeof(int32_t) * kMaxBands, c->st), "memset band counters");
       launch_vote_banded(p, b, cap, n_ctas, c->st);
       count_launch(c, 2);
     }

@@ -9,7 +9,7 @@
 namespace rvb {
 
 constexpr int kMaxBands = 64;        // row bands of the smem-tiled vote kernel
-constexpr int kVoteThreads = 512;    // threads per vote CTA (16 warps, 128 regs each)
+constexpr int kVoteThreads = 1024;   // threads per vote CTA (32 warps, <= 64 regs each: latency-bound loop)
 constexpr int kPad = 2;              // pair-index padding of each band range (culling slack)
 constexpr int kFbqCap = 64;          // per-warp exact-fallback queue entries
 constexpr int kReduceThreads = 256;
@@ -23,9 +23,9 @@ struct VotePlan {
   double inv_cell = 0;  // grid / (2*extent)   (voting.cpp:30)
   double cs = 0;        // 2*extent / grid     (voting.hpp:23)
   float Kf = 0;      // (float) inv_cell
-  float CMf = 0;     // G/2 + 1.5*2^(23-S) + 3*2^-S: one FFMA yields t on a 2^-S grid, biased +3 units
+  float CMf = 0;     // G/2 + 1.5*2^(23-S) + 2*2^-S: one FFMA yields t on a 2^-S grid, biased +2 units
   int frac_shift = 0;     // S: fixed-point resolution 2^-S of the cell coordinate t
-  uint32_t frac_mask = 0; // ((1<<S)-1) & ~7: bits & mask == 0 <=> round(t*2^S) mod 2^S in [-3, 4]
+  uint32_t frac_mask = 0; // ((1<<S)-1) & ~3: bits & mask == 0 <=> round(t*2^S) mod 2^S in [-2, 1]
   int magic_hi = 0;       // bits(1.5*2^(23-S)) >> S
   int clamp = 0;     // 1 if votes can fall outside the unit-disk rows/cols (extent <= 1)
   int r_min = 0, r_max = 0;  // stored rows [r_min, r_max]
@@ -49,17 +49,20 @@ struct VoteBuffers {
   const double* zz = nullptr;
   float4* basis_a = nullptr;   // (a1x a1y a1z a2x) rounded to f32
   float2* basis_b = nullptr;   // (a2y a2z)
-  uint32_t* ranges = nullptr;  // [n_bands][n][2]: (start | len<<16) x 2
+  // [n_bands][entry_cap] work entries of each band: ci | (start | len<<16) << 32, one per
+  // non-empty pair range of a constraint in the band (order irrelevant: integer sums)
+  unsigned long long* entries = nullptr;
+  int32_t* entry_count = nullptr;  // [kMaxBands] entries appended per band by K1
+  int64_t entry_cap = 0;           // entries stride per band (2 per constraint)
   unsigned long long* band_work = nullptr;  // [kMaxBands] pairs per band (incl. padding)
   float2* table32 = nullptr;   // [halfJ] (cos, sin) of theta_p, rounded to f32
   double2* table64 = nullptr;  // [J] (cos, sin) exactly as the reference (host libm)
   uint32_t* grid = nullptr;    // [G*G] output
   uint32_t* partials = nullptr;        // [max_slots][tile_words]
   int32_t* slot_band = nullptr;        // [max_slots]
-  int32_t* counters = nullptr;         // [0]=slot counter, [1..kMaxBands]=constraint counters per band
+  int32_t* counters = nullptr;         // [0]=slot counter, [1..kMaxBands]=entry counters per band
   unsigned long long* stats = nullptr; // [0]=pairs evaluated, [1]=fallback pairs
   int max_slots = 0;
-  int64_t layout_n = 0;                // ranges stride per band (capacity)
   const int32_t* bounds = nullptr;     // device [lo, hi) of constraints for this launch (null: [0, n))
 };
 

@@ -37,6 +37,22 @@ constexpr float kTwoPiF = 6.28318530717958647692f;
 constexpr float kRcMin = 1e-3f;     // |c| amplitude below which a circle is treated as all-band
 constexpr float kDc = 2e-6f;        // |c| below this: hemisphere flip ambiguous -> exact path
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// per-warp fallback queue in shared memory (32-bit shared-window addresses)
+__device__ __forceinline__ void sts_u32(uint32_t saddr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
+  return v;
+}
+
 // ---- K1b: band plan --------------------------------------------------------------------
 // Cheap trig for the planner: errors (~1e-5 rad) are far below the 2-pair padding (6e-3 rad at
 // J=2048); coverage only has to be a superset, ownership is decided exactly per sample.
@@ -237,7 +253,6 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
   const int64_t lo = b.bounds ? b.bounds[0] : 0, hi = b.bounds ? b.bounds[1] : n;
   const int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = i < hi;
-  const int64_t stride = b.layout_n;
   const int M = p.halfJ;
   float f1[3] = {0.f, 0.f, 0.f}, f2[3] = {0.f, 0.f, 0.f};
   if (valid) {
@@ -259,12 +274,13 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
   const float theta_a = atan2_fast(f2[2], f1[2]) + 0.5f * kPiF;  // c(theta_a + s) = -rc sin(s)
   const float inv_step = 1.f / p.step_f;
   const float pa = (theta_a + kPiF) * inv_step;
-  uint2* rp = reinterpret_cast<uint2*>(b.ranges) + i;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
   Arc2 ulo{0.f, kPiF, 0.f, 0.f, 1};  // band 0: Y >= -inf
-  for (int band = 0; band < p.n_bands; ++band) {  // uniform trip count: warp reductions below
+  for (int band = 0; band < p.n_bands; ++band) {  // uniform trip count: warp collectives below
     unsigned long long w = 0;
+    uint2 r = make_uint2(0u, 0u);
     if (valid) {
-      uint2 r;
       if (polar) {
         r = make_uint2((uint32_t)M << 16, 0u);
         w = (unsigned long long)M;
@@ -280,10 +296,23 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
         }
         r = plan_from_sets(ulo, uhi, pa, inv_step, M, &w);
       }
-      rp[(int64_t)band * stride] = r;
+    }
+    // append the non-empty ranges to the band's entry list (warp-aggregated; r.y != 0 => r.x != 0)
+    const unsigned m0 = __ballot_sync(0xFFFFFFFFu, r.x >= 0x10000u);
+    const unsigned m1 = __ballot_sync(0xFFFFFFFFu, r.y >= 0x10000u);
+    const int total = __popc(m0) + __popc(m1);
+    if (total) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&b.entry_count[band], total);
+      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      unsigned long long* ep = b.entries + (int64_t)band * b.entry_cap + base + __popc(m0 & lt_mask) +
+                               __popc(m1 & lt_mask);
+      const unsigned long long ci = (unsigned long long)(uint32_t)i;
+      if (r.x >= 0x10000u) ep[0] = ci | ((unsigned long long)r.x << 32);
+      if (r.y >= 0x10000u) ep[1] = ci | ((unsigned long long)r.y << 32);
     }
     for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xFFFFFFFFu, w, o);
-    if ((threadIdx.x & 31) == 0 && w) atomicAdd(&s_work[band], w);
+    if (lane == 0 && w) atomicAdd(&s_work[band], w);
   }
   __syncthreads();
   for (int t = threadIdx.x; t < p.n_bands; t += blockDim.x)
@@ -291,6 +320,39 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
 }
 
 // ---- K2 ------------------------------------------------------------------------------
+
+// f32 evaluation of one pair: tile-relative linear cell index `rel` (>= tile_cells: not this
+// band's tile) and whether the f32 cell is not provably the reference cell. Shared by the hot
+// loop and the exact path (which undoes the hot loop's deposit), so both see identical values.
+struct F32Geom {
+  float CMf;
+  int S;
+  uint32_t fmask;
+  uint32_t W;
+  uint32_t lin_off;  // non-clamp: (magic_hi + r0) * W + magic_hi + c_min
+  int magic_hi, G, r0, c_min;
+};
+template <bool kClamp>
+__device__ __forceinline__ uint32_t f32_cell(const F32Geom& g, float4 ba, float2 bb, float2 t, bool* flag) {
+  // x, y carry the cell scale K = G/(2E) (folded into the f32 basis by the planner)
+  const float xk = fmaf(ba.w, t.y, ba.x * t.x);
+  const float yk = fmaf(bb.x, t.y, ba.y * t.x);
+  const float c = fmaf(bb.y, t.y, ba.z * t.x);
+  const float r = rcp_approx(1.f + fabsf(c));
+  const float rs = __int_as_float(__float_as_int(r) | (~__float_as_int(c) & 0x80000000));
+  const uint32_t bx = (uint32_t)__float_as_int(fmaf(xk, rs, g.CMf));
+  const uint32_t by = (uint32_t)__float_as_int(fmaf(yk, rs, g.CMf));
+  *flag = (fabsf(c) < kDc) | ((bx & g.fmask) == 0u) | ((by & g.fmask) == 0u);
+  // the column is always inside [c_min, c_min+W) (|X| <= 1 < extent, or clamped), so one
+  // unsigned range test on the linear index is the band-ownership test
+  if (kClamp) {
+    const int row = min(max((int)(by >> g.S) - g.magic_hi, 0), g.G - 1) - g.r0;
+    const int col = min(max((int)(bx >> g.S) - g.magic_hi, 0), g.G - 1) - g.c_min;
+    return (uint32_t)(row * (int)g.W + col);
+  }
+  return (by >> g.S) * g.W + (bx >> g.S) - g.lin_off;
+}
+
 
 // Exact f64 evaluation of both twins of a queued pair; deposits the ones this band owns.
 // Cold path (~0.6% of pairs), kept out of line so the hot loop keeps its registers.
@@ -304,13 +366,29 @@ struct FbCtx {  // the few scalars the exact path needs (keeps the kernel-param 
   int G, halfJ, c_min, W, own_lo, own_hi;
 };
 
-__device__ __noinline__ void fallback_pairs(FbCtx f, const uint32_t* q, int count, int64_t c_begin, uint32_t* tile,
-                                            int r0, int hb) {
+// Exact path of queued pairs: the hot loop deposited +2 at the pair's f32 cell (if in this tile)
+// unconditionally; undo that, then deposit both twins at their exact f64 cells (row-owned).
+template <bool kClamp>
+__device__ __noinline__ void fallback_pairs(FbCtx f, F32Geom g, uint32_t q_s, int count, uint32_t my_ci,
+                                            float4 my_a, float2 my_b, const float2* tab, uint32_t* tile,
+                                            uint32_t tile_cells, int hb) {
   const int lane = threadIdx.x & 31;
+  const uint32_t e = lane < count ? lds_u32(q_s + 4u * lane) : 0u;
+  const int k = (int)(e >> 16) & 31;  // entry index within the warp's grab
+  const uint32_t ci = __shfl_sync(0xFFFFFFFFu, my_ci, k);
+  float4 ba;
+  float2 bb;
+  ba.x = __shfl_sync(0xFFFFFFFFu, my_a.x, k);
+  ba.y = __shfl_sync(0xFFFFFFFFu, my_a.y, k);
+  ba.z = __shfl_sync(0xFFFFFFFFu, my_a.z, k);
+  ba.w = __shfl_sync(0xFFFFFFFFu, my_a.w, k);
+  bb.x = __shfl_sync(0xFFFFFFFFu, my_b.x, k);
+  bb.y = __shfl_sync(0xFFFFFFFFu, my_b.y, k);
   if (lane < count) {
-    const uint32_t e = q[lane];
-    const int64_t ci = c_begin + (e >> 16);
     const int pair = (int)(e & 0xFFFFu);
+    bool fl;
+    const uint32_t rel = f32_cell<kClamp>(g, ba, bb, tab[pair], &fl);
+    if (rel < tile_cells) atomicSub(&tile[rel], 2u);
     double a1[3], a2[3];
     exact_basis(f.zx[ci], f.zy[ci], f.zz[ci], a1, a2);
     VotePlan p1;
@@ -323,7 +401,7 @@ __device__ __noinline__ void fallback_pairs(FbCtx f, const uint32_t* q, int coun
       int row, col;
       exact_sample(a1, a2, cs.x, cs.y, p1, &row, &col);
       if (row < f.own_lo || row >= f.own_hi) continue;
-      const int lr = row - r0, lc = col - f.c_min;
+      const int lr = row - g.r0, lc = col - f.c_min;
       if ((unsigned)lr < (unsigned)hb && (unsigned)lc < (unsigned)f.W)
         atomicAdd(&tile[lr * f.W + lc], 1u);
       else
@@ -333,10 +411,11 @@ __device__ __noinline__ void fallback_pairs(FbCtx f, const uint32_t* q, int coun
   __syncwarp();
 }
 
-__device__ __forceinline__ float rcp_approx(float x) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
+// table read (read-only after the prologue's barrier, so no memory clobber)
+__device__ __forceinline__ float2 lds_f2(uint32_t saddr) {
+  float2 t;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(t.x), "=f"(t.y) : "r"(saddr));
+  return t;
 }
 
 __device__ __forceinline__ void red_shared(uint32_t saddr, uint32_t v) {
@@ -350,13 +429,13 @@ __device__ __forceinline__ void red_shared_if(uint32_t saddr, uint32_t v, bool p
 }
 
 // K2: persistent, one CTA per SM, 16 warps. A CTA owns one row band's u32 tile in shared
-// memory at a time. Warps grab kWarpGrab constraints at a time from the band's global work
-// counter (no CTA barrier per chunk); when the band is exhausted the CTA flushes its tile to a
-// partial slot and steals the band with the most remaining work. Warp = one constraint; lanes
-// walk 64 consecutive sample pairs per iteration of the constraint's planned ranges (64-aligned,
-// table doubled so ranges never wrap). Pairs whose f32 cell is not provably the reference cell
-// are queued per warp and recomputed exactly in f64.
-constexpr int kWarpGrab = 16;
+// memory at a time. Warps grab 32 work entries at a time from the band's entry list (K1 appends
+// one entry per non-empty (constraint, band) pair range; lane k loads entry k and its f32 basis,
+// the warp then walks the entries, broadcasting each by shuffles); no CTA barrier per grab. When
+// the band is exhausted the CTA flushes its tile to a partial slot and steals the band with the
+// most remaining entries. Lanes walk 64 consecutive sample pairs per step of a range (32-aligned
+// lengths, table doubled so ranges never wrap). Pairs whose f32 cell is not provably the
+// reference cell are queued per warp and recomputed exactly in f64.
 
 template <bool kClamp>
 __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p, VoteBuffers b, int64_t n) {
@@ -369,8 +448,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
   __shared__ int s_band, s_slot;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t* fbq = fbq_all + warp * kFbqCap;
-  const int64_t c_lo = b.bounds ? b.bounds[0] : 0, c_hi = b.bounds ? b.bounds[1] : n;
+  uint32_t fbq_s = (uint32_t)__cvta_generic_to_shared(fbq_all + warp * kFbqCap);  // this warp's queue
   for (int k = tid; k < 2 * M + 64; k += blockDim.x) tab[k] = b.table32[k % M];
 
   if (tid == 0) {  // initial band: CTAs split across bands in proportion to planned work
@@ -393,9 +471,15 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
   for (size_t k = tid; k < p.tile_words; k += blockDim.x) tile[k] = 0u;
   __syncthreads();
   unsigned int my_fb = 0;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  const uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(tile);
-  const uint32_t dummy_s = (uint32_t)__cvta_generic_to_shared(dummy + lane);
+  unsigned lt_mask = (1u << lane) - 1u;
+  // per-lane table address (shared window): loaded by ld.shared below
+  uint32_t tab_s = (uint32_t)__cvta_generic_to_shared(tab) + 8u * (uint32_t)lane;
+  asm volatile("" : "+r"(lt_mask), "+r"(tab_s), "+r"(fbq_s));
+  // opaque to the optimizer: otherwise the shared-window base is rematerialised every step
+  uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(tile);
+  uint32_t dummy_s = (uint32_t)__cvta_generic_to_shared(dummy + lane);
+  uint32_t vote2 = 2u;
+  asm volatile("" : "+r"(tile_s), "+r"(dummy_s), "+r"(vote2));
   const float CMf = p.CMf;
   const int W = p.W, G = p.G;
   const int S = p.frac_shift;
@@ -423,105 +507,93 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     const int col_off = p.magic_hi + p.c_min; // col_local = (bits_x >> S) - col_off
     const uint32_t lin_off = (uint32_t)row_off * (uint32_t)W + (uint32_t)col_off;
     const uint32_t tile_cells = (uint32_t)hb * (uint32_t)W;
-    const uint2* rbase = reinterpret_cast<const uint2*>(b.ranges) + (int64_t)band * b.layout_n;
+    F32Geom geo;
+    geo.CMf = CMf;
+    geo.S = S;
+    geo.fmask = fmask;
+    geo.W = (uint32_t)W;
+    geo.lin_off = lin_off;
+    geo.magic_hi = p.magic_hi;
+    geo.G = G;
+    geo.r0 = r0;
+    geo.c_min = p.c_min;
+    const unsigned long long* ebase = b.entries + (int64_t)band * b.entry_cap;
+    const int n_ent = b.entry_count[band];
     int* counter = &b.counters[1 + band];
-    const float4* basis_a = b.basis_a;
-    const float2* basis_b = b.basis_b;
-    const int ci_lo = (int)c_lo, ci_hi = (int)c_hi;  // constraint counts fit in 31 bits
-    for (;;) {  // per-warp dynamic grabs of kWarpGrab constraints
+    for (;;) {  // per-warp dynamic grabs of 32 entries (lane k holds entry k: range + f32 basis)
       int g0 = 0;
-      if (lane == 0) g0 = atomicAdd(counter, kWarpGrab);
-      g0 = __shfl_sync(0xFFFFFFFFu, g0, 0) + ci_lo;
-      if (g0 >= ci_hi) break;
-      const int g1 = min(g0 + kWarpGrab, ci_hi);
+      if (lane == 0) g0 = atomicAdd(counter, 32);
+      g0 = __shfl_sync(0xFFFFFFFFu, g0, 0);
+      if (g0 >= n_ent) break;
+      const int ne = min(32, n_ent - g0);
+      uint32_t my_ci = 0, my_enc = 0;
+      float4 my_a = make_float4(0.f, 0.f, 0.f, 0.f);
+      float2 my_b = make_float2(0.f, 0.f);
+      if (lane < ne) {
+        const unsigned long long e = __ldcs(ebase + g0 + lane);
+        my_ci = (uint32_t)e;
+        my_enc = (uint32_t)(e >> 32);
+        my_a = b.basis_a[my_ci];
+        my_b = b.basis_b[my_ci];
+      }
       int qn = 0;
-      uint2 rr = rbase[g0];
-      float4 ba = basis_a[g0];
-      float2 bb = basis_b[g0];
-      for (int ci = g0; ci < g1; ++ci) {
-        uint2 rr_n = rr;
-        float4 ba_n = ba;
-        float2 bb_n = bb;
-        if (ci + 1 < g1) {  // prefetch the next constraint
-          rr_n = rbase[ci + 1];
-          ba_n = basis_a[ci + 1];
-          bb_n = basis_b[ci + 1];
-        }
-        const uint32_t local_ci = (uint32_t)(ci - g0) << 16;
-#pragma unroll 1
-        for (int rk = 0; rk < 2; ++rk) {
-          const uint32_t enc = rk == 0 ? rr.x : rr.y;
-          if (enc < 0x10000u) continue;  // empty range (len == 0)
-          const int start = (int)(enc & 0xFFFFu), len = (int)(enc >> 16);
-          const float2* tp = tab + start + lane;
-          // NP pairs per lane per step (32*NP consecutive pairs per warp); ranges are 32-aligned:
-          // 64-pair steps while they fit, then one 32-pair tail step
-          auto step = [&](int k0, auto np_tag) {
-            constexpr int NP = decltype(np_tag)::value;
-            bool flag[NP];
-            uint32_t addr[NP];
+      for (int k = 0; k < ne; ++k) {
+        const uint32_t enc = __shfl_sync(0xFFFFFFFFu, my_enc, k);
+        float4 ba;
+        float2 bb;
+        ba.x = __shfl_sync(0xFFFFFFFFu, my_a.x, k);
+        ba.y = __shfl_sync(0xFFFFFFFFu, my_a.y, k);
+        ba.z = __shfl_sync(0xFFFFFFFFu, my_a.z, k);
+        ba.w = __shfl_sync(0xFFFFFFFFu, my_a.w, k);
+        bb.x = __shfl_sync(0xFFFFFFFFu, my_b.x, k);
+        bb.y = __shfl_sync(0xFFFFFFFFu, my_b.y, k);
+        const uint32_t local_k = (uint32_t)k << 16;
+        const int start = (int)(enc & 0xFFFFu), len = (int)(enc >> 16);
+        const uint32_t tp_s = tab_s + 8u * (uint32_t)start;
+        // NP pairs per lane per step (32*NP consecutive pairs per warp); ranges are 32-aligned:
+        // 64-pair steps while they fit, then one 32-pair tail step
+        auto step = [&](int k0, auto np_tag) {
+          constexpr int NP = decltype(np_tag)::value;
+          bool flag[NP];
+          uint32_t addr[NP];
+#pragma unroll
+          for (int h = 0; h < NP; ++h) {
+            const uint32_t rel = f32_cell<kClamp>(geo, ba, bb, lds_f2(tp_s + 8u * (uint32_t)(k0 + 32 * h)), &flag[h]);
+            // deposit even if flagged: the exact path undoes it (no select on the flag here)
+            addr[h] = rel < tile_cells ? tile_s + 4u * rel : dummy_s;
+          }
+#pragma unroll
+          for (int h = 0; h < NP; ++h) red_shared(addr[h], vote2);
+          bool any = false;
+#pragma unroll
+          for (int h = 0; h < NP; ++h) any |= flag[h];
+          if (__any_sync(0xFFFFFFFFu, any)) {  // cold: queue for the exact f64 path
 #pragma unroll
             for (int h = 0; h < NP; ++h) {
-              const float2 t = tp[k0 + 32 * h];
-              // x, y carry the cell scale K = G/(2E) (folded into the f32 basis by the planner)
-              const float xk = fmaf(ba.w, t.y, ba.x * t.x);
-              const float yk = fmaf(bb.x, t.y, ba.y * t.x);
-              const float c = fmaf(bb.y, t.y, ba.z * t.x);
-              const float r = rcp_approx(1.f + fabsf(c));
-              const float rs = __int_as_float(__float_as_int(r) | (~__float_as_int(c) & 0x80000000));
-              const uint32_t bx = (uint32_t)__float_as_int(fmaf(xk, rs, CMf));
-              const uint32_t by = (uint32_t)__float_as_int(fmaf(yk, rs, CMf));
-              flag[h] = (fabsf(c) < kDc) | ((bx & fmask) == 0u) | ((by & fmask) == 0u);
-              // cell index relative to the tile; the column is always inside [c_min, c_min+W) for
-              // an unflagged pair (|X| <= 1 < extent, or clamped), so one unsigned range test on
-              // the linear index is the band-ownership test
-              uint32_t rel;
-              if (kClamp) {
-                const int row = min(max((int)(by >> S) - p.magic_hi, 0), G - 1) - r0;
-                const int col = min(max((int)(bx >> S) - p.magic_hi, 0), G - 1) - p.c_min;
-                rel = (uint32_t)(row * W + col);
-              } else {
-                rel = (by >> S) * (uint32_t)W + (bx >> S) - lin_off;
+              const unsigned fm = __ballot_sync(0xFFFFFFFFu, flag[h]);
+              if (flag[h]) {
+                int pair = start + k0 + 32 * h + lane;
+                if (pair >= M) pair -= M;
+                sts_u32(fbq_s + 4u * (uint32_t)(qn + __popc(fm & lt_mask)), local_k | (uint32_t)pair);
               }
-              const bool dep = !flag[h] && rel < tile_cells;
-              addr[h] = dep ? tile_s + 4u * rel : dummy_s;
-            }
-#pragma unroll
-            for (int h = 0; h < NP; ++h) red_shared(addr[h], 2u);
-            bool any = false;
-#pragma unroll
-            for (int h = 0; h < NP; ++h) any |= flag[h];
-            if (__any_sync(0xFFFFFFFFu, any)) {  // cold: queue for the exact f64 path
-#pragma unroll
-              for (int h = 0; h < NP; ++h) {
-                const unsigned fm = __ballot_sync(0xFFFFFFFFu, flag[h]);
-                if (flag[h]) {
-                  int pair = start + k0 + 32 * h + lane;
-                  if (pair >= M) pair -= M;
-                  fbq[qn + __popc(fm & lt_mask)] = local_ci | (uint32_t)pair;
-                }
-                qn += __popc(fm);
-                my_fb += __popc(fm);
+              qn += __popc(fm);
+              my_fb += __popc(fm);
+              __syncwarp();
+              if (qn >= 32) {
+                fallback_pairs<kClamp>(fc, geo, fbq_s, 32, my_ci, my_a, my_b, tab, tile, tile_cells, hb);
+                qn -= 32;
+                if (lane < qn) sts_u32(fbq_s + 4u * lane, lds_u32(fbq_s + 4u * (32 + lane)));
                 __syncwarp();
-                if (qn >= 32) {
-                  fallback_pairs(fc, fbq, 32, g0, tile, r0, hb);
-                  qn -= 32;
-                  if (lane < qn) fbq[lane] = fbq[32 + lane];
-                  __syncwarp();
-                }
               }
             }
-          };
-          int k0 = 0;
+          }
+        };
+        int k0 = 0;
 #pragma unroll 1
-          for (; k0 + 64 <= len; k0 += 64) step(k0, std::integral_constant<int, 2>{});
-          if (k0 < len) step(k0, std::integral_constant<int, 1>{});
-        }
-        rr = rr_n;
-        ba = ba_n;
-        bb = bb_n;
+        for (; k0 + 64 <= len; k0 += 64) step(k0, std::integral_constant<int, 2>{});
+        if (k0 < len) step(k0, std::integral_constant<int, 1>{});
       }
-      if (qn > 0) fallback_pairs(fc, fbq, qn, g0, tile, r0, hb);
+      if (qn > 0) fallback_pairs<kClamp>(fc, geo, fbq_s, qn, my_ci, my_a, my_b, tab, tile, tile_cells, hb);
     }
     // band exhausted for this CTA: flush the tile to a partial slot, steal the next band
     __syncthreads();
@@ -532,7 +604,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
       int best = -1;
       long long best_rem = 0;
       for (int q = 0; q < p.n_bands; ++q) {
-        const long long rem = (long long)(c_hi - c_lo) - *((volatile int*)&b.counters[1 + q]);
+        const long long rem = (long long)b.entry_count[q] - *((volatile int*)&b.counters[1 + q]);
         if (rem > best_rem) {
           best_rem = rem;
           best = q;
