@@ -45,7 +45,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     obj_dir.mkdir(exist_ok=True)
     common = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
               "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}"]
-    objs = []
+    extra = os.environ.get("RV_NVCC_EXTRA", "").split()  # dev sweeps only (e.g. -DRV_NP=4)
+    common += extra
+    jobs = []
     for src in SOURCES:
         obj = obj_dir / (Path(src).stem + ".o")
         cmd = [nvcc(), *ARCH, *common, *(["-fmad=false"] if src in NO_FMAD else []),
@@ -54,12 +56,17 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if src.endswith(".cpp"):
             cmd = [nvcc(), *ARCH, *[a for a in common if a != "--expt-relaxed-constexpr"], "-x", "c++", "-c",
                    str(CSRC / src), "-o", str(obj)]
-        res = subprocess.run(cmd, capture_output=True, text=True)
+        jobs.append((src, cmd, str(obj)))
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
+        results = list(ex.map(lambda j: subprocess.run(j[1], capture_output=True, text=True), jobs))
+    objs = []
+    for (src, _, obj), res in zip(jobs, results):
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
         if verbose and res.stderr:
             sys.stderr.write(res.stderr)
-        objs.append(str(obj))
+        objs.append(obj)
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs, "-cudart", "static"]
     res = subprocess.run(cmd, capture_output=True, text=True)

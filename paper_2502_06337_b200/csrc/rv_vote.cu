@@ -36,6 +36,12 @@ constexpr float kPiF = 3.14159265358979323846f;
 constexpr float kTwoPiF = 6.28318530717958647692f;
 constexpr float kRcMin = 1e-3f;     // |c| amplitude below which a circle is treated as all-band
 constexpr float kDc = 2e-6f;        // |c| below this: hemisphere flip ambiguous -> exact path
+#ifndef RV_NP
+#define RV_NP 2  // pairs per lane per full step of the vote loop (2 or 4)
+#endif
+#ifndef RV_PRED
+#define RV_PRED 0  // 1: predicated deposit instead of the per-lane sink word
+#endif
 
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
@@ -560,10 +566,22 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
           for (int h = 0; h < NP; ++h) {
             const uint32_t rel = f32_cell<kClamp>(geo, ba, bb, lds_f2(tp_s + 8u * (uint32_t)(k0 + 32 * h)), &flag[h]);
             // deposit even if flagged: the exact path undoes it (no select on the flag here)
+#if RV_PRED
+            addr[h] = rel;
+#else
             addr[h] = rel < tile_cells ? tile_s + 4u * rel : dummy_s;
+#endif
           }
 #pragma unroll
-          for (int h = 0; h < NP; ++h) red_shared(addr[h], vote2);
+          for (int h = 0; h < NP; ++h) {
+#if RV_PRED
+            asm volatile("{\n\t.reg .pred q;\n\tsetp.lt.u32 q, %1, %2;\n\t@q red.shared.add.u32 [%0], %3;\n\t}" ::"r"(
+                             tile_s + 4u * addr[h]),
+                         "r"(addr[h]), "r"(tile_cells), "r"(vote2));
+#else
+            red_shared(addr[h], vote2);
+#endif
+          }
           bool any = false;
 #pragma unroll
           for (int h = 0; h < NP; ++h) any |= flag[h];
@@ -589,8 +607,17 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
           }
         };
         int k0 = 0;
+        if constexpr (RV_NP == 4) {
 #pragma unroll 1
-        for (; k0 + 64 <= len; k0 += 64) step(k0, std::integral_constant<int, 2>{});
+          for (; k0 + 128 <= len; k0 += 128) step(k0, std::integral_constant<int, 4>{});
+          if (k0 + 64 <= len) {
+            step(k0, std::integral_constant<int, 2>{});
+            k0 += 64;
+          }
+        } else {
+#pragma unroll 1
+          for (; k0 + 64 <= len; k0 += 64) step(k0, std::integral_constant<int, 2>{});
+        }
         if (k0 < len) step(k0, std::integral_constant<int, 1>{});
       }
       if (qn > 0) fallback_pairs<kClamp>(fc, geo, fbq_s, qn, my_ci, my_a, my_b, tab, tile, tile_cells, hb);
