@@ -125,6 +125,12 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "fallback": True}
 
 
+def vote_profile():
+    """ncu --set full summary of the vote kernel committed under profiles/ (traffic, issue rate)."""
+    p = ROOT / "profiles" / "r1" / "vote_kernel_ncu.json"
+    return json.loads(p.read_text()) if p.exists() else None
+
+
 def reference_cpu(n_sample: int, reps: int, threads: int, corrs: np.ndarray):
     """The reference's own estimate_single (oracle/_ref, -O3 -march=native) on the host cores."""
     sys.path.insert(0, str(ROOT / "oracle"))
@@ -225,7 +231,7 @@ def run_device(args):
         solve_e2e()
     ctx.enable_timing(True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    vote_ms, launches, stage = [], 0, []
+    vote_ms, vote_k_ms, launches, stage = [], [], 0, []
     barrier()
     with ClockSampler(local) as clk:
         for k in range(args.steps):
@@ -237,6 +243,7 @@ def run_device(args):
             b.record(stream)
             st = ctx.stage_times()
             vote_ms.append(st["vote_ms"])
+            vote_k_ms.append(st["vote_kernel_ms"])
             launches += st["kernel_launches"]
             stage.append(st)
         barrier()
@@ -262,10 +269,11 @@ def run_device(args):
 
     t_dev = sum(dev_ms) / 1e3
     t_e2e = sum(e2e_ms) / 1e3
-    vals = torch.tensor([t_dev, t_e2e, sum(vote_ms) / 1e3], dtype=torch.float64, device=f"cuda:{local}")
+    vals = torch.tensor([t_dev, t_e2e, sum(vote_ms) / 1e3, sum(vote_k_ms) / 1e3], dtype=torch.float64,
+                        device=f"cuda:{local}")
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    t_dev, t_e2e, t_vote = vals.tolist()
+    t_dev, t_e2e, t_vote, t_vote_k = vals.tolist()
     total_corrs = (n_total if sharded else n_total * world) * args.steps
     value = total_corrs / t_dev
     e2e_value = total_corrs / t_e2e
@@ -274,17 +282,22 @@ def run_device(args):
             dist.destroy_process_group()
         return
     err_deg = float(np.degrees(np.arccos(np.clip(0.5 * (np.trace(rots[0].T @ est.rotation) - 1), -1, 1))))
-    # roofline of the dominant kernel (vote): algorithmic sample-votes per launch / launch time
+    # roofline of the dominant kernel (vote_banded_kernel): algorithmic sample-votes per launch /
+    # its average launch time (CUDA events around the kernel on the solve's stream)
     votes_per_launch = n_mine * cfg.theta_samples
-    vote_avg_s = t_vote / args.steps
+    vote_avg_s = t_vote_k / args.steps
     achieved = votes_per_launch / vote_avg_s
     peak = smem_atomic_peak(local)
-    roof = {"bound": "smem_atomic", "kernel": "vote_banded_kernel (+ plan, tile reduce)",
+    prof = vote_profile()
+    roof = {"bound": "smem_atomic", "kernel": "vote_banded_kernel",
             "achieved": achieved / 1e9, "peak": (peak / 1e9) if peak else None, "unit": "Gvotes/s",
-            "frac": (achieved / peak) if peak else None, "traffic": None,
+            "frac": (achieved / peak) if peak else None,
+            "traffic": prof.get("dram_bytes_per_launch") if prof else None,
             "peak_source": "conflict-free u32 smem atomicAdd, measured live (tools/microbench)",
             "work_per_launch": f"{votes_per_launch} sample-votes (N*J of this rank)",
-            "vote_ms_per_solve": 1e3 * vote_avg_s, "vote_share_of_solve": t_vote / t_dev}
+            "kernel_ms_per_solve": 1e3 * vote_avg_s, "kernel_share_of_solve": t_vote_k / t_dev,
+            "vote_stage_ms_per_solve": 1e3 * t_vote / args.steps,
+            "ncu": prof}
     pre_ms = statistics.mean(s["preprocess_ms"] for s in stage)
     hbm = measured_peaks().get("hbm_gbs")
     k1_gbs = (76.0 * n_mine) / (pre_ms * 1e-3) / 1e9 if pre_ms > 0 else None

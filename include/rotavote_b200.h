@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define RV_ABI_VERSION 1
+#define RV_ABI_VERSION 2
 
 typedef enum rv_status {
   RV_OK = 0,
@@ -97,6 +97,7 @@ typedef struct rv_stage_times {
   int64_t vote_samples;     /* algorithmic samples N_kept * J of all vote launches */
   int32_t vote_launches;    /* vote kernel launches in the call */
   int32_t kernel_launches;  /* all kernels launched by the call */
+  double vote_kernel_ms;    /* the band-tiled vote kernel alone (CUDA events around its launches) */
 } rv_stage_times;
 
 typedef struct rv_context rv_context;

@@ -68,6 +68,7 @@ class rv_stage_times(C.Structure):
         ("vote_samples", C.c_int64),
         ("vote_launches", C.c_int32),
         ("kernel_launches", C.c_int32),
+        ("vote_kernel_ms", C.c_double),
     ]
 
 

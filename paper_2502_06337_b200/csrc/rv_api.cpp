@@ -66,7 +66,7 @@ struct StageEvent {
   cudaEvent_t a, b;
 };
 
-enum Stage { kPrep = 0, kVote = 1, kPeaks = 2, kRefine = 3, kAngles = 4 };
+enum Stage { kPrep = 0, kVote = 1, kPeaks = 2, kRefine = 3, kAngles = 4, kVoteKernel = 5 };
 
 struct Peak {
   int ix, iy;
@@ -197,6 +197,7 @@ void end_call(rv_context* c) {
       case kVote: c->times.vote_ms += ms; break;
       case kPeaks: c->times.peaks_ms += ms; break;
       case kRefine: c->times.refine_ms += ms; break;
+      case kVoteKernel: c->times.vote_kernel_ms += ms; break;  // nested in kVote: not in total
       default: c->times.angles_ms += ms; break;
     }
   }
@@ -247,7 +248,7 @@ VotePlan make_plan(rv_context* c, int G, double E, int J) {
   p.c_max = p.r_max;
   p.W = p.c_max - p.c_min + 1;
   const size_t table_bytes = (size_t)(2 * p.halfJ + 64) * sizeof(float2);  // doubled: ranges never wrap
-  const size_t fbq_bytes = (size_t)(kVoteThreads / 32) * kFbqCap * 4 + 32 * 4;  // + lane sink words
+  const size_t fbq_bytes = (size_t)(kVoteThreads / 32) * kFbqCap * 4 + 32 * 4;  // + 32 lane sink words
   const size_t reserve = table_bytes + fbq_bytes + 1024;
   if ((size_t)c->max_smem <= reserve) return p;
   const size_t budget_words = ((size_t)c->max_smem - reserve) / 4;
@@ -266,7 +267,7 @@ VotePlan make_plan(rv_context* c, int G, double E, int J) {
     p.band_yhi[b] = b == nb - 1 ? INFINITY : (float)(-E + p.band_r0[b + 1] * p.cs + dy);
   }
   p.tile_words = (size_t)H * p.W;
-  p.smem_bytes = ((p.tile_words * 4 + 15) & ~size_t(15)) + table_bytes + fbq_bytes;
+  p.smem_bytes = (((p.tile_words + 32) * 4 + 15) & ~size_t(15)) + table_bytes + fbq_bytes;  // tile + sinks
   p.banded = p.smem_bytes <= (size_t)c->max_smem ? 1 : 0;
   return p;
 }
@@ -347,7 +348,10 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   ck(cudaMemsetAsync(b.counters, 0, sizeof(int32_t) * (2 * kMaxBands + 1), c->st), "memset counters");
   ck(cudaMemsetAsync(b.stats, 0, sizeof(unsigned long long) * 2, c->st), "memset stats");
   launch_plan(p, b, n, c->st);
-  launch_vote_banded(p, b, n, n_ctas, c->st);
+  {
+    StageScope kv(c, kVoteKernel);
+    launch_vote_banded(p, b, n, n_ctas, c->st);
+  }
   launch_vote_reduce(p, b, c->st);
   count_launch(c, 3);
   ck(cudaGetLastError(), "vote_banded");
@@ -884,7 +888,10 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
       if (k > 0)
         ck(cudaMemsetAsync(b.counters + 1, 0, sizeof(int32_t) * 2 * kMaxBands, c->st), "memset band counters");
       launch_plan(p, b, cap, c->st);
-      launch_vote_banded(p, b, cap, n_ctas, c->st);
+      {
+        StageScope kv(c, kVoteKernel);
+        launch_vote_banded(p, b, cap, n_ctas, c->st);
+      }
       count_launch(c, 2);
     }
     // copy k+1 is issued after compute k is queued: with pinned input both run concurrently;

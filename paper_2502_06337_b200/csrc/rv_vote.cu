@@ -338,8 +338,9 @@ struct F32Geom {
   uint32_t lin_off;  // non-clamp: (magic_hi + r0) * W + magic_hi + c_min
   int magic_hi, G, r0, c_min;
 };
-template <bool kClamp>
+template <bool kClamp, int kS>  // kS: compile-time fixed-point shift (0: g.S at run time)
 __device__ __forceinline__ uint32_t f32_cell(const F32Geom& g, float4 ba, float2 bb, float2 t, bool* flag) {
+  const int S = kS ? kS : g.S;
   // x, y carry the cell scale K = G/(2E) (folded into the f32 basis by the planner)
   const float xk = fmaf(ba.w, t.y, ba.x * t.x);
   const float yk = fmaf(bb.x, t.y, ba.y * t.x);
@@ -352,11 +353,11 @@ __device__ __forceinline__ uint32_t f32_cell(const F32Geom& g, float4 ba, float2
   // the column is always inside [c_min, c_min+W) (|X| <= 1 < extent, or clamped), so one
   // unsigned range test on the linear index is the band-ownership test
   if (kClamp) {
-    const int row = min(max((int)(by >> g.S) - g.magic_hi, 0), g.G - 1) - g.r0;
-    const int col = min(max((int)(bx >> g.S) - g.magic_hi, 0), g.G - 1) - g.c_min;
+    const int row = min(max((int)(by >> S) - g.magic_hi, 0), g.G - 1) - g.r0;
+    const int col = min(max((int)(bx >> S) - g.magic_hi, 0), g.G - 1) - g.c_min;
     return (uint32_t)(row * (int)g.W + col);
   }
-  return (by >> g.S) * g.W + (bx >> g.S) - g.lin_off;
+  return (by >> S) * g.W + (bx >> S) - g.lin_off;
 }
 
 
@@ -374,7 +375,7 @@ struct FbCtx {  // the few scalars the exact path needs (keeps the kernel-param 
 
 // Exact path of queued pairs: the hot loop deposited +2 at the pair's f32 cell (if in this tile)
 // unconditionally; undo that, then deposit both twins at their exact f64 cells (row-owned).
-template <bool kClamp>
+template <bool kClamp, int kS>
 __device__ __noinline__ void fallback_pairs(FbCtx f, F32Geom g, uint32_t q_s, int count, uint32_t my_ci,
                                             float4 my_a, float2 my_b, const float2* tab, uint32_t* tile,
                                             uint32_t tile_cells, int hb) {
@@ -393,7 +394,7 @@ __device__ __noinline__ void fallback_pairs(FbCtx f, F32Geom g, uint32_t q_s, in
   if (lane < count) {
     const int pair = (int)(e & 0xFFFFu);
     bool fl;
-    const uint32_t rel = f32_cell<kClamp>(g, ba, bb, tab[pair], &fl);
+    const uint32_t rel = f32_cell<kClamp, kS>(g, ba, bb, tab[pair], &fl);
     if (rel < tile_cells) atomicSub(&tile[rel], 2u);
     double a1[3], a2[3];
     exact_basis(f.zx[ci], f.zy[ci], f.zz[ci], a1, a2);
@@ -424,6 +425,8 @@ __device__ __forceinline__ float2 lds_f2(uint32_t saddr) {
   return t;
 }
 
+__device__ __forceinline__ uint32_t umin(uint32_t a, uint32_t b) { return a < b ? a : b; }
+
 __device__ __forceinline__ void red_shared(uint32_t saddr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v));
 }
@@ -443,14 +446,14 @@ __device__ __forceinline__ void red_shared_if(uint32_t saddr, uint32_t v, bool p
 // lengths, table doubled so ranges never wrap). Pairs whose f32 cell is not provably the
 // reference cell are queued per warp and recomputed exactly in f64.
 
-template <bool kClamp>
+template <bool kClamp, int kS>
 __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p, VoteBuffers b, int64_t n) {
   extern __shared__ uint4 smem_raw[];
   uint32_t* tile = reinterpret_cast<uint32_t*>(smem_raw);
-  float2* tab = reinterpret_cast<float2*>(tile + ((p.tile_words + 3) & ~size_t(3)));
+  // [tile_words] tile, [32] per-lane sink words, table, fallback queues
+  float2* tab = reinterpret_cast<float2*>(tile + ((p.tile_words + 32 + 3) & ~size_t(3)));
   const int M = p.halfJ;
   uint32_t* fbq_all = reinterpret_cast<uint32_t*>(tab + 2 * M + 64);
-  uint32_t* dummy = fbq_all + (kVoteThreads / 32) * kFbqCap;  // [32] sink words for masked lanes
   __shared__ int s_band, s_slot;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -483,9 +486,11 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
   asm volatile("" : "+r"(lt_mask), "+r"(tab_s), "+r"(fbq_s));
   // opaque to the optimizer: otherwise the shared-window base is rematerialised every step
   uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(tile);
-  uint32_t dummy_s = (uint32_t)__cvta_generic_to_shared(dummy + lane);
+  // deposits outside this band's rows go to tile rows >= hb (never flushed) or, beyond the tile,
+  // to this lane's sink word: addr = tile + 4 * min(rel, tile_words + lane)
+  uint32_t sink_rel = (uint32_t)p.tile_words + (uint32_t)lane;
   uint32_t vote2 = 2u;
-  asm volatile("" : "+r"(tile_s), "+r"(dummy_s), "+r"(vote2));
+  asm volatile("" : "+r"(tile_s), "+r"(sink_rel), "+r"(vote2));
   const float CMf = p.CMf;
   const int W = p.W, G = p.G;
   const int S = p.frac_shift;
@@ -515,7 +520,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     const uint32_t tile_cells = (uint32_t)hb * (uint32_t)W;
     F32Geom geo;
     geo.CMf = CMf;
-    geo.S = S;
+    geo.S = S;  // (run-time copy; kS != 0 overrides)
     geo.fmask = fmask;
     geo.W = (uint32_t)W;
     geo.lin_off = lin_off;
@@ -564,12 +569,12 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
           uint32_t addr[NP];
 #pragma unroll
           for (int h = 0; h < NP; ++h) {
-            const uint32_t rel = f32_cell<kClamp>(geo, ba, bb, lds_f2(tp_s + 8u * (uint32_t)(k0 + 32 * h)), &flag[h]);
+            const uint32_t rel = f32_cell<kClamp, kS>(geo, ba, bb, lds_f2(tp_s + 8u * (uint32_t)(k0 + 32 * h)), &flag[h]);
             // deposit even if flagged: the exact path undoes it (no select on the flag here)
 #if RV_PRED
             addr[h] = rel;
 #else
-            addr[h] = rel < tile_cells ? tile_s + 4u * rel : dummy_s;
+            addr[h] = tile_s + 4u * umin(rel, sink_rel);
 #endif
           }
 #pragma unroll
@@ -598,7 +603,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
               my_fb += __popc(fm);
               __syncwarp();
               if (qn >= 32) {
-                fallback_pairs<kClamp>(fc, geo, fbq_s, 32, my_ci, my_a, my_b, tab, tile, tile_cells, hb);
+                fallback_pairs<kClamp, kS>(fc, geo, fbq_s, 32, my_ci, my_a, my_b, tab, tile, tile_cells, hb);
                 qn -= 32;
                 if (lane < qn) sts_u32(fbq_s + 4u * lane, lds_u32(fbq_s + 4u * (32 + lane)));
                 __syncwarp();
@@ -620,7 +625,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
         }
         if (k0 < len) step(k0, std::integral_constant<int, 1>{});
       }
-      if (qn > 0) fallback_pairs<kClamp>(fc, geo, fbq_s, qn, my_ci, my_a, my_b, tab, tile, tile_cells, hb);
+      if (qn > 0) fallback_pairs<kClamp, kS>(fc, geo, fbq_s, qn, my_ci, my_a, my_b, tab, tile, tile_cells, hb);
     }
     // band exhausted for this CTA: flush the tile to a partial slot, steal the next band
     __syncthreads();
@@ -727,23 +732,35 @@ void launch_plan(const VotePlan& p, const VoteBuffers& b, int64_t n, cudaStream_
   plan_kernel<<<(unsigned)blocks, threads, 0, s>>>(p, b, n);
 }
 
+using VoteKernel = void (*)(VotePlan, VoteBuffers, int64_t);
+static VoteKernel vote_kernel_for(const VotePlan& p, int* slot) {
+  // S = 12 (every grid <= 1000) gets a compile-time shift; other S use the run-time variant
+  const int k = (p.clamp ? 2 : 0) + (p.frac_shift == 12 ? 1 : 0);
+  *slot = k;
+  switch (k) {
+    case 0: return vote_banded_kernel<false, 0>;
+    case 1: return vote_banded_kernel<false, 12>;
+    case 2: return vote_banded_kernel<true, 0>;
+    default: return vote_banded_kernel<true, 12>;
+  }
+}
+
 cudaError_t set_vote_smem(const VotePlan& p) {
-  static int configured[2] = {0, 0};  // largest dynamic smem opted in per instantiation
-  const int k = p.clamp ? 1 : 0;
+  static int configured[4] = {0, 0, 0, 0};  // largest dynamic smem opted in per instantiation
+  int k;
+  VoteKernel f = vote_kernel_for(p, &k);
   if ((int)p.smem_bytes <= configured[k]) return cudaSuccess;
-  const cudaError_t e = p.clamp ? cudaFuncSetAttribute(vote_banded_kernel<true>,
-                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes)
-                                : cudaFuncSetAttribute(vote_banded_kernel<false>,
-                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  const cudaError_t e =
+      cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)p.smem_bytes);
   if (e == cudaSuccess) configured[k] = (int)p.smem_bytes;
   return e;
 }
 
 void launch_vote_banded(const VotePlan& p, const VoteBuffers& b, int64_t n, int n_ctas, cudaStream_t s) {
-  if (p.clamp)
-    vote_banded_kernel<true><<<n_ctas, kVoteThreads, p.smem_bytes, s>>>(p, b, n);
-  else
-    vote_banded_kernel<false><<<n_ctas, kVoteThreads, p.smem_bytes, s>>>(p, b, n);
+  int k;
+  VoteKernel f = vote_kernel_for(p, &k);
+  f<<<n_ctas, kVoteThreads, p.smem_bytes, s>>>(p, b, n);
 }
 
 void launch_vote_reduce(const VotePlan& p, const VoteBuffers& b, cudaStream_t s) {

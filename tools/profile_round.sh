@@ -1,0 +1,9 @@
+# Round-end measurement bundle (run under gpurun on ONE B200): bench line, reference arm,
+# ncu launch list of the bench command, ncu --set full of the vote kernel. Outputs in gpurun_out/prof/.
+mkdir -p gpurun_out/prof
+python bench.py > gpurun_out/prof/bench.json 2> gpurun_out/prof/bench.err; echo bench_rc=$?
+python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/prof/bench_ref.json 2> gpurun_out/prof/bench_ref.err; echo ref_rc=$?
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/prof/launches.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/prof/ncu_launch.log 2>&1; echo ncu_launch_rc=$?
+ncu --set full --import-source on --clock-control none -k regex:vote_banded -c 1 -f -o gpurun_out/prof/vote_full \
+    python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/prof/ncu_full.log 2>&1; echo ncu_full_rc=$?

@@ -1,0 +1,96 @@
+"""Summarises ncu artefacts for profiles/: a launch list (--metrics gpu__time_duration.sum --csv)
+and an `ncu --set full` report of one kernel.
+
+  python tools/summarize_profiles.py launches.csv [full.ncu-rep] > SUMMARY.txt
+
+Shares are of the solve's own kernels (rvb:: namespace); the live microbench peak kernel and
+torch's L2-flush fill are listed but excluded from the shares.
+"""
+import collections
+import csv
+import subprocess
+import sys
+
+KEYS = ["SM Frequency", "Elapsed Cycles", "Duration", "DRAM Throughput", "Executed Ipc Active", "Issue Slots Busy",
+        "No Eligible", "Eligible Warps Per Scheduler", "Executed Instructions", "Registers Per Thread",
+        "Dynamic Shared Memory Per Block", "Achieved Occupancy", "Branch Efficiency", "L1/TEX Hit Rate"]
+RAW = ["smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+       "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+       "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+       "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+       "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+       "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+       "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum",
+       "smsp__inst_executed_op_shared_atom.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"]
+
+
+def launches(path):
+    rows = []
+    with open(path) as f:
+        lines = [ln for ln in f if ln.startswith('"')]
+    for r in csv.DictReader(lines):
+        if r.get("Metric Name") == "gpu__time_duration.sum":
+            rows.append((r["Kernel Name"], float(r["Metric Value"]) / (1e3 if r["Metric Unit"] == "ns" else 1.0)))
+    agg = collections.OrderedDict()
+    for name, us in rows:
+        a = agg.setdefault(name, [0, 0.0])
+        a[0] += 1
+        a[1] += us
+    own = sum(v[1] for k, v in agg.items() if "rvb::" in k)
+    out = ["# ncu launch list (gpu__time_duration.sum, --clock-control none; cold-cache, serialised)",
+           "# share = of the solve's own kernels (rvb::); others listed without a share"]
+    for name, (cnt, tot) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        share = f"{100 * tot / own:6.1f}%" if "rvb::" in name and own else "       "
+        out.append(f"{cnt:4d} launches  avg {tot / cnt:9.2f} us  {share}  {name[:100]}")
+    return out
+
+
+def full(path):
+    out = [f"# ncu --set full: {path}"]
+    res = subprocess.run(["ncu", "-i", path, "--page", "details", "--csv"], capture_output=True, text=True)
+    seen = set()
+    for r in csv.DictReader(res.stdout.splitlines()):
+        name = r.get("Metric Name")
+        if name in KEYS and name not in seen:
+            seen.add(name)
+            out.append(f"{name} = {r['Metric Value']} {r['Metric Unit']}")
+    res = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True)
+    rows = list(csv.reader(res.stdout.splitlines()))
+    if len(rows) > 2:
+        d = dict(zip(rows[0], rows[2]))
+        u = dict(zip(rows[0], rows[1]))
+        for k in RAW:
+            if k in d:
+                out.append(f"{k} = {d[k]} {u.get(k, '')}".rstrip())
+    return out
+
+
+def kernel_json(path):
+    """Per-launch numbers of the (single) kernel in an ncu --set full report, for bench.py."""
+    res = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True)
+    rows = list(csv.reader(res.stdout.splitlines()))
+    d, u = dict(zip(rows[0], rows[2])), dict(zip(rows[0], rows[1]))
+
+    def val(k, scale_units={"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6,
+                            "usecond": 1e-3, "msecond": 1.0}):
+        return float(d[k].replace(",", "")) * scale_units.get(u.get(k, ""), 1.0)
+
+    return {"kernel": d["Kernel Name"], "source": path.split("/")[-1],
+            "capture": "ncu --set full --clock-control none (one launch, cold cache, serialised)",
+            "duration_ms": val("gpu__time_duration.sum"),
+            "dram_bytes_per_launch": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
+            "inst_executed": val("smsp__inst_executed.sum"),
+            "issue_active_pct": val("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "shared_atom_inst": val("smsp__inst_executed_op_shared_atom.sum"),
+            "shared_atom_wavefronts": val("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum")}
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "--json":
+        import json
+        print(json.dumps(kernel_json(sys.argv[2]), indent=1))
+        sys.exit(0)
+    lines = launches(sys.argv[1])
+    if len(sys.argv) > 2:
+        lines += [""] + full(sys.argv[2])
+    print("\n".join(lines))
