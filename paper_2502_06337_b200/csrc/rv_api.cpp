@@ -119,7 +119,7 @@ struct rv_context {
   DBuf arg_keys, arg_out, sat, blur_best, blur_out, done;
   // classify / refine
   DBuf flagsA, flagsB, bcount, bscatter, bdiff, boffA, boffB, cls_result, compact_out;
-  DBuf coop_part, coop_state;  // device-resident refine_loop / anneal_axis (rv_coop.cu)
+  DBuf coop_part, coop_state, coop_bar;  // device-resident refine_loop / anneal_axis (rv_coop.cu)
   int coop_grid = 0;
   // angles / support
   DBuf bins, raw, angle_counts, angle_sums, angle_result, sup_counts, sup_result, band_flagsA, band_flagsB,
@@ -266,7 +266,7 @@ VotePlan make_plan(rv_context* c, int G, double E, int J) {
     p.band_ylo[b] = b == 0 ? -INFINITY : (float)(-E + p.band_r0[b] * p.cs - dy);
     p.band_yhi[b] = b == nb - 1 ? INFINITY : (float)(-E + p.band_r0[b + 1] * p.cs + dy);
   }
-  p.tile_words = (size_t)H * p.W;
+  p.tile_words = ((size_t)H * p.W + 3) & ~size_t(3);  // multiple of 4: 16-byte aligned partial slots
   p.smem_bytes = (((p.tile_words + 32) * 4 + 15) & ~size_t(15)) + table_bytes + fbq_bytes;  // tile + sinks
   p.banded = p.smem_bytes <= (size_t)c->max_smem ? 1 : 0;
   return p;
@@ -574,7 +574,7 @@ Cls coop_refine_dev(rv_context* c, const ConstraintSet& cs, double axis[3], int 
   double* part = c->coop_part.get<double>((size_t)c->coop_grid * 8);
   CoopState* dst = c->coop_state.get<CoopState>(1);
   ck(launch_coop_refine(cs.zx, cs.zy, cs.zz, cs.n, mode, cfg.refine ? 1 : 0, cfg.epsilon, e0, axis, fa, fb, tcount,
-                        toff, part, dst, c->coop_grid, c->st),
+                        toff, part, c->coop_bar.get<unsigned int>(2), dst, c->coop_grid, c->st),
      "coop refine launch");
   count_launch(c);
   static_assert(sizeof(CoopState) <= 4096, "pinned scratch");

@@ -1,11 +1,14 @@
 // K4': device-resident refine_loop / anneal_axis (estimator.cpp:51-69, :145-160) as ONE
 // cooperative kernel per call. Each pass is the strict classify of the constraint set (reference
-// op order, bitmask via ballot) fused with the 6 scatter sums of the same inliers; after a grid
-// barrier block 0 reduces the block partials in a fixed order, runs the 3x3 eigen-solve
-// (rv_linalg.hpp, the Eigen 3.4 restatement -- compiled here with -fmad=false so it is
-// bit-identical to the host instantiation), decides the next step and publishes it; a second
-// barrier hands the new axis to every block. No host round trip per pass.
-#include <cooperative_groups.h>
+// op order, bitmask via ballot) fused with the 6 scatter sums of the same inliers. After ONE grid
+// barrier per pass, EVERY block reduces the block partials in the same fixed order and runs the
+// same short-latency 3x3 eigen-solve (axis_from_scatter_fast, rv_linalg.hpp), so all blocks
+// reach the same decision without a second barrier; block 0 publishes the state for the host.
+// No host round trip per pass.
+//
+// Blocks own fixed contiguous tile ranges across passes, so the previous-pass flag words a block
+// compares against are its own writes: only the block partials cross blocks (read with .cg
+// after the barrier's release/acquire).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -13,8 +16,6 @@
 #include "rv_exact.cuh"
 #include "rv_internal.h"
 #include "rv_linalg.hpp"
-
-namespace cg = cooperative_groups;
 
 namespace rvb {
 namespace {
@@ -39,7 +40,8 @@ struct CoopArgs {
   uint32_t* flags1;
   int32_t* tile_count;
   int32_t* tile_offset;
-  double* block_part;  // [grid][8]
+  double* block_part;       // [grid][8]
+  unsigned int* barrier;    // [2] arrival counter, generation (zeroed before launch)
   State* state;
 };
 
@@ -48,35 +50,65 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
+// Grid barrier: release on arrival, acquire on the generation flip (no L1 invalidation needed:
+// the only cross-block data, the block partials and tile counts, are read with ld.global.cg).
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int gen;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
+    unsigned int arrived;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(bar) : "memory");
+    if (arrived == nblocks - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(gen + 1) : "memory");
+    } else {
+      unsigned int g = gen;
+      while (g == gen) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+    }
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
-  cg::grid_group grid = cg::this_grid();
   __shared__ double s_red[8][kThreads / 32];
-  __shared__ long long s_tot[kThreads];
+  __shared__ int s_cnt[kThreads / 32];
+  __shared__ double s_next[4];  // next axis (3) + next e
+  __shared__ int s_done;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t ntiles = (a.n + kTile - 1) / kTile;
+  const int64_t t_begin = ntiles * blockIdx.x / gridDim.x, t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
   double cls_axis[3] = {a.axis0[0], a.axis0[1], a.axis0[2]};
   double e = a.mode == 1 ? (a.e0 > a.eps ? a.e0 : a.eps) : a.eps;
-  int slot = 0;
+  int slot = 0, refits = 0;
   bool have_prev = false;
   for (;;) {
-    // ---- classify pass (grid-stride over 1024-constraint tiles) ----
+    // ---- classify pass over this block's tiles ----
     uint32_t* flags = slot == 0 ? a.flags0 : a.flags1;
     const uint32_t* prev = have_prev ? (slot == 0 ? a.flags1 : a.flags0) : nullptr;
     double sc[6] = {0, 0, 0, 0, 0, 0};
     long long cnt = 0;
     int diff = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int64_t t = t_begin; t < t_end; ++t) {
       const int64_t base = t * kTile;
+      double z[kPerThread][3];
+#pragma unroll
+      for (int r = 0; r < kPerThread; ++r) {  // all loads first
+        const int64_t i = base + r * kThreads + tid;
+        z[r][0] = z[r][1] = z[r][2] = 0.0;
+        if (i < a.n) {
+          z[r][0] = a.zx[i];
+          z[r][1] = a.zy[i];
+          z[r][2] = a.zz[i];
+        }
+      }
       int tcnt = 0;
 #pragma unroll
       for (int r = 0; r < kPerThread; ++r) {
         const int64_t i = base + r * kThreads + tid;
+        const double z0 = z[r][0], z1 = z[r][1], z2 = z[r][2];
         bool in = false;
-        double z0 = 0, z1 = 0, z2 = 0;
         if (i < a.n) {
-          z0 = a.zx[i];
-          z1 = a.zy[i];
-          z2 = a.zz[i];
           const double d = xa(xa(xm(cls_axis[0], z0), xm(cls_axis[1], z1)), xm(cls_axis[2], z2));
           in = fabs(d) < e;
         }
@@ -96,18 +128,17 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
           sc[5] = xa(sc[5], xm(z2, z2));
         }
       }
-      // per-tile count (each warp counted its words; sum the 8 warps of the tile)
-      if (lane == 0) s_tot[warp] = tcnt;
+      if (lane == 0) s_cnt[warp] = tcnt;
       __syncthreads();
       if (tid == 0) {
         int c = 0;
-        for (int w = 0; w < kThreads / 32; ++w) c += (int)s_tot[w];
-        a.tile_count[t] = c;
+        for (int w = 0; w < kThreads / 32; ++w) c += s_cnt[w];
+        __stcg(a.tile_count + t, c);
         cnt += c;
       }
       __syncthreads();
     }
-    // block partials: count (thread 0 holds it), diff, scatter (fixed-shape tree)
+    // block partials (fixed-shape tree): scatter[6], diff, count
     diff = __any_sync(0xFFFFFFFFu, diff);
 #pragma unroll
     for (int k = 0; k < 6; ++k) sc[k] = warp_sum_d(sc[k]);
@@ -121,17 +152,16 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
       for (int k = 0; k < 6; ++k) {
         double v = 0.0;
         for (int w = 0; w < kThreads / 32; ++w) v = xa(v, s_red[k][w]);
-        bp[k] = v;
+        __stcg(bp + k, v);
       }
       int d = 0;
       for (int w = 0; w < kThreads / 32; ++w) d |= s_red[6][w] != 0.0;
-      bp[6] = (double)d;
-      bp[7] = (double)cnt;
+      __stcg(bp + 6, (double)d);
+      __stcg(bp + 7, (double)cnt);
     }
-    grid.sync();
-    // ---- block 0: reduce (fixed order), decide, publish ----
-    if (blockIdx.x == 0) {
-      __shared__ int s_done;
+    grid_barrier(a.barrier, gridDim.x);
+    // ---- every block: reduce all partials in the same fixed order, decide ----
+    {
       double v[6] = {0, 0, 0, 0, 0, 0};
       double vc = 0.0;
       int vd = 0;
@@ -144,65 +174,75 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
       for (int k = 0; k < 6; ++k) v[k] = warp_sum_d(v[k]);
       vc = warp_sum_d(vc);
       vd = __any_sync(0xFFFFFFFFu, vd);
+      __syncthreads();  // s_red reuse
       if (lane == 0) {
         for (int k = 0; k < 6; ++k) s_red[k][warp] = v[k];
         s_red[6][warp] = (double)vd;
         s_red[7][warp] = vc;
       }
       __syncthreads();
-      if (tid == 0) {
-        double tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int w = 0; w < kThreads / 32; ++w) {
-          for (int k = 0; k < 6; ++k) tot[k] = xa(tot[k], s_red[k][w]);
-          if (s_red[6][w] != 0.0) tot[6] = 1.0;
-          tot[7] = xa(tot[7], s_red[7][w]);
+    }
+    if (tid == 0) {
+      double tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int w = 0; w < kThreads / 32; ++w) {
+        for (int k = 0; k < 6; ++k) tot[k] = xa(tot[k], s_red[k][w]);
+        if (s_red[6][w] != 0.0) tot[6] = 1.0;
+        tot[7] = xa(tot[7], s_red[7][w]);
+      }
+      const long long count = (long long)tot[7];
+      const bool differs = tot[6] != 0.0;
+      int done = 0, rank_deficient = 0;
+      double cur[3] = {cls_axis[0], cls_axis[1], cls_axis[2]};  // the set just classified is current
+      double nxt[3] = {cls_axis[0], cls_axis[1], cls_axis[2]};
+      double e_next = e;
+      if (a.mode == 0) {  // refine_loop (estimator.cpp:51-69)
+        if (!have_prev && !a.refine) done = 1;
+        if (have_prev && !differs) done = 1;  // stable
+        if (!done && (refits >= 10 || count < 2)) done = 1;
+        if (!done) {
+          if (axis_from_scatter_fast(tot, nxt)) {
+            ++refits;
+          } else {
+            rank_deficient = 1;  // RankDeficient: keep the current axis
+            done = 1;
+          }
         }
+      } else {  // anneal_axis (estimator.cpp:145-160)
+        if (count >= 2 && axis_from_scatter_fast(tot, nxt)) {
+          cur[0] = nxt[0];
+          cur[1] = nxt[1];
+          cur[2] = nxt[2];
+        }
+        nxt[0] = cur[0];
+        nxt[1] = cur[1];
+        nxt[2] = cur[2];
+        if (e <= a.eps) done = 1;
+        const double h = 0.5 * e;
+        e_next = a.eps > h ? a.eps : h;
+      }
+      if (blockIdx.x == 0) {  // publish (host reads it once at the end)
         State* st = a.state;
-        const long long count = (long long)tot[7];
-        const bool differs = tot[6] != 0.0;
-        int done = 0;
-        int refits = have_prev ? st->refits : 0;
-        if (!have_prev) st->rank_deficient = 0;
-        // the set just classified becomes the current one (estimator.cpp:63-65)
-        for (int k = 0; k < 3; ++k) st->axis[k] = cls_axis[k];
+        for (int k = 0; k < 3; ++k) {
+          st->axis[k] = cur[k];
+          st->next[k] = nxt[k];
+        }
         for (int k = 0; k < 6; ++k) st->scatter[k] = tot[k];
+        st->e = e_next;
         st->count = count;
         st->slot = slot;
-        double nxt[3] = {cls_axis[0], cls_axis[1], cls_axis[2]};
-        if (a.mode == 0) {
-          if (!have_prev && !a.refine) done = 1;
-          if (have_prev && !differs) done = 1;  // stable
-          if (!done && (refits >= 10 || count < 2)) done = 1;
-          if (!done) {
-            if (axis_from_scatter(tot, nxt)) {
-              ++refits;
-            } else {
-              st->rank_deficient = 1;  // RankDeficient: keep the current axis
-              done = 1;
-            }
-          }
-        } else {  // anneal_axis
-          double ax[3] = {cls_axis[0], cls_axis[1], cls_axis[2]};
-          if (count >= 2 && axis_from_scatter(tot, nxt)) {
-            ax[0] = nxt[0];
-            ax[1] = nxt[1];
-            ax[2] = nxt[2];
-          }
-          for (int k = 0; k < 3; ++k) {
-            st->axis[k] = ax[k];
-            nxt[k] = ax[k];
-          }
-          if (e <= a.eps) done = 1;
-          const double h = 0.5 * e;
-          st->e = a.eps > h ? a.eps : h;
-        }
-        for (int k = 0; k < 3; ++k) st->next[k] = nxt[k];
-        st->refits = refits;
         st->done = done;
-        s_done = done;
+        st->refits = refits;
+        st->rank_deficient = rank_deficient;
       }
-      __syncthreads();
-      if (s_done && a.mode == 0) {  // compaction offsets of the final set (tile order), block-parallel
+      for (int k = 0; k < 3; ++k) s_next[k] = nxt[k];
+      s_next[3] = e_next;
+      s_done = done;
+    }
+    __syncthreads();
+    const int done = s_done;
+    if (done) {
+      if (a.mode == 0 && blockIdx.x == 0) {  // compaction offsets of the final set (tile order)
+        __shared__ long long s_tot[kThreads];
         const int64_t per = (ntiles + kThreads - 1) / kThreads;
         const int64_t t0 = tid * per, t1 = t0 + per < ntiles ? t0 + per : ntiles;
         long long acc = 0;
@@ -224,13 +264,10 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
           off += __ldcg(a.tile_count + t);
         }
       }
-      __threadfence();
+      break;
     }
-    grid.sync();
-    const State* st = a.state;
-    if (__ldcg(&st->done)) break;
-    for (int k = 0; k < 3; ++k) cls_axis[k] = __ldcg(&st->next[k]);
-    if (a.mode == 1) e = __ldcg(&st->e);
+    for (int k = 0; k < 3; ++k) cls_axis[k] = s_next[k];
+    e = s_next[3];
     slot ^= 1;
     have_prev = a.mode == 0;
   }
@@ -249,8 +286,8 @@ int coop_tiles(int64_t n) { return (int)((n + kTile - 1) / kTile); }
 
 cudaError_t launch_coop_refine(const double* zx, const double* zy, const double* zz, int64_t n, int mode, int refine,
                                double eps, double e0, const double axis0[3], uint32_t* flags0, uint32_t* flags1,
-                               int32_t* tile_count, int32_t* tile_offset, double* block_part, void* state, int grid,
-                               cudaStream_t s) {
+                               int32_t* tile_count, int32_t* tile_offset, double* block_part, unsigned int* barrier,
+                               void* state, int grid, cudaStream_t s) {
   CoopArgs a;
   a.zx = zx;
   a.zy = zy;
@@ -266,8 +303,14 @@ cudaError_t launch_coop_refine(const double* zx, const double* zy, const double*
   a.tile_count = tile_count;
   a.tile_offset = tile_offset;
   a.block_part = block_part;
+  a.barrier = barrier;
   a.state = static_cast<State*>(state);
+  const int64_t ntiles = (n + kTile - 1) / kTile;
+  if (grid > ntiles) grid = (int)(ntiles > 0 ? ntiles : 1);  // every block owns >= 1 tile
+  cudaError_t e = cudaMemsetAsync(barrier, 0, 2 * sizeof(unsigned int), s);
+  if (e != cudaSuccess) return e;
   void* args[] = {&a};
+  // cooperative launch: guarantees co-residency of all blocks (required by the grid barrier)
   return cudaLaunchCooperativeKernel((void*)coop_refine_kernel, dim3(grid), dim3(kThreads), args, 0, s);
 }
 

@@ -38,7 +38,7 @@ struct VotePlan {
   float band_yhi[kMaxBands];
   float step_f = 0;             // (float)(2*pi/J)
   int banded = 0;               // 1: smem-tiled kernel; 0: exact generic global-atomic kernel
-  size_t tile_words = 0;        // H_max * W
+  size_t tile_words = 0;        // H_max * W rounded up to a multiple of 4
   size_t smem_bytes = 0;        // dynamic smem of the vote kernel
 };
 
@@ -169,7 +169,7 @@ size_t coop_state_bytes();
 // mode 0: refine_loop (estimator.cpp:51-69); mode 1: anneal_axis (estimator.cpp:145-160).
 cudaError_t launch_coop_refine(const double* zx, const double* zy, const double* zz, int64_t n, int mode, int refine,
                                double eps, double e0, const double axis0[3], uint32_t* flags0, uint32_t* flags1,
-                               int32_t* tile_count, int32_t* tile_offset, double* block_part, void* state, int grid,
-                               cudaStream_t s);
+                               int32_t* tile_count, int32_t* tile_offset, double* block_part, unsigned int* barrier,
+                               void* state, int grid, cudaStream_t s);
 
 }  // namespace rvb

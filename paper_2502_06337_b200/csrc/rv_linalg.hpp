@@ -299,6 +299,69 @@ RV_HD bool axis_from_scatter(const double s6[6], double axis[3]) {
   return true;
 }
 
+// Short-latency variant of axis_from_scatter for the device refine loop (rv_coop.cu), where the
+// eigen-solve sits on the critical path of every pass. Same contract (smallest-eigenvalue
+// eigenvector, canonicalised; false when evals[1] <= 1e-10 * evals[2]); not bit-identical to
+// the Eigen restatement (agreement ~1e-15 / relative eigen-gap, the same order as the
+// differences the device's scatter summation order already introduces). Method: closed-form
+// smallest root of the characteristic cubic (trigonometric form), two Newton steps on the cubic,
+// eigenvector = the largest cross product of two rows of M - l3 I (its exact null direction);
+// l1, l2 from the trace and the sum of principal minors.
+RV_HD bool axis_from_scatter_fast(const double s6[6], double axis[3]) {
+  double scale = 0.0;
+  for (int k = 0; k < 6; ++k) scale = fabs(s6[k]) > scale ? fabs(s6[k]) : scale;
+  if (!(scale > 0.0)) return false;  // all-zero scatter: rank deficient
+  const double inv = 1.0 / scale;
+  const double a = s6[0] * inv, b = s6[1] * inv, c = s6[2] * inv, d = s6[3] * inv, e = s6[4] * inv,
+               f = s6[5] * inv;  // M = [[a b c] [b d e] [c e f]]
+  const double c00 = d * f - e * e, c01 = c * e - b * f, c02 = b * e - c * d;
+  const double c11 = a * f - c * c, c12 = b * c - a * e, c22 = a * d - b * b;
+  const double tr = a + d + f, m2 = c00 + c11 + c22, det = a * c00 + b * c01 + c * c02;
+  // smallest eigenvalue: trigonometric solution of the characteristic cubic
+  const double q = tr / 3.0;
+  const double p1 = b * b + c * c + e * e;
+  const double p2 = (a - q) * (a - q) + (d - q) * (d - q) + (f - q) * (f - q) + 2.0 * p1;
+  double l3 = q;
+  if (p2 > 0.0) {
+    const double pp = sqrt(p2 / 6.0), ip = 1.0 / pp;
+    const double B00 = (a - q) * ip, B11 = (d - q) * ip, B22 = (f - q) * ip, B01 = b * ip, B02 = c * ip,
+                 B12 = e * ip;
+    double r = 0.5 * (B00 * (B11 * B22 - B12 * B12) - B01 * (B01 * B22 - B12 * B02) + B02 * (B01 * B12 - B11 * B02));
+    r = r < -1.0 ? -1.0 : (r > 1.0 ? 1.0 : r);
+    const double phi = acos(r) / 3.0;
+    l3 = q + 2.0 * pp * cos(phi + 2.0943951023931954923);  // + 2 pi / 3: smallest root
+  }
+  for (int it = 0; it < 2; ++it) {  // Newton on chi(l) = l^3 - tr l^2 + m2 l - det
+    const double fl = ((l3 - tr) * l3 + m2) * l3 - det;
+    const double dl = (3.0 * l3 - 2.0 * tr) * l3 + m2;
+    if (dl != 0.0) l3 -= fl / dl;
+  }
+  // l1 + l2 = tr - l3, l1 l2 = m2 - l3 (l1 + l2)
+  const double s = tr - l3, pm = m2 - l3 * s;
+  double disc = s * s - 4.0 * pm;
+  disc = disc > 0.0 ? disc : 0.0;
+  const double l1 = 0.5 * (s + sqrt(disc));
+  const double l2 = l1 > 0.0 ? pm / l1 : 0.0;
+  if (l2 <= 1e-10 * (l1 > 1e-300 ? l1 : 1e-300)) return false;  // RankDeficient
+  const double r0[3] = {a - l3, b, c}, r1[3] = {b, d - l3, e}, r2[3] = {c, e, f - l3};
+  double x01[3], x02[3], x12[3];
+  cross3(r0, r1, x01);
+  cross3(r0, r2, x02);
+  cross3(r1, r2, x12);
+  const double q01 = dot3(x01, x01), q02 = dot3(x02, x02), q12 = dot3(x12, x12);
+  const double* best = x01;
+  double qb = q01;
+  if (q02 > qb) {
+    best = x02;
+    qb = q02;
+  }
+  if (q12 > qb) best = x12;
+  double nv[3];
+  normalized3(best, nv);
+  canonicalize3(nv, axis);
+  return true;
+}
+
 // Two-sided Jacobi SVD of a 3x3 (row-major); u, v row-major, singular values descending.
 inline void svd3(const double a[9], double u[9], double v[9]) {
   double w[3][3], U[3][3], V[3][3];

@@ -252,9 +252,17 @@ __device__ __forceinline__ uint2 plan_from_sets(const Arc2& ulo, const Arc2& uhi
   return make_uint2((uint32_t)s0 | ((uint32_t)l0 << 16), nl == 2 ? ((uint32_t)s1 | ((uint32_t)l1 << 16)) : 0u);
 }
 
+// kNB > 0: n_bands <= kNB, ranges kept in registers and entries reserved once per (block, band)
+// (same-address global atomics were the planner's bottleneck); kNB == 0: any band count, one
+// reservation per (warp, band).
+template <int kNB>
 __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, int64_t n) {
   __shared__ unsigned long long s_work[kMaxBands];
-  for (int t = threadIdx.x; t < p.n_bands; t += blockDim.x) s_work[t] = 0;
+  __shared__ int s_cnt[kMaxBands], s_base[kMaxBands];
+  for (int t = threadIdx.x; t < p.n_bands; t += blockDim.x) {
+    s_work[t] = 0;
+    s_cnt[t] = 0;
+  }
   __syncthreads();
   const int64_t lo = b.bounds ? b.bounds[0] : 0, hi = b.bounds ? b.bounds[1] : n;
   const int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -282,45 +290,74 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
   const float pa = (theta_a + kPiF) * inv_step;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
+  const unsigned long long ci = (unsigned long long)(uint32_t)i;
   Arc2 ulo{0.f, kPiF, 0.f, 0.f, 1};  // band 0: Y >= -inf
-  for (int band = 0; band < p.n_bands; ++band) {  // uniform trip count: warp collectives below
-    unsigned long long w = 0;
-    uint2 r = make_uint2(0u, 0u);
-    if (valid) {
-      if (polar) {
-        r = make_uint2((uint32_t)M << 16, 0u);
-        w = (unsigned long long)M;
-      } else {
-        if (band > 0) {
-          const float y0 = p.band_ylo[band];
-          ulo = arc_ge(fmaf(y0, f1[2], f1[1]), fmaf(y0, f2[2], f2[1]), y0, theta_a, kArcDilate);
-        }
-        Arc2 uhi{0.f, 0.f, 0.f, 0.f, 0};  // last band: Y >= +inf is empty
-        if (band < p.n_bands - 1) {
-          const float y1 = p.band_yhi[band];
-          uhi = arc_ge(fmaf(y1, f1[2], f1[1]), fmaf(y1, f2[2], f2[1]), y1, theta_a, -kArcDilate);
-        }
-        r = plan_from_sets(ulo, uhi, pa, inv_step, M, &w);
-      }
+  // ranges of this constraint in band `band` (+ planned pairs into *w)
+  auto plan_band = [&](int band, unsigned long long* w) -> uint2 {
+    if (!valid) return make_uint2(0u, 0u);
+    if (polar) {
+      *w = (unsigned long long)M;
+      return make_uint2((uint32_t)M << 16, 0u);
     }
-    // append the non-empty ranges to the band's entry list (warp-aggregated; r.y != 0 => r.x != 0)
-    const unsigned m0 = __ballot_sync(0xFFFFFFFFu, r.x >= 0x10000u);
+    if (band > 0) {
+      const float y0 = p.band_ylo[band];
+      ulo = arc_ge(fmaf(y0, f1[2], f1[1]), fmaf(y0, f2[2], f2[1]), y0, theta_a, kArcDilate);
+    }
+    Arc2 uhi{0.f, 0.f, 0.f, 0.f, 0};  // last band: Y >= +inf is empty
+    if (band < p.n_bands - 1) {
+      const float y1 = p.band_yhi[band];
+      uhi = arc_ge(fmaf(y1, f1[2], f1[1]), fmaf(y1, f2[2], f2[1]), y1, theta_a, -kArcDilate);
+    }
+    return plan_from_sets(ulo, uhi, pa, inv_step, M, w);
+  };
+  // warp-level bookkeeping of one band: entry offset of this lane inside the warp's block of
+  // entries, reserved in s_cnt (kNB > 0) or directly in the global list (kNB == 0)
+  auto book = [&](int band, uint2 r, unsigned long long w, bool global) -> int {
+    const unsigned m0 = __ballot_sync(0xFFFFFFFFu, r.x >= 0x10000u);  // r.y != 0 => r.x != 0
     const unsigned m1 = __ballot_sync(0xFFFFFFFFu, r.y >= 0x10000u);
     const int total = __popc(m0) + __popc(m1);
-    if (total) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(&b.entry_count[band], total);
-      base = __shfl_sync(0xFFFFFFFFu, base, 0);
-      unsigned long long* ep = b.entries + (int64_t)band * b.entry_cap + base + __popc(m0 & lt_mask) +
-                               __popc(m1 & lt_mask);
-      const unsigned long long ci = (unsigned long long)(uint32_t)i;
-      if (r.x >= 0x10000u) ep[0] = ci | ((unsigned long long)r.x << 32);
-      if (r.y >= 0x10000u) ep[1] = ci | ((unsigned long long)r.y << 32);
-    }
+    int wbase = 0;
+    if (lane == 0 && total) wbase = global ? atomicAdd(&b.entry_count[band], total) : atomicAdd(&s_cnt[band], total);
+    wbase = __shfl_sync(0xFFFFFFFFu, wbase, 0);
     for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xFFFFFFFFu, w, o);
     if (lane == 0 && w) atomicAdd(&s_work[band], w);
+    return wbase + __popc(m0 & lt_mask) + __popc(m1 & lt_mask);
+  };
+  auto emit = [&](int band, uint2 r, int64_t off) {
+    if (r.x >= 0x10000u) {
+      unsigned long long* ep = b.entries + (int64_t)band * b.entry_cap + off;
+      ep[0] = ci | ((unsigned long long)r.x << 32);
+      if (r.y >= 0x10000u) ep[1] = ci | ((unsigned long long)r.y << 32);
+    }
+  };
+  if constexpr (kNB > 0) {
+    uint2 rr[kNB];
+    int woff[kNB];
+#pragma unroll
+    for (int band = 0; band < kNB; ++band) {
+      rr[band] = make_uint2(0u, 0u);
+      woff[band] = 0;
+      if (band < p.n_bands) {  // uniform
+        unsigned long long w = 0;
+        rr[band] = plan_band(band, &w);
+        woff[band] = book(band, rr[band], w, false);
+      }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < p.n_bands; t += blockDim.x)
+      s_base[t] = s_cnt[t] ? atomicAdd(&b.entry_count[t], s_cnt[t]) : 0;
+    __syncthreads();
+#pragma unroll
+    for (int band = 0; band < kNB; ++band)
+      if (band < p.n_bands) emit(band, rr[band], (int64_t)s_base[band] + woff[band]);
+  } else {
+    for (int band = 0; band < p.n_bands; ++band) {  // uniform trip count: warp collectives inside
+      unsigned long long w = 0;
+      const uint2 r = plan_band(band, &w);
+      emit(band, r, book(band, r, w, true));
+    }
+    __syncthreads();
   }
-  __syncthreads();
   for (int t = threadIdx.x; t < p.n_bands; t += blockDim.x)
     if (s_work[t]) atomicAdd(&b.band_work[t], s_work[t]);
 }
@@ -648,8 +685,9 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     const int slot = s_slot;
     const size_t words = (size_t)hb * W;
     if (slot < b.max_slots) {
-      uint32_t* dst = b.partials + (size_t)slot * p.tile_words;
-      for (size_t k = tid; k < words; k += blockDim.x) dst[k] = tile[k];
+      uint4* dst = reinterpret_cast<uint4*>(b.partials + (size_t)slot * p.tile_words);
+      const uint4* src = reinterpret_cast<const uint4*>(tile);
+      for (size_t k = tid; k < (words + 3) / 4; k += blockDim.x) __stcg(dst + k, src[k]);
     } else {  // cannot happen (a CTA visits each band at most once); stay exact anyway
       for (size_t k = tid; k < words; k += blockDim.x)
         if (tile[k]) atomicAdd(&b.grid[(size_t)(r0 + k / W) * G + p.c_min + k % W], tile[k]);
@@ -681,17 +719,33 @@ __global__ void __launch_bounds__(kReduceThreads) vote_reduce_kernel(VotePlan p,
   }
   __syncthreads();
   const int ns = s_n;
-  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
-    uint32_t acc = 0;
+  // 4 words per thread (tile_words is a multiple of 4: slots are 16-byte aligned), 4 slots in flight
+  const int nv = (words + 3) / 4;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    uint4 acc = make_uint4(0u, 0u, 0u, 0u);
+    auto add = [&](int slot) {
+      const uint4 x = __ldcs(reinterpret_cast<const uint4*>(b.partials + (size_t)slot * p.tile_words) + v);
+      acc.x += x.x;
+      acc.y += x.y;
+      acc.z += x.z;
+      acc.w += x.w;
+    };
     if (ns <= 1024) {
-      for (int k = 0; k < ns; ++k) acc += b.partials[(size_t)s_slots[k] * p.tile_words + w];
+      int k = 0;
+#pragma unroll 4
+      for (; k < ns; ++k) add(s_slots[k]);
     } else {
       for (int s = 0; s < used; ++s)
-        if (b.slot_band[s] == band) acc += b.partials[(size_t)s * p.tile_words + w];
+        if (b.slot_band[s] == band) add(s);
     }
-    if (acc) {
-      const int row = r0 + w / p.W, col = p.c_min + w % p.W;
-      b.grid[(size_t)row * p.G + col] += acc;
+    const uint32_t a4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int w = 4 * v + i;
+      if (w < words && a4[i]) {
+        const int row = r0 + w / p.W, col = p.c_min + w % p.W;
+        b.grid[(size_t)row * p.G + col] += a4[i];
+      }
     }
   }
 }
@@ -729,7 +783,10 @@ __global__ void deposit_one_kernel(VotePlan p, const double* z3, const double2* 
 void launch_plan(const VotePlan& p, const VoteBuffers& b, int64_t n, cudaStream_t s) {
   const int threads = 256;
   const int64_t blocks = (n + threads - 1) / threads;
-  plan_kernel<<<(unsigned)blocks, threads, 0, s>>>(p, b, n);
+  if (p.n_bands <= 8)
+    plan_kernel<8><<<(unsigned)blocks, threads, 0, s>>>(p, b, n);
+  else
+    plan_kernel<0><<<(unsigned)blocks, threads, 0, s>>>(p, b, n);
 }
 
 using VoteKernel = void (*)(VotePlan, VoteBuffers, int64_t);
@@ -764,9 +821,9 @@ void launch_vote_banded(const VotePlan& p, const VoteBuffers& b, int64_t n, int 
 }
 
 void launch_vote_reduce(const VotePlan& p, const VoteBuffers& b, cudaStream_t s) {
-  const int words = p.H_max * p.W;
-  const int bx = (words + kReduceThreads - 1) / kReduceThreads;
-  dim3 grid((unsigned)min(bx, 64), (unsigned)p.n_bands);
+  const int vecs = (p.H_max * p.W + 3) / 4;
+  const int bx = (vecs + kReduceThreads - 1) / kReduceThreads;
+  dim3 grid((unsigned)min(bx, 256), (unsigned)p.n_bands);
   vote_reduce_kernel<<<grid, kReduceThreads, 0, s>>>(p, b);
 }
 

@@ -37,7 +37,8 @@ def assert_est_equal(dev, ref: dict):
     (512, 1.05, 1000),   # J not a multiple of 128 -> exact generic kernel
     (97, 1.3, 640),      # odd grid, wide extent
     (200, 0.9, 1024),    # extent < 1: clamped cells
-    (1024, 1.05, 4096),  # finer grid, more bands
+    (1024, 1.05, 4096),  # finer grid, more bands (run-time fixed-point shift S=11)
+    (1100, 0.95, 1024),  # clamped cells with the run-time shift
 ])
 def test_accumulate_bit_exact(ctx, port, grid, extent, samples):
     rng = np.random.default_rng(grid + samples)
