@@ -20,11 +20,28 @@
 namespace rvb {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kPerThread = 4;
-constexpr int kTile = kThreads * kPerThread;  // 1024 constraints = 32 flag words per tile
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kTile = 1024;                  // compaction granularity (compact_kernel): 32 flag words
+constexpr int kPerTile = kTile / kThreads;   // elements per thread per tile
+constexpr int kChunk = 2;                    // tiles whose loads are issued together
 
 using State = CoopState;
+
+#ifdef RV_COOP_TRACE  // dev instrumentation: block 0's phase timestamps (globaltimer, ns)
+__device__ unsigned long long g_trace[8192];
+__device__ unsigned int g_trace_n;
+__device__ __forceinline__ void trace(int tag) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    const unsigned k = atomicAdd(&g_trace_n, 1u);
+    if (k < 8192) g_trace[k] = (t << 4) | (unsigned long long)tag;
+  }
+}
+#else
+__device__ __forceinline__ void trace(int) {}
+#endif
 
 struct CoopArgs {
   const double* zx;
@@ -50,29 +67,38 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// Grid barrier: release on arrival, acquire on the generation flip (no L1 invalidation needed:
-// the only cross-block data, the block partials and tile counts, are read with ld.global.cg).
-__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks) {
+// Grid barrier on a monotonically increasing arrival counter (zeroed before the launch): arrive
+// with a release-add, wait until the counter reaches this pass's target with acquire loads. No
+// L1 invalidation is needed: the only cross-block data (block partials, tile counts) are read
+// with ld.global.cg / atomics.
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned int gen;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
-    unsigned int arrived;
-    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(bar) : "memory");
-    if (arrived == nblocks - 1) {
-      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(gen + 1) : "memory");
-    } else {
-      unsigned int g = gen;
-      while (g == gen) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
-    }
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned int g;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar) : "memory");
+    } while (g < target);
   }
   __syncthreads();
 }
 
+// Fixed-shape block reduction of 8 per-thread values into warp 0 lane 0 (returned in v there).
+__device__ __forceinline__ void block_reduce8(double (&v)[8], double (*s_red)[kWarps]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = warp_sum_d(v[k]);
+  if (lane == 0)
+    for (int k = 0; k < 8; ++k) s_red[k][warp] = v[k];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = warp_sum_d(lane < kWarps ? s_red[k][lane] : 0.0);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
-  __shared__ double s_red[8][kThreads / 32];
-  __shared__ int s_cnt[kThreads / 32];
+  __shared__ double s_red[8][kWarps];
   __shared__ double s_next[4];  // next axis (3) + next e
   __shared__ int s_done;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -81,114 +107,86 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
   double cls_axis[3] = {a.axis0[0], a.axis0[1], a.axis0[2]};
   double e = a.mode == 1 ? (a.e0 > a.eps ? a.e0 : a.eps) : a.eps;
   int slot = 0, refits = 0;
+  unsigned int bar_target = 0;
   bool have_prev = false;
   for (;;) {
     // ---- classify pass over this block's tiles ----
+    trace(1);
     uint32_t* flags = slot == 0 ? a.flags0 : a.flags1;
     const uint32_t* prev = have_prev ? (slot == 0 ? a.flags1 : a.flags0) : nullptr;
-    double sc[6] = {0, 0, 0, 0, 0, 0};
-    long long cnt = 0;
-    int diff = 0;
-    for (int64_t t = t_begin; t < t_end; ++t) {
-      const int64_t base = t * kTile;
-      double z[kPerThread][3];
-#pragma unroll
-      for (int r = 0; r < kPerThread; ++r) {  // all loads first
-        const int64_t i = base + r * kThreads + tid;
-        z[r][0] = z[r][1] = z[r][2] = 0.0;
-        if (i < a.n) {
-          z[r][0] = a.zx[i];
-          z[r][1] = a.zy[i];
-          z[r][2] = a.zz[i];
-        }
-      }
-      int tcnt = 0;
-#pragma unroll
-      for (int r = 0; r < kPerThread; ++r) {
-        const int64_t i = base + r * kThreads + tid;
-        const double z0 = z[r][0], z1 = z[r][1], z2 = z[r][2];
-        bool in = false;
-        if (i < a.n) {
-          const double d = xa(xa(xm(cls_axis[0], z0), xm(cls_axis[1], z1)), xm(cls_axis[2], z2));
-          in = fabs(d) < e;
-        }
-        const unsigned word = __ballot_sync(0xFFFFFFFFu, in);
-        const int64_t w0 = base + r * kThreads + warp * 32;
-        if (lane == 0 && w0 < a.n) {
-          flags[w0 >> 5] = word;
-          if (prev && prev[w0 >> 5] != word) diff = 1;
-        }
-        tcnt += __popc(word);
-        if (in) {
-          sc[0] = xa(sc[0], xm(z0, z0));
-          sc[1] = xa(sc[1], xm(z0, z1));
-          sc[2] = xa(sc[2], xm(z0, z2));
-          sc[3] = xa(sc[3], xm(z1, z1));
-          sc[4] = xa(sc[4], xm(z1, z2));
-          sc[5] = xa(sc[5], xm(z2, z2));
-        }
-      }
-      if (lane == 0) s_cnt[warp] = tcnt;
-      __syncthreads();
-      if (tid == 0) {
-        int c = 0;
-        for (int w = 0; w < kThreads / 32; ++w) c += s_cnt[w];
-        __stcg(a.tile_count + t, c);
-        cnt += c;
-      }
-      __syncthreads();
-    }
-    // block partials (fixed-shape tree): scatter[6], diff, count
-    diff = __any_sync(0xFFFFFFFFu, diff);
-#pragma unroll
-    for (int k = 0; k < 6; ++k) sc[k] = warp_sum_d(sc[k]);
-    if (lane == 0) {
-      for (int k = 0; k < 6; ++k) s_red[k][warp] = sc[k];
-      s_red[6][warp] = (double)diff;
-    }
+    for (int64_t t = t_begin + tid; t < t_end; t += kThreads) a.tile_count[t] = 0;
     __syncthreads();
+    double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // scatter[6], diff, count
+    int diff = 0, cnt = 0;
+    for (int64_t t0 = t_begin; t0 < t_end; t0 += kChunk) {
+      double z[kChunk][kPerTile][3];
+#pragma unroll
+      for (int c = 0; c < kChunk; ++c)  // all loads of the chunk first
+#pragma unroll
+        for (int r = 0; r < kPerTile; ++r) {
+          const int64_t i = (t0 + c) * kTile + r * kThreads + tid;
+          const bool ok = t0 + c < t_end && i < a.n;
+          z[c][r][0] = ok ? a.zx[i] : 0.0;
+          z[c][r][1] = ok ? a.zy[i] : 0.0;
+          z[c][r][2] = ok ? a.zz[i] : 0.0;
+        }
+#pragma unroll
+      for (int c = 0; c < kChunk; ++c) {
+        if (t0 + c >= t_end) break;  // uniform
+#pragma unroll
+        for (int r = 0; r < kPerTile; ++r) {
+          const int64_t i = (t0 + c) * kTile + r * kThreads + tid;
+          const double z0 = z[c][r][0], z1 = z[c][r][1], z2 = z[c][r][2];
+          bool in = false;
+          if (i < a.n) {
+            const double d = xa(xa(xm(cls_axis[0], z0), xm(cls_axis[1], z1)), xm(cls_axis[2], z2));
+            in = fabs(d) < e;
+          }
+          const unsigned word = __ballot_sync(0xFFFFFFFFu, in);
+          const int64_t w0 = (t0 + c) * kTile + r * kThreads + warp * 32;
+          if (lane == 0 && w0 < a.n) {
+            flags[w0 >> 5] = word;
+            if (prev && prev[w0 >> 5] != word) diff = 1;
+            if (word) atomicAdd(a.tile_count + t0 + c, __popc(word));
+          }
+          if (in) {
+            ++cnt;
+            v[0] = xa(v[0], xm(z0, z0));
+            v[1] = xa(v[1], xm(z0, z1));
+            v[2] = xa(v[2], xm(z0, z2));
+            v[3] = xa(v[3], xm(z1, z1));
+            v[4] = xa(v[4], xm(z1, z2));
+            v[5] = xa(v[5], xm(z2, z2));
+          }
+        }
+      }
+    }
+    v[6] = (double)__any_sync(0xFFFFFFFFu, diff);  // reduced as a sum: > 0 <=> any block word differs
+    v[7] = (double)cnt;
+    trace(2);
+    block_reduce8(v, s_red);
     if (tid == 0) {
       double* bp = a.block_part + (size_t)blockIdx.x * 8;
-      for (int k = 0; k < 6; ++k) {
-        double v = 0.0;
-        for (int w = 0; w < kThreads / 32; ++w) v = xa(v, s_red[k][w]);
-        __stcg(bp + k, v);
-      }
-      int d = 0;
-      for (int w = 0; w < kThreads / 32; ++w) d |= s_red[6][w] != 0.0;
-      __stcg(bp + 6, (double)d);
-      __stcg(bp + 7, (double)cnt);
+      for (int k = 0; k < 8; ++k) __stcg(bp + k, v[k]);
     }
-    grid_barrier(a.barrier, gridDim.x);
+    trace(3);
+    bar_target += gridDim.x;
+    grid_barrier(a.barrier, bar_target);
+    trace(4);
     // ---- every block: reduce all partials in the same fixed order, decide ----
-    {
-      double v[6] = {0, 0, 0, 0, 0, 0};
-      double vc = 0.0;
-      int vd = 0;
-      for (unsigned b = tid; b < gridDim.x; b += blockDim.x) {
-        const double* bp = a.block_part + (size_t)b * 8;
-        for (int k = 0; k < 6; ++k) v[k] = xa(v[k], __ldcg(bp + k));
-        vd |= __ldcg(bp + 6) != 0.0;
-        vc = xa(vc, __ldcg(bp + 7));
-      }
-      for (int k = 0; k < 6; ++k) v[k] = warp_sum_d(v[k]);
-      vc = warp_sum_d(vc);
-      vd = __any_sync(0xFFFFFFFFu, vd);
-      __syncthreads();  // s_red reuse
-      if (lane == 0) {
-        for (int k = 0; k < 6; ++k) s_red[k][warp] = v[k];
-        s_red[6][warp] = (double)vd;
-        s_red[7][warp] = vc;
-      }
-      __syncthreads();
+    // warp k reduces value k over all block partials (fixed order: lane-strided, then the tree)
+    if (warp < 8) {
+      double acc = 0.0;
+#pragma unroll 4
+      for (unsigned b = lane; b < gridDim.x; b += 32) acc = xa(acc, __ldcg(a.block_part + (size_t)b * 8 + warp));
+      acc = warp_sum_d(acc);
+      if (lane == 0) s_red[warp][0] = acc;
     }
+    __syncthreads();
+    for (int k = 0; k < 8; ++k) v[k] = s_red[k][0];
+    trace(5);
     if (tid == 0) {
-      double tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int w = 0; w < kThreads / 32; ++w) {
-        for (int k = 0; k < 6; ++k) tot[k] = xa(tot[k], s_red[k][w]);
-        if (s_red[6][w] != 0.0) tot[6] = 1.0;
-        tot[7] = xa(tot[7], s_red[7][w]);
-      }
+      const double* tot = v;
       const long long count = (long long)tot[7];
       const bool differs = tot[6] != 0.0;
       int done = 0, rank_deficient = 0;
@@ -239,6 +237,7 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
       s_done = done;
     }
     __syncthreads();
+    trace(6);
     const int done = s_done;
     if (done) {
       if (a.mode == 0 && blockIdx.x == 0) {  // compaction offsets of the final set (tile order)
@@ -279,7 +278,7 @@ int coop_refine_grid(int sms) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coop_refine_kernel, kThreads, 0);
   if (per_sm < 1) per_sm = 1;
-  return sms * (per_sm < 4 ? per_sm : 4);
+  return sms * (per_sm < 2 ? per_sm : 2);
 }
 
 int coop_tiles(int64_t n) { return (int)((n + kTile - 1) / kTile); }
@@ -315,5 +314,22 @@ cudaError_t launch_coop_refine(const double* zx, const double* zy, const double*
 }
 
 size_t coop_state_bytes() { return sizeof(State); }
+
+}  // namespace rvb
+
+#ifdef RV_COOP_TRACE
+extern "C" int rv_debug_coop_trace(unsigned long long* out, int max) {
+  unsigned int n = 0;
+  cudaMemcpyFromSymbol(&n, rvb::g_trace_n, sizeof n);
+  if (n > 8192) n = 8192;
+  if ((int)n > max) n = (unsigned)max;
+  cudaMemcpyFromSymbol(out, rvb::g_trace, sizeof(unsigned long long) * n);
+  const unsigned int zero = 0;
+  cudaMemcpyToSymbol(rvb::g_trace_n, &zero, sizeof zero);
+  return (int)n;
+}
+#endif
+
+namespace rvb {
 
 }  // namespace rvb

@@ -303,10 +303,10 @@ RV_HD bool axis_from_scatter(const double s6[6], double axis[3]) {
 // eigen-solve sits on the critical path of every pass. Same contract (smallest-eigenvalue
 // eigenvector, canonicalised; false when evals[1] <= 1e-10 * evals[2]); not bit-identical to
 // the Eigen restatement (agreement ~1e-15 / relative eigen-gap, the same order as the
-// differences the device's scatter summation order already introduces). Method: closed-form
-// smallest root of the characteristic cubic (trigonometric form), two Newton steps on the cubic,
-// eigenvector = the largest cross product of two rows of M - l3 I (its exact null direction);
-// l1, l2 from the trace and the sum of principal minors.
+// differences the device's scatter summation order already introduces). Method: smallest root of
+// the characteristic cubic by monotone Newton from 0, eigenvector = the largest cross product of
+// two rows of M - l3 I (its exact null direction); l1, l2 from the trace and the sum of principal
+// minors. No transcendental calls: a short dependency chain for the per-pass device decision.
 RV_HD bool axis_from_scatter_fast(const double s6[6], double axis[3]) {
   double scale = 0.0;
   for (int k = 0; k < 6; ++k) scale = fabs(s6[k]) > scale ? fabs(s6[k]) : scale;
@@ -317,24 +317,17 @@ RV_HD bool axis_from_scatter_fast(const double s6[6], double axis[3]) {
   const double c00 = d * f - e * e, c01 = c * e - b * f, c02 = b * e - c * d;
   const double c11 = a * f - c * c, c12 = b * c - a * e, c22 = a * d - b * b;
   const double tr = a + d + f, m2 = c00 + c11 + c22, det = a * c00 + b * c01 + c * c02;
-  // smallest eigenvalue: trigonometric solution of the characteristic cubic
-  const double q = tr / 3.0;
-  const double p1 = b * b + c * c + e * e;
-  const double p2 = (a - q) * (a - q) + (d - q) * (d - q) + (f - q) * (f - q) + 2.0 * p1;
-  double l3 = q;
-  if (p2 > 0.0) {
-    const double pp = sqrt(p2 / 6.0), ip = 1.0 / pp;
-    const double B00 = (a - q) * ip, B11 = (d - q) * ip, B22 = (f - q) * ip, B01 = b * ip, B02 = c * ip,
-                 B12 = e * ip;
-    double r = 0.5 * (B00 * (B11 * B22 - B12 * B12) - B01 * (B01 * B22 - B12 * B02) + B02 * (B01 * B12 - B11 * B02));
-    r = r < -1.0 ? -1.0 : (r > 1.0 ? 1.0 : r);
-    const double phi = acos(r) / 3.0;
-    l3 = q + 2.0 * pp * cos(phi + 2.0943951023931954923);  // + 2 pi / 3: smallest root
-  }
-  for (int it = 0; it < 2; ++it) {  // Newton on chi(l) = l^3 - tr l^2 + m2 l - det
+  // smallest eigenvalue: Newton on chi(l) = l^3 - tr l^2 + m2 l - det from l = 0. M is PSD, so
+  // 0 <= l3 and chi is increasing and concave on [0, l3]: the iterates increase monotonically to
+  // l3 (no overshoot), quadratically once l3 << l2 (one or two steps in the refine loop).
+  double l3 = 0.0;
+  for (int it = 0; it < 32; ++it) {
     const double fl = ((l3 - tr) * l3 + m2) * l3 - det;
     const double dl = (3.0 * l3 - 2.0 * tr) * l3 + m2;
-    if (dl != 0.0) l3 -= fl / dl;
+    if (!(dl > 0.0)) break;
+    const double nl = l3 - fl / dl;
+    if (!(nl > l3)) break;  // converged (monotone sequence stopped increasing)
+    l3 = nl;
   }
   // l1 + l2 = tr - l3, l1 l2 = m2 - l3 (l1 + l2)
   const double s = tr - l3, pm = m2 - l3 * s;
