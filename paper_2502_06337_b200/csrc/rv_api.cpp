@@ -120,6 +120,7 @@ struct rv_context {
   // classify / refine
   DBuf flagsA, flagsB, bcount, bscatter, bdiff, boffA, boffB, cls_result, compact_out;
   DBuf coop_part, coop_state, coop_bar;  // device-resident refine_loop / anneal_axis (rv_coop.cu)
+  DBuf peak_out;                         // chained solve: start axis from the peak (PeakOut)
   int coop_grid = 0;
   // angles / support
   DBuf bins, raw, angle_counts, angle_sums, angle_result, sup_counts, sup_result, band_flagsA, band_flagsB,
@@ -132,6 +133,9 @@ struct rv_context {
   // pinned host scalars
   void* pinned = nullptr;
   std::vector<std::vector<int32_t>> results;
+  std::vector<int32_t> spare;       // recycled inlier vector (no page faults on the hot path)
+  int32_t* inl_host = nullptr;      // mapped pinned buffer: the compaction writes the inlier list here
+  size_t inl_cap = 0;
 
   // "last block done" counters of the single-pass reductions: must start at zero; every kernel
   // that uses one resets it before exiting.
@@ -425,8 +429,9 @@ std::vector<Peak> find_peaks_dev(rv_context* c, const uint32_t* grid, int G, dou
 std::pair<const uint32_t*, std::vector<Peak>> vote_and_peak(rv_context* c, const double* zx, const double* zy,
                                                             const double* zz, int64_t n, const rv_config& cfg,
                                                             uint32_t min_votes, bool allow_no_peak,
-                                                            const uint32_t* prevoted = nullptr) {
-  for (int attempt = 0; attempt < 2; ++attempt) {
+                                                            const uint32_t* prevoted = nullptr,
+                                                            int first_attempt = 0) {
+  for (int attempt = first_attempt; attempt < 2; ++attempt) {
     const uint32_t* grid = (attempt == 0 && prevoted)
                                ? prevoted
                                : vote(c, zx, zy, zz, n, cfg.grid, cfg.extent, cfg.theta_samples, attempt == 1);
@@ -560,30 +565,56 @@ Cls classify_dev(rv_context* c, const ConstraintSet& cs, const double axis[3], d
 // launch (rv_coop.cu): every classify pass, scatter reduction and 3x3 eigen-solve stays on the
 // device; the host reads the final state once. mode 0 returns the final classification with its
 // tile offsets ready for compaction; mode 1 returns the annealed axis in `axis`.
-Cls coop_refine_dev(rv_context* c, const ConstraintSet& cs, double axis[3], int mode, double e0, const rv_config& cfg,
-                    int* passes = nullptr) {
+// Mapped pinned inlier buffer (zero-copy target of the compaction), grow-only.
+int32_t* inlier_host_buffer(rv_context* c, size_t n) {
+  if (c->inl_cap < n) {
+    if (c->inl_host) {
+      sync(c);
+      cudaFreeHost(c->inl_host);
+      c->inl_host = nullptr;
+      c->inl_cap = 0;
+    }
+    const size_t cap = std::max<size_t>(n, 1 << 16);
+    void* p = nullptr;
+    ck(cudaHostAlloc(&p, cap * sizeof(int32_t), cudaHostAllocMapped | cudaHostAllocPortable), "pinned inliers");
+    c->inl_host = static_cast<int32_t*>(p);
+    c->inl_cap = cap;
+  }
+  return c->inl_host;
+}
+
+// Launches the cooperative loop; the final state stays on the device (CoopState*).
+CoopState* coop_refine_launch(rv_context* c, const ConstraintSet& cs, const double* axis, const double* axis_dev,
+                              int mode, double e0, const rv_config& cfg, uint32_t** flags, int32_t** offsets,
+                              CoopState* state_dst = nullptr) {
   StageScope sc(c, kRefine);
   if (c->coop_grid == 0) c->coop_grid = coop_refine_grid(c->sms);
   const int nt = std::max(1, coop_tiles(cs.n));
   const size_t words = (size_t)(cs.n + 31) / 32 + 32;
-  Cls r;
   uint32_t* fa = c->flagsA.get<uint32_t>(words);
   uint32_t* fb = c->flagsB.get<uint32_t>(words);
   int32_t* tcount = c->bcount.get<int32_t>(nt);
   int32_t* toff = c->boffA.get<int32_t>(nt);
   double* part = c->coop_part.get<double>((size_t)c->coop_grid * 8);
-  CoopState* dst = c->coop_state.get<CoopState>(1);
-  ck(launch_coop_refine(cs.zx, cs.zy, cs.zz, cs.n, mode, cfg.refine ? 1 : 0, cfg.epsilon, e0, axis, fa, fb, tcount,
-                        toff, part, c->coop_bar.get<unsigned int>(2), dst, c->coop_grid, c->st),
+  CoopState* dst = state_dst ? state_dst : c->coop_state.get<CoopState>(1);
+  ck(launch_coop_refine(cs.zx, cs.zy, cs.zz, cs.n, mode, cfg.refine ? 1 : 0, cfg.epsilon, e0, axis, axis_dev, fa, fb,
+                        tcount, toff, part, c->coop_bar.get<unsigned int>(2), dst, c->coop_grid, c->st),
      "coop refine launch");
   count_launch(c);
+  if (flags) *flags = fa;  // refine_loop: final bitmask in flags0
+  if (offsets) *offsets = toff;
+  return dst;
+}
+
+Cls coop_refine_dev(rv_context* c, const ConstraintSet& cs, double axis[3], int mode, double e0, const rv_config& cfg,
+                    int* passes = nullptr) {
+  Cls r;
+  CoopState* dst = coop_refine_launch(c, cs, axis, nullptr, mode, e0, cfg, &r.flags, &r.offsets);
   static_assert(sizeof(CoopState) <= 4096, "pinned scratch");
   CoopState* h = reinterpret_cast<CoopState*>(c->pinned);
   ck(cudaMemcpyAsync(h, dst, sizeof(CoopState), cudaMemcpyDeviceToHost, c->st), "coop state D2H");
   sync(c);
   std::memcpy(axis, h->axis, sizeof(double) * 3);
-  r.flags = h->slot == 0 ? fa : fb;
-  r.offsets = toff;
   r.count = h->count;
   r.differs = false;
   std::memcpy(r.scatter, h->scatter, sizeof r.scatter);
@@ -924,6 +955,10 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
 // estimate_single from a preprocessed constraint set (identity shortcuts already handled).
 Estimate finish_single(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
                        const uint32_t* prevoted);
+Estimate finish_single_stepped(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
+                               const uint32_t* prevoted, int first_attempt);
+Estimate rescue_single(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
+                       const uint32_t* grid, Estimate est);
 
 // estimate_single (estimator.cpp:320-371) over device-resident correspondences.
 Estimate estimate_single_dev(rv_context* c, const double* d_corrs, int64_t n, const rv_config& cfg) {
@@ -951,9 +986,93 @@ Estimate estimate_single_host(rv_context* c, const double* h_corrs, int64_t n, c
   return finish_single(c, pv.pre, pv.d_corrs, cfg, pv.grid);
 }
 
+// estimate_single after preprocess (estimator.cpp:320-371), chained on the device: vote ->
+// argmax -> start axis (peak_axis_kernel) -> refine_loop (one cooperative launch) -> compaction
+// -> angle histogram + circular mean sums, then ONE summary read-back (and the inlier list). The
+// host only validates and finishes (atan2, Rodrigues). Rare cases -- a failed exactness guard
+// (grid sum != N*J), or the rescue path -- continue on the host-stepped path below.
 Estimate finish_single(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
                        const uint32_t* prevoted) {
-  const auto [grid, peaks] = vote_and_peak(c, pre.cs.zx, pre.cs.zy, pre.cs.zz, pre.cs.n, cfg, 1, false, prevoted);
+  if (cfg.angle_bins < 8) fail(RV_ERR_INVALID_CONFIG, "angle histogram needs bin_count >= 8");
+  const ConstraintSet& cs = pre.cs;
+  const uint32_t* grid = prevoted ? prevoted
+                                  : vote(c, cs.zx, cs.zy, cs.zz, cs.n, cfg.grid, cfg.extent, cfg.theta_samples);
+  // every scalar the host needs lands in one device struct: a single read-back
+  struct Summary {
+    PeakOut pk;
+    CoopState st;
+    unsigned long long counts[2];
+    double angle[4];
+  };
+  Summary* dsum = c->peak_out.get<Summary>(1);
+  PeakOut* pk = &dsum->pk;
+  {
+    StageScope sc(c, kPeaks);
+    unsigned long long* keys = c->arg_keys.get<unsigned long long>(2 * argmax_block_count());
+    unsigned long long* okey = c->arg_out.get<unsigned long long>(2);
+    launch_argmax(grid, cfg.grid, nullptr, 0, cfg.suppression_radius, keys, okey, c->done_ptr(), c->st);
+    launch_peak_axis(okey, grid, cfg.grid, cfg.extent, 1u, pk, c->st);
+    count_launch(c, 2);
+  }
+  uint32_t* flags = nullptr;
+  int32_t* offs = nullptr;
+  CoopState* st = coop_refine_launch(c, cs, nullptr, pk->axis, 0, 0.0, cfg, &flags, &offs, &dsum->st);
+  int32_t* idx = c->compact_out.get<int32_t>((size_t)std::max<int64_t>(cs.n, 1));
+  unsigned long long* cnt = dsum->counts;
+  double* res = dsum->angle;
+  {
+    StageScope sc(c, kAngles);
+    int32_t* hidx = inlier_host_buffer(c, (size_t)std::max<int64_t>(cs.n, 1));
+    launch_compact_flags(flags, cs.n, cs.kept, offs, idx, c->st);
+    uint32_t* bins = c->bins.get<uint32_t>(cfg.angle_bins);
+    double* raw = c->raw.get<double>((size_t)std::max<int64_t>(cs.n, 1));
+    ck(cudaMemsetAsync(bins, 0, sizeof(uint32_t) * cfg.angle_bins, c->st), "memset bins");
+    ck(cudaMemsetAsync(cnt, 0, 16, c->st), "memset counts");
+    // the angle vote reads the inlier list coalesced and also streams it to mapped host memory
+    launch_vote_angles_k(nullptr, d_corrs, idx, cs.n, cfg.angle_bins, cfg.tau_deg, bins, raw, cnt, c->st, st->axis,
+                         &st->count, hidx);
+    launch_peak_angle_k(bins, cfg.angle_bins, raw, cs.n, c->angle_sums.get<double>(2 * 296), res, c->done_ptr(),
+                        c->st, &st->count);
+    count_launch(c, 3);
+  }
+  // one summary read-back
+  static_assert(sizeof(Summary) <= 4096, "pinned scratch");
+  Summary* h = reinterpret_cast<Summary*>(c->pinned);
+  ck(cudaMemcpyAsync(h, dsum, sizeof(Summary), cudaMemcpyDeviceToHost, c->st), "summary D2H");
+  sync(c);
+  const Summary sm = *h;
+  if (sm.pk.total != (unsigned long long)cs.n * (unsigned long long)cfg.theta_samples) {
+    c->times.vote_guard_reruns += 1;  // exactness guard: redo with the generic exact vote
+    return finish_single_stepped(c, pre, d_corrs, cfg, nullptr, 1);
+  }
+  if (!sm.pk.ok) fail(RV_ERR_NO_PEAK, "no accumulator cell reaches min_votes");
+  Estimate est;
+  {  // angle_dev's finish (angles.cpp:46-90)
+    if (sm.st.count > 0 && sm.counts[0] == 0) fail(RV_ERR_NO_VOTES, "no correspondence produced an angle vote");
+    if (sm.st.count == 0) fail(RV_ERR_NO_VOTES, "no correspondence produced an angle vote");
+    const double s = sm.angle[0], co = sm.angle[1], center = sm.angle[3];
+    double angle = center;
+    if (cfg.refine && !(s == 0.0 && co == 0.0)) {
+      angle = std::atan2(s, co);
+      if (angle <= -kPiD) angle += 2.0 * kPiD;
+    }
+    est.angle = angle;
+  }
+  std::memcpy(est.axis, sm.st.axis, sizeof est.axis);
+  rodrigues3(est.axis, est.angle, est.R);
+  est.votes = sm.pk.votes;
+  est.inliers = std::move(c->spare);  // the compaction already wrote the list to mapped memory
+  est.inliers.assign(c->inl_host, c->inl_host + sm.st.count);
+  const double chance = cfg.epsilon * (double)cs.n;
+  if (cfg.refine && (double)est.inliers.size() < 3.0 * chance) est = rescue_single(c, pre, d_corrs, cfg, grid, est);
+  return est;
+}
+
+// The host-stepped solve (same semantics): each stage reads its scalars back before the next.
+Estimate finish_single_stepped(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
+                               const uint32_t* prevoted, int first_attempt) {
+  const auto [grid, peaks] =
+      vote_and_peak(c, pre.cs.zx, pre.cs.zy, pre.cs.zz, pre.cs.n, cfg, 1, false, prevoted, first_attempt);
   Estimate est;
   {  // estimate_from_peak (estimator.cpp:94-101)
     double A, B, b[3], axis[3];
@@ -964,21 +1083,26 @@ Estimate finish_single(rv_context* c, const PreResult& pre, const double* d_corr
     est = build_estimate_dev(c, pre.cs, axis, cl, peaks[0].votes, d_corrs, cfg);
   }
   const double chance = cfg.epsilon * (double)pre.cs.n;
-  if (cfg.refine && (double)est.inliers.size() < 3.0 * chance) {  // estimator.cpp:352-368
-    int64_t best = model_support_dev(c, pre.cs, d_corrs, est, cfg, nullptr).coherent;
-    for (const auto& ax : rescue_axes_dev(c, grid, pre.cs, cfg)) {
-      Estimate cand;
-      try {
-        cand = build_candidate_dev(c, ax.data(), grid, pre.cs, d_corrs, cfg);
-      } catch (const RvError& e) {
-        if (e.st == RV_ERR_NO_VOTES) continue;
-        throw;
-      }
-      const int64_t coh = model_support_dev(c, pre.cs, d_corrs, cand, cfg, nullptr).coherent;
-      if (coh > best) {
-        best = coh;
-        est = std::move(cand);
-      }
+  if (cfg.refine && (double)est.inliers.size() < 3.0 * chance) est = rescue_single(c, pre, d_corrs, cfg, grid, est);
+  return est;
+}
+
+// Rescue (estimator.cpp:352-368): blurred peaks + LS-all annealed candidates, best model support.
+Estimate rescue_single(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
+                       const uint32_t* grid, Estimate est) {
+  int64_t best = model_support_dev(c, pre.cs, d_corrs, est, cfg, nullptr).coherent;
+  for (const auto& ax : rescue_axes_dev(c, grid, pre.cs, cfg)) {
+    Estimate cand;
+    try {
+      cand = build_candidate_dev(c, ax.data(), grid, pre.cs, d_corrs, cfg);
+    } catch (const RvError& e) {
+      if (e.st == RV_ERR_NO_VOTES) continue;
+      throw;
+    }
+    const int64_t coh = model_support_dev(c, pre.cs, d_corrs, cand, cfg, nullptr).coherent;
+    if (coh > best) {
+      best = coh;
+      est = std::move(cand);
     }
   }
   return est;
@@ -1291,6 +1415,7 @@ void rv_context_destroy(rv_context* c) {
   for (auto e : c->chunk_events) cudaEventDestroy(e);
   if (c->copy_st) cudaStreamDestroy(c->copy_st);
   if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->inl_host) cudaFreeHost(c->inl_host);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
 }
@@ -1315,12 +1440,17 @@ rv_status rv_context_stage_times(const rv_context* c, rv_stage_times* out) {
   return RV_OK;
 }
 
+static void recycle_results(rv_context* c) {
+  if (!c->results.empty() && c->results[0].capacity() > c->spare.capacity()) c->spare = std::move(c->results[0]);
+  c->results.clear();
+}
+
 rv_status rv_estimate_single_device(rv_context* c, const double* d_corrs, int64_t n, const rv_config* cfg,
                                     rv_estimate* out) {
   if (!c || !cfg || !out || (n > 0 && !d_corrs)) return RV_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
     cudaSetDevice(c->device);
-    c->results.clear();
+    recycle_results(c);
     Estimate e = estimate_single_dev(c, d_corrs, n, *cfg);
     to_c(e, out, seconds_since(c));
     c->results.push_back(std::move(e.inliers));
@@ -1331,7 +1461,7 @@ rv_status rv_estimate_single(rv_context* c, const double* corrs, int64_t n, cons
   if (!c || !cfg || !out || (n > 0 && !corrs)) return RV_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
     cudaSetDevice(c->device);
-    c->results.clear();
+    recycle_results(c);
     if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
     Estimate e = estimate_single_host(c, corrs, n, *cfg);
     to_c(e, out, seconds_since(c));

@@ -53,6 +53,7 @@ struct CoopArgs {
   double eps;
   double e0;
   double axis0[3];
+  const double* axis0_dev;  // optional: start axis on the device (PeakOut.axis)
   uint32_t* flags0;
   uint32_t* flags1;
   int32_t* tile_count;
@@ -105,6 +106,11 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
   const int64_t ntiles = (a.n + kTile - 1) / kTile;
   const int64_t t_begin = ntiles * blockIdx.x / gridDim.x, t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
   double cls_axis[3] = {a.axis0[0], a.axis0[1], a.axis0[2]};
+  if (a.axis0_dev) {
+    cls_axis[0] = a.axis0_dev[0];
+    cls_axis[1] = a.axis0_dev[1];
+    cls_axis[2] = a.axis0_dev[2];
+  }
   double e = a.mode == 1 ? (a.e0 > a.eps ? a.e0 : a.eps) : a.eps;
   int slot = 0, refits = 0;
   unsigned int bar_target = 0;
@@ -240,6 +246,10 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
     trace(6);
     const int done = s_done;
     if (done) {
+      if (a.mode == 0 && slot == 1) {  // the final set always ends in flags0 (own tiles' words)
+        const int64_t w_lo = t_begin * (kTile / 32), w_hi = min(t_end * (kTile / 32), (a.n + 31) / 32);
+        for (int64_t w = w_lo + tid; w < w_hi; w += kThreads) a.flags0[w] = a.flags1[w];
+      }
       if (a.mode == 0 && blockIdx.x == 0) {  // compaction offsets of the final set (tile order)
         __shared__ long long s_tot[kThreads];
         const int64_t per = (ntiles + kThreads - 1) / kThreads;
@@ -272,7 +282,61 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
   }
 }
 
+// estimate_from_peak on the device (single thread): argmax key -> peak cell, interpolate_peak
+// (estimator.cpp:32-47: 3x3 vote-weighted centroid, dy outer / dx inner), backproject
+// (voting.cpp:172-174), canonicalize (geom.cpp:34). Same op order as the host (this TU is
+// compiled without FMA contraction), so the start axis is bit-identical to the host path's.
+__global__ void peak_axis_kernel(const unsigned long long* okey, const uint32_t* grid, int G, double E,
+                                 uint32_t min_votes, PeakOut* out) {
+  const unsigned long long key = okey[0];
+  PeakOut r;
+  r.total = okey[1];
+  r.ok = 0;
+  r.ix = r.iy = 0;
+  r.votes = 0;
+  r.A = r.B = 0.0;
+  r.axis[0] = r.axis[1] = 0.0;
+  r.axis[2] = -1.0;
+  const uint32_t best = (uint32_t)(key >> 32);
+  if (key != 0 && best >= min_votes) {
+    const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu);
+    const int iy = (int)idx / G, ix = (int)idx % G;
+    const double cw = 2.0 * E / G;
+    double wsum = 0.0, asum = 0.0, bsum = 0.0;
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int x = ix + dx, y = iy + dy;
+        if (x < 0 || x >= G || y < 0 || y >= G) continue;
+        const double wv = grid[(size_t)y * G + x];
+        const double cA = -E + (x + 0.5) * cw, cB = -E + (y + 0.5) * cw;
+        wsum += wv;
+        asum += wv * cA;
+        bsum += wv * cB;
+      }
+    double A = -E + (ix + 0.5) * cw, B = -E + (iy + 0.5) * cw;
+    if (wsum > 0.0) {
+      A = asum / wsum;
+      B = bsum / wsum;
+    }
+    double b[3];
+    backproject(A, B, b);
+    canonicalize3(b, r.axis);
+    r.A = A;
+    r.B = B;
+    r.ix = ix;
+    r.iy = iy;
+    r.votes = best;
+    r.ok = 1;
+  }
+  *out = r;
+}
+
 }  // namespace
+
+void launch_peak_axis(const unsigned long long* okey, const uint32_t* grid, int G, double E, uint32_t min_votes,
+                      PeakOut* out, cudaStream_t s) {
+  peak_axis_kernel<<<1, 1, 0, s>>>(okey, grid, G, E, min_votes, out);
+}
 
 int coop_refine_grid(int sms) {
   int per_sm = 0;
@@ -284,9 +348,9 @@ int coop_refine_grid(int sms) {
 int coop_tiles(int64_t n) { return (int)((n + kTile - 1) / kTile); }
 
 cudaError_t launch_coop_refine(const double* zx, const double* zy, const double* zz, int64_t n, int mode, int refine,
-                               double eps, double e0, const double axis0[3], uint32_t* flags0, uint32_t* flags1,
-                               int32_t* tile_count, int32_t* tile_offset, double* block_part, unsigned int* barrier,
-                               void* state, int grid, cudaStream_t s) {
+                               double eps, double e0, const double axis0[3], const double* axis0_dev,
+                               uint32_t* flags0, uint32_t* flags1, int32_t* tile_count, int32_t* tile_offset,
+                               double* block_part, unsigned int* barrier, void* state, int grid, cudaStream_t s) {
   CoopArgs a;
   a.zx = zx;
   a.zy = zy;
@@ -296,7 +360,8 @@ cudaError_t launch_coop_refine(const double* zx, const double* zy, const double*
   a.refine = refine;
   a.eps = eps;
   a.e0 = e0;
-  for (int k = 0; k < 3; ++k) a.axis0[k] = axis0[k];
+  for (int k = 0; k < 3; ++k) a.axis0[k] = axis0 ? axis0[k] : 0.0;
+  a.axis0_dev = axis0_dev;
   a.flags0 = flags0;
   a.flags1 = flags1;
   a.tile_count = tile_count;

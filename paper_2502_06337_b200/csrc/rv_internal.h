@@ -127,12 +127,17 @@ int classify_blocks(int64_t n);
 void launch_classify_mode(const double* zx, const double* zy, const double* zz, int64_t n, const double axis[3],
                           double eps, int mode, const ClassifyOut& o, int32_t* block_offsets, unsigned int* done,
                           cudaStream_t s);
+// out_host (optional): mapped pinned memory receiving a copy of the list (zero-copy read-back).
 void launch_compact_flags(const uint32_t* flags, int64_t n, const int32_t* map, const int32_t* block_offsets,
-                          int32_t* out, cudaStream_t s);
+                          int32_t* out, cudaStream_t s, int32_t* out_host = nullptr);
+// axis_dev / n_dev (optional): axis and index count read on the device (n_idx is then an upper
+// bound used for the launch size).
 void launch_vote_angles_k(const double axis[3], const double* corrs, const int32_t* idx, int64_t n_idx, int bin_count,
-                          double tau, uint32_t* bins, double* raw, unsigned long long* counts, cudaStream_t s);
+                          double tau, uint32_t* bins, double* raw, unsigned long long* counts, cudaStream_t s,
+                          const double* axis_dev = nullptr, const long long* n_dev = nullptr,
+                          int32_t* idx_host = nullptr);
 void launch_peak_angle_k(const uint32_t* bins, int bin_count, const double* raw, int64_t n_raw, double* block_sums,
-                         double* result, unsigned int* done, cudaStream_t s);
+                         double* result, unsigned int* done, cudaStream_t s, const long long* n_dev = nullptr);
 void launch_model_support_k(const double* zx, const double* zy, const double* zz, const int32_t* kept,
                             const double* corrs, int64_t n, const double axis[3], double angle, double eps, double tau,
                             uint32_t* band_flags, int32_t* block_counts, int32_t* result, unsigned int* done,
@@ -158,17 +163,31 @@ struct CoopState {  // published by the kernel after each pass; read by the host
   double e;
   double scatter[6];
   long long count;  // inliers of the last classify
-  int slot;         // flags slot (0/1) holding the final inlier bitmask
+  int slot;         // flags slot of the last pass (refine_loop copies the final bitmask to flags0)
   int done;
   int refits;
   int rank_deficient;
 };
+// Peak -> start axis on the device (estimate_from_peak, estimator.cpp:94-101): the argmax key,
+// interpolate_peak (estimator.cpp:32-47), backproject, canonicalize -- the host's op order.
+struct PeakOut {
+  double axis[3];
+  double A, B;                // interpolated plane coordinates
+  unsigned long long total;   // grid sum (exactness guard)
+  int ix, iy;
+  unsigned int votes;
+  int ok;                     // 0: no cell reaches min_votes (NoPeak)
+};
+void launch_peak_axis(const unsigned long long* okey, const uint32_t* grid, int G, double E, uint32_t min_votes,
+                      PeakOut* out, cudaStream_t s);
 int coop_refine_grid(int sms);
 int coop_tiles(int64_t n);
 size_t coop_state_bytes();
 // mode 0: refine_loop (estimator.cpp:51-69); mode 1: anneal_axis (estimator.cpp:145-160).
+// axis0_dev (optional): start axis read on the device (overrides axis0).
 cudaError_t launch_coop_refine(const double* zx, const double* zy, const double* zz, int64_t n, int mode, int refine,
-                               double eps, double e0, const double axis0[3], uint32_t* flags0, uint32_t* flags1,
+                               double eps, double e0, const double axis0[3], const double* axis0_dev,
+                               uint32_t* flags0, uint32_t* flags1,
                                int32_t* tile_count, int32_t* tile_offset, double* block_part, unsigned int* barrier,
                                void* state, int grid, cudaStream_t s);
 

@@ -96,20 +96,20 @@ RV_HD void canonicalize3(const double* p, double* o) {  // geom.cpp:34
     o[2] = p[2];
   }
 }
-inline void unproject2(double A, double B, double* o) {  // geom.cpp:29-32
+RV_HD void unproject2(double A, double B, double* o) {  // geom.cpp:29-32
   const double s = 1.0 + A * A + B * B;
   o[0] = 2.0 * A / s;
   o[1] = 2.0 * B / s;
   o[2] = (A * A + B * B - 1.0) / s;
 }
-inline bool project3(const double* p, double* A, double* B) {  // geom.cpp:21-27
+RV_HD bool project3(const double* p, double* A, double* B) {  // geom.cpp:21-27
   if (p[2] >= 1.0 - 1e-9) return false;
   const double inv = 1.0 / (1.0 - p[2]);
   *A = p[0] * inv;
   *B = p[1] * inv;
   return true;
 }
-inline void backproject(double A, double B, double* o) {  // voting.cpp:172-174
+RV_HD void backproject(double A, double B, double* o) {  // voting.cpp:172-174
   double u[3];
   unproject2(A, B, u);
   normalized3(u, o);

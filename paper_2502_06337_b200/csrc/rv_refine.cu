@@ -188,7 +188,8 @@ __global__ void __launch_bounds__(kClsThreads) classify_kernel(ClsArgs a) {
 
 // bitmask -> ascending indices (through map if given). Uses block_offsets from classify.
 __global__ void __launch_bounds__(kClsThreads) compact_kernel(const uint32_t* flags, int64_t n, const int32_t* map,
-                                                             const int32_t* block_offsets, int32_t* out) {
+                                                             const int32_t* block_offsets, int32_t* out,
+                                                             int32_t* out_host) {
   __shared__ int s_pref[kClsPerBlock / 32 + 1];
   const int tid = threadIdx.x;
   const int64_t wbase = (int64_t)blockIdx.x * (kClsPerBlock / 32);
@@ -210,7 +211,9 @@ __global__ void __launch_bounds__(kClsThreads) compact_kernel(const uint32_t* fl
     if ((word >> lane) & 1u) {
       const int64_t i = (wbase + w) * 32 + lane;
       const int pos = off + s_pref[w] + __popc(word & ((1u << lane) - 1u));
-      out[pos] = map ? map[i] : (int32_t)i;
+      const int32_t v = map ? map[i] : (int32_t)i;
+      out[pos] = v;
+      if (out_host) out_host[pos] = v;
     }
   }
 }
@@ -235,6 +238,9 @@ __device__ __forceinline__ int bin_of(double angle, int n) {  // angles.cpp:25-3
 
 struct AngArgs {
   double a0, a1, a2, tau;
+  const double* axis_dev;   // optional: axis on the device
+  const long long* n_dev;   // optional: count on the device (n = upper bound)
+  int32_t* idx_host;        // optional: mapped pinned copy of idx (coalesced zero-copy read-back)
   const double* corrs;
   const int32_t* idx;
   int64_t n;
@@ -251,10 +257,15 @@ __global__ void __launch_bounds__(256) vote_angles_kernel(AngArgs a) {
     for (int k = threadIdx.x; k < a.bins_n; k += blockDim.x) s_bins[k] = 0;
   __syncthreads();
   unsigned long long contrib = 0, degen = 0;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.n; k += (int64_t)gridDim.x * blockDim.x) {
-    const double* c = a.corrs + 6 * (int64_t)a.idx[k];
+  const int64_t n = a.n_dev ? min(a.n, (int64_t)*a.n_dev) : a.n;
+  const double a0 = a.axis_dev ? a.axis_dev[0] : a.a0, a1 = a.axis_dev ? a.axis_dev[1] : a.a1,
+               a2 = a.axis_dev ? a.axis_dev[2] : a.a2;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t ik = a.idx[k];
+    if (a.idx_host) a.idx_host[k] = ik;
+    const double* c = a.corrs + 6 * (int64_t)ik;
     double ang;
-    if (corr_angle(a.a0, a.a1, a.a2, c, a.tau, &ang)) {
+    if (corr_angle(a0, a1, a2, c, a.tau, &ang)) {
       a.raw[k] = ang;
       const int b = bin_of(ang, a.bins_n);
       if (use_smem) atomicAdd(&s_bins[b], 1u);
@@ -282,8 +293,9 @@ __global__ void __launch_bounds__(256) vote_angles_kernel(AngArgs a) {
 // peak_angle sums (angles.cpp:70-90): first max bin, then sin/cos sums of raw angles within
 // 1.5 bin widths (wrapped difference) of the bin center. result: [0]=s [1]=c [2]=k [3]=center.
 __global__ void __launch_bounds__(256) peak_angle_kernel(const uint32_t* bins, int bins_n, const double* raw,
-                                                        int64_t n, double* block_sums, double* result,
-                                                        unsigned int* done) {
+                                                        int64_t n_max, double* block_sums, double* result,
+                                                        unsigned int* done, const long long* n_dev) {
+  const int64_t n = n_dev ? min(n_max, (int64_t)*n_dev) : n_max;
   __shared__ unsigned long long s_key[8];
   __shared__ double s_red[2][8];
   __shared__ bool s_last;
@@ -309,7 +321,9 @@ __global__ void __launch_bounds__(256) peak_angle_kernel(const uint32_t* bins, i
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     const double a = raw[k];
     if (a != a) continue;  // degenerate
-    double d = fmod(xs(a, center), 2.0 * kPi);
+    // fmod(x, 2 pi) is exact and equals x for |x| < 2 pi (a, center in [-pi, pi]): skip the slow call
+    const double x = xs(a, center);
+    double d = fabs(x) < 2.0 * kPi ? x : fmod(x, 2.0 * kPi);
     if (d <= -kPi) d = xa(d, 2.0 * kPi);
     if (d > kPi) d = xs(d, 2.0 * kPi);
     if (fabs(d) <= window) {
@@ -547,16 +561,20 @@ void launch_classify_mode(const double* zx, const double* zy, const double* zz, 
 }
 
 void launch_compact_flags(const uint32_t* flags, int64_t n, const int32_t* map, const int32_t* block_offsets,
-                          int32_t* out, cudaStream_t s) {
-  compact_kernel<<<classify_blocks(n), kClsThreads, 0, s>>>(flags, n, map, block_offsets, out);
+                          int32_t* out, cudaStream_t s, int32_t* out_host) {
+  compact_kernel<<<classify_blocks(n), kClsThreads, 0, s>>>(flags, n, map, block_offsets, out, out_host);
 }
 
 void launch_vote_angles_k(const double axis[3], const double* corrs, const int32_t* idx, int64_t n_idx, int bin_count,
-                          double tau, uint32_t* bins, double* raw, unsigned long long* counts, cudaStream_t s) {
+                          double tau, uint32_t* bins, double* raw, unsigned long long* counts, cudaStream_t s,
+                          const double* axis_dev, const long long* n_dev, int32_t* idx_host) {
   AngArgs a;
-  a.a0 = axis[0];
-  a.a1 = axis[1];
-  a.a2 = axis[2];
+  a.idx_host = idx_host;
+  a.a0 = axis ? axis[0] : 0.0;
+  a.a1 = axis ? axis[1] : 0.0;
+  a.a2 = axis ? axis[2] : 0.0;
+  a.axis_dev = axis_dev;
+  a.n_dev = n_dev;
   a.tau = tau;
   a.corrs = corrs;
   a.idx = idx;
@@ -572,10 +590,10 @@ void launch_vote_angles_k(const double axis[3], const double* corrs, const int32
 }
 
 void launch_peak_angle_k(const uint32_t* bins, int bin_count, const double* raw, int64_t n_raw, double* block_sums,
-                         double* result, unsigned int* done, cudaStream_t s) {
+                         double* result, unsigned int* done, cudaStream_t s, const long long* n_dev) {
   const int64_t want = (n_raw + 255) / 256;
   const int blocks = (int)(want < 1 ? 1 : (want > 296 ? 296 : want));
-  peak_angle_kernel<<<blocks, 256, 0, s>>>(bins, bin_count, raw, n_raw, block_sums, result, done);
+  peak_angle_kernel<<<blocks, 256, 0, s>>>(bins, bin_count, raw, n_raw, block_sums, result, done, n_dev);
 }
 
 void launch_model_support_k(const double* zx, const double* zy, const double* zz, const int32_t* kept,

@@ -159,6 +159,14 @@ __device__ __forceinline__ void runs_push(Runs& r, int lo, int hi) {
   }
 }
 
+// x mod M in [0, M) (M = J/2 pairs; a power of two for every J the reference ships, else the
+// generic integer modulo)
+__device__ __forceinline__ int wrap_pair(int x, int M) {
+  if ((M & (M - 1)) == 0) return x & (M - 1);
+  x %= M;
+  return x < 0 ? x + M : x;
+}
+
 // Ranges of one band from its lower/upper arc sets: S = U_lo \ U_hi, padded, merged, wrapped.
 __device__ __forceinline__ uint2 plan_from_sets(const Arc2& ulo, const Arc2& uhi, float pa, float inv_step, int M,
                                                 unsigned long long* work) {
@@ -224,8 +232,8 @@ __device__ __forceinline__ uint2 plan_from_sets(const Arc2& ulo, const Arc2& uhi
       nl = 1;
     }
   }
-  int s0 = ((L0 % M) + M) % M, l0 = H0 - L0 + 1;
-  int s1 = ((L1 % M) + M) % M, l1 = nl == 2 ? H1 - L1 + 1 : 0;
+  int s0 = wrap_pair(L0, M), l0 = H0 - L0 + 1;
+  int s1 = wrap_pair(L1, M), l1 = nl == 2 ? H1 - L1 + 1 : 0;
   if (l0 >= M || l1 >= M) {
     *work += (unsigned long long)M;
     return full;
@@ -234,7 +242,7 @@ __device__ __forceinline__ uint2 plan_from_sets(const Arc2& ulo, const Arc2& uhi
   l0 = (l0 + 31) & ~31;
   if (nl == 2) {
     l1 = (l1 + 31) & ~31;
-    const int d01 = ((s1 - s0) % M + M) % M, d10 = ((s0 - s1) % M + M) % M;
+    const int d01 = wrap_pair(s1 - s0, M), d10 = wrap_pair(s0 - s1, M);
     if (d01 < l0) {
       l0 = (max(l0, d01 + l1) + 31) & ~31;
       nl = 1;
@@ -331,25 +339,23 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
     }
   };
   if constexpr (kNB > 0) {
-    uint2 rr[kNB];
-    int woff[kNB];
-#pragma unroll
-    for (int band = 0; band < kNB; ++band) {
-      rr[band] = make_uint2(0u, 0u);
-      woff[band] = 0;
-      if (band < p.n_bands) {  // uniform
-        unsigned long long w = 0;
-        rr[band] = plan_band(band, &w);
-        woff[band] = book(band, rr[band], w, false);
-      }
+    // per-thread ranges/offsets parked in shared memory (a rolled band loop keeps the code small)
+    __shared__ uint2 s_r[kNB][256];
+    __shared__ int s_off[kNB][256];
+#pragma unroll 1
+    for (int band = 0; band < p.n_bands; ++band) {  // uniform
+      unsigned long long w = 0;
+      const uint2 r = plan_band(band, &w);
+      s_r[band][threadIdx.x] = r;
+      s_off[band][threadIdx.x] = book(band, r, w, false);
     }
     __syncthreads();
     for (int t = threadIdx.x; t < p.n_bands; t += blockDim.x)
       s_base[t] = s_cnt[t] ? atomicAdd(&b.entry_count[t], s_cnt[t]) : 0;
     __syncthreads();
-#pragma unroll
-    for (int band = 0; band < kNB; ++band)
-      if (band < p.n_bands) emit(band, rr[band], (int64_t)s_base[band] + woff[band]);
+#pragma unroll 1
+    for (int band = 0; band < p.n_bands; ++band)
+      emit(band, s_r[band][threadIdx.x], (int64_t)s_base[band] + s_off[band][threadIdx.x]);
   } else {
     for (int band = 0; band < p.n_bands; ++band) {  // uniform trip count: warp collectives inside
       unsigned long long w = 0;

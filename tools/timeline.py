@@ -1,0 +1,54 @@
+"""Dev probe: device timeline of one C3 solve via torch.profiler (CUPTI activity records of every
+kernel / memset / memcpy in the process, including the library's own launches). Prints each
+activity with its start offset, duration and the idle gap before it."""
+import json
+import sys
+import tempfile
+from pathlib import Path
+
+import torch
+from torch.profiler import ProfilerActivity, profile
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import paper_2502_06337_b200 as rv  # noqa: E402
+from paper_2502_06337_b200 import synth  # noqa: E402
+
+key = sys.argv[1] if len(sys.argv) > 1 else "c3"
+host = len(sys.argv) > 2 and sys.argv[2] == "host"
+corrs, _, _ = synth.make_config(key)
+ctx = rv.Context(0)
+ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+d = torch.from_numpy(corrs).cuda()
+h = torch.empty((corrs.shape[0], 6), dtype=torch.float64, pin_memory=True)
+h.numpy()[:] = corrs
+cfg = rv.EstimatorConfig()
+
+
+def solve():
+    if host:
+        return ctx.estimate_single(h.numpy(), cfg)
+    return ctx.estimate_single_device(d.data_ptr(), corrs.shape[0], cfg)
+
+
+for _ in range(3):
+    solve()
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    solve()
+    torch.cuda.synchronize()
+with tempfile.NamedTemporaryFile(suffix=".json") as f:
+    prof.export_chrome_trace(f.name)
+    ev = json.load(open(f.name))["traceEvents"]
+acts = [e for e in ev if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memset", "gpu_memcpy")]
+acts.sort(key=lambda e: e["ts"])
+t0 = acts[0]["ts"]
+end_prev = t0
+busy = 0.0
+for e in acts:
+    gap = e["ts"] - end_prev
+    print(f"{e['ts'] - t0:9.1f} us  dur {e['dur']:8.1f}  gap {gap:7.1f}  {e['cat']:10s} {e['name'][:70]}")
+    end_prev = max(end_prev, e["ts"] + e["dur"])
+    busy += e["dur"]
+span = end_prev - t0
+print(f"span {span:.1f} us, busy {busy:.1f} us, idle {span - busy:.1f} us")
