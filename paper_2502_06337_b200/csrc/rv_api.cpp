@@ -846,8 +846,13 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
     ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     c->chunk_events.push_back(e);
   }
+  // chunk k+1's copy overlaps chunk k's compute (which is slower per element than the copy), so
+  // only the first copy is exposed: geometric schedule 1/16, 3/16, 6/16, 6/16, bounds aligned to
+  // the preprocess tile (1024 correspondences)
+  static const int64_t kCum[5] = {0, 1, 4, 10, 16};
   std::vector<int64_t> bounds(C + 1);
-  for (int k = 0; k <= C; ++k) bounds[k] = k == C ? n : std::min<int64_t>(n, ((n * k / C) + 255) / 256 * 256);
+  for (int k = 0; k <= C; ++k)
+    bounds[k] = k == C ? n : std::min<int64_t>(n, ((C == 4 ? n * kCum[k] / 16 : 0) + 1023) / 1024 * 1024);
   StageScope sc(c, kVote);
   // order the copy stream after everything already queued on the compute stream (buffer reuse)
   cudaEvent_t start = take_event(c);

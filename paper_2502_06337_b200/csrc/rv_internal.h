@@ -93,7 +93,7 @@ struct PrepBuffers {
 };
 int prep_blocks(int64_t n);
 void launch_preprocess(const PrepBuffers& b, int64_t n, double tau_z, int normalize, cudaStream_t s);
-// One chunk [elem_lo, elem_hi) of a pipelined preprocess (elem_lo multiple of 256; chunks in order).
+// One chunk [elem_lo, elem_hi) of a pipelined preprocess (elem_lo multiple of 1024; chunks in order).
 void launch_preprocess_range(const PrepBuffers& b, int64_t n, int64_t elem_lo, int64_t elem_hi, double tau_z,
                              int normalize, cudaStream_t s);
 

@@ -17,65 +17,95 @@ namespace rvb {
 namespace {
 
 constexpr int kPrepThreads = 256;
+constexpr int kPrepPer = 4;                             // elements per thread (r-major in the block)
+constexpr int kPrepTile = kPrepThreads * kPrepPer;      // 1024 correspondences per block
+constexpr int kPrepWarps = kPrepThreads / 32;
 
 template <bool kVec>
 __global__ void __launch_bounds__(kPrepThreads) preprocess_kernel(PrepBuffers b, int64_t n, int64_t elem_hi,
                                                                   double tau_z, int normalize) {
   __shared__ int s_bid;
-  __shared__ int s_warp_kept[kPrepThreads / 32];
+  __shared__ int s_cnt[kPrepPer * kPrepWarps];  // kept per (round, warp), then its exclusive scan
+  __shared__ int s_total;
   __shared__ long long s_excl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_bid = atomicAdd(b.block_counter, 1);
   __syncthreads();
   const int bid = s_bid;
-  const int64_t i = (int64_t)bid * kPrepThreads + tid;
-  double x0 = 0, x1 = 0, x2 = 0, y0 = 0, y1 = 0, y2 = 0;
-  bool valid = i < n;
-  if (valid) {
-    if (kVec) {
-      const double2* p = reinterpret_cast<const double2*>(b.corrs + 6 * i);
-      const double2 u = p[0], v = p[1], w = p[2];
-      x0 = u.x; x1 = u.y; x2 = v.x; y0 = v.y; y1 = w.x; y2 = w.y;
-    } else {
-      const double* p = b.corrs + 6 * i;
-      x0 = p[0]; x1 = p[1]; x2 = p[2]; y0 = p[3]; y1 = p[4]; y2 = p[5];
+  const int64_t base = (int64_t)bid * kPrepTile;
+  double c[kPrepPer][6];
+#pragma unroll
+  for (int r = 0; r < kPrepPer; ++r) {  // all loads first (coalesced per round)
+    const int64_t i = base + r * kPrepThreads + tid;
+    for (int k = 0; k < 6; ++k) c[r][k] = 0.0;
+    if (i < n) {
+      if (kVec) {
+        const double2* p = reinterpret_cast<const double2*>(b.corrs + 6 * i);
+        const double2 u = p[0], v = p[1], w = p[2];
+        c[r][0] = u.x; c[r][1] = u.y; c[r][2] = v.x; c[r][3] = v.y; c[r][4] = w.x; c[r][5] = w.y;
+      } else {
+        const double* p = b.corrs + 6 * i;
+        for (int k = 0; k < 6; ++k) c[r][k] = p[k];
+      }
     }
   }
-  if (normalize) {
-    const double nx = __dsqrt_rn(xdot(x0, x1, x2, x0, x1, x2));
-    const double ny = __dsqrt_rn(xdot(y0, y1, y2, y0, y1, y2));
-    if (nx > 0.0) { x0 = xd(x0, nx); x1 = xd(x1, nx); x2 = xd(x2, nx); }
-    if (ny > 0.0) { y0 = xd(y0, ny); y1 = xd(y1, ny); y2 = xd(y2, ny); }
+  double zo[kPrepPer][3];
+  bool keep[kPrepPer], drop[kPrepPer];
+  unsigned km[kPrepPer];
+#pragma unroll
+  for (int r = 0; r < kPrepPer; ++r) {
+    const int64_t i = base + r * kPrepThreads + tid;
+    double x0 = c[r][0], x1 = c[r][1], x2 = c[r][2], y0 = c[r][3], y1 = c[r][4], y2 = c[r][5];
+    if (normalize) {
+      const double nx = __dsqrt_rn(xdot(x0, x1, x2, x0, x1, x2));
+      const double ny = __dsqrt_rn(xdot(y0, y1, y2, y0, y1, y2));
+      if (nx > 0.0) { x0 = xd(x0, nx); x1 = xd(x1, nx); x2 = xd(x2, nx); }
+      if (ny > 0.0) { y0 = xd(y0, ny); y1 = xd(y1, ny); y2 = xd(y2, ny); }
+    }
+    const double d0 = xs(y0, x0), d1 = xs(y1, x1), d2 = xs(y2, x2);
+    const double len = __dsqrt_rn(xdot(d0, d1, d2, d0, d1, d2));
+    const bool valid = i < n;
+    drop[r] = valid && (len < tau_z);
+    keep[r] = valid && !drop[r];
+    zo[r][0] = xd(d0, len);
+    zo[r][1] = xd(d1, len);
+    zo[r][2] = xd(d2, len);
+    km[r] = __ballot_sync(0xFFFFFFFFu, keep[r]);
+    if (lane == 0) s_cnt[r * kPrepWarps + warp] = __popc(km[r]);
   }
-  const double d0 = xs(y0, x0), d1 = xs(y1, x1), d2 = xs(y2, x2);
-  const double len = __dsqrt_rn(xdot(d0, d1, d2, d0, d1, d2));
-  const bool drop = valid && (len < tau_z);
-  const bool keep = valid && !drop;
-  const unsigned km = __ballot_sync(0xFFFFFFFFu, keep);
-  if (lane == 0) s_warp_kept[warp] = __popc(km);
   __syncthreads();
-  int before = 0, total = 0;
-  for (int w = 0; w < kPrepThreads / 32; ++w) {
-    const int c = s_warp_kept[w];
-    if (w < warp) before += c;
-    total += c;
-  }
-  if (warp == 0) {
+  if (warp == 0) {  // exclusive scan of the 32 (round, warp) counts in element order
+    const int v = s_cnt[lane];
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    s_cnt[lane] = incl - v;
     const long long e = lookback_exclusive(reinterpret_cast<unsigned long long*>(b.status), bid, total);
-    if (lane == 0) s_excl = e;
+    if (lane == 0) {
+      s_excl = e;
+      s_total = total;
+    }
   }
   __syncthreads();
   const long long excl = s_excl;
-  const long long rank = excl + before + __popc(km & ((1u << lane) - 1u));
-  if (keep) {
-    b.zx[rank] = xd(d0, len);
-    b.zy[rank] = xd(d1, len);
-    b.zz[rank] = xd(d2, len);
-    b.kept[rank] = (int32_t)i;
-  } else if (drop) {
-    b.dropped[i - rank] = (int32_t)i;
+#pragma unroll
+  for (int r = 0; r < kPrepPer; ++r) {
+    const int64_t i = base + r * kPrepThreads + tid;
+    const long long rank = excl + s_cnt[r * kPrepWarps + warp] + __popc(km[r] & ((1u << lane) - 1u));
+    if (keep[r]) {
+      b.zx[rank] = zo[r][0];
+      b.zy[rank] = zo[r][1];
+      b.zz[rank] = zo[r][2];
+      b.kept[rank] = (int32_t)i;
+    } else if (drop[r]) {
+      b.dropped[i - rank] = (int32_t)i;
+    }
   }
-  const int64_t block_end = (int64_t)(bid + 1) * kPrepThreads;
+  const int total = s_total;
+  const int64_t block_end = base + kPrepTile;
   if (tid == 0 && block_end >= n) {  // the last block publishes the totals
     b.totals[0] = (int32_t)(excl + total);
     b.totals[1] = (int32_t)(n - (excl + total));
@@ -124,7 +154,7 @@ __global__ void __launch_bounds__(kGatherThreads)
 
 }  // namespace
 
-int prep_blocks(int64_t n) { return (int)((n + kPrepThreads - 1) / kPrepThreads); }
+int prep_blocks(int64_t n) { return (int)((n + kPrepTile - 1) / kPrepTile); }
 
 void launch_preprocess(const PrepBuffers& b, int64_t n, double tau_z, int normalize, cudaStream_t s) {
   const int blocks = prep_blocks(n);
@@ -137,7 +167,7 @@ void launch_preprocess(const PrepBuffers& b, int64_t n, double tau_z, int normal
 
 void launch_preprocess_range(const PrepBuffers& b, int64_t n, int64_t elem_lo, int64_t elem_hi, double tau_z,
                              int normalize, cudaStream_t s) {
-  const int blocks = (int)((elem_hi - elem_lo + kPrepThreads - 1) / kPrepThreads);
+  const int blocks = (int)((elem_hi - elem_lo + kPrepTile - 1) / kPrepTile);
   if (blocks <= 0) return;
   const bool vec = (reinterpret_cast<uintptr_t>(b.corrs) & 15u) == 0;
   if (vec)
