@@ -12,6 +12,7 @@
 #include <deque>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numbers>
@@ -839,20 +840,32 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
   if (J < 1) fail(RV_ERR_INVALID_CONFIG, "theta_samples must be >= 1");
   ensure_tables(c, J);
   const VotePlan& p = cached_plan(c, G, cfg.extent, J);
-  const int C = (p.banded && n >= (int64_t)1 << 18) ? 4 : 1;
+  // chunk k+1's copy overlaps chunk k's compute (~1.4x slower per correspondence than the copy).
+  // Default 1, 2, 5, 8 sixteenths (measured best of the schedules tried): only the first 3 MB copy
+  // is exposed, and each extra chunk costs a vote-launch tail. Bounds are aligned to the
+  // preprocess tile (1024). Dev knob: RV_PIPE_CUM="0,1,3,8,16" (cumulative sixteenths).
+  static const std::vector<int64_t> kCum = [] {
+    std::vector<int64_t> v{0, 1, 3, 8, 16};
+    if (const char* e = std::getenv("RV_PIPE_CUM")) {
+      std::vector<int64_t> w;
+      for (const char* q = e; *q;) {
+        w.push_back(std::strtoll(q, const_cast<char**>(&q), 10));
+        if (*q == ',') ++q;
+      }
+      if (w.size() >= 2 && w.front() == 0 && w.back() == 16) v = w;
+    }
+    return v;
+  }();
+  const int C = (p.banded && n >= (int64_t)1 << 18) ? (int)kCum.size() - 1 : 1;
   if (!c->copy_st) ck(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking), "copy stream");
   while ((int)c->chunk_events.size() < C) {
     cudaEvent_t e;
     ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     c->chunk_events.push_back(e);
   }
-  // chunk k+1's copy overlaps chunk k's compute (which is slower per element than the copy), so
-  // only the first copy is exposed: geometric schedule 1/16, 3/16, 6/16, 6/16, bounds aligned to
-  // the preprocess tile (1024 correspondences)
-  static const int64_t kCum[5] = {0, 1, 4, 10, 16};
   std::vector<int64_t> bounds(C + 1);
   for (int k = 0; k <= C; ++k)
-    bounds[k] = k == C ? n : std::min<int64_t>(n, ((C == 4 ? n * kCum[k] / 16 : 0) + 1023) / 1024 * 1024);
+    bounds[k] = k == C ? n : std::min<int64_t>(n, ((C > 1 ? n * kCum[k] / 16 : 0) + 1023) / 1024 * 1024);
   StageScope sc(c, kVote);
   // order the copy stream after everything already queued on the compute stream (buffer reuse)
   cudaEvent_t start = take_event(c);
@@ -922,7 +935,7 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
       // entry lists and their counters are per chunk (reused: the stream orders chunk k's vote
       // before chunk k+1's plan)
       if (k > 0)
-        ck(cudaMemsetAsync(b.counters + 1, 0, sizeof(int32_t) * 2 * kMaxBands, c->st), "memset band counters");
+        launch_zero_i32(b.counters + 1, 2 * kMaxBands, c->st);
       launch_plan(p, b, cap, c->st);
       {
         StageScope kv(c, kVoteKernel);

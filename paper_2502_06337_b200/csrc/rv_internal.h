@@ -71,6 +71,7 @@ void launch_plan(const VotePlan& p, const VoteBuffers& b, int64_t n, cudaStream_
 // K2: band-tiled vote into smem tiles, flushed to partial slots; then tile reduction.
 void launch_vote_banded(const VotePlan& p, const VoteBuffers& b, int64_t n, int n_ctas, cudaStream_t s);
 cudaError_t set_vote_smem(const VotePlan& p);  // opt-in dynamic smem (once per size)
+void launch_zero_i32(int32_t* p, int n, cudaStream_t s);
 void launch_vote_reduce(const VotePlan& p, const VoteBuffers& b, cudaStream_t s);
 // Exact generic vote (any config): one thread per (constraint, sample), global atomics.
 void launch_vote_generic(const VotePlan& p, const VoteBuffers& b, int64_t n, cudaStream_t s);

@@ -839,6 +839,13 @@ void launch_vote_generic(const VotePlan& p, const VoteBuffers& b, int64_t n, cud
   vote_generic_kernel<<<(unsigned)blocks, threads, 0, s>>>(p, b.zx, b.zy, b.zz, b.table64, b.grid, n);
 }
 
+// Small counter reset as a kernel: a cudaMemsetAsync can queue behind a concurrent H2D on the
+// copy engine (pipelined host-input path).
+__global__ void zero_i32_kernel(int32_t* p, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0;
+}
+void launch_zero_i32(int32_t* p, int n, cudaStream_t s) { zero_i32_kernel<<<1, 256, 0, s>>>(p, n); }
+
 void launch_deposit_one(const VotePlan& p, const double* z3, const double2* table64, uint32_t* grid,
                         cudaStream_t s) {
   deposit_one_kernel<<<1, 256, 0, s>>>(p, z3, table64, grid);
