@@ -143,15 +143,44 @@ __global__ void sat_rows_kernel(const uint32_t* grid, int G, unsigned long long*
 }
 
 // SAT column pass: sat[y][x] += sat[y-1][x] down every column; row 0 = 0.
-__global__ void sat_cols_kernel(int G, unsigned long long* sat) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+// Column prefix sums of the (G+1)^2 SAT in two levels: the rows are cut into kSatSeg segments;
+// thread (x, seg) sums its segment, a per-column scan of the segment totals in shared memory,
+// then each thread rescans its segment with the carried prefix (loads issued in batches).
+constexpr int kSatSeg = 16;
+constexpr int kSatCols = 16;  // columns per block -> blockDim = kSatCols * kSatSeg = 256
+__global__ void __launch_bounds__(kSatCols * kSatSeg) sat_cols_kernel(int G, unsigned long long* sat) {
+  __shared__ unsigned long long s_seg[kSatSeg][kSatCols];
+  const int cx = threadIdx.x % kSatCols, seg = threadIdx.x / kSatCols;
+  const int x = blockIdx.x * kSatCols + cx;
   const int W = G + 1;
-  if (x >= W) return;
-  sat[x] = 0ull;
-  unsigned long long acc = 0;
-  for (int y = 1; y <= G; ++y) {
-    acc += sat[(size_t)y * W + x];
-    sat[(size_t)y * W + x] = acc;
+  const int len = (G + kSatSeg - 1) / kSatSeg;
+  const int y0 = 1 + seg * len, y1 = min(G + 1, y0 + len);
+  unsigned long long tot = 0;
+  if (x < W) {
+    if (seg == 0) sat[x] = 0ull;
+    for (int y = y0; y < y1; y += 8) {
+      unsigned long long v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = y + k < y1 ? sat[(size_t)(y + k) * W + x] : 0ull;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) tot += v[k];
+    }
+  }
+  s_seg[seg][cx] = tot;
+  __syncthreads();
+  unsigned long long carry = 0;
+  for (int q = 0; q < seg; ++q) carry += s_seg[q][cx];
+  if (x < W) {
+    for (int y = y0; y < y1; y += 8) {
+      unsigned long long v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = y + k < y1 ? sat[(size_t)(y + k) * W + x] : 0ull;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        carry += v[k];
+        if (y + k < y1) sat[(size_t)(y + k) * W + x] = carry;
+      }
+    }
   }
 }
 
@@ -219,19 +248,36 @@ __global__ void __launch_bounds__(256) blur_box_kernel(const unsigned long long*
     s_last = atomicAdd(done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (s_last && threadIdx.x == 0) {
-    volatile unsigned long long* bb = block_best;
-    for (int k = 0; k < radii.n; ++k) {
-      unsigned long long s = 0, i = ~0ull;
-      for (unsigned b = 0; b < gridDim.x; ++b) {
-        const unsigned long long cs = bb[((size_t)b * 8 + k) * 2], ci = bb[((size_t)b * 8 + k) * 2 + 1];
-        if (better(cs, ci, s, i)) {
-          s = cs;
-          i = ci;
-        }
+  if (!s_last) return;
+  // last block: parallel reduction (better() is a total order: the result is order-independent)
+  for (int k = 0; k < radii.n; ++k) {
+    unsigned long long s = 0, i = ~0ull;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+      const unsigned long long cs = __ldcg(block_best + ((size_t)b * 8 + k) * 2);
+      const unsigned long long ci = __ldcg(block_best + ((size_t)b * 8 + k) * 2 + 1);
+      if (better(cs, ci, s, i)) {
+        s = cs;
+        i = ci;
       }
-      out_best[2 * k] = s;
-      out_best[2 * k + 1] = i;
+    }
+    __syncthreads();
+    s_sum[k][threadIdx.x] = s;
+    s_idx[k][threadIdx.x] = i;
+  }
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+      for (int k = 0; k < radii.n; ++k)
+        if (better(s_sum[k][threadIdx.x + o], s_idx[k][threadIdx.x + o], s_sum[k][threadIdx.x], s_idx[k][threadIdx.x])) {
+          s_sum[k][threadIdx.x] = s_sum[k][threadIdx.x + o];
+          s_idx[k][threadIdx.x] = s_idx[k][threadIdx.x + o];
+        }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < radii.n; ++k) {
+      out_best[2 * k] = s_sum[k][0];
+      out_best[2 * k + 1] = s_idx[k][0];
     }
     *done = 0u;
   }
@@ -262,7 +308,7 @@ void launch_blur_argmax(const uint32_t* grid, int G, const int* radii, int n_rad
                         cudaStream_t s) {
   const int t = G >= 1024 ? 1024 : (G >= 256 ? 256 : 32);
   sat_rows_kernel<<<G, t, 0, s>>>(grid, G, sat);
-  sat_cols_kernel<<<(G + 1 + 127) / 128, 128, 0, s>>>(G, sat);
+  sat_cols_kernel<<<(G + 1 + kSatCols - 1) / kSatCols, kSatCols * kSatSeg, 0, s>>>(G, sat);
   Radii rr;
   rr.n = n_radii < 8 ? n_radii : 8;
   for (int k = 0; k < rr.n; ++k) rr.r[k] = radii[k];

@@ -350,12 +350,26 @@ __global__ void __launch_bounds__(256) peak_angle_kernel(const uint32_t* bins, i
     s_last = atomicAdd(done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (s_last && threadIdx.x == 0) {
-    volatile double* bsum = block_sums;
+  if (!s_last) return;
+  // last block: fixed-order parallel reduction (thread t: blocks t, t+256, ...; then the tree)
+  double s2[2] = {0.0, 0.0};
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+    s2[0] = xa(s2[0], __ldcg(block_sums + 2 * b));
+    s2[1] = xa(s2[1], __ldcg(block_sums + 2 * b + 1));
+  }
+  for (int k = 0; k < 2; ++k)
+    for (int o = 16; o > 0; o >>= 1) s2[k] = xa(s2[k], __shfl_xor_sync(0xFFFFFFFFu, s2[k], o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    s_red[0][threadIdx.x >> 5] = s2[0];
+    s_red[1][threadIdx.x >> 5] = s2[1];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
     double s = 0, c = 0;
-    for (unsigned b = 0; b < gridDim.x; ++b) {
-      s = xa(s, bsum[2 * b]);
-      c = xa(c, bsum[2 * b + 1]);
+    for (int ww = 0; ww < 8; ++ww) {
+      s = xa(s, s_red[0][ww]);
+      c = xa(c, s_red[1][ww]);
     }
     result[0] = s;
     result[1] = c;
@@ -426,15 +440,31 @@ __global__ void __launch_bounds__(kClsThreads) model_support_kernel(SupArgs a) {
     s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (s_last && tid == 0) {
-    volatile int32_t* bc = a.block_counts;
-    long long c = 0, b = 0;
-    for (unsigned k = 0; k < gridDim.x; ++k) {
-      c += bc[2 * k];
-      b += bc[2 * k + 1];
+  if (!s_last) return;
+  // last block: parallel integer reduction (order-free)
+  long long c = 0, b = 0;
+  for (unsigned k = tid; k < gridDim.x; k += blockDim.x) {
+    c += __ldcg(a.block_counts + 2 * k);
+    b += __ldcg(a.block_counts + 2 * k + 1);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    b += __shfl_xor_sync(0xFFFFFFFFu, b, o);
+  }
+  __shared__ long long s_cb[2][kClsThreads / 32];
+  if ((tid & 31) == 0) {
+    s_cb[0][tid >> 5] = c;
+    s_cb[1][tid >> 5] = b;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    long long cc = 0, bb = 0;
+    for (int w = 0; w < kClsThreads / 32; ++w) {
+      cc += s_cb[0][w];
+      bb += s_cb[1][w];
     }
-    a.result[0] = (int32_t)c;
-    a.result[1] = (int32_t)b;
+    a.result[0] = (int32_t)cc;
+    a.result[1] = (int32_t)bb;
     *a.done = 0u;
   }
 }
@@ -516,19 +546,46 @@ __global__ void __launch_bounds__(kClsThreads) near_identity_kernel(NearArgs a) 
     s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (s_last && tid == 0) {
-    volatile int32_t* bc = a.block_count;
-    volatile double* bh = a.block_h;
-    long long c = 0;
-    double hh[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (unsigned b = 0; b < gridDim.x; ++b) {
-      a.block_offsets[b] = (int32_t)c;
-      c += bc[b];
-      for (int k = 0; k < 9; ++k) hh[k] = xa(hh[k], bh[(size_t)b * 9 + k]);
+  if (!s_last) return;
+  // last block: each thread owns a contiguous run of blocks (sequential sums), exclusive scan of
+  // the run counts, fixed tree for the 9 Kabsch sums
+  const int nb = gridDim.x;
+  const int per = (nb + kClsThreads - 1) / kClsThreads;
+  const int b0 = tid * per, b1 = min(nb, b0 + per);
+  long long tc = 0;
+  double hh[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int b = b0; b < b1; ++b) {
+    tc += __ldcg(a.block_count + b);
+    for (int k = 0; k < 9; ++k) hh[k] = xa(hh[k], __ldcg(a.block_h + (size_t)b * 9 + k));
+  }
+  __shared__ long long s_run[kClsThreads];
+  __shared__ double s_h[9][kClsThreads / 32];
+  s_run[tid] = tc;
+  for (int k = 0; k < 9; ++k)
+    for (int o = 16; o > 0; o >>= 1) hh[k] = xa(hh[k], __shfl_xor_sync(0xFFFFFFFFu, hh[k], o));
+  if ((tid & 31) == 0)
+    for (int k = 0; k < 9; ++k) s_h[k][tid >> 5] = hh[k];
+  __syncthreads();
+  if (tid == 0) {
+    long long acc = 0;
+    for (int t = 0; t < kClsThreads; ++t) {
+      const long long x = s_run[t];
+      s_run[t] = acc;
+      acc += x;
     }
-    a.result[0] = (double)c;
-    for (int k = 0; k < 9; ++k) a.result[1 + k] = hh[k];
+    a.result[0] = (double)acc;
+    for (int k = 0; k < 9; ++k) {
+      double v = 0.0;
+      for (int w = 0; w < kClsThreads / 32; ++w) v = xa(v, s_h[k][w]);
+      a.result[1 + k] = v;
+    }
     *a.done = 0u;
+  }
+  __syncthreads();
+  long long off = s_run[tid];
+  for (int b = b0; b < b1; ++b) {
+    a.block_offsets[b] = (int32_t)off;
+    off += __ldcg(a.block_count + b);
   }
 }
 

@@ -42,6 +42,10 @@ constexpr float kDc = 2e-6f;        // |c| below this: hemisphere flip ambiguous
 #ifndef RV_PRED
 #define RV_PRED 0  // 1: predicated deposit instead of the per-lane sink word
 #endif
+#ifndef RV_STEP_UNROLL
+#define RV_STEP_UNROLL 1  // unroll of the 64-pair step loop
+#endif
+constexpr int kStepUnroll = RV_STEP_UNROLL;
 
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
@@ -663,7 +667,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
             k0 += 64;
           }
         } else {
-#pragma unroll 1
+#pragma unroll kStepUnroll
           for (; k0 + 64 <= len; k0 += 64) step(k0, std::integral_constant<int, 2>{});
         }
         if (k0 < len) step(k0, std::integral_constant<int, 1>{});
