@@ -226,9 +226,19 @@ VotePlan make_plan(rv_context* c, int G, double E, int J) {
   p.banded = 0;
   // twins j, j+J/2 and 64-aligned pair ranges; queue entries hold the pair in 16 bits
   const bool twins_ok = (J % 128 == 0) && p.halfJ <= 32768;
-  // t + 1.5*2^(23-S) must stay inside [2^(22-S)... 2^(24-S)): t in [-2^(22-S), 2^(22-S))
-  int S = 12;
-  while (S >= 8 && G + 8 >= (1 << (22 - S))) --S;
+  // Fixed-point shift S of the f32 filter (K2 item 2), the largest S <= 13 with
+  //  (range)    t = G/2 + X*K, |X| <= 1, stays inside the magic binade: |t| < 2^(22-S);
+  //  (accuracy) the flag window [-2u, 2u), u = 2^-S, covers the f32 error bound:
+  //             |t32 - t| <= K*6e-7 (inputs, FMUL/FFMA, FADD, rcp.approx) + u/2  <  2u,
+  //             checked with a 10% allowance (6.6e-7). No S -> the exact generic kernel.
+  const double Kc = p.inv_cell;
+  auto shift_ok = [&](int S) {
+    const double half = std::ldexp(1.0, 22 - S);
+    const double lo = 0.5 * G - 1.01 * Kc - 4.0, hi = 0.5 * G + 1.01 * Kc + 4.0;
+    return lo >= -half && hi < half && Kc * 6.6e-7 < 1.5 * std::ldexp(1.0, -S);
+  };
+  int S = 13;
+  while (S >= 8 && !shift_ok(S)) --S;
   if (!twins_ok || S < 8) return p;
   p.frac_shift = S;
   p.frac_mask = ((1u << S) - 1u) & ~3u;

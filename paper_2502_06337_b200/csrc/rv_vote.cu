@@ -8,11 +8,11 @@
 //  * Twins. Samples j and j+J/2 are antipodal, so after the hemisphere flip they land on
 //    the same plane point (up to ~1e-15). K2 evaluates one "pair" per twin and deposits 2.
 //  * f32 filter + exact f64 fallback. The pair is evaluated in f32 from an f64 basis; the
-//    cell coordinate t is produced on a 2^-10 grid by one FFMA against a magic constant.
-//    Worst-case |t32 - t64| <= 2.1e-4 cell (derivation in DESIGN.md), so whenever the
-//    fractional part of t32 is >= 1.46e-3 from an integer (and |c| >= 2e-6, no hemisphere
-//    ambiguity) the f32 cell IS the reference cell. Otherwise the pair is queued and both
-//    twins are recomputed exactly in f64 (same op order, no FMA) -- ~0.6% of pairs.
+//    cell coordinate t is produced on a 2^-S grid (S <= 13, chosen per geometry by make_plan) by
+//    one FFMA against a magic constant. |t32 - t64| <= K*6e-7 + 2^-(S+1) cells, so
+//    whenever t32 is at least 2*2^-S from an integer (and |c| >= 2e-6, no hemisphere ambiguity)
+//    the f32 cell IS the reference cell. Otherwise the pair is queued and both twins are
+//    recomputed exactly in f64 (same op order, no FMA) -- ~0.2% of pairs.
 //  * Band tiling. The grid's reachable rows are split into bands that fit one CTA's shared
 //    memory (u32 counters, 1 CTA/SM). K1 computes per (constraint, band) the pair-index
 //    ranges whose projected points can fall in the band (analytic circle/line intersection,
@@ -801,19 +801,23 @@ void launch_plan(const VotePlan& p, const VoteBuffers& b, int64_t n, cudaStream_
 
 using VoteKernel = void (*)(VotePlan, VoteBuffers, int64_t);
 static VoteKernel vote_kernel_for(const VotePlan& p, int* slot) {
-  // S = 12 (every grid <= 1000) gets a compile-time shift; other S use the run-time variant
-  const int k = (p.clamp ? 2 : 0) + (p.frac_shift == 12 ? 1 : 0);
+  // S = 13 / 12 (every grid <= 1000 at the reference extents) get a compile-time shift; other S
+  // use the run-time variant
+  const int ks = p.frac_shift == 13 ? 2 : (p.frac_shift == 12 ? 1 : 0);
+  const int k = (p.clamp ? 3 : 0) + ks;
   *slot = k;
   switch (k) {
     case 0: return vote_banded_kernel<false, 0>;
     case 1: return vote_banded_kernel<false, 12>;
-    case 2: return vote_banded_kernel<true, 0>;
-    default: return vote_banded_kernel<true, 12>;
+    case 2: return vote_banded_kernel<false, 13>;
+    case 3: return vote_banded_kernel<true, 0>;
+    case 4: return vote_banded_kernel<true, 12>;
+    default: return vote_banded_kernel<true, 13>;
   }
 }
 
 cudaError_t set_vote_smem(const VotePlan& p) {
-  static int configured[4] = {0, 0, 0, 0};  // largest dynamic smem opted in per instantiation
+  static int configured[6] = {0, 0, 0, 0, 0, 0};  // largest dynamic smem opted in per instantiation
   int k;
   VoteKernel f = vote_kernel_for(p, &k);
   if ((int)p.smem_bytes <= configured[k]) return cudaSuccess;

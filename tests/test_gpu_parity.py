@@ -39,11 +39,21 @@ def assert_est_equal(dev, ref: dict):
     (200, 0.9, 1024),    # extent < 1: clamped cells
     (1024, 1.05, 4096),  # finer grid, more bands (run-time fixed-point shift S=11)
     (1100, 0.95, 1024),  # clamped cells with the run-time shift
+    (256, 0.5, 1024),    # small extent: clamped, compile-time S=13
+    (512, 0.2, 1024),    # very small extent: large cell scale K -> run-time S=10
 ])
 def test_accumulate_bit_exact(ctx, port, grid, extent, samples):
     rng = np.random.default_rng(grid + samples)
     z = unit_rows(rng, 3000)
     assert np.array_equal(ctx.accumulate(z, grid, extent, samples), port.accumulate(z, grid, extent, samples))
+
+
+def test_accumulate_bit_exact_large_default(ctx, port):
+    # the f32 filter's error budget is tightest at the default geometry (S=13): 40k random
+    # constraints = 41M sampled pairs against the oracle
+    rng = np.random.default_rng(20250206)
+    z = unit_rows(rng, 40000)
+    assert np.array_equal(ctx.accumulate(z), port.accumulate(z))
 
 
 def test_accumulate_adversarial_constraints(ctx, port):
