@@ -121,8 +121,10 @@ struct rv_context {
   // classify / refine
   DBuf flagsA, flagsB, bcount, bscatter, bdiff, boffA, boffB, cls_result, compact_out;
   DBuf coop_part, coop_state, coop_bar;  // device-resident refine_loop / anneal_axis (rv_coop.cu)
-  DBuf peak_out;                         // chained solve: start axis from the peak (PeakOut)
+  DBuf peak_out;                         // chained solve: device Summary (peak, state, angles)
+  DBuf red_keys;                         // fused argmax scratch of the tile reduction
   int coop_grid = 0;
+  bool coop_bar_ready = false;
   // angles / support
   DBuf bins, raw, angle_counts, angle_sums, angle_result, sup_counts, sup_result, band_flagsA, band_flagsB,
       band_idx, band_vals, near_h, near_result;
@@ -319,9 +321,37 @@ void ensure_tables(rv_context* c, int J) {
   c->table_J = J;
 }
 
+// Device summary of a chained single solve: every scalar the host needs, read back in one copy.
+struct Summary {
+  PeakOut pk;
+  CoopState st;
+  unsigned long long counts[2];
+  double angle[4];
+};
+Summary* summary_buf(rv_context* c) { return c->peak_out.get<Summary>(1); }
+
+// Optional outputs fused into the vote's tile reduction (banded kernel only).
+struct VoteFused {
+  unsigned long long* key_out = nullptr;  // [2]: argmax key, grid sum
+  PeakOut* peak = nullptr;                // start axis (estimate_from_peak)
+  bool done = false;                      // set by vote(): the reduction produced them
+};
+void set_fused(rv_context* c, VoteBuffers& b, VoteFused* f, const VotePlan& p) {
+  if (!f) return;
+  const int vecs = (p.H_max * p.W + 3) / 4;
+  const int bx = std::min((vecs + kReduceThreads - 1) / kReduceThreads, 256);
+  b.red_keys = c->red_keys.get<unsigned long long>((size_t)2 * bx * p.n_bands);
+  b.red_out = f->key_out;
+  b.red_done = c->done_ptr();
+  b.peak = f->peak;
+  b.peak_min_votes = 1u;
+  f->done = true;
+}
+
 // accumulate (voting.cpp:88-118) over device SoA constraints into the context grid.
+// prezeroed: the grid and the band counters were already cleared (by the preprocess kernel).
 uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* zz, int64_t n, int G, double E,
-               int J, bool force_generic = false) {
+               int J, bool force_generic = false, bool prezeroed = false, VoteFused* fused = nullptr) {
   if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no constraints to accumulate");
   if (G < 1 || !(E > 0.0)) fail(RV_ERR_INVALID_CONFIG, "accumulator needs grid >= 1, extent > 0");
   if (J < 1) fail(RV_ERR_INVALID_CONFIG, "theta_samples must be >= 1");
@@ -329,7 +359,8 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   const VotePlan& p = cached_plan(c, G, E, J);
   uint32_t* grid = c->grid.get<uint32_t>((size_t)G * G);
   StageScope sc(c, kVote);
-  ck(cudaMemsetAsync(grid, 0, sizeof(uint32_t) * (size_t)G * G, c->st), "memset grid");
+  if (!prezeroed || !p.banded || force_generic)
+    ck(cudaMemsetAsync(grid, 0, sizeof(uint32_t) * (size_t)G * G, c->st), "memset grid");
   VoteBuffers b;
   b.zx = zx;
   b.zy = zy;
@@ -359,9 +390,12 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   b.max_slots = n_ctas * p.n_bands;
   b.partials = c->partials.get<uint32_t>((size_t)b.max_slots * p.tile_words);
   b.slot_band = c->slot_band.get<int32_t>(b.max_slots);
-  ck(cudaMemsetAsync(b.band_work, 0, sizeof(unsigned long long) * kMaxBands, c->st), "memset band_work");
-  ck(cudaMemsetAsync(b.counters, 0, sizeof(int32_t) * (2 * kMaxBands + 1), c->st), "memset counters");
-  ck(cudaMemsetAsync(b.stats, 0, sizeof(unsigned long long) * 2, c->st), "memset stats");
+  if (!prezeroed) {
+    ck(cudaMemsetAsync(b.band_work, 0, sizeof(unsigned long long) * kMaxBands, c->st), "memset band_work");
+    ck(cudaMemsetAsync(b.counters, 0, sizeof(int32_t) * (2 * kMaxBands + 1), c->st), "memset counters");
+    ck(cudaMemsetAsync(b.stats, 0, sizeof(unsigned long long) * 2, c->st), "memset stats");
+  }
+  set_fused(c, b, fused, p);
   launch_plan(p, b, n, c->st);
   {
     StageScope kv(c, kVoteKernel);
@@ -595,9 +629,15 @@ int32_t* inlier_host_buffer(rv_context* c, size_t n) {
 }
 
 // Launches the cooperative loop; the final state stays on the device (CoopState*).
+struct CoopFused {  // optional work fused into the last pass of refine_loop
+  int32_t* compact_out = nullptr;
+  uint32_t* zero_bins = nullptr;
+  int n_bins = 0;
+  unsigned long long* zero_counts = nullptr;
+};
 CoopState* coop_refine_launch(rv_context* c, const ConstraintSet& cs, const double* axis, const double* axis_dev,
                               int mode, double e0, const rv_config& cfg, uint32_t** flags, int32_t** offsets,
-                              CoopState* state_dst = nullptr) {
+                              CoopState* state_dst = nullptr, const CoopFused* fz = nullptr) {
   StageScope sc(c, kRefine);
   if (c->coop_grid == 0) c->coop_grid = coop_refine_grid(c->sms);
   const int nt = std::max(1, coop_tiles(cs.n));
@@ -608,8 +648,14 @@ CoopState* coop_refine_launch(rv_context* c, const ConstraintSet& cs, const doub
   int32_t* toff = c->boffA.get<int32_t>(nt);
   double* part = c->coop_part.get<double>((size_t)c->coop_grid * 8);
   CoopState* dst = state_dst ? state_dst : c->coop_state.get<CoopState>(1);
+  if (!c->coop_bar_ready) {  // the kernel leaves its barrier counters at zero; clear them once
+    ck(cudaMemsetAsync(c->coop_bar.get<unsigned int>(2), 0, 2 * sizeof(unsigned int), c->st), "coop barrier");
+    c->coop_bar_ready = true;
+  }
   ck(launch_coop_refine(cs.zx, cs.zy, cs.zz, cs.n, mode, cfg.refine ? 1 : 0, cfg.epsilon, e0, axis, axis_dev, fa, fb,
-                        tcount, toff, part, c->coop_bar.get<unsigned int>(2), dst, c->coop_grid, c->st),
+                        tcount, toff, part, c->coop_bar.get<unsigned int>(2), dst, c->coop_grid, c->st, cs.kept,
+                        fz ? fz->compact_out : nullptr, fz ? fz->zero_bins : nullptr, fz ? fz->n_bins : 0,
+                        fz ? fz->zero_counts : nullptr),
      "coop refine launch");
   count_launch(c);
   if (flags) *flags = fa;  // refine_loop: final bitmask in flags0
@@ -772,11 +818,30 @@ Estimate build_candidate_dev(rv_context* c, const double start[3], const uint32_
 struct PreResult {
   ConstraintSet cs;
   int64_t n_dropped = 0;
+  bool vote_zeroed = false;  // the preprocess kernel cleared the vote grid and counters
 };
 
-PreResult preprocess_dev(rv_context* c, const double* d_corrs, int64_t n, double tau_z, int normalize) {
-  StageScope sc(c, kPrep);
+// vcfg (optional): also clear the state of the vote that follows (banded plans).
+PreResult preprocess_dev(rv_context* c, const double* d_corrs, int64_t n, double tau_z, int normalize,
+                         const rv_config* vcfg = nullptr) {
+  bool zeroed = false;
   PrepBuffers b;
+  if (vcfg && vcfg->grid >= 1 && vcfg->extent > 0.0 && vcfg->theta_samples >= 1) {
+    ensure_tables(c, vcfg->theta_samples);
+    const VotePlan& p = cached_plan(c, vcfg->grid, vcfg->extent, vcfg->theta_samples);
+    if (p.banded) {  // the same grow-only buffers vote() will take
+      b.zero_ptr[0] = c->grid.get<uint32_t>((size_t)vcfg->grid * vcfg->grid);
+      b.zero_n[0] = (int64_t)vcfg->grid * vcfg->grid;
+      b.zero_ptr[1] = reinterpret_cast<uint32_t*>(c->band_work.get<unsigned long long>(kMaxBands));
+      b.zero_n[1] = 2 * kMaxBands;
+      b.zero_ptr[2] = reinterpret_cast<uint32_t*>(c->counters.get<int32_t>(2 * kMaxBands + 1));
+      b.zero_n[2] = 2 * kMaxBands + 1;
+      b.zero_ptr[3] = reinterpret_cast<uint32_t*>(c->stats.get<unsigned long long>(2));
+      b.zero_n[3] = 4;
+      zeroed = true;
+    }
+  }
+  StageScope sc(c, kPrep);
   b.corrs = d_corrs;
   b.zx = c->zx.get<double>(n);
   b.zy = c->zy.get<double>(n);
@@ -803,6 +868,7 @@ PreResult preprocess_dev(rv_context* c, const double* d_corrs, int64_t n, double
   r.cs.kept = b.kept;
   r.cs.n = h[0];
   r.n_dropped = h[1];
+  r.vote_zeroed = zeroed;
   return r;
 }
 
@@ -839,6 +905,7 @@ struct PipelinedVote {
   PreResult pre;
   const uint32_t* grid = nullptr;
   const double* d_corrs = nullptr;
+  bool peak_ready = false;  // argmax + start axis fused into the final tile reduction
 };
 
 PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n, const rv_config& cfg) {
@@ -959,6 +1026,11 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
   }
   int32_t* h = reinterpret_cast<int32_t*>(c->pinned);
   if (p.banded) {
+    VoteFused vf;
+    vf.key_out = c->arg_out.get<unsigned long long>(2);
+    vf.peak = &summary_buf(c)->pk;
+    set_fused(c, b, &vf, p);
+    out.peak_ready = vf.done;
     launch_vote_reduce(p, b, c->st);
     count_launch(c);
   }
@@ -982,7 +1054,7 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
 
 // estimate_single from a preprocessed constraint set (identity shortcuts already handled).
 Estimate finish_single(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
-                       const uint32_t* prevoted);
+                       const uint32_t* prevoted, bool peak_ready = false);
 Estimate finish_single_stepped(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
                                const uint32_t* prevoted, int first_attempt);
 Estimate rescue_single(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
@@ -991,7 +1063,7 @@ Estimate rescue_single(rv_context* c, const PreResult& pre, const double* d_corr
 // estimate_single (estimator.cpp:320-371) over device-resident correspondences.
 Estimate estimate_single_dev(rv_context* c, const double* d_corrs, int64_t n, const rv_config& cfg) {
   if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
-  const PreResult pre = preprocess_dev(c, d_corrs, n, cfg.tau_z, cfg.normalize_inputs);
+  const PreResult pre = preprocess_dev(c, d_corrs, n, cfg.tau_z, cfg.normalize_inputs, &cfg);
   if (pre.cs.n == 0) {
     std::vector<int32_t> all(n);
     for (int64_t i = 0; i < n; ++i) all[i] = (int32_t)i;
@@ -1011,7 +1083,7 @@ Estimate estimate_single_host(rv_context* c, const double* h_corrs, int64_t n, c
     return identity_estimate(std::move(all));
   }
   if (pv.pre.n_dropped * 10 >= n * 9) return identity_estimate(dropped_list(c, pv.pre.n_dropped));
-  return finish_single(c, pv.pre, pv.d_corrs, cfg, pv.grid);
+  return finish_single(c, pv.pre, pv.d_corrs, cfg, pv.grid, pv.peak_ready);
 }
 
 // estimate_single after preprocess (estimator.cpp:320-371), chained on the device: vote ->
@@ -1020,21 +1092,20 @@ Estimate estimate_single_host(rv_context* c, const double* h_corrs, int64_t n, c
 // host only validates and finishes (atan2, Rodrigues). Rare cases -- a failed exactness guard
 // (grid sum != N*J), or the rescue path -- continue on the host-stepped path below.
 Estimate finish_single(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
-                       const uint32_t* prevoted) {
+                       const uint32_t* prevoted, bool peak_ready) {
   if (cfg.angle_bins < 8) fail(RV_ERR_INVALID_CONFIG, "angle histogram needs bin_count >= 8");
   const ConstraintSet& cs = pre.cs;
-  const uint32_t* grid = prevoted ? prevoted
-                                  : vote(c, cs.zx, cs.zy, cs.zz, cs.n, cfg.grid, cfg.extent, cfg.theta_samples);
-  // every scalar the host needs lands in one device struct: a single read-back
-  struct Summary {
-    PeakOut pk;
-    CoopState st;
-    unsigned long long counts[2];
-    double angle[4];
-  };
-  Summary* dsum = c->peak_out.get<Summary>(1);
+  Summary* dsum = summary_buf(c);
   PeakOut* pk = &dsum->pk;
-  {
+  const uint32_t* grid = prevoted;
+  if (!prevoted) {  // vote with find_peaks(K=1) + start axis fused into its tile reduction
+    VoteFused vf;
+    vf.key_out = c->arg_out.get<unsigned long long>(2);
+    vf.peak = pk;
+    grid = vote(c, cs.zx, cs.zy, cs.zz, cs.n, cfg.grid, cfg.extent, cfg.theta_samples, false, pre.vote_zeroed, &vf);
+    peak_ready = vf.done;
+  }
+  if (!peak_ready) {
     StageScope sc(c, kPeaks);
     unsigned long long* keys = c->arg_keys.get<unsigned long long>(2 * argmax_block_count());
     unsigned long long* okey = c->arg_out.get<unsigned long long>(2);
@@ -1042,26 +1113,26 @@ Estimate finish_single(rv_context* c, const PreResult& pre, const double* d_corr
     launch_peak_axis(okey, grid, cfg.grid, cfg.extent, 1u, pk, c->st);
     count_launch(c, 2);
   }
-  uint32_t* flags = nullptr;
-  int32_t* offs = nullptr;
-  CoopState* st = coop_refine_launch(c, cs, nullptr, pk->axis, 0, 0.0, cfg, &flags, &offs, &dsum->st);
   int32_t* idx = c->compact_out.get<int32_t>((size_t)std::max<int64_t>(cs.n, 1));
   unsigned long long* cnt = dsum->counts;
   double* res = dsum->angle;
+  uint32_t* bins = c->bins.get<uint32_t>(cfg.angle_bins);
+  CoopFused fz;  // compaction + clearing the angle histogram ride on the last refine pass
+  fz.compact_out = idx;
+  fz.zero_bins = bins;
+  fz.n_bins = cfg.angle_bins;
+  fz.zero_counts = cnt;
+  CoopState* st = coop_refine_launch(c, cs, nullptr, pk->axis, 0, 0.0, cfg, nullptr, nullptr, &dsum->st, &fz);
   {
     StageScope sc(c, kAngles);
     int32_t* hidx = inlier_host_buffer(c, (size_t)std::max<int64_t>(cs.n, 1));
-    launch_compact_flags(flags, cs.n, cs.kept, offs, idx, c->st);
-    uint32_t* bins = c->bins.get<uint32_t>(cfg.angle_bins);
     double* raw = c->raw.get<double>((size_t)std::max<int64_t>(cs.n, 1));
-    ck(cudaMemsetAsync(bins, 0, sizeof(uint32_t) * cfg.angle_bins, c->st), "memset bins");
-    ck(cudaMemsetAsync(cnt, 0, 16, c->st), "memset counts");
     // the angle vote reads the inlier list coalesced and also streams it to mapped host memory
     launch_vote_angles_k(nullptr, d_corrs, idx, cs.n, cfg.angle_bins, cfg.tau_deg, bins, raw, cnt, c->st, st->axis,
                          &st->count, hidx);
     launch_peak_angle_k(bins, cfg.angle_bins, raw, cs.n, c->angle_sums.get<double>(2 * 296), res, c->done_ptr(),
                         c->st, &st->count);
-    count_launch(c, 3);
+    count_launch(c, 2);
   }
   // one summary read-back
   static_assert(sizeof(Summary) <= 4096, "pinned scratch");

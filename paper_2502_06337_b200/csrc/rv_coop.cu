@@ -59,8 +59,14 @@ struct CoopArgs {
   int32_t* tile_count;
   int32_t* tile_offset;
   double* block_part;       // [grid][8]
-  unsigned int* barrier;    // [2] arrival counter, generation (zeroed before launch)
+  unsigned int* barrier;    // [2] arrival / exit counters (zero at launch; the last block to exit resets them)
   State* state;
+  // optional (refine_loop): compaction of the final set fused into the last pass
+  const int32_t* kept;      // kept -> input index map (null: identity)
+  int32_t* compact_out;     // inlier input indices in order (null: only tile offsets)
+  uint32_t* zero_bins;      // angle histogram to clear for the angle vote that follows
+  int n_bins;
+  unsigned long long* zero_counts;  // [2]
 };
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -250,7 +256,57 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
         const int64_t w_lo = t_begin * (kTile / 32), w_hi = min(t_end * (kTile / 32), (a.n + 31) / 32);
         for (int64_t w = w_lo + tid; w < w_hi; w += kThreads) a.flags0[w] = a.flags1[w];
       }
-      if (a.mode == 0 && blockIdx.x == 0) {  // compaction offsets of the final set (tile order)
+      trace(7);
+      if (a.mode == 0 && a.compact_out) {
+        // fused compaction: this block's offset = inliers in tiles [0, t_begin) (tile counts are
+        // final after the last barrier), then its own tiles in order
+        __shared__ long long s_pre[kWarps];
+        long long pre = 0;
+        for (int64_t t = tid; t < t_begin; t += kThreads) pre += __ldcg(a.tile_count + t);
+        for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xFFFFFFFFu, pre, o);
+        if (lane == 0) s_pre[warp] = pre;
+        __syncthreads();  // also orders the flags0 copy above
+        long long off = 0;
+        for (int w = 0; w < kWarps; ++w) off += s_pre[w];
+        // all own flag words at once: block-wide exclusive popc scan, then one warp per word
+        const int64_t nwords = (a.n + 31) / 32;
+        const int64_t w_lo = t_begin * (kTile / 32);
+        const int64_t w_hi = min(t_end * (kTile / 32), nwords);
+        __shared__ int s_wsum[kWarps];
+        for (int64_t c0 = w_lo; c0 < w_hi; c0 += kThreads) {  // chunks of kThreads words
+          const int64_t wi = c0 + tid;
+          const uint32_t word = wi < w_hi ? a.flags0[wi] : 0u;
+          const int cnt = __popc(word);
+          int incl = cnt;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          if (lane == 31) s_wsum[warp] = incl;
+          __syncthreads();
+          int wpre = 0, ctot = 0;
+          for (int w = 0; w < kWarps; ++w) {
+            wpre += w < warp ? s_wsum[w] : 0;
+            ctot += s_wsum[w];
+          }
+          const long long wbase_pos = off + wpre + (incl - cnt);  // first output slot of this word
+          // each thread writes its own word's set bits (independent loads across threads)
+          uint32_t m = word;
+          long long pos = wbase_pos;
+          while (m) {
+            const int bit = __ffs(m) - 1;
+            m &= m - 1u;
+            const int64_t i = wi * 32 + bit;
+            a.compact_out[pos++] = a.kept ? __ldg(a.kept + i) : (int32_t)i;
+          }
+          off += ctot;
+          __syncthreads();
+        }
+        if (blockIdx.x == 0) {
+          for (int k = tid; k < a.n_bins; k += kThreads) a.zero_bins[k] = 0u;
+          if (tid < 2 && a.zero_counts) a.zero_counts[tid] = 0ull;
+        }
+      } else if (a.mode == 0 && blockIdx.x == 0) {  // compaction offsets of the final set (tile order)
         __shared__ long long s_tot[kThreads];
         const int64_t per = (ntiles + kThreads - 1) / kThreads;
         const int64_t t0 = tid * per, t1 = t0 + per < ntiles ? t0 + per : ntiles;
@@ -273,6 +329,15 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
           off += __ldcg(a.tile_count + t);
         }
       }
+      trace(8);
+      // exit: the last block out resets the barrier counters for the next launch
+      if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(a.barrier + 1, 1u) == gridDim.x - 1) {
+          a.barrier[0] = 0u;
+          a.barrier[1] = 0u;
+        }
+      }
       break;
     }
     for (int k = 0; k < 3; ++k) cls_axis[k] = s_next[k];
@@ -282,53 +347,10 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
   }
 }
 
-// estimate_from_peak on the device (single thread): argmax key -> peak cell, interpolate_peak
-// (estimator.cpp:32-47: 3x3 vote-weighted centroid, dy outer / dx inner), backproject
-// (voting.cpp:172-174), canonicalize (geom.cpp:34). Same op order as the host (this TU is
-// compiled without FMA contraction), so the start axis is bit-identical to the host path's.
+// estimate_from_peak on the device (single thread): see exact_peak_axis (rv_exact.cuh).
 __global__ void peak_axis_kernel(const unsigned long long* okey, const uint32_t* grid, int G, double E,
                                  uint32_t min_votes, PeakOut* out) {
-  const unsigned long long key = okey[0];
-  PeakOut r;
-  r.total = okey[1];
-  r.ok = 0;
-  r.ix = r.iy = 0;
-  r.votes = 0;
-  r.A = r.B = 0.0;
-  r.axis[0] = r.axis[1] = 0.0;
-  r.axis[2] = -1.0;
-  const uint32_t best = (uint32_t)(key >> 32);
-  if (key != 0 && best >= min_votes) {
-    const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu);
-    const int iy = (int)idx / G, ix = (int)idx % G;
-    const double cw = 2.0 * E / G;
-    double wsum = 0.0, asum = 0.0, bsum = 0.0;
-    for (int dy = -1; dy <= 1; ++dy)
-      for (int dx = -1; dx <= 1; ++dx) {
-        const int x = ix + dx, y = iy + dy;
-        if (x < 0 || x >= G || y < 0 || y >= G) continue;
-        const double wv = grid[(size_t)y * G + x];
-        const double cA = -E + (x + 0.5) * cw, cB = -E + (y + 0.5) * cw;
-        wsum += wv;
-        asum += wv * cA;
-        bsum += wv * cB;
-      }
-    double A = -E + (ix + 0.5) * cw, B = -E + (iy + 0.5) * cw;
-    if (wsum > 0.0) {
-      A = asum / wsum;
-      B = bsum / wsum;
-    }
-    double b[3];
-    backproject(A, B, b);
-    canonicalize3(b, r.axis);
-    r.A = A;
-    r.B = B;
-    r.ix = ix;
-    r.iy = iy;
-    r.votes = best;
-    r.ok = 1;
-  }
-  *out = r;
+  exact_peak_axis(okey[0], okey[1], grid, G, E, min_votes, out);
 }
 
 }  // namespace
@@ -350,7 +372,9 @@ int coop_tiles(int64_t n) { return (int)((n + kTile - 1) / kTile); }
 cudaError_t launch_coop_refine(const double* zx, const double* zy, const double* zz, int64_t n, int mode, int refine,
                                double eps, double e0, const double axis0[3], const double* axis0_dev,
                                uint32_t* flags0, uint32_t* flags1, int32_t* tile_count, int32_t* tile_offset,
-                               double* block_part, unsigned int* barrier, void* state, int grid, cudaStream_t s) {
+                               double* block_part, unsigned int* barrier, void* state, int grid, cudaStream_t s,
+                               const int32_t* kept, int32_t* compact_out, uint32_t* zero_bins, int n_bins,
+                               unsigned long long* zero_counts) {
   CoopArgs a;
   a.zx = zx;
   a.zy = zy;
@@ -369,10 +393,13 @@ cudaError_t launch_coop_refine(const double* zx, const double* zy, const double*
   a.block_part = block_part;
   a.barrier = barrier;
   a.state = static_cast<State*>(state);
+  a.kept = kept;
+  a.compact_out = compact_out;
+  a.zero_bins = zero_bins;
+  a.n_bins = n_bins;
+  a.zero_counts = zero_counts;
   const int64_t ntiles = (n + kTile - 1) / kTile;
   if (grid > ntiles) grid = (int)(ntiles > 0 ? ntiles : 1);  // every block owns >= 1 tile
-  cudaError_t e = cudaMemsetAsync(barrier, 0, 2 * sizeof(unsigned int), s);
-  if (e != cudaSuccess) return e;
   void* args[] = {&a};
   // cooperative launch: guarantees co-residency of all blocks (required by the grid barrier)
   return cudaLaunchCooperativeKernel((void*)coop_refine_kernel, dim3(grid), dim3(kThreads), args, 0, s);

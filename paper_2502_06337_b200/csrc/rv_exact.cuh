@@ -68,4 +68,65 @@ __device__ __forceinline__ void exact_sample(const double a1[3], const double a2
   *row = exact_cell_of(xm(y, inv), p.E, p.inv_cell, p.G);
 }
 
+// estimate_from_peak (estimator.cpp:94-101) from an argmax key: the peak cell, interpolate_peak
+// (estimator.cpp:32-47: 3x3 vote-weighted centroid, dy outer / dx inner), backproject
+// (voting.cpp:172-174: unproject + normalize), canonicalize (geom.cpp:34) -- every operation
+// explicitly rounded, in the host's order, so the start axis is bit-identical to the host path's.
+__device__ __forceinline__ void exact_peak_axis(unsigned long long key, unsigned long long total,
+                                                const uint32_t* grid, int G, double E, uint32_t min_votes,
+                                                PeakOut* out) {
+  PeakOut r;
+  r.total = total;
+  r.ok = 0;
+  r.ix = r.iy = 0;
+  r.votes = 0;
+  r.A = r.B = 0.0;
+  r.axis[0] = r.axis[1] = 0.0;
+  r.axis[2] = -1.0;
+  const uint32_t best = (uint32_t)(key >> 32);
+  if (key != 0 && best >= min_votes) {
+    const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu);
+    const int iy = (int)idx / G, ix = (int)idx % G;
+    const double cw = xd(xm(2.0, E), (double)G);
+    double wsum = 0.0, asum = 0.0, bsum = 0.0;
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int x = ix + dx, y = iy + dy;
+        if (x < 0 || x >= G || y < 0 || y >= G) continue;
+        const double wv = (double)__ldcg(grid + (size_t)y * G + x);
+        const double cA = xa(-E, xm(xa((double)x, 0.5), cw)), cB = xa(-E, xm(xa((double)y, 0.5), cw));
+        wsum = xa(wsum, wv);
+        asum = xa(asum, xm(wv, cA));
+        bsum = xa(bsum, xm(wv, cB));
+      }
+    double A = xa(-E, xm(xa((double)ix, 0.5), cw)), B = xa(-E, xm(xa((double)iy, 0.5), cw));
+    if (wsum > 0.0) {
+      A = xd(asum, wsum);
+      B = xd(bsum, wsum);
+    }
+    const double AA = xm(A, A), BB = xm(B, B);
+    const double s = xa(xa(1.0, AA), BB);
+    const double u0 = xd(xm(2.0, A), s), u1 = xd(xm(2.0, B), s), u2 = xd(xs(xa(AA, BB), 1.0), s);
+    const double n2 = xa(xa(xm(u0, u0), xm(u1, u1)), xm(u2, u2));
+    double b0 = u0, b1 = u1, b2 = u2;
+    if (n2 > 0.0) {
+      const double q = __dsqrt_rn(n2);
+      b0 = xd(u0, q);
+      b1 = xd(u1, q);
+      b2 = xd(u2, q);
+    }
+    const bool flip = b2 > 0.0;
+    r.axis[0] = flip ? -b0 : b0;
+    r.axis[1] = flip ? -b1 : b1;
+    r.axis[2] = flip ? -b2 : b2;
+    r.A = A;
+    r.B = B;
+    r.ix = ix;
+    r.iy = iy;
+    r.votes = best;
+    r.ok = 1;
+  }
+  *out = r;
+}
+
 }  // namespace rvb

@@ -64,6 +64,13 @@ struct VoteBuffers {
   unsigned long long* stats = nullptr; // [0]=pairs evaluated, [1]=fallback pairs
   int max_slots = 0;
   const int32_t* bounds = nullptr;     // device [lo, hi) of constraints for this launch (null: [0, n))
+  // optional, fused into the tile reduction: argmax key + grid sum (find_peaks K=1 and the
+  // exactness guard) and the start axis (estimate_from_peak)
+  unsigned long long* red_keys = nullptr;  // [2 * reduce blocks] scratch
+  unsigned long long* red_out = nullptr;   // [2]: argmax key, grid sum (null: not computed)
+  unsigned int* red_done = nullptr;        // last-block counter (zero; reset by the kernel)
+  struct PeakOut* peak = nullptr;          // null: no start axis
+  uint32_t peak_min_votes = 1;
 };
 
 // K1: constraint basis (exact f64 -> f32) and band culling plan per constraint.
@@ -91,6 +98,9 @@ struct PrepBuffers {
   int32_t* block_counter = nullptr;      // dynamic block id (zeroed before launch)
   int32_t* totals = nullptr;             // [0]=n_kept [1]=n_dropped
   int32_t* chunk_hi = nullptr;           // optional: kept count through the end of this launch's range
+  // side job: word ranges to clear (the next vote's grid and counters -- saves separate memsets)
+  uint32_t* zero_ptr[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t zero_n[4] = {0, 0, 0, 0};
 };
 int prep_blocks(int64_t n);
 void launch_preprocess(const PrepBuffers& b, int64_t n, double tau_z, int normalize, cudaStream_t s);
@@ -190,6 +200,8 @@ cudaError_t launch_coop_refine(const double* zx, const double* zy, const double*
                                double eps, double e0, const double axis0[3], const double* axis0_dev,
                                uint32_t* flags0, uint32_t* flags1,
                                int32_t* tile_count, int32_t* tile_offset, double* block_part, unsigned int* barrier,
-                               void* state, int grid, cudaStream_t s);
+                               void* state, int grid, cudaStream_t s, const int32_t* kept = nullptr,
+                               int32_t* compact_out = nullptr, uint32_t* zero_bins = nullptr, int n_bins = 0,
+                               unsigned long long* zero_counts = nullptr);
 
 }  // namespace rvb

@@ -30,6 +30,13 @@ __global__ void __launch_bounds__(kPrepThreads) preprocess_kernel(PrepBuffers b,
   __shared__ long long s_excl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_bid = atomicAdd(b.block_counter, 1);
+  {  // side job: clear the next vote's state (grid-stride over the launch's threads)
+    const int64_t gstride = (int64_t)gridDim.x * kPrepThreads, g0 = (int64_t)blockIdx.x * kPrepThreads + tid;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (b.zero_ptr[q])
+        for (int64_t w = g0; w < b.zero_n[q]; w += gstride) b.zero_ptr[q][w] = 0u;
+  }
   __syncthreads();
   const int bid = s_bid;
   const int64_t base = (int64_t)bid * kPrepTile;

@@ -729,6 +729,8 @@ __global__ void __launch_bounds__(kReduceThreads) vote_reduce_kernel(VotePlan p,
   }
   __syncthreads();
   const int ns = s_n;
+  const bool fused = b.red_out != nullptr;
+  unsigned long long best = 0, gsum = 0;
   // 4 words per thread (tile_words is a multiple of 4: slots are 16-byte aligned), 4 slots in flight
   const int nv = (words + 3) / 4;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
@@ -752,11 +754,75 @@ __global__ void __launch_bounds__(kReduceThreads) vote_reduce_kernel(VotePlan p,
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int w = 4 * v + i;
-      if (w < words && a4[i]) {
+      if (w < words) {
         const int row = r0 + w / p.W, col = p.c_min + w % p.W;
-        b.grid[(size_t)row * p.G + col] += a4[i];
+        const size_t gi = (size_t)row * p.G + col;
+        if (fused) {  // final cell value (the exact path may have added to the global grid)
+          const uint32_t val = b.grid[gi] + a4[i];
+          if (a4[i]) b.grid[gi] = val;
+          gsum += val;
+          if (val) best = max(best, ((unsigned long long)val << 32) | (0xFFFFFFFFu - (uint32_t)gi));
+        } else if (a4[i]) {
+          b.grid[gi] += a4[i];
+        }
       }
     }
+  }
+  if (!fused) return;
+  // fused find_peaks(K=1) argmax + exactness-guard sum (argmax_kernel's key: count, then lowest
+  // index), and on the last block estimate_from_peak (exact_peak_axis)
+  __shared__ unsigned long long s_best[kReduceThreads / 32], s_sum[kReduceThreads / 32];
+  __shared__ bool s_last;
+  for (int o = 16; o > 0; o >>= 1) {
+    best = max(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
+    gsum += __shfl_xor_sync(0xFFFFFFFFu, gsum, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_best[threadIdx.x >> 5] = best;
+    s_sum[threadIdx.x >> 5] = gsum;
+  }
+  __syncthreads();
+  const unsigned nblk = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
+  if (threadIdx.x == 0) {
+    unsigned long long bb = 0, ss = 0;
+    for (int w = 0; w < kReduceThreads / 32; ++w) {
+      bb = max(bb, s_best[w]);
+      ss += s_sum[w];
+    }
+    __stcg(b.red_keys + 2 * bid, bb);
+    __stcg(b.red_keys + 2 * bid + 1, ss);
+    __threadfence();
+    s_last = atomicAdd(b.red_done, 1u) == nblk - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  best = 0;
+  gsum = 0;
+  for (unsigned k = threadIdx.x; k < nblk; k += blockDim.x) {
+    best = max(best, __ldcg(b.red_keys + 2 * k));
+    gsum += __ldcg(b.red_keys + 2 * k + 1);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    best = max(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
+    gsum += __shfl_xor_sync(0xFFFFFFFFu, gsum, o);
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    s_best[threadIdx.x >> 5] = best;
+    s_sum[threadIdx.x >> 5] = gsum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long bb = 0, ss = 0;
+    for (int w = 0; w < kReduceThreads / 32; ++w) {
+      bb = max(bb, s_best[w]);
+      ss += s_sum[w];
+    }
+    b.red_out[0] = bb;
+    b.red_out[1] = ss;
+    *b.red_done = 0u;
+    if (b.peak) exact_peak_axis(bb, ss, b.grid, p.G, p.E, b.peak_min_votes, b.peak);
   }
 }
 

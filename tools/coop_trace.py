@@ -24,20 +24,23 @@ for rep in range(2):
     torch.cuda.synchronize()
 n = lib.rv_debug_coop_trace(buf, 8192)
 ev = [(int(x) >> 4, int(x) & 15) for x in buf[:n]]
-ph = {1: [], 2: [], 3: [], 4: [], 5: [], 6: []}
+ph = {1: [], 2: [], 3: [], 4: [], 5: [], 6: [], 7: [], 8: []}
 passes = 0
 for k in range(1, len(ev)):
     t, tag = ev[k]
     tp, tagp = ev[k - 1]
-    if tag in (2, 3, 4, 5, 6) and tagp == tag - 1:
+    if tag in (2, 3, 4, 5, 6, 8) and tagp == tag - 1:
         ph[tag].append(t - tp)
     if tag == 1 and tagp == 6:
         ph[1].append(t - tp)
     if tag == 1:
         passes += 1
-names = {2: "classify", 3: "block reduce", 4: "barrier", 5: "partials reduce", 6: "decision", 1: "loop"}
+names = {2: "classify", 3: "block reduce", 4: "barrier", 5: "partials reduce", 6: "decision", 1: "loop",
+         8: "final flags+compaction"}
 print(f"passes={passes}")
-for tag in (2, 3, 4, 5, 6, 1):
+tail = [(t, tag) for t, tag in ev if tag in (6, 7, 8, 9, 10)]
+print("last events:", [(tag, round((t - tail[-6][0]) / 1e3, 2)) for t, tag in tail[-6:]])
+for tag in (2, 3, 4, 5, 6, 1, 8):
     if ph[tag]:
         a = np.array(ph[tag]) / 1e3
         print(f"{names[tag]:>16}: mean {a.mean():7.2f} us  median {np.median(a):7.2f}  max {a.max():7.2f}  n={a.size}")
