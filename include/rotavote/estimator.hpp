@@ -147,4 +147,22 @@ inline std::vector<RotationEstimate> estimate_multi(std::span<const Corresponden
   return out;
 }
 
+// EXTENSION (not in the reference): one-pass top-K multi-model mode --
+// one vote, find_peaks(K = max_models), the single-model finish per peak and estimate_multi's
+// acceptance rules, without the sequential strip-and-revote. See rv_estimate_multi_onepass.
+inline std::vector<RotationEstimate> estimate_multi_onepass(std::span<const Correspondence> correspondences,
+                                                            const EstimatorConfig& cfg) {
+  if (correspondences.empty()) throw EmptyInput("no correspondences");
+  const std::vector<double> flat = detail::flatten(correspondences);
+  const rv_config c = detail::to_c(cfg);
+  const int cap = cfg.max_models > 0 ? cfg.max_models : 1;
+  std::vector<rv_estimate> es(static_cast<std::size_t>(cap));
+  int32_t nm = 0;
+  detail::check(rv_estimate_multi_onepass(detail::context(), flat.data(),
+                                          static_cast<int64_t>(correspondences.size()), &c, es.data(), cap, &nm));
+  std::vector<RotationEstimate> out;
+  for (int k = 0; k < nm && k < cap; ++k) out.push_back(detail::to_est(es[k], k));
+  return out;
+}
+
 }  // namespace rotavote

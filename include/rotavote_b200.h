@@ -128,6 +128,17 @@ rv_status rv_estimate_multi(rv_context* ctx, const double* corrs, int64_t n, con
 rv_status rv_estimate_multi_device(rv_context* ctx, const double* d_corrs, int64_t n,
                                    const rv_config* cfg, rv_estimate* out, int32_t capacity,
                                    int32_t* n_models);
+/* EXTENSION (no reference counterpart): one-pass top-K multi-model mode.
+ * One vote over all correspondences, find_peaks(K = max_models) with the reference NMS
+ * (voting.cpp:120-170) at peak_vote_floor (estimator.cpp:311-318), then per peak the
+ * single-model finish (estimator.cpp:94-101, :51-92) and estimate_multi's acceptance rules
+ * (consensus floor, model_support coherence, dedupe_overlap; estimator.cpp:411-452) -- without
+ * the sequential strip-and-revote, so K models cost one vote. Models in descending axis_votes. */
+rv_status rv_estimate_multi_onepass(rv_context* ctx, const double* corrs, int64_t n, const rv_config* cfg,
+                                    rv_estimate* out, int32_t capacity, int32_t* n_models);
+rv_status rv_estimate_multi_onepass_device(rv_context* ctx, const double* d_corrs, int64_t n,
+                                           const rv_config* cfg, rv_estimate* out, int32_t capacity,
+                                           int32_t* n_models);
 /* ---- sharded solve (one process per GPU; the caller runs the collectives) ------------- */
 /* Vote of one contiguous shard of the correspondences: preprocess the shard and deposit its
  * constraints' samples into d_grid (grid*grid uint32, device, overwritten). Integer grids of all

@@ -170,6 +170,29 @@ class Context:
                                                        C.byref(nm)))
         return [self._estimate(out[k], k) for k in range(nm.value)]
 
+    def estimate_multi_onepass(self, corrs, cfg: EstimatorConfig | None = None) -> list[RotationEstimate]:
+        """EXTENSION: one vote, top-K NMS peaks, per-peak refine; no re-votes."""
+        cfg = cfg or EstimatorConfig()
+        a = _f64(corrs, 6)
+        cap = max(1, cfg.max_models)
+        out = (rv_estimate * cap)()
+        nm = C.c_int32()
+        c = cfg.to_c()
+        self._check(self._lib.rv_estimate_multi_onepass(self.handle, _ptr(a, C.c_double), a.shape[0] if a.size else 0,
+                                                        C.byref(c), out, cap, C.byref(nm)))
+        return [self._estimate(out[k], k) for k in range(nm.value)]
+
+    def estimate_multi_onepass_device(self, dptr: int, n: int,
+                                      cfg: EstimatorConfig | None = None) -> list[RotationEstimate]:
+        cfg = cfg or EstimatorConfig()
+        cap = max(1, cfg.max_models)
+        out = (rv_estimate * cap)()
+        nm = C.c_int32()
+        c = cfg.to_c()
+        self._check(self._lib.rv_estimate_multi_onepass_device(self.handle, C.c_void_p(dptr), n, C.byref(c), out, cap,
+                                                               C.byref(nm)))
+        return [self._estimate(out[k], k) for k in range(nm.value)]
+
     # ---- sharded solve (device pointers; collectives are the caller's) ----------------------
     def vote_shard(self, dptr: int, n: int, grid_dptr: int, cfg: EstimatorConfig | None = None) -> int:
         """Preprocess + vote one shard into the device grid at grid_dptr; returns kept count."""

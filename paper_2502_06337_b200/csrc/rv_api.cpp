@@ -1239,6 +1239,63 @@ bool near_identity_dev(rv_context* c, const double* d_corrs, const ConstraintSet
   return true;
 }
 
+// One-pass top-K multi-model mode (an extension, not in the reference):
+// ONE vote over all constraints, find_peaks with K = max_models (the reference's greedy NMS with
+// the equatorial mirror, voting.cpp:120-170) at the reference's peak_vote_floor, then per peak
+// the reference's single-model finish (estimate_from_peak + refine_loop + build_estimate) and its
+// acceptance rules (consensus floor, model_support coherence, inlier-overlap dedupe). Unlike the
+// sequential estimate_multi it does not strip inliers and re-vote, so K models cost one vote.
+// Models are returned in peak order (descending axis_votes).
+std::vector<Estimate> estimate_multi_onepass_dev(rv_context* c, const double* d_corrs, int64_t n,
+                                                 const rv_config& cfg) {
+  if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
+  const PreResult pre = preprocess_dev(c, d_corrs, n, cfg.tau_z, cfg.normalize_inputs, &cfg);
+  if (pre.cs.n == 0) fail(RV_ERR_ALL_DEGENERATE, "every correspondence pair is degenerate (x ~ y)");
+  const double chance = cfg.epsilon * (double)pre.cs.n;
+  const int64_t consensus_floor = (int64_t)std::max(2.0, cfg.consensus_floor_mult * chance);
+  const uint32_t* grid = vote(c, pre.cs.zx, pre.cs.zy, pre.cs.zz, pre.cs.n, cfg.grid, cfg.extent,
+                              cfg.theta_samples, false, pre.vote_zeroed);
+  std::vector<Peak> peaks;
+  try {
+    peaks = find_peaks_dev(c, grid, cfg.grid, cfg.extent, std::max(1, cfg.max_models), cfg.suppression_radius,
+                           rv_peak_vote_floor(&cfg, pre.cs.n));
+  } catch (const RvError& e) {
+    if (e.st != RV_ERR_NO_PEAK) throw;
+    return {};
+  }
+  std::vector<Estimate> out;
+  for (const Peak& pk : peaks) {
+    double A, B, b[3], axis[3];
+    interpolate_peak_dev(c, grid, cfg.grid, cfg.extent, pk, &A, &B);
+    backproject(A, B, b);
+    canonicalize3(b, axis);
+    Estimate est;
+    try {
+      const Cls cl = refine_loop_dev(c, pre.cs, axis, cfg);
+      est = build_estimate_dev(c, pre.cs, axis, cl, pk.votes, d_corrs, cfg);
+    } catch (const RvError& e) {
+      if (e.st == RV_ERR_NO_VOTES) continue;
+      throw;
+    }
+    const Support sup = model_support_dev(c, pre.cs, d_corrs, est, cfg, nullptr);
+    if ((int64_t)est.inliers.size() < consensus_floor ||
+        sup.coherent < std::max<int64_t>(8, (int64_t)est.inliers.size() / 5))
+      continue;
+    bool duplicate = false;
+    for (const auto& e : out) {
+      std::vector<int32_t> common;
+      std::set_intersection(e.inliers.begin(), e.inliers.end(), est.inliers.begin(), est.inliers.end(),
+                            std::back_inserter(common));
+      if ((double)common.size() > cfg.dedupe_overlap * (double)est.inliers.size()) {
+        duplicate = true;
+        break;
+      }
+    }
+    if (!duplicate) out.push_back(std::move(est));
+  }
+  return out;
+}
+
 // estimate_multi (estimator.cpp:373-493)
 std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, int64_t n, const rv_config& cfg) {
   if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
@@ -1569,14 +1626,14 @@ rv_status rv_estimate_single(rv_context* c, const double* corrs, int64_t n, cons
 }
 
 static rv_status multi_impl(rv_context* c, const double* d, int64_t n, const rv_config* cfg, rv_estimate* out,
-                            int32_t capacity, int32_t* n_models, bool host) {
+                            int32_t capacity, int32_t* n_models, bool host, bool onepass = false) {
   return guarded(c, [&] {
     cudaSetDevice(c->device);
     c->results.clear();
     *n_models = 0;
     if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
     const double* dd = host ? upload_corrs(c, d, n) : d;
-    std::vector<Estimate> v = estimate_multi_dev(c, dd, n, *cfg);
+    std::vector<Estimate> v = onepass ? estimate_multi_onepass_dev(c, dd, n, *cfg) : estimate_multi_dev(c, dd, n, *cfg);
     const double el = seconds_since(c);
     for (size_t k = 0; k < v.size(); ++k) {
       if ((int32_t)k < capacity) to_c(v[k], out + k, el);
@@ -1596,6 +1653,18 @@ rv_status rv_estimate_multi_device(rv_context* c, const double* d_corrs, int64_t
                                    rv_estimate* out, int32_t capacity, int32_t* n_models) {
   if (!c || !cfg || !out || !n_models || (n > 0 && !d_corrs)) return RV_ERR_INVALID_ARGUMENT;
   return multi_impl(c, d_corrs, n, cfg, out, capacity, n_models, false);
+}
+
+rv_status rv_estimate_multi_onepass(rv_context* c, const double* corrs, int64_t n, const rv_config* cfg,
+                                    rv_estimate* out, int32_t capacity, int32_t* n_models) {
+  if (!c || !cfg || !out || !n_models || (n > 0 && !corrs)) return RV_ERR_INVALID_ARGUMENT;
+  return multi_impl(c, corrs, n, cfg, out, capacity, n_models, true, true);
+}
+
+rv_status rv_estimate_multi_onepass_device(rv_context* c, const double* d_corrs, int64_t n, const rv_config* cfg,
+                                           rv_estimate* out, int32_t capacity, int32_t* n_models) {
+  if (!c || !cfg || !out || !n_models || (n > 0 && !d_corrs)) return RV_ERR_INVALID_ARGUMENT;
+  return multi_impl(c, d_corrs, n, cfg, out, capacity, n_models, false, true);
 }
 
 rv_status rv_vote_shard(rv_context* c, const double* d_corrs, int64_t n, const rv_config* cfg, uint32_t* d_grid,

@@ -279,3 +279,21 @@ def test_full_size_multi_recovers_three(ctx):
     assert len(ms) == 3
     errs = [min(orc.rotation_error_deg(r, m.rotation) for m in ms) for r in rots]
     assert max(errs) < 0.1
+
+
+# ---- one-pass top-K multi-model mode (an extension: no reference twin) ----
+@pytest.mark.gpu
+def test_multi_onepass_recovers_the_sequential_models(ctx, port):
+    corrs, rots, _ = synth.make_config("c5", 50_000)
+    cfg = rv.EstimatorConfig(max_models=3)
+    seq = port.estimate_multi(corrs, orc.default_config(max_models=3))
+    one = ctx.estimate_multi_onepass(corrs, cfg)
+    assert len(one) == len(seq) == 3
+    assert [m.axis_votes for m in one] == sorted([m.axis_votes for m in one], reverse=True)
+    for r in rots:  # every ground-truth rotation is found by both modes to the same accuracy class
+        e_one = min(orc.rotation_error_deg(r, m.rotation) for m in one)
+        e_seq = min(orc.rotation_error_deg(r, m["rotation"]) for m in seq)
+        assert e_one < 0.5 and e_seq < 0.5
+    # the first (strongest) model is the same peak as the sequential first round
+    assert one[0].axis_votes == seq[0]["axis_votes"]
+    assert np.array_equal(one[0].inliers, seq[0]["inliers"])
