@@ -484,6 +484,130 @@ __device__ __forceinline__ void red_shared_if(uint32_t saddr, uint32_t v, bool p
       "r"((uint32_t)pred));
 }
 
+// The work-entry loop of one band tile (shared by the band-tiled vote and the fused front kernel):
+// per-warp dynamic grabs of 32 entries from `counter` (lane k holds entry k: range + f32 basis),
+// 64-pair steps, deposit-always into the tile, exact path for flagged pairs. fetch(j) returns
+// entry j of the band's list (j < n_ent).
+struct VoteCtx {
+  const float2* tab;
+  uint32_t tab_s;
+  uint32_t* tile;
+  uint32_t tile_s, sink_rel, vote2, fbq_s;
+  unsigned lt_mask;
+  int M;
+  uint32_t tile_cells;
+  int hb;
+  const float4* basis_a;
+  const float2* basis_b;
+};
+template <bool kClamp, int kS, class Fetch>
+__device__ __forceinline__ void vote_entries(const VoteCtx& v, const F32Geom& geo, const FbCtx& fc, Fetch fetch,
+                                             int n_ent, int* counter, unsigned int& my_fb) {
+  const int lane = threadIdx.x & 31;
+  const float2* tab = v.tab;
+  const uint32_t tab_s = v.tab_s, tile_s = v.tile_s, sink_rel = v.sink_rel, vote2 = v.vote2, fbq_s = v.fbq_s;
+  const unsigned lt_mask = v.lt_mask;
+  const int M = v.M, hb = v.hb;
+  const uint32_t tile_cells = v.tile_cells;
+  uint32_t* tile = v.tile;
+  for (;;) {  // per-warp dynamic grabs of 32 entries (lane k holds entry k: range + f32 basis)
+    int g0 = 0;
+    if (lane == 0) g0 = atomicAdd(counter, 32);
+    g0 = __shfl_sync(0xFFFFFFFFu, g0, 0);
+    if (g0 >= n_ent) break;
+    const int ne = min(32, n_ent - g0);
+    uint32_t my_ci = 0, my_enc = 0;
+    float4 my_a = make_float4(0.f, 0.f, 0.f, 0.f);
+    float2 my_b = make_float2(0.f, 0.f);
+    if (lane < ne) {
+      const unsigned long long e = fetch(g0 + lane);
+      my_ci = (uint32_t)e;
+      my_enc = (uint32_t)(e >> 32);
+      my_a = v.basis_a[my_ci];
+      my_b = v.basis_b[my_ci];
+    }
+    int qn = 0;
+    for (int k = 0; k < ne; ++k) {
+      const uint32_t enc = __shfl_sync(0xFFFFFFFFu, my_enc, k);
+      float4 ba;
+      float2 bb;
+      ba.x = __shfl_sync(0xFFFFFFFFu, my_a.x, k);
+      ba.y = __shfl_sync(0xFFFFFFFFu, my_a.y, k);
+      ba.z = __shfl_sync(0xFFFFFFFFu, my_a.z, k);
+      ba.w = __shfl_sync(0xFFFFFFFFu, my_a.w, k);
+      bb.x = __shfl_sync(0xFFFFFFFFu, my_b.x, k);
+      bb.y = __shfl_sync(0xFFFFFFFFu, my_b.y, k);
+      const uint32_t local_k = (uint32_t)k << 16;
+      const int start = (int)(enc & 0xFFFFu), len = (int)(enc >> 16);
+      const uint32_t tp_s = tab_s + 8u * (uint32_t)start;
+      // NP pairs per lane per step (32*NP consecutive pairs per warp); ranges are 32-aligned:
+      // 64-pair steps while they fit, then one 32-pair tail step
+      auto step = [&](int k0, auto np_tag) {
+        constexpr int NP = decltype(np_tag)::value;
+        bool flag[NP];
+        uint32_t addr[NP];
+#pragma unroll
+        for (int h = 0; h < NP; ++h) {
+          const uint32_t rel = f32_cell<kClamp, kS>(geo, ba, bb, lds_f2(tp_s + 8u * (uint32_t)(k0 + 32 * h)), &flag[h]);
+          // deposit even if flagged: the exact path undoes it (no select on the flag here)
+#if RV_PRED
+          addr[h] = rel;
+#else
+          addr[h] = tile_s + 4u * umin(rel, sink_rel);
+#endif
+        }
+#pragma unroll
+        for (int h = 0; h < NP; ++h) {
+#if RV_PRED
+          asm volatile("{\n\t.reg .pred q;\n\tsetp.lt.u32 q, %1, %2;\n\t@q red.shared.add.u32 [%0], %3;\n\t}" ::"r"(
+                           tile_s + 4u * addr[h]),
+                       "r"(addr[h]), "r"(tile_cells), "r"(vote2));
+#else
+          red_shared(addr[h], vote2);
+#endif
+        }
+        bool any = false;
+#pragma unroll
+        for (int h = 0; h < NP; ++h) any |= flag[h];
+        if (__any_sync(0xFFFFFFFFu, any)) {  // cold: queue for the exact f64 path
+#pragma unroll
+          for (int h = 0; h < NP; ++h) {
+            const unsigned fm = __ballot_sync(0xFFFFFFFFu, flag[h]);
+            if (flag[h]) {
+              int pair = start + k0 + 32 * h + lane;
+              if (pair >= M) pair -= M;
+              sts_u32(fbq_s + 4u * (uint32_t)(qn + __popc(fm & lt_mask)), local_k | (uint32_t)pair);
+            }
+            qn += __popc(fm);
+            my_fb += __popc(fm);
+            __syncwarp();
+            if (qn >= 32) {
+              fallback_pairs<kClamp, kS>(fc, geo, fbq_s, 32, my_ci, my_a, my_b, tab, tile, tile_cells, hb);
+              qn -= 32;
+              if (lane < qn) sts_u32(fbq_s + 4u * lane, lds_u32(fbq_s + 4u * (32 + lane)));
+              __syncwarp();
+            }
+          }
+        }
+      };
+      int k0 = 0;
+      if constexpr (RV_NP == 4) {
+#pragma unroll 1
+        for (; k0 + 128 <= len; k0 += 128) step(k0, std::integral_constant<int, 4>{});
+        if (k0 + 64 <= len) {
+          step(k0, std::integral_constant<int, 2>{});
+          k0 += 64;
+        }
+      } else {
+#pragma unroll kStepUnroll
+        for (; k0 + 64 <= len; k0 += 64) step(k0, std::integral_constant<int, 2>{});
+      }
+      if (k0 < len) step(k0, std::integral_constant<int, 1>{});
+    }
+    if (qn > 0) fallback_pairs<kClamp, kS>(fc, geo, fbq_s, qn, my_ci, my_a, my_b, tab, tile, tile_cells, hb);
+  }
+}
+
 // K2: persistent, one CTA per SM, 16 warps. A CTA owns one row band's u32 tile in shared
 // memory at a time. Warps grab 32 work entries at a time from the band's entry list (K1 appends
 // one entry per non-empty (constraint, band) pair range; lane k loads entry k and its f32 basis,
@@ -578,102 +702,8 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     const unsigned long long* ebase = b.entries + (int64_t)band * b.entry_cap;
     const int n_ent = b.entry_count[band];
     int* counter = &b.counters[1 + band];
-    for (;;) {  // per-warp dynamic grabs of 32 entries (lane k holds entry k: range + f32 basis)
-      int g0 = 0;
-      if (lane == 0) g0 = atomicAdd(counter, 32);
-      g0 = __shfl_sync(0xFFFFFFFFu, g0, 0);
-      if (g0 >= n_ent) break;
-      const int ne = min(32, n_ent - g0);
-      uint32_t my_ci = 0, my_enc = 0;
-      float4 my_a = make_float4(0.f, 0.f, 0.f, 0.f);
-      float2 my_b = make_float2(0.f, 0.f);
-      if (lane < ne) {
-        const unsigned long long e = __ldcs(ebase + g0 + lane);
-        my_ci = (uint32_t)e;
-        my_enc = (uint32_t)(e >> 32);
-        my_a = b.basis_a[my_ci];
-        my_b = b.basis_b[my_ci];
-      }
-      int qn = 0;
-      for (int k = 0; k < ne; ++k) {
-        const uint32_t enc = __shfl_sync(0xFFFFFFFFu, my_enc, k);
-        float4 ba;
-        float2 bb;
-        ba.x = __shfl_sync(0xFFFFFFFFu, my_a.x, k);
-        ba.y = __shfl_sync(0xFFFFFFFFu, my_a.y, k);
-        ba.z = __shfl_sync(0xFFFFFFFFu, my_a.z, k);
-        ba.w = __shfl_sync(0xFFFFFFFFu, my_a.w, k);
-        bb.x = __shfl_sync(0xFFFFFFFFu, my_b.x, k);
-        bb.y = __shfl_sync(0xFFFFFFFFu, my_b.y, k);
-        const uint32_t local_k = (uint32_t)k << 16;
-        const int start = (int)(enc & 0xFFFFu), len = (int)(enc >> 16);
-        const uint32_t tp_s = tab_s + 8u * (uint32_t)start;
-        // NP pairs per lane per step (32*NP consecutive pairs per warp); ranges are 32-aligned:
-        // 64-pair steps while they fit, then one 32-pair tail step
-        auto step = [&](int k0, auto np_tag) {
-          constexpr int NP = decltype(np_tag)::value;
-          bool flag[NP];
-          uint32_t addr[NP];
-#pragma unroll
-          for (int h = 0; h < NP; ++h) {
-            const uint32_t rel = f32_cell<kClamp, kS>(geo, ba, bb, lds_f2(tp_s + 8u * (uint32_t)(k0 + 32 * h)), &flag[h]);
-            // deposit even if flagged: the exact path undoes it (no select on the flag here)
-#if RV_PRED
-            addr[h] = rel;
-#else
-            addr[h] = tile_s + 4u * umin(rel, sink_rel);
-#endif
-          }
-#pragma unroll
-          for (int h = 0; h < NP; ++h) {
-#if RV_PRED
-            asm volatile("{\n\t.reg .pred q;\n\tsetp.lt.u32 q, %1, %2;\n\t@q red.shared.add.u32 [%0], %3;\n\t}" ::"r"(
-                             tile_s + 4u * addr[h]),
-                         "r"(addr[h]), "r"(tile_cells), "r"(vote2));
-#else
-            red_shared(addr[h], vote2);
-#endif
-          }
-          bool any = false;
-#pragma unroll
-          for (int h = 0; h < NP; ++h) any |= flag[h];
-          if (__any_sync(0xFFFFFFFFu, any)) {  // cold: queue for the exact f64 path
-#pragma unroll
-            for (int h = 0; h < NP; ++h) {
-              const unsigned fm = __ballot_sync(0xFFFFFFFFu, flag[h]);
-              if (flag[h]) {
-                int pair = start + k0 + 32 * h + lane;
-                if (pair >= M) pair -= M;
-                sts_u32(fbq_s + 4u * (uint32_t)(qn + __popc(fm & lt_mask)), local_k | (uint32_t)pair);
-              }
-              qn += __popc(fm);
-              my_fb += __popc(fm);
-              __syncwarp();
-              if (qn >= 32) {
-                fallback_pairs<kClamp, kS>(fc, geo, fbq_s, 32, my_ci, my_a, my_b, tab, tile, tile_cells, hb);
-                qn -= 32;
-                if (lane < qn) sts_u32(fbq_s + 4u * lane, lds_u32(fbq_s + 4u * (32 + lane)));
-                __syncwarp();
-              }
-            }
-          }
-        };
-        int k0 = 0;
-        if constexpr (RV_NP == 4) {
-#pragma unroll 1
-          for (; k0 + 128 <= len; k0 += 128) step(k0, std::integral_constant<int, 4>{});
-          if (k0 + 64 <= len) {
-            step(k0, std::integral_constant<int, 2>{});
-            k0 += 64;
-          }
-        } else {
-#pragma unroll kStepUnroll
-          for (; k0 + 64 <= len; k0 += 64) step(k0, std::integral_constant<int, 2>{});
-        }
-        if (k0 < len) step(k0, std::integral_constant<int, 1>{});
-      }
-      if (qn > 0) fallback_pairs<kClamp, kS>(fc, geo, fbq_s, qn, my_ci, my_a, my_b, tab, tile, tile_cells, hb);
-    }
+    VoteCtx v{tab, tab_s, tile, tile_s, sink_rel, vote2, fbq_s, lt_mask, M, tile_cells, hb, b.basis_a, b.basis_b};
+    vote_entries<kClamp, kS>(v, geo, fc, [&](int j) { return __ldcs(ebase + j); }, n_ent, counter, my_fb);
     // band exhausted for this CTA: flush the tile to a partial slot, steal the next band
     __syncthreads();
     if (tid == 0) {
