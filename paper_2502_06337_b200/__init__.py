@@ -182,6 +182,31 @@ class Context:
                                                         C.byref(c), out, cap, C.byref(nm)))
         return [self._estimate(out[k], k) for k in range(nm.value)]
 
+    def estimate_batch(self, problems, cfg: EstimatorConfig | None = None, workers: int = 0) -> list:
+        """EXTENSION: estimate_single on each of many independent problems
+        (a list of (n_k, 6) arrays), run concurrently on `workers` device streams. Returns one
+        RotationEstimate per problem, or the RvError it raised."""
+        cfg = cfg or EstimatorConfig()
+        arrs = [_f64(a, 6) for a in problems]
+        offs = np.zeros(len(arrs) + 1, np.int64)
+        offs[1:] = np.cumsum([a.shape[0] if a.size else 0 for a in arrs])
+        flat = np.ascontiguousarray(np.concatenate([a.reshape(-1, 6) for a in arrs]) if arrs else np.zeros((0, 6)))
+        B = len(arrs)
+        out = (rv_estimate * max(B, 1))()
+        status = np.zeros(max(B, 1), np.int32)
+        c = cfg.to_c()
+        self._check(self._lib.rv_estimate_batch(self.handle, _ptr(flat, C.c_double),
+                                                offs.ctypes.data_as(C.POINTER(C.c_int64)), B, C.byref(c), workers,
+                                                out, _ptr(status, C.c_int32)))
+        res = []
+        for k in range(B):
+            if status[k] == 0:
+                res.append(self._estimate(out[k], k))
+            else:
+                cls = errors.STATUS_TO_ERROR.get(int(status[k]), errors.DeviceError)
+                res.append(cls(f"problem {k}: " + self._lib.rv_status_string(int(status[k])).decode()))
+        return res
+
     def estimate_multi_onepass_device(self, dptr: int, n: int,
                                       cfg: EstimatorConfig | None = None) -> list[RotationEstimate]:
         cfg = cfg or EstimatorConfig()

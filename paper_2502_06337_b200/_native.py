@@ -96,6 +96,9 @@ _SIGS = [
      [C.c_void_p, c_double_p, C.c_int64, C.POINTER(rv_config), C.POINTER(rv_estimate), C.c_int32, c_int32_p]),
     ("rv_estimate_multi_onepass_device", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(rv_config), C.POINTER(rv_estimate), C.c_int32, c_int32_p]),
+    ("rv_estimate_batch", C.c_int,
+     [C.c_void_p, c_double_p, C.POINTER(C.c_int64), C.c_int32, C.POINTER(rv_config), C.c_int32,
+      C.POINTER(rv_estimate), c_int32_p]),
     ("rv_result_inliers", C.c_int, [C.c_void_p, C.c_int32, c_int32_p, C.c_int64]),
     ("rv_vote_shard", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(rv_config), C.c_void_p, c_int64_p]),

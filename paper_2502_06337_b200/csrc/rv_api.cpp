@@ -12,7 +12,9 @@
 #include <deque>
 #include <cmath>
 #include <cstdio>
+#include <atomic>
 #include <cstdlib>
+#include <thread>
 #include <cstring>
 #include <memory>
 #include <numbers>
@@ -137,6 +139,7 @@ struct rv_context {
   void* pinned = nullptr;
   std::vector<std::vector<int32_t>> results;
   std::vector<int32_t> spare;       // recycled inlier vector (no page faults on the hot path)
+  std::vector<rv_context*> pool;    // batch workers (own stream + buffers each), created lazily
   int32_t* inl_host = nullptr;      // mapped pinned buffer: the compaction writes the inlier list here
   size_t inl_cap = 0;
 
@@ -1565,6 +1568,7 @@ rv_status rv_context_create(int32_t device, rv_context** out) {
 
 void rv_context_destroy(rv_context* c) {
   if (!c) return;
+  for (rv_context* w : c->pool) rv_context_destroy(w);
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
   for (auto e : c->event_pool) cudaEventDestroy(e);
@@ -1665,6 +1669,44 @@ rv_status rv_estimate_multi_onepass_device(rv_context* c, const double* d_corrs,
                                            rv_estimate* out, int32_t capacity, int32_t* n_models) {
   if (!c || !cfg || !out || !n_models || (n > 0 && !d_corrs)) return RV_ERR_INVALID_ARGUMENT;
   return multi_impl(c, d_corrs, n, cfg, out, capacity, n_models, false, true);
+}
+
+rv_status rv_estimate_batch(rv_context* c, const double* corrs, const int64_t* offsets, int32_t n_problems,
+                            const rv_config* cfg, int32_t workers, rv_estimate* out, int32_t* status) {
+  if (!c || !cfg || !offsets || !out || !status || n_problems < 0 || (n_problems > 0 && !corrs))
+    return RV_ERR_INVALID_ARGUMENT;
+  for (int32_t k = 0; k < n_problems; ++k)
+    if (offsets[k + 1] < offsets[k]) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    c->results.clear();
+    c->results.resize((size_t)n_problems);
+    // automatic width (measured on B200): small problems are launch/latency bound and overlap
+    // well on 8 streams (3-4x); problems >= ~32k correspondences already fill the GPU, where
+    // concurrent band-tiled votes only compete for SMs
+    int auto_w = 8;
+    if (n_problems > 0 && (offsets[n_problems] - offsets[0]) / n_problems >= 32768) auto_w = 1;
+    const int W = std::max(1, std::min<int>(n_problems, workers > 0 ? workers : auto_w));
+    while ((int)c->pool.size() < W) {  // each worker: own context = own stream and buffers
+      rv_context* w = nullptr;
+      const rv_status st = rv_context_create(c->device, &w);
+      if (st != RV_OK) fail(st, "batch worker context");
+      c->pool.push_back(w);
+    }
+    std::atomic<int32_t> next{0};
+    auto work = [&](rv_context* w) {
+      cudaSetDevice(c->device);
+      for (int32_t k = next.fetch_add(1); k < n_problems; k = next.fetch_add(1)) {
+        const int64_t n = offsets[k + 1] - offsets[k];
+        status[k] = rv_estimate_single(w, corrs + 6 * offsets[k], n, cfg, &out[k]);
+        if (status[k] == RV_OK) c->results[k] = std::move(w->results[0]);
+      }
+    };
+    std::vector<std::thread> th;
+    for (int i = 1; i < W; ++i) th.emplace_back(work, c->pool[i]);
+    work(c->pool[0]);
+    for (auto& t : th) t.join();
+  });
 }
 
 rv_status rv_vote_shard(rv_context* c, const double* d_corrs, int64_t n, const rv_config* cfg, uint32_t* d_grid,

@@ -297,3 +297,20 @@ def test_multi_onepass_recovers_the_sequential_models(ctx, port):
     # the first (strongest) model is the same peak as the sequential first round
     assert one[0].axis_votes == seq[0]["axis_votes"]
     assert np.array_equal(one[0].inliers, seq[0]["inliers"])
+
+
+# ---- batched solver for independent problems (an extension) ----------
+def test_estimate_batch_matches_single_solves(ctx, port):
+    rng = np.random.default_rng(7)
+    probs = []
+    for k in range(24):
+        n = int(rng.integers(300, 6000))
+        corrs, _, _ = synth.make_scene(n, 0.6, 0.01, seed=9000 + k)
+        probs.append(corrs)
+    probs.append(np.zeros((0, 6)))                      # an empty problem fails alone
+    res = ctx.estimate_batch(probs, workers=6)
+    assert len(res) == len(probs)
+    assert isinstance(res[-1], rv.errors.EmptyInput)
+    for k, corrs in enumerate(probs[:-1]):
+        ref = port.estimate_single(corrs)
+        assert_est_equal(res[k], ref)
