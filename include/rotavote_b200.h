@@ -150,6 +150,21 @@ rv_status rv_estimate_multi_onepass_device(rv_context* ctx, const double* d_corr
  * rv_result_inliers(ctx, k, ...) its inlier indices, relative to offsets[k]. */
 rv_status rv_estimate_batch(rv_context* ctx, const double* corrs, const int64_t* offsets, int32_t n_problems,
                             const rv_config* cfg, int32_t workers, rv_estimate* out, int32_t* status);
+/* ---- baselines: consensus scoring on the device ---------------- */
+/* consensus_count (baselines.cpp:16-24) of m candidate axes (m x 3) over n constraints (n x 3):
+ * counts_out[k] = #{i : |axes_k . z_i| < epsilon} (strict; the reference's op order). */
+rv_status rv_consensus_counts(rv_context* ctx, const double* axes, int32_t m, const double* z, int64_t n,
+                              double epsilon, uint32_t* counts_out);
+/* pair<Vec3,int> grid_oracle_axis(span<const Vec3>, const OracleConfig&) -- baselines.hpp:38-39,
+ * baselines.cpp:159-174: exhaustive consensus over the Fibonacci layout of oracle_direction
+ * (baselines.cpp:150-157); ties keep the lowest direction index. */
+rv_status rv_grid_oracle_axis(rv_context* ctx, const double* z, int64_t n, int32_t directions, double epsilon,
+                              double axis_out[3], int32_t* count_out);
+/* RotationEstimate ransac_rotation(span<const Correspondence>, int iterations, double epsilon,
+ * uint64_t seed) -- baselines.hpp:22-23, baselines.cpp:31-109: the same seeded hypothesis stream
+ * (std::mt19937_64), all hypotheses scored on the device at once, then the reference's refit. */
+rv_status rv_ransac_rotation(rv_context* ctx, const double* corrs, int64_t n, int32_t iterations, double epsilon,
+                             uint64_t seed, rv_estimate* out);
 /* ---- sharded solve (one process per GPU; the caller runs the collectives) ------------- */
 /* Vote of one contiguous shard of the correspondences: preprocess the shard and deposit its
  * constraints' samples into d_grid (grid*grid uint32, device, overwritten). Integer grids of all

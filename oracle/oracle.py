@@ -168,6 +168,28 @@ class Oracle:
         self._ck(f(_p(zz, C.c_double), C.c_int64(zz.shape[0]), _p(out, C.c_double)), "refine_axis")
         return out
 
+    # ---- baselines (reference library only: baselines.cpp) ----------------------------------
+    def grid_oracle_axis(self, z, directions=10000, eps=0.015):
+        assert self.kind != "port", "baselines are checked against the compiled reference only"
+        zz = np.ascontiguousarray(z, dtype=np.float64).reshape(-1, 3)
+        ax = np.empty(3)
+        cnt = C.c_int32()
+        f = self._fn("grid_oracle_axis")
+        f.restype = C.c_int
+        self._ck(f(_p(zz, C.c_double), C.c_int64(zz.shape[0]), C.c_int32(directions), C.c_double(eps),
+                   _p(ax, C.c_double), C.byref(cnt)), "grid_oracle_axis")
+        return ax, cnt.value
+
+    def ransac_rotation(self, corrs, iterations=1000, eps=0.015, seed=0):
+        assert self.kind != "port", "baselines are checked against the compiled reference only"
+        a = np.ascontiguousarray(corrs, dtype=np.float64).reshape(-1, 6)
+        e = EstRef()
+        f = self._fn("ransac_rotation")
+        f.restype = C.c_int
+        self._ck(f(_p(a, C.c_double), C.c_int64(a.shape[0]), C.c_int32(iterations), C.c_double(eps),
+                   C.c_uint64(seed), C.byref(e)), "ransac_rotation")
+        return self._est(e)
+
     # ---- solver --------------------------------------------------------------------------
     def _est(self, e):
         inl = np.ctypeslib.as_array(e.inliers, shape=(e.n_inliers,)).copy() if e.n_inliers else np.zeros(0, np.int32)

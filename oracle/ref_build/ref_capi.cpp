@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "rotavote/errors.hpp"
+#include "rotavote/baselines.hpp"
 #include "rotavote/estimator.hpp"
 #include "rotavote/voting.hpp"
 
@@ -195,6 +196,23 @@ int64_t ref_classify_inliers(const double axis[3], const double* z, int64_t n, d
   const auto v = classify_inliers(Vec3(axis[0], axis[1], axis[2]), to_vecs(z, n), eps);
   std::memcpy(out, v.data(), sizeof(int32_t) * v.size());
   return static_cast<int64_t>(v.size());
+}
+
+int ref_grid_oracle_axis(const double* z, int64_t n, int32_t directions, double eps, double axis_out[3],
+                         int32_t* count_out) {
+  return guarded([&] {
+    OracleConfig oc;
+    oc.directions = directions;
+    oc.epsilon = eps;
+    const auto r = grid_oracle_axis(to_vecs(z, n), oc);
+    for (int k = 0; k < 3; ++k) axis_out[k] = r.first(k);
+    *count_out = r.second;
+  });
+}
+
+int ref_ransac_rotation(const double* corrs, int64_t n, int32_t iterations, double eps, uint64_t seed,
+                        ref_estimate* out) {
+  return guarded([&] { fill(ransac_rotation(to_corrs(corrs, n), iterations, eps, seed), out); });
 }
 
 int ref_refine_axis(const double* z, int64_t n, double axis_out[3]) {

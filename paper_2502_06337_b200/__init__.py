@@ -207,6 +207,34 @@ class Context:
                 res.append(cls(f"problem {k}: " + self._lib.rv_status_string(int(status[k])).decode()))
         return res
 
+    # ---- baselines (reference baselines.hpp) -------------------------
+    def consensus_counts(self, axes, z, epsilon: float = 0.015) -> np.ndarray:
+        """consensus_count (baselines.cpp:16-24) of every axis over z, on the device."""
+        a = _f64(axes, 3)
+        zz = _f64(z, 3)
+        out = np.zeros(a.shape[0] if a.size else 0, np.uint32)
+        self._check(self._lib.rv_consensus_counts(self.handle, _ptr(a, C.c_double), out.size, _ptr(zz, C.c_double),
+                                                  zz.shape[0] if zz.size else 0, epsilon,
+                                                  out.ctypes.data_as(C.POINTER(C.c_uint32))))
+        return out
+
+    def grid_oracle_axis(self, z, directions: int = 10000, epsilon: float = 0.015) -> tuple[np.ndarray, int]:
+        """grid_oracle_axis (baselines.hpp:38-39): best Fibonacci direction and its consensus."""
+        zz = _f64(z, 3)
+        ax = np.zeros(3)
+        cnt = C.c_int32()
+        self._check(self._lib.rv_grid_oracle_axis(self.handle, _ptr(zz, C.c_double), zz.shape[0] if zz.size else 0,
+                                                  directions, epsilon, _ptr(ax, C.c_double), C.byref(cnt)))
+        return ax, int(cnt.value)
+
+    def ransac_rotation(self, corrs, iterations: int = 1000, epsilon: float = 0.015, seed: int = 0) -> RotationEstimate:
+        """ransac_rotation (baselines.hpp:22-23): the reference's seeded stream, scored on the device."""
+        a = _f64(corrs, 6)
+        e = rv_estimate()
+        self._check(self._lib.rv_ransac_rotation(self.handle, _ptr(a, C.c_double), a.shape[0] if a.size else 0,
+                                                 iterations, epsilon, C.c_uint64(seed), C.byref(e)))
+        return self._estimate(e, 0)
+
     def estimate_multi_onepass_device(self, dptr: int, n: int,
                                       cfg: EstimatorConfig | None = None) -> list[RotationEstimate]:
         cfg = cfg or EstimatorConfig()

@@ -99,6 +99,12 @@ _SIGS = [
     ("rv_estimate_batch", C.c_int,
      [C.c_void_p, c_double_p, C.POINTER(C.c_int64), C.c_int32, C.POINTER(rv_config), C.c_int32,
       C.POINTER(rv_estimate), c_int32_p]),
+    ("rv_consensus_counts", C.c_int,
+     [C.c_void_p, c_double_p, C.c_int32, c_double_p, C.c_int64, C.c_double, C.POINTER(C.c_uint32)]),
+    ("rv_grid_oracle_axis", C.c_int,
+     [C.c_void_p, c_double_p, C.c_int64, C.c_int32, C.c_double, c_double_p, c_int32_p]),
+    ("rv_ransac_rotation", C.c_int,
+     [C.c_void_p, c_double_p, C.c_int64, C.c_int32, C.c_double, C.c_uint64, C.POINTER(rv_estimate)]),
     ("rv_result_inliers", C.c_int, [C.c_void_p, C.c_int32, c_int32_p, C.c_int64]),
     ("rv_vote_shard", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(rv_config), C.c_void_p, c_int64_p]),

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <atomic>
 #include <cstdlib>
+#include <random>
 #include <thread>
 #include <cstring>
 #include <memory>
@@ -125,6 +126,7 @@ struct rv_context {
   DBuf coop_part, coop_state, coop_bar;  // device-resident refine_loop / anneal_axis (rv_coop.cu)
   DBuf peak_out;                         // chained solve: device Summary (peak, state, angles)
   DBuf red_keys;                         // fused argmax scratch of the tile reduction
+  DBuf cons_axes, cons_counts, cons_z, cons_idx;  // baseline consensus scoring
   int coop_grid = 0;
   bool coop_bar_ready = false;
   // angles / support
@@ -1706,6 +1708,215 @@ rv_status rv_estimate_batch(rv_context* c, const double* corrs, const int64_t* o
     for (int i = 1; i < W; ++i) th.emplace_back(work, c->pool[i]);
     work(c->pool[0]);
     for (auto& t : th) t.join();
+  });
+}
+
+// ---- baselines (reference baselines.cpp) ------------------------------
+// Consensus scoring of many axes is the O(M*N) part and runs on the device (consensus_kernel);
+// the hypothesis generation of ransac_rotation is the reference's sequential RNG stream on the
+// host (std::mt19937_64 + std::uniform_int_distribution, libstdc++ -- the same stream).
+std::vector<uint32_t> consensus_counts_dev(rv_context* c, const double* h_axes, int m, const double* d_z_aos,
+                                           int64_t n, double eps) {
+  std::vector<uint32_t> out((size_t)std::max(m, 0));
+  if (m <= 0) return out;
+  double* da = c->cons_axes.get<double>((size_t)3 * m);
+  uint32_t* dc = c->cons_counts.get<uint32_t>((size_t)m);
+  ck(cudaMemcpyAsync(da, h_axes, sizeof(double) * 3 * m, cudaMemcpyHostToDevice, c->st), "H2D axes");
+  ck(cudaMemsetAsync(dc, 0, sizeof(uint32_t) * m, c->st), "memset counts");
+  launch_consensus_counts(da, m, d_z_aos, n, eps, dc, c->sms, c->st);
+  count_launch(c);
+  ck(cudaMemcpyAsync(out.data(), dc, sizeof(uint32_t) * m, cudaMemcpyDeviceToHost, c->st), "D2H counts");
+  sync(c);
+  return out;
+}
+
+const double* upload_aos(rv_context* c, DBuf& buf, const double* h, int64_t n_doubles) {
+  double* d = buf.get<double>((size_t)std::max<int64_t>(n_doubles, 1));
+  if (n_doubles > 0)
+    ck(cudaMemcpyAsync(d, h, sizeof(double) * n_doubles, cudaMemcpyHostToDevice, c->st), "H2D");
+  return d;
+}
+
+// oracle_direction (baselines.cpp:150-157): Fibonacci spiral over the southern hemisphere.
+void oracle_direction_host(int k, int directions, double out[3]) {
+  constexpr double golden_angle = 2.399963229728653;
+  const double cz = -(k + 0.5) / directions;
+  const double sz = std::sqrt(std::max(0.0, 1.0 - cz * cz));
+  const double phi = golden_angle * k;
+  out[0] = sz * std::cos(phi);
+  out[1] = sz * std::sin(phi);
+  out[2] = cz;
+}
+
+// correspondence_angle (angles.cpp:36-44) on the host, the reference's op order; false =
+// DegenerateProjection.
+bool corr_angle_host(const double a[3], const double* x, const double* y, double tau, double* angle) {
+  double b[3], g[3], bg[3];
+  cross3(a, x, b);
+  cross3(a, y, g);
+  if (std::sqrt(dot3(b, b)) <= tau || std::sqrt(dot3(g, g)) <= tau) return false;
+  cross3(b, g, bg);
+  *angle = std::atan2(dot3(bg, a), dot3(b, g));
+  return true;
+}
+
+rv_status rv_grid_oracle_axis(rv_context* c, const double* z, int64_t n, int32_t directions, double epsilon,
+                              double axis_out[3], int32_t* count_out) {
+  if (!c || !axis_out || !count_out || (n > 0 && !z)) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no constraints");
+    if (directions < 100) fail(RV_ERR_INVALID_CONFIG, "oracle needs at least 100 directions");
+    std::vector<double> dirs((size_t)3 * directions);
+    for (int k = 0; k < directions; ++k) oracle_direction_host(k, directions, &dirs[3 * (size_t)k]);
+    const double* dz = upload_aos(c, c->cons_z, z, 3 * n);
+    const std::vector<uint32_t> cnt = consensus_counts_dev(c, dirs.data(), directions, dz, n, epsilon);
+    int best = -1, bk = 0;  // strict '>' in direction order: ties keep the lowest index
+    for (int k = 0; k < directions; ++k)
+      if ((int)cnt[k] > best) {
+        best = (int)cnt[k];
+        bk = k;
+      }
+    std::memcpy(axis_out, &dirs[3 * (size_t)bk], sizeof(double) * 3);
+    *count_out = best;
+  });
+}
+
+rv_status rv_consensus_counts(rv_context* c, const double* axes, int32_t m, const double* z, int64_t n,
+                              double epsilon, uint32_t* counts_out) {
+  if (!c || m < 0 || n < 0 || (m > 0 && (!axes || !counts_out)) || (n > 0 && !z)) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (m == 0) return;
+    if (n == 0) {
+      std::memset(counts_out, 0, sizeof(uint32_t) * m);
+      return;
+    }
+    const double* dz = upload_aos(c, c->cons_z, z, 3 * n);
+    const std::vector<uint32_t> cnt = consensus_counts_dev(c, axes, m, dz, n, epsilon);
+    std::memcpy(counts_out, cnt.data(), sizeof(uint32_t) * m);
+  });
+}
+
+rv_status rv_ransac_rotation(rv_context* c, const double* corrs, int64_t n, int32_t iterations, double epsilon,
+                             uint64_t seed, rv_estimate* out) {
+  if (!c || !out || (n > 0 && !corrs)) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    c->results.clear();
+    constexpr double kTauZ = 1e-9, kTauDeg = 1e-6;
+    if (n < 2) fail(RV_ERR_NO_CONSENSUS, "need at least two correspondences");
+    // preprocess(correspondences, kTauZ, true) -- estimator.cpp:259-285 op order, on the host:
+    // the hypothesis stream below consumes z sequentially anyway
+    std::vector<double> z;
+    std::vector<int32_t> kept;
+    z.reserve((size_t)3 * n);
+    kept.reserve((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+      double x[3] = {corrs[6 * i], corrs[6 * i + 1], corrs[6 * i + 2]};
+      double y[3] = {corrs[6 * i + 3], corrs[6 * i + 4], corrs[6 * i + 5]};
+      const double nx = std::sqrt(dot3(x, x)), ny = std::sqrt(dot3(y, y));
+      if (nx > 0.0)
+        for (double& v : x) v /= nx;
+      if (ny > 0.0)
+        for (double& v : y) v /= ny;
+      const double d[3] = {y[0] - x[0], y[1] - x[1], y[2] - x[2]};
+      const double len = std::sqrt(dot3(d, d));
+      if (len < kTauZ) continue;
+      z.push_back(d[0] / len);
+      z.push_back(d[1] / len);
+      z.push_back(d[2] / len);
+      kept.push_back((int32_t)i);
+    }
+    const size_t nz = kept.size();
+    if (nz < 2) fail(RV_ERR_NO_CONSENSUS, "fewer than two usable constraints");
+    // hypotheses: the reference's loop (baselines.cpp:41-77) minus the scoring
+    std::mt19937_64 rng(seed);
+    std::uniform_int_distribution<std::size_t> pick(0, nz - 1);
+    std::vector<double> axes;
+    std::vector<double> angles;
+    const long attempt_cap = 50L * iterations + 100;
+    long attempts = 0;
+    for (int it = 0; it < iterations && attempts < attempt_cap; ++it) {
+      ++attempts;
+      const std::size_t i = pick(rng);
+      const std::size_t j = pick(rng);
+      if (i == j) {
+        --it;
+        continue;
+      }
+      double ax[3];
+      cross3(&z[3 * i], &z[3 * j], ax);
+      const double nrm = std::sqrt(dot3(ax, ax));
+      if (nrm <= 1e-9) {
+        --it;
+        continue;
+      }
+      const double u[3] = {ax[0] / nrm, ax[1] / nrm, ax[2] / nrm};
+      double a[3];
+      canonicalize3(u, a);
+      double angle;
+      const double* cr = corrs + 6 * (size_t)kept[i];
+      if (!corr_angle_host(a, cr, cr + 3, kTauDeg, &angle)) {
+        --it;
+        continue;
+      }
+      axes.insert(axes.end(), a, a + 3);
+      angles.push_back(angle);
+    }
+    const int m = (int)angles.size();
+    const double* dz = upload_aos(c, c->cons_z, z.data(), (int64_t)z.size());
+    const std::vector<uint32_t> score = consensus_counts_dev(c, axes.data(), m, dz, (int64_t)nz, epsilon);
+    int best_score = 0, bk = -1;
+    for (int k = 0; k < m; ++k)
+      if ((int)score[k] > best_score) {
+        best_score = (int)score[k];
+        bk = k;
+      }
+    if (best_score < 2) fail(RV_ERR_NO_CONSENSUS, "best hypothesis explains fewer than two constraints");
+    double best_axis[3] = {axes[3 * bk], axes[3 * bk + 1], axes[3 * bk + 2]};
+    double best_angle = angles[bk];
+    // local refit (baselines.cpp:80-94): classify, refine_axis on the consensus set, reclassify
+    const ConstraintSet cs = upload_constraints(c, z.data(), (int64_t)nz);
+    auto classify = [&](const double* axis) {
+      const Cls cl = classify_dev(c, cs, axis, epsilon, 0, nullptr, 0);
+      std::vector<int32_t> v((size_t)cl.count);
+      int32_t* idx = compact_dev(c, cs, cl);
+      if (cl.count) ck(cudaMemcpyAsync(v.data(), idx, 4 * cl.count, cudaMemcpyDeviceToHost, c->st), "D2H");
+      sync(c);
+      return std::make_pair(v, cl);
+    };
+    auto [inl, cl] = classify(best_axis);
+    if (inl.size() >= 2) {
+      double refit[3];
+      if (axis_from_scatter(cl.scatter, refit)) {  // RankDeficient: keep the hypothesis axis
+        std::memcpy(best_axis, refit, sizeof refit);
+        inl = classify(best_axis).first;
+      }
+    }
+    Estimate est;
+    est.inliers.reserve(inl.size());
+    for (int32_t i : inl) est.inliers.push_back(kept[(size_t)i]);
+    try {  // vote_angles + peak_angle(refine) over the inliers; NoVotes keeps the sample angle
+      const double* dcorr = upload_aos(c, c->corrs, corrs, 6 * n);
+      int32_t* didx = c->cons_idx.get<int32_t>(std::max<size_t>(est.inliers.size(), 1));
+      if (!est.inliers.empty())
+        ck(cudaMemcpyAsync(didx, est.inliers.data(), 4 * est.inliers.size(), cudaMemcpyHostToDevice, c->st), "H2D");
+      rv_config acfg;
+      rv_config_default(&acfg);
+      acfg.angle_bins = 1024;
+      acfg.tau_deg = kTauDeg;
+      acfg.refine = 1;
+      best_angle = angle_dev(c, best_axis, dcorr, didx, (int64_t)est.inliers.size(), acfg);
+    } catch (const RvError& e) {
+      if (e.st != RV_ERR_NO_VOTES) throw;
+    }
+    std::memcpy(est.axis, best_axis, sizeof est.axis);
+    est.angle = best_angle;
+    rodrigues3(est.axis, est.angle, est.R);
+    est.votes = (uint32_t)best_score;
+    to_c(est, out, seconds_since(c));
+    c->results.push_back(std::move(est.inliers));
   });
 }
 

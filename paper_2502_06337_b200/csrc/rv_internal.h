@@ -153,6 +153,10 @@ void launch_model_support_k(const double* zx, const double* zy, const double* zz
                             const double* corrs, int64_t n, const double axis[3], double angle, double eps, double tau,
                             uint32_t* band_flags, int32_t* block_counts, int32_t* result, unsigned int* done,
                             cudaStream_t s);
+// consensus_count (baselines.cpp:16-24) of m axes (AoS m x 3) over n constraints (AoS n x 3); counts
+// must be zeroed. Exact: f32 filter with an f64 re-check near the band edge.
+void launch_consensus_counts(const double* axes, int m, const double* z, int64_t n, double eps, uint32_t* counts,
+                             int sms, cudaStream_t s);
 void launch_strip_k(const double* zx, const double* zy, const double* zz, int64_t n, const double axis[3], double strip,
                     uint8_t* removed, cudaStream_t s);
 void launch_strip_identity_k(const double* corrs, const int32_t* kept, int64_t n, int normalize, uint8_t* removed,

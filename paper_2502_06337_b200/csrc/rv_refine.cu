@@ -589,9 +589,72 @@ __global__ void __launch_bounds__(kClsThreads) near_identity_kernel(NearArgs a) 
   }
 }
 
+// Consensus counts of many candidate axes over one constraint set (baselines.cpp:16-24 consensus_count,
+// the scoring of grid_oracle_axis and ransac_rotation): count_k = #{i : |a_k . z_i| < eps}, strict,
+// with the reference's op order. Threads own axes (one register counter each); z is staged through
+// shared memory in tiles (f32 for the filter, f64 for the exact re-check): a pair whose f32 dot is
+// within kConsDelta of eps is re-evaluated exactly (|d32 - d64| <= ~4e-7 for unit vectors).
+constexpr int kConsAxes = 256;   // axes per block (threads)
+constexpr int kConsTile = 1024;  // constraints per shared-memory tile
+constexpr double kConsDelta = 4e-6;
+__global__ void __launch_bounds__(kConsAxes) consensus_kernel(const double* axes, int m, const double* z, int64_t n,
+                                                             int64_t z_per_block, double eps, uint32_t* counts) {
+  __shared__ float s_z32[kConsTile][3];
+  __shared__ double s_z64[kConsTile][3];
+  const int k = blockIdx.y * kConsAxes + threadIdx.x;
+  double a0 = 0, a1 = 0, a2 = 0;
+  if (k < m) {
+    a0 = axes[3 * k];
+    a1 = axes[3 * k + 1];
+    a2 = axes[3 * k + 2];
+  }
+  const float f0 = (float)a0, f1 = (float)a1, f2 = (float)a2;
+  const float lo = (float)(eps - kConsDelta), hi = (float)(eps + kConsDelta);
+  uint32_t cnt = 0;
+  const int64_t z0 = (int64_t)blockIdx.x * z_per_block, z1 = z0 + z_per_block < n ? z0 + z_per_block : n;
+  for (int64_t t0 = z0; t0 < z1; t0 += kConsTile) {
+    const int len = (int)(z1 - t0 < kConsTile ? z1 - t0 : (int64_t)kConsTile);
+    __syncthreads();
+    for (int q = threadIdx.x; q < 3 * len; q += blockDim.x) {
+      const double v = z[3 * t0 + q];
+      s_z64[q / 3][q % 3] = v;
+      s_z32[q / 3][q % 3] = (float)v;
+    }
+    __syncthreads();
+    if (k < m) {
+#pragma unroll 4
+      for (int i = 0; i < len; ++i) {
+        const float d = fabsf(fmaf(f2, s_z32[i][2], fmaf(f1, s_z32[i][1], f0 * s_z32[i][0])));
+        if (d < lo) {
+          ++cnt;
+        } else if (d < hi) {  // near the band edge: the reference's exact evaluation
+          const double dd = xa(xa(xm(a0, s_z64[i][0]), xm(a1, s_z64[i][1])), xm(a2, s_z64[i][2]));
+          if (fabs(dd) < eps) ++cnt;
+        }
+      }
+    }
+  }
+  if (k < m && cnt) atomicAdd(counts + k, cnt);
+}
+
 }  // namespace
 
 int classify_blocks(int64_t n) { return (int)((n + kClsPerBlock - 1) / kClsPerBlock); }
+
+void launch_consensus_counts(const double* axes, int m, const double* z, int64_t n, double eps, uint32_t* counts,
+                             int sms, cudaStream_t s) {
+  if (m <= 0 || n <= 0) return;
+  const int by = (m + kConsAxes - 1) / kConsAxes;
+  // enough z-blocks for ~4 blocks per SM overall, each a multiple of the tile
+  int64_t bx = (4LL * sms + by - 1) / by;
+  const int64_t tiles = (n + kConsTile - 1) / kConsTile;
+  if (bx > tiles) bx = tiles;
+  if (bx < 1) bx = 1;
+  int64_t per = (n + bx - 1) / bx;
+  per = (per + kConsTile - 1) / kConsTile * kConsTile;
+  bx = (n + per - 1) / per;
+  consensus_kernel<<<dim3((unsigned)bx, (unsigned)by), kConsAxes, 0, s>>>(axes, m, z, n, per, eps, counts);
+}
 
 void launch_classify_mode(const double* zx, const double* zy, const double* zz, int64_t n, const double axis[3],
                           double eps, int mode, const ClassifyOut& o, int32_t* block_offsets, unsigned int* done,

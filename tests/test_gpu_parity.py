@@ -314,3 +314,37 @@ def test_estimate_batch_matches_single_solves(ctx, port):
     for k, corrs in enumerate(probs[:-1]):
         ref = port.estimate_single(corrs)
         assert_est_equal(res[k], ref)
+
+
+# ---- baseline consensus kernels vs the compiled reference -----------
+def test_grid_oracle_axis_matches_reference(ctx, ref):
+    corrs, _, _ = synth.make_config("c2", 20_000)
+    z, _, _ = ref.preprocess(corrs)
+    ax_r, cnt_r = ref.grid_oracle_axis(z, 2000, 0.015)
+    ax_d, cnt_d = ctx.grid_oracle_axis(z, 2000, 0.015)
+    assert cnt_d == cnt_r and np.array_equal(ax_d, ax_r)
+
+
+def test_consensus_counts_exact_at_band_edges(ctx, ref):
+    rng = np.random.default_rng(3)
+    z = unit_rows(rng, 5000)
+    axes = unit_rows(rng, 300)
+    # constraints placed exactly at |a.z| = eps +- 1 ulp-ish for the first axis
+    a0 = axes[0]
+    t = np.cross(a0, [0.0, 0.0, 1.0])
+    t /= np.linalg.norm(t)
+    edge = np.array([np.cos(np.arcsin(e)) * t + e * a0 for e in (0.015, 0.015 - 1e-12, 0.015 + 1e-12, -0.015)])
+    z = np.concatenate([z, edge])
+    got = ctx.consensus_counts(axes, z, 0.015)
+    want = np.array([len(ref.classify_inliers(a, z, 0.015)) for a in axes], np.uint32)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("seed", [0, 7])
+def test_ransac_rotation_matches_reference(ctx, ref, seed):
+    corrs, _, _ = synth.make_config("c1")
+    r = ref.ransac_rotation(corrs, 300, 0.015, seed)
+    d = ctx.ransac_rotation(corrs, 300, 0.015, seed)
+    assert d.axis_votes == r["axis_votes"]
+    assert np.array_equal(d.inliers, r["inliers"])
+    assert orc.rotation_error_deg(d.rotation, r["rotation"]) <= ROT_TOL_DEG
