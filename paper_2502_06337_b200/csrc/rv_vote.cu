@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <type_traits>
 
 #include "rv_exact.cuh"
@@ -913,14 +914,22 @@ static VoteKernel vote_kernel_for(const VotePlan& p, int* slot) {
 }
 
 cudaError_t set_vote_smem(const VotePlan& p) {
-  static int configured[6] = {0, 0, 0, 0, 0, 0};  // largest dynamic smem opted in per instantiation
+  // largest dynamic smem opted in, per (device, instantiation): the attribute is per device, and
+  // worker threads of one process (batch API) may race here
+  constexpr int kDevs = 16;
+  static int configured[kDevs][6] = {};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
   int k;
   VoteKernel f = vote_kernel_for(p, &k);
-  if ((int)p.smem_bytes <= configured[k]) return cudaSuccess;
+  std::lock_guard<std::mutex> lock(mu);
+  int* slot = dev >= 0 && dev < kDevs ? &configured[dev][k] : nullptr;
+  if (slot && (int)p.smem_bytes <= *slot) return cudaSuccess;
   const cudaError_t e =
       cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)p.smem_bytes);
-  if (e == cudaSuccess) configured[k] = (int)p.smem_bytes;
+  if (e == cudaSuccess && slot) *slot = (int)p.smem_bytes;
   return e;
 }
 
