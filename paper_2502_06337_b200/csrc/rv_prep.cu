@@ -16,10 +16,11 @@
 namespace rvb {
 namespace {
 
-constexpr int kPrepThreads = 256;
-constexpr int kPrepPer = 4;                             // elements per thread (r-major in the block)
+constexpr int kPrepThreads = 512;
+constexpr int kPrepPer = 2;                             // elements per thread (r-major in the block)
 constexpr int kPrepTile = kPrepThreads * kPrepPer;      // 1024 correspondences per block
 constexpr int kPrepWarps = kPrepThreads / 32;
+static_assert(kPrepPer * kPrepWarps == 32, "one warp scans the (round, warp) counts");
 
 template <bool kVec>
 __global__ void __launch_bounds__(kPrepThreads) preprocess_kernel(PrepBuffers b, int64_t n, int64_t elem_hi,
