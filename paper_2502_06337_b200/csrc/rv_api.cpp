@@ -332,6 +332,7 @@ struct Summary {
   CoopState st;
   unsigned long long counts[2];
   double angle[4];
+  unsigned long long n_kept;  // in-order constraint sets: kept pairs, counted by the preprocess
 };
 Summary* summary_buf(rv_context* c) { return c->peak_out.get<Summary>(1); }
 
@@ -343,9 +344,7 @@ struct VoteFused {
 };
 void set_fused(rv_context* c, VoteBuffers& b, VoteFused* f, const VotePlan& p) {
   if (!f) return;
-  const int vecs = (p.H_max * p.W + 3) / 4;
-  const int bx = std::min((vecs + kReduceThreads - 1) / kReduceThreads, 256);
-  b.red_keys = c->red_keys.get<unsigned long long>((size_t)2 * bx * p.n_bands);
+  b.red_keys = c->red_keys.get<unsigned long long>((size_t)2 * vote_reduce_blocks_x(p) * p.n_bands);
   b.red_out = f->key_out;
   b.red_done = c->done_ptr();
   b.peak = f->peak;
@@ -824,7 +823,21 @@ struct PreResult {
   ConstraintSet cs;
   int64_t n_dropped = 0;
   bool vote_zeroed = false;  // the preprocess kernel cleared the vote grid and counters
+  bool inorder = false;      // cs = all n pairs in input order (z = NaN: dropped), kept = null;
+                             // the kept count is only on the device (Summary::n_kept)
 };
+
+// The side job of the preprocess kernel: clear the state of the banded vote that follows.
+void set_vote_zeroing(rv_context* c, int G, PrepBuffers* b) {
+  b->zero_ptr[0] = c->grid.get<uint32_t>((size_t)G * G);
+  b->zero_n[0] = (int64_t)G * G;
+  b->zero_ptr[1] = reinterpret_cast<uint32_t*>(c->band_work.get<unsigned long long>(kMaxBands));
+  b->zero_n[1] = 2 * kMaxBands;
+  b->zero_ptr[2] = reinterpret_cast<uint32_t*>(c->counters.get<int32_t>(2 * kMaxBands + 1));
+  b->zero_n[2] = 2 * kMaxBands + 1;
+  b->zero_ptr[3] = reinterpret_cast<uint32_t*>(c->stats.get<unsigned long long>(2));
+  b->zero_n[3] = 4;
+}
 
 // vcfg (optional): also clear the state of the vote that follows (banded plans).
 PreResult preprocess_dev(rv_context* c, const double* d_corrs, int64_t n, double tau_z, int normalize,
@@ -835,14 +848,7 @@ PreResult preprocess_dev(rv_context* c, const double* d_corrs, int64_t n, double
     ensure_tables(c, vcfg->theta_samples);
     const VotePlan& p = cached_plan(c, vcfg->grid, vcfg->extent, vcfg->theta_samples);
     if (p.banded) {  // the same grow-only buffers vote() will take
-      b.zero_ptr[0] = c->grid.get<uint32_t>((size_t)vcfg->grid * vcfg->grid);
-      b.zero_n[0] = (int64_t)vcfg->grid * vcfg->grid;
-      b.zero_ptr[1] = reinterpret_cast<uint32_t*>(c->band_work.get<unsigned long long>(kMaxBands));
-      b.zero_n[1] = 2 * kMaxBands;
-      b.zero_ptr[2] = reinterpret_cast<uint32_t*>(c->counters.get<int32_t>(2 * kMaxBands + 1));
-      b.zero_n[2] = 2 * kMaxBands + 1;
-      b.zero_ptr[3] = reinterpret_cast<uint32_t*>(c->stats.get<unsigned long long>(2));
-      b.zero_n[3] = 4;
+      set_vote_zeroing(c, vcfg->grid, &b);
       zeroed = true;
     }
   }
@@ -875,6 +881,48 @@ PreResult preprocess_dev(rv_context* c, const double* d_corrs, int64_t n, double
   r.n_dropped = h[1];
   r.vote_zeroed = zeroed;
   return r;
+}
+
+// In-order preprocess (single solves with a banded plan): z written at the input index with NaN
+// for dropped pairs, no compaction, no host sync -- the kept count lands in Summary::n_kept and
+// the host reads it with the solve's one summary. The vote's state is cleared as a side job.
+bool banded_plan(rv_context* c, const rv_config& cfg) {
+  if (cfg.grid < 1 || !(cfg.extent > 0.0) || cfg.theta_samples < 1) return false;
+  ensure_tables(c, cfg.theta_samples);
+  return cached_plan(c, cfg.grid, cfg.extent, cfg.theta_samples).banded;
+}
+
+PrepBuffers inorder_buffers(rv_context* c, const double* d_corrs, int64_t n) {
+  PrepBuffers b;
+  b.corrs = d_corrs;
+  b.zx = c->zx.get<double>(n);
+  b.zy = c->zy.get<double>(n);
+  b.zz = c->zz.get<double>(n);
+  b.kept_total = &summary_buf(c)->n_kept;
+  ck(cudaMemsetAsync(b.kept_total, 0, sizeof(unsigned long long), c->st), "memset kept count");
+  return b;
+}
+
+PreResult inorder_result(const PrepBuffers& b, int64_t n) {
+  PreResult r;
+  r.cs.zx = b.zx;
+  r.cs.zy = b.zy;
+  r.cs.zz = b.zz;
+  r.cs.kept = nullptr;
+  r.cs.n = n;
+  r.vote_zeroed = true;
+  r.inorder = true;
+  return r;
+}
+
+PreResult preprocess_inorder_dev(rv_context* c, const double* d_corrs, int64_t n, const rv_config& cfg) {
+  PrepBuffers b = inorder_buffers(c, d_corrs, n);
+  set_vote_zeroing(c, cfg.grid, &b);
+  StageScope sc(c, kPrep);
+  launch_preprocess_inorder(b, n, 0, n, cfg.tau_z, cfg.normalize_inputs, c->st);
+  count_launch(c);
+  ck(cudaGetLastError(), "preprocess");
+  return inorder_result(b, n);
 }
 
 const double* upload_corrs(rv_context* c, const double* corrs, int64_t n) {
@@ -960,34 +1008,20 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
     ck(cudaEventRecord(c->chunk_events[k], c->copy_st), "record chunk");
   };
   issue_copy(0);
-  // preprocess state
-  PrepBuffers pb;
-  pb.corrs = d;
-  pb.zx = c->zx.get<double>(n);
-  pb.zy = c->zy.get<double>(n);
-  pb.zz = c->zz.get<double>(n);
-  pb.kept = c->kept.get<int32_t>(n);
-  pb.dropped = c->dropped.get<int32_t>(n);
-  const int nb_prep = prep_blocks(n);
-  pb.status = c->status.get<unsigned long long>(nb_prep);
-  int32_t* misc = c->misc32.get<int32_t>(8);
-  pb.block_counter = misc;
-  pb.totals = misc + 2;
-  int32_t* chunk_hi = c->chunk_hi.get<int32_t>(C + 1);
-  ck(cudaMemsetAsync(pb.status, 0, sizeof(unsigned long long) * nb_prep, c->st), "memset status");
-  ck(cudaMemsetAsync(misc, 0, sizeof(int32_t) * 8, c->st), "memset misc");
-  ck(cudaMemsetAsync(chunk_hi, 0, sizeof(int32_t) * (C + 1), c->st), "memset chunk_hi");
-  // vote state
   uint32_t* grid = c->grid.get<uint32_t>((size_t)G * G);
   VoteBuffers b;
-  b.zx = pb.zx;
-  b.zy = pb.zy;
-  b.zz = pb.zz;
   b.grid = grid;
   b.table64 = c->table64.get<double2>(J);
   b.table32 = c->table32.get<float2>(std::max(J / 2, 1));
-  int n_ctas = c->sms;
+  int32_t* h = reinterpret_cast<int32_t*>(c->pinned);
   if (p.banded) {
+    // in-order constraint set: chunk k's z land at their input indices, so each chunk's plan and
+    // vote cover exactly [bounds[k], bounds[k+1]) -- no device-side chunk bounds, no host sync
+    PrepBuffers pb = inorder_buffers(c, d, n);
+    set_vote_zeroing(c, G, &pb);  // chunk 0's preprocess clears the vote state
+    b.zx = pb.zx;
+    b.zy = pb.zy;
+    b.zz = pb.zz;
     b.basis_a = c->basis_a.get<float4>(n);
     b.basis_b = c->basis_b.get<float2>(n);
     b.entry_cap = 2 * n;
@@ -997,40 +1031,30 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
     b.entry_count = b.counters + kMaxBands + 1;
     b.stats = c->stats.get<unsigned long long>(2);
     const int64_t est_pairs = (n / C) * (int64_t)p.halfJ;
-    n_ctas = (int)std::clamp<int64_t>(est_pairs >> 20, std::min(p.n_bands, c->sms), c->sms);
+    const int n_ctas = (int)std::clamp<int64_t>(est_pairs >> 20, std::min(p.n_bands, c->sms), c->sms);
     b.max_slots = C * n_ctas * p.n_bands;
     b.partials = c->partials.get<uint32_t>((size_t)b.max_slots * p.tile_words);
     b.slot_band = c->slot_band.get<int32_t>(b.max_slots);
-    ck(cudaMemsetAsync(b.band_work, 0, sizeof(unsigned long long) * kMaxBands, c->st), "memset band_work");
-    ck(cudaMemsetAsync(b.counters, 0, sizeof(int32_t) * (2 * kMaxBands + 1), c->st), "memset counters");
-    ck(cudaMemsetAsync(b.stats, 0, sizeof(unsigned long long) * 2, c->st), "memset stats");
-  }
-  ck(cudaMemsetAsync(grid, 0, sizeof(uint32_t) * (size_t)G * G, c->st), "memset grid");
-  for (int k = 0; k < C; ++k) {
-    ck(cudaStreamWaitEvent(c->st, c->chunk_events[k], 0), "wait chunk");
-    pb.chunk_hi = chunk_hi + k + 1;
-    launch_preprocess_range(pb, n, bounds[k], bounds[k + 1], cfg.tau_z, cfg.normalize_inputs, c->st);
-    count_launch(c);
-    if (p.banded) {
-      b.bounds = chunk_hi + k;
-      const int64_t cap = bounds[k + 1] - bounds[k];
+    for (int k = 0; k < C; ++k) {
+      ck(cudaStreamWaitEvent(c->st, c->chunk_events[k], 0), "wait chunk");
+      launch_preprocess_inorder(pb, n, bounds[k], bounds[k + 1], cfg.tau_z, cfg.normalize_inputs, c->st);
+      if (k == 0)
+        for (int q = 0; q < 4; ++q) pb.zero_ptr[q] = nullptr;
       // entry lists and their counters are per chunk (reused: the stream orders chunk k's vote
       // before chunk k+1's plan)
-      if (k > 0)
-        launch_zero_i32(b.counters + 1, 2 * kMaxBands, c->st);
+      if (k > 0) launch_zero_i32(b.counters + 1, 2 * kMaxBands, c->st);
+      b.range_lo = bounds[k];
+      const int64_t cap = bounds[k + 1] - bounds[k];
       launch_plan(p, b, cap, c->st);
       {
         StageScope kv(c, kVoteKernel);
         launch_vote_banded(p, b, cap, n_ctas, c->st);
       }
-      count_launch(c, 2);
+      count_launch(c, k > 0 ? 4 : 3);
+      // copy k+1 is issued after compute k is queued: with pinned input both run concurrently;
+      // with pageable input the host stages copy k+1 while the device computes chunk k
+      if (k + 1 < C) issue_copy(k + 1);
     }
-    // copy k+1 is issued after compute k is queued: with pinned input both run concurrently;
-    // with pageable input the host stages copy k+1 while the device computes chunk k
-    if (k + 1 < C) issue_copy(k + 1);
-  }
-  int32_t* h = reinterpret_cast<int32_t*>(c->pinned);
-  if (p.banded) {
     VoteFused vf;
     vf.key_out = c->arg_out.get<unsigned long long>(2);
     vf.peak = &summary_buf(c)->pk;
@@ -1038,36 +1062,76 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
     out.peak_ready = vf.done;
     launch_vote_reduce(p, b, c->st);
     count_launch(c);
-  }
-  ck(cudaGetLastError(), "pipelined vote");
-  ck(cudaMemcpyAsync(h, pb.totals, 8, cudaMemcpyDeviceToHost, c->st), "totals D2H");
-  sync(c);
-  out.pre.cs.zx = pb.zx;
-  out.pre.cs.zy = pb.zy;
-  out.pre.cs.zz = pb.zz;
-  out.pre.cs.kept = pb.kept;
-  out.pre.cs.n = h[0];
-  out.pre.n_dropped = h[1];
-  if (!p.banded && out.pre.cs.n > 0)  // generic path: vote once all constraints are in
-    out.grid = vote(c, pb.zx, pb.zy, pb.zz, out.pre.cs.n, G, cfg.extent, J);
-  else
+    ck(cudaGetLastError(), "pipelined vote");
+    out.pre = inorder_result(pb, n);
     out.grid = grid;
-  c->times.vote_samples += out.pre.cs.n * (int64_t)J;
-  c->times.vote_launches += 1;
+  } else {  // generic vote: compacting preprocess, then one vote once all constraints are in
+    PrepBuffers pb;
+    pb.corrs = d;
+    pb.zx = c->zx.get<double>(n);
+    pb.zy = c->zy.get<double>(n);
+    pb.zz = c->zz.get<double>(n);
+    pb.kept = c->kept.get<int32_t>(n);
+    pb.dropped = c->dropped.get<int32_t>(n);
+    const int nb_prep = prep_blocks(n);
+    pb.status = c->status.get<unsigned long long>(nb_prep);
+    int32_t* misc = c->misc32.get<int32_t>(8);
+    pb.block_counter = misc;
+    pb.totals = misc + 2;
+    ck(cudaMemsetAsync(pb.status, 0, sizeof(unsigned long long) * nb_prep, c->st), "memset status");
+    ck(cudaMemsetAsync(misc, 0, sizeof(int32_t) * 8, c->st), "memset misc");
+    for (int k = 0; k < C; ++k) {
+      ck(cudaStreamWaitEvent(c->st, c->chunk_events[k], 0), "wait chunk");
+      launch_preprocess_range(pb, n, bounds[k], bounds[k + 1], cfg.tau_z, cfg.normalize_inputs, c->st);
+      count_launch(c);
+      if (k + 1 < C) issue_copy(k + 1);
+    }
+    ck(cudaMemcpyAsync(h, pb.totals, 8, cudaMemcpyDeviceToHost, c->st), "totals D2H");
+    sync(c);
+    out.pre.cs.zx = pb.zx;
+    out.pre.cs.zy = pb.zy;
+    out.pre.cs.zz = pb.zz;
+    out.pre.cs.kept = pb.kept;
+    out.pre.cs.n = h[0];
+    out.pre.n_dropped = h[1];
+    out.grid = out.pre.cs.n > 0 ? vote(c, pb.zx, pb.zy, pb.zz, out.pre.cs.n, G, cfg.extent, J) : grid;
+  }
   return out;
 }
 
 // estimate_single from a preprocessed constraint set (identity shortcuts already handled).
 Estimate finish_single(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
-                       const uint32_t* prevoted, bool peak_ready = false);
+                       const uint32_t* prevoted, bool peak_ready = false, bool* identity = nullptr);
 Estimate finish_single_stepped(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
                                const uint32_t* prevoted, int first_attempt);
 Estimate rescue_single(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
                        const uint32_t* grid, Estimate est);
 
+// The identity shortcuts of estimate_single (estimator.cpp:326-340) after an in-order solve saw
+// them in the summary: redo the bookkeeping with the compacting preprocess (rare).
+Estimate identity_from_inorder(rv_context* c, const double* d_corrs, int64_t n, const rv_config& cfg) {
+  const PreResult pc = preprocess_dev(c, d_corrs, n, cfg.tau_z, cfg.normalize_inputs);
+  if (pc.cs.n == 0) {
+    std::vector<int32_t> all(n);
+    for (int64_t i = 0; i < n; ++i) all[i] = (int32_t)i;
+    return identity_estimate(std::move(all));
+  }
+  return identity_estimate(dropped_list(c, pc.n_dropped));
+}
+
 // estimate_single (estimator.cpp:320-371) over device-resident correspondences.
 Estimate estimate_single_dev(rv_context* c, const double* d_corrs, int64_t n, const rv_config& cfg) {
   if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
+  static const bool inorder = [] {  // dev A/B knob: RV_INORDER=0 takes the compacting path
+    const char* e = std::getenv("RV_INORDER");
+    return !(e && e[0] == '0');
+  }();
+  if (inorder && cfg.angle_bins >= 8 && banded_plan(c, cfg)) {  // in-order chain: no host sync until the summary
+    const PreResult pre = preprocess_inorder_dev(c, d_corrs, n, cfg);
+    bool identity = false;
+    Estimate est = finish_single(c, pre, d_corrs, cfg, nullptr, false, &identity);
+    return identity ? identity_from_inorder(c, d_corrs, n, cfg) : est;
+  }
   const PreResult pre = preprocess_dev(c, d_corrs, n, cfg.tau_z, cfg.normalize_inputs, &cfg);
   if (pre.cs.n == 0) {
     std::vector<int32_t> all(n);
@@ -1082,6 +1146,11 @@ Estimate estimate_single_dev(rv_context* c, const double* d_corrs, int64_t n, co
 Estimate estimate_single_host(rv_context* c, const double* h_corrs, int64_t n, const rv_config& cfg) {
   if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
   const PipelinedVote pv = prep_and_vote_host(c, h_corrs, n, cfg);
+  if (pv.pre.inorder) {
+    bool identity = false;
+    Estimate est = finish_single(c, pv.pre, pv.d_corrs, cfg, pv.grid, pv.peak_ready, &identity);
+    return identity ? identity_from_inorder(c, pv.d_corrs, n, cfg) : est;
+  }
   if (pv.pre.cs.n == 0) {
     std::vector<int32_t> all(n);
     for (int64_t i = 0; i < n; ++i) all[i] = (int32_t)i;
@@ -1097,7 +1166,7 @@ Estimate estimate_single_host(rv_context* c, const double* h_corrs, int64_t n, c
 // host only validates and finishes (atan2, Rodrigues). Rare cases -- a failed exactness guard
 // (grid sum != N*J), or the rescue path -- continue on the host-stepped path below.
 Estimate finish_single(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
-                       const uint32_t* prevoted, bool peak_ready) {
+                       const uint32_t* prevoted, bool peak_ready, bool* identity) {
   if (cfg.angle_bins < 8) fail(RV_ERR_INVALID_CONFIG, "angle histogram needs bin_count >= 8");
   const ConstraintSet& cs = pre.cs;
   Summary* dsum = summary_buf(c);
@@ -1145,8 +1214,22 @@ Estimate finish_single(rv_context* c, const PreResult& pre, const double* d_corr
   ck(cudaMemcpyAsync(h, dsum, sizeof(Summary), cudaMemcpyDeviceToHost, c->st), "summary D2H");
   sync(c);
   const Summary sm = *h;
-  if (sm.pk.total != (unsigned long long)cs.n * (unsigned long long)cfg.theta_samples) {
+  const int64_t n_kept = pre.inorder ? (int64_t)sm.n_kept : cs.n;
+  if (pre.inorder) {
+    if (prevoted) c->times.vote_launches += 1;
+    c->times.vote_samples += (n_kept - (prevoted ? 0 : cs.n)) * (int64_t)cfg.theta_samples;
+    if (n_kept == 0 || (cs.n - n_kept) * 10 >= cs.n * 9) {  // estimator.cpp:326-340 shortcuts
+      if (!identity) fail(RV_ERR_INVALID_ARGUMENT, "in-order solve without an identity handler");
+      *identity = true;
+      return Estimate{};
+    }
+  }
+  if (sm.pk.total != (unsigned long long)n_kept * (unsigned long long)cfg.theta_samples) {
     c->times.vote_guard_reruns += 1;  // exactness guard: redo with the generic exact vote
+    if (pre.inorder) {  // ... over the compacted constraint set
+      const PreResult pc = preprocess_dev(c, d_corrs, cs.n, cfg.tau_z, cfg.normalize_inputs);
+      return finish_single_stepped(c, pc, d_corrs, cfg, nullptr, 1);
+    }
     return finish_single_stepped(c, pre, d_corrs, cfg, nullptr, 1);
   }
   if (!sm.pk.ok) fail(RV_ERR_NO_PEAK, "no accumulator cell reaches min_votes");
@@ -1167,8 +1250,15 @@ Estimate finish_single(rv_context* c, const PreResult& pre, const double* d_corr
   est.votes = sm.pk.votes;
   est.inliers = std::move(c->spare);  // the compaction already wrote the list to mapped memory
   est.inliers.assign(c->inl_host, c->inl_host + sm.st.count);
-  const double chance = cfg.epsilon * (double)cs.n;
-  if (cfg.refine && (double)est.inliers.size() < 3.0 * chance) est = rescue_single(c, pre, d_corrs, cfg, grid, est);
+  const double chance = cfg.epsilon * (double)n_kept;
+  if (cfg.refine && (double)est.inliers.size() < 3.0 * chance) {
+    if (pre.inorder) {  // the rescue path works on the compacted constraint set; the grid is the same
+      const PreResult pc = preprocess_dev(c, d_corrs, cs.n, cfg.tau_z, cfg.normalize_inputs);
+      est = rescue_single(c, pc, d_corrs, cfg, grid, est);
+    } else {
+      est = rescue_single(c, pre, d_corrs, cfg, grid, est);
+    }
+  }
   return est;
 }
 

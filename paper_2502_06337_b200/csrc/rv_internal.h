@@ -63,7 +63,8 @@ struct VoteBuffers {
   int32_t* counters = nullptr;         // [0]=slot counter, [1..kMaxBands]=entry counters per band
   unsigned long long* stats = nullptr; // [0]=pairs evaluated, [1]=fallback pairs
   int max_slots = 0;
-  const int32_t* bounds = nullptr;     // device [lo, hi) of constraints for this launch (null: [0, n))
+  const int32_t* bounds = nullptr;     // device [lo, hi) of constraints for this launch (null: [range_lo, range_lo + n))
+  int64_t range_lo = 0;
   // optional, fused into the tile reduction: argmax key + grid sum (find_peaks K=1 and the
   // exactness guard) and the start axis (estimate_from_peak)
   unsigned long long* red_keys = nullptr;  // [2 * reduce blocks] scratch
@@ -79,6 +80,7 @@ void launch_plan(const VotePlan& p, const VoteBuffers& b, int64_t n, cudaStream_
 void launch_vote_banded(const VotePlan& p, const VoteBuffers& b, int64_t n, int n_ctas, cudaStream_t s);
 cudaError_t set_vote_smem(const VotePlan& p);  // opt-in dynamic smem (once per size)
 void launch_zero_i32(int32_t* p, int n, cudaStream_t s);
+int vote_reduce_blocks_x(const VotePlan& p);  // blocks per band of vote_reduce_kernel
 void launch_vote_reduce(const VotePlan& p, const VoteBuffers& b, cudaStream_t s);
 // Exact generic vote (any config): one thread per (constraint, sample), global atomics.
 void launch_vote_generic(const VotePlan& p, const VoteBuffers& b, int64_t n, cudaStream_t s);
@@ -98,6 +100,9 @@ struct PrepBuffers {
   int32_t* block_counter = nullptr;      // dynamic block id (zeroed before launch)
   int32_t* totals = nullptr;             // [0]=n_kept [1]=n_dropped
   int32_t* chunk_hi = nullptr;           // optional: kept count through the end of this launch's range
+  // in-order mode (launch_preprocess_inorder): z written at the input index (NaN = dropped), no
+  // compaction; the kept count is added to *kept_total (zeroed before the first launch)
+  unsigned long long* kept_total = nullptr;
   // side job: word ranges to clear (the next vote's grid and counters -- saves separate memsets)
   uint32_t* zero_ptr[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t zero_n[4] = {0, 0, 0, 0};
@@ -107,6 +112,9 @@ void launch_preprocess(const PrepBuffers& b, int64_t n, double tau_z, int normal
 // One chunk [elem_lo, elem_hi) of a pipelined preprocess (elem_lo multiple of 1024; chunks in order).
 void launch_preprocess_range(const PrepBuffers& b, int64_t n, int64_t elem_lo, int64_t elem_hi, double tau_z,
                              int normalize, cudaStream_t s);
+// In-order preprocess of [elem_lo, elem_hi) (elem_lo multiple of 1024): no look-back, no index maps.
+void launch_preprocess_inorder(const PrepBuffers& b, int64_t n, int64_t elem_lo, int64_t elem_hi, double tau_z,
+                               int normalize, cudaStream_t s);
 
 // K3: peak search over a device grid (rv_peaks.cu).
 struct Disk {

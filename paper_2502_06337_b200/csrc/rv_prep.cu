@@ -22,15 +22,15 @@ constexpr int kPrepTile = kPrepThreads * kPrepPer;      // 1024 correspondences 
 constexpr int kPrepWarps = kPrepThreads / 32;
 static_assert(kPrepPer * kPrepWarps == 32, "one warp scans the (round, warp) counts");
 
-template <bool kVec>
-__global__ void __launch_bounds__(kPrepThreads) preprocess_kernel(PrepBuffers b, int64_t n, int64_t elem_hi,
+template <bool kVec, bool kInOrder>
+__global__ void __launch_bounds__(kPrepThreads) preprocess_kernel(PrepBuffers b, int64_t n, int64_t elem_lo, int64_t elem_hi,
                                                                   double tau_z, int normalize) {
   __shared__ int s_bid;
   __shared__ int s_cnt[kPrepPer * kPrepWarps];  // kept per (round, warp), then its exclusive scan
   __shared__ int s_total;
   __shared__ long long s_excl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_bid = atomicAdd(b.block_counter, 1);
+  if (tid == 0 && !kInOrder) s_bid = atomicAdd(b.block_counter, 1);
   {  // side job: clear the next vote's state (grid-stride over the launch's threads)
     const int64_t gstride = (int64_t)gridDim.x * kPrepThreads, g0 = (int64_t)blockIdx.x * kPrepThreads + tid;
 #pragma unroll
@@ -38,8 +38,8 @@ __global__ void __launch_bounds__(kPrepThreads) preprocess_kernel(PrepBuffers b,
       if (b.zero_ptr[q])
         for (int64_t w = g0; w < b.zero_n[q]; w += gstride) b.zero_ptr[q][w] = 0u;
   }
-  __syncthreads();
-  const int bid = s_bid;
+  if (!kInOrder) __syncthreads();
+  const int bid = kInOrder ? (int)(elem_lo / kPrepTile) + blockIdx.x : s_bid;
   const int64_t base = (int64_t)bid * kPrepTile;
   double c[kPrepPer][6];
 #pragma unroll
@@ -80,6 +80,25 @@ __global__ void __launch_bounds__(kPrepThreads) preprocess_kernel(PrepBuffers b,
     zo[r][2] = xd(d2, len);
     km[r] = __ballot_sync(0xFFFFFFFFu, keep[r]);
     if (lane == 0) s_cnt[r * kPrepWarps + warp] = __popc(km[r]);
+  }
+  if constexpr (kInOrder) {  // z at the input index, NaN marks a dropped pair; count the kept ones
+#pragma unroll
+    for (int r = 0; r < kPrepPer; ++r) {
+      const int64_t i = base + r * kPrepThreads + tid;
+      if (i < n) {
+        const double q = __longlong_as_double(0x7FF8000000000000ll);
+        b.zx[i] = keep[r] ? zo[r][0] : q;
+        b.zy[i] = keep[r] ? zo[r][1] : q;
+        b.zz[i] = keep[r] ? zo[r][2] : q;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int v = s_cnt[lane];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+      if (lane == 0 && v) atomicAdd(b.kept_total, (unsigned long long)v);
+    }
+    return;
   }
   __syncthreads();
   if (warp == 0) {  // exclusive scan of the 32 (round, warp) counts in element order
@@ -168,9 +187,9 @@ void launch_preprocess(const PrepBuffers& b, int64_t n, double tau_z, int normal
   const int blocks = prep_blocks(n);
   const bool vec = (reinterpret_cast<uintptr_t>(b.corrs) & 15u) == 0;
   if (vec)
-    preprocess_kernel<true><<<blocks, kPrepThreads, 0, s>>>(b, n, n, tau_z, normalize);
+    preprocess_kernel<true, false><<<blocks, kPrepThreads, 0, s>>>(b, n, 0, n, tau_z, normalize);
   else
-    preprocess_kernel<false><<<blocks, kPrepThreads, 0, s>>>(b, n, n, tau_z, normalize);
+    preprocess_kernel<false, false><<<blocks, kPrepThreads, 0, s>>>(b, n, 0, n, tau_z, normalize);
 }
 
 void launch_preprocess_range(const PrepBuffers& b, int64_t n, int64_t elem_lo, int64_t elem_hi, double tau_z,
@@ -179,9 +198,20 @@ void launch_preprocess_range(const PrepBuffers& b, int64_t n, int64_t elem_lo, i
   if (blocks <= 0) return;
   const bool vec = (reinterpret_cast<uintptr_t>(b.corrs) & 15u) == 0;
   if (vec)
-    preprocess_kernel<true><<<blocks, kPrepThreads, 0, s>>>(b, n, elem_hi, tau_z, normalize);
+    preprocess_kernel<true, false><<<blocks, kPrepThreads, 0, s>>>(b, n, elem_lo, elem_hi, tau_z, normalize);
   else
-    preprocess_kernel<false><<<blocks, kPrepThreads, 0, s>>>(b, n, elem_hi, tau_z, normalize);
+    preprocess_kernel<false, false><<<blocks, kPrepThreads, 0, s>>>(b, n, elem_lo, elem_hi, tau_z, normalize);
+}
+
+void launch_preprocess_inorder(const PrepBuffers& b, int64_t n, int64_t elem_lo, int64_t elem_hi, double tau_z,
+                               int normalize, cudaStream_t s) {
+  const int blocks = (int)((elem_hi - elem_lo + kPrepTile - 1) / kPrepTile);
+  if (blocks <= 0) return;
+  const bool vec = (reinterpret_cast<uintptr_t>(b.corrs) & 15u) == 0;
+  if (vec)
+    preprocess_kernel<true, true><<<blocks, kPrepThreads, 0, s>>>(b, n, elem_lo, elem_hi, tau_z, normalize);
+  else
+    preprocess_kernel<false, true><<<blocks, kPrepThreads, 0, s>>>(b, n, elem_lo, elem_hi, tau_z, normalize);
 }
 
 void launch_gather_residual(const double* zx, const double* zy, const double* zz, const int32_t* kept,

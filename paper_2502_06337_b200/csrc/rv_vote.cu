@@ -37,6 +37,9 @@ constexpr float kPiF = 3.14159265358979323846f;
 constexpr float kTwoPiF = 6.28318530717958647692f;
 constexpr float kRcMin = 1e-3f;     // |c| amplitude below which a circle is treated as all-band
 constexpr float kDc = 2e-6f;        // |c| below this: hemisphere flip ambiguous -> exact path
+#ifndef RV_RED_GROUPS
+#define RV_RED_GROUPS 2
+#endif
 #ifndef RV_NP
 #define RV_NP 2  // pairs per lane per full step of the vote loop (2 or 4)
 #endif
@@ -277,14 +280,20 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
     s_cnt[t] = 0;
   }
   __syncthreads();
-  const int64_t lo = b.bounds ? b.bounds[0] : 0, hi = b.bounds ? b.bounds[1] : n;
+  const int64_t lo = b.bounds ? b.bounds[0] : b.range_lo, hi = b.bounds ? b.bounds[1] : b.range_lo + n;
   const int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = i < hi;
+  double z0 = 0.0, z1 = 0.0, z2 = 0.0;
+  if (i < hi) {
+    z0 = b.zx[i];
+    z1 = b.zy[i];
+    z2 = b.zz[i];
+  }
+  const bool valid = i < hi && !isnan(z0);  // in-order constraint sets mark dropped pairs with NaN
   const int M = p.halfJ;
   float f1[3] = {0.f, 0.f, 0.f}, f2[3] = {0.f, 0.f, 0.f};
   if (valid) {
     double a1[3], a2[3];
-    exact_basis(b.zx[i], b.zy[i], b.zz[i], a1, a2);
+    exact_basis(z0, z1, z2, a1, a2);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       f1[k] = __double2float_rn(a1[k]);
@@ -742,6 +751,8 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
 }
 
 // Sum the partial tiles of every band into the output grid.
+constexpr int kRedGroups = RV_RED_GROUPS;  // slot groups per block
+constexpr int kRedVecs = kReduceThreads / kRedGroups;
 __global__ void __launch_bounds__(kReduceThreads) vote_reduce_kernel(VotePlan p, VoteBuffers b) {
   __shared__ int s_slots[1024];
   __shared__ int s_n;
@@ -762,42 +773,61 @@ __global__ void __launch_bounds__(kReduceThreads) vote_reduce_kernel(VotePlan p,
   const int ns = s_n;
   const bool fused = b.red_out != nullptr;
   unsigned long long best = 0, gsum = 0;
-  // 4 words per thread (tile_words is a multiple of 4: slots are 16-byte aligned), 4 slots in flight
+  // 4 words per thread (tile_words is a multiple of 4: slots are 16-byte aligned); the block's
+  // threads form kRedGroups slot groups over kRedVecs vectors (more loads in flight per vector),
+  // combined through shared memory
   const int nv = (words + 3) / 4;
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+  const int vl = threadIdx.x % kRedVecs, g = threadIdx.x / kRedVecs;
+  __shared__ uint4 s_acc[kRedGroups - 1][kRedVecs];
+  for (int v0 = blockIdx.x * kRedVecs; v0 < nv; v0 += gridDim.x * kRedVecs) {
+    const int v = v0 + vl;
     uint4 acc = make_uint4(0u, 0u, 0u, 0u);
-    auto add = [&](int slot) {
-      const uint4 x = __ldcs(reinterpret_cast<const uint4*>(b.partials + (size_t)slot * p.tile_words) + v);
-      acc.x += x.x;
-      acc.y += x.y;
-      acc.z += x.z;
-      acc.w += x.w;
-    };
-    if (ns <= 1024) {
-      int k = 0;
+    if (v < nv) {
+      auto add = [&](int slot) {
+        const uint4 x = __ldcs(reinterpret_cast<const uint4*>(b.partials + (size_t)slot * p.tile_words) + v);
+        acc.x += x.x;
+        acc.y += x.y;
+        acc.z += x.z;
+        acc.w += x.w;
+      };
+      if (ns <= 1024) {
 #pragma unroll 4
-      for (; k < ns; ++k) add(s_slots[k]);
-    } else {
-      for (int s = 0; s < used; ++s)
-        if (b.slot_band[s] == band) add(s);
+        for (int k = g; k < ns; k += kRedGroups) add(s_slots[k]);
+      } else {
+        for (int s = g; s < used; s += kRedGroups)
+          if (b.slot_band[s] == band) add(s);
+      }
     }
-    const uint32_t a4[4] = {acc.x, acc.y, acc.z, acc.w};
+    if (g > 0) s_acc[g - 1][vl] = acc;
+    __syncthreads();
+    if (g == 0 && v < nv) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int w = 4 * v + i;
-      if (w < words) {
-        const int row = r0 + w / p.W, col = p.c_min + w % p.W;
-        const size_t gi = (size_t)row * p.G + col;
-        if (fused) {  // final cell value (the exact path may have added to the global grid)
-          const uint32_t val = b.grid[gi] + a4[i];
-          if (a4[i]) b.grid[gi] = val;
-          gsum += val;
-          if (val) best = max(best, ((unsigned long long)val << 32) | (0xFFFFFFFFu - (uint32_t)gi));
-        } else if (a4[i]) {
-          b.grid[gi] += a4[i];
+      for (int q = 0; q < kRedGroups - 1; ++q) {
+        const uint4 x = s_acc[q][vl];
+        acc.x += x.x;
+        acc.y += x.y;
+        acc.z += x.z;
+        acc.w += x.w;
+      }
+      const uint32_t a4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int w = 4 * v + i;
+        if (w < words) {
+          const int row = r0 + w / p.W, col = p.c_min + w % p.W;
+          const size_t gi = (size_t)row * p.G + col;
+          if (fused) {  // final cell value (the exact path may have added to the global grid)
+            const uint32_t val = b.grid[gi] + a4[i];
+            if (a4[i]) b.grid[gi] = val;
+            gsum += val;
+            if (val) best = max(best, ((unsigned long long)val << 32) | (0xFFFFFFFFu - (uint32_t)gi));
+          } else if (a4[i]) {
+            b.grid[gi] += a4[i];
+          }
         }
       }
     }
+    __syncthreads();
   }
   if (!fused) return;
   // fused find_peaks(K=1) argmax + exactness-guard sum (argmax_kernel's key: count, then lowest
@@ -939,10 +969,13 @@ void launch_vote_banded(const VotePlan& p, const VoteBuffers& b, int64_t n, int 
   f<<<n_ctas, kVoteThreads, p.smem_bytes, s>>>(p, b, n);
 }
 
-void launch_vote_reduce(const VotePlan& p, const VoteBuffers& b, cudaStream_t s) {
+int vote_reduce_blocks_x(const VotePlan& p) {
   const int vecs = (p.H_max * p.W + 3) / 4;
-  const int bx = (vecs + kReduceThreads - 1) / kReduceThreads;
-  dim3 grid((unsigned)min(bx, 256), (unsigned)p.n_bands);
+  return min((vecs + kRedVecs - 1) / kRedVecs, 1024);
+}
+
+void launch_vote_reduce(const VotePlan& p, const VoteBuffers& b, cudaStream_t s) {
+  dim3 grid((unsigned)vote_reduce_blocks_x(p), (unsigned)p.n_bands);
   vote_reduce_kernel<<<grid, kReduceThreads, 0, s>>>(p, b);
 }
 

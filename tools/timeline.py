@@ -15,7 +15,9 @@ import paper_2502_06337_b200 as rv  # noqa: E402
 from paper_2502_06337_b200 import synth  # noqa: E402
 
 key = sys.argv[1] if len(sys.argv) > 1 else "c3"
-host = len(sys.argv) > 2 and sys.argv[2] == "host"
+host = "host" in sys.argv[2:]
+flush_l2 = "flush" in sys.argv[2:]  # like bench.py: 256 MiB write + sync before the solve
+show_api = "api" in sys.argv[2:]  # also list the host-side CUDA runtime calls
 corrs, _, _ = synth.make_config(key)
 ctx = rv.Context(0)
 ctx.set_stream(torch.cuda.current_stream().cuda_stream)
@@ -31,16 +33,22 @@ def solve():
     return ctx.estimate_single_device(d.data_ptr(), corrs.shape[0], cfg)
 
 
+flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 for _ in range(3):
     solve()
 torch.cuda.synchronize()
-with profile(activities=[ProfilerActivity.CUDA]) as prof:
+if flush_l2:
+    flush.zero_()
+    torch.cuda.synchronize()
+acts_kind = [ProfilerActivity.CUDA] + ([ProfilerActivity.CPU] if show_api else [])
+with profile(activities=acts_kind) as prof:
     solve()
     torch.cuda.synchronize()
 with tempfile.NamedTemporaryFile(suffix=".json") as f:
     prof.export_chrome_trace(f.name)
     ev = json.load(open(f.name))["traceEvents"]
-acts = [e for e in ev if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memset", "gpu_memcpy")]
+cats = ("kernel", "gpu_memset", "gpu_memcpy") + (("cuda_runtime", "cuda_driver") if show_api else ())
+acts = [e for e in ev if e.get("ph") == "X" and e.get("cat") in cats]
 acts.sort(key=lambda e: e["ts"])
 t0 = acts[0]["ts"]
 end_prev = t0
@@ -48,6 +56,8 @@ busy = 0.0
 for e in acts:
     gap = e["ts"] - end_prev
     print(f"{e['ts'] - t0:9.1f} us  dur {e['dur']:8.1f}  gap {gap:7.1f}  {e['cat']:10s} {e['name'][:70]}")
+    if e["cat"] in ("cuda_runtime", "cuda_driver"):
+        continue
     end_prev = max(end_prev, e["ts"] + e["dur"])
     busy += e["dur"]
 span = end_prev - t0
