@@ -627,6 +627,24 @@ __device__ __forceinline__ void vote_entries(const VoteCtx& v, const F32Geom& ge
 // lengths, table doubled so ranges never wrap). Pairs whose f32 cell is not provably the
 // reference cell are queued per warp and recomputed exactly in f64.
 
+#ifdef RV_VOTE_TRACE  // dev instrumentation: per-CTA phase timestamps (globaltimer, ns)
+__device__ unsigned long long g_vtrace[2 * 65536];
+__device__ unsigned int g_vtrace_n;
+__device__ __forceinline__ void vtrace(int tag, int band) {
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    const unsigned k = atomicAdd(&g_vtrace_n, 1u);
+    if (k < 65536) {
+      g_vtrace[2 * k] = t;
+      g_vtrace[2 * k + 1] = ((unsigned long long)blockIdx.x << 16) | ((unsigned)tag << 8) | (unsigned)(band & 255);
+    }
+  }
+}
+#else
+__device__ __forceinline__ void vtrace(int, int) {}
+#endif
+
 template <bool kClamp, int kS>
 __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p, VoteBuffers b, int64_t n) {
   extern __shared__ uint4 smem_raw[];
@@ -658,8 +676,10 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     }
     s_band = band;
   }
+  vtrace(0, 0);
   for (size_t k = tid; k < p.tile_words; k += blockDim.x) tile[k] = 0u;
   __syncthreads();
+  vtrace(1, s_band);
   unsigned int my_fb = 0;
   unsigned lt_mask = (1u << lane) - 1u;
   // per-lane table address (shared window): loaded by ld.shared below
@@ -716,6 +736,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     vote_entries<kClamp, kS>(v, geo, fc, [&](int j) { return __ldcs(ebase + j); }, n_ent, counter, my_fb);
     // band exhausted for this CTA: flush the tile to a partial slot, steal the next band
     __syncthreads();
+    vtrace(2, band);
     if (tid == 0) {
       const int slot = atomicAdd(&b.counters[0], 1);
       s_slot = slot;
@@ -743,10 +764,12 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
         if (tile[k]) atomicAdd(&b.grid[(size_t)(r0 + k / W) * G + p.c_min + k % W], tile[k]);
     }
     __syncthreads();
+    vtrace(3, band);
     if (s_band >= 0)
       for (size_t k = tid; k < p.tile_words; k += blockDim.x) tile[k] = 0u;
     __syncthreads();
   }
+  vtrace(4, 0);
   if (lane == 0 && my_fb) atomicAdd(&b.stats[1], (unsigned long long)my_fb);
 }
 
@@ -998,3 +1021,16 @@ void launch_deposit_one(const VotePlan& p, const double* z3, const double2* tabl
 }
 
 }  // namespace rvb
+
+#ifdef RV_VOTE_TRACE
+extern "C" int rv_debug_vote_trace(unsigned long long* out, int max_events) {
+  unsigned int n = 0;
+  cudaMemcpyFromSymbol(&n, rvb::g_vtrace_n, sizeof n);
+  if (n > 65536) n = 65536;
+  if ((int)n > max_events) n = (unsigned)max_events;
+  cudaMemcpyFromSymbol(out, rvb::g_vtrace, sizeof(unsigned long long) * 2 * n);
+  const unsigned int zero = 0;
+  cudaMemcpyToSymbol(rvb::g_vtrace_n, &zero, sizeof zero);
+  return (int)n;
+}
+#endif

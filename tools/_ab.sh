@@ -1,5 +1,4 @@
-for v in red2 red4 red8 red2 red4 red8; do cp _variants/$v.so paper_2502_06337_b200/_lib/librotavote_b200.so
-python tools/timeline.py c3 > gpurun_out/tl_dev.txt 2>&1
-python tools/timeline.py c3 host > gpurun_out/tl_host.txt 2>&1
-echo $v $(grep reduce gpurun_out/tl_dev.txt | awk '{print $4}') $(grep reduce gpurun_out/tl_host.txt | awk '{print $4}') $(grep span gpurun_out/tl_dev.txt gpurun_out/tl_host.txt | awk '{print $2}')
+for cum in 0,1,3,8,16 0,1,3,7,12,16 0,1,3,6,10,16 0,1,2,4,7,11,16 0,1,3,6,11,16 0,1,3,8,16 0,1,3,7,12,16; do
+RV_PIPE_CUM=$cum python bench.py --steps 20 --warmup 3 > gpurun_out/b.json 2>/dev/null; python -c "
+import json; d=json.load(open('gpurun_out/b.json')); print('$cum', round(d['ms_per_step'],4), d['e2e']['value'])"
 done
