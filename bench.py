@@ -306,9 +306,20 @@ def run_device(args):
             "kernel_ms_per_solve": 1e3 * vote_avg_s, "kernel_share_of_solve": t_vote_k / t_dev,
             "vote_stage_ms_per_solve": 1e3 * t_vote / args.steps,
             "ncu": prof}
+    clocks = clk.summary()
+    if prof and prof.get("inst_executed") and clocks.get("sm_mhz"):
+        # the vote kernel is issue-bound: warp instructions of one launch (ncu) / its live launch
+        # time, against 4 issue slots per SM per clock at the sampled SM clock
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        ach = prof["inst_executed"] / vote_avg_s
+        pk = 4.0 * sms * clocks["sm_mhz"] * 1e6
+        roof["issue"] = {"bound": "instruction issue", "achieved": ach / 1e9, "peak": pk / 1e9,
+                         "unit": "G warp-inst/s", "frac": ach / pk,
+                         "inst_per_launch": prof["inst_executed"], "source": "ncu inst_executed x live launch time"}
     pre_ms = statistics.mean(s["preprocess_ms"] for s in stage)
     hbm = measured_peaks().get("hbm_gbs")
-    k1_gbs = (76.0 * n_mine) / (pre_ms * 1e-3) / 1e9 if pre_ms > 0 else None
+    # in-order preprocess (single solves): 48 B read + 24 B of z written per correspondence
+    k1_gbs = (72.0 * n_mine) / (pre_ms * 1e-3) / 1e9 if pre_ms > 0 else None
     cpu = None
     if world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
@@ -333,10 +344,10 @@ def run_device(args):
             "roofline": roof,
             "roofline_k1": {"bound": "hbm", "kernel": "preprocess_kernel", "achieved": k1_gbs, "peak": hbm,
                             "unit": "GB/s", "frac": (k1_gbs / hbm) if (hbm and k1_gbs) else None,
-                            "traffic": None, "bytes_per_corr": 76},
+                            "traffic": None, "bytes_per_corr": 72},
             "stage_ms": {k: statistics.mean(s[k] for s in stage) for k in
                          ("preprocess_ms", "vote_ms", "peaks_ms", "refine_ms", "angles_ms")},
-            "gpu_launches": launches, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "gpu_launches": launches, "cpu_baseline": cpu, "clocks": clocks,
             "accuracy": {"rot_err_deg_vs_truth": err_deg, "inliers": int(est.inliers.size)}}
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -250,6 +250,29 @@ def test_pipelined_host_path_matches_device_path(ctx):
     assert st["vote_guard_reruns"] == 0
 
 
+def test_inorder_path_with_dropped_pairs(ctx, port):
+    # single solves keep the constraint set in input order (z = NaN marks a dropped pair); with
+    # 20% scattered degenerate pairs the pipelined host path (4 chunks), the device path and the
+    # oracle must agree, and >= 90% dropped takes the identity shortcut with the dropped list
+    import torch
+    corrs, _, _ = synth.make_config("c3", 300_000)
+    rng = np.random.default_rng(131)
+    drop = rng.random(corrs.shape[0]) < 0.2
+    corrs[drop, 3:] = corrs[drop, :3]
+    e_host = ctx.estimate_single(corrs)
+    d = torch.from_numpy(corrs).cuda()
+    e_dev = ctx.estimate_single_device(d.data_ptr(), corrs.shape[0])
+    r = port.estimate_single(corrs)
+    assert_est_equal(e_host, r)
+    assert_est_equal(e_dev, r)
+    assert not np.isin(e_host.inliers, np.nonzero(drop)[0]).any()
+    small, _, _ = synth.make_scene(5000, 0.5, 0.01, seed=137)
+    small[:4600, 3:] = small[:4600, :3]
+    e = ctx.estimate_single(small)
+    assert np.allclose(e.rotation, np.eye(3)) and np.array_equal(e.inliers, np.arange(4600))
+    assert np.array_equal(e.inliers, port.estimate_single(small)["inliers"])
+
+
 @pytest.mark.parametrize("world", [2, 8])
 def test_sharded_vote_protocol_single_gpu(ctx, world):
     # the multi-GPU protocol emulated sequentially on one GPU (no cross-kernel waits): per-shard

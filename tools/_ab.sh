@@ -1,4 +1,4 @@
-for cum in 0,1,3,8,16 0,1,3,7,12,16 0,1,3,6,10,16 0,1,2,4,7,11,16 0,1,3,6,11,16 0,1,3,8,16 0,1,3,7,12,16; do
-RV_PIPE_CUM=$cum python bench.py --steps 20 --warmup 3 > gpurun_out/b.json 2>/dev/null; python -c "
-import json; d=json.load(open('gpurun_out/b.json')); print('$cum', round(d['ms_per_step'],4), d['e2e']['value'])"
+for v in orig q; do cp _variants/$v.so paper_2502_06337_b200/_lib/librotavote_b200.so
+ncu --set full --clock-control none -k regex:vote_banded -s 2 -c 1 -f -o gpurun_out/vote_$v python tools/profile_vote.py c3 3 > gpurun_out/ncu_$v.log 2>&1; echo $v rc=$?
 done
+cp _variants/q.so paper_2502_06337_b200/_lib/librotavote_b200.so

@@ -7,3 +7,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
     python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/prof/ncu_launch.log 2>&1; echo ncu_launch_rc=$?
 ncu --set full --import-source on --clock-control none -k regex:vote_banded -c 1 -f -o gpurun_out/prof/vote_full \
     python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/prof/ncu_full.log 2>&1; echo ncu_full_rc=$?
+ncu --set full --import-source on --clock-control none -k "regex:preprocess_kernel|plan_kernel|vote_reduce|coop_refine|vote_angles|peak_angle" \
+    -c 6 -f -o gpurun_out/prof/secondary python tools/profile_vote.py c3 1 > gpurun_out/prof/ncu_secondary.log 2>&1; echo ncu_secondary_rc=$?
+python tools/timeline.py c3 dev flush > gpurun_out/prof/timeline_c3.txt 2>&1
+python tools/timeline.py c3 host flush > gpurun_out/prof/timeline_c3_host.txt 2>&1
+python tools/gpu_check.py > gpurun_out/prof/gpu_check.log 2>&1; echo gpu_check_rc=$?

@@ -5,6 +5,10 @@ cp gpurun_out/prof/bench.json $P/bench_r1_c3.json
 cp gpurun_out/prof/bench_ref.json $P/bench_ref_r1.json
 cp gpurun_out/prof/launches.csv $P/launches_r1.csv
 cp gpurun_out/prof/vote_full.ncu-rep $P/vote_banded_r1.ncu-rep
+if [ -f gpurun_out/prof/secondary.ncu-rep ]; then
+  cp gpurun_out/prof/secondary.ncu-rep $P/secondary_r1.ncu-rep
+  python tools/summarize_profiles.py --kernels $P/secondary_r1.ncu-rep > $P/SECONDARY_r1.txt
+fi
 [ -f gpurun_out/prof/timeline_c3.txt ] && grep -v Warn gpurun_out/prof/timeline_c3.txt | grep -v _warn_once > $P/timeline_c3_device.txt
 [ -f gpurun_out/prof/timeline_c3_host.txt ] && grep -v Warn gpurun_out/prof/timeline_c3_host.txt | grep -v _warn_once > $P/timeline_c3_e2e.txt
 [ -f gpurun_out/prof/gpu_check.log ] && cut -c1-600 gpurun_out/prof/gpu_check.log > $P/gpu_check_r1.txt

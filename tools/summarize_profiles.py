@@ -85,7 +85,34 @@ def kernel_json(path):
             "shared_atom_wavefronts": val("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum")}
 
 
+def per_kernel(path):
+    """One block per kernel launch of an ncu --set full report holding several kernels."""
+    res = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True)
+    rows = list(csv.reader(res.stdout.splitlines()))
+    if len(rows) < 3:
+        return [f"# {path}: no launches"]
+    h, u = rows[0], rows[1]
+    keys = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "dram read"),
+            ("dram__bytes_write.sum", "dram write"),
+            ("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "memory throughput %"),
+            ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+            ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+            ("launch__registers_per_thread", "registers/thread"), ("launch__grid_size", "grid"),
+            ("launch__block_size", "block")]
+    out = [f"# ncu --set full, one launch per kernel: {path}"]
+    for r in rows[2:]:
+        d = dict(zip(h, r))
+        out.append(f"{d.get('Kernel Name', '?')[:110]}")
+        for k, label in keys:
+            if k in d:
+                out.append(f"    {label:22s} {d[k]} {u[h.index(k)]}".rstrip())
+    return out
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "--kernels":
+        print("\n".join(per_kernel(sys.argv[2])))
+        sys.exit(0)
     if sys.argv[1] == "--json":
         import json
         print(json.dumps(kernel_json(sys.argv[2]), indent=1))
