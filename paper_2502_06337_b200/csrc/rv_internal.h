@@ -101,8 +101,13 @@ struct PrepBuffers {
   int32_t* totals = nullptr;             // [0]=n_kept [1]=n_dropped
   int32_t* chunk_hi = nullptr;           // optional: kept count through the end of this launch's range
   // in-order mode (launch_preprocess_inorder): z written at the input index (NaN = dropped), no
-  // compaction; the kept count is added to *kept_total (zeroed before the first launch)
+  // compaction. Blocks add their kept counts to *kept_acc (zero at rest); the last block of a
+  // launch (ticket on *kept_done, reset by it) moves the sum to *kept_total and re-zeroes the
+  // accumulator when `kept_publish` is set (the final launch of a solve) -- no memset needed.
   unsigned long long* kept_total = nullptr;
+  unsigned long long* kept_acc = nullptr;
+  unsigned int* kept_done = nullptr;
+  int kept_publish = 1;
   // side job: word ranges to clear (the next vote's grid and counters -- saves separate memsets)
   uint32_t* zero_ptr[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t zero_n[4] = {0, 0, 0, 0};

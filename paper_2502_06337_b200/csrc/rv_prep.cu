@@ -96,7 +96,15 @@ __global__ void __launch_bounds__(kPrepThreads) preprocess_kernel(PrepBuffers b,
     if (warp == 0) {
       int v = s_cnt[lane];
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-      if (lane == 0 && v) atomicAdd(b.kept_total, (unsigned long long)v);
+      if (lane == 0) {
+        if (v) atomicAdd(b.kept_acc, (unsigned long long)v);
+        __threadfence();
+        if (atomicAdd(b.kept_done, 1u) == gridDim.x - 1) {  // last block of this launch
+          __threadfence();
+          if (b.kept_publish) *b.kept_total = atomicExch(b.kept_acc, 0ull);
+          *b.kept_done = 0u;
+        }
+      }
     }
     return;
   }

@@ -273,6 +273,29 @@ def test_inorder_path_with_dropped_pairs(ctx, port):
     assert np.array_equal(e.inliers, port.estimate_single(small)["inliers"])
 
 
+def test_graph_replay_of_device_solves(ctx, port):
+    # repeated device-resident solves with the same (pointer, n, config) replay a captured CUDA
+    # graph; results must equal the eager solve, follow new data written to the same buffer, and
+    # survive buffer reallocations in between (the graph is re-captured, never replayed stale)
+    import torch
+    a, _, _ = synth.make_config("c3", 300_000)
+    b, _, _ = synth.make_scene(300_000, 0.5, 0.01, seed=149)
+    d = torch.from_numpy(a).cuda()
+    runs = [ctx.estimate_single_device(d.data_ptr(), a.shape[0]) for _ in range(4)]
+    for e in runs[1:]:
+        assert np.array_equal(e.inliers, runs[0].inliers) and np.array_equal(e.rotation, runs[0].rotation)
+    assert_est_equal(runs[-1], port.estimate_single(a))
+    d.copy_(torch.from_numpy(b))  # new contents, same pointer: the replay must see them
+    eb = ctx.estimate_single_device(d.data_ptr(), b.shape[0])
+    assert_est_equal(eb, port.estimate_single(b))
+    big, _, _ = synth.make_config("c3")  # larger solve: grows (reallocates) the context buffers
+    db = torch.from_numpy(big).cuda()
+    ctx.estimate_single_device(db.data_ptr(), big.shape[0])
+    for _ in range(3):
+        e = ctx.estimate_single_device(d.data_ptr(), b.shape[0])
+        assert np.array_equal(e.inliers, eb.inliers) and np.array_equal(e.rotation, eb.rotation)
+
+
 @pytest.mark.parametrize("world", [2, 8])
 def test_sharded_vote_protocol_single_gpu(ctx, world):
     # the multi-GPU protocol emulated sequentially on one GPU (no cross-kernel waits): per-shard
