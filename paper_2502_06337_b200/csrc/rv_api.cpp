@@ -90,6 +90,11 @@ struct Estimate {
   uint32_t votes = 0;
   std::vector<int32_t> inliers;
   double elapsed = 0;
+  // single solves through the C-ABI: the inlier list stays in the context's mapped buffer (the
+  // kernels streamed it there) and rv_result_inliers copies it once, straight from there
+  const int32_t* view = nullptr;
+  int64_t view_n = 0;
+  int64_t n_inliers() const { return view ? view_n : (int64_t)inliers.size(); }
 };
 
 // Constraint set on the device (SoA) with its kept map (constraint -> input index).
@@ -159,6 +164,9 @@ struct rv_context {
   void* pinned = nullptr;
   std::vector<std::vector<int32_t>> results;
   std::vector<int32_t> spare;       // recycled inlier vector (no page faults on the hot path)
+  bool allow_view = false;          // set by the single-solve entry points (see Estimate::view)
+  const int32_t* result0_view = nullptr;  // results[0] lives in the mapped buffer (view)
+  int64_t result0_view_n = 0;
   std::vector<rv_context*> pool;    // batch workers (own stream + buffers each), created lazily
   int32_t* inl_host = nullptr;      // mapped pinned buffer: the compaction writes the inlier list here
   size_t inl_cap = 0;
@@ -209,6 +217,7 @@ struct StageScope {
 };
 
 void begin_call(rv_context* c) {
+  c->allow_view = false;  // only the single-solve entry points opt in (after begin_call)
   c->times = rv_stage_times{};
   c->events.clear();
   c->event_used = 0;
@@ -1411,10 +1420,16 @@ Estimate complete_single(rv_context* c, const PreResult& pre, const double* d_co
   std::memcpy(est.axis, sm.st.axis, sizeof est.axis);
   rodrigues3(est.axis, est.angle, est.R);
   est.votes = sm.pk.votes;
-  est.inliers = std::move(c->spare);  // the compaction already wrote the list to mapped memory
-  est.inliers.assign(c->inl_host, c->inl_host + sm.st.count);
   const double chance = cfg.epsilon * (double)n_kept;
-  if (cfg.refine && (double)est.inliers.size() < 3.0 * chance) {
+  const bool rescue = cfg.refine && (double)sm.st.count < 3.0 * chance;
+  if (c->allow_view && !rescue) {  // the compaction already wrote the list to mapped memory
+    est.view = c->inl_host;
+    est.view_n = (int64_t)sm.st.count;
+    return est;
+  }
+  est.inliers = std::move(c->spare);
+  est.inliers.assign(c->inl_host, c->inl_host + sm.st.count);
+  if (rescue) {
     if (pre.inorder) {  // the rescue path works on the compacted constraint set; the grid is the same
       const PreResult pc = preprocess_dev(c, d_corrs, cs.n, cfg.tau_z, cfg.normalize_inputs);
       est = rescue_single(c, pc, d_corrs, cfg, grid, est);
@@ -1703,7 +1718,7 @@ void to_c(const Estimate& e, rv_estimate* o, double elapsed) {
   o->angle = e.angle;
   std::memcpy(o->rotation, e.R, sizeof o->rotation);
   o->axis_votes = e.votes;
-  o->n_inliers = (int64_t)e.inliers.size();
+  o->n_inliers = e.n_inliers();
   o->elapsed_s = elapsed;
 }
 
@@ -1865,9 +1880,32 @@ rv_status rv_context_stage_times(const rv_context* c, rv_stage_times* out) {
   return RV_OK;
 }
 
+static void clear_results(rv_context* c) {
+  c->results.clear();
+  c->result0_view = nullptr;
+  c->result0_view_n = 0;
+}
+
 static void recycle_results(rv_context* c) {
   if (!c->results.empty() && c->results[0].capacity() > c->spare.capacity()) c->spare = std::move(c->results[0]);
   c->results.clear();
+  c->result0_view = nullptr;
+  c->result0_view_n = 0;
+}
+
+// Store a single-solve estimate's inliers as results[0] (a view into the mapped buffer if the
+// solve left them there).
+static void push_single_result(rv_context* c, Estimate& e) {
+  c->results.push_back(std::move(e.inliers));
+  c->result0_view = e.view;
+  c->result0_view_n = e.view_n;
+}
+
+// results[0] of a worker context as an owned vector (a view would be overwritten by the worker's
+// next solve).
+static std::vector<int32_t> take_result0(rv_context* w) {
+  if (w->result0_view) return std::vector<int32_t>(w->result0_view, w->result0_view + w->result0_view_n);
+  return std::move(w->results[0]);
 }
 
 rv_status rv_estimate_single_device(rv_context* c, const double* d_corrs, int64_t n, const rv_config* cfg,
@@ -1876,9 +1914,11 @@ rv_status rv_estimate_single_device(rv_context* c, const double* d_corrs, int64_
   return guarded(c, [&] {
     cudaSetDevice(c->device);
     recycle_results(c);
+    c->allow_view = true;
     Estimate e = estimate_single_dev(c, d_corrs, n, *cfg);
+    c->allow_view = false;
     to_c(e, out, seconds_since(c));
-    c->results.push_back(std::move(e.inliers));
+    push_single_result(c, e);
   });
 }
 
@@ -1888,9 +1928,11 @@ rv_status rv_estimate_single(rv_context* c, const double* corrs, int64_t n, cons
     cudaSetDevice(c->device);
     recycle_results(c);
     if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
+    c->allow_view = true;
     Estimate e = estimate_single_host(c, corrs, n, *cfg);
+    c->allow_view = false;
     to_c(e, out, seconds_since(c));
-    c->results.push_back(std::move(e.inliers));
+    push_single_result(c, e);
   });
 }
 
@@ -1898,7 +1940,7 @@ static rv_status multi_impl(rv_context* c, const double* d, int64_t n, const rv_
                             int32_t capacity, int32_t* n_models, bool host, bool onepass = false) {
   return guarded(c, [&] {
     cudaSetDevice(c->device);
-    c->results.clear();
+    clear_results(c);
     *n_models = 0;
     if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
     const double* dd = host ? upload_corrs(c, d, n) : d;
@@ -1944,7 +1986,7 @@ rv_status rv_estimate_batch(rv_context* c, const double* corrs, const int64_t* o
     if (offsets[k + 1] < offsets[k]) return RV_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
     cudaSetDevice(c->device);
-    c->results.clear();
+    clear_results(c);
     c->results.resize((size_t)n_problems);
     // automatic width (measured on B200): small problems are launch/latency bound and overlap
     // well on 8 streams (3-4x); problems >= ~32k correspondences already fill the GPU, where
@@ -1964,7 +2006,7 @@ rv_status rv_estimate_batch(rv_context* c, const double* corrs, const int64_t* o
       for (int32_t k = next.fetch_add(1); k < n_problems; k = next.fetch_add(1)) {
         const int64_t n = offsets[k + 1] - offsets[k];
         status[k] = rv_estimate_single(w, corrs + 6 * offsets[k], n, cfg, &out[k]);
-        if (status[k] == RV_OK) c->results[k] = std::move(w->results[0]);
+        if (status[k] == RV_OK) c->results[k] = take_result0(w);
       }
     };
     std::vector<std::thread> th;
@@ -2066,7 +2108,7 @@ rv_status rv_ransac_rotation(rv_context* c, const double* corrs, int64_t n, int3
   if (!c || !out || (n > 0 && !corrs)) return RV_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
     cudaSetDevice(c->device);
-    c->results.clear();
+    clear_results(c);
     constexpr double kTauZ = 1e-9, kTauDeg = 1e-6;
     if (n < 2) fail(RV_ERR_NO_CONSENSUS, "need at least two correspondences");
     // preprocess(correspondences, kTauZ, true) -- estimator.cpp:259-285 op order, on the host:
@@ -2213,7 +2255,7 @@ rv_status rv_estimate_single_prevoted(rv_context* c, const double* d_corrs, int6
   if (!c || !cfg || !out || !d_grid || (n > 0 && !d_corrs)) return RV_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
     cudaSetDevice(c->device);
-    c->results.clear();
+    clear_results(c);
     if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
     const PreResult pre = preprocess_dev(c, d_corrs, n, cfg->tau_z, cfg->normalize_inputs);
     Estimate e;
@@ -2238,6 +2280,12 @@ rv_status rv_estimate_single_prevoted(rv_context* c, const double* d_corrs, int6
 
 rv_status rv_result_inliers(rv_context* c, int32_t model, int32_t* dst, int64_t capacity) {
   if (!c || model < 0 || model >= (int32_t)c->results.size()) return RV_ERR_INVALID_ARGUMENT;
+  if (model == 0 && c->result0_view) {
+    const int64_t m = c->result0_view_n;
+    if (m > capacity || (!dst && m > 0)) return RV_ERR_INVALID_ARGUMENT;
+    if (m > 0) std::memcpy(dst, c->result0_view, sizeof(int32_t) * (size_t)m);
+    return RV_OK;
+  }
   const auto& v = c->results[model];
   if ((int64_t)v.size() > capacity || (!dst && !v.empty())) return RV_ERR_INVALID_ARGUMENT;
   if (!v.empty()) std::memcpy(dst, v.data(), sizeof(int32_t) * v.size());
