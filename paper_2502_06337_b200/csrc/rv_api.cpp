@@ -149,7 +149,8 @@ struct rv_context {
   cudaStream_t copy_st = nullptr;         // H2D copies of the pipelined host path
   cudaStream_t cap_st = nullptr;          // capture stream of the solve graphs
   struct SolveGraph {                     // device-resident single solve, captured once, replayed
-    const double* corrs = nullptr;
+    const double* corrs = nullptr;        // device input, or the pinned host input (host = true)
+    bool host = false;
     int64_t n = 0;
     rv_config cfg{};
     uint64_t gen = 0;
@@ -1159,6 +1160,14 @@ const uint32_t* enqueue_single(rv_context* c, const PreResult& pre, const double
 Estimate complete_single(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
                          const uint32_t* grid, bool prevoted, bool* identity);
 
+bool graphs_enabled() {  // dev A/B knob: RV_GRAPHS=0 always enqueues kernel by kernel
+  static const bool on = [] {
+    const char* e = std::getenv("RV_GRAPHS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool same_cfg(const rv_config& a, const rv_config& b) {
   return a.grid == b.grid && a.extent == b.extent && a.theta_samples == b.theta_samples && a.epsilon == b.epsilon &&
          a.angle_bins == b.angle_bins && a.max_models == b.max_models && a.min_votes_frac == b.min_votes_frac &&
@@ -1187,15 +1196,16 @@ rv_stage_times count_delta(const rv_stage_times& after, const rv_stage_times& be
   return d;
 }
 
-rv_context::SolveGraph* graph_slot(rv_context* c, const double* d, int64_t n, const rv_config& cfg) {
+rv_context::SolveGraph* graph_slot(rv_context* c, const double* d, int64_t n, const rv_config& cfg, bool host) {
   for (auto& g : c->graphs)
-    if (g.corrs == d && g.n == n && same_cfg(g.cfg, cfg)) return &g;
+    if (g.corrs == d && g.host == host && g.n == n && same_cfg(g.cfg, cfg)) return &g;
   if (c->graphs.size() >= 8) {  // small LRU-less cache: drop the oldest entry
     if (c->graphs.front().exec) cudaGraphExecDestroy(c->graphs.front().exec);
     c->graphs.erase(c->graphs.begin());
   }
   rv_context::SolveGraph g;
   g.corrs = d;
+  g.host = host;
   g.n = n;
   g.cfg = cfg;
   g.gen = ~0ull;
@@ -1203,10 +1213,12 @@ rv_context::SolveGraph* graph_slot(rv_context* c, const double* d, int64_t n, co
   return &c->graphs.back();
 }
 
-// Capture the device part of an in-order single solve (memset, preprocess, plan, vote, reduce,
-// cooperative refine, angle kernels, summary D2H) into g->exec. Returns false (and leaves the
-// stream untouched) when the capture fails or a buffer moved while capturing.
-bool capture_single(rv_context* c, rv_context::SolveGraph* g, const double* d_corrs, int64_t n, const rv_config& cfg) {
+// Capture the device part of an in-order single solve (preprocess, plan, vote, reduce, cooperative
+// refine, angle kernels, summary D2H; with host input also the chunked H2D copies on the copy
+// stream, forked from and joined back into the capture) into g->exec. Returns false (and leaves
+// the streams untouched) when the capture fails or a buffer moved while capturing.
+template <typename Enqueue>
+bool capture_single(rv_context* c, rv_context::SolveGraph* g, Enqueue&& enqueue) {
   if (!c->cap_st) ck(cudaStreamCreateWithFlags(&c->cap_st, cudaStreamNonBlocking), "capture stream");
   const uint64_t gen = g_buf_gen.load();
   const rv_stage_times before = c->times;
@@ -1219,8 +1231,7 @@ bool capture_single(rv_context* c, rv_context::SolveGraph* g, const double* d_co
   }
   cudaGraph_t graph = nullptr;
   try {
-    const PreResult pre = preprocess_inorder_dev(c, d_corrs, n, cfg);
-    enqueue_single(c, pre, d_corrs, cfg, nullptr, false);
+    enqueue();
   } catch (...) {
     cudaStreamEndCapture(c->cap_st, &graph);
     if (graph) cudaGraphDestroy(graph);
@@ -1256,17 +1267,18 @@ Estimate estimate_single_dev(rv_context* c, const double* d_corrs, int64_t n, co
     const char* e = std::getenv("RV_INORDER");
     return !(e && e[0] == '0');
   }();
-  static const bool graphs = [] {  // dev A/B knob: RV_GRAPHS=0 always enqueues kernel by kernel
-    const char* e = std::getenv("RV_GRAPHS");
-    return !(e && e[0] == '0');
-  }();
+  const bool graphs = graphs_enabled();
   if (inorder && cfg.angle_bins >= 8 && banded_plan(c, cfg)) {  // in-order chain: no host sync until the summary
     // A repeated (input, n, config) replays the captured solve graph: one launch for the whole
     // device chain (no per-kernel host latency between the stages).
-    rv_context::SolveGraph* g = graphs && !c->timing ? graph_slot(c, d_corrs, n, cfg) : nullptr;
+    rv_context::SolveGraph* g = graphs && !c->timing ? graph_slot(c, d_corrs, n, cfg, false) : nullptr;
     // capture on the second eager-equivalent call (the first one allocated every buffer); the
     // host counters a replay adds are those the eager run of the same key recorded
-    if (g && !g->exec && g->seen > 0 && g->gen == g_buf_gen.load()) capture_single(c, g, d_corrs, n, cfg);
+    if (g && !g->exec && g->seen > 0 && g->gen == g_buf_gen.load())
+      capture_single(c, g, [&] {
+        const PreResult pre = preprocess_inorder_dev(c, d_corrs, n, cfg);
+        enqueue_single(c, pre, d_corrs, cfg, nullptr, false);
+      });
     if (g && g->exec && g->gen == g_buf_gen.load()) {
       ck(cudaGraphLaunch(g->exec, c->st), "solve graph launch");
       add_counts(c->times, g->delta);
@@ -1308,12 +1320,57 @@ Estimate estimate_single_dev(rv_context* c, const double* d_corrs, int64_t n, co
 }
 
 // estimate_single with host input: pipelined H2D + preprocess + vote, then the same solve.
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 Estimate estimate_single_host(rv_context* c, const double* h_corrs, int64_t n, const rv_config& cfg) {
   if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
+  // Repeated solves from the same pinned host buffer replay a captured graph of the whole
+  // pipelined solve (chunked H2D on the copy stream + the in-order device chain): the copy
+  // engine and the SMs run without waiting for the host to issue the next copy or launch.
+  rv_context::SolveGraph* g = nullptr;
+  if (graphs_enabled() && !c->timing && cfg.angle_bins >= 8 && banded_plan(c, cfg) && host_pinned(h_corrs))
+    g = graph_slot(c, h_corrs, n, cfg, true);
+  if (g && !g->exec && g->seen > 0 && g->gen == g_buf_gen.load())
+    capture_single(c, g, [&] {
+      const PipelinedVote pv = prep_and_vote_host(c, h_corrs, n, cfg);
+      enqueue_single(c, pv.pre, pv.d_corrs, cfg, pv.grid, pv.peak_ready);
+    });
+  if (g && g->exec && g->gen == g_buf_gen.load()) {
+    ck(cudaGraphLaunch(g->exec, c->st), "solve graph launch");
+    add_counts(c->times, g->delta);
+    sync(c);
+    PreResult pre;
+    pre.cs.zx = c->zx.get<double>(n);
+    pre.cs.zy = c->zy.get<double>(n);
+    pre.cs.zz = c->zz.get<double>(n);
+    pre.cs.n = n;
+    pre.vote_zeroed = true;
+    pre.inorder = true;
+    const double* d_corrs = c->corrs.get<double>((size_t)n * 6);
+    bool identity = false;
+    Estimate est = complete_single(c, pre, d_corrs, cfg, c->grid.get<uint32_t>((size_t)cfg.grid * cfg.grid), true,
+                                   &identity);
+    return identity ? identity_from_inorder(c, d_corrs, n, cfg) : est;
+  }
+  const rv_stage_times t0 = c->times;
   const PipelinedVote pv = prep_and_vote_host(c, h_corrs, n, cfg);
   if (pv.pre.inorder) {
+    const uint32_t* grid = enqueue_single(c, pv.pre, pv.d_corrs, cfg, pv.grid, pv.peak_ready);
+    if (g) {
+      g->delta = count_delta(c->times, t0);
+      g->gen = g_buf_gen.load();
+      g->seen += 1;
+    }
+    sync(c);
     bool identity = false;
-    Estimate est = finish_single(c, pv.pre, pv.d_corrs, cfg, pv.grid, pv.peak_ready, &identity);
+    Estimate est = complete_single(c, pv.pre, pv.d_corrs, cfg, grid, true, &identity);
     return identity ? identity_from_inorder(c, pv.d_corrs, n, cfg) : est;
   }
   if (pv.pre.cs.n == 0) {

@@ -288,6 +288,15 @@ def test_graph_replay_of_device_solves(ctx, port):
     d.copy_(torch.from_numpy(b))  # new contents, same pointer: the replay must see them
     eb = ctx.estimate_single_device(d.data_ptr(), b.shape[0])
     assert_est_equal(eb, port.estimate_single(b))
+    # pinned host input: the pipelined solve (chunked H2D + chain) is captured and replayed too
+    h = torch.empty((a.shape[0], 6), dtype=torch.float64, pin_memory=True)
+    h.numpy()[:] = a
+    hr = [ctx.estimate_single(h.numpy()) for _ in range(4)]
+    for e in hr:
+        assert np.array_equal(e.inliers, runs[0].inliers) and np.array_equal(e.rotation, runs[0].rotation)
+    h.numpy()[:] = b
+    eh = ctx.estimate_single(h.numpy())
+    assert np.array_equal(eh.inliers, eb.inliers) and np.array_equal(eh.rotation, eb.rotation)
     big, _, _ = synth.make_config("c3")  # larger solve: grows (reallocates) the context buffers
     db = torch.from_numpy(big).cuda()
     ctx.estimate_single_device(db.data_ptr(), big.shape[0])
