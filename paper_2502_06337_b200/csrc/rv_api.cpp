@@ -297,6 +297,19 @@ VotePlan make_plan(rv_context* c, int G, double E, int J) {
   p.c_min = p.r_min;
   p.c_max = p.r_max;
   p.W = p.c_max - p.c_min + 1;
+  // full-width tiles when the grid rows are 16-byte multiples: the vote flushes a band tile into
+  // the grid with TMA bulk reduce-adds (no partial slots to reduce); costs the unreachable
+  // columns of shared memory per row (24 of 516 at the defaults; the band count is unchanged)
+  static const bool bulk_on = [] {
+    const char* e = std::getenv("RV_BULK");
+    return !(e && e[0] == '0');
+  }();
+  if (bulk_on && G % 4 == 0) {
+    p.bulk = 1;
+    p.c_min = 0;
+    p.c_max = G - 1;
+    p.W = G + 4;  // row stride: 16-byte rows for the bulk copies, rows offset by 4 banks
+  }
   const size_t table_bytes = (size_t)(2 * p.halfJ + 64) * sizeof(float2);  // doubled: ranges never wrap
   const size_t fbq_bytes = (size_t)(kVoteThreads / 32) * kFbqCap * 4 + 32 * 4;  // + 32 lane sink words
   const size_t reserve = table_bytes + fbq_bytes + 1024;
@@ -419,9 +432,11 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   // enough CTAs to keep every SM busy, but not more than the work can feed (~1M pairs per CTA)
   const int64_t est_pairs = n * (int64_t)p.halfJ;
   const int n_ctas = (int)std::clamp<int64_t>(est_pairs >> 20, std::min(p.n_bands, c->sms), c->sms);
-  b.max_slots = n_ctas * p.n_bands;
-  b.partials = c->partials.get<uint32_t>((size_t)b.max_slots * p.tile_words);
-  b.slot_band = c->slot_band.get<int32_t>(b.max_slots);
+  b.max_slots = p.bulk ? 0 : n_ctas * p.n_bands;  // bulk: tiles are reduced into the grid directly
+  if (!p.bulk) {
+    b.partials = c->partials.get<uint32_t>((size_t)b.max_slots * p.tile_words);
+    b.slot_band = c->slot_band.get<int32_t>(b.max_slots);
+  }
   if (!prezeroed) {
     ck(cudaMemsetAsync(b.band_work, 0, sizeof(unsigned long long) * kMaxBands, c->st), "memset band_work");
     ck(cudaMemsetAsync(b.counters, 0, sizeof(int32_t) * (2 * kMaxBands + 1), c->st), "memset counters");
@@ -433,8 +448,11 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
     StageScope kv(c, kVoteKernel);
     launch_vote_banded(p, b, n, n_ctas, c->st);
   }
-  launch_vote_reduce(p, b, c->st);
-  count_launch(c, 3);
+  if (!p.bulk || b.red_out) {  // bulk tiles are already in the grid: reduce only for the fused argmax
+    launch_vote_reduce(p, b, c->st);
+    count_launch(c);
+  }
+  count_launch(c, 2);
   ck(cudaGetLastError(), "vote_banded");
   if (c->timing) {
     unsigned long long st[2], work[kMaxBands];
@@ -1067,9 +1085,11 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
     b.stats = c->stats.get<unsigned long long>(2);
     const int64_t est_pairs = (n / C) * (int64_t)p.halfJ;
     const int n_ctas = (int)std::clamp<int64_t>(est_pairs >> 20, std::min(p.n_bands, c->sms), c->sms);
-    b.max_slots = C * n_ctas * p.n_bands;
-    b.partials = c->partials.get<uint32_t>((size_t)b.max_slots * p.tile_words);
-    b.slot_band = c->slot_band.get<int32_t>(b.max_slots);
+    b.max_slots = p.bulk ? 0 : C * n_ctas * p.n_bands;
+    if (!p.bulk) {
+      b.partials = c->partials.get<uint32_t>((size_t)b.max_slots * p.tile_words);
+      b.slot_band = c->slot_band.get<int32_t>(b.max_slots);
+    }
     for (int k = 0; k < C; ++k) {
       ck(cudaStreamWaitEvent(c->st, c->chunk_events[k], 0), "wait chunk");
       pb.kept_publish = k == C - 1;  // chunk counts accumulate; the last chunk publishes the total

@@ -38,6 +38,8 @@ struct VotePlan {
   float band_yhi[kMaxBands];
   float step_f = 0;             // (float)(2*pi/J)
   int banded = 0;               // 1: smem-tiled kernel; 0: exact generic global-atomic kernel
+  int bulk = 0;                 // 1: full-width tiles (c_min = 0, W = G, G % 4 == 0) flushed into the
+                                //    grid by TMA bulk reduce-adds (no partial slots, no slot reduction)
   size_t tile_words = 0;        // H_max * W rounded up to a multiple of 4
   size_t smem_bytes = 0;        // dynamic smem of the vote kernel
 };

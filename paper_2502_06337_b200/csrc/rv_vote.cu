@@ -737,10 +737,28 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     // band exhausted for this CTA: flush the tile to a partial slot, steal the next band
     __syncthreads();
     vtrace(2, band);
+    if (p.bulk && warp == 0) {
+      // the TMA engine adds each tile row (G words; tile row stride W = G + 4 keeps the ATOMS
+      // bank spread) into its grid row (L2 reduce-adds, integer: order-free); the lanes wait only
+      // until the tile has been read, then it can be cleared
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const unsigned long long dst = reinterpret_cast<unsigned long long>(b.grid + (size_t)r0 * G);
+      for (int r = lane; r < hb; r += 32)
+        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u32 [%0], [%1], %2;" ::"l"(
+                         dst + (unsigned long long)r * (unsigned)G * 4u),
+                     "r"(tile_s + (uint32_t)r * (uint32_t)W * 4u), "r"((uint32_t)G * 4u)
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
     if (tid == 0) {
-      const int slot = atomicAdd(&b.counters[0], 1);
-      s_slot = slot;
-      if (slot < b.max_slots) b.slot_band[slot] = band;
+      if (p.bulk) {
+        s_slot = b.max_slots;  // no partial slot
+      } else {
+        const int slot = atomicAdd(&b.counters[0], 1);
+        s_slot = slot;
+        if (slot < b.max_slots) b.slot_band[slot] = band;
+      }
       int best = -1;
       long long best_rem = 0;
       for (int q = 0; q < p.n_bands; ++q) {
@@ -755,7 +773,9 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     __syncthreads();
     const int slot = s_slot;
     const size_t words = (size_t)hb * W;
-    if (slot < b.max_slots) {
+    if (p.bulk) {
+      // flushed by the bulk reduce above
+    } else if (slot < b.max_slots) {
       uint4* dst = reinterpret_cast<uint4*>(b.partials + (size_t)slot * p.tile_words);
       const uint4* src = reinterpret_cast<const uint4*>(tile);
       for (size_t k = tid; k < (words + 3) / 4; k += blockDim.x) __stcg(dst + k, src[k]);
@@ -770,6 +790,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     __syncthreads();
   }
   vtrace(4, 0);
+  if (p.bulk && warp == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // flushes landed
   if (lane == 0 && my_fb) atomicAdd(&b.stats[1], (unsigned long long)my_fb);
 }
 
@@ -836,7 +857,7 @@ __global__ void __launch_bounds__(kReduceThreads) vote_reduce_kernel(VotePlan p,
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int w = 4 * v + i;
-        if (w < words) {
+        if (w < words && w % p.W <= p.c_max - p.c_min) {  // (bulk tiles: padded row stride)
           const int row = r0 + w / p.W, col = p.c_min + w % p.W;
           const size_t gi = (size_t)row * p.G + col;
           if (fused) {  // final cell value (the exact path may have added to the global grid)
