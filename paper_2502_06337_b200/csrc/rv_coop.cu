@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "rv_exact.cuh"
 #include "rv_internal.h"
@@ -67,6 +68,9 @@ struct CoopArgs {
   uint32_t* zero_bins;      // angle histogram to clear for the angle vote that follows
   int n_bins;
   unsigned long long* zero_counts;  // [2]
+  // > 0: the block's constraint slice stays resident in shared memory after the first pass
+  // (SoA, z_cap elements per coordinate); later passes classify from there
+  int z_cap;
 };
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -105,6 +109,7 @@ __device__ __forceinline__ void block_reduce8(double (&v)[8], double (*s_red)[kW
 }
 
 __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
+  extern __shared__ double s_z[];  // [3][z_cap] when a.z_cap > 0
   __shared__ double s_red[8][kWarps];
   __shared__ double s_next[4];  // next axis (3) + next e
   __shared__ int s_done;
@@ -121,6 +126,9 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
   int slot = 0, refits = 0;
   unsigned int bar_target = 0;
   bool have_prev = false;
+  bool first_pass = true;
+  const int64_t e_begin = t_begin * kTile;
+  const int64_t cap = a.z_cap;
   for (;;) {
     // ---- classify pass over this block's tiles ----
     trace(1);
@@ -132,15 +140,30 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
     int diff = 0, cnt = 0;
     for (int64_t t0 = t_begin; t0 < t_end; t0 += kChunk) {
       double z[kChunk][kPerTile][3];
+      uint32_t pw[kChunk][kPerTile];  // the previous pass's flag words (batched with the z loads)
 #pragma unroll
       for (int c = 0; c < kChunk; ++c)  // all loads of the chunk first
 #pragma unroll
         for (int r = 0; r < kPerTile; ++r) {
           const int64_t i = (t0 + c) * kTile + r * kThreads + tid;
           const bool ok = t0 + c < t_end && i < a.n;
-          z[c][r][0] = ok ? a.zx[i] : 0.0;
-          z[c][r][1] = ok ? a.zy[i] : 0.0;
-          z[c][r][2] = ok ? a.zz[i] : 0.0;
+          const int64_t wq = (t0 + c) * kTile + r * kThreads + warp * 32;
+          pw[c][r] = (prev && t0 + c < t_end && wq < a.n) ? __ldcg(prev + (wq >> 5)) : 0u;
+          const int64_t li = i - e_begin;  // the same thread owns element i in every pass
+          if (cap > 0 && !first_pass) {
+            z[c][r][0] = ok ? s_z[li] : 0.0;
+            z[c][r][1] = ok ? s_z[cap + li] : 0.0;
+            z[c][r][2] = ok ? s_z[2 * cap + li] : 0.0;
+          } else {
+            z[c][r][0] = ok ? a.zx[i] : 0.0;
+            z[c][r][1] = ok ? a.zy[i] : 0.0;
+            z[c][r][2] = ok ? a.zz[i] : 0.0;
+            if (cap > 0 && ok) {
+              s_z[li] = z[c][r][0];
+              s_z[cap + li] = z[c][r][1];
+              s_z[2 * cap + li] = z[c][r][2];
+            }
+          }
         }
 #pragma unroll
       for (int c = 0; c < kChunk; ++c) {
@@ -158,7 +181,7 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
           const int64_t w0 = (t0 + c) * kTile + r * kThreads + warp * 32;
           if (lane == 0 && w0 < a.n) {
             flags[w0 >> 5] = word;
-            if (prev && prev[w0 >> 5] != word) diff = 1;
+            if (prev && pw[c][r] != word) diff = 1;
             if (word) atomicAdd(a.tile_count + t0 + c, __popc(word));
           }
           if (in) {
@@ -344,6 +367,7 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
     e = s_next[3];
     slot ^= 1;
     have_prev = a.mode == 0;
+    first_pass = false;
   }
 }
 
@@ -400,9 +424,43 @@ cudaError_t launch_coop_refine(const double* zx, const double* zy, const double*
   a.zero_counts = zero_counts;
   const int64_t ntiles = (n + kTile - 1) / kTile;
   if (grid > ntiles) grid = (int)(ntiles > 0 ? ntiles : 1);  // every block owns >= 1 tile
+  // keep each block's slice of z in shared memory across the passes when it fits (N <= ~1.1M
+  // at 148 blocks); the block count (one per SM) is unchanged by the shared memory it takes
+  static int smem_max = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
+  }();
+  const int64_t per_block = (ntiles + grid - 1) / grid * kTile;
+  static const size_t static_bytes = [] {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(coop_refine_kernel));
+    return fa.sharedSizeBytes + 1024;  // + the runtime's reserved shared memory per block
+  }();
+  size_t dyn = (size_t)(3 * per_block) * sizeof(double);
+  a.z_cap = (int)per_block;
+  if (mode != 0 && mode != 1) a.z_cap = 0;
+  if (dyn + static_bytes > (size_t)smem_max) {
+    a.z_cap = 0;
+    dyn = 0;
+  }
+  if (dyn > 0) {
+    static std::mutex mu;
+    static size_t configured[16] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev < 0 || dev >= 16 || configured[dev] < dyn) {
+      const cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(coop_refine_kernel),
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+      if (e != cudaSuccess) return e;
+      if (dev >= 0 && dev < 16) configured[dev] = dyn;
+    }
+  }
   void* args[] = {&a};
   // cooperative launch: guarantees co-residency of all blocks (required by the grid barrier)
-  return cudaLaunchCooperativeKernel((void*)coop_refine_kernel, dim3(grid), dim3(kThreads), args, 0, s);
+  return cudaLaunchCooperativeKernel((void*)coop_refine_kernel, dim3(grid), dim3(kThreads), args, dyn, s);
 }
 
 size_t coop_state_bytes() { return sizeof(State); }
