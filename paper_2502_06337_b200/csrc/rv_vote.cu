@@ -341,8 +341,8 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
     int wbase = 0;
     if (lane == 0 && total) wbase = global ? atomicAdd(&b.entry_count[band], total) : atomicAdd(&s_cnt[band], total);
     wbase = __shfl_sync(0xFFFFFFFFu, wbase, 0);
-    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xFFFFFFFFu, w, o);
-    if (lane == 0 && w) atomicAdd(&s_work[band], w);
+    const unsigned ws = __reduce_add_sync(0xFFFFFFFFu, (unsigned)w);  // w <= J/2 pairs per lane
+    if (lane == 0 && ws) atomicAdd(&s_work[band], (unsigned long long)ws);
     return wbase + __popc(m0 & lt_mask) + __popc(m1 & lt_mask);
   };
   auto emit = [&](int band, uint2 r, int64_t off) {
