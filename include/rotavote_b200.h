@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define RV_ABI_VERSION 2
+#define RV_ABI_VERSION 3
 
 typedef enum rv_status {
   RV_OK = 0,
@@ -43,7 +43,10 @@ typedef enum rv_status {
   RV_ERR_CUDA = 11,                 /* CUDA runtime failure (message in rv_context_last_error) */
   RV_ERR_NCCL = 12,
   RV_ERR_INVALID_ARGUMENT = 13,
-  RV_ERR_NO_DEVICE = 14
+  RV_ERR_NO_DEVICE = 14,
+  RV_ERR_PARSE = 15,                /* rotavote::ParseError (line in error_line) */
+  RV_ERR_EMPTY_FILE = 16,           /* rotavote::EmptyFile */
+  RV_ERR_IO = 17                    /* rotavote::IoError */
 } rv_status;
 
 /* EstimatorConfig, estimator.hpp:13-29 -- same fields, same defaults (rv_config_default). */
@@ -176,6 +179,24 @@ rv_status rv_vote_shard(rv_context* ctx, const double* d_corrs_shard, int64_t n_
  * (the summed shard grids): preprocess, then peak / refine / angle / rescue as usual. */
 rv_status rv_estimate_single_prevoted(rv_context* ctx, const double* d_corrs, int64_t n, const rv_config* cfg,
                                       const uint32_t* d_grid, rv_estimate* out);
+
+/* ---- CSV ingest ------------------------------------------
+ * read_correspondences (io.hpp:11-13, io.cpp:66-101): CSV rows x0,x1,x2,y0,y1,y2 with an
+ * optional header line, parsed ON THE DEVICE (delimiter index + exact decimal->binary
+ * conversion; the rare fields outside the exact fast path use the host's std::from_chars). The
+ * rows land in context-owned device memory: *d_rows (n_rows x 6 f64, the reference's
+ * Correspondence layout) stays valid until the next CSV call on the context and can be passed
+ * straight to rv_estimate_single_device. Errors follow the reference: RV_ERR_PARSE with the
+ * 1-based line in *error_line and the reference's message in rv_context_last_error
+ * ("expected 6 fields, got N", "not a number: 'x'", "empty field"), RV_ERR_EMPTY_FILE, RV_ERR_IO. */
+rv_status rv_parse_correspondences_csv(rv_context* ctx, const char* text, int64_t nbytes, const double** d_rows,
+                                       int64_t* n_rows, int64_t* error_line);
+rv_status rv_read_correspondences_csv(rv_context* ctx, const char* path, const double** d_rows, int64_t* n_rows,
+                                      int64_t* error_line);
+
+/* Copy `bytes` from device memory (e.g. the rows of a CSV call) to host memory, ordered after the
+ * context's work. */
+rv_status rv_device_to_host(rv_context* ctx, void* dst, const void* d_src, int64_t bytes);
 
 /* Inliers (ascending input indices) of model `model` of the last estimate call. */
 rv_status rv_result_inliers(rv_context* ctx, int32_t model, int32_t* dst, int64_t capacity);

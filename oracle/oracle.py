@@ -168,6 +168,26 @@ class Oracle:
         self._ck(f(_p(zz, C.c_double), C.c_int64(zz.shape[0]), _p(out, C.c_double)), "refine_axis")
         return out
 
+    # ---- I/O (reference library only: io.cpp) ------------------------------------------------
+    def read_correspondences(self, path):
+        """The reference's read_correspondences (io.cpp:66-101): (rows, None) or (None, (kind,
+        message, line)) with kind in {"ParseError", "EmptyFile", "IoError"}."""
+        assert self.kind != "port", "I/O is checked against the compiled reference only"
+        out = C.POINTER(C.c_double)()
+        n, line = C.c_int64(), C.c_int64()
+        msg = C.create_string_buffer(1024)
+        f = self._fn("read_correspondences")
+        f.restype = C.c_int
+        st = f(str(path).encode(), C.byref(out), C.byref(n), C.byref(line), msg, C.c_int64(1024))
+        if st == 0:
+            rows = np.ctypeslib.as_array(out, shape=(n.value * 6,)).copy().reshape(-1, 6) if n.value else np.empty((0, 6))
+            self._fn("free")(out)
+            return rows, None
+        kinds = {15: "ParseError", 16: "EmptyFile", 17: "IoError"}
+        if st not in kinds:
+            raise OracleError(st, "read_correspondences")
+        return None, (kinds[st], msg.value.decode(), int(line.value))
+
     # ---- baselines (reference library only: baselines.cpp) ----------------------------------
     def grid_oracle_axis(self, z, directions=10000, eps=0.015):
         assert self.kind != "port", "baselines are checked against the compiled reference only"

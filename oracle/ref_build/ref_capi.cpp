@@ -13,6 +13,7 @@
 #include "rotavote/errors.hpp"
 #include "rotavote/baselines.hpp"
 #include "rotavote/estimator.hpp"
+#include "rotavote/io.hpp"
 #include "rotavote/voting.hpp"
 
 using namespace rotavote;
@@ -220,5 +221,47 @@ int ref_refine_axis(const double* z, int64_t n, double axis_out[3]) {
     const Vec3 a = refine_axis(to_vecs(z, n));
     for (int k = 0; k < 3; ++k) axis_out[k] = a(k);
   });
+}
+
+// read_correspondences (io.cpp:66-101) -- the parity oracle and CPU baseline of the device CSV
+// ingest. Returns 0 (rows in *out, grown with malloc; free with ref_free), 15 ParseError
+// (message + line), 16 EmptyFile, 17 IoError (message), 99 other.
+int ref_read_correspondences(const char* path, double** out, int64_t* n, int64_t* line, char* msg, int64_t msg_cap) {
+  auto put = [&](const std::string& m) {
+    if (msg && msg_cap > 0) {
+      std::strncpy(msg, m.c_str(), (size_t)msg_cap - 1);
+      msg[msg_cap - 1] = 0;
+    }
+  };
+  *out = nullptr;
+  *n = 0;
+  *line = 0;
+  try {
+    const auto v = read_correspondences(path);
+    double* p = static_cast<double*>(std::malloc(sizeof(double) * 6 * (v.empty() ? 1 : v.size())));
+    for (size_t i = 0; i < v.size(); ++i) {
+      p[6 * i + 0] = v[i].x.x();
+      p[6 * i + 1] = v[i].x.y();
+      p[6 * i + 2] = v[i].x.z();
+      p[6 * i + 3] = v[i].y.x();
+      p[6 * i + 4] = v[i].y.y();
+      p[6 * i + 5] = v[i].y.z();
+    }
+    *out = p;
+    *n = static_cast<int64_t>(v.size());
+    return 0;
+  } catch (const ParseError& e) {
+    *line = e.line;
+    put(e.what());
+    return 15;
+  } catch (const EmptyFile& e) {
+    put(e.what());
+    return 16;
+  } catch (const IoError& e) {
+    put(e.what());
+    return 17;
+  } catch (...) {
+    return 99;
+  }
 }
 }

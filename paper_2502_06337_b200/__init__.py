@@ -17,8 +17,8 @@ import numpy as np
 
 from . import errors
 from ._native import check, lib, rv_config, rv_estimate, rv_peak, rv_stage_times
-from .errors import (AllDegenerate, DegenerateProjection, EmptyInput, Error, InvalidConfig, NoConsensus,  # noqa: F401
-                     NoPeak, NoVotes, PoleProximity, RankDeficient)
+from .errors import (AllDegenerate, DegenerateProjection, EmptyFile, EmptyInput, Error, InvalidConfig,  # noqa: F401
+                     IoError, NoConsensus, NoPeak, NoVotes, ParseError, PoleProximity, RankDeficient)
 
 __all__ = [
     "EstimatorConfig", "RotationEstimate", "Peak", "Context", "default_context", "errors",
@@ -139,6 +139,44 @@ class Context:
         self._check(self._lib.rv_estimate_single(self.handle, _ptr(a, C.c_double), a.shape[0] if a.size else 0,
                                                  C.byref(c), C.byref(e)))
         return self._estimate(e, 0)
+
+    # ---- CSV ingest (io.cpp:66-101 read_correspondences), parsed on the device ----
+    def _csv(self, call) -> tuple[int, int]:
+        d = C.c_void_p()
+        n = C.c_int64()
+        line = C.c_int64()
+        st = call(d, n, line)
+        if st == 15:  # ParseError carries the line
+            detail = lib().rv_context_last_error(self.handle)
+            raise errors.ParseError(detail.decode() if detail else "parse error", int(line.value))
+        self._check(st)
+        return int(d.value or 0), int(n.value)
+
+    def parse_correspondences_device(self, text: bytes) -> tuple[int, int]:
+        """CSV text -> (device pointer, rows): n x 6 f64 in context memory, valid until the next CSV
+        call on this context (pass it to estimate_single_device)."""
+        return self._csv(lambda d, n, l: self._lib.rv_parse_correspondences_csv(
+            self.handle, text, len(text), C.byref(d), C.byref(n), C.byref(l)))
+
+    def read_correspondences_device(self, path: str) -> tuple[int, int]:
+        return self._csv(lambda d, n, l: self._lib.rv_read_correspondences_csv(
+            self.handle, str(path).encode(), C.byref(d), C.byref(n), C.byref(l)))
+
+    def _rows_to_host(self, dptr: int, n: int) -> np.ndarray:
+        out = np.empty((n, 6), np.float64)
+        if n:
+            self._check(self._lib.rv_device_to_host(self.handle, out.ctypes.data_as(C.c_void_p), C.c_void_p(dptr),
+                                                    out.nbytes))
+        return out
+
+    def read_correspondences(self, path: str) -> np.ndarray:
+        """read_correspondences (io.hpp:13): n x 6 f64 [x0,x1,x2,y0,y1,y2] rows on the host."""
+        d, n = self.read_correspondences_device(path)
+        return self._rows_to_host(d, n)
+
+    def parse_correspondences(self, text: bytes) -> np.ndarray:
+        d, n = self.parse_correspondences_device(text)
+        return self._rows_to_host(d, n)
 
     def estimate_single_device(self, dptr: int, n: int, cfg: EstimatorConfig | None = None) -> RotationEstimate:
         """Same solve on correspondences already resident in HBM (device pointer, n x 6 f64)."""

@@ -127,6 +127,11 @@ _SIGS = [
     ("rv_peak_angle", C.c_int,
      [C.c_void_p, c_uint32_p, C.c_int32, C.c_uint64, C.c_int32, c_double_p, C.c_int64, c_double_p]),
     ("rv_peak_vote_floor", C.c_uint32, [C.POINTER(rv_config), C.c_int64]),
+    ("rv_parse_correspondences_csv", C.c_int,
+     [C.c_void_p, C.c_char_p, C.c_int64, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("rv_read_correspondences_csv", C.c_int,
+     [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("rv_device_to_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
     ("rv_rodrigues", None, [c_double_p, C.c_double, c_double_p]),
     ("rv_rotation_error", C.c_double, [c_double_p, c_double_p]),
     ("rv_project", C.c_int, [c_double_p, c_double_p, c_double_p]),

@@ -15,7 +15,7 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "librotavote_b200.so"
 INCLUDE = PKG.parent / "include"
-SOURCES = ["rv_prep.cu", "rv_vote.cu", "rv_peaks.cu", "rv_refine.cu", "rv_coop.cu", "rv_api.cpp"]
+SOURCES = ["rv_prep.cu", "rv_vote.cu", "rv_peaks.cu", "rv_refine.cu", "rv_coop.cu", "rv_io.cu", "rv_api.cpp"]
 # translation units whose device arithmetic must follow the host op order exactly
 NO_FMAD = {"rv_coop.cu"}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <charconv>
+#include <string_view>
 #include <array>
 #include <iterator>
 #include <chrono>
@@ -137,6 +139,11 @@ struct rv_context {
   DBuf peak_out;                         // chained solve: device Summary (peak, state, angles)
   DBuf red_keys;                         // fused argmax scratch of the tile reduction
   DBuf kept_acc;                          // in-order preprocess: kept-count accumulator + ticket
+  // CSV ingest (rv_io.cu)
+  DBuf csv_text, csv_chunk, csv_misc, csv_dpos, csv_dline, csv_nl, csv_status, csv_row, csv_block, csv_out, csv_fb,
+      csv_fix_idx, csv_fix_val;
+  char* csv_pinned = nullptr;             // pinned staging of file contents
+  size_t csv_pinned_cap = 0;
   bool kept_acc_ready = false;
   DBuf cons_axes, cons_counts, cons_z, cons_idx;  // baseline consensus scoring
   int coop_grid = 0;
@@ -1891,6 +1898,9 @@ const char* rv_status_string(rv_status st) {
     case RV_ERR_NCCL: return "NcclError";
     case RV_ERR_INVALID_ARGUMENT: return "InvalidArgument";
     case RV_ERR_NO_DEVICE: return "NoDevice";
+    case RV_ERR_PARSE: return "ParseError";
+    case RV_ERR_EMPTY_FILE: return "EmptyFile";
+    case RV_ERR_IO: return "IoError";
   }
   return "unknown";
 }
@@ -1933,6 +1943,7 @@ void rv_context_destroy(rv_context* c) {
   if (c->cap_st) cudaStreamDestroy(c->cap_st);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->inl_host) cudaFreeHost(c->inl_host);
+  if (c->csv_pinned) cudaFreeHost(c->csv_pinned);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
 }
@@ -2352,6 +2363,251 @@ rv_status rv_estimate_single_prevoted(rv_context* c, const double* d_corrs, int6
     }
     to_c(e, out, seconds_since(c));
     c->results.push_back(std::move(e.inliers));
+  });
+}
+
+
+// ---------------------------------------------------------------------------------------
+// CSV ingest (io.cpp:66-101 read_correspondences) -- device parse, host reference logic for
+// the header decision, the rare fallback fields and the exact error messages.
+
+// parse_double (io.cpp:16-29): trim " \t\r", the whole rest must be a from_chars float literal.
+bool ref_parse_double(std::string_view f, double* v, std::string* err) {
+  const auto b = f.find_first_not_of(" \t\r");
+  if (b == std::string_view::npos) {
+    if (err) *err = "empty field";
+    return false;
+  }
+  const auto e = f.find_last_not_of(" \t\r");
+  f = f.substr(b, e - b + 1);
+  double x = 0.0;
+  const auto [ptr, ec] = std::from_chars(f.data(), f.data() + f.size(), x);
+  if (ec != std::errc{} || ptr != f.data() + f.size()) {
+    if (err) *err = "not a number: '" + std::string(f) + "'";
+    return false;
+  }
+  *v = x;
+  return true;
+}
+
+// The reference's handling of one physical line (io.cpp:71-97): the first error message, or
+// "" when the line is blank, a header (line 1) or a valid row.
+std::string ref_line_error(std::string_view line, int line_number) {
+  if (!line.empty() && line.back() == '\r') line.remove_suffix(1);
+  if (line.find_first_not_of(" \t") == std::string_view::npos) return "";
+  std::vector<std::string_view> fields;
+  for (size_t pos = 0;;) {
+    const size_t nx = line.find(',', pos);
+    if (nx == std::string_view::npos) {
+      fields.push_back(line.substr(pos));
+      break;
+    }
+    fields.push_back(line.substr(pos, nx - pos));
+    pos = nx + 1;
+  }
+  double v;
+  if (line_number == 1 && !ref_parse_double(fields[0], &v, nullptr)) return "";  // header
+  if (fields.size() != 6) return "expected 6 fields, got " + std::to_string(fields.size());
+  // io.cpp:89-92 parses each Vec3's three fields as constructor arguments; GCC evaluates them
+  // right to left, so the first reported bad field is the first failing of 2,1,0 then 5,4,3
+  std::string err;
+  for (const int k : {2, 1, 0, 5, 4, 3})
+    if (!ref_parse_double(fields[(size_t)k], &v, &err)) return err;
+  return "";
+}
+
+std::string_view nth_line(const char* text, int64_t nbytes, int64_t line_number) {
+  const char* p = text;
+  const char* end = text + nbytes;
+  for (int64_t k = 1; k < line_number && p < end; ++k) {
+    const void* nl = std::memchr(p, '\n', (size_t)(end - p));
+    p = nl ? static_cast<const char*>(nl) + 1 : end;
+  }
+  const void* nl = std::memchr(p, '\n', (size_t)(end - p));
+  return std::string_view(p, (size_t)((nl ? static_cast<const char*>(nl) : end) - p));
+}
+
+const double* parse_csv_dev(rv_context* c, const char* text, int64_t nbytes, const std::string& name, int64_t* n_rows,
+                            int64_t* err_line) {
+  *n_rows = 0;
+  *err_line = 0;
+  if (nbytes <= 0) fail(RV_ERR_EMPTY_FILE, "no data in " + name);
+  const bool add_nl = text[nbytes - 1] != '\n';
+  const int64_t total = nbytes + (add_nl ? 1 : 0);
+  if (total >= ((int64_t)1 << 32)) fail(RV_ERR_INVALID_ARGUMENT, "CSV text larger than 4 GB");
+  CsvBuffers b;
+  uint8_t* dtext = c->csv_text.get<uint8_t>((size_t)total + 16);
+  b.text = dtext;
+  b.nbytes = total;
+  ck(cudaMemcpyAsync(dtext, text, (size_t)nbytes, cudaMemcpyHostToDevice, c->st), "CSV H2D");
+  static const char kNl = '\n';
+  if (add_nl) ck(cudaMemcpyAsync(dtext + nbytes, &kNl, 1, cudaMemcpyHostToDevice, c->st), "CSV newline");
+  {  // header decision on the host (io.cpp:76-84): line 1, non-blank, first field not a number
+    std::string_view l1 = nth_line(text, nbytes, 1);
+    if (!l1.empty() && l1.back() == '\r') l1.remove_suffix(1);
+    double v;
+    b.skip_first = l1.find_first_not_of(" \t") != std::string_view::npos &&
+                   !ref_parse_double(l1.substr(0, l1.find(',')), &v, nullptr);
+  }
+  const int nchunks = csv_chunks(total);
+  b.chunk = c->csv_chunk.get<int2>((size_t)nchunks);
+  int32_t* misc = c->csv_misc.get<int32_t>(8);  // [0,1] totals, [2] err_line, [3] nrows, [4] fb_count
+  b.totals = reinterpret_cast<int2*>(misc);
+  StageScope sc(c, kPrep);
+  ck(launch_csv_parse(b, c->st, 0), "CSV census");
+  count_launch(c, 2);
+  int32_t* h = reinterpret_cast<int32_t*>(c->pinned);
+  ck(cudaMemcpyAsync(h, misc, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->st), "CSV totals");
+  sync(c);
+  b.nfields = h[0];
+  b.nlines = h[1];
+  const int nl = b.nlines;
+  b.dpos = c->csv_dpos.get<uint32_t>((size_t)b.nfields);
+  b.dline = c->csv_dline.get<int32_t>((size_t)b.nfields);
+  b.nl_delim = c->csv_nl.get<int32_t>((size_t)nl);
+  b.status = c->csv_status.get<int8_t>((size_t)nl);
+  b.row = c->csv_row.get<int32_t>((size_t)nl);
+  b.block = c->csv_block.get<int32_t>((size_t)(nl + 1023) / 1024 + 1);
+  b.nrows = misc + 3;
+  b.out = c->csv_out.get<double>((size_t)nl * 6);
+  b.cap_rows = nl;
+  b.err_line = reinterpret_cast<unsigned int*>(misc + 2);
+  b.fb_cap = 1 << 16;
+  b.fb = c->csv_fb.get<CsvFallback>((size_t)b.fb_cap);
+  b.fb_count = misc + 4;
+  ck(cudaMemsetAsync(misc + 2, 0xFF, sizeof(int32_t), c->st), "CSV err_line");
+  ck(cudaMemsetAsync(misc + 4, 0, sizeof(int32_t), c->st), "CSV fb_count");
+  ck(launch_csv_parse(b, c->st, 1), "CSV parse");
+  count_launch(c, 6);
+  ck(cudaMemcpyAsync(h, misc, 5 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->st), "CSV summary");
+  sync(c);
+  uint32_t errl = (uint32_t)h[2];
+  const int64_t nrows = h[3];
+  const int64_t nfb = h[4];
+  if (nfb > 0) {  // the rare fields outside the device's exact fast path: the host's from_chars
+    std::vector<int64_t> idx;
+    std::vector<double> val;
+    if (nfb <= b.fb_cap) {
+      std::vector<CsvFallback> fb((size_t)nfb);
+      ck(cudaMemcpyAsync(fb.data(), b.fb, sizeof(CsvFallback) * (size_t)nfb, cudaMemcpyDeviceToHost, c->st),
+         "CSV fallback D2H");
+      sync(c);
+      for (const auto& f : fb) {
+        double v;
+        if (ref_parse_double(std::string_view(text + f.start, (size_t)(f.end - f.start)), &v, nullptr)) {
+          idx.push_back(f.row * 6 + f.col);
+          val.push_back(v);
+        } else {
+          errl = std::min<uint32_t>(errl, (uint32_t)(f.line + 1));
+        }
+      }
+    } else {  // too many to queue: the host parses every row the device marked as data
+      std::vector<int8_t> st((size_t)nl);
+      std::vector<int32_t> rw((size_t)nl);
+      ck(cudaMemcpyAsync(st.data(), b.status, (size_t)nl, cudaMemcpyDeviceToHost, c->st), "CSV status");
+      ck(cudaMemcpyAsync(rw.data(), b.row, sizeof(int32_t) * (size_t)nl, cudaMemcpyDeviceToHost, c->st), "CSV rows");
+      sync(c);
+      const char* p = text;
+      for (int64_t l = 0; l < nl; ++l) {
+        const void* q = std::memchr(p, '\n', (size_t)(text + nbytes - p));
+        const char* e = q ? static_cast<const char*>(q) : text + nbytes;
+        if (st[(size_t)l] == 1) {
+          std::string_view line(p, (size_t)(e - p));
+          if (!line.empty() && line.back() == '\r') line.remove_suffix(1);
+          size_t pos = 0;
+          for (int col = 0; col < 6; ++col) {
+            const size_t nx = col < 5 ? line.find(',', pos) : line.size();
+            double v;
+            if (ref_parse_double(line.substr(pos, nx - pos), &v, nullptr)) {
+              idx.push_back((int64_t)rw[(size_t)l] * 6 + col);
+              val.push_back(v);
+            } else {
+              errl = std::min<uint32_t>(errl, (uint32_t)(l + 1));
+            }
+            pos = nx + 1;
+          }
+        }
+        p = e + 1;
+      }
+    }
+    if (!idx.empty()) {
+      int64_t* di = c->csv_fix_idx.get<int64_t>(idx.size());
+      double* dv = c->csv_fix_val.get<double>(val.size());
+      ck(cudaMemcpyAsync(di, idx.data(), sizeof(int64_t) * idx.size(), cudaMemcpyHostToDevice, c->st), "CSV fix idx");
+      ck(cudaMemcpyAsync(dv, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice, c->st), "CSV fix val");
+      launch_csv_scatter(di, dv, (int)idx.size(), b.out, c->st);
+      count_launch(c);
+      sync(c);  // the host vectors go out of scope
+    }
+  }
+  if (errl != 0xFFFFFFFFu) {
+    *err_line = errl;
+    std::string msg = ref_line_error(nth_line(text, nbytes, errl), (int)errl);
+    if (msg.empty()) msg = "parse error";
+    fail(RV_ERR_PARSE, msg);
+  }
+  if (nrows == 0) fail(RV_ERR_EMPTY_FILE, (b.skip_first ? "no correspondence rows in " : "no data in ") + name);
+  *n_rows = nrows;
+  return b.out;
+}
+
+rv_status rv_device_to_host(rv_context* c, void* dst, const void* d_src, int64_t bytes) {
+  if (!c || bytes < 0 || (bytes > 0 && (!dst || !d_src))) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (bytes > 0) ck(cudaMemcpyAsync(dst, d_src, (size_t)bytes, cudaMemcpyDeviceToHost, c->st), "D2H");
+    sync(c);
+  });
+}
+
+rv_status rv_parse_correspondences_csv(rv_context* c, const char* text, int64_t nbytes, const double** d_rows,
+                                       int64_t* n_rows, int64_t* error_line) {
+  if (!c || !d_rows || !n_rows || !error_line || (nbytes > 0 && !text) || nbytes < 0) return RV_ERR_INVALID_ARGUMENT;
+  *d_rows = nullptr;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    *d_rows = parse_csv_dev(c, text, nbytes, "<memory>", n_rows, error_line);
+  });
+}
+
+rv_status rv_read_correspondences_csv(rv_context* c, const char* path, const double** d_rows, int64_t* n_rows,
+                                      int64_t* error_line) {
+  if (!c || !path || !d_rows || !n_rows || !error_line) return RV_ERR_INVALID_ARGUMENT;
+  *d_rows = nullptr;
+  *n_rows = 0;
+  *error_line = 0;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    FILE* f = std::fopen(path, "rb");
+    if (!f) fail(RV_ERR_IO, std::string("cannot open for reading: ") + path);
+    std::fseek(f, 0, SEEK_END);
+    const long sz = std::ftell(f);
+    std::fseek(f, 0, SEEK_SET);
+    if (sz < 0) {
+      std::fclose(f);
+      fail(RV_ERR_IO, std::string("cannot read: ") + path);
+    }
+    if ((size_t)sz + 1 > c->csv_pinned_cap) {  // pinned staging: the H2D runs at full PCIe rate
+      if (c->csv_pinned) {
+        sync(c);
+        cudaFreeHost(c->csv_pinned);
+        c->csv_pinned = nullptr;
+        c->csv_pinned_cap = 0;
+      }
+      void* p = nullptr;
+      const size_t cap = (size_t)sz + 1 + (size_t)sz / 4;
+      if (cudaHostAlloc(&p, cap, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        std::fclose(f);
+        fail(RV_ERR_OUT_OF_MEMORY, "pinned CSV staging");
+      }
+      c->csv_pinned = static_cast<char*>(p);
+      c->csv_pinned_cap = cap;
+    }
+    const size_t got = sz > 0 ? std::fread(c->csv_pinned, 1, (size_t)sz, f) : 0;
+    std::fclose(f);
+    if (got != (size_t)sz) fail(RV_ERR_IO, std::string("cannot read: ") + path);
+    *d_rows = parse_csv_dev(c, c->csv_pinned, (int64_t)sz, path, n_rows, error_line);
   });
 }
 

@@ -223,4 +223,37 @@ cudaError_t launch_coop_refine(const double* zx, const double* zy, const double*
                                int32_t* compact_out = nullptr, uint32_t* zero_bins = nullptr, int n_bins = 0,
                                unsigned long long* zero_counts = nullptr);
 
+// ---- CSV ingest (rv_io.cu; io.cpp:66-101) ------------------------------------------------
+struct CsvFallback {  // a field the device left to the host's from_chars
+  int64_t start, end;   // byte range before trimming (line '\r' already removed)
+  int64_t row;
+  int32_t col, line;    // line: 0-based physical line
+};
+struct CsvBuffers {
+  const uint8_t* text = nullptr;  // ends with '\n'
+  int64_t nbytes = 0;
+  int2* chunk = nullptr;          // per-8KB-chunk delimiter/newline counts -> exclusive offsets
+  int2* totals = nullptr;         // (delimiters, newlines)
+  uint32_t* dpos = nullptr;       // byte position of every ',' / '\n'
+  int32_t* dline = nullptr;       // 0-based line of every delimiter
+  int32_t* nl_delim = nullptr;    // delimiter index of every newline
+  int nlines = 0, nfields = 0;
+  int skip_first = 0;             // line 1 is a header (decided by the host, io.cpp:76-84)
+  int8_t* status = nullptr;       // per line: blank / data / header / bad field count
+  int32_t* row = nullptr;         // per line: data flag -> row index (exclusive scan)
+  int32_t* block = nullptr;       // scan scratch
+  int32_t* nrows = nullptr;       // total rows
+  double* out = nullptr;          // rows x 6 f64 (the reference's Correspondence layout)
+  int64_t cap_rows = 0;
+  unsigned int* err_line = nullptr;  // min 1-based line with an error (~0u: none)
+  CsvFallback* fb = nullptr;
+  int fb_cap = 0;
+  int32_t* fb_count = nullptr;
+};
+int csv_chunks(int64_t nbytes);
+// stage 0: delimiter census + scan (the host then reads `totals`); stage 1: index, lines, rows,
+// fields (the host then reads err_line / nrows / fb_count)
+cudaError_t launch_csv_parse(const CsvBuffers& b, cudaStream_t s, int stage);
+void launch_csv_scatter(const int64_t* idx, const double* vals, int n, double* out, cudaStream_t s);
+
 }  // namespace rvb

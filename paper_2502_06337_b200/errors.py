@@ -42,6 +42,22 @@ class InvalidConfig(Error):
     pass
 
 
+class IoError(Error):
+    pass
+
+
+class EmptyFile(Error):
+    pass
+
+
+class ParseError(Error):
+    """rotavote::ParseError: message "<what> (line N)", the 1-based line in .line."""
+
+    def __init__(self, msg: str, line: int = 0):
+        super().__init__(f"{msg} (line {line})")
+        self.line = line
+
+
 class DeviceError(Error):
     """CUDA / NCCL / allocation failures of the device path (no reference counterpart)."""
 
@@ -58,6 +74,9 @@ STATUS_TO_ERROR = {
     9: PoleProximity,
     10: DeviceError,
     11: DeviceError,
+    15: ParseError,
+    16: EmptyFile,
+    17: IoError,
     12: DeviceError,
     13: DeviceError,
     14: DeviceError,
