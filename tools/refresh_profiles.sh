@@ -11,6 +11,8 @@ if [ -f gpurun_out/prof/secondary.ncu-rep ]; then
 fi
 [ -f gpurun_out/prof/timeline_c3.txt ] && grep -v Warn gpurun_out/prof/timeline_c3.txt | grep -v _warn_once > $P/timeline_c3_device.txt
 [ -f gpurun_out/prof/timeline_c3_host.txt ] && grep -v Warn gpurun_out/prof/timeline_c3_host.txt | grep -v _warn_once > $P/timeline_c3_e2e.txt
+[ -f gpurun_out/prof/io_bench.json ] && cp gpurun_out/prof/io_bench.json $P/io_bench_r1.json
+[ -f gpurun_out/prof/pytest_gpu.log ] && tail -3 gpurun_out/prof/pytest_gpu.log > $P/pytest_gpu_r1.txt
 [ -f gpurun_out/prof/gpu_check.log ] && cut -c1-600 gpurun_out/prof/gpu_check.log > $P/gpu_check_r1.txt
 python tools/summarize_profiles.py --json $P/vote_banded_r1.ncu-rep | sed "s#\"source\": \"vote_banded_r1.ncu-rep\"#\"source\": \"$P/vote_banded_r1.ncu-rep\"#" > $P/vote_kernel_ncu.json
 { echo "# Round 1 measurement bundle (tools/profile_round.sh on one B200; see DESIGN.md section 6)"
