@@ -144,6 +144,8 @@ struct rv_context {
       csv_fix_idx, csv_fix_val;
   char* csv_pinned = nullptr;             // pinned staging of file contents
   size_t csv_pinned_cap = 0;
+  double* in_pinned = nullptr;            // pinned staging of small pageable single-solve inputs
+  size_t in_pinned_cap = 0;
   bool kept_acc_ready = false;
   DBuf cons_axes, cons_counts, cons_z, cons_idx;  // baseline consensus scoring
   int coop_grid = 0;
@@ -1328,6 +1330,10 @@ Estimate estimate_single_dev(rv_context* c, const double* d_corrs, int64_t n, co
     const uint32_t* grid = enqueue_single(c, pre, d_corrs, cfg, nullptr, false);
     if (g) {  // remember this enqueue's host counters and the buffer generation it ran with
       g->delta = count_delta(c->times, t0);
+      if (g->exec) {  // captured before a buffer moved: stale pointers, never replay it again
+        cudaGraphExecDestroy(g->exec);
+        g->exec = nullptr;
+      }
       g->gen = g_buf_gen.load();
       g->seen += 1;
     }
@@ -1356,8 +1362,37 @@ bool host_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+// Small pageable inputs are staged into a context-owned pinned buffer first (n x 48 B, a few
+// microseconds): the H2D then runs at DMA speed and the staged solve is graph-replayable (the
+// staging pointer repeats), which is what many small independent solves (estimate_batch) need.
+constexpr int64_t kStageMaxRows = (int64_t)1 << 18;
+const double* stage_small_input(rv_context* c, const double* h, int64_t n) {
+  if (n > kStageMaxRows || host_pinned(h)) return h;
+  const size_t bytes = sizeof(double) * 6 * (size_t)n;
+  if (bytes > c->in_pinned_cap) {
+    if (c->in_pinned) {
+      sync(c);
+      cudaFreeHost(c->in_pinned);
+      c->in_pinned = nullptr;
+      c->in_pinned_cap = 0;
+    }
+    void* p = nullptr;
+    const size_t cap = std::max<size_t>(bytes, (size_t)48 << 10);
+    g_buf_gen.fetch_add(1);
+    if (cudaHostAlloc(&p, cap, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      return h;
+    }
+    c->in_pinned = static_cast<double*>(p);
+    c->in_pinned_cap = cap;
+  }
+  std::memcpy(c->in_pinned, h, bytes);  // (every call ends synchronised: no copy still reads it)
+  return c->in_pinned;
+}
+
 Estimate estimate_single_host(rv_context* c, const double* h_corrs, int64_t n, const rv_config& cfg) {
   if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
+  h_corrs = stage_small_input(c, h_corrs, n);
   // Repeated solves from the same pinned host buffer replay a captured graph of the whole
   // pipelined solve (chunked H2D on the copy stream + the in-order device chain): the copy
   // engine and the SMs run without waiting for the host to issue the next copy or launch.
@@ -1392,6 +1427,10 @@ Estimate estimate_single_host(rv_context* c, const double* h_corrs, int64_t n, c
     const uint32_t* grid = enqueue_single(c, pv.pre, pv.d_corrs, cfg, pv.grid, pv.peak_ready);
     if (g) {
       g->delta = count_delta(c->times, t0);
+      if (g->exec) {  // captured before a buffer moved: stale pointers, never replay it again
+        cudaGraphExecDestroy(g->exec);
+        g->exec = nullptr;
+      }
       g->gen = g_buf_gen.load();
       g->seen += 1;
     }
@@ -1944,6 +1983,7 @@ void rv_context_destroy(rv_context* c) {
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->inl_host) cudaFreeHost(c->inl_host);
   if (c->csv_pinned) cudaFreeHost(c->csv_pinned);
+  if (c->in_pinned) cudaFreeHost(c->in_pinned);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
 }

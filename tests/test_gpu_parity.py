@@ -303,6 +303,21 @@ def test_graph_replay_of_device_solves(ctx, port):
     for _ in range(3):
         e = ctx.estimate_single_device(d.data_ptr(), b.shape[0])
         assert np.array_equal(e.inliers, eb.inliers) and np.array_equal(e.rotation, eb.rotation)
+    # a graph captured before a reallocation is never replayed again, even after the key's next
+    # eager run re-arms it (regression: the staged small-input path hit exactly this)
+    e_a = runs[0]
+    ctx.estimate_single_device(db.data_ptr(), big.shape[0])  # grow again between the eager runs
+    for data, want in ((a, e_a), (b, eb), (a, e_a)):
+        d.copy_(torch.from_numpy(data))
+        for _ in range(2):
+            e = ctx.estimate_single_device(d.data_ptr(), data.shape[0])
+            assert np.array_equal(e.inliers, want.inliers) and np.array_equal(e.rotation, want.rotation)
+    small = [synth.make_scene(200, 0.2, 0.01, seed=229 + k)[0] for k in range(4)]
+    want_small = [port.estimate_single(x) for x in small]
+    for rep in range(3):  # staged pageable small inputs: eager, capture, replays
+        for x, w in zip(small, want_small):
+            assert_est_equal(ctx.estimate_single(x), w)
+        ctx.estimate_single(big[:300_000])  # a different solve in between (buffer growth on rep 0)
 
 
 @pytest.mark.parametrize("world", [2, 8])
