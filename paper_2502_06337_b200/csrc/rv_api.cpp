@@ -404,6 +404,13 @@ void set_fused(rv_context* c, VoteBuffers& b, VoteFused* f, const VotePlan& p) {
 
 // accumulate (voting.cpp:88-118) over device SoA constraints into the context grid.
 // prezeroed: the grid and the band counters were already cleared (by the preprocess kernel).
+// CTAs of a band-tiled vote launch: one per ~16k planned pairs (a CTA's fixed cost -- clearing and
+// flushing its tile -- is a few microseconds, so even small problems spread over many SMs), at
+// least one per band, at most one per SM.
+int vote_ctas(const rv_context* c, const VotePlan& p, int64_t est_pairs) {
+  return (int)std::clamp<int64_t>(est_pairs >> 14, std::min(p.n_bands, c->sms), c->sms);
+}
+
 uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* zz, int64_t n, int G, double E,
                int J, bool force_generic = false, bool prezeroed = false, VoteFused* fused = nullptr) {
   if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no constraints to accumulate");
@@ -440,7 +447,7 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   b.stats = c->stats.get<unsigned long long>(2);
   // enough CTAs to keep every SM busy, but not more than the work can feed (~1M pairs per CTA)
   const int64_t est_pairs = n * (int64_t)p.halfJ;
-  const int n_ctas = (int)std::clamp<int64_t>(est_pairs >> 20, std::min(p.n_bands, c->sms), c->sms);
+  const int n_ctas = vote_ctas(c, p, est_pairs);
   b.max_slots = p.bulk ? 0 : n_ctas * p.n_bands;  // bulk: tiles are reduced into the grid directly
   if (!p.bulk) {
     b.partials = c->partials.get<uint32_t>((size_t)b.max_slots * p.tile_words);
@@ -1059,15 +1066,19 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
   for (int k = 0; k <= C; ++k)
     bounds[k] = k == C ? n : std::min<int64_t>(n, ((C > 1 ? n * kCum[k] / 16 : 0) + 1023) / 1024 * 1024);
   StageScope sc(c, kVote);
-  // order the copy stream after everything already queued on the compute stream (buffer reuse)
-  cudaEvent_t start = take_event(c);
-  ck(cudaEventRecord(start, c->st), "record");
-  ck(cudaStreamWaitEvent(c->copy_st, start, 0), "wait");
+  // one chunk: the copy goes on the compute stream itself (no cross-stream dependency to resolve);
+  // several: on the copy stream, ordered after everything already queued on the compute stream
+  cudaStream_t cs = C > 1 ? c->copy_st : c->st;
+  if (C > 1) {
+    cudaEvent_t start = take_event(c);
+    ck(cudaEventRecord(start, c->st), "record");
+    ck(cudaStreamWaitEvent(c->copy_st, start, 0), "wait");
+  }
   auto issue_copy = [&](int k) {
     ck(cudaMemcpyAsync(d + 6 * bounds[k], h_corrs + 6 * bounds[k], sizeof(double) * 6 * (bounds[k + 1] - bounds[k]),
-                       cudaMemcpyHostToDevice, c->copy_st),
+                       cudaMemcpyHostToDevice, cs),
        "H2D chunk");
-    ck(cudaEventRecord(c->chunk_events[k], c->copy_st), "record chunk");
+    if (C > 1) ck(cudaEventRecord(c->chunk_events[k], cs), "record chunk");
   };
   issue_copy(0);
   uint32_t* grid = c->grid.get<uint32_t>((size_t)G * G);
@@ -1093,14 +1104,14 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
     b.entry_count = b.counters + kMaxBands + 1;
     b.stats = c->stats.get<unsigned long long>(2);
     const int64_t est_pairs = (n / C) * (int64_t)p.halfJ;
-    const int n_ctas = (int)std::clamp<int64_t>(est_pairs >> 20, std::min(p.n_bands, c->sms), c->sms);
+    const int n_ctas = vote_ctas(c, p, est_pairs);
     b.max_slots = p.bulk ? 0 : C * n_ctas * p.n_bands;
     if (!p.bulk) {
       b.partials = c->partials.get<uint32_t>((size_t)b.max_slots * p.tile_words);
       b.slot_band = c->slot_band.get<int32_t>(b.max_slots);
     }
     for (int k = 0; k < C; ++k) {
-      ck(cudaStreamWaitEvent(c->st, c->chunk_events[k], 0), "wait chunk");
+      if (C > 1) ck(cudaStreamWaitEvent(c->st, c->chunk_events[k], 0), "wait chunk");
       pb.kept_publish = k == C - 1;  // chunk counts accumulate; the last chunk publishes the total
       launch_preprocess_inorder(pb, n, bounds[k], bounds[k + 1], cfg.tau_z, cfg.normalize_inputs, c->st);
       if (k == 0)
@@ -1146,7 +1157,7 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
     ck(cudaMemsetAsync(pb.status, 0, sizeof(unsigned long long) * nb_prep, c->st), "memset status");
     ck(cudaMemsetAsync(misc, 0, sizeof(int32_t) * 8, c->st), "memset misc");
     for (int k = 0; k < C; ++k) {
-      ck(cudaStreamWaitEvent(c->st, c->chunk_events[k], 0), "wait chunk");
+      if (C > 1) ck(cudaStreamWaitEvent(c->st, c->chunk_events[k], 0), "wait chunk");
       launch_preprocess_range(pb, n, bounds[k], bounds[k + 1], cfg.tau_z, cfg.normalize_inputs, c->st);
       count_launch(c);
       if (k + 1 < C) issue_copy(k + 1);

@@ -41,12 +41,14 @@ __global__ void __launch_bounds__(kPrepThreads) preprocess_kernel(PrepBuffers b,
   if (!kInOrder) __syncthreads();
   const int bid = kInOrder ? (int)(elem_lo / kPrepTile) + blockIdx.x : s_bid;
   const int64_t base = (int64_t)bid * kPrepTile;
+  // in-order launches may carry extra blocks that only clear (small inputs): stay inside the range
+  const int64_t lim = kInOrder ? elem_hi : n;
   double c[kPrepPer][6];
 #pragma unroll
   for (int r = 0; r < kPrepPer; ++r) {  // all loads first (coalesced per round)
     const int64_t i = base + r * kPrepThreads + tid;
     for (int k = 0; k < 6; ++k) c[r][k] = 0.0;
-    if (i < n) {
+    if (i < lim) {
       if (kVec) {
         const double2* p = reinterpret_cast<const double2*>(b.corrs + 6 * i);
         const double2 u = p[0], v = p[1], w = p[2];
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(kPrepThreads) preprocess_kernel(PrepBuffers b,
     }
     const double d0 = xs(y0, x0), d1 = xs(y1, x1), d2 = xs(y2, x2);
     const double len = __dsqrt_rn(xdot(d0, d1, d2, d0, d1, d2));
-    const bool valid = i < n;
+    const bool valid = i < lim;
     drop[r] = valid && (len < tau_z);
     keep[r] = valid && !drop[r];
     zo[r][0] = xd(d0, len);
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(kPrepThreads) preprocess_kernel(PrepBuffers b,
 #pragma unroll
     for (int r = 0; r < kPrepPer; ++r) {
       const int64_t i = base + r * kPrepThreads + tid;
-      if (i < n) {
+      if (i < lim) {
         const double q = __longlong_as_double(0x7FF8000000000000ll);
         b.zx[i] = keep[r] ? zo[r][0] : q;
         b.zy[i] = keep[r] ? zo[r][1] : q;
@@ -213,8 +215,13 @@ void launch_preprocess_range(const PrepBuffers& b, int64_t n, int64_t elem_lo, i
 
 void launch_preprocess_inorder(const PrepBuffers& b, int64_t n, int64_t elem_lo, int64_t elem_hi, double tau_z,
                                int normalize, cudaStream_t s) {
-  const int blocks = (int)((elem_hi - elem_lo + kPrepTile - 1) / kPrepTile);
+  int blocks = (int)((elem_hi - elem_lo + kPrepTile - 1) / kPrepTile);
   if (blocks <= 0) return;
+  int64_t zmax = 0;  // the clearing side job: enough blocks for ~16 words per thread
+  for (int q = 0; q < 4; ++q)
+    if (b.zero_ptr[q]) zmax = zmax > b.zero_n[q] ? zmax : b.zero_n[q];
+  const int zblocks = (int)((zmax + 16 * kPrepThreads - 1) / (16 * kPrepThreads));
+  if (zblocks > blocks) blocks = zblocks;
   const bool vec = (reinterpret_cast<uintptr_t>(b.corrs) & 15u) == 0;
   if (vec)
     preprocess_kernel<true, true><<<blocks, kPrepThreads, 0, s>>>(b, n, elem_lo, elem_hi, tau_z, normalize);

@@ -509,6 +509,7 @@ struct VoteCtx {
   int hb;
   const float4* basis_a;
   const float2* basis_b;
+  int grab;  // entries per warp grab (<= 32)
 };
 template <bool kClamp, int kS, class Fetch>
 __device__ __forceinline__ void vote_entries(const VoteCtx& v, const F32Geom& geo, const FbCtx& fc, Fetch fetch,
@@ -520,12 +521,13 @@ __device__ __forceinline__ void vote_entries(const VoteCtx& v, const F32Geom& ge
   const int M = v.M, hb = v.hb;
   const uint32_t tile_cells = v.tile_cells;
   uint32_t* tile = v.tile;
-  for (;;) {  // per-warp dynamic grabs of 32 entries (lane k holds entry k: range + f32 basis)
+  const int grab = v.grab;
+  for (;;) {  // per-warp dynamic grabs of up to 32 entries (lane k holds entry k: range + f32 basis)
     int g0 = 0;
-    if (lane == 0) g0 = atomicAdd(counter, 32);
+    if (lane == 0) g0 = atomicAdd(counter, grab);
     g0 = __shfl_sync(0xFFFFFFFFu, g0, 0);
     if (g0 >= n_ent) break;
-    const int ne = min(32, n_ent - g0);
+    const int ne = min(grab, n_ent - g0);
     uint32_t my_ci = 0, my_enc = 0;
     float4 my_a = make_float4(0.f, 0.f, 0.f, 0.f);
     float2 my_b = make_float2(0.f, 0.f);
@@ -732,7 +734,11 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     const unsigned long long* ebase = b.entries + (int64_t)band * b.entry_cap;
     const int n_ent = b.entry_count[band];
     int* counter = &b.counters[1 + band];
-    VoteCtx v{tab, tab_s, tile, tile_s, sink_rel, vote2, fbq_s, lt_mask, M, tile_cells, hb, b.basis_a, b.basis_b};
+    // grab size: 32 entries when every warp of the launch still gets several grabs, smaller for
+    // small problems (otherwise a handful of warps would walk all entries while the rest idle)
+    const int per = (int)(((long long)gridDim.x * (kVoteThreads / 32) * 4) / p.n_bands);
+    const int grab = max(1, min(32, n_ent / max(per, 1)));
+    VoteCtx v{tab, tab_s, tile, tile_s, sink_rel, vote2, fbq_s, lt_mask, M, tile_cells, hb, b.basis_a, b.basis_b, grab};
     vote_entries<kClamp, kS>(v, geo, fc, [&](int j) { return __ldcs(ebase + j); }, n_ent, counter, my_fb);
     // band exhausted for this CTA: flush the tile to a partial slot, steal the next band
     __syncthreads();

@@ -49,6 +49,9 @@ def analyse(label):
                           for ev in L.values()]) / 1e3
         zero = np.array([sum(e2[0] - e3[0] for e3, e2 in zip(ev, ev[1:]) if e3[1] == 3 and e2[1] == 2)
                          for ev in L.values()]) / 1e3  # zero + the next visit's votes (upper bound)
+        slow = max(L.values(), key=lambda ev: ev[-1][0])
+        t_s = slow[0][0]
+        print(f"  slowest cta: " + " ".join(f"tag{e[1]}@{(e[0] - t_s) / 1e3:.1f}(b{e[2]})" for e in slow))
         print(f"{label} launch {k}: ctas={len(L)} span={ends.max():.1f}us start max={starts.max():.1f} "
               f"init med={np.median(init):.1f} end min/med/max={ends.min():.1f}/{np.median(ends):.1f}/{ends.max():.1f} "
               f"visits mean={visits.mean():.2f} max={visits.max()} flush/cta med={np.median(flush):.1f}us "
