@@ -19,7 +19,7 @@ for n, B in ((1000, 256), (10000, 128), (100000, 16)):
         ctx.estimate_single(p)
     t1 = time.perf_counter()
     for w in (4, 8, 16):
-        ctx.estimate_batch(probs[:w])
+        ctx.estimate_batch(probs[:3 * w], workers=w)  # warm: allocations + graph capture per worker
         t2 = time.perf_counter()
         res = ctx.estimate_batch(probs, workers=w)
         t3 = time.perf_counter()
