@@ -236,6 +236,25 @@ def test_full_size_properties(ctx, key):
     assert orc.rotation_error_deg(rots[0], e1.rotation) < (0.05 if key == "c3" else 1.0)
 
 
+def test_beyond_c3_size_properties(ctx):
+    # N = 3e6: the cooperative refine's per-block slice no longer fits shared memory (global-load
+    # path), the pipelined host path runs 4 large chunks; size-independent properties hold
+    import torch
+    corrs, rots, _ = synth.make_config("c3", 3_000_000)
+    d = torch.from_numpy(corrs).cuda()
+    e_dev = ctx.estimate_single_device(d.data_ptr(), corrs.shape[0])
+    e_host = ctx.estimate_single(corrs)
+    assert np.array_equal(e_dev.inliers, e_host.inliers) and np.array_equal(e_dev.rotation, e_host.rotation)
+    z, kept, _ = ctx.preprocess(corrs)
+    a = e_dev.axis
+    dd = np.abs(z[:, 0] * a[0] + z[:, 1] * a[1] + z[:, 2] * a[2])
+    assert np.array_equal(kept[np.nonzero(dd < 0.015)[0]], e_dev.inliers)  # strict predicate, input order
+    grid = ctx.accumulate(z)
+    assert int(grid.sum(dtype=np.uint64)) == z.shape[0] * 2048
+    assert orc.rotation_error_deg(rots[0], e_dev.rotation) < 0.05
+    assert ctx.stage_times()["vote_guard_reruns"] == 0
+
+
 def test_pipelined_host_path_matches_device_path(ctx):
     # estimate_single with host input overlaps chunked H2D with preprocess/plan/vote; the result
     # must be identical to the device-resident solve (same grid => same peak, inliers, rotation)
