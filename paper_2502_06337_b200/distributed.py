@@ -55,3 +55,22 @@ def sharded_estimate_single(shard: torch.Tensor, n_total: int, cfg, backend, gro
     dist.all_reduce(grid, op=dist.ReduceOp.SUM, group=group)  # int32 wrap-around == uint32 sum
     corrs = all_gather_rows(shard, n_total, group)
     return backend.finish(corrs, grid, cfg)
+
+
+def batch_estimate(problems, cfg, solve_batch, group=None):
+    """Batches of independent problems across GPUs (SURVEY.md 8(e) last item, 8(f) row 2): problem k
+    goes to rank k % P -- replicas, no data-path collective -- each rank solves its share with
+    `solve_batch(list_of_problems, cfg)` (Context.estimate_batch on the rank's GPU: worker streams)
+    and one object all-gather gives every rank all results in problem order."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    mine = list(range(rank, len(problems), world))
+    results = solve_batch([problems[k] for k in mine], cfg) if mine else []
+    gathered = [None] * world
+    dist.all_gather_object(gathered, list(zip(mine, results)), group=group)
+    out = [None] * len(problems)
+    for part in gathered:
+        for k, r in part:
+            out[k] = r
+    return out
+

@@ -84,3 +84,35 @@ def test_shard_bounds_partition():
             b = [rvd.shard_bounds(n, world, r) for r in range(world)]
             assert b[0][0] == 0 and b[-1][1] == n
             assert all(b[r][1] == b[r + 1][0] for r in range(world - 1))
+
+
+def batch_worker(rank, world, port, problems, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root / "oracle"))
+    import oracle as orc
+    port_ = orc.Oracle("port")
+    solve = lambda ps, cfg: [port_.estimate_single(p) for p in ps]  # noqa: E731 (CPU stand-in)
+    res = rvd.batch_estimate(problems, None, solve)
+    out[rank] = [(r["inliers"], r["rotation"]) for r in res]
+    dist.destroy_process_group()
+
+
+def test_batch_round_robin_across_ranks():
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "oracle"))
+    import oracle as orc
+    problems = [synth.make_scene(400, 0.5, 0.01, seed=700 + k)[0] for k in range(5)]
+    ref = [orc.Oracle("port").estimate_single(p) for p in problems]
+    world = 2
+    out = mp.Manager().dict()
+    mp.spawn(batch_worker, args=(world, free_port(), problems, out), nprocs=world, join=True)
+    for rank in range(world):
+        assert len(out[rank]) == len(problems)
+        for (inl, rot), r in zip(out[rank], ref):
+            assert np.array_equal(inl, r["inliers"]) and np.array_equal(rot, r["rotation"])
+
