@@ -160,6 +160,8 @@ struct rv_context {
   struct SolveGraph {                     // device-resident single solve, captured once, replayed
     const double* corrs = nullptr;        // device input, or the pinned host input (host = true)
     bool host = false;
+    const void* aux = nullptr;            // prevoted solves / shard votes: the grid
+    int kind = 0;                         // 0 single solve, 1 prevoted finish, 2 shard vote
     int64_t n = 0;
     rv_config cfg{};
     uint64_t gen = 0;
@@ -1236,9 +1238,11 @@ rv_stage_times count_delta(const rv_stage_times& after, const rv_stage_times& be
   return d;
 }
 
-rv_context::SolveGraph* graph_slot(rv_context* c, const double* d, int64_t n, const rv_config& cfg, bool host) {
+rv_context::SolveGraph* graph_slot(rv_context* c, const double* d, int64_t n, const rv_config& cfg, bool host,
+                                   const void* aux = nullptr, int kind = 0) {
   for (auto& g : c->graphs)
-    if (g.corrs == d && g.host == host && g.n == n && same_cfg(g.cfg, cfg)) return &g;
+    if (g.corrs == d && g.host == host && g.aux == aux && g.kind == kind && g.n == n && same_cfg(g.cfg, cfg))
+      return &g;
   if (c->graphs.size() >= 8) {  // small LRU-less cache: drop the oldest entry
     if (c->graphs.front().exec) cudaGraphExecDestroy(c->graphs.front().exec);
     c->graphs.erase(c->graphs.begin());
@@ -1246,6 +1250,8 @@ rv_context::SolveGraph* graph_slot(rv_context* c, const double* d, int64_t n, co
   rv_context::SolveGraph g;
   g.corrs = d;
   g.host = host;
+  g.aux = aux;
+  g.kind = kind;
   g.n = n;
   g.cfg = cfg;
   g.gen = ~0ull;
@@ -2376,6 +2382,40 @@ rv_status rv_vote_shard(rv_context* c, const double* d_corrs, int64_t n, const r
       sync(c);
       return;
     }
+    if (banded_plan(c, *cfg)) {  // in-order preprocess + band-tiled vote, graph-replayed
+      unsigned long long* hk = reinterpret_cast<unsigned long long*>(c->pinned);
+      auto enqueue = [&] {
+        PrepBuffers b = inorder_buffers(c, d_corrs, n);
+        set_vote_zeroing(c, cfg->grid, &b);
+        launch_preprocess_inorder(b, n, 0, n, cfg->tau_z, cfg->normalize_inputs, c->st);
+        count_launch(c);
+        const uint32_t* g = vote(c, b.zx, b.zy, b.zz, n, cfg->grid, cfg->extent, cfg->theta_samples, false, true);
+        ck(cudaMemcpyAsync(d_grid, g, sizeof(uint32_t) * cells, cudaMemcpyDeviceToDevice, c->st), "D2D grid");
+        ck(cudaMemcpyAsync(hk, b.kept_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st), "kept");
+      };
+      rv_context::SolveGraph* gr =
+          graphs_enabled() && !c->timing ? graph_slot(c, d_corrs, n, *cfg, false, d_grid, 2) : nullptr;
+      if (gr && !gr->exec && gr->seen > 0 && gr->gen == g_buf_gen.load()) capture_single(c, gr, enqueue);
+      if (gr && gr->exec && gr->gen == g_buf_gen.load()) {
+        ck(cudaGraphLaunch(gr->exec, c->st), "shard graph launch");
+        add_counts(c->times, gr->delta);
+      } else {
+        const rv_stage_times t0 = c->times;
+        enqueue();
+        if (gr) {
+          if (gr->exec) {
+            cudaGraphExecDestroy(gr->exec);
+            gr->exec = nullptr;
+          }
+          gr->delta = count_delta(c->times, t0);
+          gr->gen = g_buf_gen.load();
+          gr->seen += 1;
+        }
+      }
+      sync(c);
+      *n_kept = (int64_t)*hk;  // (an all-degenerate shard votes nothing: the grid stays zero)
+      return;
+    }
     const PreResult pre = preprocess_dev(c, d_corrs, n, cfg->tau_z, cfg->normalize_inputs);
     *n_kept = pre.cs.n;
     if (pre.cs.n == 0) {  // an all-degenerate shard votes nothing
@@ -2389,6 +2429,54 @@ rv_status rv_vote_shard(rv_context* c, const double* d_corrs, int64_t n, const r
   });
 }
 
+// The finish of a sharded solve (distributed.py): in-order preprocess of all correspondences,
+// the supplied (all-reduced) grid copied in, then the chained single-solve finish -- captured and
+// replayed like the other single solves when (input, grid, n, config) repeat.
+Estimate estimate_prevoted_dev(rv_context* c, const double* d_corrs, int64_t n, const rv_config& cfg,
+                               const uint32_t* d_grid) {
+  const size_t cells = (size_t)cfg.grid * cfg.grid;
+  auto enqueue = [&]() -> PreResult {
+    PrepBuffers b = inorder_buffers(c, d_corrs, n);  // (no clearing side job: the grid is given)
+    launch_preprocess_inorder(b, n, 0, n, cfg.tau_z, cfg.normalize_inputs, c->st);
+    count_launch(c);
+    uint32_t* g = c->grid.get<uint32_t>(cells);
+    ck(cudaMemcpyAsync(g, d_grid, sizeof(uint32_t) * cells, cudaMemcpyDeviceToDevice, c->st), "D2D grid");
+    PreResult pre = inorder_result(b, n);
+    enqueue_single(c, pre, d_corrs, cfg, g, false);
+    return pre;
+  };
+  rv_context::SolveGraph* g =
+      graphs_enabled() && !c->timing ? graph_slot(c, d_corrs, n, cfg, false, d_grid, 1) : nullptr;
+  if (g && !g->exec && g->seen > 0 && g->gen == g_buf_gen.load()) capture_single(c, g, [&] { enqueue(); });
+  PreResult pre;
+  if (g && g->exec && g->gen == g_buf_gen.load()) {
+    ck(cudaGraphLaunch(g->exec, c->st), "solve graph launch");
+    add_counts(c->times, g->delta);
+    pre.cs.zx = c->zx.get<double>(n);
+    pre.cs.zy = c->zy.get<double>(n);
+    pre.cs.zz = c->zz.get<double>(n);
+    pre.cs.n = n;
+    pre.vote_zeroed = true;
+    pre.inorder = true;
+  } else {
+    const rv_stage_times t0 = c->times;
+    pre = enqueue();
+    if (g) {
+      if (g->exec) {
+        cudaGraphExecDestroy(g->exec);
+        g->exec = nullptr;
+      }
+      g->delta = count_delta(c->times, t0);
+      g->gen = g_buf_gen.load();
+      g->seen += 1;
+    }
+  }
+  sync(c);
+  bool identity = false;
+  Estimate est = complete_single(c, pre, d_corrs, cfg, c->grid.get<uint32_t>(cells), true, &identity);
+  return identity ? identity_from_inorder(c, d_corrs, n, cfg) : est;
+}
+
 rv_status rv_estimate_single_prevoted(rv_context* c, const double* d_corrs, int64_t n, const rv_config* cfg,
                                       const uint32_t* d_grid, rv_estimate* out) {
   if (!c || !cfg || !out || !d_grid || (n > 0 && !d_corrs)) return RV_ERR_INVALID_ARGUMENT;
@@ -2396,6 +2484,12 @@ rv_status rv_estimate_single_prevoted(rv_context* c, const double* d_corrs, int6
     cudaSetDevice(c->device);
     clear_results(c);
     if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
+    if (cfg->angle_bins >= 8 && banded_plan(c, *cfg)) {  // in-order chain, graph-replayed
+      Estimate e = estimate_prevoted_dev(c, d_corrs, n, *cfg, d_grid);
+      to_c(e, out, seconds_since(c));
+      c->results.push_back(std::move(e.inliers));
+      return;
+    }
     const PreResult pre = preprocess_dev(c, d_corrs, n, cfg->tau_z, cfg->normalize_inputs);
     Estimate e;
     if (pre.cs.n == 0) {
