@@ -2579,7 +2579,8 @@ const double* parse_csv_dev(rv_context* c, const char* text, int64_t nbytes, con
   if (nbytes <= 0) fail(RV_ERR_EMPTY_FILE, "no data in " + name);
   const bool add_nl = text[nbytes - 1] != '\n';
   const int64_t total = nbytes + (add_nl ? 1 : 0);
-  if (total >= ((int64_t)1 << 32)) fail(RV_ERR_INVALID_ARGUMENT, "CSV text larger than 4 GB");
+  // int32 delimiter / line / row counts and u32 byte positions: texts below 2 GB
+  if (total >= ((int64_t)1 << 31)) fail(RV_ERR_INVALID_ARGUMENT, "CSV text of 2 GB or more");
   CsvBuffers b;
   uint8_t* dtext = c->csv_text.get<uint8_t>((size_t)total + 16);
   b.text = dtext;

@@ -16,7 +16,7 @@
 //
 // Errors: every bad line reports its 1-based physical line number with atomicMin; the host
 // re-runs the reference's line logic on the first one for the exact message. Layout: the text
-// must end with '\n' (the host appends one); delimiter positions are u32 (text < 4 GB).
+// must end with '\n' (the host appends one); counts are int32 and positions u32 (text < 2 GB).
 #include <cuda_runtime.h>
 
 #include <cstdint>
