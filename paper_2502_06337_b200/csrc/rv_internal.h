@@ -9,7 +9,10 @@
 namespace rvb {
 
 constexpr int kMaxBands = 64;        // row bands of the smem-tiled vote kernel
-constexpr int kVoteThreads = 1024;   // threads per vote CTA (32 warps, <= 64 regs each: latency-bound loop)
+#ifndef RV_VOTE_THREADS
+#define RV_VOTE_THREADS 1024
+#endif
+constexpr int kVoteThreads = RV_VOTE_THREADS;  // threads per vote CTA (32 warps, <= 64 regs each: latency-bound loop)
 constexpr int kPad = 2;              // pair-index padding of each band range (culling slack)
 constexpr int kFbqCap = 64;          // per-warp exact-fallback queue entries
 constexpr int kReduceThreads = 256;
