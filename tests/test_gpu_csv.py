@@ -146,3 +146,15 @@ def test_device_rows_feed_the_solver(ctx, tmp_path):
     e_dev = ctx.estimate_single_device(dptr, n)
     e_host = ctx.estimate_single(corrs)
     assert np.array_equal(e_dev.inliers, e_host.inliers) and np.array_equal(e_dev.rotation, e_host.rotation)
+
+
+def test_parse_from_memory_matches_file(ctx, ref, tmp_path):
+    corrs, _, _ = synth.make_config("c1")
+    text = ("x0,x1,x2,y0,y1,y2\r\n" + "\r\n".join(",".join(repr(float(v)) for v in r) for r in corrs)).encode()
+    rows_mem = ctx.parse_correspondences(text)
+    rows_file, err = ref.read_correspondences(write(tmp_path, "m.csv", text))
+    assert err is None and np.array_equal(rows_mem.view(np.uint64), rows_file.view(np.uint64))
+    assert np.array_equal(rows_mem.view(np.uint64), corrs.view(np.uint64))
+    with pytest.raises(rv.ParseError) as e:
+        ctx.parse_correspondences(b"1,2,3,4,5,6\n1,2,3\n")
+    assert e.value.line == 2 and "expected 6 fields, got 3" in str(e.value)
