@@ -2573,8 +2573,9 @@ std::string_view nth_line(const char* text, int64_t nbytes, int64_t line_number)
   return std::string_view(p, (size_t)((nl ? static_cast<const char*>(nl) : end) - p));
 }
 
+// uploaded: the text is already in c->csv_text (the file path streams it there while reading).
 const double* parse_csv_dev(rv_context* c, const char* text, int64_t nbytes, const std::string& name, int64_t* n_rows,
-                            int64_t* err_line) {
+                            int64_t* err_line, bool uploaded = false) {
   *n_rows = 0;
   *err_line = 0;
   if (nbytes <= 0) fail(RV_ERR_EMPTY_FILE, "no data in " + name);
@@ -2586,7 +2587,7 @@ const double* parse_csv_dev(rv_context* c, const char* text, int64_t nbytes, con
   uint8_t* dtext = c->csv_text.get<uint8_t>((size_t)total + 16);
   b.text = dtext;
   b.nbytes = total;
-  ck(cudaMemcpyAsync(dtext, text, (size_t)nbytes, cudaMemcpyHostToDevice, c->st), "CSV H2D");
+  if (!uploaded) ck(cudaMemcpyAsync(dtext, text, (size_t)nbytes, cudaMemcpyHostToDevice, c->st), "CSV H2D");
   static const char kNl = '\n';
   if (add_nl) ck(cudaMemcpyAsync(dtext + nbytes, &kNl, 1, cudaMemcpyHostToDevice, c->st), "CSV newline");
   {  // header decision on the host (io.cpp:76-84): line 1, non-blank, first field not a number
@@ -2758,7 +2759,10 @@ rv_status rv_read_correspondences_csv(rv_context* c, const char* path, const dou
     if (nthr <= 1) {
       ok = (sz > 0 ? std::fread(c->csv_pinned, 1, (size_t)sz, f) : 0) == (size_t)sz;
     } else {
+      // each part is copied to the device as soon as its read finishes (in part order): the H2D
+      // of the early parts overlaps the reads of the later ones
       const int fd = fileno(f);
+      uint8_t* dtext = c->csv_text.get<uint8_t>((size_t)sz + 1 + 16);
       std::vector<std::thread> th;
       std::vector<char> part_ok((size_t)nthr, 1);
       for (int t = 0; t < nthr; ++t)
@@ -2773,12 +2777,20 @@ rv_status rv_read_correspondences_csv(rv_context* c, const char* path, const dou
             off += r;
           }
         });
-      for (auto& x : th) x.join();
-      for (char b : part_ok) ok = ok && b;
+      for (int t = 0; t < nthr; ++t) {
+        th[(size_t)t].join();
+        ok = ok && part_ok[(size_t)t];
+        const int64_t lo = (int64_t)sz * t / nthr, hi = (int64_t)sz * (t + 1) / nthr;
+        if (ok) ck(cudaMemcpyAsync(dtext + lo, c->csv_pinned + lo, (size_t)(hi - lo), cudaMemcpyHostToDevice, c->st),
+                   "CSV H2D part");
+      }
     }
     std::fclose(f);
-    if (!ok) fail(RV_ERR_IO, std::string("cannot read: ") + path);
-    *d_rows = parse_csv_dev(c, c->csv_pinned, (int64_t)sz, path, n_rows, error_line);
+    if (!ok) {
+      sync(c);
+      fail(RV_ERR_IO, std::string("cannot read: ") + path);
+    }
+    *d_rows = parse_csv_dev(c, c->csv_pinned, (int64_t)sz, path, n_rows, error_line, nthr > 1);
   });
 }
 
