@@ -1685,6 +1685,7 @@ std::vector<Estimate> estimate_multi_onepass_dev(rv_context* c, const double* d_
     return {};
   }
   std::vector<Estimate> out;
+  std::vector<std::vector<uint64_t>> out_bits;  // inlier bitsets of the accepted models (dedupe)
   for (const Peak& pk : peaks) {
     double A, B, b[3], axis[3];
     interpolate_peak_dev(c, grid, cfg.grid, cfg.extent, pk, &A, &B);
@@ -1703,16 +1704,20 @@ std::vector<Estimate> estimate_multi_onepass_dev(rv_context* c, const double* d_
         sup.coherent < std::max<int64_t>(8, (int64_t)est.inliers.size() / 5))
       continue;
     bool duplicate = false;
-    for (const auto& e : out) {
-      std::vector<int32_t> common;
-      std::set_intersection(e.inliers.begin(), e.inliers.end(), est.inliers.begin(), est.inliers.end(),
-                            std::back_inserter(common));
-      if ((double)common.size() > cfg.dedupe_overlap * (double)est.inliers.size()) {
+    for (const auto& bits : out_bits) {  // |intersection| via the accepted model's bitset
+      int64_t common = 0;
+      for (const int32_t i : est.inliers) common += (bits[(size_t)i >> 6] >> (i & 63)) & 1u;
+      if ((double)common > cfg.dedupe_overlap * (double)est.inliers.size()) {
         duplicate = true;
         break;
       }
     }
-    if (!duplicate) out.push_back(std::move(est));
+    if (!duplicate) {
+      std::vector<uint64_t> bits((size_t)(n + 63) / 64, 0);
+      for (const int32_t i : est.inliers) bits[(size_t)i >> 6] |= 1ull << (i & 63);
+      out_bits.push_back(std::move(bits));
+      out.push_back(std::move(est));
+    }
   }
   return out;
 }
