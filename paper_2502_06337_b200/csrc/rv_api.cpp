@@ -1732,6 +1732,7 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
   uint8_t* removed = c->removed.get<uint8_t>(pre.cs.n);
   ck(cudaMemsetAsync(removed, 0, pre.cs.n, c->st), "memset removed");
   std::vector<Estimate> out;
+  std::vector<std::vector<uint64_t>> out_bits;  // inlier bitsets of the accepted models (dedupe)
   while ((int)out.size() < cfg.max_models) {
     // residual (estimator.cpp:392-398)
     ConstraintSet sub;
@@ -1802,16 +1803,20 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
       identity_model = true;
     }
     bool duplicate = false;
-    for (const auto& e : out) {
-      std::vector<int32_t> common;
-      std::set_intersection(e.inliers.begin(), e.inliers.end(), est.inliers.begin(), est.inliers.end(),
-                            std::back_inserter(common));
-      if ((double)common.size() > cfg.dedupe_overlap * (double)est.inliers.size()) {
+    for (const auto& bits : out_bits) {  // |intersection| via the accepted models' inlier bitsets
+      int64_t common = 0;
+      for (const int32_t i : est.inliers) common += (bits[(size_t)i >> 6] >> (i & 63)) & 1u;
+      if ((double)common > cfg.dedupe_overlap * (double)est.inliers.size()) {
         duplicate = true;
         break;
       }
     }
     if (duplicate) break;
+    {
+      std::vector<uint64_t> bits((size_t)(n + 63) / 64, 0);
+      for (const int32_t i : est.inliers) bits[(size_t)i >> 6] |= 1ull << (i & 63);
+      out_bits.push_back(std::move(bits));
+    }
     if (identity_model) {
       launch_strip_identity_k(d_corrs, pre.cs.kept, pre.cs.n, cfg.normalize_inputs, removed, c->st);
       count_launch(c);
