@@ -140,6 +140,7 @@ struct rv_context {
   DBuf peak_out;                         // chained solve: device Summary (peak, state, angles)
   DBuf red_keys;                         // fused argmax scratch of the tile reduction
   DBuf kept_acc;                          // in-order preprocess: kept-count accumulator + ticket
+  DBuf sort_tmp;                          // CUB radix-sort scratch (multi-model strip percentile)
   // CSV ingest (rv_io.cu)
   DBuf csv_text, csv_chunk, csv_misc, csv_dpos, csv_dline, csv_nl, csv_status, csv_row, csv_block, csv_out, csv_fb,
       csv_fix_idx, csv_fix_val;
@@ -1823,35 +1824,31 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
     } else {
       double strip = 2.0 * cfg.epsilon;
       if (sup.band > 0) {
-        // 95th-percentile band value (nth_element) over the band members
+        // 95th-percentile band value over the band members (nth_element's q-th smallest): flag
+        // offsets, compaction, |a.z| gather and a radix sort on the device; two scalar reads
         const int nb = classify_blocks(pre.cs.n);
-        int32_t* offs = c->boffB.get<int32_t>(nb);
-        std::vector<uint32_t> hf((size_t)(pre.cs.n + 31) / 32);
-        ck(cudaMemcpyAsync(hf.data(), best_band, sizeof(uint32_t) * hf.size(), cudaMemcpyDeviceToHost, c->st),
-           "band flags D2H");
+        int32_t* offs = c->boffB.get<int32_t>((size_t)nb + 1);
+        int32_t* dtot = c->misc32.get<int32_t>(8) + 6;
+        launch_flag_offsets(best_band, pre.cs.n, offs, dtot, c->st);
+        int32_t* h = reinterpret_cast<int32_t*>(c->pinned);
+        ck(cudaMemcpyAsync(h, dtot, sizeof(int32_t), cudaMemcpyDeviceToHost, c->st), "band count D2H");
         sync(c);
-        std::vector<int32_t> hoffs(nb);
-        int64_t acc = 0;
-        for (int bk = 0; bk < nb; ++bk) {
-          hoffs[bk] = (int32_t)acc;
-          for (int w = 0; w < 32; ++w) {
-            const size_t wi = (size_t)bk * 32 + w;
-            if (wi < hf.size()) acc += __builtin_popcount(hf[wi]);
-          }
-        }
-        ck(cudaMemcpyAsync(offs, hoffs.data(), sizeof(int32_t) * nb, cudaMemcpyHostToDevice, c->st), "offs H2D");
-        int32_t* bidx = c->band_idx.get<int32_t>((size_t)std::max<int64_t>(acc, 1));
-        launch_compact_flags(best_band, pre.cs.n, nullptr, offs, bidx, c->st);
-        double* bv = c->band_vals.get<double>((size_t)std::max<int64_t>(acc, 1));
-        launch_gather_dot_k(pre.cs.zx, pre.cs.zy, pre.cs.zz, bidx, acc, est.axis, bv, c->st);
-        count_launch(c, 2);
-        std::vector<double> band(acc);
-        ck(cudaMemcpyAsync(band.data(), bv, sizeof(double) * acc, cudaMemcpyDeviceToHost, c->st), "band D2H");
-        sync(c);
-        if (!band.empty()) {
-          const size_t q = std::min(band.size() - 1, (band.size() * 95) / 100);
-          std::nth_element(band.begin(), band.begin() + (std::ptrdiff_t)q, band.end());
-          strip = std::max(strip, 1.25 * band[q]);
+        const int64_t acc = h[0];
+        if (acc > 0) {
+          int32_t* bidx = c->band_idx.get<int32_t>((size_t)acc);
+          launch_compact_flags(best_band, pre.cs.n, nullptr, offs, bidx, c->st);
+          double* bv = c->band_vals.get<double>((size_t)acc * 2);
+          launch_gather_dot_k(pre.cs.zx, pre.cs.zy, pre.cs.zz, bidx, acc, est.axis, bv, c->st);
+          size_t tb = 0;
+          ck(sort_doubles(nullptr, &tb, bv, bv + acc, (int)acc, c->st), "sort size");
+          void* tmp = c->sort_tmp.get<uint8_t>(tb);
+          ck(sort_doubles(tmp, &tb, bv, bv + acc, (int)acc, c->st), "band sort");
+          count_launch(c, 5);
+          const size_t q = std::min<size_t>((size_t)acc - 1, ((size_t)acc * 95) / 100);
+          double* hv = reinterpret_cast<double*>(c->pinned);
+          ck(cudaMemcpyAsync(hv, bv + acc + q, sizeof(double), cudaMemcpyDeviceToHost, c->st), "band q D2H");
+          sync(c);
+          strip = std::max(strip, 1.25 * hv[0]);
         }
       }
       launch_strip_k(pre.cs.zx, pre.cs.zy, pre.cs.zz, pre.cs.n, est.axis, strip, removed, c->st);

@@ -259,4 +259,6 @@ int csv_chunks(int64_t nbytes);
 cudaError_t launch_csv_parse(const CsvBuffers& b, cudaStream_t s, int stage);
 void launch_csv_scatter(const int64_t* idx, const double* vals, int n, double* out, cudaStream_t s);
 
+void launch_flag_offsets(const uint32_t* flags, int64_t n, int32_t* offsets, int32_t* total, cudaStream_t s);
+cudaError_t sort_doubles(void* temp, size_t* temp_bytes, const double* in, double* out, int n, cudaStream_t s);
 }  // namespace rvb

@@ -10,6 +10,8 @@
 
 #include <cstdint>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "rv_exact.cuh"
 #include "rv_internal.h"
 
@@ -788,4 +790,56 @@ void launch_strip_identity_k(const double* corrs, const int32_t* kept, int64_t n
   if (n <= 0) return;
   strip_identity_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(corrs, kept, n, normalize, removed);
 }
+
+// ---- band percentile of estimate_multi's strip width (estimator.cpp:452-466) on the device ----
+namespace {
+__global__ void flag_block_counts_kernel(const uint32_t* flags, int64_t nwords, int nb, int32_t* counts) {
+  const int bk = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bk >= nb) return;
+  int acc = 0;
+  for (int w = 0; w < 32; ++w) {
+    const int64_t wi = (int64_t)bk * 32 + w;
+    if (wi < nwords) acc += __popc(flags[wi]);
+  }
+  counts[bk] = acc;
+}
+
+// exclusive scan of n ints in place by one block; the total to *total
+__global__ void __launch_bounds__(1024) scan_i32_kernel(int32_t* v, int n, int32_t* total) {
+  __shared__ int32_t s[1024];
+  const int per = (n + 1023) / 1024;
+  const int lo = threadIdx.x * per, hi = min(lo + per, n);
+  int acc = 0;
+  for (int i = lo; i < hi; ++i) acc += v[i];
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int x = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
+    __syncthreads();
+    s[threadIdx.x] += x;
+    __syncthreads();
+  }
+  int run = threadIdx.x ? s[threadIdx.x - 1] : 0;
+  for (int i = lo; i < hi; ++i) {
+    const int x = v[i];
+    v[i] = run;
+    run += x;
+  }
+  if (threadIdx.x == 1023) *total = s[1023];
+}
+}  // namespace
+
+// Per-1024-bit-block offsets of a flag mask (exclusive popcount scan) and the total set bits.
+void launch_flag_offsets(const uint32_t* flags, int64_t n, int32_t* offsets, int32_t* total, cudaStream_t s) {
+  const int64_t nwords = (n + 31) / 32;
+  const int nb = (int)((nwords + 31) / 32);
+  flag_block_counts_kernel<<<(nb + 255) / 256, 256, 0, s>>>(flags, nwords, nb, offsets);
+  scan_i32_kernel<<<1, 1024, 0, s>>>(offsets, nb, total);
+}
+
+// Ascending sort of n doubles (CUB radix sort); temp == nullptr queries *temp_bytes.
+cudaError_t sort_doubles(void* temp, size_t* temp_bytes, const double* in, double* out, int n, cudaStream_t s) {
+  return cub::DeviceRadixSort::SortKeys(temp, *temp_bytes, in, out, n, 0, 64, s);
+}
 }  // namespace rvb
+
