@@ -97,7 +97,8 @@ struct Estimate {
   // kernels streamed it there) and rv_result_inliers copies it once, straight from there
   const int32_t* view = nullptr;
   int64_t view_n = 0;
-  int64_t n_inliers() const { return view ? view_n : (int64_t)inliers.size(); }
+  int64_t dev_count = -1;  // >= 0: inliers not read back (still in the context's compaction buffer)
+  int64_t n_inliers() const { return view ? view_n : dev_count >= 0 ? dev_count : (int64_t)inliers.size(); }
 };
 
 // Constraint set on the device (SoA) with its kept map (constraint -> input index).
@@ -141,6 +142,7 @@ struct rv_context {
   DBuf red_keys;                         // fused argmax scratch of the tile reduction
   DBuf kept_acc;                          // in-order preprocess: kept-count accumulator + ticket
   DBuf sort_tmp;                          // CUB radix-sort scratch (multi-model strip percentile)
+  DBuf best_idx;                          // multi-model: inlier list of the best candidate so far
   // CSV ingest (rv_io.cu)
   DBuf csv_text, csv_chunk, csv_misc, csv_dpos, csv_dline, csv_nl, csv_status, csv_row, csv_block, csv_out, csv_fb,
       csv_fix_idx, csv_fix_val;
@@ -813,6 +815,8 @@ Estimate build_estimate_dev(rv_context* c, const ConstraintSet& cs, const double
          "inliers D2H");
       sync(c);
     }
+  } else {
+    est.dev_count = cl.count;
   }
   return est;
 }
@@ -875,14 +879,14 @@ std::vector<std::array<double, 3>> rescue_axes_dev(rv_context* c, const uint32_t
 
 // build_candidate (estimator.cpp:183-194). Throws NoVotes.
 Estimate build_candidate_dev(rv_context* c, const double start[3], const uint32_t* grid, const ConstraintSet& cs,
-                             const double* corrs, const rv_config& cfg) {
+                             const double* corrs, const rv_config& cfg, bool want_inliers = true) {
   double axis[3] = {start[0], start[1], start[2]};
   const Cls cl = refine_loop_dev(c, cs, axis, cfg);
   uint32_t votes = 0;
   double A, B;
   if (project3(axis, &A, &B))
     votes = grid_cell(c, grid, cfg.grid, coord_to_cell(A, cfg.grid, cfg.extent), coord_to_cell(B, cfg.grid, cfg.extent));
-  return build_estimate_dev(c, cs, axis, cl, votes, corrs, cfg);
+  return build_estimate_dev(c, cs, axis, cl, votes, corrs, cfg, want_inliers);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1776,10 +1780,12 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
       canonicalize3(b, s0);
       starts.push_back({s0[0], s0[1], s0[2]});
       for (const auto& a : rescue_axes_dev(c, grid, sub, cfg)) starts.push_back(a);
+      // candidates keep their inlier lists on the device; only the winner's is read back
+      int32_t* best_idx = c->best_idx.get<int32_t>((size_t)std::max<int64_t>(pre.cs.n, 1));
       for (size_t s = 0; s < starts.size(); ++s) {
         Estimate cand;
         try {
-          cand = build_candidate_dev(c, starts[s].data(), grid, pre.cs, d_corrs, cfg);
+          cand = build_candidate_dev(c, starts[s].data(), grid, pre.cs, d_corrs, cfg, false);
         } catch (const RvError& e) {
           if (e.st == RV_ERR_NO_VOTES) continue;
           throw;
@@ -1787,11 +1793,22 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
         if (s == 0) cand.votes = peaks[0].votes;
         const Support cs = model_support_dev(c, pre.cs, d_corrs, cand, cfg, cand_band);
         if (!have || cs.coherent > sup.coherent) {
+          if (cand.dev_count > 0)
+            ck(cudaMemcpyAsync(best_idx, c->compact_out.get<int32_t>((size_t)cand.dev_count), sizeof(int32_t) *
+                               (size_t)cand.dev_count, cudaMemcpyDeviceToDevice, c->st), "best inliers D2D");
           est = std::move(cand);
           sup = cs;
           std::swap(best_band, cand_band);
           have = true;
         }
+      }
+      if (have && est.dev_count >= 0) {
+        est.inliers.resize((size_t)est.dev_count);
+        if (est.dev_count > 0)
+          ck(cudaMemcpyAsync(est.inliers.data(), best_idx, sizeof(int32_t) * (size_t)est.dev_count,
+                             cudaMemcpyDeviceToHost, c->st), "inliers D2H");
+        sync(c);
+        est.dev_count = -1;
       }
     }
     bool identity_model = false;
