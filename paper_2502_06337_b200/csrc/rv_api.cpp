@@ -1727,6 +1727,50 @@ std::vector<Estimate> estimate_multi_onepass_dev(rv_context* c, const double* d_
   return out;
 }
 
+// build_candidate (refine_loop + build_estimate from a start axis) chained on the device for the
+// multi-model rounds: one cooperative refine launch with the compaction fused, the angle vote and
+// peak on the refined axis/count, ONE summary read-back. The inlier list stays in compact_out
+// (dev_count); votes are left 0 (only the winning candidate's are looked up).
+Estimate build_candidate_chained(rv_context* c, const double start[3], const ConstraintSet& cs,
+                                 const double* corrs, const rv_config& cfg) {
+  if (cfg.angle_bins < 8) fail(RV_ERR_INVALID_CONFIG, "angle histogram needs bin_count >= 8");
+  Summary* dsum = summary_buf(c);
+  int32_t* idx = c->compact_out.get<int32_t>((size_t)std::max<int64_t>(cs.n, 1));
+  uint32_t* bins = c->bins.get<uint32_t>(cfg.angle_bins);
+  CoopFused fz;
+  fz.compact_out = idx;
+  fz.zero_bins = bins;
+  fz.n_bins = cfg.angle_bins;
+  fz.zero_counts = dsum->counts;
+  CoopState* st = coop_refine_launch(c, cs, start, nullptr, 0, 0.0, cfg, nullptr, nullptr, &dsum->st, &fz);
+  {
+    StageScope sc(c, kAngles);
+    double* raw = c->raw.get<double>((size_t)std::max<int64_t>(cs.n, 1));
+    launch_vote_angles_k(nullptr, corrs, idx, cs.n, cfg.angle_bins, cfg.tau_deg, bins, raw, dsum->counts, c->st,
+                         st->axis, &st->count, nullptr);
+    launch_peak_angle_k(bins, cfg.angle_bins, raw, cs.n, c->angle_sums.get<double>(2 * 296), dsum->angle,
+                        c->done_ptr(), c->st, &st->count);
+    count_launch(c, 2);
+  }
+  Summary* h = reinterpret_cast<Summary*>(c->pinned);
+  ck(cudaMemcpyAsync(h, dsum, sizeof(Summary), cudaMemcpyDeviceToHost, c->st), "candidate D2H");
+  sync(c);
+  const Summary sm = *h;
+  if (sm.counts[0] == 0) fail(RV_ERR_NO_VOTES, "no correspondence produced an angle vote");  // angle_dev
+  Estimate est;
+  std::memcpy(est.axis, sm.st.axis, sizeof est.axis);
+  const double s = sm.angle[0], co = sm.angle[1], center = sm.angle[3];
+  double angle = center;
+  if (cfg.refine && !(s == 0.0 && co == 0.0)) {
+    angle = std::atan2(s, co);
+    if (angle <= -kPiD) angle += 2.0 * kPiD;
+  }
+  est.angle = angle;
+  rodrigues3(est.axis, est.angle, est.R);
+  est.dev_count = (int64_t)sm.st.count;
+  return est;
+}
+
 // estimate_multi (estimator.cpp:373-493)
 std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, int64_t n, const rv_config& cfg) {
   if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
@@ -1785,12 +1829,12 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
       for (size_t s = 0; s < starts.size(); ++s) {
         Estimate cand;
         try {
-          cand = build_candidate_dev(c, starts[s].data(), grid, pre.cs, d_corrs, cfg, false);
+          cand = build_candidate_chained(c, starts[s].data(), pre.cs, d_corrs, cfg);
         } catch (const RvError& e) {
           if (e.st == RV_ERR_NO_VOTES) continue;
           throw;
         }
-        if (s == 0) cand.votes = peaks[0].votes;
+        cand.votes = s == 0 ? peaks[0].votes : 0u;  // (s > 0: looked up below if it wins)
         const Support cs = model_support_dev(c, pre.cs, d_corrs, cand, cfg, cand_band);
         if (!have || cs.coherent > sup.coherent) {
           if (cand.dev_count > 0)
@@ -1801,6 +1845,12 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
           std::swap(best_band, cand_band);
           have = true;
         }
+      }
+      if (have && est.votes == 0) {  // build_candidate's vote lookup at the refined axis, winner only
+        double A, B;
+        if (project3(est.axis, &A, &B))
+          est.votes = grid_cell(c, grid, cfg.grid, coord_to_cell(A, cfg.grid, cfg.extent),
+                                coord_to_cell(B, cfg.grid, cfg.extent));
       }
       if (have && est.dev_count >= 0) {
         est.inliers.resize((size_t)est.dev_count);
