@@ -1613,13 +1613,20 @@ Estimate finish_single_stepped(rv_context* c, const PreResult& pre, const double
 }
 
 // Rescue (estimator.cpp:352-368): blurred peaks + LS-all annealed candidates, best model support.
+Estimate build_candidate_chained(rv_context* c, const double start[3], const ConstraintSet& cs,
+                                 const double* corrs, const rv_config& cfg);
+
 Estimate rescue_single(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
                        const uint32_t* grid, Estimate est) {
   int64_t best = model_support_dev(c, pre.cs, d_corrs, est, cfg, nullptr).coherent;
+  // candidates run as chained device sequences with their inlier lists left on the device; the
+  // winner's list and vote count are read once at the end
+  int32_t* best_idx = c->best_idx.get<int32_t>((size_t)std::max<int64_t>(pre.cs.n, 1));
+  bool cand_won = false;
   for (const auto& ax : rescue_axes_dev(c, grid, pre.cs, cfg)) {
     Estimate cand;
     try {
-      cand = build_candidate_dev(c, ax.data(), grid, pre.cs, d_corrs, cfg);
+      cand = build_candidate_chained(c, ax.data(), pre.cs, d_corrs, cfg);
     } catch (const RvError& e) {
       if (e.st == RV_ERR_NO_VOTES) continue;
       throw;
@@ -1627,8 +1634,26 @@ Estimate rescue_single(rv_context* c, const PreResult& pre, const double* d_corr
     const int64_t coh = model_support_dev(c, pre.cs, d_corrs, cand, cfg, nullptr).coherent;
     if (coh > best) {
       best = coh;
+      if (cand.dev_count > 0)
+        ck(cudaMemcpyAsync(best_idx, c->compact_out.get<int32_t>((size_t)cand.dev_count),
+                           sizeof(int32_t) * (size_t)cand.dev_count, cudaMemcpyDeviceToDevice, c->st),
+           "best inliers D2D");
       est = std::move(cand);
+      cand_won = true;
     }
+  }
+  if (cand_won) {
+    double A, B;  // build_candidate's vote lookup at the refined axis
+    est.votes = project3(est.axis, &A, &B) ? grid_cell(c, grid, cfg.grid, coord_to_cell(A, cfg.grid, cfg.extent),
+                                                        coord_to_cell(B, cfg.grid, cfg.extent))
+                                            : 0u;
+    est.inliers.resize((size_t)est.dev_count);
+    if (est.dev_count > 0)
+      ck(cudaMemcpyAsync(est.inliers.data(), best_idx, sizeof(int32_t) * (size_t)est.dev_count,
+                         cudaMemcpyDeviceToHost, c->st),
+         "inliers D2H");
+    sync(c);
+    est.dev_count = -1;
   }
   return est;
 }
