@@ -143,6 +143,7 @@ struct rv_context {
   DBuf kept_acc;                          // in-order preprocess: kept-count accumulator + ticket
   DBuf sort_tmp;                          // CUB radix-sort scratch (multi-model strip percentile)
   DBuf best_idx;                          // multi-model: inlier list of the best candidate so far
+  DBuf cand_sums, cand_idx, cand_sup, cand_band;  // batched rescue candidates (per-candidate slots)
   // CSV ingest (rv_io.cu)
   DBuf csv_text, csv_chunk, csv_misc, csv_dpos, csv_dline, csv_nl, csv_status, csv_row, csv_block, csv_out, csv_fb,
       csv_fix_idx, csv_fix_val;
@@ -1616,44 +1617,115 @@ Estimate finish_single_stepped(rv_context* c, const PreResult& pre, const double
 Estimate build_candidate_chained(rv_context* c, const double start[3], const ConstraintSet& cs,
                                  const double* corrs, const rv_config& cfg);
 
+// K rescue candidates (build_candidate + model_support each, estimator.cpp:352-368 / 452-466)
+// evaluated as ONE device sequence: every candidate's refine (cooperative, compaction fused),
+// angle vote and peak are queued back to back with per-candidate summary and inlier slots, read
+// back once; the host finishes each angle (libm atan2, as angle_dev) and queues the K model-support
+// passes, read back once. Result per candidate: estimate (inliers left in its slot: dev_count),
+// coherent/band support, and whether it produced angle votes at all (NoVotes -> skipped).
+struct CandResult {
+  Estimate est;
+  int64_t coherent = 0, band = 0;
+  bool ok = false;
+  const int32_t* d_idx = nullptr;   // its inlier list on the device
+  const uint32_t* d_band = nullptr; // its support band flags (when requested)
+};
+std::vector<CandResult> evaluate_candidates(rv_context* c, const std::vector<std::array<double, 3>>& starts,
+                                            const ConstraintSet& cs, const double* corrs, const rv_config& cfg,
+                                            bool want_band) {
+  const size_t K = starts.size();
+  std::vector<CandResult> out(K);
+  if (K == 0) return out;
+  if (cfg.angle_bins < 8) fail(RV_ERR_INVALID_CONFIG, "angle histogram needs bin_count >= 8");
+  const size_t nn = (size_t)std::max<int64_t>(cs.n, 1);
+  const size_t bw = (size_t)(cs.n + 31) / 32 + 32;
+  Summary* sums = c->cand_sums.get<Summary>(K);
+  int32_t* idx = c->cand_idx.get<int32_t>(K * nn);
+  int32_t* sup = c->cand_sup.get<int32_t>(2 * K);
+  uint32_t* band = want_band ? c->cand_band.get<uint32_t>(K * bw) : nullptr;
+  uint32_t* bins = c->bins.get<uint32_t>(cfg.angle_bins);
+  double* raw = c->raw.get<double>(nn);
+  double* asums = c->angle_sums.get<double>(2 * 296);
+  for (size_t k = 0; k < K; ++k) {  // queue every candidate: no read-back in between
+    CoopFused fz;
+    fz.compact_out = idx + k * nn;
+    fz.zero_bins = bins;
+    fz.n_bins = cfg.angle_bins;
+    fz.zero_counts = sums[k].counts;
+    CoopState* st = coop_refine_launch(c, cs, starts[k].data(), nullptr, 0, 0.0, cfg, nullptr, nullptr, &sums[k].st,
+                                       &fz);
+    launch_vote_angles_k(nullptr, corrs, idx + k * nn, cs.n, cfg.angle_bins, cfg.tau_deg, bins, raw, sums[k].counts,
+                         c->st, st->axis, &st->count, nullptr);
+    launch_peak_angle_k(bins, cfg.angle_bins, raw, cs.n, asums, sums[k].angle, c->done_ptr(), c->st, &st->count);
+    count_launch(c, 2);
+  }
+  std::vector<Summary> hs(K);
+  ck(cudaMemcpyAsync(hs.data(), sums, sizeof(Summary) * K, cudaMemcpyDeviceToHost, c->st), "candidates D2H");
+  sync(c);
+  int32_t* bc = c->sup_counts.get<int32_t>((size_t)classify_blocks(cs.n) * 2);
+  for (size_t k = 0; k < K; ++k) {
+    const Summary& sm = hs[k];
+    CandResult& r = out[k];
+    if (sm.counts[0] == 0) continue;  // angle_dev: NoVotes -> the candidate is skipped
+    Estimate& e = r.est;
+    std::memcpy(e.axis, sm.st.axis, sizeof e.axis);
+    const double sv = sm.angle[0], co = sm.angle[1], center = sm.angle[3];
+    double angle = center;
+    if (cfg.refine && !(sv == 0.0 && co == 0.0)) {
+      angle = std::atan2(sv, co);
+      if (angle <= -kPiD) angle += 2.0 * kPiD;
+    }
+    e.angle = angle;
+    rodrigues3(e.axis, e.angle, e.R);
+    e.dev_count = (int64_t)sm.st.count;
+    r.d_idx = idx + k * nn;
+    r.d_band = band ? band + k * bw : nullptr;
+    r.ok = true;
+    launch_model_support_k(cs.zx, cs.zy, cs.zz, cs.kept, corrs, cs.n, e.axis, e.angle, cfg.epsilon, cfg.tau_deg,
+                           band ? band + k * bw : nullptr, bc, sup + 2 * k, c->done_ptr(), c->st);
+    count_launch(c);
+  }
+  std::vector<int32_t> hsup(2 * K);
+  ck(cudaMemcpyAsync(hsup.data(), sup, sizeof(int32_t) * 2 * K, cudaMemcpyDeviceToHost, c->st), "supports D2H");
+  sync(c);
+  for (size_t k = 0; k < K; ++k) {
+    out[k].coherent = hsup[2 * k];
+    out[k].band = hsup[2 * k + 1];
+  }
+  return out;
+}
+
+// The winner of a candidate batch: vote lookup at its axis (build_candidate) and its inlier list.
+void materialize_candidate(rv_context* c, const uint32_t* grid, const rv_config& cfg, const CandResult& r,
+                           Estimate* est, bool look_up_votes) {
+  if (look_up_votes) {
+    double A, B;
+    est->votes = project3(est->axis, &A, &B) ? grid_cell(c, grid, cfg.grid, coord_to_cell(A, cfg.grid, cfg.extent),
+                                                          coord_to_cell(B, cfg.grid, cfg.extent))
+                                              : 0u;
+  }
+  est->inliers.resize((size_t)est->dev_count);
+  if (est->dev_count > 0)
+    ck(cudaMemcpyAsync(est->inliers.data(), r.d_idx, sizeof(int32_t) * (size_t)est->dev_count,
+                       cudaMemcpyDeviceToHost, c->st),
+       "inliers D2H");
+  sync(c);
+  est->dev_count = -1;
+}
+
 Estimate rescue_single(rv_context* c, const PreResult& pre, const double* d_corrs, const rv_config& cfg,
                        const uint32_t* grid, Estimate est) {
   int64_t best = model_support_dev(c, pre.cs, d_corrs, est, cfg, nullptr).coherent;
-  // candidates run as chained device sequences with their inlier lists left on the device; the
-  // winner's list and vote count are read once at the end
-  int32_t* best_idx = c->best_idx.get<int32_t>((size_t)std::max<int64_t>(pre.cs.n, 1));
-  bool cand_won = false;
-  for (const auto& ax : rescue_axes_dev(c, grid, pre.cs, cfg)) {
-    Estimate cand;
-    try {
-      cand = build_candidate_chained(c, ax.data(), pre.cs, d_corrs, cfg);
-    } catch (const RvError& e) {
-      if (e.st == RV_ERR_NO_VOTES) continue;
-      throw;
+  const auto res = evaluate_candidates(c, rescue_axes_dev(c, grid, pre.cs, cfg), pre.cs, d_corrs, cfg, false);
+  const CandResult* win = nullptr;
+  for (const auto& r : res)  // in order, strictly better than the incumbent (estimator.cpp:360-367)
+    if (r.ok && r.coherent > best) {
+      best = r.coherent;
+      win = &r;
     }
-    const int64_t coh = model_support_dev(c, pre.cs, d_corrs, cand, cfg, nullptr).coherent;
-    if (coh > best) {
-      best = coh;
-      if (cand.dev_count > 0)
-        ck(cudaMemcpyAsync(best_idx, c->compact_out.get<int32_t>((size_t)cand.dev_count),
-                           sizeof(int32_t) * (size_t)cand.dev_count, cudaMemcpyDeviceToDevice, c->st),
-           "best inliers D2D");
-      est = std::move(cand);
-      cand_won = true;
-    }
-  }
-  if (cand_won) {
-    double A, B;  // build_candidate's vote lookup at the refined axis
-    est.votes = project3(est.axis, &A, &B) ? grid_cell(c, grid, cfg.grid, coord_to_cell(A, cfg.grid, cfg.extent),
-                                                        coord_to_cell(B, cfg.grid, cfg.extent))
-                                            : 0u;
-    est.inliers.resize((size_t)est.dev_count);
-    if (est.dev_count > 0)
-      ck(cudaMemcpyAsync(est.inliers.data(), best_idx, sizeof(int32_t) * (size_t)est.dev_count,
-                         cudaMemcpyDeviceToHost, c->st),
-         "inliers D2H");
-    sync(c);
-    est.dev_count = -1;
+  if (win) {
+    est = win->est;
+    materialize_candidate(c, grid, cfg, *win, &est, true);
   }
   return est;
 }
