@@ -1921,41 +1921,24 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
       canonicalize3(b, s0);
       starts.push_back({s0[0], s0[1], s0[2]});
       for (const auto& a : rescue_axes_dev(c, grid, sub, cfg)) starts.push_back(a);
-      // candidates keep their inlier lists on the device; only the winner's is read back
-      int32_t* best_idx = c->best_idx.get<int32_t>((size_t)std::max<int64_t>(pre.cs.n, 1));
-      for (size_t s = 0; s < starts.size(); ++s) {
-        Estimate cand;
-        try {
-          cand = build_candidate_chained(c, starts[s].data(), pre.cs, d_corrs, cfg);
-        } catch (const RvError& e) {
-          if (e.st == RV_ERR_NO_VOTES) continue;
-          throw;
+      // all candidates as one device batch (per-candidate slots, two read-backs); the first usable
+      // one wins unless a later one has strictly more coherent support (estimator.cpp:415-433)
+      const auto res = evaluate_candidates(c, starts, pre.cs, d_corrs, cfg, true);
+      const CandResult* win = nullptr;
+      size_t win_k = 0;
+      for (size_t k = 0; k < res.size(); ++k)
+        if (res[k].ok && (!win || res[k].coherent > win->coherent)) {
+          win = &res[k];
+          win_k = k;
         }
-        cand.votes = s == 0 ? peaks[0].votes : 0u;  // (s > 0: looked up below if it wins)
-        const Support cs = model_support_dev(c, pre.cs, d_corrs, cand, cfg, cand_band);
-        if (!have || cs.coherent > sup.coherent) {
-          if (cand.dev_count > 0)
-            ck(cudaMemcpyAsync(best_idx, c->compact_out.get<int32_t>((size_t)cand.dev_count), sizeof(int32_t) *
-                               (size_t)cand.dev_count, cudaMemcpyDeviceToDevice, c->st), "best inliers D2D");
-          est = std::move(cand);
-          sup = cs;
-          std::swap(best_band, cand_band);
-          have = true;
-        }
-      }
-      if (have && est.votes == 0) {  // build_candidate's vote lookup at the refined axis, winner only
-        double A, B;
-        if (project3(est.axis, &A, &B))
-          est.votes = grid_cell(c, grid, cfg.grid, coord_to_cell(A, cfg.grid, cfg.extent),
-                                coord_to_cell(B, cfg.grid, cfg.extent));
-      }
-      if (have && est.dev_count >= 0) {
-        est.inliers.resize((size_t)est.dev_count);
-        if (est.dev_count > 0)
-          ck(cudaMemcpyAsync(est.inliers.data(), best_idx, sizeof(int32_t) * (size_t)est.dev_count,
-                             cudaMemcpyDeviceToHost, c->st), "inliers D2H");
-        sync(c);
-        est.dev_count = -1;
+      if (win) {
+        est = win->est;
+        sup.coherent = win->coherent;
+        sup.band = win->band;
+        best_band = const_cast<uint32_t*>(win->d_band);
+        est.votes = win_k == 0 ? peaks[0].votes : 0u;
+        materialize_candidate(c, grid, cfg, *win, &est, win_k != 0);
+        have = true;
       }
     }
     bool identity_model = false;
