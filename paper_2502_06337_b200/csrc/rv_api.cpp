@@ -97,7 +97,7 @@ struct Estimate {
   // kernels streamed it there) and rv_result_inliers copies it once, straight from there
   const int32_t* view = nullptr;
   int64_t view_n = 0;
-  int64_t dev_count = -1;  // >= 0: inliers not read back (still in the context's compaction buffer)
+  int64_t dev_count = -1;  // >= 0: inliers not read back yet (left in a device buffer)
   int64_t n_inliers() const { return view ? view_n : dev_count >= 0 ? dev_count : (int64_t)inliers.size(); }
 };
 
@@ -142,7 +142,6 @@ struct rv_context {
   DBuf red_keys;                         // fused argmax scratch of the tile reduction
   DBuf kept_acc;                          // in-order preprocess: kept-count accumulator + ticket
   DBuf sort_tmp;                          // CUB radix-sort scratch (multi-model strip percentile)
-  DBuf best_idx;                          // multi-model: inlier list of the best candidate so far
   DBuf cand_sums, cand_idx, cand_sup, cand_band;  // batched rescue candidates (per-candidate slots)
   // CSV ingest (rv_io.cu)
   DBuf csv_text, csv_chunk, csv_misc, csv_dpos, csv_dline, csv_nl, csv_status, csv_row, csv_block, csv_out, csv_fb,
@@ -879,17 +878,6 @@ std::vector<std::array<double, 3>> rescue_axes_dev(rv_context* c, const uint32_t
 }
 
 // build_candidate (estimator.cpp:183-194). Throws NoVotes.
-Estimate build_candidate_dev(rv_context* c, const double start[3], const uint32_t* grid, const ConstraintSet& cs,
-                             const double* corrs, const rv_config& cfg, bool want_inliers = true) {
-  double axis[3] = {start[0], start[1], start[2]};
-  const Cls cl = refine_loop_dev(c, cs, axis, cfg);
-  uint32_t votes = 0;
-  double A, B;
-  if (project3(axis, &A, &B))
-    votes = grid_cell(c, grid, cfg.grid, coord_to_cell(A, cfg.grid, cfg.extent), coord_to_cell(B, cfg.grid, cfg.extent));
-  return build_estimate_dev(c, cs, axis, cl, votes, corrs, cfg, want_inliers);
-}
-
 // ---------------------------------------------------------------------------------------
 struct PreResult {
   ConstraintSet cs;
@@ -1614,9 +1602,6 @@ Estimate finish_single_stepped(rv_context* c, const PreResult& pre, const double
 }
 
 // Rescue (estimator.cpp:352-368): blurred peaks + LS-all annealed candidates, best model support.
-Estimate build_candidate_chained(rv_context* c, const double start[3], const ConstraintSet& cs,
-                                 const double* corrs, const rv_config& cfg);
-
 // K rescue candidates (build_candidate + model_support each, estimator.cpp:352-368 / 452-466)
 // evaluated as ONE device sequence: every candidate's refine (cooperative, compaction fused),
 // angle vote and peak are queued back to back with per-candidate summary and inlier slots, read
@@ -1824,50 +1809,6 @@ std::vector<Estimate> estimate_multi_onepass_dev(rv_context* c, const double* d_
   return out;
 }
 
-// build_candidate (refine_loop + build_estimate from a start axis) chained on the device for the
-// multi-model rounds: one cooperative refine launch with the compaction fused, the angle vote and
-// peak on the refined axis/count, ONE summary read-back. The inlier list stays in compact_out
-// (dev_count); votes are left 0 (only the winning candidate's are looked up).
-Estimate build_candidate_chained(rv_context* c, const double start[3], const ConstraintSet& cs,
-                                 const double* corrs, const rv_config& cfg) {
-  if (cfg.angle_bins < 8) fail(RV_ERR_INVALID_CONFIG, "angle histogram needs bin_count >= 8");
-  Summary* dsum = summary_buf(c);
-  int32_t* idx = c->compact_out.get<int32_t>((size_t)std::max<int64_t>(cs.n, 1));
-  uint32_t* bins = c->bins.get<uint32_t>(cfg.angle_bins);
-  CoopFused fz;
-  fz.compact_out = idx;
-  fz.zero_bins = bins;
-  fz.n_bins = cfg.angle_bins;
-  fz.zero_counts = dsum->counts;
-  CoopState* st = coop_refine_launch(c, cs, start, nullptr, 0, 0.0, cfg, nullptr, nullptr, &dsum->st, &fz);
-  {
-    StageScope sc(c, kAngles);
-    double* raw = c->raw.get<double>((size_t)std::max<int64_t>(cs.n, 1));
-    launch_vote_angles_k(nullptr, corrs, idx, cs.n, cfg.angle_bins, cfg.tau_deg, bins, raw, dsum->counts, c->st,
-                         st->axis, &st->count, nullptr);
-    launch_peak_angle_k(bins, cfg.angle_bins, raw, cs.n, c->angle_sums.get<double>(2 * 296), dsum->angle,
-                        c->done_ptr(), c->st, &st->count);
-    count_launch(c, 2);
-  }
-  Summary* h = reinterpret_cast<Summary*>(c->pinned);
-  ck(cudaMemcpyAsync(h, dsum, sizeof(Summary), cudaMemcpyDeviceToHost, c->st), "candidate D2H");
-  sync(c);
-  const Summary sm = *h;
-  if (sm.counts[0] == 0) fail(RV_ERR_NO_VOTES, "no correspondence produced an angle vote");  // angle_dev
-  Estimate est;
-  std::memcpy(est.axis, sm.st.axis, sizeof est.axis);
-  const double s = sm.angle[0], co = sm.angle[1], center = sm.angle[3];
-  double angle = center;
-  if (cfg.refine && !(s == 0.0 && co == 0.0)) {
-    angle = std::atan2(s, co);
-    if (angle <= -kPiD) angle += 2.0 * kPiD;
-  }
-  est.angle = angle;
-  rodrigues3(est.axis, est.angle, est.R);
-  est.dev_count = (int64_t)sm.st.count;
-  return est;
-}
-
 // estimate_multi (estimator.cpp:373-493)
 std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, int64_t n, const rv_config& cfg) {
   if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
@@ -1912,7 +1853,6 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
     Support sup;
     bool have = false;
     uint32_t* best_band = c->band_flagsA.get<uint32_t>((size_t)(pre.cs.n + 31) / 32 + 32);
-    uint32_t* cand_band = c->band_flagsB.get<uint32_t>((size_t)(pre.cs.n + 31) / 32 + 32);
     if (have_peak) {
       std::vector<std::array<double, 3>> starts;
       double A, B, b[3], s0[3];
