@@ -50,6 +50,35 @@ constexpr float kDc = 2e-6f;        // |c| below this: hemisphere flip ambiguous
 #define RV_STEP_UNROLL 1  // unroll of the 64-pair step loop
 #endif
 constexpr int kStepUnroll = RV_STEP_UNROLL;
+#ifndef RV_FB_INLINE
+#define RV_FB_INLINE __forceinline__  // exact path inlined: as a call, the ABI forced per-step remats (dev knob)
+#endif
+#ifndef RV_PACK
+#define RV_PACK 1  // 1: a lane's two pairs of a 64-pair step are adjacent and evaluated with f32x2 math
+#endif
+static_assert(!(RV_PACK && RV_NP != 2), "packed steps walk 2 adjacent pairs per lane");
+
+// sm_100 packed f32 pairs (FMUL2/FFMA2: one issue slot for two IEEE round-to-nearest ops, each
+// lane of the pair bit-identical to the scalar FMUL/FFMA)
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(f32x2 v, uint32_t& a, uint32_t& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(a), "=r"(b) : "l"(v));
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
 
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
@@ -240,6 +269,9 @@ __device__ __forceinline__ uint2 plan_from_sets(const Arc2& ulo, const Arc2& uhi
       nl = 1;
     }
   }
+  // even starts (M is a multiple of 64): K2's packed steps give each lane two adjacent pairs
+  L0 &= ~1;
+  L1 &= ~1;
   int s0 = wrap_pair(L0, M), l0 = H0 - L0 + 1;
   int s1 = wrap_pair(L1, M), l1 = nl == 2 ? H1 - L1 + 1 : 0;
   if (l0 >= M || l1 >= M) {
@@ -395,9 +427,10 @@ struct F32Geom {
   uint32_t lin_off;  // non-clamp: (magic_hi + r0) * W + magic_hi + c_min
   int magic_hi, G, r0, c_min;
 };
+template <bool kClamp, int kS>
+__device__ __forceinline__ uint32_t cell_of_bits(const F32Geom& g, float c, uint32_t bx, uint32_t by, bool* flag);
 template <bool kClamp, int kS>  // kS: compile-time fixed-point shift (0: g.S at run time)
 __device__ __forceinline__ uint32_t f32_cell(const F32Geom& g, float4 ba, float2 bb, float2 t, bool* flag) {
-  const int S = kS ? kS : g.S;
   // x, y carry the cell scale K = G/(2E) (folded into the f32 basis by the planner)
   const float xk = fmaf(ba.w, t.y, ba.x * t.x);
   const float yk = fmaf(bb.x, t.y, ba.y * t.x);
@@ -406,6 +439,38 @@ __device__ __forceinline__ uint32_t f32_cell(const F32Geom& g, float4 ba, float2
   const float rs = __int_as_float(__float_as_int(r) | (~__float_as_int(c) & 0x80000000));
   const uint32_t bx = (uint32_t)__float_as_int(fmaf(xk, rs, g.CMf));
   const uint32_t by = (uint32_t)__float_as_int(fmaf(yk, rs, g.CMf));
+  return cell_of_bits<kClamp, kS>(g, c, bx, by, flag);
+}
+
+// Two pairs of f32_cell at once, t = {cos_a, cos_b, sin_a, sin_b}: the same IEEE operations in
+// the same order, lane-parallel in f32x2, so each cell and flag is bit-identical to f32_cell's
+// (the exact path recomputes a queued pair with the scalar f32_cell to undo its deposit).
+template <bool kClamp, int kS>
+__device__ __forceinline__ void f32_cell2(const F32Geom& g, float4 ba, float2 bb, float4 t, uint32_t* rel,
+                                          bool* flag) {
+  const f32x2 C = pk2(t.x, t.y), Sn = pk2(t.z, t.w);
+  const f32x2 X = fma2(pk2(ba.w, ba.w), Sn, mul2(pk2(ba.x, ba.x), C));
+  const f32x2 Y = fma2(pk2(bb.x, bb.x), Sn, mul2(pk2(ba.y, ba.y), C));
+  const f32x2 Cc = fma2(pk2(bb.y, bb.y), Sn, mul2(pk2(ba.z, ba.z), C));
+  uint32_t cb[2];
+  upk2(Cc, cb[0], cb[1]);
+  float rs[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float r = rcp_approx(1.f + fabsf(__uint_as_float(cb[h])));
+    rs[h] = __int_as_float(__float_as_int(r) | (int)(~cb[h] & 0x80000000u));
+  }
+  const f32x2 RS = pk2(rs[0], rs[1]), CM = pk2(g.CMf, g.CMf);
+  uint32_t bx[2], by[2];
+  upk2(fma2(X, RS, CM), bx[0], bx[1]);
+  upk2(fma2(Y, RS, CM), by[0], by[1]);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) rel[h] = cell_of_bits<kClamp, kS>(g, __uint_as_float(cb[h]), bx[h], by[h], &flag[h]);
+}
+
+template <bool kClamp, int kS>
+__device__ __forceinline__ uint32_t cell_of_bits(const F32Geom& g, float c, uint32_t bx, uint32_t by, bool* flag) {
+  const int S = kS ? kS : g.S;
   *flag = (fabsf(c) < kDc) | ((bx & g.fmask) == 0u) | ((by & g.fmask) == 0u);
   // the column is always inside [c_min, c_min+W) (|X| <= 1 < extent, or clamped), so one
   // unsigned range test on the linear index is the band-ownership test
@@ -430,10 +495,21 @@ struct FbCtx {  // the few scalars the exact path needs (keeps the kernel-param 
   int G, halfJ, c_min, W, own_lo, own_hi;
 };
 
+// (cos, sin) of pair p in the shared table. RV_PACK layout: float4 q = {cos_2q, cos_2q+1,
+// sin_2q, sin_2q+1}, so one LDS.128 feeds a lane's two adjacent pairs as f32x2 operands.
+__device__ __forceinline__ float2 tab_pair(const float2* tab, int p) {
+#if RV_PACK
+  const float* t = reinterpret_cast<const float*>(tab) + 4 * (p >> 1) + (p & 1);
+  return make_float2(t[0], t[2]);
+#else
+  return tab[p];
+#endif
+}
+
 // Exact path of queued pairs: the hot loop deposited +2 at the pair's f32 cell (if in this tile)
 // unconditionally; undo that, then deposit both twins at their exact f64 cells (row-owned).
 template <bool kClamp, int kS>
-__device__ __noinline__ void fallback_pairs(FbCtx f, F32Geom g, uint32_t q_s, int count, uint32_t my_ci,
+__device__ RV_FB_INLINE void fallback_pairs(FbCtx f, F32Geom g, uint32_t q_s, int count, uint32_t my_ci,
                                             float4 my_a, float2 my_b, const float2* tab, uint32_t* tile,
                                             uint32_t tile_cells, int hb) {
   const int lane = threadIdx.x & 31;
@@ -451,7 +527,7 @@ __device__ __noinline__ void fallback_pairs(FbCtx f, F32Geom g, uint32_t q_s, in
   if (lane < count) {
     const int pair = (int)(e & 0xFFFFu);
     bool fl;
-    const uint32_t rel = f32_cell<kClamp, kS>(g, ba, bb, tab[pair], &fl);
+    const uint32_t rel = f32_cell<kClamp, kS>(g, ba, bb, tab_pair(tab, pair), &fl);
     if (rel < tile_cells) atomicSub(&tile[rel], 2u);
     double a1[3], a2[3];
     exact_basis(f.zx[ci], f.zy[ci], f.zz[ci], a1, a2);
@@ -479,6 +555,12 @@ __device__ __noinline__ void fallback_pairs(FbCtx f, F32Geom g, uint32_t q_s, in
 __device__ __forceinline__ float2 lds_f2(uint32_t saddr) {
   float2 t;
   asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(t.x), "=f"(t.y) : "r"(saddr));
+  return t;
+}
+
+__device__ __forceinline__ float lds_f1(uint32_t saddr) {
+  float t;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(t) : "r"(saddr));
   return t;
 }
 
@@ -552,15 +634,38 @@ __device__ __forceinline__ void vote_entries(const VoteCtx& v, const F32Geom& ge
       const uint32_t local_k = (uint32_t)k << 16;
       const int start = (int)(enc & 0xFFFFu), len = (int)(enc >> 16);
       const uint32_t tp_s = tab_s + 8u * (uint32_t)start;
+#if RV_PACK  // tab_s = table + 16*lane (packed steps); the scalar tail reads pair start + lane
+      const uint32_t tp1_s = tp_s - 8u * (uint32_t)lane - 4u * (uint32_t)(lane & 1);
+#endif
       // NP pairs per lane per step (32*NP consecutive pairs per warp); ranges are 32-aligned:
       // 64-pair steps while they fit, then one 32-pair tail step
       auto step = [&](int k0, auto np_tag) {
         constexpr int NP = decltype(np_tag)::value;
         bool flag[NP];
         uint32_t addr[NP];
+        uint32_t relp[NP];
+        // pair of (lane, h): packed steps walk adjacent pairs k0 + 2*lane + h, the others k0 + 32*h + lane
+        constexpr bool kPacked = RV_PACK && NP == 2;
+        if constexpr (kPacked) {
+          float4 t4;
+          asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+              : "=f"(t4.x), "=f"(t4.y), "=f"(t4.z), "=f"(t4.w)
+              : "r"(tp_s + 8u * (uint32_t)k0));
+          f32_cell2<kClamp, kS>(geo, ba, bb, t4, relp, flag);
+        }
 #pragma unroll
         for (int h = 0; h < NP; ++h) {
-          const uint32_t rel = f32_cell<kClamp, kS>(geo, ba, bb, lds_f2(tp_s + 8u * (uint32_t)(k0 + 32 * h)), &flag[h]);
+          float2 t;
+          if constexpr (!kPacked) {
+#if RV_PACK  // scalar (tail) step over the packed layout: lane's pair k0 + lane
+            const uint32_t a1 = tp1_s + 8u * (uint32_t)(k0 + 32 * h);
+            t = make_float2(lds_f1(a1), lds_f1(a1 + 8u));
+#else
+            t = lds_f2(tp_s + 8u * (uint32_t)(k0 + 32 * h));
+#endif
+            relp[h] = f32_cell<kClamp, kS>(geo, ba, bb, t, &flag[h]);
+          }
+          const uint32_t rel = relp[h];
           // deposit even if flagged: the exact path undoes it (no select on the flag here)
 #if RV_PRED
           addr[h] = rel;
@@ -586,7 +691,7 @@ __device__ __forceinline__ void vote_entries(const VoteCtx& v, const F32Geom& ge
           for (int h = 0; h < NP; ++h) {
             const unsigned fm = __ballot_sync(0xFFFFFFFFu, flag[h]);
             if (flag[h]) {
-              int pair = start + k0 + 32 * h + lane;
+              int pair = kPacked ? start + k0 + 2 * lane + h : start + k0 + 32 * h + lane;
               if (pair >= M) pair -= M;
               sts_u32(fbq_s + 4u * (uint32_t)(qn + __popc(fm & lt_mask)), local_k | (uint32_t)pair);
             }
@@ -659,7 +764,14 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t fbq_s = (uint32_t)__cvta_generic_to_shared(fbq_all + warp * kFbqCap);  // this warp's queue
+#if RV_PACK  // pair p of the doubled table lives in float4 p/2 = {cos_2q, cos_2q+1, sin_2q, sin_2q+1}
+  for (int q = tid; q < M + 32; q += blockDim.x) {
+    const float2 e = b.table32[(2 * q) % M], o = b.table32[(2 * q + 1) % M];
+    reinterpret_cast<float4*>(tab)[q] = make_float4(e.x, o.x, e.y, o.y);
+  }
+#else
   for (int k = tid; k < 2 * M + 64; k += blockDim.x) tab[k] = b.table32[k % M];
+#endif
 
   if (tid == 0) {  // initial band: CTAs split across bands in proportion to planned work
     unsigned long long total = 0;
@@ -685,7 +797,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
   unsigned int my_fb = 0;
   unsigned lt_mask = (1u << lane) - 1u;
   // per-lane table address (shared window): loaded by ld.shared below
-  uint32_t tab_s = (uint32_t)__cvta_generic_to_shared(tab) + 8u * (uint32_t)lane;
+  uint32_t tab_s = (uint32_t)__cvta_generic_to_shared(tab) + (RV_PACK ? 16u : 8u) * (uint32_t)lane;
   asm volatile("" : "+r"(lt_mask), "+r"(tab_s), "+r"(fbq_s));
   // opaque to the optimizer: otherwise the shared-window base is rematerialised every step
   uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(tile);
