@@ -124,3 +124,15 @@ def test_identity_and_all_dropped(port):
     x /= np.linalg.norm(x, axis=1, keepdims=True)
     e = port.estimate_single(np.concatenate([x, x], axis=1))
     assert np.allclose(e["rotation"], np.eye(3)) and e["inliers"].size == 20
+
+
+@pytest.mark.parametrize("key", ["c3", "c4", "c5"])
+def test_fullsize_golden_inputs_reproduce(key):
+    # the full-size goldens (tests/golden/make_golden_full.py) pin the generator's output bytes;
+    # the GPU tests regenerate the same input on the box
+    import hashlib
+    from conftest import golden
+    from paper_2502_06337_b200 import synth
+    g = golden(f"{key}_full")
+    corrs, _, _ = synth.make_config(key)
+    assert hashlib.sha256(corrs.tobytes()).digest() == bytes(g["corrs_sha256"])
