@@ -131,7 +131,7 @@ struct rv_context {
   // residual (estimate_multi)
   DBuf rzx, rzy, rzz, rkept, removed;
   // vote
-  DBuf basis_a, basis_b, ranges, band_work, table32, table64, grid, partials, slot_band, counters, stats;
+  DBuf basis_a, basis_b, ranges, band_work, table32, table64, grid, partials, slot_band, counters, stats, degen;
   int table_J = -1;
   // peaks
   DBuf arg_keys, arg_out, sat, blur_best, blur_out, done;
@@ -325,7 +325,7 @@ VotePlan make_plan(rv_context* c, int G, double E, int J) {
     p.c_max = G - 1;
     p.W = G + 4;  // row stride: 16-byte rows for the bulk copies, rows offset by 4 banks
   }
-  const size_t table_bytes = (size_t)(2 * p.halfJ + 64) * sizeof(float2);  // doubled: ranges never wrap
+  const size_t table_bytes = (size_t)(2 * p.halfJ + 64) * sizeof(float2);  // J samples (packed) + 64 slack
   const size_t fbq_bytes = (size_t)(kVoteThreads / 32) * kFbqCap * 4 + 32 * 4;  // + 32 lane sink words
   const size_t reserve = table_bytes + fbq_bytes + 1024;
   if ((size_t)c->max_smem <= reserve) return p;
@@ -339,10 +339,11 @@ VotePlan make_plan(rv_context* c, int G, double E, int J) {
   p.n_bands = nb;
   p.H_max = H;
   for (int b = 0; b <= nb; ++b) p.band_r0[b] = std::min(p.r_min + b * H, p.r_max + 1);
-  const double dy = 1e-5;  // culling margin (plane units) >> f32 error of the interval math
+  // band boundaries in plane units; the planner solves each boundary once and dilates / erodes
+  // the solution for the bands on either side (culling margin)
   for (int b = 0; b < nb; ++b) {
-    p.band_ylo[b] = b == 0 ? -INFINITY : (float)(-E + p.band_r0[b] * p.cs - dy);
-    p.band_yhi[b] = b == nb - 1 ? INFINITY : (float)(-E + p.band_r0[b + 1] * p.cs + dy);
+    p.band_ylo[b] = b == 0 ? -INFINITY : (float)(-E + p.band_r0[b] * p.cs);
+    p.band_yhi[b] = b == nb - 1 ? INFINITY : (float)(-E + p.band_r0[b + 1] * p.cs);
   }
   p.tile_words = ((size_t)H * p.W + 3) & ~size_t(3);  // multiple of 4: 16-byte aligned partial slots
   p.smem_bytes = (((p.tile_words + 32) * 4 + 15) & ~size_t(15)) + table_bytes + fbq_bytes;  // tile + sinks
@@ -370,12 +371,11 @@ void ensure_tables(rv_context* c, int J) {
     const double theta = -std::numbers::pi + j * step;
     t64[j] = make_double2(std::cos(theta), std::sin(theta));
   }
-  const int M = J / 2;
-  std::vector<float2> t32(std::max(M, 1));
-  for (int j = 0; j < M; ++j) t32[j] = make_float2((float)t64[j].x, (float)t64[j].y);
+  std::vector<float2> t32(std::max(J, 1));  // every sample: the vote reads canonical samples only
+  for (int j = 0; j < J; ++j) t32[j] = make_float2((float)t64[j].x, (float)t64[j].y);
   ck(cudaMemcpyAsync(c->table64.get<double2>(J), t64.data(), sizeof(double2) * J, cudaMemcpyHostToDevice, c->st),
      "table64");
-  ck(cudaMemcpyAsync(c->table32.get<float2>(std::max(M, 1)), t32.data(), sizeof(float2) * std::max(M, 1),
+  ck(cudaMemcpyAsync(c->table32.get<float2>(std::max(J, 1)), t32.data(), sizeof(float2) * std::max(J, 1),
                      cudaMemcpyHostToDevice, c->st),
      "table32");
   sync(c);
@@ -434,7 +434,7 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   b.zz = zz;
   b.grid = grid;
   b.table64 = c->table64.get<double2>(J);
-  b.table32 = c->table32.get<float2>(std::max(J / 2, 1));
+  b.table32 = c->table32.get<float2>(std::max(J, 1));
   c->times.vote_samples += n * (int64_t)J;
   c->times.vote_launches += 1;
   if (!p.banded || force_generic) {
@@ -445,10 +445,11 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   }
   b.basis_a = c->basis_a.get<float4>(n);
   b.basis_b = c->basis_b.get<float2>(n);
-  b.entry_cap = 2 * n;
+  b.entry_cap = kEntriesPerConstraint * n;
+  b.degen = c->degen.get<int32_t>(n);
   b.entries = c->ranges.get<unsigned long long>((size_t)b.entry_cap * p.n_bands);
   b.band_work = c->band_work.get<unsigned long long>(kMaxBands);
-  b.counters = c->counters.get<int32_t>(2 * kMaxBands + 1);
+  b.counters = c->counters.get<int32_t>(kCounterWords);
   b.entry_count = b.counters + kMaxBands + 1;
   b.stats = c->stats.get<unsigned long long>(2);
   // enough CTAs to keep every SM busy, but not more than the work can feed (~1M pairs per CTA)
@@ -461,7 +462,7 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   }
   if (!prezeroed) {
     ck(cudaMemsetAsync(b.band_work, 0, sizeof(unsigned long long) * kMaxBands, c->st), "memset band_work");
-    ck(cudaMemsetAsync(b.counters, 0, sizeof(int32_t) * (2 * kMaxBands + 1), c->st), "memset counters");
+    ck(cudaMemsetAsync(b.counters, 0, sizeof(int32_t) * kCounterWords, c->st), "memset counters");
     ck(cudaMemsetAsync(b.stats, 0, sizeof(unsigned long long) * 2, c->st), "memset stats");
   }
   set_fused(c, b, fused, p);
@@ -893,8 +894,8 @@ void set_vote_zeroing(rv_context* c, int G, PrepBuffers* b) {
   b->zero_n[0] = (int64_t)G * G;
   b->zero_ptr[1] = reinterpret_cast<uint32_t*>(c->band_work.get<unsigned long long>(kMaxBands));
   b->zero_n[1] = 2 * kMaxBands;
-  b->zero_ptr[2] = reinterpret_cast<uint32_t*>(c->counters.get<int32_t>(2 * kMaxBands + 1));
-  b->zero_n[2] = 2 * kMaxBands + 1;
+  b->zero_ptr[2] = reinterpret_cast<uint32_t*>(c->counters.get<int32_t>(kCounterWords));
+  b->zero_n[2] = kCounterWords;
   b->zero_ptr[3] = reinterpret_cast<uint32_t*>(c->stats.get<unsigned long long>(2));
   b->zero_n[3] = 4;
 }
@@ -1082,7 +1083,7 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
   VoteBuffers b;
   b.grid = grid;
   b.table64 = c->table64.get<double2>(J);
-  b.table32 = c->table32.get<float2>(std::max(J / 2, 1));
+  b.table32 = c->table32.get<float2>(std::max(J, 1));
   int32_t* h = reinterpret_cast<int32_t*>(c->pinned);
   if (p.banded) {
     // in-order constraint set: chunk k's z land at their input indices, so each chunk's plan and
@@ -1094,10 +1095,11 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
     b.zz = pb.zz;
     b.basis_a = c->basis_a.get<float4>(n);
     b.basis_b = c->basis_b.get<float2>(n);
-    b.entry_cap = 2 * n;
+    b.entry_cap = kEntriesPerConstraint * n;
+    b.degen = c->degen.get<int32_t>(n);
     b.entries = c->ranges.get<unsigned long long>((size_t)b.entry_cap * p.n_bands);
     b.band_work = c->band_work.get<unsigned long long>(kMaxBands);
-    b.counters = c->counters.get<int32_t>(2 * kMaxBands + 1);
+    b.counters = c->counters.get<int32_t>(kCounterWords);
     b.entry_count = b.counters + kMaxBands + 1;
     b.stats = c->stats.get<unsigned long long>(2);
     const int64_t est_pairs = (n / C) * (int64_t)p.halfJ;
@@ -1115,7 +1117,7 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
         for (int q = 0; q < 4; ++q) pb.zero_ptr[q] = nullptr;
       // entry lists and their counters are per chunk (reused: the stream orders chunk k's vote
       // before chunk k+1's plan)
-      if (k > 0) launch_zero_i32(b.counters + 1, 2 * kMaxBands, c->st);
+      if (k > 0) launch_zero_i32(b.counters + 1, kCounterWords - 1, c->st);
       b.range_lo = bounds[k];
       const int64_t cap = bounds[k + 1] - bounds[k];
       launch_plan(p, b, cap, c->st);

@@ -13,7 +13,13 @@ constexpr int kMaxBands = 64;        // row bands of the smem-tiled vote kernel
 #define RV_VOTE_THREADS 1024
 #endif
 constexpr int kVoteThreads = RV_VOTE_THREADS;  // threads per vote CTA (32 warps, <= 64 regs each: latency-bound loop)
-constexpr int kPad = 2;              // pair-index padding of each band range (culling slack)
+constexpr int kPad = 2;              // sample-index padding of each band range (culling slack)
+// vote counters: [0] slot counter, [1..kMaxBands] entry grab counters, [kMaxBands+1..2*kMaxBands]
+// entries per band, [2*kMaxBands+1] degenerate constraints listed, [2*kMaxBands+2] their grab counter
+constexpr int kCounterWords = 2 * kMaxBands + 3;
+constexpr int kDegenCount = 2 * kMaxBands + 1;
+constexpr int kDegenGrab = 2 * kMaxBands + 2;
+constexpr int kEntriesPerConstraint = 3;  // per band: <= 2 sample ranges, one of them split at J
 constexpr int kFbqCap = 64;          // per-warp exact-fallback queue entries
 constexpr int kReduceThreads = 256;
 
@@ -52,20 +58,23 @@ struct VoteBuffers {
   const double* zx = nullptr;  // constraints SoA (f64)
   const double* zy = nullptr;
   const double* zz = nullptr;
-  float4* basis_a = nullptr;   // (a1x a1y a1z a2x) rounded to f32
-  float2* basis_b = nullptr;   // (a2y a2z)
+  float4* basis_a = nullptr;   // fl32 of (K a1x, K a1y, -a1z, K a2x), K = G/(2E)
+  float2* basis_b = nullptr;   // fl32 of (K a2y, -a2z)
   // [n_bands][entry_cap] work entries of each band: ci | (start | len<<16) << 32, one per
-  // non-empty pair range of a constraint in the band (order irrelevant: integer sums)
+  // non-empty range of CANONICAL samples (c <= 0, exactly as the reference decides it) of a
+  // constraint in the band; start is a sample index in [0, J) (order irrelevant: integer sums)
   unsigned long long* entries = nullptr;
+  int32_t* degen = nullptr;        // [n] constraints without a clean canonical half circle
+                                   // (z = +-e3 exactly): voted sample by sample in f64
   int32_t* entry_count = nullptr;  // [kMaxBands] entries appended per band by K1
-  int64_t entry_cap = 0;           // entries stride per band (2 per constraint)
+  int64_t entry_cap = 0;           // entries stride per band (kEntriesPerConstraint per constraint)
   unsigned long long* band_work = nullptr;  // [kMaxBands] pairs per band (incl. padding)
-  float2* table32 = nullptr;   // [halfJ] (cos, sin) of theta_p, rounded to f32
+  float2* table32 = nullptr;   // [J] (cos, sin) of theta_j, rounded to f32
   double2* table64 = nullptr;  // [J] (cos, sin) exactly as the reference (host libm)
   uint32_t* grid = nullptr;    // [G*G] output
   uint32_t* partials = nullptr;        // [max_slots][tile_words]
   int32_t* slot_band = nullptr;        // [max_slots]
-  int32_t* counters = nullptr;         // [0]=slot counter, [1..kMaxBands]=entry counters per band
+  int32_t* counters = nullptr;         // [kCounterWords] (layout above)
   unsigned long long* stats = nullptr; // [0]=pairs evaluated, [1]=fallback pairs
   int max_slots = 0;
   const int32_t* bounds = nullptr;     // device [lo, hi) of constraints for this launch (null: [range_lo, range_lo + n))

@@ -2,24 +2,28 @@
 //
 // Reference semantics (voting.cpp:25-45, :88-118): every constraint z deposits exactly J
 // votes, one per sample theta_j = -pi + j*2pi/J of the great circle {v : z.v = 0}; each
-// sample is flipped to the southern hemisphere, stereographically projected and counted in
-// its cell of a G x G uint32 grid. The device result is BIT-EXACT with that definition:
+// sample is flipped to the southern hemisphere (iff c > 0), stereographically projected and
+// counted in its cell of a G x G uint32 grid. The device result is BIT-EXACT with that definition:
 //
-//  * Twins. Samples j and j+J/2 are antipodal, so after the hemisphere flip they land on
-//    the same plane point (up to ~1e-15). K2 evaluates one "pair" per twin and deposits 2.
-//  * f32 filter + exact f64 fallback. The pair is evaluated in f32 from an f64 basis; the
-//    cell coordinate t is produced on a 2^-S grid (S <= 13, chosen per geometry by make_plan) by
-//    one FFMA against a magic constant. |t32 - t64| <= K*6e-7 + 2^-(S+1) cells, so
-//    whenever t32 is at least 2*2^-S from an integer (and |c| >= 2e-6, no hemisphere ambiguity)
-//    the f32 cell IS the reference cell. Otherwise the pair is queued and both twins are
-//    recomputed exactly in f64 (same op order, no FMA) -- ~0.2% of pairs.
+//  * Canonical half circle. Samples j and j+J/2 are antipodal; after the flip they land on the
+//    same plane point (up to ~1e-15). Exactly one of each pair has c <= 0 (is "canonical"), and
+//    the canonical samples form J/2 consecutive sample indices j0 .. j0+J/2-1 (mod J). K1 finds j0
+//    with the reference's own f64 test (so K2 never decides a hemisphere), deposits the rare pairs
+//    with both / neither twin canonical (|c| at the rounding level) exactly, and K2 evaluates
+//    only canonical samples, depositing 2 each.
+//  * f32 filter + exact f64 fallback. A sample is evaluated in f32 from an f64 basis; the cell
+//    coordinate t is produced on a 2^-S grid (S <= 13, chosen per geometry by make_plan) by one
+//    FFMA against a magic constant. |t32 - t64| <= K*6e-7 + 2^-(S+1) cells, so
+//    whenever t32 is at least 2*2^-S from an integer the f32 cell IS the reference cell.
+//    Otherwise the sample is queued and both twins are recomputed exactly in f64 (same op order,
+//    no FMA) -- ~0.15% of samples.
 //  * Band tiling. The grid's reachable rows are split into bands that fit one CTA's shared
-//    memory (u32 counters, 1 CTA/SM). K1 computes per (constraint, band) the pair-index
+//    memory (u32 counters, 1 CTA/SM). K1 computes per (constraint, band) the canonical sample
 //    ranges whose projected points can fall in the band (analytic circle/line intersection,
-//    padded), so K2 only evaluates pairs near its band; an exact ownership test on the row
+//    padded), so K2 only evaluates samples near its band; an exact ownership test on the row
 //    decides the deposit, so a sample is counted by exactly one band.
-//  * Tiles are flushed once per (CTA, band) to partial slots; a reduction kernel sums the
-//    slots of each band (integer sums: order-free, deterministic).
+//  * Tiles are flushed once per (CTA, band) into the grid by TMA bulk reduce-adds (or partial
+//    slots summed by a reduction kernel): integer sums, order-free, deterministic.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -36,27 +40,12 @@ namespace {
 constexpr float kPiF = 3.14159265358979323846f;
 constexpr float kTwoPiF = 6.28318530717958647692f;
 constexpr float kRcMin = 1e-3f;     // |c| amplitude below which a circle is treated as all-band
-constexpr float kDc = 2e-6f;        // |c| below this: hemisphere flip ambiguous -> exact path
+#ifndef RV_FLAT
+#define RV_FLAT 0  // 1: one flat (entry, step) loop per band instead of nested entry / step loops
+#endif
 #ifndef RV_RED_GROUPS
 #define RV_RED_GROUPS 2
 #endif
-#ifndef RV_NP
-#define RV_NP 2  // pairs per lane per full step of the vote loop (2 or 4)
-#endif
-#ifndef RV_PRED
-#define RV_PRED 0  // 1: predicated deposit instead of the per-lane sink word
-#endif
-#ifndef RV_STEP_UNROLL
-#define RV_STEP_UNROLL 1  // unroll of the 64-pair step loop
-#endif
-constexpr int kStepUnroll = RV_STEP_UNROLL;
-#ifndef RV_FB_INLINE
-#define RV_FB_INLINE __forceinline__  // exact path inlined: as a call, the ABI forced per-step remats (dev knob)
-#endif
-#ifndef RV_PACK
-#define RV_PACK 1  // 1: a lane's two pairs of a 64-pair step are adjacent and evaluated with f32x2 math
-#endif
-static_assert(!(RV_PACK && RV_NP != 2), "packed steps walk 2 adjacent pairs per lane");
 
 // sm_100 packed f32 pairs (FMUL2/FFMA2: one issue slot for two IEEE round-to-nearest ops, each
 // lane of the pair bit-identical to the scalar FMUL/FFMA)
@@ -129,26 +118,33 @@ struct Arc2 {
   int n;
 };
 
-// { s in [0, pi] : A cos(theta_a + s) + B sin(theta_a + s) >= y0 } -- on the canonical arc this is
-// { Y(s) >= y0 } because 1 - c > 0 there. `dil` widens (>0) or narrows (<0) the interval by ~10x the
-// trig approximation error (atan2_fast <= 2.1e-4 rad), so a nearly-empty interval is never lost.
-constexpr float kArcDilate = 2e-3f;
-__device__ __forceinline__ Arc2 arc_ge(float A, float B, float y0, float theta_a, float dil) {
-  Arc2 r{0.f, 0.f, 0.f, 0.f, 0};
+// The trig part of { s in [0, pi] : A cos(theta_a + s) + B sin(theta_a + s) >= y0 } (on the
+// canonical arc this is { Y(s) >= y0 }, since 1 - c > 0 there), solved ONCE per band boundary and
+// then dilated (lower set of the band above) or eroded (upper set of the band below).
+// state 0: empty, 1: all of [0, pi], 2: sig +- alpha. A ratio within 2e-5 above 1 still counts as a
+// (tangent) visit: the f32 error of y0/R is ~3e-7, so no near-tangent visit is ever lost.
+struct ArcG {
+  float sig, alpha;
+  int state;
+};
+constexpr float kArcDilate = 2e-3f;  // >> acos/atan2_fast error near tangency (~8e-4 rad)
+__device__ __forceinline__ ArcG arc_solve(float A, float B, float y0, float theta_a) {
   const float R = sqrtf(fmaf(A, A, B * B));
-  if (!(R > 0.f)) {
-    if (y0 <= 0.f) r = Arc2{0.f, kPiF, 0.f, 0.f, 1};
-    return r;
-  }
+  if (!(R > 0.f)) return ArcG{0.f, 0.f, y0 <= 0.f ? 1 : 0};
   const float ratio = __fdividef(y0, R);
-  if (ratio <= -1.f) return Arc2{0.f, kPiF, 0.f, 0.f, 1};
-  if (!(ratio < 1.f)) return r;
-  const float alpha = acos_fast(ratio);
+  if (ratio <= -1.f) return ArcG{0.f, 0.f, 1};
+  if (!(ratio < 1.00002f)) return ArcG{0.f, 0.f, 0};
   float sig = atan2_fast(B, A) - theta_a;
   sig -= kTwoPiF * floorf((sig + kPiF) * (1.f / kTwoPiF));
-  const float half = alpha + dil;
-  const float lo0 = fmaxf(sig - half, 0.f), hi0 = fminf(sig + half, kPiF);
-  const float lo1 = fmaxf(sig - half + kTwoPiF, 0.f), hi1 = fminf(sig + half + kTwoPiF, kPiF);
+  return ArcG{sig, acos_fast(fminf(ratio, 1.f)), 2};
+}
+__device__ __forceinline__ Arc2 arc_dilate(const ArcG& g, float dil) {
+  Arc2 r{0.f, 0.f, 0.f, 0.f, 0};
+  if (g.state == 1) return Arc2{0.f, kPiF, 0.f, 0.f, 1};
+  if (g.state == 0) return r;
+  const float half = g.alpha + dil;
+  const float lo0 = fmaxf(g.sig - half, 0.f), hi0 = fminf(g.sig + half, kPiF);
+  const float lo1 = fmaxf(g.sig - half + kTwoPiF, 0.f), hi1 = fminf(g.sig + half + kTwoPiF, kPiF);
   if (lo0 <= hi0) {
     r.a0 = lo0;
     r.b0 = hi0;
@@ -166,12 +162,16 @@ __device__ __forceinline__ Arc2 arc_ge(float A, float B, float y0, float theta_a
   return r;
 }
 
-// Appends an integer pair interval [lo, hi] (u coordinates, increasing starts) to a running
-// merge of at most 3 output intervals held in registers.
-struct Runs {
-  int l0, h0, l1, h1, l2, h2, n;
+// Up to two inclusive sample ranges (increasing), clipped to the exact canonical arc [A0, A1];
+// a third disjoint range is merged into its nearer neighbour (a superset: every evaluated sample is
+// canonical, and the row ownership test decides the deposit).
+struct Runs2 {
+  int l0, h0, l1, h1, n;
 };
-__device__ __forceinline__ void runs_push(Runs& r, int lo, int hi) {
+__device__ __forceinline__ void runs_push(Runs2& r, int lo, int hi, int A0, int A1) {
+  lo = max(lo, A0);
+  hi = min(hi, A1);
+  if (lo > hi) return;
   if (r.n == 0) {
     r.l0 = lo;
     r.h0 = hi;
@@ -183,30 +183,72 @@ __device__ __forceinline__ void runs_push(Runs& r, int lo, int hi) {
       r.h1 = hi;
       r.n = 2;
     }
-  } else if (r.n == 2) {
-    if (lo <= r.h1 + 1) r.h1 = max(r.h1, hi);
-    else {
-      r.l2 = lo;
-      r.h2 = hi;
-      r.n = 3;
-    }
+  } else if (lo <= r.h1 + 1) {
+    r.h1 = max(r.h1, hi);
+  } else if (r.l1 - r.h0 <= lo - r.h1) {  // close the smaller gap
+    r.h0 = r.h1;
+    r.l1 = lo;
+    r.h1 = hi;
   } else {
-    if (lo <= r.h2 + 1) r.h2 = max(r.h2, hi);
-    else r.n = 4;  // overflow: caller goes conservative
+    r.h1 = hi;
   }
 }
 
-// x mod M in [0, M) (M = J/2 pairs; a power of two for every J the reference ships, else the
-// generic integer modulo)
-__device__ __forceinline__ int wrap_pair(int x, int M) {
-  if ((M & (M - 1)) == 0) return x & (M - 1);
-  x %= M;
-  return x < 0 ? x + M : x;
+// Entries (start | len << 16, start in [0, J)) of one band from its lower/upper arc sets:
+// S = U_lo \ U_hi mapped to sample indices u = pa + s/step, padded, clipped to the canonical arc,
+// merged, and split where the sample index wraps at J. Up to 3 entries (zero = none).
+struct Ent3 {
+  uint32_t e0, e1, e2;
+};
+__device__ __forceinline__ void ent_put(Ent3& o, int& k, int lo, int hi, int J) {
+  const uint32_t v = (uint32_t)lo | ((uint32_t)(hi - lo + 1) << 16);
+  if (k == 0) o.e0 = v;
+  else if (k == 1) o.e1 = v;
+  else o.e2 = v;
+  ++k;
+}
+// Final entries of one band from its (<= 2) runs inside the canonical arc [A0, A1] (A0 even, A1
+// odd): each run is widened to an even start and a whole number of 64-sample steps where the arc
+// and the neighbouring run leave room (extra samples are canonical and land outside the band, in
+// the vote's sink -- they never overlap another entry of this constraint and band, so nothing is
+// counted twice), then split where the sample index wraps at J, at a step boundary (the last step
+// before the wrap reads the table's 64-sample slack), so the vote's step grid never shifts.
+__device__ __forceinline__ Ent3 finalize_runs(const Runs2& runs, int A0, int A1, int J,
+                                              unsigned long long* work) {
+  Ent3 o{0u, 0u, 0u};
+  int k = 0;
+  int prev_hi = A0 - 1;
+  for (int r = 0; r < runs.n; ++r) {
+    int lo = (r == 0 ? runs.l0 : runs.l1) & ~1;
+    int hi = (r == 0 ? runs.h0 : runs.h1) | 1;
+    const int ub = (r == 0 && runs.n == 2) ? (runs.l1 & ~1) - 1 : A1;
+    lo = max(lo, prev_hi + 1);
+    int need = ((hi - lo + 64) & ~63) - (hi - lo + 1);
+    const int up = min(need, ub - hi);
+    hi += up;
+    need -= up;
+    lo -= min(need, lo - (prev_hi + 1));
+    prev_hi = hi;
+    *work += (unsigned long long)((hi - lo + 64) & ~63);
+    if (hi < J) {
+      ent_put(o, k, lo, hi, J);
+    } else if (lo >= J) {
+      ent_put(o, k, lo - J, hi - J, J);
+    } else {
+      const int cut = lo + (((J - lo) + 63) & ~63);  // first step boundary at or after J
+      if (cut > hi) {
+        ent_put(o, k, lo, hi, J);  // its last step crosses J: read from the slack
+      } else {
+        ent_put(o, k, lo, cut - 1, J);
+        ent_put(o, k, cut - J, hi - J, J);
+      }
+    }
+  }
+  return o;
 }
 
-// Ranges of one band from its lower/upper arc sets: S = U_lo \ U_hi, padded, merged, wrapped.
-__device__ __forceinline__ uint2 plan_from_sets(const Arc2& ulo, const Arc2& uhi, float pa, float inv_step, int M,
-                                                unsigned long long* work) {
+__device__ __forceinline__ Ent3 entries_from_sets(const Arc2& ulo, const Arc2& uhi, float pa, float inv_step, int A0,
+                                                  int A1, int J, unsigned long long* work) {
   // gaps of uhi inside [0, pi] (sorted): [0, a0], [b0, a1], [b_last, pi]
   float g[6];
   int ng;
@@ -230,7 +272,7 @@ __device__ __forceinline__ uint2 plan_from_sets(const Arc2& ulo, const Arc2& uhi
     ng = 3;
   }
   const float lo_a[2] = {ulo.a0, ulo.a1}, lo_b[2] = {ulo.b0, ulo.b1};
-  Runs runs{0, 0, 0, 0, 0, 0, 0};
+  Runs2 runs{0, 0, 0, 0, 0};
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
 #pragma unroll
@@ -240,67 +282,38 @@ __device__ __forceinline__ uint2 plan_from_sets(const Arc2& ulo, const Arc2& uhi
         // end, so it holds no sample of this band
         const float s1 = fmaxf(lo_a[i], g[2 * j]), s2 = fminf(lo_b[i], g[2 * j + 1]);
         if (s1 < s2)
-          runs_push(runs, __float2int_rd(fmaf(s1, inv_step, pa)) - kPad, __float2int_ru(fmaf(s2, inv_step, pa)) + kPad);
+          runs_push(runs, __float2int_rd(fmaf(s1, inv_step, pa)) - kPad, __float2int_ru(fmaf(s2, inv_step, pa)) + kPad,
+                    A0, A1);
       }
     }
   }
-  const uint2 full = make_uint2((uint32_t)M << 16, 0u);
-  if (runs.n == 0) return make_uint2(0u, 0u);
-  if (runs.n > 3) {
-    *work += (unsigned long long)M;
-    return full;
-  }
-  // u spans [pa - pad, pa + M + pad]: the last run may wrap onto the first
-  int nl = runs.n;
-  int L0 = runs.l0, H0 = runs.h0, L1 = runs.l1, H1 = runs.h1;
-  if (nl == 3) {
-    if (runs.h2 - M >= runs.l0 - 1) {  // join last with first across the wrap
-      L0 = runs.l2;
-      H0 = runs.h0 + M;
-      nl = 2;  // (L0,H0) and (l1,h1)
-    } else {
-      *work += (unsigned long long)M;
-      return full;
-    }
-  } else if (nl == 2) {
-    if (H1 - M >= L0 - 1) {
-      L0 = L1;
-      H0 = runs.h0 + M;
-      nl = 1;
-    }
-  }
-  // even starts (M is a multiple of 64): K2's packed steps give each lane two adjacent pairs
-  L0 &= ~1;
-  L1 &= ~1;
-  int s0 = wrap_pair(L0, M), l0 = H0 - L0 + 1;
-  int s1 = wrap_pair(L1, M), l1 = nl == 2 ? H1 - L1 + 1 : 0;
-  if (l0 >= M || l1 >= M) {
-    *work += (unsigned long long)M;
-    return full;
-  }
-  // 32-pair alignment (K2 walks 32 consecutive pairs per lane-step) and a final overlap merge
-  l0 = (l0 + 31) & ~31;
-  if (nl == 2) {
-    l1 = (l1 + 31) & ~31;
-    const int d01 = wrap_pair(s1 - s0, M), d10 = wrap_pair(s0 - s1, M);
-    if (d01 < l0) {
-      l0 = (max(l0, d01 + l1) + 31) & ~31;
-      nl = 1;
-    } else if (d10 < l1) {
-      s0 = s1;
-      l0 = (max(l1, d10 + l0) + 31) & ~31;
-      nl = 1;
-    }
-  }
-  if (l0 >= M || (nl == 2 && l0 + l1 >= M)) {
-    *work += (unsigned long long)M;
-    return full;
-  }
-  *work += (unsigned long long)(l0 + (nl == 2 ? l1 : 0));
-  return make_uint2((uint32_t)s0 | ((uint32_t)l0 << 16), nl == 2 ? ((uint32_t)s1 | ((uint32_t)l1 << 16)) : 0u);
+  return finalize_runs(runs, A0, A1, J, work);
 }
 
-// kNB > 0: n_bands <= kNB, ranges kept in registers and entries reserved once per (block, band)
+// Reference hemisphere decision (voting.cpp:36-38: flip iff c > 0) of sample j in [0, 2J).
+__device__ __forceinline__ bool canonical(const double a1[3], const double a2[3], const double2* t64, int j, int J) {
+  const double2 cs = t64[j >= J ? j - J : j];
+  return !(xa(xm(a1[2], cs.x), xm(a2[2], cs.y)) > 0.0);
+}
+
+// One sample exactly (f64, reference op order) into the global grid.
+__device__ __forceinline__ void exact_global(const double a1[3], const double a2[3], const double2* t64, int j,
+                                             const VotePlan& p, uint32_t* grid) {
+  const double2 cs = t64[j >= p.J ? j - p.J : j];
+  int row, col;
+  exact_sample(a1, a2, cs.x, cs.y, p, &row, &col);
+  atomicAdd(&grid[(size_t)row * p.G + col], 1u);
+}
+
+// K1b: per constraint, the exact f64 basis (orthonormal_basis, geom.cpp:36-43) and its f32 copy for
+// the vote; the CANONICAL half circle in sample space -- the J/2 consecutive samples j0 .. j0+J/2-1
+// whose hemisphere test c <= 0 holds in the reference's own f64 arithmetic (voting.cpp:36-38), so
+// the vote never decides a hemisphere; and per row band the sample ranges whose projected points
+// can fall in the band (analytic circle/line intersection, padded, superset). The few pairs whose
+// two twins are BOTH (or NEITHER) canonical -- |c| at the rounding level -- are deposited here
+// exactly; constraints without a clean canonical half circle (z = +-e3 exactly: c == 0) are listed
+// for the vote kernel's exact sample-by-sample path.
+// kNB > 0: n_bands <= kNB, entries kept in shared memory and reserved once per (block, band)
 // (same-address global atomics were the planner's bottleneck); kNB == 0: any band count, one
 // reservation per (warp, band).
 template <int kNB>
@@ -320,79 +333,124 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
     z1 = b.zy[i];
     z2 = b.zz[i];
   }
-  const bool valid = i < hi && !isnan(z0);  // in-order constraint sets mark dropped pairs with NaN
-  const int M = p.halfJ;
-  float f1[3] = {0.f, 0.f, 0.f}, f2[3] = {0.f, 0.f, 0.f};
+  bool valid = i < hi && !isnan(z0);  // in-order constraint sets mark dropped pairs with NaN
+  const int M = p.halfJ, J = p.J;
+  float f1y = 0.f, f2y = 0.f, f1z = 0.f, f2z = 0.f;  // fl32 of a1y, a2y, a1z, a2z (arc solves)
+  int A0 = 0, A1 = -1;  // canonical samples of the fast path: [A0, A1] (unwrapped, in [0, 2J))
+  float theta_a = 0.f, pa = 0.f;
+  const float inv_step = 1.f / p.step_f;
   if (valid) {
     double a1[3], a2[3];
     exact_basis(z0, z1, z2, a1, a2);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      f1[k] = __double2float_rn(a1[k]);
-      f2[k] = __double2float_rn(a2[k]);
-    }
-    // the vote reads fl32(K * a_xy) (one rounding, like fl32(a_xy)): saves a multiply per pair
     const double K = p.inv_cell;
-    b.basis_a[i] = make_float4(__double2float_rn(a1[0] * K), __double2float_rn(a1[1] * K), f1[2],
+    // the vote reads fl32(K * a_xy) (one rounding, like fl32(a_xy)) and fl32(-a_z): c' = 1 - c is
+    // then two FFMAs from the constant 1
+    b.basis_a[i] = make_float4(__double2float_rn(a1[0] * K), __double2float_rn(a1[1] * K), __double2float_rn(-a1[2]),
                                __double2float_rn(a2[0] * K));
-    b.basis_b[i] = make_float2(__double2float_rn(a2[1] * K), f2[2]);
+    b.basis_b[i] = make_float2(__double2float_rn(a2[1] * K), __double2float_rn(-a2[2]));
+    f1y = __double2float_rn(a1[1]);
+    f2y = __double2float_rn(a2[1]);
+    f1z = __double2float_rn(a1[2]);
+    f2z = __double2float_rn(a2[2]);
+    // c(theta) = rc cos(theta - phi): the canonical arc (c <= 0) starts at theta_a = phi + pi/2
+    theta_a = atan2_fast(f2z, f1z) + 0.5f * kPiF;
+    pa = (theta_a + kPiF) * inv_step;  // its sample coordinate, in [J/4, 5J/4]
+    const int jc = __float2int_ru(pa);
+    // exact start: the false -> true transition of canonical(j) next to jc
+    unsigned sm = 0;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) sm |= (unsigned)canonical(a1, a2, b.table64, jc - 3 + q, J) << q;
+    int j0 = -1;
+#pragma unroll
+    for (int q = 1; q < 6; ++q)
+      if (j0 < 0 && !((sm >> (q - 1)) & 1u) && ((sm >> q) & 1u)) j0 = jc - 3 + q;
+    int e = -1;  // exact end: first non-canonical sample after the arc (normally j0 + M)
+    if (j0 >= 0) {
+      unsigned em = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) em |= (unsigned)canonical(a1, a2, b.table64, j0 + M - 2 + q, J) << q;
+#pragma unroll
+      for (int q = 1; q < 4; ++q)
+        if (e < 0 && ((em >> (q - 1)) & 1u) && !((em >> q) & 1u)) e = j0 + M - 2 + q;
+    }
+    if (j0 < 0 || e < 0 || f1z == 0.f && f2z == 0.f) {
+      // no clean canonical half circle: every sample of this constraint goes the exact way
+      const int k = atomicAdd(&b.counters[kDegenCount], 1);
+      b.degen[k] = (int)i;
+      valid = false;
+    } else {
+      A0 = j0;
+      A1 = e - 1;
+      if (e == j0 + M + 1) {  // pair j0: both twins canonical -> both deposited exactly, separately
+        exact_global(a1, a2, b.table64, j0, p, b.grid);
+        exact_global(a1, a2, b.table64, j0 + M, p, b.grid);
+        A0 = j0 + 1;
+        A1 = j0 + M - 1;
+      } else if (e == j0 + M - 1) {  // pair j0 - 1: neither twin canonical
+        exact_global(a1, a2, b.table64, j0 - 1, p, b.grid);
+        exact_global(a1, a2, b.table64, j0 + M - 1, p, b.grid);
+      }
+      // the vote walks adjacent sample pairs from even indices: an odd first / even last sample of
+      // the arc is deposited here exactly (both twins), so every entry can start even and end odd
+      auto exact_pair = [&](int j) {
+        const int q = (j >= J ? j - J : j) % M;
+        exact_global(a1, a2, b.table64, q, p, b.grid);
+        exact_global(a1, a2, b.table64, q + M, p, b.grid);
+      };
+      if (A0 & 1) exact_pair(A0++);
+      if (!(A1 & 1)) exact_pair(A1--);
+    }
   }
-  // near-polar constraint: c ~ 0 everywhere, every band sees all pairs
-  const bool polar = !(sqrtf(fmaf(f1[2], f1[2], f2[2] * f2[2])) >= kRcMin);
-  const float theta_a = atan2_fast(f2[2], f1[2]) + 0.5f * kPiF;  // c(theta_a + s) = -rc sin(s)
-  const float inv_step = 1.f / p.step_f;
-  const float pa = (theta_a + kPiF) * inv_step;
+  // near-polar constraint: the projected arc hugs the rim, every band sees the whole arc
+  const bool polar = !(sqrtf(fmaf(f1z, f1z, f2z * f2z)) >= kRcMin);
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const unsigned long long ci = (unsigned long long)(uint32_t)i;
-  Arc2 ulo{0.f, kPiF, 0.f, 0.f, 1};  // band 0: Y >= -inf
-  // ranges of this constraint in band `band` (+ planned pairs into *w)
-  auto plan_band = [&](int band, unsigned long long* w) -> uint2 {
-    if (!valid) return make_uint2(0u, 0u);
-    if (polar) {
-      *w = (unsigned long long)M;
-      return make_uint2((uint32_t)M << 16, 0u);
-    }
-    if (band > 0) {
-      const float y0 = p.band_ylo[band];
-      ulo = arc_ge(fmaf(y0, f1[2], f1[1]), fmaf(y0, f2[2], f2[1]), y0, theta_a, kArcDilate);
-    }
-    Arc2 uhi{0.f, 0.f, 0.f, 0.f, 0};  // last band: Y >= +inf is empty
+  ArcG g_lo{0.f, 0.f, 1};  // band 0: Y >= -inf
+  // entries of this constraint in band `band` (+ planned samples into *w)
+  auto plan_band = [&](int band, unsigned long long* w) -> Ent3 {
+    if (!valid) return Ent3{0u, 0u, 0u};
+    if (polar) return finalize_runs(Runs2{A0, A1, 0, 0, 1}, A0, A1, J, w);
+    ArcG g_hi{0.f, 0.f, 0};  // last band: Y >= +inf is empty
     if (band < p.n_bands - 1) {
-      const float y1 = p.band_yhi[band];
-      uhi = arc_ge(fmaf(y1, f1[2], f1[1]), fmaf(y1, f2[2], f2[1]), y1, theta_a, -kArcDilate);
+      const float y1 = p.band_ylo[band + 1];
+      g_hi = arc_solve(fmaf(y1, f1z, f1y), fmaf(y1, f2z, f2y), y1, theta_a);
     }
-    return plan_from_sets(ulo, uhi, pa, inv_step, M, w);
+    const Arc2 ulo = arc_dilate(g_lo, kArcDilate), uhi = arc_dilate(g_hi, -kArcDilate);
+    g_lo = g_hi;  // the upper boundary of this band is the lower boundary of the next
+    return entries_from_sets(ulo, uhi, pa, inv_step, A0, A1, J, w);
   };
   // warp-level bookkeeping of one band: entry offset of this lane inside the warp's block of
   // entries, reserved in s_cnt (kNB > 0) or directly in the global list (kNB == 0)
-  auto book = [&](int band, uint2 r, unsigned long long w, bool global) -> int {
-    const unsigned m0 = __ballot_sync(0xFFFFFFFFu, r.x >= 0x10000u);  // r.y != 0 => r.x != 0
-    const unsigned m1 = __ballot_sync(0xFFFFFFFFu, r.y >= 0x10000u);
-    const int total = __popc(m0) + __popc(m1);
+  auto book = [&](int band, const Ent3& r, unsigned long long w, bool global) -> int {
+    const unsigned m0 = __ballot_sync(0xFFFFFFFFu, r.e0 != 0u);  // entries are filled in order
+    const unsigned m1 = __ballot_sync(0xFFFFFFFFu, r.e1 != 0u);
+    const unsigned m2 = __ballot_sync(0xFFFFFFFFu, r.e2 != 0u);
+    const int total = __popc(m0) + __popc(m1) + __popc(m2);
     int wbase = 0;
     if (lane == 0 && total) wbase = global ? atomicAdd(&b.entry_count[band], total) : atomicAdd(&s_cnt[band], total);
     wbase = __shfl_sync(0xFFFFFFFFu, wbase, 0);
-    const unsigned ws = __reduce_add_sync(0xFFFFFFFFu, (unsigned)w);  // w <= J/2 pairs per lane
+    const unsigned ws = __reduce_add_sync(0xFFFFFFFFu, (unsigned)w);  // w <= J + 128 per lane
     if (lane == 0 && ws) atomicAdd(&s_work[band], (unsigned long long)ws);
-    return wbase + __popc(m0 & lt_mask) + __popc(m1 & lt_mask);
+    return wbase + __popc(m0 & lt_mask) + __popc(m1 & lt_mask) + __popc(m2 & lt_mask);
   };
-  auto emit = [&](int band, uint2 r, int64_t off) {
-    if (r.x >= 0x10000u) {
-      unsigned long long* ep = b.entries + (int64_t)band * b.entry_cap + off;
-      ep[0] = ci | ((unsigned long long)r.x << 32);
-      if (r.y >= 0x10000u) ep[1] = ci | ((unsigned long long)r.y << 32);
-    }
+  auto emit = [&](int band, const Ent3& r, int64_t off) {
+    unsigned long long* ep = b.entries + (int64_t)band * b.entry_cap + off;
+    if (r.e0) ep[0] = ci | ((unsigned long long)r.e0 << 32);
+    if (r.e1) ep[1] = ci | ((unsigned long long)r.e1 << 32);
+    if (r.e2) ep[2] = ci | ((unsigned long long)r.e2 << 32);
   };
   if constexpr (kNB > 0) {
-    // per-thread ranges/offsets parked in shared memory (a rolled band loop keeps the code small)
-    __shared__ uint2 s_r[kNB][256];
+    // per-thread entries/offsets parked in shared memory (a rolled band loop keeps the code small)
+    __shared__ uint32_t s_r[kNB][3][256];
     __shared__ int s_off[kNB][256];
 #pragma unroll 1
     for (int band = 0; band < p.n_bands; ++band) {  // uniform
       unsigned long long w = 0;
-      const uint2 r = plan_band(band, &w);
-      s_r[band][threadIdx.x] = r;
+      const Ent3 r = plan_band(band, &w);
+      s_r[band][0][threadIdx.x] = r.e0;
+      s_r[band][1][threadIdx.x] = r.e1;
+      s_r[band][2][threadIdx.x] = r.e2;
       s_off[band][threadIdx.x] = book(band, r, w, false);
     }
     __syncthreads();
@@ -401,11 +459,12 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
     __syncthreads();
 #pragma unroll 1
     for (int band = 0; band < p.n_bands; ++band)
-      emit(band, s_r[band][threadIdx.x], (int64_t)s_base[band] + s_off[band][threadIdx.x]);
+      emit(band, Ent3{s_r[band][0][threadIdx.x], s_r[band][1][threadIdx.x], s_r[band][2][threadIdx.x]},
+           (int64_t)s_base[band] + s_off[band][threadIdx.x]);
   } else {
     for (int band = 0; band < p.n_bands; ++band) {  // uniform trip count: warp collectives inside
       unsigned long long w = 0;
-      const uint2 r = plan_band(band, &w);
+      const Ent3 r = plan_band(band, &w);
       emit(band, r, book(band, r, w, true));
     }
     __syncthreads();
@@ -416,9 +475,12 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
 
 // ---- K2 ------------------------------------------------------------------------------
 
-// f32 evaluation of one pair: tile-relative linear cell index `rel` (>= tile_cells: not this
-// band's tile) and whether the f32 cell is not provably the reference cell. Shared by the hot
-// loop and the exact path (which undoes the hot loop's deposit), so both see identical values.
+// f32 evaluation of one canonical sample: tile-relative linear cell index `rel` (>= tile_cells: not
+// this band's tile) and whether the f32 cell is not provably the reference cell. The sample is
+// canonical (c <= 0 in the reference's own arithmetic, decided by the planner), so there is no
+// hemisphere logic: c' = 1 - c from two FFMAs off the constant 1, r = rcp.approx(c'). Shared by the
+// hot loop (packed, f32_cell2) and the exact path (which undoes the hot loop's deposit), so both
+// see identical values.
 struct F32Geom {
   float CMf;
   int S;
@@ -428,50 +490,9 @@ struct F32Geom {
   int magic_hi, G, r0, c_min;
 };
 template <bool kClamp, int kS>
-__device__ __forceinline__ uint32_t cell_of_bits(const F32Geom& g, float c, uint32_t bx, uint32_t by, bool* flag);
-template <bool kClamp, int kS>  // kS: compile-time fixed-point shift (0: g.S at run time)
-__device__ __forceinline__ uint32_t f32_cell(const F32Geom& g, float4 ba, float2 bb, float2 t, bool* flag) {
-  // x, y carry the cell scale K = G/(2E) (folded into the f32 basis by the planner)
-  const float xk = fmaf(ba.w, t.y, ba.x * t.x);
-  const float yk = fmaf(bb.x, t.y, ba.y * t.x);
-  const float c = fmaf(bb.y, t.y, ba.z * t.x);
-  const float r = rcp_approx(1.f + fabsf(c));
-  const float rs = __int_as_float(__float_as_int(r) | (~__float_as_int(c) & 0x80000000));
-  const uint32_t bx = (uint32_t)__float_as_int(fmaf(xk, rs, g.CMf));
-  const uint32_t by = (uint32_t)__float_as_int(fmaf(yk, rs, g.CMf));
-  return cell_of_bits<kClamp, kS>(g, c, bx, by, flag);
-}
-
-// Two pairs of f32_cell at once, t = {cos_a, cos_b, sin_a, sin_b}: the same IEEE operations in
-// the same order, lane-parallel in f32x2, so each cell and flag is bit-identical to f32_cell's
-// (the exact path recomputes a queued pair with the scalar f32_cell to undo its deposit).
-template <bool kClamp, int kS>
-__device__ __forceinline__ void f32_cell2(const F32Geom& g, float4 ba, float2 bb, float4 t, uint32_t* rel,
-                                          bool* flag) {
-  const f32x2 C = pk2(t.x, t.y), Sn = pk2(t.z, t.w);
-  const f32x2 X = fma2(pk2(ba.w, ba.w), Sn, mul2(pk2(ba.x, ba.x), C));
-  const f32x2 Y = fma2(pk2(bb.x, bb.x), Sn, mul2(pk2(ba.y, ba.y), C));
-  const f32x2 Cc = fma2(pk2(bb.y, bb.y), Sn, mul2(pk2(ba.z, ba.z), C));
-  uint32_t cb[2];
-  upk2(Cc, cb[0], cb[1]);
-  float rs[2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const float r = rcp_approx(1.f + fabsf(__uint_as_float(cb[h])));
-    rs[h] = __int_as_float(__float_as_int(r) | (int)(~cb[h] & 0x80000000u));
-  }
-  const f32x2 RS = pk2(rs[0], rs[1]), CM = pk2(g.CMf, g.CMf);
-  uint32_t bx[2], by[2];
-  upk2(fma2(X, RS, CM), bx[0], bx[1]);
-  upk2(fma2(Y, RS, CM), by[0], by[1]);
-#pragma unroll
-  for (int h = 0; h < 2; ++h) rel[h] = cell_of_bits<kClamp, kS>(g, __uint_as_float(cb[h]), bx[h], by[h], &flag[h]);
-}
-
-template <bool kClamp, int kS>
-__device__ __forceinline__ uint32_t cell_of_bits(const F32Geom& g, float c, uint32_t bx, uint32_t by, bool* flag) {
+__device__ __forceinline__ uint32_t cell_of_bits(const F32Geom& g, uint32_t bx, uint32_t by, bool* flag) {
   const int S = kS ? kS : g.S;
-  *flag = (fabsf(c) < kDc) | ((bx & g.fmask) == 0u) | ((by & g.fmask) == 0u);
+  *flag = ((bx & g.fmask) == 0u) | ((by & g.fmask) == 0u);
   // the column is always inside [c_min, c_min+W) (|X| <= 1 < extent, or clamped), so one
   // unsigned range test on the linear index is the band-ownership test
   if (kClamp) {
@@ -481,87 +502,120 @@ __device__ __forceinline__ uint32_t cell_of_bits(const F32Geom& g, float c, uint
   }
   return (by >> S) * g.W + (bx >> S) - g.lin_off;
 }
+// ba = (K a1x, K a1y, -a1z, K a2x), bb = (K a2y, -a2z), t = (cos, sin) of the sample
+template <bool kClamp, int kS>
+__device__ __forceinline__ uint32_t f32_cell(const F32Geom& g, float4 ba, float2 bb, float2 t, bool* flag) {
+  const float xk = fmaf(ba.w, t.y, ba.x * t.x);
+  const float yk = fmaf(bb.x, t.y, ba.y * t.x);
+  const float cp = fmaf(bb.y, t.y, fmaf(ba.z, t.x, 1.f));
+  const float r = rcp_approx(cp);
+  const uint32_t bx = (uint32_t)__float_as_int(fmaf(xk, r, g.CMf));
+  const uint32_t by = (uint32_t)__float_as_int(fmaf(yk, r, g.CMf));
+  return cell_of_bits<kClamp, kS>(g, bx, by, flag);
+}
 
+// Two adjacent samples of f32_cell at once, t = {cos_a, cos_b, sin_a, sin_b}: the same IEEE
+// operations in the same order, lane-parallel in f32x2 (sm_100 FMUL2/FFMA2), so each cell and
+// flag is bit-identical to f32_cell's.
+template <bool kClamp, int kS>
+__device__ __forceinline__ void f32_cell2(const F32Geom& g, float4 ba, float2 bb, float4 t, f32x2 one2,
+                                          uint32_t* rel, bool* flag) {
+  const f32x2 C = pk2(t.x, t.y), Sn = pk2(t.z, t.w);
+  const f32x2 X = fma2(pk2(ba.w, ba.w), Sn, mul2(pk2(ba.x, ba.x), C));
+  const f32x2 Y = fma2(pk2(bb.x, bb.x), Sn, mul2(pk2(ba.y, ba.y), C));
+  const f32x2 CP = fma2(pk2(bb.y, bb.y), Sn, fma2(pk2(ba.z, ba.z), C, one2));
+  uint32_t cb[2];
+  upk2(CP, cb[0], cb[1]);
+  const f32x2 R = pk2(rcp_approx(__uint_as_float(cb[0])), rcp_approx(__uint_as_float(cb[1])));
+  const f32x2 CM = pk2(g.CMf, g.CMf);
+  uint32_t bx[2], by[2];
+  upk2(fma2(X, R, CM), bx[0], bx[1]);
+  upk2(fma2(Y, R, CM), by[0], by[1]);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) rel[h] = cell_of_bits<kClamp, kS>(g, bx[h], by[h], &flag[h]);
+}
 
-// Exact f64 evaluation of both twins of a queued pair; deposits the ones this band owns.
-// Cold path (~0.6% of pairs), kept out of line so the hot loop keeps its registers.
-struct FbCtx {  // the few scalars the exact path needs (keeps the kernel-param struct in cbank)
+// (cos, sin) of sample j in the shared table: float4 q = {cos_2q, cos_2q+1, sin_2q, sin_2q+1}, so
+// one LDS.128 feeds a lane's two adjacent samples as f32x2 operands.
+__device__ __forceinline__ float2 tab_sample(const float4* tab, int j) {
+  const float* t = reinterpret_cast<const float*>(tab) + 4 * (j >> 1) + (j & 1);
+  return make_float2(t[0], t[2]);
+}
+
+// Everything the exact path needs, parked in shared memory at kernel start (and per band): the
+// cold path reads it there (its loads cannot be hoisted past the queue stores), so none of it is
+// kept in registers or re-loaded from the constant bank around the hot step loop.
+struct ColdCtx {
   const double* zx;
   const double* zy;
   const double* zz;
   const double2* table64;
+  const float4* basis_a;
+  const float2* basis_b;
   uint32_t* grid;
   double E, inv_cell;
-  int G, halfJ, c_min, W, own_lo, own_hi;
+  int G, W, c_min, J, M;
+  int r0, hb, own_lo, own_hi;  // current band
 };
 
-// (cos, sin) of pair p in the shared table. RV_PACK layout: float4 q = {cos_2q, cos_2q+1,
-// sin_2q, sin_2q+1}, so one LDS.128 feeds a lane's two adjacent pairs as f32x2 operands.
-__device__ __forceinline__ float2 tab_pair(const float2* tab, int p) {
-#if RV_PACK
-  const float* t = reinterpret_cast<const float*>(tab) + 4 * (p >> 1) + (p & 1);
-  return make_float2(t[0], t[2]);
-#else
-  return tab[p];
-#endif
+__device__ __forceinline__ void set_cold_band(ColdCtx& c, const VotePlan& p, int band) {
+  c.r0 = p.band_r0[band];
+  c.hb = p.band_r0[band + 1] - c.r0;
+  c.own_lo = band == 0 ? 0 : c.r0;
+  c.own_hi = band == p.n_bands - 1 ? p.G : c.r0 + c.hb;
 }
 
-// Exact path of queued pairs: the hot loop deposited +2 at the pair's f32 cell (if in this tile)
-// unconditionally; undo that, then deposit both twins at their exact f64 cells (row-owned).
+// Exact path of queued samples: the hot loop deposited +2 at the sample's f32 cell (if in this
+// tile) unconditionally; undo that, then deposit BOTH twins of its pair (samples p and p + J/2,
+// each with the reference's own hemisphere decision) at their exact f64 cells (row-owned).
+#ifndef RV_FB_NOINLINE
+#define RV_FB_NOINLINE 1  // exact path as a real call: its registers stay out of the hot loop
+#endif
+#if RV_FB_NOINLINE
+#define RV_FB_ATTR __noinline__
+#else
+#define RV_FB_ATTR __forceinline__
+#endif
 template <bool kClamp, int kS>
-__device__ RV_FB_INLINE void fallback_pairs(FbCtx f, F32Geom g, uint32_t q_s, int count, uint32_t my_ci,
-                                            float4 my_a, float2 my_b, const float2* tab, uint32_t* tile,
-                                            uint32_t tile_cells, int hb) {
+__device__ RV_FB_ATTR void fallback_samples(const ColdCtx* cc_s, const F32Geom& g, uint32_t q_s, int count,
+                                                 uint32_t my_ci, const float4* tab, uint32_t* tile) {
+  const volatile ColdCtx& f = *cc_s;
   const int lane = threadIdx.x & 31;
   const uint32_t e = lane < count ? lds_u32(q_s + 4u * lane) : 0u;
   const int k = (int)(e >> 16) & 31;  // entry index within the warp's grab
   const uint32_t ci = __shfl_sync(0xFFFFFFFFu, my_ci, k);
-  float4 ba;
-  float2 bb;
-  ba.x = __shfl_sync(0xFFFFFFFFu, my_a.x, k);
-  ba.y = __shfl_sync(0xFFFFFFFFu, my_a.y, k);
-  ba.z = __shfl_sync(0xFFFFFFFFu, my_a.z, k);
-  ba.w = __shfl_sync(0xFFFFFFFFu, my_a.w, k);
-  bb.x = __shfl_sync(0xFFFFFFFFu, my_b.x, k);
-  bb.y = __shfl_sync(0xFFFFFFFFu, my_b.y, k);
   if (lane < count) {
-    const int pair = (int)(e & 0xFFFFu);
+    const float4 ba = __ldg(f.basis_a + ci);
+    const float2 bb = __ldg(f.basis_b + ci);
+    const int j = (int)(e & 0xFFFFu);
     bool fl;
-    const uint32_t rel = f32_cell<kClamp, kS>(g, ba, bb, tab_pair(tab, pair), &fl);
-    if (rel < tile_cells) atomicSub(&tile[rel], 2u);
+    const int r0 = f.r0, hb = f.hb, own_lo = f.own_lo, own_hi = f.own_hi, W = f.W, G = f.G, c_min = f.c_min;
+    const uint32_t rel = f32_cell<kClamp, kS>(g, ba, bb, tab_sample(tab, j), &fl);
+    if (rel < (uint32_t)hb * (uint32_t)W) atomicSub(&tile[rel], 2u);
     double a1[3], a2[3];
     exact_basis(f.zx[ci], f.zy[ci], f.zz[ci], a1, a2);
+    const int M = f.M, J = f.J, jj = j >= J ? j - J : j;  // (the last step of a range may cross J)
+    const int pr = jj >= M ? jj - M : jj;
     VotePlan p1;
     p1.E = f.E;
     p1.inv_cell = f.inv_cell;
-    p1.G = f.G;
+    p1.G = G;
+    const double2* t64 = f.table64;
+    uint32_t* grid = f.grid;
 #pragma unroll
     for (int tw = 0; tw < 2; ++tw) {
-      const double2 cs = f.table64[pair + tw * f.halfJ];
+      const double2 cs = t64[pr + tw * M];
       int row, col;
       exact_sample(a1, a2, cs.x, cs.y, p1, &row, &col);
-      if (row < f.own_lo || row >= f.own_hi) continue;
-      const int lr = row - g.r0, lc = col - f.c_min;
-      if ((unsigned)lr < (unsigned)hb && (unsigned)lc < (unsigned)f.W)
-        atomicAdd(&tile[lr * f.W + lc], 1u);
+      if (row < own_lo || row >= own_hi) continue;
+      const int lr = row - r0, lc = col - c_min;
+      if ((unsigned)lr < (unsigned)hb && (unsigned)lc < (unsigned)W)
+        atomicAdd(&tile[lr * W + lc], 1u);
       else
-        atomicAdd(&f.grid[(size_t)row * f.G + col], 1u);
+        atomicAdd(&grid[(size_t)row * G + col], 1u);
     }
   }
   __syncwarp();
-}
-
-// table read (read-only after the prologue's barrier, so no memory clobber)
-__device__ __forceinline__ float2 lds_f2(uint32_t saddr) {
-  float2 t;
-  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(t.x), "=f"(t.y) : "r"(saddr));
-  return t;
-}
-
-__device__ __forceinline__ float lds_f1(uint32_t saddr) {
-  float t;
-  asm("ld.shared.f32 %0, [%1];" : "=f"(t) : "r"(saddr));
-  return t;
 }
 
 __device__ __forceinline__ uint32_t umin(uint32_t a, uint32_t b) { return a < b ? a : b; }
@@ -570,169 +624,18 @@ __device__ __forceinline__ void red_shared(uint32_t saddr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v));
 }
 
-__device__ __forceinline__ void red_shared_if(uint32_t saddr, uint32_t v, bool pred) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.add.u32 [%0], %1;\n\t}" ::"r"(saddr), "r"(v),
-      "r"((uint32_t)pred));
-}
-
-// The work-entry loop of one band tile (shared by the band-tiled vote and the fused front kernel):
-// per-warp dynamic grabs of 32 entries from `counter` (lane k holds entry k: range + f32 basis),
-// 64-pair steps, deposit-always into the tile, exact path for flagged pairs. fetch(j) returns
-// entry j of the band's list (j < n_ent).
-struct VoteCtx {
-  const float2* tab;
-  uint32_t tab_s;
-  uint32_t* tile;
-  uint32_t tile_s, sink_rel, vote2, fbq_s;
-  unsigned lt_mask;
-  int M;
-  uint32_t tile_cells;
-  int hb;
-  const float4* basis_a;
-  const float2* basis_b;
-  int grab;  // entries per warp grab (<= 32)
-};
-template <bool kClamp, int kS, class Fetch>
-__device__ __forceinline__ void vote_entries(const VoteCtx& v, const F32Geom& geo, const FbCtx& fc, Fetch fetch,
-                                             int n_ent, int* counter, unsigned int& my_fb) {
-  const int lane = threadIdx.x & 31;
-  const float2* tab = v.tab;
-  const uint32_t tab_s = v.tab_s, tile_s = v.tile_s, sink_rel = v.sink_rel, vote2 = v.vote2, fbq_s = v.fbq_s;
-  const unsigned lt_mask = v.lt_mask;
-  const int M = v.M, hb = v.hb;
-  const uint32_t tile_cells = v.tile_cells;
-  uint32_t* tile = v.tile;
-  const int grab = v.grab;
-  for (;;) {  // per-warp dynamic grabs of up to 32 entries (lane k holds entry k: range + f32 basis)
-    int g0 = 0;
-    if (lane == 0) g0 = atomicAdd(counter, grab);
-    g0 = __shfl_sync(0xFFFFFFFFu, g0, 0);
-    if (g0 >= n_ent) break;
-    const int ne = min(grab, n_ent - g0);
-    uint32_t my_ci = 0, my_enc = 0;
-    float4 my_a = make_float4(0.f, 0.f, 0.f, 0.f);
-    float2 my_b = make_float2(0.f, 0.f);
-    if (lane < ne) {
-      const unsigned long long e = fetch(g0 + lane);
-      my_ci = (uint32_t)e;
-      my_enc = (uint32_t)(e >> 32);
-      my_a = v.basis_a[my_ci];
-      my_b = v.basis_b[my_ci];
-    }
-    int qn = 0;
-    for (int k = 0; k < ne; ++k) {
-      const uint32_t enc = __shfl_sync(0xFFFFFFFFu, my_enc, k);
-      float4 ba;
-      float2 bb;
-      ba.x = __shfl_sync(0xFFFFFFFFu, my_a.x, k);
-      ba.y = __shfl_sync(0xFFFFFFFFu, my_a.y, k);
-      ba.z = __shfl_sync(0xFFFFFFFFu, my_a.z, k);
-      ba.w = __shfl_sync(0xFFFFFFFFu, my_a.w, k);
-      bb.x = __shfl_sync(0xFFFFFFFFu, my_b.x, k);
-      bb.y = __shfl_sync(0xFFFFFFFFu, my_b.y, k);
-      const uint32_t local_k = (uint32_t)k << 16;
-      const int start = (int)(enc & 0xFFFFu), len = (int)(enc >> 16);
-      const uint32_t tp_s = tab_s + 8u * (uint32_t)start;
-#if RV_PACK  // tab_s = table + 16*lane (packed steps); the scalar tail reads pair start + lane
-      const uint32_t tp1_s = tp_s - 8u * (uint32_t)lane - 4u * (uint32_t)(lane & 1);
-#endif
-      // NP pairs per lane per step (32*NP consecutive pairs per warp); ranges are 32-aligned:
-      // 64-pair steps while they fit, then one 32-pair tail step
-      auto step = [&](int k0, auto np_tag) {
-        constexpr int NP = decltype(np_tag)::value;
-        bool flag[NP];
-        uint32_t addr[NP];
-        uint32_t relp[NP];
-        // pair of (lane, h): packed steps walk adjacent pairs k0 + 2*lane + h, the others k0 + 32*h + lane
-        constexpr bool kPacked = RV_PACK && NP == 2;
-        if constexpr (kPacked) {
-          float4 t4;
-          asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-              : "=f"(t4.x), "=f"(t4.y), "=f"(t4.z), "=f"(t4.w)
-              : "r"(tp_s + 8u * (uint32_t)k0));
-          f32_cell2<kClamp, kS>(geo, ba, bb, t4, relp, flag);
-        }
-#pragma unroll
-        for (int h = 0; h < NP; ++h) {
-          float2 t;
-          if constexpr (!kPacked) {
-#if RV_PACK  // scalar (tail) step over the packed layout: lane's pair k0 + lane
-            const uint32_t a1 = tp1_s + 8u * (uint32_t)(k0 + 32 * h);
-            t = make_float2(lds_f1(a1), lds_f1(a1 + 8u));
-#else
-            t = lds_f2(tp_s + 8u * (uint32_t)(k0 + 32 * h));
-#endif
-            relp[h] = f32_cell<kClamp, kS>(geo, ba, bb, t, &flag[h]);
-          }
-          const uint32_t rel = relp[h];
-          // deposit even if flagged: the exact path undoes it (no select on the flag here)
-#if RV_PRED
-          addr[h] = rel;
-#else
-          addr[h] = tile_s + 4u * umin(rel, sink_rel);
-#endif
-        }
-#pragma unroll
-        for (int h = 0; h < NP; ++h) {
-#if RV_PRED
-          asm volatile("{\n\t.reg .pred q;\n\tsetp.lt.u32 q, %1, %2;\n\t@q red.shared.add.u32 [%0], %3;\n\t}" ::"r"(
-                           tile_s + 4u * addr[h]),
-                       "r"(addr[h]), "r"(tile_cells), "r"(vote2));
-#else
-          red_shared(addr[h], vote2);
-#endif
-        }
-        bool any = false;
-#pragma unroll
-        for (int h = 0; h < NP; ++h) any |= flag[h];
-        if (__any_sync(0xFFFFFFFFu, any)) {  // cold: queue for the exact f64 path
-#pragma unroll
-          for (int h = 0; h < NP; ++h) {
-            const unsigned fm = __ballot_sync(0xFFFFFFFFu, flag[h]);
-            if (flag[h]) {
-              int pair = kPacked ? start + k0 + 2 * lane + h : start + k0 + 32 * h + lane;
-              if (pair >= M) pair -= M;
-              sts_u32(fbq_s + 4u * (uint32_t)(qn + __popc(fm & lt_mask)), local_k | (uint32_t)pair);
-            }
-            qn += __popc(fm);
-            my_fb += __popc(fm);
-            __syncwarp();
-            if (qn >= 32) {
-              fallback_pairs<kClamp, kS>(fc, geo, fbq_s, 32, my_ci, my_a, my_b, tab, tile, tile_cells, hb);
-              qn -= 32;
-              if (lane < qn) sts_u32(fbq_s + 4u * lane, lds_u32(fbq_s + 4u * (32 + lane)));
-              __syncwarp();
-            }
-          }
-        }
-      };
-      int k0 = 0;
-      if constexpr (RV_NP == 4) {
-#pragma unroll 1
-        for (; k0 + 128 <= len; k0 += 128) step(k0, std::integral_constant<int, 4>{});
-        if (k0 + 64 <= len) {
-          step(k0, std::integral_constant<int, 2>{});
-          k0 += 64;
-        }
-      } else {
-#pragma unroll kStepUnroll
-        for (; k0 + 64 <= len; k0 += 64) step(k0, std::integral_constant<int, 2>{});
-      }
-      if (k0 < len) step(k0, std::integral_constant<int, 1>{});
-    }
-    if (qn > 0) fallback_pairs<kClamp, kS>(fc, geo, fbq_s, qn, my_ci, my_a, my_b, tab, tile, tile_cells, hb);
-  }
-}
-
-// K2: persistent, one CTA per SM, 16 warps. A CTA owns one row band's u32 tile in shared
-// memory at a time. Warps grab 32 work entries at a time from the band's entry list (K1 appends
-// one entry per non-empty (constraint, band) pair range; lane k loads entry k and its f32 basis,
-// the warp then walks the entries, broadcasting each by shuffles); no CTA barrier per grab. When
-// the band is exhausted the CTA flushes its tile to a partial slot and steals the band with the
-// most remaining entries. Lanes walk 64 consecutive sample pairs per step of a range (32-aligned
-// lengths, table doubled so ranges never wrap). Pairs whose f32 cell is not provably the
-// reference cell are queued per warp and recomputed exactly in f64.
+// K2: persistent, one CTA per SM, 32 warps. A CTA owns one row band's u32 tile in shared memory
+// at a time. Warps grab up to 32 work entries at a time from the band's entry list (K1b appends
+// one entry per range of canonical samples of a constraint in the band; lane k loads entry k and
+// its f32 basis, the warp then walks the entries, broadcasting each by shuffles); no CTA barrier
+// per grab. A range is walked 64 samples per step, lane l taking the adjacent samples a+2l and
+// a+2l+1 (one LDS.128 of the packed table, f32x2 math); the first and last steps of a range are
+// masked where it starts odd or ends mid-step. Every sample deposits +2 (its twin lands in the same
+// cell unless flagged) -- out-of-band and masked samples into never-flushed tile rows or the lane's
+// sink word. Samples whose f32 cell is not provably the reference cell are queued per warp and
+// recomputed exactly in f64 with both twins. When the band is exhausted the CTA flushes its tile
+// (TMA bulk reduce-adds, or a partial slot) and steals the band with the most remaining entries.
+// Degenerate constraints (no clean canonical half circle) are voted sample by sample at the end.
 
 #ifdef RV_VOTE_TRACE  // dev instrumentation: per-CTA phase timestamps (globaltimer, ns)
 __device__ unsigned long long g_vtrace[2 * 65536];
@@ -756,22 +659,22 @@ template <bool kClamp, int kS>
 __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p, VoteBuffers b, int64_t n) {
   extern __shared__ uint4 smem_raw[];
   uint32_t* tile = reinterpret_cast<uint32_t*>(smem_raw);
-  // [tile_words] tile, [32] per-lane sink words, table, fallback queues
-  float2* tab = reinterpret_cast<float2*>(tile + ((p.tile_words + 32 + 3) & ~size_t(3)));
-  const int M = p.halfJ;
-  uint32_t* fbq_all = reinterpret_cast<uint32_t*>(tab + 2 * M + 64);
+  // [tile_words] tile, [32] per-lane sink words, packed table (J/2 + 32 float4), fallback queues
+  float4* tab = reinterpret_cast<float4*>(tile + ((p.tile_words + 32 + 3) & ~size_t(3)));
+  const int M = p.halfJ, J = p.J;
+  uint32_t* fbq_all = reinterpret_cast<uint32_t*>(tab + M + 32);
   __shared__ int s_band, s_slot;
+  __shared__ ColdCtx s_cold;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t fbq_s = (uint32_t)__cvta_generic_to_shared(fbq_all + warp * kFbqCap);  // this warp's queue
-#if RV_PACK  // pair p of the doubled table lives in float4 p/2 = {cos_2q, cos_2q+1, sin_2q, sin_2q+1}
   for (int q = tid; q < M + 32; q += blockDim.x) {
-    const float2 e = b.table32[(2 * q) % M], o = b.table32[(2 * q + 1) % M];
-    reinterpret_cast<float4*>(tab)[q] = make_float4(e.x, o.x, e.y, o.y);
+    int j0 = 2 * q, j1 = 2 * q + 1;
+    j0 = j0 >= J ? j0 - J : j0;
+    j1 = j1 >= J ? j1 - J : j1;
+    const float2 e = b.table32[j0], o = b.table32[j1];
+    tab[q] = make_float4(e.x, o.x, e.y, o.y);
   }
-#else
-  for (int k = tid; k < 2 * M + 64; k += blockDim.x) tab[k] = b.table32[k % M];
-#endif
 
   if (tid == 0) {  // initial band: CTAs split across bands in proportion to planned work
     unsigned long long total = 0;
@@ -789,6 +692,21 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
       }
     }
     s_band = band;
+    set_cold_band(s_cold, p, band);
+    s_cold.zx = b.zx;
+    s_cold.zy = b.zy;
+    s_cold.zz = b.zz;
+    s_cold.table64 = b.table64;
+    s_cold.basis_a = b.basis_a;
+    s_cold.basis_b = b.basis_b;
+    s_cold.grid = b.grid;
+    s_cold.E = p.E;
+    s_cold.inv_cell = p.inv_cell;
+    s_cold.G = p.G;
+    s_cold.W = p.W;
+    s_cold.c_min = p.c_min;
+    s_cold.J = p.J;
+    s_cold.M = p.halfJ;
   }
   vtrace(0, 0);
   for (size_t k = tid; k < p.tile_words; k += blockDim.x) tile[k] = 0u;
@@ -796,8 +714,9 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
   vtrace(1, s_band);
   unsigned int my_fb = 0;
   unsigned lt_mask = (1u << lane) - 1u;
-  // per-lane table address (shared window): loaded by ld.shared below
-  uint32_t tab_s = (uint32_t)__cvta_generic_to_shared(tab) + (RV_PACK ? 16u : 8u) * (uint32_t)lane;
+  // per-lane table address (shared window): lane l's float4 of a step at even sample a is
+  // tab_s + 8 a (tab_s = table + 16 l)
+  uint32_t tab_s = (uint32_t)__cvta_generic_to_shared(tab) + 16u * (uint32_t)lane;
   asm volatile("" : "+r"(lt_mask), "+r"(tab_s), "+r"(fbq_s));
   // opaque to the optimizer: otherwise the shared-window base is rematerialised every step
   uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(tile);
@@ -806,29 +725,18 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
   uint32_t sink_rel = (uint32_t)p.tile_words + (uint32_t)lane;
   uint32_t vote2 = 2u;
   asm volatile("" : "+r"(tile_s), "+r"(sink_rel), "+r"(vote2));
+  const f32x2 one2 = pk2(1.f, 1.f);
   const float CMf = p.CMf;
   const int W = p.W, G = p.G;
   const int S = p.frac_shift;
   const uint32_t fmask = p.frac_mask;
-  FbCtx fc;
-  fc.zx = b.zx;
-  fc.zy = b.zy;
-  fc.zz = b.zz;
-  fc.table64 = b.table64;
-  fc.grid = b.grid;
-  fc.E = p.E;
-  fc.inv_cell = p.inv_cell;
-  fc.G = G;
-  fc.halfJ = M;
-  fc.c_min = p.c_min;
-  fc.W = W;
 
   for (;;) {
-    const int band = s_band;
+    // REDUX broadcasts (uniform-register results): the band, its entry count and each grab offset
+    // are provably warp-uniform, so the vote loops carry no divergence checks
+    const int band = __reduce_max_sync(0xFFFFFFFFu, s_band);
     if (band < 0) break;
     const int r0 = p.band_r0[band], hb = p.band_r0[band + 1] - r0;
-    fc.own_lo = band == 0 ? 0 : r0;
-    fc.own_hi = band == p.n_bands - 1 ? G : r0 + hb;
     const int row_off = p.magic_hi + r0;      // row_local = (bits_y >> S) - row_off
     const int col_off = p.magic_hi + p.c_min; // col_local = (bits_x >> S) - col_off
     const uint32_t lin_off = (uint32_t)row_off * (uint32_t)W + (uint32_t)col_off;
@@ -844,14 +752,145 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     geo.r0 = r0;
     geo.c_min = p.c_min;
     const unsigned long long* ebase = b.entries + (int64_t)band * b.entry_cap;
-    const int n_ent = b.entry_count[band];
+    const int n_ent = __reduce_max_sync(0xFFFFFFFFu, b.entry_count[band]);
     int* counter = &b.counters[1 + band];
     // grab size: 32 entries when every warp of the launch still gets several grabs, smaller for
     // small problems (otherwise a handful of warps would walk all entries while the rest idle)
     const int per = (int)(((long long)gridDim.x * (kVoteThreads / 32) * 4) / p.n_bands);
     const int grab = max(1, min(32, n_ent / max(per, 1)));
-    VoteCtx v{tab, tab_s, tile, tile_s, sink_rel, vote2, fbq_s, lt_mask, M, tile_cells, hb, b.basis_a, b.basis_b, grab};
-    vote_entries<kClamp, kS>(v, geo, fc, [&](int j) { return __ldcs(ebase + j); }, n_ent, counter, my_fb);
+    // One flat loop over (entry, step): a new entry is set up when the current one has no steps
+    // left (a uniform branch), so loop-invariant state stays in registers across entries.
+    // Entries are fetched in per-warp grabs of up to 32 (lane k holds entry k); flagged samples
+    // are queued per warp and the queue is drained before every new grab (it names grab entries).
+    uint32_t my_ci = 0, my_enc = 0;
+    int k = 0, ne = 0, qn = 0, left = 0;
+    uint32_t tp = 0;
+    float4 ba = make_float4(0.f, 0.f, 0.f, 0.f);
+    float2 bb = make_float2(0.f, 0.f);
+    // one step: samples a + 2 lane + {0, 1} (a = the step's even first sample, recovered from the
+    // table address tp); masked steps drop samples outside [mstart, mstart + mlen)
+    auto step = [&](uint32_t tpa, bool masked, int kk, int mstart, int mlen) {
+      float4 t4;
+      asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(t4.x), "=f"(t4.y), "=f"(t4.z), "=f"(t4.w) : "r"(tpa));
+      uint32_t rel[2];
+      bool flag[2];
+      f32_cell2<kClamp, kS>(geo, ba, bb, t4, one2, rel, flag);
+      if (masked) {
+        const int a = (int)((tpa - tab_s) >> 3);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const bool ok = (uint32_t)(a + 2 * lane + h - mstart) < (uint32_t)mlen;
+          rel[h] = ok ? rel[h] : 0xFFFFFFFFu;
+          flag[h] = flag[h] && ok;
+        }
+      }
+      // deposit even if flagged: the exact path undoes it (no select on the flag here)
+      red_shared(tile_s + 4u * umin(rel[0], sink_rel), vote2);
+      red_shared(tile_s + 4u * umin(rel[1], sink_rel), vote2);
+      if (__any_sync(0xFFFFFFFFu, flag[0] | flag[1])) {  // cold: queue for the exact f64 path
+        const uint32_t j = (uint32_t)((tpa - tab_s) >> 3) + 2u * lane;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const unsigned fm = __ballot_sync(0xFFFFFFFFu, flag[h]);
+          if (flag[h]) sts_u32(fbq_s + 4u * (uint32_t)(qn + __popc(fm & lt_mask)), ((uint32_t)kk << 16) | (j + h));
+          qn += __popc(fm);
+          my_fb += __popc(fm);
+          __syncwarp();
+          if (qn >= 32) {
+            fallback_samples<kClamp, kS>(&s_cold, geo, fbq_s, 32, my_ci, tab, tile);
+            qn -= 32;
+            if (lane < qn) sts_u32(fbq_s + 4u * lane, lds_u32(fbq_s + 4u * (32 + lane)));
+            __syncwarp();
+          }
+        }
+      }
+    };
+#if !RV_FLAT
+    // nested variant: grab loop / entry loop / step loop
+    for (;;) {
+      int g0 = 0;
+      if (lane == 0) g0 = atomicAdd(counter, grab);
+      g0 = __reduce_max_sync(0xFFFFFFFFu, g0);
+      if (g0 >= n_ent) break;
+      ne = min(grab, n_ent - g0);
+      my_ci = 0;
+      my_enc = 0;
+      if (lane < ne) {
+        const unsigned long long e = __ldcs(ebase + g0 + lane);
+        my_ci = (uint32_t)e;
+        my_enc = (uint32_t)(e >> 32);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(b.basis_a + my_ci));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(b.basis_b + my_ci));
+      }
+      qn = 0;
+      for (int kk = 0; kk < ne; ++kk) {
+        const uint32_t enc = __reduce_max_sync(0xFFFFFFFFu, lane == kk ? my_enc : 0u);
+        const uint32_t cik = __reduce_max_sync(0xFFFFFFFFu, lane == kk ? my_ci : 0u);
+        ba = __ldg(b.basis_a + cik);
+        bb = __ldg(b.basis_b + cik);
+        const int start = (int)(enc & 0xFFFFu), len = (int)(enc >> 16);
+        if ((start & 1) | (len & 63)) {  // rare: a range the planner could not align
+          const int a0 = start & ~1;
+          const int nst = (start + len - a0 + 63) >> 6;
+          uint32_t tpm = tab_s + 8u * (uint32_t)a0;
+#pragma unroll 1
+          for (int q = 0; q < nst; ++q, tpm += 512u) step(tpm, true, kk, start, len);
+          continue;
+        }
+        uint32_t tpf = tab_s + 8u * (uint32_t)start;
+#pragma unroll 1
+        for (int r = len >> 6; r > 0; --r, tpf += 512u) step(tpf, false, kk, 0, 0);
+      }
+      if (qn > 0) fallback_samples<kClamp, kS>(&s_cold, geo, fbq_s, qn, my_ci, tab, tile);
+    }
+#else
+    int kcur = 0;
+    for (;;) {
+      if (left == 0) {  // next entry (warp-uniform)
+        if (k == ne) {
+          if (qn > 0) fallback_samples<kClamp, kS>(&s_cold, geo, fbq_s, qn, my_ci, tab, tile);
+          qn = 0;
+          int g0 = 0;
+          if (lane == 0) g0 = atomicAdd(counter, grab);
+          // REDUX broadcasts (uniform-register results): everything derived from them is provably
+          // warp-uniform, so the loop carries no divergence checks around its votes
+          g0 = __reduce_max_sync(0xFFFFFFFFu, g0);
+          if (g0 >= n_ent) break;
+          ne = min(grab, n_ent - g0);
+          k = 0;
+          my_ci = 0;
+          my_enc = 0;
+          if (lane < ne) {
+            const unsigned long long e = __ldcs(ebase + g0 + lane);
+            my_ci = (uint32_t)e;
+            my_enc = (uint32_t)(e >> 32);
+            // warm L1 with this entry's basis: the warp reads it back as one broadcast load
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(b.basis_a + my_ci));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(b.basis_b + my_ci));
+          }
+        }
+        const uint32_t enc = __reduce_max_sync(0xFFFFFFFFu, lane == k ? my_enc : 0u);
+        const uint32_t cik = __reduce_max_sync(0xFFFFFFFFu, lane == k ? my_ci : 0u);
+        ba = __ldg(b.basis_a + cik);
+        bb = __ldg(b.basis_b + cik);
+        kcur = k++;
+        const int start = (int)(enc & 0xFFFFu), len = (int)(enc >> 16);
+        if ((start & 1) | (len & 63)) {  // rare: a range the planner could not align
+          const int a0 = start & ~1;
+          const int nst = (start + len - a0 + 63) >> 6;
+          uint32_t tpm = tab_s + 8u * (uint32_t)a0;
+#pragma unroll 1
+          for (int q = 0; q < nst; ++q, tpm += 512u) step(tpm, true, kcur, start, len);
+          continue;
+        }
+        tp = tab_s + 8u * (uint32_t)start;
+        left = len >> 6;
+      }
+      step(tp, false, kcur, 0, 0);
+      tp += 512u;
+      --left;
+    }
+#endif
     // band exhausted for this CTA: flush the tile to a partial slot, steal the next band
     __syncthreads();
     vtrace(2, band);
@@ -887,6 +926,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
         }
       }
       s_band = best;
+      if (best >= 0) set_cold_band(s_cold, p, best);
     }
     __syncthreads();
     const int slot = s_slot;
@@ -908,6 +948,30 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     __syncthreads();
   }
   vtrace(4, 0);
+  // degenerate constraints (planner list): one warp per constraint, lanes over all J samples,
+  // exact f64 with the reference's per-sample hemisphere decision, global atomics
+  const int nd = b.counters[kDegenCount];
+  if (nd > 0) {
+    VotePlan p1;
+    p1.E = p.E;
+    p1.inv_cell = p.inv_cell;
+    p1.G = G;
+    for (;;) {
+      int d = 0;
+      if (lane == 0) d = atomicAdd(&b.counters[kDegenGrab], 1);
+      d = __shfl_sync(0xFFFFFFFFu, d, 0);
+      if (d >= nd) break;
+      const int ci = b.degen[d];
+      double a1[3], a2[3];
+      exact_basis(b.zx[ci], b.zy[ci], b.zz[ci], a1, a2);
+      for (int j = lane; j < J; j += 32) {
+        const double2 cs = b.table64[j];
+        int row, col;
+        exact_sample(a1, a2, cs.x, cs.y, p1, &row, &col);
+        atomicAdd(&b.grid[(size_t)row * G + col], 1u);
+      }
+    }
+  }
   if (p.bulk && warp == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // flushes landed
   if (lane == 0 && my_fb) atomicAdd(&b.stats[1], (unsigned long long)my_fb);
 }

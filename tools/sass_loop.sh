@@ -1,6 +1,7 @@
 #!/bin/bash
-# dev: compile rv_vote.cu to a cubin (same flags as build.py) and print the hot step loop of
-# vote_banded_kernel<false,13>: instruction count between the loop head and its back-edge.
+# dev: compile rv_vote.cu to a cubin (same flags as build.py) and print the hot full-step loop of
+# vote_banded_kernel<false,13>: the innermost backward-branch loop that holds an LDS.128 and two
+# ATOMS.ADD (SHOW=1 lists it).
 set -e
 OUT=${OUT:-/tmp/rv_vote.cubin}
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++20 -Xcompiler -ffp-contract=off \
@@ -8,25 +9,33 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++20 -Xcompiler
 cuobjdump -sass $OUT | awk '/Function : .*vote_banded_kernelILb0ELi13E/{p=1;next} p&&/Function : /{p=0} p' \
   | sed 's@/\* 0x[0-9a-f]* \*/@@' | grep -v '^\s*$' > /tmp/v13.sass
 python3 - <<'PY'
-import re
+import re, os, collections
 L=[l.strip() for l in open('/tmp/v13.sass')]
-addr=[(int(m.group(1),16), l) for l in L for m in [re.match(r'/\*([0-9a-f]+)\*/\s*(.*)', l)] if m]
-# find ATOMS.ADD in the hot loop: first ATOMS.ADD; back-edge = first backward BRA after it targeting <= that
-first=[a for a,l in addr if 'ATOMS.ADD' in l][0]
-for a,l in addr:
-    m=re.search(r'BRA(\.U)? .*0x([0-9a-f]+)', l)
-    if m and a>first and int(m.group(2),16)<first:
-        head=int(m.group(2),16); back=a; break
-# hot path: head .. the predicated branch that skips the cold (flagged-pair) block, then its
-# target .. back-edge
-atoms=[a for a,l in addr if head<=a<=back and 'ATOMS.ADD' in l]
-skip=[(a,l) for a,l in addr if a>atoms[-1] and re.search(r'@!?P\d+\s+BRA', l)][0]
-tgt=int(re.search(r'0x([0-9a-f]+)', skip[1].split('BRA')[1]).group(1),16)
-hot=[(a,l) for a,l in addr if head<=a<=skip[0] or tgt<=a<=back]
-print(f"hot step loop: {len(hot)} instructions per iteration ({len(atoms)} ATOMS)")
-import collections
-c=collections.Counter(re.sub(r'^@!?U?P\w+\s+','',l.split('*/',1)[1].strip()).split()[0].split('.')[0] for a,l in hot)
+addr=[(int(m.group(1),16), m.group(2).rstrip(' ;')) for l in L for m in [re.match(r'/\*([0-9a-f]+)\*/\s*(.*)', l)] if m]
+idx={a:i for i,(a,_) in enumerate(addr)}
+best=None
+for i,(a,l) in enumerate(addr):
+    m=re.search(r'BRA(?:\.U)?\s+(?:!?U?P\d+,\s*)?(0x[0-9a-f]+)', l)
+    if not m: continue
+    t=int(m.group(1),16)
+    if t>=a or t not in idx: continue
+    body=addr[idx[t]:i+1]
+    if sum('ATOMS.ADD RZ' in x for _,x in body)==2 and any('LDS.128' in x for _,x in body):
+        if best is None or len(body)<len(best): best=body
+if best is None:
+    print("hot loop not found"); raise SystemExit
+# exclude the cold block: from the first predicated forward branch after the last ATOMS to its target
+at=[k for k,(a,x) in enumerate(best) if 'ATOMS.ADD RZ' in x][-1]
+hot=best
+for k in range(at, len(best)):
+    m=re.search(r'@!?P\d+\s+BRA\s+(0x[0-9a-f]+)', best[k][1])
+    if m:
+        tgt=int(m.group(1),16)
+        hot=[x for x in best if x[0]<=best[k][0] or x[0]>=tgt]
+        break
+print(f"hot step loop: {len(hot)} instructions per iteration (loop body incl. cold block: {len(best)})")
+c=collections.Counter(re.sub(r'^@!?U?P\w+\s+','',x).split()[0].split('.')[0] for a,x in hot)
 print(dict(c.most_common()))
-if __import__('os').environ.get('SHOW'):
-    for a,l in hot: print(l)
+if os.environ.get('SHOW'):
+    for a,x in hot: print(f"  {a:#06x} {x}")
 PY
