@@ -40,9 +40,6 @@ namespace {
 constexpr float kPiF = 3.14159265358979323846f;
 constexpr float kTwoPiF = 6.28318530717958647692f;
 constexpr float kRcMin = 1e-3f;     // |c| amplitude below which a circle is treated as all-band
-#ifndef RV_FLAT
-#define RV_FLAT 0  // 1: one flat (entry, step) loop per band instead of nested entry / step loops
-#endif
 #ifndef RV_RED_GROUPS
 #define RV_RED_GROUPS 2
 #endif
@@ -78,6 +75,14 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // per-warp fallback queue in shared memory (32-bit shared-window addresses)
 __device__ __forceinline__ void sts_u32(uint32_t saddr, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u2(uint32_t saddr, uint32_t a, uint32_t b) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(saddr), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ uint2 lds_u2(uint32_t saddr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(saddr) : "memory");
+  return v;
 }
 __device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
   uint32_t v;
@@ -578,16 +583,15 @@ __device__ __forceinline__ void set_cold_band(ColdCtx& c, const VotePlan& p, int
 #endif
 template <bool kClamp, int kS>
 __device__ RV_FB_ATTR void fallback_samples(const ColdCtx* cc_s, const F32Geom& g, uint32_t q_s, int count,
-                                                 uint32_t my_ci, const float4* tab, uint32_t* tile) {
+                                            const float4* tab, uint32_t* tile) {
   const volatile ColdCtx& f = *cc_s;
   const int lane = threadIdx.x & 31;
-  const uint32_t e = lane < count ? lds_u32(q_s + 4u * lane) : 0u;
-  const int k = (int)(e >> 16) & 31;  // entry index within the warp's grab
-  const uint32_t ci = __shfl_sync(0xFFFFFFFFu, my_ci, k);
+  const uint2 e = lane < count ? lds_u2(q_s + 8u * lane) : make_uint2(0u, 0u);  // (constraint, sample)
+  const uint32_t ci = e.x;
   if (lane < count) {
     const float4 ba = __ldg(f.basis_a + ci);
     const float2 bb = __ldg(f.basis_b + ci);
-    const int j = (int)(e & 0xFFFFu);
+    const int j = (int)e.y;
     bool fl;
     const int r0 = f.r0, hb = f.hb, own_lo = f.own_lo, own_hi = f.own_hi, W = f.W, G = f.G, c_min = f.c_min;
     const uint32_t rel = f32_cell<kClamp, kS>(g, ba, bb, tab_sample(tab, j), &fl);
@@ -758,18 +762,15 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     // small problems (otherwise a handful of warps would walk all entries while the rest idle)
     const int per = (int)(((long long)gridDim.x * (kVoteThreads / 32) * 4) / p.n_bands);
     const int grab = max(1, min(32, n_ent / max(per, 1)));
-    // One flat loop over (entry, step): a new entry is set up when the current one has no steps
-    // left (a uniform branch), so loop-invariant state stays in registers across entries.
     // Entries are fetched in per-warp grabs of up to 32 (lane k holds entry k); flagged samples
-    // are queued per warp and the queue is drained before every new grab (it names grab entries).
+    // are queued per warp as (constraint, sample) and drained in batches of up to 32.
     uint32_t my_ci = 0, my_enc = 0;
-    int k = 0, ne = 0, qn = 0, left = 0;
-    uint32_t tp = 0;
+    int ne = 0, qn = 0;
     float4 ba = make_float4(0.f, 0.f, 0.f, 0.f);
     float2 bb = make_float2(0.f, 0.f);
     // one step: samples a + 2 lane + {0, 1} (a = the step's even first sample, recovered from the
     // table address tp); masked steps drop samples outside [mstart, mstart + mlen)
-    auto step = [&](uint32_t tpa, bool masked, int kk, int mstart, int mlen) {
+    auto step = [&](uint32_t tpa, bool masked, uint32_t cik, int mstart, int mlen) {
       float4 t4;
       asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(t4.x), "=f"(t4.y), "=f"(t4.z), "=f"(t4.w) : "r"(tpa));
       uint32_t rel[2];
@@ -788,28 +789,30 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
       red_shared(tile_s + 4u * umin(rel[0], sink_rel), vote2);
       red_shared(tile_s + 4u * umin(rel[1], sink_rel), vote2);
       if (__any_sync(0xFFFFFFFFu, flag[0] | flag[1])) {  // cold: queue for the exact f64 path
+        // queue entries are (constraint, sample), so the queue outlives the grab; it is drained
+        // before it would pass 32 entries (one exact-path batch = one sample per lane)
         const uint32_t j = (uint32_t)((tpa - tab_s) >> 3) + 2u * lane;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const unsigned fm = __ballot_sync(0xFFFFFFFFu, flag[h]);
-          if (flag[h]) sts_u32(fbq_s + 4u * (uint32_t)(qn + __popc(fm & lt_mask)), ((uint32_t)kk << 16) | (j + h));
-          qn += __popc(fm);
-          my_fb += __popc(fm);
-          __syncwarp();
-          if (qn >= 32) {
-            fallback_samples<kClamp, kS>(&s_cold, geo, fbq_s, 32, my_ci, tab, tile);
-            qn -= 32;
-            if (lane < qn) sts_u32(fbq_s + 4u * lane, lds_u32(fbq_s + 4u * (32 + lane)));
-            __syncwarp();
+          const int c = __popc(fm);
+          if (qn + c > 32) {
+            fallback_samples<kClamp, kS>(&s_cold, geo, fbq_s, qn, tab, tile);
+            qn = 0;
           }
+          if (flag[h]) sts_u2(fbq_s + 8u * (uint32_t)(qn + __popc(fm & lt_mask)), cik, j + h);
+          qn += c;
+          my_fb += c;
+          __syncwarp();
         }
       }
     };
-#if !RV_FLAT
-    // nested variant: grab loop / entry loop / step loop
+    // grab loop / entry loop / step loop
     for (;;) {
       int g0 = 0;
       if (lane == 0) g0 = atomicAdd(counter, grab);
+      // REDUX broadcasts (uniform-register results): everything derived from them is provably
+      // warp-uniform, so the loops carry no divergence checks around their votes
       g0 = __reduce_max_sync(0xFFFFFFFFu, g0);
       if (g0 >= n_ent) break;
       ne = min(grab, n_ent - g0);
@@ -819,10 +822,10 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
         const unsigned long long e = __ldcs(ebase + g0 + lane);
         my_ci = (uint32_t)e;
         my_enc = (uint32_t)(e >> 32);
+        // warm L1 with this entry's basis: the warp reads it back as one broadcast load
         asm volatile("prefetch.global.L1 [%0];" ::"l"(b.basis_a + my_ci));
         asm volatile("prefetch.global.L1 [%0];" ::"l"(b.basis_b + my_ci));
       }
-      qn = 0;
       for (int kk = 0; kk < ne; ++kk) {
         const uint32_t enc = __reduce_max_sync(0xFFFFFFFFu, lane == kk ? my_enc : 0u);
         const uint32_t cik = __reduce_max_sync(0xFFFFFFFFu, lane == kk ? my_ci : 0u);
@@ -834,63 +837,15 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
           const int nst = (start + len - a0 + 63) >> 6;
           uint32_t tpm = tab_s + 8u * (uint32_t)a0;
 #pragma unroll 1
-          for (int q = 0; q < nst; ++q, tpm += 512u) step(tpm, true, kk, start, len);
+          for (int q = 0; q < nst; ++q, tpm += 512u) step(tpm, true, cik, start, len);
           continue;
         }
         uint32_t tpf = tab_s + 8u * (uint32_t)start;
 #pragma unroll 1
-        for (int r = len >> 6; r > 0; --r, tpf += 512u) step(tpf, false, kk, 0, 0);
+        for (int r = len >> 6; r > 0; --r, tpf += 512u) step(tpf, false, cik, 0, 0);
       }
-      if (qn > 0) fallback_samples<kClamp, kS>(&s_cold, geo, fbq_s, qn, my_ci, tab, tile);
     }
-#else
-    int kcur = 0;
-    for (;;) {
-      if (left == 0) {  // next entry (warp-uniform)
-        if (k == ne) {
-          if (qn > 0) fallback_samples<kClamp, kS>(&s_cold, geo, fbq_s, qn, my_ci, tab, tile);
-          qn = 0;
-          int g0 = 0;
-          if (lane == 0) g0 = atomicAdd(counter, grab);
-          // REDUX broadcasts (uniform-register results): everything derived from them is provably
-          // warp-uniform, so the loop carries no divergence checks around its votes
-          g0 = __reduce_max_sync(0xFFFFFFFFu, g0);
-          if (g0 >= n_ent) break;
-          ne = min(grab, n_ent - g0);
-          k = 0;
-          my_ci = 0;
-          my_enc = 0;
-          if (lane < ne) {
-            const unsigned long long e = __ldcs(ebase + g0 + lane);
-            my_ci = (uint32_t)e;
-            my_enc = (uint32_t)(e >> 32);
-            // warm L1 with this entry's basis: the warp reads it back as one broadcast load
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(b.basis_a + my_ci));
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(b.basis_b + my_ci));
-          }
-        }
-        const uint32_t enc = __reduce_max_sync(0xFFFFFFFFu, lane == k ? my_enc : 0u);
-        const uint32_t cik = __reduce_max_sync(0xFFFFFFFFu, lane == k ? my_ci : 0u);
-        ba = __ldg(b.basis_a + cik);
-        bb = __ldg(b.basis_b + cik);
-        kcur = k++;
-        const int start = (int)(enc & 0xFFFFu), len = (int)(enc >> 16);
-        if ((start & 1) | (len & 63)) {  // rare: a range the planner could not align
-          const int a0 = start & ~1;
-          const int nst = (start + len - a0 + 63) >> 6;
-          uint32_t tpm = tab_s + 8u * (uint32_t)a0;
-#pragma unroll 1
-          for (int q = 0; q < nst; ++q, tpm += 512u) step(tpm, true, kcur, start, len);
-          continue;
-        }
-        tp = tab_s + 8u * (uint32_t)start;
-        left = len >> 6;
-      }
-      step(tp, false, kcur, 0, 0);
-      tp += 512u;
-      --left;
-    }
-#endif
+    if (qn > 0) fallback_samples<kClamp, kS>(&s_cold, geo, fbq_s, qn, tab, tile);  // before the flush
     // band exhausted for this CTA: flush the tile to a partial slot, steal the next band
     __syncthreads();
     vtrace(2, band);
