@@ -90,6 +90,45 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
   return v;
 }
 
+// f32 evaluation of one canonical sample: tile-relative linear cell index `rel` (>= tile_cells: not
+// this band's tile) and whether the f32 cell is not provably the reference cell. The sample is
+// canonical (c <= 0 in the reference's own arithmetic, decided by the planner), so there is no
+// hemisphere logic: c' = 1 - c from two FFMAs off the constant 1, r = rcp.approx(c'). Shared by the
+// hot loop (packed, f32_cell2) and the exact path (which undoes the hot loop's deposit), so both
+// see identical values.
+struct F32Geom {
+  float CMf;
+  int S;
+  uint32_t fmask;
+  uint32_t W;
+  uint32_t lin_off;  // non-clamp: (magic_hi + r0) * W + magic_hi + c_min
+  int magic_hi, G, r0, c_min;
+};
+template <bool kClamp, int kS>
+__device__ __forceinline__ uint32_t cell_of_bits(const F32Geom& g, uint32_t bx, uint32_t by, bool* flag) {
+  const int S = kS ? kS : g.S;
+  *flag = ((bx & g.fmask) == 0u) | ((by & g.fmask) == 0u);
+  // the column is always inside [c_min, c_min+W) (|X| <= 1 < extent, or clamped), so one
+  // unsigned range test on the linear index is the band-ownership test
+  if (kClamp) {
+    const int row = min(max((int)(by >> S) - g.magic_hi, 0), g.G - 1) - g.r0;
+    const int col = min(max((int)(bx >> S) - g.magic_hi, 0), g.G - 1) - g.c_min;
+    return (uint32_t)(row * (int)g.W + col);
+  }
+  return (by >> S) * g.W + (bx >> S) - g.lin_off;
+}
+// ba = (K a1x, K a1y, -a1z, K a2x), bb = (K a2y, -a2z), t = (cos, sin) of the sample
+template <bool kClamp, int kS>
+__device__ __forceinline__ uint32_t f32_cell(const F32Geom& g, float4 ba, float2 bb, float2 t, bool* flag) {
+  const float xk = fmaf(ba.w, t.y, ba.x * t.x);
+  const float yk = fmaf(bb.x, t.y, ba.y * t.x);
+  const float cp = fmaf(bb.y, t.y, fmaf(ba.z, t.x, 1.f));
+  const float r = rcp_approx(cp);
+  const uint32_t bx = (uint32_t)__float_as_int(fmaf(xk, r, g.CMf));
+  const uint32_t by = (uint32_t)__float_as_int(fmaf(yk, r, g.CMf));
+  return cell_of_bits<kClamp, kS>(g, bx, by, flag);
+}
+
 // ---- K1b: band plan --------------------------------------------------------------------
 // Cheap trig for the planner: errors (~1e-5 rad) are far below the 2-pair padding (6e-3 rad at
 // J=2048); coverage only has to be a superset, ownership is decided exactly per sample.
@@ -397,8 +436,31 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
       }
       // the vote walks adjacent sample pairs from even indices: an odd first / even last sample of
       // the arc is deposited here exactly (both twins), so every entry can start even and end odd
+      // (the f32 filter first, exactly as the vote evaluates it: an unflagged cell is the
+      // reference cell of both twins; a flagged pair goes the exact way)
+      const float4 fa = make_float4(__double2float_rn(a1[0] * K), __double2float_rn(a1[1] * K),
+                                    __double2float_rn(-a1[2]), __double2float_rn(a2[0] * K));
+      const float2 fb = make_float2(__double2float_rn(a2[1] * K), __double2float_rn(-a2[2]));
+      F32Geom gg;
+      gg.CMf = p.CMf;
+      gg.S = p.frac_shift;
+      gg.fmask = p.frac_mask;
+      gg.W = (uint32_t)p.G;
+      gg.lin_off = (uint32_t)p.magic_hi * (uint32_t)p.G + (uint32_t)p.magic_hi;
+      gg.magic_hi = p.magic_hi;
+      gg.G = p.G;
+      gg.r0 = 0;
+      gg.c_min = 0;
       auto exact_pair = [&](int j) {
-        const int q = (j >= J ? j - J : j) % M;
+        const int jj = j >= J ? j - J : j;
+        bool fl;
+        const uint32_t cell = p.clamp ? f32_cell<true, 0>(gg, fa, fb, b.table32[jj], &fl)
+                                      : f32_cell<false, 0>(gg, fa, fb, b.table32[jj], &fl);
+        if (!fl) {
+          atomicAdd(&b.grid[cell], 2u);
+          return;
+        }
+        const int q = jj % M;
         exact_global(a1, a2, b.table64, q, p, b.grid);
         exact_global(a1, a2, b.table64, q + M, p, b.grid);
       };
@@ -479,45 +541,6 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
 }
 
 // ---- K2 ------------------------------------------------------------------------------
-
-// f32 evaluation of one canonical sample: tile-relative linear cell index `rel` (>= tile_cells: not
-// this band's tile) and whether the f32 cell is not provably the reference cell. The sample is
-// canonical (c <= 0 in the reference's own arithmetic, decided by the planner), so there is no
-// hemisphere logic: c' = 1 - c from two FFMAs off the constant 1, r = rcp.approx(c'). Shared by the
-// hot loop (packed, f32_cell2) and the exact path (which undoes the hot loop's deposit), so both
-// see identical values.
-struct F32Geom {
-  float CMf;
-  int S;
-  uint32_t fmask;
-  uint32_t W;
-  uint32_t lin_off;  // non-clamp: (magic_hi + r0) * W + magic_hi + c_min
-  int magic_hi, G, r0, c_min;
-};
-template <bool kClamp, int kS>
-__device__ __forceinline__ uint32_t cell_of_bits(const F32Geom& g, uint32_t bx, uint32_t by, bool* flag) {
-  const int S = kS ? kS : g.S;
-  *flag = ((bx & g.fmask) == 0u) | ((by & g.fmask) == 0u);
-  // the column is always inside [c_min, c_min+W) (|X| <= 1 < extent, or clamped), so one
-  // unsigned range test on the linear index is the band-ownership test
-  if (kClamp) {
-    const int row = min(max((int)(by >> S) - g.magic_hi, 0), g.G - 1) - g.r0;
-    const int col = min(max((int)(bx >> S) - g.magic_hi, 0), g.G - 1) - g.c_min;
-    return (uint32_t)(row * (int)g.W + col);
-  }
-  return (by >> S) * g.W + (bx >> S) - g.lin_off;
-}
-// ba = (K a1x, K a1y, -a1z, K a2x), bb = (K a2y, -a2z), t = (cos, sin) of the sample
-template <bool kClamp, int kS>
-__device__ __forceinline__ uint32_t f32_cell(const F32Geom& g, float4 ba, float2 bb, float2 t, bool* flag) {
-  const float xk = fmaf(ba.w, t.y, ba.x * t.x);
-  const float yk = fmaf(bb.x, t.y, ba.y * t.x);
-  const float cp = fmaf(bb.y, t.y, fmaf(ba.z, t.x, 1.f));
-  const float r = rcp_approx(cp);
-  const uint32_t bx = (uint32_t)__float_as_int(fmaf(xk, r, g.CMf));
-  const uint32_t by = (uint32_t)__float_as_int(fmaf(yk, r, g.CMf));
-  return cell_of_bits<kClamp, kS>(g, bx, by, flag);
-}
 
 // Two adjacent samples of f32_cell at once, t = {cos_a, cos_b, sin_a, sin_b}: the same IEEE
 // operations in the same order, lane-parallel in f32x2 (sm_100 FMUL2/FFMA2), so each cell and
