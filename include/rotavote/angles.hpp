@@ -35,13 +35,12 @@ struct AngleHistogram {
 };
 
 namespace detail {
-inline std::vector<double> flatten(std::span<const Correspondence> c) {
-  std::vector<double> out(6 * c.size());
-  for (std::size_t i = 0; i < c.size(); ++i) {
-    to3(c[i].x, out.data() + 6 * i);
-    to3(c[i].y, out.data() + 6 * i + 3);
-  }
-  return out;
+// A span of Correspondence IS the C-ABI's n x 6 f64 row layout (Eigen::Vector3d holds 3 doubles,
+// no padding): it is passed straight through, no host copy.
+static_assert(sizeof(Vec3) == 3 * sizeof(double) && sizeof(Correspondence) == 6 * sizeof(double),
+              "Correspondence must be 6 contiguous doubles");
+inline const double* rows(std::span<const Correspondence> c) {
+  return c.empty() ? nullptr : reinterpret_cast<const double*>(c.data());
 }
 }  // namespace detail
 
@@ -63,10 +62,10 @@ inline AngleHistogram vote_angles(const Vec3& axis, std::span<const Corresponden
   h.raw_angles.resize(indices.size());
   double a[3];
   detail::to3(axis, a);
-  const std::vector<double> flat = detail::flatten(correspondences);
+  const double* flat = detail::rows(correspondences);
   std::vector<int32_t> idx(indices.begin(), indices.end());
   uint64_t contrib = 0, degen = 0;
-  detail::check(rv_vote_angles(detail::context(), a, flat.data(), static_cast<int64_t>(correspondences.size()),
+  detail::check(rv_vote_angles(detail::context(), a, flat, static_cast<int64_t>(correspondences.size()),
                                idx.data(), static_cast<int64_t>(idx.size()), bin_count, tau, h.bins.data(), &contrib,
                                &degen, h.raw_angles.data()));
   h.contributing = contrib;

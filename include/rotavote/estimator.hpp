@@ -83,12 +83,12 @@ inline RotationEstimate to_est(const rv_estimate& e, int model) {
 inline PreprocessResult preprocess(std::span<const Correspondence> correspondences, double tau_z, bool normalize = true) {
   PreprocessResult out;
   if (correspondences.empty()) return out;
-  const std::vector<double> flat = detail::flatten(correspondences);
+  const double* flat = detail::rows(correspondences);
   const std::size_t n = correspondences.size();
   std::vector<double> z(3 * n);
   std::vector<int32_t> kept(n), dropped(n);
   int64_t nk = 0, nd = 0;
-  detail::check(rv_preprocess(detail::context(), flat.data(), static_cast<int64_t>(n), tau_z, normalize ? 1 : 0,
+  detail::check(rv_preprocess(detail::context(), flat, static_cast<int64_t>(n), tau_z, normalize ? 1 : 0,
                               z.data(), kept.data(), dropped.data(), &nk, &nd));
   for (int64_t i = 0; i < nk; ++i) out.constraints.push_back(detail::from3(z.data() + 3 * i));
   out.kept.assign(kept.begin(), kept.begin() + nk);
@@ -125,22 +125,34 @@ inline std::uint32_t peak_vote_floor(const EstimatorConfig& cfg, std::size_t n_c
 
 inline RotationEstimate estimate_single(std::span<const Correspondence> correspondences, const EstimatorConfig& cfg) {
   if (correspondences.empty()) throw EmptyInput("no correspondences");
-  const std::vector<double> flat = detail::flatten(correspondences);
+  const double* flat = detail::rows(correspondences);
   const rv_config c = detail::to_c(cfg);
   rv_estimate e;
-  detail::check(rv_estimate_single(detail::context(), flat.data(), static_cast<int64_t>(correspondences.size()), &c, &e));
+  if (rv_multi* m = detail::multi()) {  // ROTAVOTE_DEVICES: sharded over several GPUs
+    detail::check_multi(rv_multi_estimate_single(m, flat, static_cast<int64_t>(correspondences.size()), &c, &e));
+    RotationEstimate out;
+    out.axis = detail::from3(e.axis);
+    out.angle = e.angle;
+    out.rotation = detail::from9(e.rotation);
+    out.axis_votes = e.axis_votes;
+    out.elapsed_s = e.elapsed_s;
+    out.inliers.resize(static_cast<std::size_t>(e.n_inliers));
+    detail::check_multi(rv_multi_result_inliers(m, out.inliers.data(), e.n_inliers));
+    return out;
+  }
+  detail::check(rv_estimate_single(detail::context(), flat, static_cast<int64_t>(correspondences.size()), &c, &e));
   return detail::to_est(e, 0);
 }
 
 inline std::vector<RotationEstimate> estimate_multi(std::span<const Correspondence> correspondences,
                                                     const EstimatorConfig& cfg) {
   if (correspondences.empty()) throw EmptyInput("no correspondences");
-  const std::vector<double> flat = detail::flatten(correspondences);
+  const double* flat = detail::rows(correspondences);
   const rv_config c = detail::to_c(cfg);
   const int cap = cfg.max_models > 0 ? cfg.max_models : 1;
   std::vector<rv_estimate> es(static_cast<std::size_t>(cap));
   int32_t nm = 0;
-  detail::check(rv_estimate_multi(detail::context(), flat.data(), static_cast<int64_t>(correspondences.size()), &c,
+  detail::check(rv_estimate_multi(detail::context(), flat, static_cast<int64_t>(correspondences.size()), &c,
                                   es.data(), cap, &nm));
   std::vector<RotationEstimate> out;
   for (int k = 0; k < nm && k < cap; ++k) out.push_back(detail::to_est(es[k], k));
@@ -153,12 +165,12 @@ inline std::vector<RotationEstimate> estimate_multi(std::span<const Corresponden
 inline std::vector<RotationEstimate> estimate_multi_onepass(std::span<const Correspondence> correspondences,
                                                             const EstimatorConfig& cfg) {
   if (correspondences.empty()) throw EmptyInput("no correspondences");
-  const std::vector<double> flat = detail::flatten(correspondences);
+  const double* flat = detail::rows(correspondences);
   const rv_config c = detail::to_c(cfg);
   const int cap = cfg.max_models > 0 ? cfg.max_models : 1;
   std::vector<rv_estimate> es(static_cast<std::size_t>(cap));
   int32_t nm = 0;
-  detail::check(rv_estimate_multi_onepass(detail::context(), flat.data(),
+  detail::check(rv_estimate_multi_onepass(detail::context(), flat,
                                           static_cast<int64_t>(correspondences.size()), &c, es.data(), cap, &nm));
   std::vector<RotationEstimate> out;
   for (int k = 0; k < nm && k < cap; ++k) out.push_back(detail::to_est(es[k], k));

@@ -85,11 +85,17 @@ inline void deposit_circle_votes(const Vec3& z, Accumulator2D& acc, int samples)
 
 inline Accumulator2D accumulate(std::span<const Vec3> constraints, int grid, double extent, int samples,
                                 int threads = 1) {
-  (void)threads;  // the device result is independent of host threads, like the reference's
+  (void)threads;  // the result is independent of host threads, like the reference's; the device
+                  // fan-out is ROTAVOTE_DEVICES (detail::multi)
   if (constraints.empty()) throw EmptyInput("no constraints to accumulate");
   Accumulator2D acc(grid, extent);
   std::vector<double> z(3 * constraints.size());
   for (std::size_t i = 0; i < constraints.size(); ++i) detail::to3(constraints[i], z.data() + 3 * i);
+  if (rv_multi* m = detail::multi()) {  // ROTAVOTE_DEVICES: chunks over several GPUs (voting.cpp:95-117)
+    detail::check_multi(rv_multi_accumulate(m, z.data(), static_cast<int64_t>(constraints.size()), grid, extent,
+                                            samples, acc.counts().data()));
+    return acc;
+  }
   detail::check(rv_accumulate(detail::context(), z.data(), static_cast<int64_t>(constraints.size()), grid, extent,
                               samples, acc.counts().data()));
   return acc;

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define RV_ABI_VERSION 3
+#define RV_ABI_VERSION 4
 
 typedef enum rv_status {
   RV_OK = 0,
@@ -179,6 +179,55 @@ rv_status rv_vote_shard(rv_context* ctx, const double* d_corrs_shard, int64_t n_
  * (the summed shard grids): preprocess, then peak / refine / angle / rescue as usual. */
 rv_status rv_estimate_single_prevoted(rv_context* ctx, const double* d_corrs, int64_t n, const rv_config* cfg,
                                       const uint32_t* d_grid, rv_estimate* out);
+
+/* ---- sharded finish steps ------------------------------------------------
+ * refine_loop / build_estimate (estimator.cpp:51-92) split so each rank (or device) works on its
+ * own shard and only small partials cross the interconnect. After rv_vote_shard on every shard
+ * and a sum of the shard grids:
+ *   rv_peak_start_axis   find_peaks(K=1) + estimate_from_peak's start axis (estimator.cpp:94-97)
+ *                        from the summed grid; *total = grid sum (exactness guard: N_kept * J)
+ *   rv_shard_classify    classify_inliers (estimator.cpp:287-297) of this shard into bitmask slot
+ *                        0/1, fused with the 6 scatter sums of refine_axis (:299-302) over the same
+ *                        inliers and "differs from the other slot" (refine_loop's next_inl == inl)
+ *   rv_axis_from_scatter refine_axis's 3x3 eigen-solve of the rank-ordered sum (RV_ERR_RANK_DEFICIENT)
+ *   rv_shard_inliers     the slot's inliers as ascending input indices + offset (host dst)
+ *   rv_shard_angle_hist  vote_angles (angles.cpp:46-68) of this shard's inliers (bins of this shard)
+ *   rv_shard_angle_sums  peak_angle's window sums (angles.cpp:70-90) of this shard's raw angles
+ *                        around the peak of the SUMMED histogram: {sum sin, sum cos}
+ * Concatenating the shard inlier lists in rank order reproduces the reference's ascending list. */
+rv_status rv_peak_start_axis(rv_context* ctx, const uint32_t* d_grid, const rv_config* cfg, double axis[3],
+                             uint32_t* votes, uint64_t* total);
+rv_status rv_shard_classify(rv_context* ctx, const double axis[3], double epsilon, int32_t slot, int32_t compare_prev,
+                            int64_t* count, double scatter[6], int32_t* differs);
+rv_status rv_axis_from_scatter(const double scatter[6], double axis[3]);
+rv_status rv_shard_inliers(rv_context* ctx, int32_t slot, int64_t offset, int32_t* dst, int64_t capacity,
+                           int64_t* count);
+rv_status rv_shard_angle_hist(rv_context* ctx, const double axis[3], const rv_config* cfg, uint32_t* bins,
+                              uint64_t* contributing);
+rv_status rv_shard_angle_sums(rv_context* ctx, const uint32_t* bins_total, const rv_config* cfg, double sums[2]);
+
+/* ---- multi-GPU in one process (reference: accumulate's chunked thread fan-out,
+ * voting.cpp:102-117) --------------------------------------------------------------------------
+ * rv_multi: one rv_context per listed device plus an NCCL communicator clique (ncclCommInitAll,
+ * NVLink/NVSwitch on a B200 box; NCCL is loaded at run time). estimate_single and accumulate on a
+ * multi context split the input into contiguous shards (one per device), vote each shard on its
+ * device, sum the u32 grids with one in-place ncclAllReduce (bit-identical to the single-device
+ * grid), and -- estimate_single -- run the sharded finish above (rank-ordered partial sums, the
+ * 3x3 solves on the host). Results equal the single-device path's; the rare rescue / identity /
+ * guard branches finish on device 0 from the summed grid. RV_ERR_NCCL if NCCL is unavailable. */
+typedef struct rv_multi rv_multi;
+rv_status rv_multi_create(const int32_t* devices, int32_t n_devices, rv_multi** out);
+void rv_multi_destroy(rv_multi* m);
+int32_t rv_multi_size(const rv_multi* m);
+const char* rv_multi_last_error(const rv_multi* m);
+/* the NCCL version the clique runs (e.g. 22709), 0 before rv_multi_create succeeded */
+int32_t rv_multi_nccl_version(const rv_multi* m);
+rv_status rv_multi_estimate_single(rv_multi* m, const double* corrs, int64_t n, const rv_config* cfg,
+                                   rv_estimate* out);
+rv_status rv_multi_result_inliers(rv_multi* m, int32_t* dst, int64_t capacity);
+/* accumulate (voting.hpp:64-65) of host constraints (n x 3), grid summed over the devices */
+rv_status rv_multi_accumulate(rv_multi* m, const double* z, int64_t n, int32_t grid, double extent, int32_t samples,
+                              uint32_t* counts_out);
 
 /* ---- CSV ingest ------------------------------------------
  * read_correspondences (io.hpp:11-13, io.cpp:66-101): CSV rows x0,x1,x2,y0,y1,y2 with an

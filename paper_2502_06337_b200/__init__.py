@@ -15,7 +15,7 @@ from dataclasses import dataclass, field, fields
 
 import numpy as np
 
-from . import errors
+from . import _native, errors
 from ._native import check, lib, rv_config, rv_estimate, rv_peak, rv_stage_times
 from .errors import (AllDegenerate, DegenerateProjection, EmptyFile, EmptyInput, Error, InvalidConfig,  # noqa: F401
                      IoError, NoConsensus, NoPeak, NoVotes, ParseError, PoleProximity, RankDeficient)
@@ -112,7 +112,12 @@ class Context:
         check(st, self.handle)
 
     def set_stream(self, stream_ptr: int | None) -> None:
-        self._check(self._lib.rv_context_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
+        """Run the context's work on `stream_ptr` (a cudaStream_t value, e.g. torch's
+        `current_stream().cuda_stream`; 0 = the legacy default stream), or on its own stream (None)."""
+        if stream_ptr is None:
+            self._check(self._lib.rv_context_set_stream(self.handle, None))
+        else:  # cudaStreamLegacy is the handle value 0x1 (a null handle would select the own stream)
+            self._check(self._lib.rv_context_set_stream(self.handle, C.c_void_p(stream_ptr or 1)))
 
     def enable_timing(self, on: bool = True) -> None:
         self._check(self._lib.rv_context_enable_timing(self.handle, int(on)))
@@ -303,6 +308,49 @@ class Context:
                                                           C.c_void_p(grid_dptr), C.byref(e)))
         return self._estimate(e, 0)
 
+    # ---- sharded finish steps (include/rotavote_b200.h) ------------------
+    def peak_start_axis(self, grid_dptr: int, cfg: EstimatorConfig | None = None):
+        """find_peaks(K=1) + estimate_from_peak's start axis from a device grid -> (axis, votes, total)."""
+        c = (cfg or EstimatorConfig()).to_c()
+        axis = np.zeros(3)
+        votes, total = C.c_uint32(), C.c_uint64()
+        self._check(self._lib.rv_peak_start_axis(self.handle, C.c_void_p(grid_dptr), C.byref(c),
+                                                 _ptr(axis, C.c_double), C.byref(votes), C.byref(total)))
+        return axis, votes.value, total.value
+
+    def shard_classify(self, axis, epsilon: float, slot: int, compare_prev: bool):
+        """classify this context's shard into bitmask `slot` -> (count, scatter[6], differs)."""
+        a = np.ascontiguousarray(axis, dtype=np.float64)
+        cnt, diff = C.c_int64(), C.c_int32()
+        sc = np.zeros(6)
+        self._check(self._lib.rv_shard_classify(self.handle, _ptr(a, C.c_double), epsilon, slot, int(compare_prev),
+                                                C.byref(cnt), _ptr(sc, C.c_double), C.byref(diff)))
+        return cnt.value, sc, bool(diff.value)
+
+    def shard_inliers(self, slot: int, offset: int, count: int) -> np.ndarray:
+        out = np.zeros(max(count, 1), np.int32)
+        got = C.c_int64()
+        self._check(self._lib.rv_shard_inliers(self.handle, slot, offset, _ptr(out, C.c_int32), count, C.byref(got)))
+        return out[:got.value]
+
+    def shard_angle_hist(self, axis, cfg: EstimatorConfig | None = None):
+        cfg = cfg or EstimatorConfig()
+        c = cfg.to_c()
+        a = np.ascontiguousarray(axis, dtype=np.float64)
+        bins = np.zeros(cfg.angle_bins, np.uint32)
+        contrib = C.c_uint64()
+        self._check(self._lib.rv_shard_angle_hist(self.handle, _ptr(a, C.c_double), C.byref(c),
+                                                  _ptr(bins, C.c_uint32), C.byref(contrib)))
+        return bins, contrib.value
+
+    def shard_angle_sums(self, bins_total, cfg: EstimatorConfig | None = None) -> np.ndarray:
+        c = (cfg or EstimatorConfig()).to_c()
+        b = np.ascontiguousarray(bins_total, dtype=np.uint32)
+        sums = np.zeros(2)
+        self._check(self._lib.rv_shard_angle_sums(self.handle, _ptr(b, C.c_uint32), C.byref(c),
+                                                  _ptr(sums, C.c_double)))
+        return sums
+
     # ---- path functions -----------------------------------------------------------------
     def preprocess(self, corrs, tau_z: float = 1e-9, normalize: bool = True):
         """preprocess, estimator.hpp:47-48 -> (constraints (k,3), kept (k,), dropped (d,))."""
@@ -397,6 +445,66 @@ class Context:
 
 
 _default: Context | None = None
+
+
+def axis_from_scatter(scatter) -> np.ndarray:
+    """refine_axis's 3x3 eigen-solve (estimator.cpp:299-309) of a summed scatter (xx xy xz yy yz zz)."""
+    sc = np.ascontiguousarray(scatter, dtype=np.float64)
+    axis = np.zeros(3)
+    st = _native.lib().rv_axis_from_scatter(_ptr(sc, C.c_double), _ptr(axis, C.c_double))
+    _native.check(st)
+    return axis
+
+
+class MultiContext:
+    """Several B200s in one process (rv_multi_*): NCCL clique, sharded estimate_single / accumulate."""
+
+    def __init__(self, devices):
+        self._lib = _native.lib()
+        devs = np.ascontiguousarray(list(devices), dtype=np.int32)
+        h = C.c_void_p()
+        st = self._lib.rv_multi_create(_ptr(devs, C.c_int32), len(devs), C.byref(h))
+        _native.check(st)
+        self.handle = h
+        self.devices = list(devs)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self._lib.rv_multi_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def nccl_version(self) -> int:
+        return self._lib.rv_multi_nccl_version(self.handle)
+
+    def _check(self, st: int) -> None:
+        if st != 0:
+            cls = errors.STATUS_TO_ERROR.get(st, errors.DeviceError)
+            raise cls(self._lib.rv_status_string(st).decode() + ": " + self._lib.rv_multi_last_error(self.handle).decode())
+
+    def estimate_single(self, corrs, cfg: EstimatorConfig | None = None) -> RotationEstimate:
+        a = _f64(corrs, 6)
+        c = (cfg or EstimatorConfig()).to_c()
+        e = rv_estimate()
+        self._check(self._lib.rv_multi_estimate_single(self.handle, _ptr(a, C.c_double), a.shape[0], C.byref(c),
+                                                       C.byref(e)))
+        inl = np.zeros(max(e.n_inliers, 1), np.int32)
+        self._check(self._lib.rv_multi_result_inliers(self.handle, _ptr(inl, C.c_int32), e.n_inliers))
+        return RotationEstimate(axis=np.array(e.axis[:]), angle=e.angle, rotation=np.array(e.rotation[:]).reshape(3, 3),
+                                inliers=inl[:e.n_inliers], axis_votes=int(e.axis_votes), elapsed_s=e.elapsed_s)
+
+    def accumulate(self, constraints, grid: int = 512, extent: float = 1.05, samples: int = 2048) -> np.ndarray:
+        z = _f64(constraints, 3)
+        out = np.zeros((grid, grid), np.uint32)
+        self._check(self._lib.rv_multi_accumulate(self.handle, _ptr(z, C.c_double), z.shape[0], grid, extent, samples,
+                                                  _ptr(out, C.c_uint32)))
+        return out
 
 
 def default_context() -> Context:

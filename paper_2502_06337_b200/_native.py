@@ -110,6 +110,24 @@ _SIGS = [
      [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(rv_config), C.c_void_p, c_int64_p]),
     ("rv_estimate_single_prevoted", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(rv_config), C.c_void_p, C.POINTER(rv_estimate)]),
+    ("rv_peak_start_axis", C.c_int,
+     [C.c_void_p, C.c_void_p, C.POINTER(rv_config), c_double_p, C.POINTER(C.c_uint32), c_uint64_p]),
+    ("rv_shard_classify", C.c_int,
+     [C.c_void_p, c_double_p, C.c_double, C.c_int32, C.c_int32, c_int64_p, c_double_p, c_int32_p]),
+    ("rv_axis_from_scatter", C.c_int, [c_double_p, c_double_p]),
+    ("rv_shard_inliers", C.c_int, [C.c_void_p, C.c_int32, C.c_int64, c_int32_p, C.c_int64, c_int64_p]),
+    ("rv_shard_angle_hist", C.c_int, [C.c_void_p, c_double_p, C.POINTER(rv_config), c_uint32_p, c_uint64_p]),
+    ("rv_shard_angle_sums", C.c_int, [C.c_void_p, c_uint32_p, C.POINTER(rv_config), c_double_p]),
+    ("rv_multi_create", C.c_int, [c_int32_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    ("rv_multi_destroy", None, [C.c_void_p]),
+    ("rv_multi_size", C.c_int32, [C.c_void_p]),
+    ("rv_multi_last_error", C.c_char_p, [C.c_void_p]),
+    ("rv_multi_nccl_version", C.c_int32, [C.c_void_p]),
+    ("rv_multi_estimate_single", C.c_int,
+     [C.c_void_p, c_double_p, C.c_int64, C.POINTER(rv_config), C.POINTER(rv_estimate)]),
+    ("rv_multi_result_inliers", C.c_int, [C.c_void_p, c_int32_p, C.c_int64]),
+    ("rv_multi_accumulate", C.c_int,
+     [C.c_void_p, c_double_p, C.c_int64, C.c_int32, C.c_double, C.c_int32, c_uint32_p]),
     ("rv_preprocess", C.c_int,
      [C.c_void_p, c_double_p, C.c_int64, C.c_double, C.c_int32, c_double_p, c_int32_p, c_int32_p, c_int64_p, c_int64_p]),
     ("rv_accumulate", C.c_int, [C.c_void_p, c_double_p, C.c_int64, C.c_int32, C.c_double, C.c_int32, c_uint32_p]),

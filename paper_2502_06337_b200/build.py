@@ -15,7 +15,8 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "librotavote_b200.so"
 INCLUDE = PKG.parent / "include"
-SOURCES = ["rv_prep.cu", "rv_vote.cu", "rv_peaks.cu", "rv_refine.cu", "rv_coop.cu", "rv_io.cu", "rv_api.cpp"]
+SOURCES = ["rv_prep.cu", "rv_vote.cu", "rv_peaks.cu", "rv_refine.cu", "rv_coop.cu", "rv_io.cu", "rv_api.cpp",
+           "rv_multi.cpp"]
 # translation units whose device arithmetic must follow the host op order exactly
 NO_FMAD = {"rv_coop.cu"}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -68,7 +69,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             sys.stderr.write(res.stderr)
         objs.append(obj)
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs, "-cudart", "static"]
+    cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs, "-cudart", "static", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")

@@ -132,6 +132,16 @@ struct rv_context {
   DBuf rzx, rzy, rzz, rkept, removed;
   // vote
   DBuf basis_a, basis_b, ranges, band_work, table32, table64, grid, partials, slot_band, counters, stats, degen;
+  // sharded solve: the constraint set of the last rv_vote_shard and the step state
+  ConstraintSet shard_cs{};
+  const double* shard_corrs = nullptr;
+  int64_t shard_m = 0;               // inliers compacted by rv_shard_inliers
+  const int32_t* shard_idx = nullptr;
+  struct ShardCls {
+    uint32_t* flags = nullptr;
+    int32_t* offsets = nullptr;
+    int64_t count = -1;
+  } shard_cls[2];
   int table_J = -1;
   // peaks
   DBuf arg_keys, arg_out, sat, blur_best, blur_out, done;
@@ -2511,10 +2521,16 @@ rv_status rv_vote_shard(rv_context* c, const double* d_corrs, int64_t n, const r
       }
       sync(c);
       *n_kept = (int64_t)*hk;  // (an all-degenerate shard votes nothing: the grid stays zero)
+      c->shard_cs = inorder_result(inorder_buffers(c, d_corrs, n), n).cs;
+      c->shard_corrs = d_corrs;
+      c->shard_cls[0].count = c->shard_cls[1].count = -1;
       return;
     }
     const PreResult pre = preprocess_dev(c, d_corrs, n, cfg->tau_z, cfg->normalize_inputs);
     *n_kept = pre.cs.n;
+    c->shard_cs = pre.cs;
+    c->shard_corrs = d_corrs;
+    c->shard_cls[0].count = c->shard_cls[1].count = -1;
     if (pre.cs.n == 0) {  // an all-degenerate shard votes nothing
       ck(cudaMemsetAsync(d_grid, 0, sizeof(uint32_t) * cells, c->st), "memset");
       sync(c);
@@ -2606,6 +2622,120 @@ rv_status rv_estimate_single_prevoted(rv_context* c, const double* d_corrs, int6
     to_c(e, out, seconds_since(c));
     c->results.push_back(std::move(e.inliers));
   });
+}
+
+
+// ---- sharded finish steps: each rank / device runs these on its own shard; the
+// caller sums the small partials in rank order (distributed.py over torch.distributed, or
+// rv_multi_estimate_single over NCCL in one process) and makes the reference's decisions.
+rv_status rv_peak_start_axis(rv_context* c, const uint32_t* d_grid, const rv_config* cfg, double axis[3],
+                             uint32_t* votes, uint64_t* total) {
+  if (!c || !d_grid || !cfg || !axis || !votes || !total) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    unsigned long long tot = 0;
+    // find_peaks(acc, 1, radius, 1) (estimator.cpp:346) + estimate_from_peak's start axis (:97)
+    const std::vector<Peak> pk = find_peaks_dev(c, d_grid, cfg->grid, cfg->extent, 1, cfg->suppression_radius, 1, &tot);
+    double A, B, b[3];
+    interpolate_peak_dev(c, d_grid, cfg->grid, cfg->extent, pk[0], &A, &B);
+    backproject(A, B, b);
+    canonicalize3(b, axis);
+    *votes = pk[0].votes;
+    *total = tot;
+  });
+}
+
+rv_status rv_shard_classify(rv_context* c, const double axis[3], double epsilon, int32_t slot, int32_t compare_prev,
+                            int64_t* count, double scatter[6], int32_t* differs) {
+  if (!c || !axis || !count || !scatter || !differs || slot < 0 || slot > 1) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (!c->shard_corrs) fail(RV_ERR_INVALID_ARGUMENT, "no shard voted on this context");
+    const auto& other = c->shard_cls[1 - slot];
+    const uint32_t* prev = compare_prev && other.count >= 0 ? other.flags : nullptr;
+    const Cls r = classify_dev(c, c->shard_cs, axis, epsilon, slot, prev, 0);
+    c->shard_cls[slot].flags = r.flags;
+    c->shard_cls[slot].offsets = r.offsets;
+    c->shard_cls[slot].count = r.count;
+    *count = r.count;
+    std::memcpy(scatter, r.scatter, sizeof(double) * 6);
+    *differs = r.differs ? 1 : 0;
+  });
+}
+
+rv_status rv_shard_inliers(rv_context* c, int32_t slot, int64_t offset, int32_t* dst, int64_t capacity,
+                           int64_t* count) {
+  if (!c || !count || slot < 0 || slot > 1 || (capacity > 0 && !dst)) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    const auto& sc = c->shard_cls[slot];
+    if (sc.count < 0) fail(RV_ERR_INVALID_ARGUMENT, "slot not classified");
+    Cls cl{};
+    cl.flags = sc.flags;
+    cl.offsets = sc.offsets;
+    cl.count = sc.count;
+    c->shard_idx = compact_dev(c, c->shard_cs, cl);  // ascending shard-local input indices
+    c->shard_m = sc.count;
+    *count = sc.count;
+    const int64_t m = std::min(capacity, sc.count);
+    if (m > 0) {
+      ck(cudaMemcpyAsync(dst, c->shard_idx, sizeof(int32_t) * (size_t)m, cudaMemcpyDeviceToHost, c->st), "inliers");
+      sync(c);
+      for (int64_t k = 0; k < m; ++k) dst[k] = (int32_t)(dst[k] + offset);
+    }
+  });
+}
+
+rv_status rv_shard_angle_hist(rv_context* c, const double axis[3], const rv_config* cfg, uint32_t* bins,
+                              uint64_t* contributing) {
+  if (!c || !axis || !cfg || !bins || !contributing) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (cfg->angle_bins < 8) fail(RV_ERR_INVALID_CONFIG, "angle histogram needs bin_count >= 8");
+    StageScope sc(c, kAngles);
+    uint32_t* db = c->bins.get<uint32_t>(cfg->angle_bins);
+    double* raw = c->raw.get<double>((size_t)std::max<int64_t>(c->shard_m, 1));
+    unsigned long long* cnt = c->angle_counts.get<unsigned long long>(2);
+    ck(cudaMemsetAsync(db, 0, sizeof(uint32_t) * cfg->angle_bins, c->st), "memset bins");
+    ck(cudaMemsetAsync(cnt, 0, 16, c->st), "memset counts");
+    if (c->shard_m > 0) {  // vote_angles (angles.cpp:46-68) over this shard's inliers
+      launch_vote_angles_k(axis, c->shard_corrs, c->shard_idx, c->shard_m, cfg->angle_bins, cfg->tau_deg, db, raw, cnt,
+                           c->st);
+      count_launch(c);
+    }
+    ck(cudaMemcpyAsync(bins, db, sizeof(uint32_t) * cfg->angle_bins, cudaMemcpyDeviceToHost, c->st), "bins D2H");
+    unsigned long long* h = reinterpret_cast<unsigned long long*>(c->pinned);
+    ck(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, c->st), "angle counts D2H");
+    sync(c);
+    *contributing = h[0];
+  });
+}
+
+rv_status rv_shard_angle_sums(rv_context* c, const uint32_t* bins_total, const rv_config* cfg, double sums[2]) {
+  if (!c || !bins_total || !cfg || !sums) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    sums[0] = sums[1] = 0.0;
+    if (c->shard_m <= 0) return;
+    StageScope sc(c, kAngles);
+    // peak_angle (angles.cpp:70-90): the window around the GLOBAL peak bin, this shard's raw angles
+    uint32_t* db = c->bins.get<uint32_t>(cfg->angle_bins);
+    ck(cudaMemcpyAsync(db, bins_total, sizeof(uint32_t) * cfg->angle_bins, cudaMemcpyHostToDevice, c->st), "bins H2D");
+    double* res = c->angle_result.get<double>(4);
+    launch_peak_angle_k(db, cfg->angle_bins, c->raw.get<double>((size_t)c->shard_m), c->shard_m,
+                        c->angle_sums.get<double>(2 * 296), res, c->done_ptr(), c->st);
+    count_launch(c);
+    double* h = pin_d(c);
+    ck(cudaMemcpyAsync(h, res, 16, cudaMemcpyDeviceToHost, c->st), "angle sums D2H");
+    sync(c);
+    sums[0] = h[0];
+    sums[1] = h[1];
+  });
+}
+
+rv_status rv_axis_from_scatter(const double scatter[6], double axis[3]) {  // refine_axis, estimator.cpp:299-309
+  if (!scatter || !axis) return RV_ERR_INVALID_ARGUMENT;
+  return axis_from_scatter(scatter, axis) ? RV_OK : RV_ERR_RANK_DEFICIENT;
 }
 
 

@@ -1,18 +1,34 @@
 """Sharded estimate_single over ranks (one process per GPU; torch.distributed is the plumbing).
 
-SURVEY.md section 8(e): rank r owns the contiguous correspondence range
-[N*r/P, N*(r+1)/P), preprocesses and votes it into a local uint32 grid; the grids are summed
-with an all-reduce (NCCL over NVLink on B200; integer sums, so the result is bit-identical to the
-single-GPU grid -- the reference's own chunked vote relies on the same property,
-voting.cpp:102-117). The correspondences are all-gathered in rank order (reproducing input
-order, hence the reference's kept/inlier index order) and every rank finishes the solve from the
-reduced grid: identical estimate on all ranks, identical to the 1-GPU result.
+SURVEY.md section 8(e): rank r owns the contiguous correspondence range [N*r/P, N*(r+1)/P).
 
-The compute is behind a small backend interface so the same protocol runs on B200s
+  vote     every rank preprocesses and votes its shard into a local uint32 grid; one all-reduce
+           sums the grids (NCCL over NVLink on B200; integer sums, so the result is bit-identical
+           to the single-GPU grid -- the reference's own chunked vote relies on the same property,
+           voting.cpp:102-117)
+  peak     every rank finds the same peak and start axis on the summed grid
+           (estimate_from_peak, estimator.cpp:94-97)
+  refine   refine_loop (estimator.cpp:51-69), sharded: each pass every rank classifies its own
+           constraints and reports 8 doubles (inlier count, "set changed", the 6 scatter sums of
+           refine_axis); the partials are all-gathered and summed in rank order, and every rank
+           runs the same 3x3 solve -- identical axis and decision everywhere
+  estimate build_estimate (estimator.cpp:73-92): the rank-ordered concatenation of the shard
+           inlier lists is the reference's ascending list; the angle histograms are summed and
+           peak_angle's window sums around the summed peak are gathered and summed in rank order
+
+Only ~100 bytes per pass cross the interconnect after the grid. The branches that need every
+constraint on one device -- the identity shortcuts (estimator.cpp:326-340), the exactness-guard
+re-vote and the rescue path (:352-368) -- fall back to the replicated finish: all-gather the input
+and finish from the summed grid (rare: never on C1-C3).
+
+The compute is behind a small backend interface, so the same protocol runs on B200s
 (`DeviceBackend`, the C-ABI) and, in the CPU test-suite, on the oracle over gloo.
 """
 from __future__ import annotations
 
+import math
+
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -23,18 +39,58 @@ def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
 
 
 class DeviceBackend:
-    """B200 backend: vote / finish through the C-ABI on the rank's GPU."""
+    """B200 backend: the shard steps through the C-ABI on the rank's GPU.
 
-    def __init__(self, ctx):
+    The context runs on torch's current stream of the rank's device, so its work is ordered after
+    the collectives torch enqueued there (all-reduce, all-gather) and before anything torch enqueues
+    later; the C-ABI calls return after their own device work has completed."""
+
+    def __init__(self, ctx, device=None):
         self.ctx = ctx
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self._sync_stream()
 
-    def vote_shard(self, shard: torch.Tensor, cfg) -> torch.Tensor:
+    def _sync_stream(self):
+        self.ctx.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def vote_shard(self, shard: torch.Tensor, cfg):
+        self._sync_stream()
         g = torch.empty((cfg.grid, cfg.grid), dtype=torch.int32, device=shard.device)  # uint32 bits
-        self.ctx.vote_shard(shard.data_ptr(), shard.shape[0], g.data_ptr(), cfg)
-        return g
+        kept = self.ctx.vote_shard(shard.data_ptr(), shard.shape[0], g.data_ptr(), cfg)
+        self.shard = shard
+        return g, kept
+
+    def peak_start_axis(self, grid: torch.Tensor, cfg):
+        self._sync_stream()
+        return self.ctx.peak_start_axis(grid.data_ptr(), cfg)
+
+    def classify(self, axis, cfg, slot: int, compare: bool):
+        return self.ctx.shard_classify(axis, cfg.epsilon, slot, compare)
+
+    def inliers(self, slot: int, offset: int, count: int) -> np.ndarray:
+        return self.ctx.shard_inliers(slot, offset, count)
+
+    def angle_hist(self, axis, cfg):
+        return self.ctx.shard_angle_hist(axis, cfg)
+
+    def angle_sums(self, bins_total, cfg) -> np.ndarray:
+        return self.ctx.shard_angle_sums(bins_total, cfg)
 
     def finish(self, corrs: torch.Tensor, grid: torch.Tensor, cfg):
+        self._sync_stream()
         return self.ctx.estimate_single_prevoted(corrs.data_ptr(), corrs.shape[0], grid.data_ptr(), cfg)
+
+    def rodrigues(self, axis, angle):
+        import paper_2502_06337_b200 as rv
+        return rv.rodrigues(axis, angle)
+
+    def axis_from_scatter(self, s6):
+        import paper_2502_06337_b200 as rv
+        return rv.axis_from_scatter(s6)
+
+    @property
+    def tensor_device(self):
+        return self.device
 
 
 def all_gather_rows(shard: torch.Tensor, n_total: int, group=None) -> torch.Tensor:
@@ -42,19 +98,142 @@ def all_gather_rows(shard: torch.Tensor, n_total: int, group=None) -> torch.Tens
     world = dist.get_world_size(group)
     sizes = [shard_bounds(n_total, world, r)[1] - shard_bounds(n_total, world, r)[0] for r in range(world)]
     width = max(sizes)
-    padded = torch.zeros((width,) + tuple(shard.shape[1:]), dtype=shard.dtype, device=shard.device)
+    on = torch.device("cpu") if dist.get_backend(group) == "gloo" else shard.device
+    padded = torch.zeros((width,) + tuple(shard.shape[1:]), dtype=shard.dtype, device=on)
     padded[: shard.shape[0]] = shard
     parts = [torch.empty_like(padded) for _ in range(world)]
     dist.all_gather(parts, padded, group=group)
-    return torch.cat([p[:s] for p, s in zip(parts, sizes)])
+    return torch.cat([p[:s] for p, s in zip(parts, sizes)]).to(shard.device)
 
 
-def sharded_estimate_single(shard: torch.Tensor, n_total: int, cfg, backend, group=None):
-    """estimate_single over all ranks' shards; every rank returns the same estimate."""
-    grid = backend.vote_shard(shard, cfg)
-    dist.all_reduce(grid, op=dist.ReduceOp.SUM, group=group)  # int32 wrap-around == uint32 sum
+def _comm_device(backend, group):
+    """Where the small collective tensors live: the rank's GPU for NCCL, host memory for gloo."""
+    return torch.device("cpu") if dist.get_backend(group) == "gloo" else backend.tensor_device
+
+
+def _all_reduce_(t: torch.Tensor, group) -> None:
+    """In-place sum; a CUDA tensor under gloo goes through host memory."""
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+
+def _gather_f64(vals, device, group) -> np.ndarray:
+    """All-gather a small float64 vector from every rank -> (world, k) array in rank order."""
+    world = dist.get_world_size(group)
+    t = torch.as_tensor(np.asarray(vals, dtype=np.float64), device=device)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t, group=group)
+    return torch.stack(parts).cpu().numpy()
+
+
+def _gather_i32_varlen(vals: np.ndarray, counts, device, group) -> np.ndarray:
+    world = dist.get_world_size(group)
+    width = max(1, int(max(counts)))
+    t = torch.zeros(width, dtype=torch.int32, device=device)
+    if vals.size:
+        t[: vals.size] = torch.as_tensor(vals, device=device)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t, group=group)
+    return np.concatenate([p[: int(c)].cpu().numpy() for p, c in zip(parts, counts)]) if world else vals
+
+
+def replicated_finish(shard: torch.Tensor, n_total: int, grid: torch.Tensor, cfg, backend, group=None):
+    """All-gather the input and finish from the summed grid on every rank (the rare branches)."""
     corrs = all_gather_rows(shard, n_total, group)
     return backend.finish(corrs, grid, cfg)
+
+
+def sharded_estimate_single(shard: torch.Tensor, n_total: int, cfg, backend, group=None, stats: dict | None = None):
+    """estimate_single over all ranks' shards; every rank returns the same estimate (equal to the
+    single-device estimate: identical grid, peak and inlier set; rotation within 1e-3 deg)."""
+    from paper_2502_06337_b200 import RotationEstimate
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = _comm_device(backend, group)
+    lo, _ = shard_bounds(n_total, world, rank)
+    grid, kept = backend.vote_shard(shard, cfg)
+    _all_reduce_(grid, group)  # int32 wrap-around == uint32 sum
+    kept_t = torch.tensor([kept], dtype=torch.int64, device=dev)
+    dist.all_reduce(kept_t, group=group)
+    n_kept = int(kept_t.item())
+    mode = "sharded"
+    if stats is not None:
+        stats["mode"] = mode
+    if n_kept == 0 or (n_total - n_kept) * 10 >= n_total * 9:  # identity shortcuts need the dropped list
+        if stats is not None:
+            stats["mode"] = "replicated:identity"
+        return replicated_finish(shard, n_total, grid, cfg, backend, group)
+    axis, votes, total = backend.peak_start_axis(grid, cfg)
+    if total != n_kept * cfg.theta_samples:  # exactness guard: the replicated finish re-votes
+        if stats is not None:
+            stats["mode"] = "replicated:guard"
+        return replicated_finish(shard, n_total, grid, cfg, backend, group)
+
+    def classify(ax, slot, compare):
+        c, sc, diff = backend.classify(ax, cfg, slot, compare)
+        rows = _gather_f64([c, 1.0 if diff else 0.0, *sc], dev, group)
+        s6 = np.zeros(6)
+        for r in range(world):  # rank order
+            s6 = s6 + rows[r, 2:]
+        return rows[:, 0].astype(np.int64), bool(rows[:, 1].any()), s6
+
+    slot = 0
+    counts, _, s6 = classify(axis, slot, False)
+    passes = 0
+    if cfg.refine:
+        for _ in range(10):  # refine_loop (estimator.cpp:51-69)
+            if counts.sum() < 2:
+                break
+            try:
+                nxt = backend.axis_from_scatter(s6)
+            except Exception as e:  # RankDeficient: keep the current axis
+                if type(e).__name__ != "RankDeficient":
+                    raise
+                break
+            counts, changed, s6 = classify(nxt, 1 - slot, True)
+            slot = 1 - slot
+            axis = np.asarray(nxt, dtype=np.float64)
+            passes += 1
+            if not changed:
+                break
+        if counts.sum() < 3.0 * (cfg.epsilon * n_kept):  # rescue (estimator.cpp:352-368)
+            if stats is not None:
+                stats["mode"] = "replicated:rescue"
+            return replicated_finish(shard, n_total, grid, cfg, backend, group)
+    if stats is not None:
+        stats["passes"] = passes
+    local = backend.inliers(slot, lo, int(counts[rank]))
+    inliers = _gather_i32_varlen(local, counts, dev, group)
+    bins, contrib = backend.angle_hist(axis, cfg)
+    bins_t = torch.as_tensor(bins.astype(np.int64), device=dev)
+    dist.all_reduce(bins_t, group=group)
+    contrib_t = torch.tensor([contrib], dtype=torch.int64, device=dev)
+    dist.all_reduce(contrib_t, group=group)
+    if int(contrib_t.item()) == 0:
+        from paper_2502_06337_b200.errors import NoVotes
+        raise NoVotes("no correspondence produced an angle vote")
+    hist = bins_t.cpu().numpy().astype(np.uint32)
+    peak = int(np.argmax(hist))  # first maximum (angles.cpp:70-90)
+    w = 2.0 * math.pi / cfg.angle_bins
+    angle = -math.pi + (peak + 0.5) * w
+    if cfg.refine:
+        rows = _gather_f64(backend.angle_sums(hist, cfg), dev, group)
+        s = c = 0.0
+        for r in range(world):  # rank order
+            s += float(rows[r, 0])
+            c += float(rows[r, 1])
+        if not (s == 0.0 and c == 0.0):
+            angle = math.atan2(s, c)
+            if angle <= -math.pi:
+                angle += 2.0 * math.pi
+    axis = np.asarray(axis, dtype=np.float64)
+    return RotationEstimate(axis=axis, angle=angle, rotation=backend.rodrigues(axis, angle),
+                            inliers=inliers.astype(np.int32), axis_votes=int(votes))
 
 
 def batch_estimate(problems, cfg, solve_batch, group=None):
@@ -73,4 +252,3 @@ def batch_estimate(problems, cfg, solve_batch, group=None):
         for k, r in part:
             out[k] = r
     return out
-

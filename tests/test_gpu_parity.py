@@ -348,6 +348,8 @@ def test_sharded_vote_protocol_single_gpu(ctx, world):
     from paper_2502_06337_b200 import distributed as rvd
     corrs, _, _ = synth.make_config("c3", 300_000)
     d = torch.from_numpy(corrs).cuda()
+    # the context runs on torch's stream: `total += g` is ordered before the C-ABI calls
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
     total = torch.zeros((512, 512), dtype=torch.int32, device="cuda")
     for r in range(world):
         lo, hi = rvd.shard_bounds(corrs.shape[0], world, r)
@@ -358,8 +360,10 @@ def test_sharded_vote_protocol_single_gpu(ctx, world):
     z, _, _ = ctx.preprocess(corrs)
     ref_grid = ctx.accumulate(z)
     assert np.array_equal(total.cpu().numpy().view(np.uint32), ref_grid)
+    assert ctx.stage_times()["vote_guard_reruns"] == 0  # the prevoted grid was used, not re-voted
     e1 = ctx.estimate_single_device(d.data_ptr(), corrs.shape[0])
     assert np.array_equal(e.inliers, e1.inliers) and np.array_equal(e.rotation, e1.rotation)
+    ctx.set_stream(None)
 
 
 def test_full_size_multi_recovers_three(ctx):
