@@ -7,15 +7,19 @@ One step = one full solve (preprocess, vote, peak, refine, angle vote, rotation)
   value  = correspondences/sec of the device-resident solve (inputs already in HBM), all ranks
   e2e    = the same through the public C-ABI with host buffers: pinned H2D of the 48 MB input
            and D2H of the estimate + inlier list inside the timed region
+  e2e_pageable = the reference user's call: C++ rotavote::estimate_single on a fresh
+           std::vector<Correspondence> (pageable memory), host clock (tools/e2e/e2e_pageable.cpp)
   roofline: dominant kernel = the band-tiled vote (K2), bound by shared-memory atomics/ALU;
            peak = conflict-free u32 shared-atomic rate measured live on this box
-  cpu_baseline: the reference (oracle/_ref, unmodified sources, reference flags) on the host
-           cores, bounded sample, rank 0 at N=1 only
+  cpu_baseline / cpu_baseline_1thread: the reference (oracle/_ref, unmodified sources, reference
+           flags) on the host cores (cfg.threads = nproc, and the reference default 1), rank 0 at N=1
 
-Multi-GPU (torchrun, --mode sharded, default): one C3 problem, correspondences sharded across
-ranks, per-rank vote, NCCL all-reduce of the uint32 grid, all-gather of the input, replicated
-finish ("scaling": "strong"); --mode replicas: one independent problem per rank ("weak").
-Device time = max over ranks.
+Multi-GPU (--gpus N: re-launches itself under torchrun when WORLD_SIZE is unset; --mode sharded,
+default): one C3 problem, correspondences sharded across ranks, per-rank vote, NCCL all-reduce of
+the uint32 grid, sharded refine_loop / angle vote with rank-ordered partial sums
+(distributed.sharded_estimate_single; "scaling": "strong"); --mode replicas: one
+independent problem per rank ("weak"). Device time = max over ranks. NCCL_DEBUG=INFO lines go to
+stderr.
 `--impl reference` runs the reference CPU implementation instead (rank 0 only).
 """
 from __future__ import annotations
@@ -151,6 +155,27 @@ def reference_cpu(n_sample: int, reps: int, threads: int, corrs: np.ndarray):
     return kind, times
 
 
+def pageable_e2e(corrs: np.ndarray, steps: int, warmup: int, d2h_bytes: int):
+    """The reference user's path: rotavote::estimate_single (C++ drop-in, estimator.hpp:63-64) on a
+    fresh std::vector<Correspondence> in pageable memory, host clock around the call
+    (tools/e2e/e2e_pageable.cpp)."""
+    import subprocess
+    import tempfile
+    exe = ROOT / "tools" / "_bin" / "e2e_pageable"
+    if not exe.exists():
+        return {"unavailable": "tools/_bin/e2e_pageable not built (tools/e2e: make)"}
+    with tempfile.NamedTemporaryFile(suffix=".f64") as f:
+        np.ascontiguousarray(corrs, dtype=np.float64).tofile(f.name)
+        r = subprocess.run([str(exe), f.name, str(corrs.shape[0]), str(steps), str(warmup)], capture_output=True,
+                           text=True, timeout=600)
+    if r.returncode != 0:
+        return {"unavailable": (r.stderr or r.stdout)[-300:]}
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    return {"value": d["value"], "unit": UNIT, "ms_per_step": d["ms_per_step"],
+            "h2d_bytes_per_step": int(corrs.shape[0] * 48), "d2h_bytes_per_step": d2h_bytes,
+            "path": "C++ rotavote::estimate_single on a fresh std::vector<Correspondence> (pageable), steady_clock"}
+
+
 def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
@@ -166,7 +191,7 @@ def run_reference(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per_solve * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE generator)",
-            "config": config_block(n_sample, 1, {"sample": f"first {n_sample} correspondences of the C3 scene"}),
+            "config": config_block(n_sample, 1),
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads,
                              "kind": "reference" if kind.startswith("ref") else "port",
@@ -182,7 +207,10 @@ def run_device(args):
 
     rank, world, local = env_rank()
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (nranks) on stderr
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     import paper_2502_06337_b200 as rv
     from paper_2502_06337_b200 import distributed as rvd
@@ -320,7 +348,7 @@ def run_device(args):
     hbm = measured_peaks().get("hbm_gbs")
     # in-order preprocess (single solves): 48 B read + 24 B of z written per correspondence
     k1_gbs = (72.0 * n_mine) / (pre_ms * 1e-3) / 1e9 if pre_ms > 0 else None
-    cpu = None
+    cpu = cpu1 = None
     if world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         kind, times = reference_cpu(args.cpu_sample, 3, threads, corrs)
@@ -329,6 +357,15 @@ def run_device(args):
                "kind": "reference" if kind.startswith("ref") else "port",
                "sample": f"reference estimate_single on the first {args.cpu_sample} C3 correspondences, median of "
                          f"3, cfg.threads={threads}"}
+        # the reference default (cfg.threads = 1, estimator.hpp:28): one bounded run
+        kind1, times1 = reference_cpu(args.cpu_sample, 1, 1, corrs)
+        cpu1 = {"value": args.cpu_sample / times1[0], "unit": UNIT, "cores": 1,
+                "kind": "reference" if kind1.startswith("ref") else "port",
+                "sample": f"reference estimate_single on the first {args.cpu_sample} C3 correspondences, one run, "
+                          f"cfg.threads=1 (the reference default)"}
+    e2e_pageable = None
+    if world == 1 and not args.no_pageable:
+        e2e_pageable = pageable_e2e(corrs, args.steps, warm, int(d2h_bytes))
     extra = {"parallelism": (f"sharded{world} (contiguous shards, NCCL all-reduce of the uint32 grid, "
                              f"all-gather of the input)") if sharded else
              (f"replicas{world}" if world > 1 else "single"),
@@ -347,7 +384,8 @@ def run_device(args):
                             "traffic": None, "bytes_per_corr": 72},
             "stage_ms": {k: statistics.mean(s[k] for s in stage) for k in
                          ("preprocess_ms", "vote_ms", "peaks_ms", "refine_ms", "angles_ms")},
-            "gpu_launches": launches, "cpu_baseline": cpu, "clocks": clocks,
+            "e2e_pageable": e2e_pageable,
+            "gpu_launches": launches, "cpu_baseline": cpu, "cpu_baseline_1thread": cpu1, "clocks": clocks,
             "accuracy": {"rot_err_deg_vs_truth": err_deg, "inliers": int(est.inliers.size)}}
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -365,7 +403,23 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
                     help="N>1: shard one C3 problem across ranks (strong) or one problem per rank (weak)")
+    ap.add_argument("--no-pageable", action="store_true")
     args = ap.parse_args()
+    world_env = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and world_env is None:
+        # one process per GPU: re-launch this command under torchrun with --gpus ranks
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")            # communicator lines (nranks) ...
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # ... on stderr: stdout keeps the one JSON line
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+        os.execvpe(sys.executable, cmd, env)
+    if world_env is not None and int(world_env) != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={world_env} but --gpus {args.gpus}")
     if args.impl == "reference":
         run_reference(args)
     else:

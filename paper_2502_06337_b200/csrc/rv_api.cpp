@@ -18,6 +18,8 @@
 #include <cstdlib>
 #include <random>
 #include <thread>
+#include <mutex>
+#include <condition_variable>
 #include <unistd.h>
 #include <cstring>
 #include <memory>
@@ -110,6 +112,76 @@ struct ConstraintSet {
   int64_t n = 0;
 };
 
+// Parallel host memcpy (pageable -> pinned staging of large single-solve inputs): a few worker
+// threads, each copying a contiguous slice; the caller copies the first slice itself.
+class CopyPool {
+ public:
+  explicit CopyPool(int threads) {
+    for (int t = 1; t < threads; ++t)
+      th_.emplace_back([this, t] {
+        int seen = 0;
+        for (;;) {
+          Job j;
+          {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+            j = job_;
+          }
+          slice(j, t);
+          std::lock_guard<std::mutex> lk(mu_);
+          if (--pending_ == 0) done_.notify_all();
+        }
+      });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  void copy(void* dst, const void* src, size_t bytes) {
+    const int parts = (int)th_.size() + 1;
+    if (parts == 1 || bytes < ((size_t)1 << 20)) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    Job j{static_cast<char*>(dst), static_cast<const char*>(src), bytes, parts};
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = j;
+      pending_ = parts - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    slice(j, 0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+  }
+
+ private:
+  struct Job {
+    char* dst = nullptr;
+    const char* src = nullptr;
+    size_t bytes = 0;
+    int parts = 1;
+  };
+  static void slice(const Job& j, int t) {
+    const size_t lo = (j.bytes * (size_t)t / (size_t)j.parts) & ~(size_t)63;
+    const size_t hi = t + 1 == j.parts ? j.bytes : (j.bytes * (size_t)(t + 1) / (size_t)j.parts) & ~(size_t)63;
+    if (hi > lo) std::memcpy(j.dst + lo, j.src + lo, hi - lo);
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  Job job_;
+  int gen_ = 0, pending_ = 0;
+  bool stop_ = false;
+};
+
 }  // namespace
 
 struct rv_context {
@@ -160,6 +232,9 @@ struct rv_context {
   size_t csv_pinned_cap = 0;
   double* in_pinned = nullptr;            // pinned staging of small pageable single-solve inputs
   size_t in_pinned_cap = 0;
+  double* big_pinned = nullptr;           // pinned staging of large pageable inputs (chunked, parallel copies)
+  size_t big_pinned_cap = 0;
+  std::unique_ptr<CopyPool> copy_pool;
   bool kept_acc_ready = false;
   DBuf cons_axes, cons_counts, cons_z, cons_idx;  // baseline consensus scoring
   int coop_grid = 0;
@@ -1038,6 +1113,15 @@ struct PipelinedVote {
   bool peak_ready = false;  // argmax + start axis fused into the final tile reduction
 };
 
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n, const rv_config& cfg) {
   PipelinedVote out;
   double* d = c->corrs.get<double>((size_t)n * 6);
@@ -1063,7 +1147,22 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
     }
     return v;
   }();
-  const int C = (p.banded && n >= (int64_t)1 << 18) ? (int)kCum.size() - 1 : 1;
+  // pageable input is staged through pinned memory by host threads (below); the host copy is then
+  // the slow stage, so it gets 16 equal chunks: each chunk's DMA + compute hides under the next
+  // chunk's host copy, and only one sixteenth of the compute trails the last copy
+  static const std::vector<int64_t> kCumStaged = [] {
+    std::vector<int64_t> v;
+    for (int k = 0; k <= 16; ++k) v.push_back(k);
+    return v;
+  }();
+  static const int kPageable = [] {  // dev knob: 0 staging (default), 1 register in place, 2 plain
+    const char* e = std::getenv("RV_PAGEABLE");
+    return e ? std::atoi(e) : 0;
+  }();
+  const bool pipelined = p.banded && n >= (int64_t)1 << 18;
+  const bool staged = pipelined && kPageable == 0 && !host_pinned(h_corrs);
+  const std::vector<int64_t>& cum = staged ? kCumStaged : kCum;
+  const int C = pipelined ? (int)cum.size() - 1 : 1;
   if (!c->copy_st) ck(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking), "copy stream");
   while ((int)c->chunk_events.size() < C) {
     cudaEvent_t e;
@@ -1072,7 +1171,7 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
   }
   std::vector<int64_t> bounds(C + 1);
   for (int k = 0; k <= C; ++k)
-    bounds[k] = k == C ? n : std::min<int64_t>(n, ((C > 1 ? n * kCum[k] / 16 : 0) + 1023) / 1024 * 1024);
+    bounds[k] = k == C ? n : std::min<int64_t>(n, ((C > 1 ? n * cum[k] / 16 : 0) + 1023) / 1024 * 1024);
   StageScope sc(c, kVote);
   // one chunk: the copy goes on the compute stream itself (no cross-stream dependency to resolve);
   // several: on the copy stream, ordered after everything already queued on the compute stream
@@ -1082,10 +1181,48 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
     ck(cudaEventRecord(start, c->st), "record");
     ck(cudaStreamWaitEvent(c->copy_st, start, 0), "wait");
   }
+  // Large pageable input (what a std::vector<Correspondence> caller passes): each chunk is first
+  // copied into a context-owned pinned buffer by a few host threads in parallel, then DMA'd
+  // asynchronously -- the host copies chunk k+1 while the device copies and computes chunk k (a
+  // pageable cudaMemcpyAsync would stage through the driver's buffers at single-thread speed).
+  const double* src = h_corrs;
+  bool registered = false;
+  if (C > 1 && kPageable == 1 && !host_pinned(h_corrs)) {
+    registered = cudaHostRegister(const_cast<double*>(h_corrs), sizeof(double) * 6 * (size_t)n,
+                                  cudaHostRegisterReadOnly) == cudaSuccess;
+    if (!registered) cudaGetLastError();
+  }
+  if (staged) {
+    const size_t bytes = sizeof(double) * 6 * (size_t)n;
+    if (bytes > c->big_pinned_cap) {
+      if (c->big_pinned) {
+        sync(c);
+        cudaFreeHost(c->big_pinned);
+        c->big_pinned = nullptr;
+        c->big_pinned_cap = 0;
+      }
+      void* q = nullptr;
+      if (cudaHostAlloc(&q, bytes, cudaHostAllocDefault) == cudaSuccess) {
+        c->big_pinned = static_cast<double*>(q);
+        c->big_pinned_cap = bytes;
+      } else {
+        cudaGetLastError();
+      }
+    }
+    if (c->big_pinned) {
+      if (!c->copy_pool) {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        unsigned nt = std::min(4u, hw);  // 4: the measured best on a 16-vCPU B200 host (memory-bound)
+        if (const char* e = std::getenv("RV_COPY_THREADS")) nt = (unsigned)std::max(1, std::atoi(e));  // dev knob
+        c->copy_pool = std::make_unique<CopyPool>((int)nt);
+      }
+      src = c->big_pinned;
+    }
+  }
   auto issue_copy = [&](int k) {
-    ck(cudaMemcpyAsync(d + 6 * bounds[k], h_corrs + 6 * bounds[k], sizeof(double) * 6 * (bounds[k + 1] - bounds[k]),
-                       cudaMemcpyHostToDevice, cs),
-       "H2D chunk");
+    const size_t bytes = sizeof(double) * 6 * (size_t)(bounds[k + 1] - bounds[k]);
+    if (src != h_corrs) c->copy_pool->copy(c->big_pinned + 6 * bounds[k], h_corrs + 6 * bounds[k], bytes);
+    ck(cudaMemcpyAsync(d + 6 * bounds[k], src + 6 * bounds[k], bytes, cudaMemcpyHostToDevice, cs), "H2D chunk");
     if (C > 1) ck(cudaEventRecord(c->chunk_events[k], cs), "record chunk");
   };
   issue_copy(0);
@@ -1180,6 +1317,10 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
     out.pre.cs.n = h[0];
     out.pre.n_dropped = h[1];
     out.grid = out.pre.cs.n > 0 ? vote(c, pb.zx, pb.zy, pb.zz, out.pre.cs.n, G, cfg.extent, J) : grid;
+  }
+  if (registered) {  // every chunk copy has been issued: wait for the last, then unpin
+    ck(cudaEventSynchronize(c->chunk_events[C - 1]), "H2D done");
+    cudaHostUnregister(const_cast<double*>(h_corrs));
   }
   return out;
 }
@@ -1377,15 +1518,6 @@ Estimate estimate_single_dev(rv_context* c, const double* d_corrs, int64_t n, co
 }
 
 // estimate_single with host input: pipelined H2D + preprocess + vote, then the same solve.
-bool host_pinned(const void* p) {
-  cudaPointerAttributes a{};
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeHost;
-}
-
 // Small pageable inputs are staged into a context-owned pinned buffer first (n x 48 B, a few
 // microseconds): the H2D then runs at DMA speed and the staged solve is graph-replayable (the
 // staging pointer repeats), which is what many small independent solves (estimate_batch) need.
@@ -2108,6 +2240,8 @@ void rv_context_destroy(rv_context* c) {
   if (c->inl_host) cudaFreeHost(c->inl_host);
   if (c->csv_pinned) cudaFreeHost(c->csv_pinned);
   if (c->in_pinned) cudaFreeHost(c->in_pinned);
+  if (c->big_pinned) cudaFreeHost(c->big_pinned);
+  c->copy_pool.reset();
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
 }
