@@ -101,6 +101,8 @@ typedef struct rv_stage_times {
   int32_t vote_launches;    /* vote kernel launches in the call */
   int32_t kernel_launches;  /* all kernels launched by the call */
   double vote_kernel_ms;    /* the band-tiled vote kernel alone (CUDA events around its launches) */
+  int64_t csv_host_fields;  /* CSV fields outside the device parser's exact fast path, parsed by the
+                               host's std::from_chars (rv_*_correspondences_csv) */
 } rv_stage_times;
 
 typedef struct rv_context rv_context;

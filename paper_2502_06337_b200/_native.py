@@ -69,6 +69,7 @@ class rv_stage_times(C.Structure):
         ("vote_launches", C.c_int32),
         ("kernel_launches", C.c_int32),
         ("vote_kernel_ms", C.c_double),
+        ("csv_host_fields", C.c_int64),
     ]
 
 

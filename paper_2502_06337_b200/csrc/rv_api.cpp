@@ -216,7 +216,7 @@ struct rv_context {
   } shard_cls[2];
   int table_J = -1;
   // peaks
-  DBuf arg_keys, arg_out, sat, blur_best, blur_out, done;
+  DBuf arg_keys, arg_out, sat, blur_best, blur_out, done, peak_mask;
   // classify / refine
   DBuf flagsA, flagsB, bcount, bscatter, bdiff, boffA, boffB, cls_result, compact_out;
   DBuf coop_part, coop_state, coop_bar;  // device-resident refine_loop / anneal_axis (rv_coop.cu)
@@ -595,9 +595,22 @@ std::vector<Peak> find_peaks_dev(rv_context* c, const uint32_t* grid, int G, dou
   const double cs = 2.0 * E / G;
   unsigned long long* keys = c->arg_keys.get<unsigned long long>(2 * argmax_block_count());
   unsigned long long* okey = c->arg_out.get<unsigned long long>(2);
+  // up to max_direct_disks() suppression disks go to the argmax kernel directly; beyond that (any
+  // K, like the reference) the disks are painted into a G*G suppression bit image incrementally
+  uint32_t* mask = nullptr;
+  size_t painted = 0;
   for (int k = 0; k < max_peaks; ++k) {
-    if (disks.size() > 16) fail(RV_ERR_INVALID_CONFIG, "find_peaks: more than 8 peaks with mirrors unsupported");
-    launch_argmax(grid, G, disks.data(), (int)disks.size(), radius, keys, okey, c->done_ptr(), c->st);
+    if (!mask && (int)disks.size() > max_direct_disks()) {
+      const size_t words = ((size_t)G * G + 31) / 32;
+      mask = c->peak_mask.get<uint32_t>(words);
+      ck(cudaMemsetAsync(mask, 0, sizeof(uint32_t) * words, c->st), "memset peak mask");
+    }
+    if (mask && painted < disks.size()) {
+      launch_mark_disks(mask, G, disks.data() + painted, (int)(disks.size() - painted), radius, c->st);
+      count_launch(c);
+      painted = disks.size();
+    }
+    launch_argmax(grid, G, disks.data(), (int)disks.size(), radius, keys, okey, c->done_ptr(), c->st, mask);
     count_launch(c);
     unsigned long long* hk = reinterpret_cast<unsigned long long*>(c->pinned);
     ck(cudaMemcpyAsync(hk, okey, 16, cudaMemcpyDeviceToHost, c->st), "argmax D2H");
@@ -2497,27 +2510,28 @@ rv_status rv_ransac_rotation(rv_context* c, const double* corrs, int64_t n, int3
     clear_results(c);
     constexpr double kTauZ = 1e-9, kTauDeg = 1e-6;
     if (n < 2) fail(RV_ERR_NO_CONSENSUS, "need at least two correspondences");
-    // preprocess(correspondences, kTauZ, true) -- estimator.cpp:259-285 op order, on the host:
-    // the hypothesis stream below consumes z sequentially anyway
-    std::vector<double> z;
-    std::vector<int32_t> kept;
-    z.reserve((size_t)3 * n);
-    kept.reserve((size_t)n);
-    for (int64_t i = 0; i < n; ++i) {
-      double x[3] = {corrs[6 * i], corrs[6 * i + 1], corrs[6 * i + 2]};
-      double y[3] = {corrs[6 * i + 3], corrs[6 * i + 4], corrs[6 * i + 5]};
-      const double nx = std::sqrt(dot3(x, x)), ny = std::sqrt(dot3(y, y));
-      if (nx > 0.0)
-        for (double& v : x) v /= nx;
-      if (ny > 0.0)
-        for (double& v : y) v /= ny;
-      const double d[3] = {y[0] - x[0], y[1] - x[1], y[2] - x[2]};
-      const double len = std::sqrt(dot3(d, d));
-      if (len < kTauZ) continue;
-      z.push_back(d[0] / len);
-      z.push_back(d[1] / len);
-      z.push_back(d[2] / len);
-      kept.push_back((int32_t)i);
+    // preprocess(correspondences, kTauZ, true) (baselines.cpp:35, estimator.cpp:259-285) on the
+    // device -- the solver's own kernel; the hypothesis stream below draws constraint pairs
+    // sequentially from the host RNG, so the compacted z and kept map come back to the host
+    const double* dcorr = upload_corrs(c, corrs, n);
+    const PreResult pre = preprocess_dev(c, dcorr, n, kTauZ, 1);
+    // preprocess throws AllDegenerate when every pair is dropped (estimator.cpp:280-283)
+    if (pre.cs.n == 0) fail(RV_ERR_ALL_DEGENERATE, "every correspondence pair is degenerate (x ~ y)");
+    const ConstraintSet cs = pre.cs;
+    std::vector<double> z((size_t)3 * (size_t)cs.n);
+    std::vector<int32_t> kept((size_t)cs.n);
+    if (cs.n > 0) {
+      std::vector<double> sx((size_t)cs.n), sy((size_t)cs.n), sz((size_t)cs.n);
+      ck(cudaMemcpyAsync(sx.data(), cs.zx, 8 * (size_t)cs.n, cudaMemcpyDeviceToHost, c->st), "D2H zx");
+      ck(cudaMemcpyAsync(sy.data(), cs.zy, 8 * (size_t)cs.n, cudaMemcpyDeviceToHost, c->st), "D2H zy");
+      ck(cudaMemcpyAsync(sz.data(), cs.zz, 8 * (size_t)cs.n, cudaMemcpyDeviceToHost, c->st), "D2H zz");
+      ck(cudaMemcpyAsync(kept.data(), cs.kept, 4 * (size_t)cs.n, cudaMemcpyDeviceToHost, c->st), "D2H kept");
+      sync(c);
+      for (int64_t i = 0; i < cs.n; ++i) {
+        z[(size_t)(3 * i)] = sx[(size_t)i];
+        z[(size_t)(3 * i + 1)] = sy[(size_t)i];
+        z[(size_t)(3 * i + 2)] = sz[(size_t)i];
+      }
     }
     const size_t nz = kept.size();
     if (nz < 2) fail(RV_ERR_NO_CONSENSUS, "fewer than two usable constraints");
@@ -2568,7 +2582,7 @@ rv_status rv_ransac_rotation(rv_context* c, const double* corrs, int64_t n, int3
     double best_axis[3] = {axes[3 * bk], axes[3 * bk + 1], axes[3 * bk + 2]};
     double best_angle = angles[bk];
     // local refit (baselines.cpp:80-94): classify, refine_axis on the consensus set, reclassify
-    const ConstraintSet cs = upload_constraints(c, z.data(), (int64_t)nz);
+    // (on the device-resident preprocess output)
     auto classify = [&](const double* axis) {
       const Cls cl = classify_dev(c, cs, axis, epsilon, 0, nullptr, 0);
       std::vector<int32_t> v((size_t)cl.count);
@@ -2589,13 +2603,12 @@ rv_status rv_ransac_rotation(rv_context* c, const double* corrs, int64_t n, int3
     est.inliers.reserve(inl.size());
     for (int32_t i : inl) est.inliers.push_back(kept[(size_t)i]);
     try {  // vote_angles + peak_angle(refine) over the inliers; NoVotes keeps the sample angle
-      const double* dcorr = upload_aos(c, c->corrs, corrs, 6 * n);
       int32_t* didx = c->cons_idx.get<int32_t>(std::max<size_t>(est.inliers.size(), 1));
       if (!est.inliers.empty())
         ck(cudaMemcpyAsync(didx, est.inliers.data(), 4 * est.inliers.size(), cudaMemcpyHostToDevice, c->st), "H2D");
       rv_config acfg;
       rv_config_default(&acfg);
-      acfg.angle_bins = 1024;
+      acfg.angle_bins = 1024;  // baselines.cpp:99
       acfg.tau_deg = kTauDeg;
       acfg.refine = 1;
       best_angle = angle_dev(c, best_axis, dcorr, didx, (int64_t)est.inliers.size(), acfg);
@@ -2992,6 +3005,7 @@ const double* parse_csv_dev(rv_context* c, const char* text, int64_t nbytes, con
   uint32_t errl = (uint32_t)h[2];
   const int64_t nrows = h[3];
   const int64_t nfb = h[4];
+  c->times.csv_host_fields += nfb;
   if (nfb > 0) {  // the rare fields outside the device's exact fast path: the host's from_chars
     std::vector<int64_t> idx;
     std::vector<double> val;

@@ -143,7 +143,11 @@ int argmax_block_count();
 // Argmax over cells not inside any disk (radius r): key = (count << 32) | (~index), count > 0.
 void launch_argmax(const uint32_t* grid, int G, const Disk* disks, int n_disks, int r,
                    unsigned long long* block_keys, unsigned long long* out_key, unsigned int* done,
-                   cudaStream_t s);
+                   cudaStream_t s,
+                   const uint32_t* mask = nullptr);
+// find_peaks with more disks than the argmax kernel takes directly: a G*G suppression bit image
+int max_direct_disks();
+void launch_mark_disks(uint32_t* mask, int G, const Disk* disks, int n_disks, int r, cudaStream_t s);
 int blur_block_count();
 // Box-blurred argmax for up to 8 radii at once (voting.cpp:176-216). sat: (G+1)^2 u64 scratch;
 // block_best: [blur_block_count()][8][2]; out_best: [n_radii][2] = (sum, index).

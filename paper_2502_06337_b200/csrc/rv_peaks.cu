@@ -36,7 +36,10 @@ __device__ __forceinline__ bool masked(const DiskSet& d, int x, int y) {
 }
 
 // Also sums every cell (u64) into out_key[1]: the vote's exactness guard (sum == N*J).
+// With `mask` (any number of suppression disks: a G*G bit image maintained by mark_disks_kernel),
+// masked cells are skipped by one bit test; otherwise the (<= kMaxDisks) disks are tested directly.
 __global__ void __launch_bounds__(kArgThreads) argmax_kernel(const uint32_t* grid, int G, DiskSet disks,
+                                                             const uint32_t* mask,
                                                              unsigned long long* block_keys,
                                                              unsigned long long* out_key, unsigned int* done) {
   __shared__ unsigned long long s_red[kArgThreads / 32];
@@ -55,7 +58,8 @@ __global__ void __launch_bounds__(kArgThreads) argmax_kernel(const uint32_t* gri
       for (int k = 0; k < 4; ++k) {
         if (c[k] == 0) continue;
         const int64_t idx = q * 4 + k;
-        if (disks.n && masked(disks, (int)(idx % G), (int)(idx / G))) continue;
+        if (mask ? ((mask[idx >> 5] >> (idx & 31)) & 1u) : (disks.n && masked(disks, (int)(idx % G), (int)(idx / G))))
+          continue;
         best = umax64(best, ((unsigned long long)c[k] << 32) | (0xFFFFFFFFu - (uint32_t)idx));
       }
     }
@@ -64,7 +68,8 @@ __global__ void __launch_bounds__(kArgThreads) argmax_kernel(const uint32_t* gri
       const uint32_t c = grid[idx];
       sum += c;
       if (c == 0) continue;
-      if (disks.n && masked(disks, (int)(idx % G), (int)(idx / G))) continue;
+      if (mask ? ((mask[idx >> 5] >> (idx & 31)) & 1u) : (disks.n && masked(disks, (int)(idx % G), (int)(idx / G))))
+        continue;
       best = umax64(best, ((unsigned long long)c << 32) | (0xFFFFFFFFu - (uint32_t)idx));
     }
   }
@@ -114,6 +119,20 @@ __global__ void __launch_bounds__(kArgThreads) argmax_kernel(const uint32_t* gri
       out_key[1] = ss;
       *done = 0u;
     }
+  }
+}
+
+// Sets the bits of every cell within distance r of each disk centre (clipped to the grid) --
+// find_peaks' suppression (voting.cpp:145-152, the same dx*dx + dy*dy <= r*r disk).
+__global__ void mark_disks_kernel(uint32_t* mask, int G, DiskSet d) {
+  const int side = 2 * d.r + 1;
+  const int k = blockIdx.y;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < side * side; t += gridDim.x * blockDim.x) {
+    const int dx = t % side - d.r, dy = t / side - d.r;
+    const int x = d.cx[k] + dx, y = d.cy[k] + dy;
+    if (dx * dx + dy * dy > d.r2 || x < 0 || x >= G || y < 0 || y >= G) continue;
+    const int64_t idx = (int64_t)y * G + x;
+    atomicOr(&mask[idx >> 5], 1u << (idx & 31));
   }
 }
 
@@ -289,16 +308,33 @@ int argmax_block_count() { return 296; }
 
 void launch_argmax(const uint32_t* grid, int G, const Disk* disks, int n_disks, int r,
                    unsigned long long* block_keys, unsigned long long* out_key, unsigned int* done,
-                   cudaStream_t s) {
+                   cudaStream_t s, const uint32_t* mask) {
   DiskSet d;
-  d.n = n_disks < kMaxDisks ? n_disks : kMaxDisks;
+  d.n = mask ? 0 : (n_disks < kMaxDisks ? n_disks : kMaxDisks);
   d.r = r;
   d.r2 = r * r;
   for (int k = 0; k < d.n; ++k) {
     d.cx[k] = disks[k].cx;
     d.cy[k] = disks[k].cy;
   }
-  argmax_kernel<<<argmax_block_count(), kArgThreads, 0, s>>>(grid, G, d, block_keys, out_key, done);
+  argmax_kernel<<<argmax_block_count(), kArgThreads, 0, s>>>(grid, G, d, mask, block_keys, out_key, done);
+}
+
+int max_direct_disks() { return kMaxDisks; }
+
+void launch_mark_disks(uint32_t* mask, int G, const Disk* disks, int n_disks, int r, cudaStream_t s) {
+  for (int off = 0; off < n_disks; off += kMaxDisks) {
+    DiskSet d;
+    d.n = n_disks - off < kMaxDisks ? n_disks - off : kMaxDisks;
+    d.r = r;
+    d.r2 = r * r;
+    for (int k = 0; k < d.n; ++k) {
+      d.cx[k] = disks[off + k].cx;
+      d.cy[k] = disks[off + k].cy;
+    }
+    const int cells = (2 * r + 1) * (2 * r + 1);
+    mark_disks_kernel<<<dim3((unsigned)((cells + 255) / 256), (unsigned)d.n), 256, 0, s>>>(mask, G, d);
+  }
 }
 
 int blur_block_count() { return 148; }

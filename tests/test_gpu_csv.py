@@ -124,9 +124,18 @@ def test_random_literals_bit_exact(ctx, ref, tmp_path):
     lits = random_literals(rng, 240_000)
     lits = lits[: len(lits) // 6 * 6]
     rows = [",".join(lits[i:i + 6]) for i in range(0, len(lits), 6)]
-    dev, refr = run_both(ctx, ref, write(tmp_path, "r.csv", "\n".join(rows) + "\n"))
+    path = write(tmp_path, "r.csv", "\n".join(rows) + "\n")
+    dev, refr = run_both(ctx, ref, path)
     assert dev[0] == "ok" and dev[1].shape[0] == len(rows)  # rows compared, not just an error
     assert_same(dev, refr)
+
+def test_host_fallback_fields_are_counted(ctx):
+    # fields outside the device's exact fast path (subnormal results, a decimal halfway between
+    # two doubles) are parsed by the host's from_chars and counted
+    ctx.parse_correspondences_device(b"4.9e-324,2.5e-320,9007199254740993,1,2,3\n3,4,5,6,7,8\n")
+    assert ctx.stage_times()["csv_host_fields"] >= 2
+    ctx.parse_correspondences_device(b"1,2,3,4,5,6\n")
+    assert ctx.stage_times()["csv_host_fields"] == 0
 
 
 def test_first_error_line_wins_across_paths(ctx, ref, tmp_path):

@@ -164,6 +164,27 @@ def test_find_peaks_nms_and_mirror(ctx, port):
         ctx.find_peaks(np.zeros((64, 64), np.uint32), 1, 4, 1)
 
 
+def test_find_peaks_any_k(ctx, port):
+    # the reference's find_peaks takes any max_peaks (voting.cpp:120-170): beyond the argmax
+    # kernel's direct disks the suppression becomes a device bit image; K = 40 on a busy grid,
+    # several radii, mirrors included, must match the oracle peak for peak
+    corrs, _, _ = synth.make_config("c5", 20_000)
+    z, _, _ = port.preprocess(corrs)
+    grid = port.accumulate(z)
+    for k, r, mv in ((40, 8, 1), (25, 3, 1), (60, 16, 1), (30, 6, 500)):
+        dev = ctx.find_peaks(grid, k, r, mv)
+        ref = port.find_peaks(grid, k, r, mv)
+        assert [(p.ix, p.iy, p.votes) for p in dev] == [(p[0], p[1], p[4]) for p in ref]
+    # an equatorial ring of peaks: every peak brings its mirror disk
+    g = np.zeros((128, 128), np.uint32)
+    for t in range(24):
+        a = 2 * np.pi * t / 24
+        g[int(64 + 60 * np.sin(a)), int(64 + 60 * np.cos(a))] = 100 + t
+    dev = ctx.find_peaks(g, 24, 2, 1)
+    ref = port.find_peaks(g, 24, 2, 1)
+    assert [(p.ix, p.iy, p.votes) for p in dev] == [(p[0], p[1], p[4]) for p in ref]
+
+
 def test_blurred_argmax_ties_and_edges(ctx, port):
     g = np.zeros((64, 64), np.uint32)
     g[0, 0] = 5
