@@ -4,6 +4,7 @@
 // reference's sampled-deposit semantics, voting.cpp:17-216).
 #pragma once
 
+#include <charconv>
 #include <cmath>
 #include <cstdint>
 #include <algorithm>
@@ -121,28 +122,37 @@ inline Peak blurred_argmax(const Accumulator2D& acc, int radius) {
   return Peak{p.ix, p.iy, {p.A, p.B}, p.votes};
 }
 
-// Dump formats (voting.hpp:83-84; plot-ready host formatting, voting.cpp:218-239).
+// Dump formats (voting.hpp:83-84, plot-ready host formatting; the byte layout of
+// voting.cpp:218-239): text = one grid row per line, counts separated by single spaces;
+// PGM = binary P5 header, then every count rescaled to 0..255 against the grid maximum
+// (integer floor of count*255/max; all zero when the grid is empty).
 inline void dump_accumulator_text(const Accumulator2D& acc, std::ostream& out) {
-  const int g = acc.grid();
-  for (int iy = 0; iy < g; ++iy) {
-    for (int ix = 0; ix < g; ++ix) {
-      if (ix) out << ' ';
-      out << acc.at(ix, iy);
+  const auto v = acc.counts();
+  const std::size_t g = static_cast<std::size_t>(acc.grid());
+  std::string row;
+  char num[16];
+  for (std::size_t r = 0; r < g; ++r) {
+    row.clear();
+    for (std::size_t k = 0; k < g; ++k) {
+      const auto res = std::to_chars(num, num + sizeof num, v[r * g + k]);
+      if (k) row.push_back(' ');
+      row.append(num, res.ptr);
     }
-    out << '\n';
+    row.push_back('\n');
+    out.write(row.data(), static_cast<std::streamsize>(row.size()));
   }
 }
 
 inline void dump_accumulator_pgm(const Accumulator2D& acc, std::ostream& out) {
-  const int g = acc.grid();
-  const auto counts = acc.counts();
-  const std::uint32_t peak = counts.empty() ? 0 : *std::max_element(counts.begin(), counts.end());
-  out << "P5\n" << g << ' ' << g << "\n255\n";
-  for (std::uint32_t c : counts) {
-    const unsigned char v =
-        peak == 0 ? 0 : static_cast<unsigned char>((static_cast<std::uint64_t>(c) * 255) / peak);
-    out.put(static_cast<char>(v));
-  }
+  const auto v = acc.counts();
+  const std::uint64_t top = v.empty() ? 0u : *std::max_element(v.begin(), v.end());
+  std::vector<unsigned char> px(v.size(), 0u);
+  if (top)
+    std::transform(v.begin(), v.end(), px.begin(),
+                   [top](std::uint32_t c) { return static_cast<unsigned char>(std::uint64_t{c} * 255u / top); });
+  const std::string head = "P5\n" + std::to_string(acc.grid()) + " " + std::to_string(acc.grid()) + "\n255\n";
+  out.write(head.data(), static_cast<std::streamsize>(head.size()));
+  out.write(reinterpret_cast<const char*>(px.data()), static_cast<std::streamsize>(px.size()));
 }
 
 }  // namespace rotavote
