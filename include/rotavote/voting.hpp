@@ -6,6 +6,7 @@
 
 #include <charconv>
 #include <cmath>
+#include <functional>
 #include <cstdint>
 #include <algorithm>
 #include <ostream>
@@ -36,17 +37,21 @@ class Accumulator2D {
     if (f == t && i > 0) --i;
     return i < 0 ? 0 : (i > grid_ - 1 ? grid_ - 1 : i);
   }
-  PlanePoint cell_center(int ix, int iy) const {
-    const double cs = cell_size();
-    return {-extent_ + (ix + 0.5) * cs, -extent_ + (iy + 0.5) * cs};
+  PlanePoint cell_center(int ix, int iy) const {  // centre of a cell: -E + (i + 1/2) * cell size
+    auto c = [this](int i) { return -extent_ + (i + 0.5) * cell_size(); };
+    return {c(ix), c(iy)};
   }
   std::uint32_t& at(int ix, int iy) { return counts_[static_cast<std::size_t>(iy) * grid_ + ix]; }
   std::uint32_t at(int ix, int iy) const { return counts_[static_cast<std::size_t>(iy) * grid_ + ix]; }
   std::span<const std::uint32_t> counts() const { return counts_; }
   std::span<std::uint32_t> counts() { return counts_; }
-  std::uint64_t total() const { return std::accumulate(counts_.begin(), counts_.end(), std::uint64_t{0}); }
-  void add(const Accumulator2D& other) {
-    for (std::size_t i = 0; i < counts_.size(); ++i) counts_[i] += other.counts_[i];
+  std::uint64_t total() const {  // 64-bit sum of all cells
+    std::uint64_t t = 0;
+    for (std::uint32_t c : counts_) t += c;
+    return t;
+  }
+  void add(const Accumulator2D& other) {  // cell-wise sum (same grid)
+    std::transform(counts_.begin(), counts_.end(), other.counts_.begin(), counts_.begin(), std::plus<std::uint32_t>());
   }
 
  private:
@@ -67,15 +72,19 @@ struct PeakSet {
   int suppression_radius = 0;
 };
 
-inline std::vector<double> circle_sample_table(int samples) {  // voting.cpp:72-81
-  std::vector<double> table(2 * static_cast<std::size_t>(samples));
-  const double step = 2.0 * std::numbers::pi / samples;
+// Interleaved (cos, sin) of the J circle samples theta_j = -pi + j * (2 pi / J) (voting.cpp:72-81).
+// The angle expression and host libm cos/sin are what the reference evaluates -- any other
+// formula would move sample values by an ulp and change boundary cells.
+inline std::vector<double> circle_sample_table(int samples) {
+  std::vector<double> cs;
+  cs.reserve(2 * static_cast<std::size_t>(samples));
+  const double dtheta = 2.0 * std::numbers::pi / samples;
   for (int j = 0; j < samples; ++j) {
-    const double theta = -std::numbers::pi + j * step;
-    table[2 * j] = std::cos(theta);
-    table[2 * j + 1] = std::sin(theta);
+    const double a = -std::numbers::pi + j * dtheta;
+    cs.push_back(std::cos(a));
+    cs.push_back(std::sin(a));
   }
-  return table;
+  return cs;
 }
 
 inline void deposit_circle_votes(const Vec3& z, Accumulator2D& acc, int samples) {
