@@ -40,6 +40,9 @@ namespace {
 constexpr float kPiF = 3.14159265358979323846f;
 constexpr float kTwoPiF = 6.28318530717958647692f;
 constexpr float kRcMin = 1e-3f;     // |c| amplitude below which a circle is treated as all-band
+#ifndef RV_BCAST_REDUX
+#define RV_BCAST_REDUX 1  // 0: broadcast each entry with shuffles (A/B knob; REDUX measured ~1.5% faster)
+#endif
 #ifndef RV_RED_GROUPS
 #define RV_RED_GROUPS 2
 #endif
@@ -850,12 +853,19 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
         asm volatile("prefetch.global.L1 [%0];" ::"l"(b.basis_b + my_ci));
       }
       for (int kk = 0; kk < ne; ++kk) {
+#if RV_BCAST_REDUX
         const uint32_t enc = __reduce_max_sync(0xFFFFFFFFu, lane == kk ? my_enc : 0u);
         const uint32_t cik = __reduce_max_sync(0xFFFFFFFFu, lane == kk ? my_ci : 0u);
+#else
+        // shuffles for the entry; the loop trip count below goes through REDUX, so the step
+        // loop stays provably warp-uniform
+        const uint32_t enc = __shfl_sync(0xFFFFFFFFu, my_enc, kk);
+        const uint32_t cik = __shfl_sync(0xFFFFFFFFu, my_ci, kk);
+#endif
         ba = __ldg(b.basis_a + cik);
         bb = __ldg(b.basis_b + cik);
         const int start = (int)(enc & 0xFFFFu), len = (int)(enc >> 16);
-        if ((start & 1) | (len & 63)) {  // rare: a range the planner could not align
+        if (__any_sync(0xFFFFFFFFu, (start & 1) | (len & 63))) {  // rare: a range the planner could not align
           const int a0 = start & ~1;
           const int nst = (start + len - a0 + 63) >> 6;
           uint32_t tpm = tab_s + 8u * (uint32_t)a0;
@@ -865,7 +875,8 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
         }
         uint32_t tpf = tab_s + 8u * (uint32_t)start;
 #pragma unroll 1
-        for (int r = len >> 6; r > 0; --r, tpf += 512u) step(tpf, false, cik, 0, 0);
+        for (int r = __reduce_max_sync(0xFFFFFFFFu, (unsigned)len >> 6); r > 0; --r, tpf += 512u)
+          step(tpf, false, cik, 0, 0);
       }
     }
     if (qn > 0) fallback_samples<kClamp, kS>(&s_cold, geo, fbq_s, qn, tab, tile);  // before the flush
