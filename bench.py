@@ -131,8 +131,11 @@ def measured_peaks():
 
 def vote_profile():
     """ncu --set full summary of the vote kernel committed under profiles/ (traffic, issue rate)."""
-    p = ROOT / "profiles" / "r1" / "vote_kernel_ncu.json"
-    return json.loads(p.read_text()) if p.exists() else None
+    for rnd in ("r2", "r1"):  # the latest committed capture
+        p = ROOT / "profiles" / rnd / "vote_kernel_ncu.json"
+        if p.exists():
+            return json.loads(p.read_text())
+    return None
 
 
 def reference_cpu(n_sample: int, reps: int, threads: int, corrs: np.ndarray):

@@ -1,22 +1,25 @@
-# Copy a tools/profile_round.sh bundle (gpurun_out/prof) into profiles/r1 and regenerate the summary.
+# Copy a tools/profile_round.sh bundle (gpurun_out/prof) into profiles/<round> and regenerate the summary.
+# usage: bash tools/refresh_profiles.sh r2
 set -e
-P=profiles/r1
-cp gpurun_out/prof/bench.json $P/bench_r1_c3.json
-cp gpurun_out/prof/bench_ref.json $P/bench_ref_r1.json
-cp gpurun_out/prof/launches.csv $P/launches_r1.csv
-cp gpurun_out/prof/vote_full.ncu-rep $P/vote_banded_r1.ncu-rep
+R=${1:-r2}
+P=profiles/$R
+mkdir -p $P
+cp gpurun_out/prof/bench.json $P/bench_${R}_c3.json
+cp gpurun_out/prof/bench_ref.json $P/bench_ref_${R}.json
+cp gpurun_out/prof/launches.csv $P/launches_${R}.csv
+cp gpurun_out/prof/vote_full.ncu-rep $P/vote_banded_${R}.ncu-rep
 if [ -f gpurun_out/prof/secondary.ncu-rep ]; then
-  cp gpurun_out/prof/secondary.ncu-rep $P/secondary_r1.ncu-rep
-  python tools/summarize_profiles.py --kernels $P/secondary_r1.ncu-rep > $P/SECONDARY_r1.txt
+  cp gpurun_out/prof/secondary.ncu-rep $P/secondary_${R}.ncu-rep
+  python tools/summarize_profiles.py --kernels $P/secondary_${R}.ncu-rep > $P/SECONDARY_${R}.txt
 fi
 [ -f gpurun_out/prof/timeline_c3.txt ] && grep -v Warn gpurun_out/prof/timeline_c3.txt | grep -v _warn_once > $P/timeline_c3_device.txt
 [ -f gpurun_out/prof/timeline_c3_host.txt ] && grep -v Warn gpurun_out/prof/timeline_c3_host.txt | grep -v _warn_once > $P/timeline_c3_e2e.txt
-[ -f gpurun_out/prof/io_bench.json ] && cp gpurun_out/prof/io_bench.json $P/io_bench_r1.json
-[ -f gpurun_out/prof/pytest_gpu.log ] && tail -3 gpurun_out/prof/pytest_gpu.log > $P/pytest_gpu_r1.txt
-[ -f gpurun_out/prof/gpu_check.log ] && cut -c1-600 gpurun_out/prof/gpu_check.log > $P/gpu_check_r1.txt
-python tools/summarize_profiles.py --json $P/vote_banded_r1.ncu-rep | sed "s#\"source\": \"vote_banded_r1.ncu-rep\"#\"source\": \"$P/vote_banded_r1.ncu-rep\"#" > $P/vote_kernel_ncu.json
-{ echo "# Round 1 measurement bundle (tools/profile_round.sh on one B200; see DESIGN.md section 6)"
+[ -f gpurun_out/prof/io_bench.json ] && cp gpurun_out/prof/io_bench.json $P/io_bench_${R}.json
+[ -f gpurun_out/prof/pytest_gpu.log ] && tail -3 gpurun_out/prof/pytest_gpu.log > $P/pytest_gpu_${R}.txt
+[ -f gpurun_out/prof/gpu_check.log ] && cut -c1-600 gpurun_out/prof/gpu_check.log > $P/gpu_check_${R}.txt
+python tools/summarize_profiles.py --json $P/vote_banded_${R}.ncu-rep | sed "s#\"source\": \"vote_banded_${R}.ncu-rep\"#\"source\": \"$P/vote_banded_${R}.ncu-rep\"#" > $P/vote_kernel_ncu.json
+{ echo "# Round $R measurement bundle (tools/profile_round.sh on one B200; see DESIGN.md section 6)"
   echo "# launch list = ncu of 'python bench.py --steps 2 --warmup 3 --no-cpu' (device solves AND pipelined e2e"
-  echo "# solves, whose vote runs in 4 chunks: per-launch averages mix both; shares are what matter)"
-  python tools/summarize_profiles.py $P/launches_r1.csv $P/vote_banded_r1.ncu-rep; } > $P/SUMMARY_r1.txt
+  echo "# solves, whose vote runs in 4 chunks from pinned input: per-launch averages mix both; shares are what matter)"
+  python tools/summarize_profiles.py $P/launches_${R}.csv $P/vote_banded_${R}.ncu-rep; } > $P/SUMMARY_${R}.txt
 echo refreshed
