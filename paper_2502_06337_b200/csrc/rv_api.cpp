@@ -639,6 +639,20 @@ std::vector<Peak> find_peaks_dev(rv_context* c, const uint32_t* grid, int G, dou
   return out;
 }
 
+// A failed exactness guard (the planner under- or over-covered a sample) is counted and repaired by
+// an exact re-vote; RV_STRICT_GUARD=1 (the GPU test-suite) turns it into an error instead, so a
+// coverage bug cannot hide behind the repair.
+void guard_failed(rv_context* c, unsigned long long total, unsigned long long expect) {
+  static const bool strict = [] {
+    const char* e = std::getenv("RV_STRICT_GUARD");
+    return e && e[0] == '1';
+  }();
+  c->times.vote_guard_reruns += 1;
+  if (strict)
+    fail(RV_ERR_CUDA, "exactness guard: vote grid sums to " + std::to_string(total) + ", expected " +
+                          std::to_string(expect) + " (RV_STRICT_GUARD)");
+}
+
 // accumulate + find_peaks(K=1) with the exactness guard: every constraint deposits exactly J
 // votes (voting.cpp:33-44), so the grid must sum to n*J. If the band planner ever under-covered a
 // sample the sum would be short: the vote is then redone with the generic exact kernel.
@@ -668,7 +682,7 @@ std::pair<const uint32_t*, std::vector<Peak>> vote_and_peak(rv_context* c, const
       }
     }
     if (total == (unsigned long long)n * (unsigned long long)cfg.theta_samples) return {grid, peaks};
-    c->times.vote_guard_reruns += 1;
+    guard_failed(c, total, (unsigned long long)n * (unsigned long long)cfg.theta_samples);
   }
   fail(RV_ERR_CUDA, "vote grid total mismatch after exact rerun");
 }
@@ -1689,7 +1703,8 @@ Estimate complete_single(rv_context* c, const PreResult& pre, const double* d_co
     }
   }
   if (sm.pk.total != (unsigned long long)n_kept * (unsigned long long)cfg.theta_samples) {
-    c->times.vote_guard_reruns += 1;  // exactness guard: redo with the generic exact vote
+    // exactness guard: redo with the generic exact vote
+    guard_failed(c, sm.pk.total, (unsigned long long)n_kept * (unsigned long long)cfg.theta_samples);
     if (pre.inorder) {  // ... over the compacted constraint set
       const PreResult pc = preprocess_dev(c, d_corrs, cs.n, cfg.tau_z, cfg.normalize_inputs);
       return finish_single_stepped(c, pc, d_corrs, cfg, nullptr, 1);

@@ -43,6 +43,9 @@ constexpr float kRcMin = 1e-3f;     // |c| amplitude below which a circle is tre
 #ifndef RV_BCAST_REDUX
 #define RV_BCAST_REDUX 1  // 0: broadcast each entry with shuffles (A/B knob; REDUX measured ~1.5% faster)
 #endif
+#ifndef RV_UNIFORM_STEP
+#define RV_UNIFORM_STEP 1
+#endif
 #ifndef RV_RED_GROUPS
 #define RV_RED_GROUPS 2
 #endif
@@ -167,29 +170,47 @@ struct Arc2 {
 
 // The trig part of { s in [0, pi] : A cos(theta_a + s) + B sin(theta_a + s) >= y0 } (on the
 // canonical arc this is { Y(s) >= y0 }, since 1 - c > 0 there), solved ONCE per band boundary and
-// then dilated (lower set of the band above) or eroded (upper set of the band below).
-// state 0: empty, 1: all of [0, pi], 2: sig +- alpha. A ratio within 2e-5 above 1 still counts as a
-// (tangent) visit: the f32 error of y0/R is ~3e-7, so no near-tangent visit is ever lost.
+// then dilated (lower set of the band above) or eroded (upper set of the band below). A, B and y0
+// carry f32 errors (~4e-7 absolute), so the two uses solve shifted levels: the SUPERSET solves
+// y0 - kArcSlack, the SUBSET y0 + kArcSlack. This keeps both sides right where the level is
+// ill-conditioned -- a near-constant Y (R ~ 0, e.g. z = +-e2 gives Y == 0 on a band boundary) and
+// near-tangent visits -- on top of the angular dilation for the trig errors.
+// state 0: empty, 1: all of [0, pi], 2: sig +- alpha.
 struct ArcG {
-  float sig, alpha;
-  int state;
+  float sig, a_sup, a_sub;
+  int st_sup, st_sub;
 };
 constexpr float kArcDilate = 2e-3f;  // >> acos/atan2_fast error near tangency (~8e-4 rad)
+constexpr float kArcSlack = 2e-6f;   // >> the f32 error of A cos + B sin - y0 (plane units)
 __device__ __forceinline__ ArcG arc_solve(float A, float B, float y0, float theta_a) {
   const float R = sqrtf(fmaf(A, A, B * B));
-  if (!(R > 0.f)) return ArcG{0.f, 0.f, y0 <= 0.f ? 1 : 0};
-  const float ratio = __fdividef(y0, R);
-  if (ratio <= -1.f) return ArcG{0.f, 0.f, 1};
-  if (!(ratio < 1.00002f)) return ArcG{0.f, 0.f, 0};
-  float sig = atan2_fast(B, A) - theta_a;
-  sig -= kTwoPiF * floorf((sig + kPiF) * (1.f / kTwoPiF));
-  return ArcG{sig, acos_fast(fminf(ratio, 1.f)), 2};
+  ArcG g{0.f, 0.f, 0.f, 0, 0};
+  const float lo = y0 - kArcSlack, hi = y0 + kArcSlack;
+  if (!(R > 0.f)) {
+    g.st_sup = lo <= 0.f ? 1 : 0;
+    g.st_sub = hi <= 0.f ? 1 : 0;
+    return g;
+  }
+  const float inv = __fdividef(1.f, R);
+  const float r_sup = lo * inv, r_sub = hi * inv;
+  g.st_sup = r_sup <= -1.f ? 1 : (r_sup < 1.f ? 2 : 0);
+  g.st_sub = r_sub <= -1.f ? 1 : (r_sub < 1.f ? 2 : 0);
+  if (g.st_sup == 2 || g.st_sub == 2) {
+    float sig = atan2_fast(B, A) - theta_a;
+    sig -= kTwoPiF * floorf((sig + kPiF) * (1.f / kTwoPiF));
+    g.sig = sig;
+    g.a_sup = acos_fast(fmaxf(r_sup, -1.f));
+    g.a_sub = acos_fast(fminf(r_sub, 1.f));
+  }
+  return g;
 }
 __device__ __forceinline__ Arc2 arc_dilate(const ArcG& g, float dil) {
   Arc2 r{0.f, 0.f, 0.f, 0.f, 0};
-  if (g.state == 1) return Arc2{0.f, kPiF, 0.f, 0.f, 1};
-  if (g.state == 0) return r;
-  const float half = g.alpha + dil;
+  const int st = dil > 0.f ? g.st_sup : g.st_sub;
+  if (st == 1) return Arc2{0.f, kPiF, 0.f, 0.f, 1};
+  if (st == 0) return r;
+  const float half = (dil > 0.f ? g.a_sup : g.a_sub) + dil;
+  if (half < 0.f) return r;
   const float lo0 = fmaxf(g.sig - half, 0.f), hi0 = fminf(g.sig + half, kPiF);
   const float lo1 = fmaxf(g.sig - half + kTwoPiF, 0.f), hi1 = fminf(g.sig + half + kTwoPiF, kPiF);
   if (lo0 <= hi0) {
@@ -476,12 +497,12 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const unsigned long long ci = (unsigned long long)(uint32_t)i;
-  ArcG g_lo{0.f, 0.f, 1};  // band 0: Y >= -inf
+  ArcG g_lo{0.f, 0.f, 0.f, 1, 1};  // band 0: Y >= -inf
   // entries of this constraint in band `band` (+ planned samples into *w)
   auto plan_band = [&](int band, unsigned long long* w) -> Ent3 {
     if (!valid) return Ent3{0u, 0u, 0u};
     if (polar) return finalize_runs(Runs2{A0, A1, 0, 0, 1}, A0, A1, J, w);
-    ArcG g_hi{0.f, 0.f, 0};  // last band: Y >= +inf is empty
+    ArcG g_hi{0.f, 0.f, 0.f, 0, 0};  // last band: Y >= +inf is empty
     if (band < p.n_bands - 1) {
       const float y1 = p.band_ylo[band + 1];
       g_hi = arc_solve(fmaf(y1, f1z, f1y), fmaf(y1, f2z, f2y), y1, theta_a);
@@ -816,21 +837,28 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
       red_shared(tile_s + 4u * umin(rel[1], sink_rel), vote2);
       if (__any_sync(0xFFFFFFFFu, flag[0] | flag[1])) {  // cold: queue for the exact f64 path
         // queue entries are (constraint, sample), so the queue outlives the grab; it is drained
-        // before it would pass 32 entries (one exact-path batch = one sample per lane)
+        // before it would pass 32 entries (one exact-path batch = one sample per lane). Both
+        // samples of the step are compacted at once (one capacity check).
         const uint32_t j = (uint32_t)((tpa - tab_s) >> 3) + 2u * lane;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const unsigned fm = __ballot_sync(0xFFFFFFFFu, flag[h]);
-          const int c = __popc(fm);
-          if (qn + c > 32) {
-            fallback_samples<kClamp, kS>(&s_cold, geo, fbq_s, qn, tab, tile);
-            qn = 0;
-          }
-          if (flag[h]) sts_u2(fbq_s + 8u * (uint32_t)(qn + __popc(fm & lt_mask)), cik, j + h);
-          qn += c;
-          my_fb += c;
-          __syncwarp();
+        const unsigned fm0 = __ballot_sync(0xFFFFFFFFu, flag[0]), fm1 = __ballot_sync(0xFFFFFFFFu, flag[1]);
+        const int c0 = __popc(fm0), c = c0 + __popc(fm1);
+        if (qn + c > 32) {
+          fallback_samples<kClamp, kS>(&s_cold, geo, fbq_s, qn, tab, tile);
+          qn = 0;
         }
+        if (c <= 32) {
+          if (flag[0]) sts_u2(fbq_s + 8u * (uint32_t)(qn + __popc(fm0 & lt_mask)), cik, j);
+          if (flag[1]) sts_u2(fbq_s + 8u * (uint32_t)(qn + c0 + __popc(fm1 & lt_mask)), cik, j + 1u);
+          qn += c;
+        } else {  // more than 32 flagged samples in one step (never seen): two batches
+          if (flag[0]) sts_u2(fbq_s + 8u * (uint32_t)__popc(fm0 & lt_mask), cik, j);
+          __syncwarp();
+          fallback_samples<kClamp, kS>(&s_cold, geo, fbq_s, c0, tab, tile);
+          if (flag[1]) sts_u2(fbq_s + 8u * (uint32_t)__popc(fm1 & lt_mask), cik, j + 1u);
+          qn = c - c0;
+        }
+        my_fb += c;
+        __syncwarp();
       }
     };
     // grab loop / entry loop / step loop
@@ -865,7 +893,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
         ba = __ldg(b.basis_a + cik);
         bb = __ldg(b.basis_b + cik);
         const int start = (int)(enc & 0xFFFFu), len = (int)(enc >> 16);
-        if (__any_sync(0xFFFFFFFFu, (start & 1) | (len & 63))) {  // rare: a range the planner could not align
+        if ((start & 1) | (len & 63)) {  // rare: a range the planner could not align (enc is uniform)
           const int a0 = start & ~1;
           const int nst = (start + len - a0 + 63) >> 6;
           uint32_t tpm = tab_s + 8u * (uint32_t)a0;
@@ -873,10 +901,19 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
           for (int q = 0; q < nst; ++q, tpm += 512u) step(tpm, true, cik, start, len);
           continue;
         }
+#if RV_UNIFORM_STEP
+        // uniform step offset (UR): the loop is one UIADD3 + UISETP + BRA.U, the lane's table
+        // address is its fixed base + the offset
+        const uint32_t u0 = 8u * (uint32_t)start;
+        const uint32_t uend = u0 + 8u * (uint32_t)len;  // len is a multiple of 64 here
+#pragma unroll 1
+        for (uint32_t u = u0; u != uend; u += 512u) step(tab_s + u, false, cik, 0, 0);
+#else
         uint32_t tpf = tab_s + 8u * (uint32_t)start;
 #pragma unroll 1
         for (int r = __reduce_max_sync(0xFFFFFFFFu, (unsigned)len >> 6); r > 0; --r, tpf += 512u)
           step(tpf, false, cik, 0, 0);
+#endif
       }
     }
     if (qn > 0) fallback_samples<kClamp, kS>(&s_cold, geo, fbq_s, qn, tab, tile);  // before the flush

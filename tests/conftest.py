@@ -1,4 +1,5 @@
 """Shared fixtures. `-m "not gpu"` runs here (no GPU); `-m gpu` runs on a B200 through the C-ABI."""
+import os
 import sys
 from pathlib import Path
 
@@ -10,6 +11,11 @@ GOLDEN = ROOT / "tests" / "golden"
 for p in (str(ROOT), str(ROOT / "oracle")):
     if p not in sys.path:
         sys.path.insert(0, p)
+
+
+# a failed vote exactness guard (band-plan coverage bug) is an error in the tests, not a silent
+# exact re-vote (rv_api.cpp guard_failed)
+os.environ.setdefault("RV_STRICT_GUARD", "1")
 
 
 def pytest_configure(config):

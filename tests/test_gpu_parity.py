@@ -68,6 +68,40 @@ def test_accumulate_adversarial_constraints(ctx, port):
         assert np.array_equal(ctx.accumulate(z, grid, 1.05, samples), port.accumulate(z, grid, 1.05, samples))
 
 
+def tangent_constraints(grid: int, extent: float) -> np.ndarray:
+    """Great circles whose projected arc is tangent (from above and below) to EVERY grid row
+    boundary Y = -E + r * 2E/G inside the unit disk: the planner's band boundaries are among them,
+    and a tangent visit is its ill-conditioned case. The image of the great circle with unit normal
+    n is the circle of centre -(nx, ny)/nz and radius 1/|nz| (stereographic projection)."""
+    out = []
+    cs = 2.0 * extent / grid
+    for r in range(1, grid):
+        y0 = -extent + r * cs
+        if abs(y0) >= 0.999 or abs(y0) < 1e-9:
+            continue
+        for cx in (0.0, 0.4 * np.sqrt(1.0 - y0 * y0)):
+            for top in (True, False):  # the circle's top (bottom) point touches Y = y0
+                cy = (y0 * y0 - 1.0 - cx * cx) / (2.0 * y0) if top else (1.0 + cx * cx - y0 * y0) / (2.0 * y0)
+                rad = np.sqrt(1.0 + cx * cx + cy * cy)
+                if (top and not (y0 - cy > 0)) or (not top and not (cy - y0 > 0)) or abs(abs(cy + (rad if top else -rad)) - abs(y0)) > 1e-9:
+                    continue
+                nz = 1.0 / rad
+                out.append([-cx * nz, -cy * nz, nz])
+    z = np.array(out)
+    return z / np.linalg.norm(z, axis=1, keepdims=True)
+
+
+@pytest.mark.parametrize("grid,extent,samples", [(512, 1.05, 2048), (256, 1.05, 1024), (1024, 1.05, 4096),
+                                                 (200, 0.9, 1024)])
+def test_accumulate_row_boundary_tangents(ctx, port, grid, extent, samples):
+    # tangent visits of every row boundary (so of every band boundary) plus z = +-e2, whose arc is
+    # the row boundary Y = 0 itself when G/2 is a band boundary; with RV_STRICT_GUARD a coverage
+    # gap of the band plan is an error, not a silent exact re-vote
+    z = np.concatenate([tangent_constraints(grid, extent), [[0.0, 1.0, 0.0], [0.0, -1.0, 0.0]]])
+    assert z.shape[0] > grid
+    assert np.array_equal(ctx.accumulate(z, grid, extent, samples), port.accumulate(z, grid, extent, samples))
+
+
 @pytest.mark.parametrize("key", ["c1", "c2", "c3", "c4", "c5"])
 def test_config_golden(ctx, key):
     g = golden(key)
