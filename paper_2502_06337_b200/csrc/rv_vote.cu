@@ -148,6 +148,11 @@ __device__ __forceinline__ float atan2_fast(float y, float x) {
   if (x < 0.f) r = 3.14159274f - r;
   return y < 0.f ? -r : r;
 }
+__device__ __forceinline__ float sqrt_approx(float x) {  // MUFU.SQRT, ~1 ulp: fine for culling
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ float acos_fast(float x) {  // Abramowitz-Stegun 4.4.46, |err| <= 2e-8 (+f32)
   const float ax = fminf(fabsf(x), 1.f);
   float p = -0.0012624911f;
@@ -158,204 +163,164 @@ __device__ __forceinline__ float acos_fast(float x) {  // Abramowitz-Stegun 4.4.
   p = fmaf(p, ax, 0.0889789874f);
   p = fmaf(p, ax, -0.2145988016f);
   p = fmaf(p, ax, 1.5707963050f);
-  const float r = sqrtf(1.f - ax) * p;
+  const float r = sqrt_approx(1.f - ax) * p;
   return x < 0.f ? kPiF - r : r;
 }
 
-// Up to two disjoint, sorted intervals of s in [0, pi] (register-resident, no dynamic indexing).
-struct Arc2 {
-  float a0, b0, a1, b1;
-  int n;
+// One band boundary (level y0) in SAMPLE space on the whole circle (sample u <-> theta = -pi +
+// u * step). For every sample, Y >= y0 on the canonical arc (where 1 - c > 0) is equivalent to
+// A cos(theta) + B sin(theta) >= y0 with A = a1y + y0 a1z, B = a2y + y0 a2z -- on the whole circle
+// this is the stereographic image of the UNflipped point, so the level sets of all boundaries are
+// single arcs centred at atan2(B, A), NESTED in y0. A, B and y0 carry f32 errors (~4e-7 absolute),
+// so the two uses solve shifted levels: the OUTER arc (a superset: the band above) solves
+// y0 - kArcSlack and is dilated, the INNER arc (a subset: the band below subtracts it) solves
+// y0 + kArcSlack and is eroded -- by kArcDilate (>> the fast-trig error, incl. near tangency) plus
+// kPad samples. This keeps both sides right where the level is ill-conditioned: near-tangent
+// visits, and a near-constant A cos + B sin (R ~ 0: z = +-e2 has Y == 0 on a band boundary).
+// State: 0 empty, 1 the whole circle, 2 the arc [lo, hi] (integers, unwrapped around c).
+struct Bnd {
+  int olo, ohi, ilo, ihi;
+  int ost, ist;
+  float c;
+};
+constexpr float kArcDilate = 2e-3f;  // rad, >> acos/atan2_fast error near tangency (~8e-4 rad)
+constexpr float kArcSlack = 2e-6f;   // plane units, >> the f32 error of A cos + B sin - y0
+__device__ __forceinline__ Bnd band_boundary(float A, float B, float y0, float inv_step, float pad_s, int J) {
+  Bnd r;
+  const float R = sqrt_approx(fmaf(A, A, B * B));
+  const float lo = y0 - kArcSlack, hi = y0 + kArcSlack;
+  float r_sup, r_sub;
+  if (R > 0.f) {
+    const float inv = __fdividef(1.f, R);
+    r_sup = lo * inv;
+    r_sub = hi * inv;
+  } else {  // constant 0 >= level: decided by the level's sign
+    r_sup = lo <= 0.f ? -2.f : 2.f;
+    r_sub = hi <= 0.f ? -2.f : 2.f;
+  }
+  r.ost = r_sup <= -1.f ? 1 : (r_sup < 1.f ? 2 : 0);
+  r.ist = r_sub <= -1.f ? 1 : (r_sub < 1.f ? 2 : 0);
+  r.c = (atan2_fast(B, A) + kPiF) * inv_step;
+  const float wo = acos_fast(fmaxf(r_sup, -1.f)) * inv_step + pad_s;
+  const float wi = acos_fast(fminf(r_sub, 1.f)) * inv_step - pad_s;
+  r.olo = __float2int_rd(r.c - wo);
+  r.ohi = __float2int_ru(r.c + wo);
+  if (r.ost == 2 && r.ohi - r.olo + 1 >= J) r.ost = 1;  // the dilated arc covers the circle
+  r.ilo = __float2int_ru(r.c - wi);
+  r.ihi = __float2int_rd(r.c + wi);
+  if (r.ist == 2 && r.ilo > r.ihi) r.ist = 0;  // eroded to nothing
+  return r;
+}
+
+// Up to two inclusive sample runs (increasing) inside the canonical arc [A0, A1] (n = 0, 1, 2).
+struct Runs2 {
+  int l0, h0, l1, h1, n;
+};
+// Entries (start | len << 16, start in [0, J)) of one band: e0 / e1 from the first / second run,
+// e2 the part of a run past the wrap at J (at most one run crosses J); zero = none.
+struct Ent3 {
+  uint32_t e0, e1, e2;
 };
 
-// The trig part of { s in [0, pi] : A cos(theta_a + s) + B sin(theta_a + s) >= y0 } (on the
-// canonical arc this is { Y(s) >= y0 }, since 1 - c > 0 there), solved ONCE per band boundary and
-// then dilated (lower set of the band above) or eroded (upper set of the band below). A, B and y0
-// carry f32 errors (~4e-7 absolute), so the two uses solve shifted levels: the SUPERSET solves
-// y0 - kArcSlack, the SUBSET y0 + kArcSlack. This keeps both sides right where the level is
-// ill-conditioned -- a near-constant Y (R ~ 0, e.g. z = +-e2 gives Y == 0 on a band boundary) and
-// near-tangent visits -- on top of the angular dilation for the trig errors.
-// state 0: empty, 1: all of [0, pi], 2: sig +- alpha.
-struct ArcG {
-  float sig, a_sup, a_sub;
-  int st_sup, st_sub;
-};
-constexpr float kArcDilate = 2e-3f;  // >> acos/atan2_fast error near tangency (~8e-4 rad)
-constexpr float kArcSlack = 2e-6f;   // >> the f32 error of A cos + B sin - y0 (plane units)
-__device__ __forceinline__ ArcG arc_solve(float A, float B, float y0, float theta_a) {
-  const float R = sqrtf(fmaf(A, A, B * B));
-  ArcG g{0.f, 0.f, 0.f, 0, 0};
-  const float lo = y0 - kArcSlack, hi = y0 + kArcSlack;
-  if (!(R > 0.f)) {
-    g.st_sup = lo <= 0.f ? 1 : 0;
-    g.st_sub = hi <= 0.f ? 1 : 0;
-    return g;
-  }
-  const float inv = __fdividef(1.f, R);
-  const float r_sup = lo * inv, r_sub = hi * inv;
-  g.st_sup = r_sup <= -1.f ? 1 : (r_sup < 1.f ? 2 : 0);
-  g.st_sub = r_sub <= -1.f ? 1 : (r_sub < 1.f ? 2 : 0);
-  if (g.st_sup == 2 || g.st_sub == 2) {
-    float sig = atan2_fast(B, A) - theta_a;
-    sig -= kTwoPiF * floorf((sig + kPiF) * (1.f / kTwoPiF));
-    g.sig = sig;
-    g.a_sup = acos_fast(fmaxf(r_sup, -1.f));
-    g.a_sub = acos_fast(fminf(r_sub, 1.f));
-  }
-  return g;
+// The part of the circle run [x, y] (y - x < J) inside the canonical arc [A0, A1] (unwrapped,
+// A1 - A0 < J): a main piece [m_lo, m_hi] and, when the run wraps past A0 + J, the piece
+// [A0, w_hi] at the arc start (empty pieces: m_lo > m_hi, w_hi < A0).
+__device__ __forceinline__ void canon_pieces(int x, int y, int A0, int A1, int J, int* m_lo, int* m_hi,
+                                             int* w_hi) {
+  int t = x - A0;  // in (-2J, 2J): reduce mod J without a division
+  t += t < 0 ? J : 0;
+  t += t < 0 ? J : 0;
+  t -= t >= J ? J : 0;
+  const int xs = A0 + t, ys = xs + (y - x);
+  *m_lo = xs;
+  *m_hi = min(ys, A1);
+  *w_hi = min(A1, ys - J);
 }
-__device__ __forceinline__ Arc2 arc_dilate(const ArcG& g, float dil) {
-  Arc2 r{0.f, 0.f, 0.f, 0.f, 0};
-  const int st = dil > 0.f ? g.st_sup : g.st_sub;
-  if (st == 1) return Arc2{0.f, kPiF, 0.f, 0.f, 1};
-  if (st == 0) return r;
-  const float half = (dil > 0.f ? g.a_sup : g.a_sub) + dil;
-  if (half < 0.f) return r;
-  const float lo0 = fmaxf(g.sig - half, 0.f), hi0 = fminf(g.sig + half, kPiF);
-  const float lo1 = fmaxf(g.sig - half + kTwoPiF, 0.f), hi1 = fminf(g.sig + half + kTwoPiF, kPiF);
-  if (lo0 <= hi0) {
-    r.a0 = lo0;
-    r.b0 = hi0;
-    r.n = 1;
-    if (lo1 <= hi1) {
-      r.a1 = lo1;
-      r.b1 = hi1;
-      r.n = 2;
+
+// Sample runs of band b inside the canonical arc: the outer arc of its lower boundary minus the
+// inner arc of its upper boundary (nested on the circle: at most two circle runs), intersected
+// with [A0, A1]. The pieces are disjoint; touching ones are merged, and three are merged to two
+// across the smaller gap (a superset: the vote's row test decides every deposit). Straight-line
+// code (selects): the warp's lanes stay converged.
+__device__ __forceinline__ Runs2 band_runs(const Bnd& lo_b, const Bnd& hi_b, int A0, int A1, int J) {
+  const bool none = lo_b.ost == 0 || hi_b.ist == 1 || A0 > A1;
+  const bool in_empty = hi_b.ist == 0, out_full = lo_b.ost == 1;
+  const float d = hi_b.c - lo_b.c;  // the inner arc next to the outer one (same turn)
+  const int sh = d > 0.5f * (float)J ? -J : (d < -0.5f * (float)J ? J : 0);
+  // circle run 0: the outer arc, the whole circle from A0, the circle minus the inner arc, or the
+  // part of the outer arc before the inner one; circle run 1: the part after it
+  const int x0 = out_full ? (in_empty ? A0 : hi_b.ihi + 1) : lo_b.olo;
+  const int y0 = out_full ? (in_empty ? A0 + J - 1 : hi_b.ilo - 1 + J) : (in_empty ? lo_b.ohi : hi_b.ilo + sh - 1);
+  const int x1 = hi_b.ihi + sh + 1, y1 = lo_b.ohi;
+  const bool v0 = !none && x0 <= y0, v1 = !none && !out_full && !in_empty && x1 <= y1;
+  int m0lo, m0hi, w0, m1lo, m1hi, w1;
+  canon_pieces(x0, y0, A0, A1, J, &m0lo, &m0hi, &w0);
+  canon_pieces(x1, y1, A0, A1, J, &m1lo, &m1hi, &w1);
+  // pieces in increasing order: the wrapped one at A0 (at most one run wraps), then the mains
+  const int wh = max(v0 ? w0 : A0 - 1, v1 ? w1 : A0 - 1);
+  const bool pw = wh >= A0;
+  const bool p0 = v0 && m0lo <= m0hi, p1 = v1 && m1lo <= m1hi;
+  const bool sw = p1 && (!p0 || m1lo < m0lo);
+  const int alo = sw ? m1lo : m0lo, ahi = sw ? m1hi : m0hi, blo = sw ? m0lo : m1lo, bhi = sw ? m0hi : m1hi;
+  const bool pa = p0 || p1, pb = p0 && p1;
+  // compact the valid pieces into c0 <= c1 (<= the third, blo..bhi)
+  const int c0lo = pw ? A0 : alo, c0hi = pw ? wh : ahi;
+  const int c1lo = pw ? alo : blo, c1hi = pw ? ahi : bhi;
+  const int k = (int)pw + (int)pa + (int)pb;
+  Runs2 r{c0lo, c0hi, c1lo, c1hi, min(k, 2)};
+  if (k == 3) {  // merge across the smaller gap
+    if (c1lo - c0hi <= blo - c1hi) {
+      r.h0 = c1hi;
+      r.l1 = blo;
+      r.h1 = bhi;
+    } else {
+      r.h1 = bhi;
     }
-  } else if (lo1 <= hi1) {
-    r.a0 = lo1;
-    r.b0 = hi1;
+  }
+  if (r.n == 2 && r.l1 <= r.h0 + 1) {  // touching
+    r.h0 = max(r.h0, r.h1);
     r.n = 1;
   }
   return r;
 }
 
-// Up to two inclusive sample ranges (increasing), clipped to the exact canonical arc [A0, A1];
-// a third disjoint range is merged into its nearer neighbour (a superset: every evaluated sample is
-// canonical, and the row ownership test decides the deposit).
-struct Runs2 {
-  int l0, h0, l1, h1, n;
-};
-__device__ __forceinline__ void runs_push(Runs2& r, int lo, int hi, int A0, int A1) {
-  lo = max(lo, A0);
-  hi = min(hi, A1);
-  if (lo > hi) return;
-  if (r.n == 0) {
-    r.l0 = lo;
-    r.h0 = hi;
-    r.n = 1;
-  } else if (r.n == 1) {
-    if (lo <= r.h0 + 1) r.h0 = max(r.h0, hi);
-    else {
-      r.l1 = lo;
-      r.h1 = hi;
-      r.n = 2;
-    }
-  } else if (lo <= r.h1 + 1) {
-    r.h1 = max(r.h1, hi);
-  } else if (r.l1 - r.h0 <= lo - r.h1) {  // close the smaller gap
-    r.h0 = r.h1;
-    r.l1 = lo;
-    r.h1 = hi;
-  } else {
-    r.h1 = hi;
-  }
-}
-
-// Entries (start | len << 16, start in [0, J)) of one band from its lower/upper arc sets:
-// S = U_lo \ U_hi mapped to sample indices u = pa + s/step, padded, clipped to the canonical arc,
-// merged, and split where the sample index wraps at J. Up to 3 entries (zero = none).
-struct Ent3 {
-  uint32_t e0, e1, e2;
-};
-__device__ __forceinline__ void ent_put(Ent3& o, int& k, int lo, int hi, int J) {
-  const uint32_t v = (uint32_t)lo | ((uint32_t)(hi - lo + 1) << 16);
-  if (k == 0) o.e0 = v;
-  else if (k == 1) o.e1 = v;
-  else o.e2 = v;
-  ++k;
-}
 // Final entries of one band from its (<= 2) runs inside the canonical arc [A0, A1] (A0 even, A1
 // odd): each run is widened to an even start and a whole number of 64-sample steps where the arc
 // and the neighbouring run leave room (extra samples are canonical and land outside the band, in
 // the vote's sink -- they never overlap another entry of this constraint and band, so nothing is
 // counted twice), then split where the sample index wraps at J, at a step boundary (the last step
 // before the wrap reads the table's 64-sample slack), so the vote's step grid never shifts.
-__device__ __forceinline__ Ent3 finalize_runs(const Runs2& runs, int A0, int A1, int J,
-                                              unsigned long long* work) {
-  Ent3 o{0u, 0u, 0u};
-  int k = 0;
-  int prev_hi = A0 - 1;
-  for (int r = 0; r < runs.n; ++r) {
-    int lo = (r == 0 ? runs.l0 : runs.l1) & ~1;
-    int hi = (r == 0 ? runs.h0 : runs.h1) | 1;
-    const int ub = (r == 0 && runs.n == 2) ? (runs.l1 & ~1) - 1 : A1;
-    lo = max(lo, prev_hi + 1);
-    int need = ((hi - lo + 64) & ~63) - (hi - lo + 1);
-    const int up = min(need, ub - hi);
-    hi += up;
-    need -= up;
-    lo -= min(need, lo - (prev_hi + 1));
-    prev_hi = hi;
-    *work += (unsigned long long)((hi - lo + 64) & ~63);
-    if (hi < J) {
-      ent_put(o, k, lo, hi, J);
-    } else if (lo >= J) {
-      ent_put(o, k, lo - J, hi - J, J);
-    } else {
-      const int cut = lo + (((J - lo) + 63) & ~63);  // first step boundary at or after J
-      if (cut > hi) {
-        ent_put(o, k, lo, hi, J);  // its last step crosses J: read from the slack
-      } else {
-        ent_put(o, k, lo, cut - 1, J);
-        ent_put(o, k, cut - J, hi - J, J);
-      }
-    }
-  }
-  return o;
+// Straight-line over two run slots.
+__device__ __forceinline__ void finalize_run(int lo, int hi, int prev_hi, int ub, int J, uint32_t* ea, uint32_t* eb,
+                                             int* hi_out, unsigned long long* work) {
+  lo = max(lo & ~1, prev_hi + 1);
+  hi |= 1;
+  int need = ((hi - lo + 64) & ~63) - (hi - lo + 1);
+  const int up = min(need, ub - hi);
+  hi += up;
+  need -= up;
+  lo -= min(need, lo - (prev_hi + 1));
+  *hi_out = hi;
+  *work += (unsigned long long)((hi - lo + 64) & ~63);
+  const int cut = lo + (((J - lo) + 63) & ~63);  // first step boundary at or after J
+  const bool below = hi < J, above = lo >= J, split = !below && !above && cut <= hi;
+  const int s0 = above ? lo - J : lo, h0 = above ? hi - J : (split ? cut - 1 : hi);
+  *ea = (uint32_t)s0 | ((uint32_t)(h0 - s0 + 1) << 16);
+  *eb = split ? ((uint32_t)(cut - J) | ((uint32_t)(hi - cut + 1) << 16)) : 0u;
 }
-
-__device__ __forceinline__ Ent3 entries_from_sets(const Arc2& ulo, const Arc2& uhi, float pa, float inv_step, int A0,
-                                                  int A1, int J, unsigned long long* work) {
-  // gaps of uhi inside [0, pi] (sorted): [0, a0], [b0, a1], [b_last, pi]
-  float g[6];
-  int ng;
-  if (uhi.n == 0) {
-    g[0] = 0.f;
-    g[1] = kPiF;
-    ng = 1;
-  } else if (uhi.n == 1) {
-    g[0] = 0.f;
-    g[1] = uhi.a0;
-    g[2] = uhi.b0;
-    g[3] = kPiF;
-    ng = 2;
-  } else {
-    g[0] = 0.f;
-    g[1] = uhi.a0;
-    g[2] = uhi.b0;
-    g[3] = uhi.a1;
-    g[4] = uhi.b1;
-    g[5] = kPiF;
-    ng = 3;
-  }
-  const float lo_a[2] = {ulo.a0, ulo.a1}, lo_b[2] = {ulo.b0, ulo.b1};
-  Runs2 runs{0, 0, 0, 0, 0};
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      if (i < ulo.n && j < ng) {
-        // strict: a zero-length gap/piece only arises where U_hi (eroded) robustly covers an arc
-        // end, so it holds no sample of this band
-        const float s1 = fmaxf(lo_a[i], g[2 * j]), s2 = fminf(lo_b[i], g[2 * j + 1]);
-        if (s1 < s2)
-          runs_push(runs, __float2int_rd(fmaf(s1, inv_step, pa)) - kPad, __float2int_ru(fmaf(s2, inv_step, pa)) + kPad,
-                    A0, A1);
-      }
-    }
-  }
-  return finalize_runs(runs, A0, A1, J, work);
+__device__ __forceinline__ Ent3 finalize_runs(const Runs2& runs, int A0, int A1, int J, unsigned long long* work) {
+  Ent3 o{0u, 0u, 0u};
+  uint32_t a0, b0, a1, b1;
+  int h0, h1;
+  unsigned long long w0 = 0, w1 = 0;
+  finalize_run(runs.l0, runs.h0, A0 - 1, runs.n == 2 ? (runs.l1 & ~1) - 1 : A1, J, &a0, &b0, &h0, &w0);
+  finalize_run(runs.l1, runs.h1, h0, A1, J, &a1, &b1, &h1, &w1);
+  const bool one = runs.n >= 1, two = runs.n == 2;
+  *work += (one ? w0 : 0ull) + (two ? w1 : 0ull);
+  o.e0 = one ? a0 : 0u;
+  o.e1 = two ? a1 : 0u;
+  o.e2 = (one ? b0 : 0u) | (two ? b1 : 0u);
+  return o;
 }
 
 // Reference hemisphere decision (voting.cpp:36-38: flip iff c > 0) of sample j in [0, 2J).
@@ -377,22 +342,19 @@ __device__ __forceinline__ void exact_global(const double a1[3], const double a2
 // the vote; the CANONICAL half circle in sample space -- the J/2 consecutive samples j0 .. j0+J/2-1
 // whose hemisphere test c <= 0 holds in the reference's own f64 arithmetic (voting.cpp:36-38), so
 // the vote never decides a hemisphere; and per row band the sample ranges whose projected points
-// can fall in the band (analytic circle/line intersection, padded, superset). The few pairs whose
-// two twins are BOTH (or NEITHER) canonical -- |c| at the rounding level -- are deposited here
-// exactly; constraints without a clean canonical half circle (z = +-e3 exactly: c == 0) are listed
-// for the vote kernel's exact sample-by-sample path.
+// can fall in the band (band_boundary / band_runs: nested level arcs, padded, superset). The few
+// pairs whose two twins are BOTH (or NEITHER) canonical -- |c| at the rounding level -- are
+// deposited here exactly; constraints without a clean canonical half circle (z = +-e3 exactly:
+// c == 0) are listed for the vote kernel's exact sample-by-sample path.
 // kNB > 0: n_bands <= kNB, entries kept in shared memory and reserved once per (block, band)
-// (same-address global atomics were the planner's bottleneck); kNB == 0: any band count, one
-// reservation per (warp, band).
-template <int kNB>
-__global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, int64_t n) {
-  __shared__ unsigned long long s_work[kMaxBands];
-  __shared__ int s_cnt[kMaxBands], s_base[kMaxBands];
-  for (int t = threadIdx.x; t < p.n_bands; t += blockDim.x) {
-    s_work[t] = 0;
-    s_cnt[t] = 0;
-  }
-  __syncthreads();
+// (same-address global atomics were the planner's bottleneck); kExact: n_bands == kNB (the band
+// loop unrolled); kNB == 0: any band count, one reservation per (warp, band).
+constexpr int kPlanThreads = 256;
+template <int kNB, bool kExact>
+__global__ void __launch_bounds__(kPlanThreads) plan_kernel(VotePlan p, VoteBuffers b, int64_t n) {
+  constexpr int kWarps = kPlanThreads / 32;
+  __shared__ uint32_t s_wcnt[kMaxBands][kWarps], s_wwork[kMaxBands][kWarps];
+  __shared__ int s_base[kMaxBands];
   const int64_t lo = b.bounds ? b.bounds[0] : b.range_lo, hi = b.bounds ? b.bounds[1] : b.range_lo + n;
   const int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double z0 = 0.0, z1 = 0.0, z2 = 0.0;
@@ -403,9 +365,8 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
   }
   bool valid = i < hi && !isnan(z0);  // in-order constraint sets mark dropped pairs with NaN
   const int M = p.halfJ, J = p.J;
-  float f1y = 0.f, f2y = 0.f, f1z = 0.f, f2z = 0.f;  // fl32 of a1y, a2y, a1z, a2z (arc solves)
+  float f1y = 0.f, f2y = 0.f, f1z = 0.f, f2z = 0.f;  // fl32 of a1y, a2y, a1z, a2z (boundary solves)
   int A0 = 0, A1 = -1;  // canonical samples of the fast path: [A0, A1] (unwrapped, in [0, 2J))
-  float theta_a = 0.f, pa = 0.f;
   const float inv_step = 1.f / p.step_f;
   if (valid) {
     double a1[3], a2[3];
@@ -413,33 +374,40 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
     const double K = p.inv_cell;
     // the vote reads fl32(K * a_xy) (one rounding, like fl32(a_xy)) and fl32(-a_z): c' = 1 - c is
     // then two FFMAs from the constant 1
-    b.basis_a[i] = make_float4(__double2float_rn(a1[0] * K), __double2float_rn(a1[1] * K), __double2float_rn(-a1[2]),
-                               __double2float_rn(a2[0] * K));
-    b.basis_b[i] = make_float2(__double2float_rn(a2[1] * K), __double2float_rn(-a2[2]));
+    const float4 fa = make_float4(__double2float_rn(a1[0] * K), __double2float_rn(a1[1] * K),
+                                  __double2float_rn(-a1[2]), __double2float_rn(a2[0] * K));
+    const float2 fb = make_float2(__double2float_rn(a2[1] * K), __double2float_rn(-a2[2]));
+    b.basis_a[i] = fa;
+    b.basis_b[i] = fb;
     f1y = __double2float_rn(a1[1]);
     f2y = __double2float_rn(a2[1]);
     f1z = __double2float_rn(a1[2]);
     f2z = __double2float_rn(a2[2]);
-    // c(theta) = rc cos(theta - phi): the canonical arc (c <= 0) starts at theta_a = phi + pi/2
-    theta_a = atan2_fast(f2z, f1z) + 0.5f * kPiF;
-    pa = (theta_a + kPiF) * inv_step;  // its sample coordinate, in [J/4, 5J/4]
-    const int jc = __float2int_ru(pa);
-    // exact start: the false -> true transition of canonical(j) next to jc
-    unsigned sm = 0;
+    // c(theta) = rc cos(theta - phi): the canonical arc (c <= 0) starts at theta_a = phi + pi/2,
+    // sample coordinate pa in [J/4, 5J/4]; the exact start is the false -> true transition of
+    // canonical(j), normally at ceil(pa), and the exact end normally M samples later
+    const float theta_a = atan2_fast(f2z, f1z) + 0.5f * kPiF;
+    const int jc = __float2int_ru((theta_a + kPiF) * inv_step);
+    int j0 = -1, e = -1;
+    if (!canonical(a1, a2, b.table64, jc - 1, J) && canonical(a1, a2, b.table64, jc, J) &&
+        canonical(a1, a2, b.table64, jc + M - 1, J) && !canonical(a1, a2, b.table64, jc + M, J)) {
+      j0 = jc;
+      e = jc + M;
+    } else {  // rare: |c| at the rounding level next to an end, or pa next to an integer
+      unsigned sm = 0;
 #pragma unroll
-    for (int q = 0; q < 6; ++q) sm |= (unsigned)canonical(a1, a2, b.table64, jc - 3 + q, J) << q;
-    int j0 = -1;
+      for (int q = 0; q < 6; ++q) sm |= (unsigned)canonical(a1, a2, b.table64, jc - 3 + q, J) << q;
 #pragma unroll
-    for (int q = 1; q < 6; ++q)
-      if (j0 < 0 && !((sm >> (q - 1)) & 1u) && ((sm >> q) & 1u)) j0 = jc - 3 + q;
-    int e = -1;  // exact end: first non-canonical sample after the arc (normally j0 + M)
-    if (j0 >= 0) {
-      unsigned em = 0;
+      for (int q = 1; q < 6; ++q)
+        if (j0 < 0 && !((sm >> (q - 1)) & 1u) && ((sm >> q) & 1u)) j0 = jc - 3 + q;
+      if (j0 >= 0) {  // exact end: first non-canonical sample after the arc (normally j0 + M)
+        unsigned em = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) em |= (unsigned)canonical(a1, a2, b.table64, j0 + M - 2 + q, J) << q;
+        for (int q = 0; q < 4; ++q) em |= (unsigned)canonical(a1, a2, b.table64, j0 + M - 2 + q, J) << q;
 #pragma unroll
-      for (int q = 1; q < 4; ++q)
-        if (e < 0 && ((em >> (q - 1)) & 1u) && !((em >> q) & 1u)) e = j0 + M - 2 + q;
+        for (int q = 1; q < 4; ++q)
+          if (e < 0 && ((em >> (q - 1)) & 1u) && !((em >> q) & 1u)) e = j0 + M - 2 + q;
+      }
     }
     if (j0 < 0 || e < 0 || f1z == 0.f && f2z == 0.f) {
       // no clean canonical half circle: every sample of this constraint goes the exact way
@@ -462,9 +430,6 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
       // the arc is deposited here exactly (both twins), so every entry can start even and end odd
       // (the f32 filter first, exactly as the vote evaluates it: an unflagged cell is the
       // reference cell of both twins; a flagged pair goes the exact way)
-      const float4 fa = make_float4(__double2float_rn(a1[0] * K), __double2float_rn(a1[1] * K),
-                                    __double2float_rn(-a1[2]), __double2float_rn(a2[0] * K));
-      const float2 fb = make_float2(__double2float_rn(a2[1] * K), __double2float_rn(-a2[2]));
       F32Geom gg;
       gg.CMf = p.CMf;
       gg.S = p.frac_shift;
@@ -492,51 +457,68 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
       if (!(A1 & 1)) exact_pair(A1--);
     }
   }
-  // near-polar constraint: the projected arc hugs the rim, every band sees the whole arc
-  const bool polar = !(sqrtf(fmaf(f1z, f1z, f2z * f2z)) >= kRcMin);
-  const int lane = threadIdx.x & 31;
+  if (!valid) {
+    A0 = 0;
+    A1 = -1;  // no ranges
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   const unsigned long long ci = (unsigned long long)(uint32_t)i;
-  ArcG g_lo{0.f, 0.f, 0.f, 1, 1};  // band 0: Y >= -inf
+  const float pad_s = kArcDilate * inv_step + (float)kPad;
+  Bnd b_lo;  // band 0's lower boundary: Y >= -inf, the whole circle
+  b_lo.ost = 1;
+  b_lo.ist = 1;
+  b_lo.olo = b_lo.ohi = b_lo.ilo = b_lo.ihi = 0;
+  b_lo.c = 0.f;
   // entries of this constraint in band `band` (+ planned samples into *w)
   auto plan_band = [&](int band, unsigned long long* w) -> Ent3 {
-    if (!valid) return Ent3{0u, 0u, 0u};
-    if (polar) return finalize_runs(Runs2{A0, A1, 0, 0, 1}, A0, A1, J, w);
-    ArcG g_hi{0.f, 0.f, 0.f, 0, 0};  // last band: Y >= +inf is empty
-    if (band < p.n_bands - 1) {
+    Bnd b_hi;  // the last band's upper boundary: Y >= +inf, empty
+    b_hi.ost = 0;
+    b_hi.ist = 0;
+    b_hi.olo = b_hi.ohi = b_hi.ilo = b_hi.ihi = 0;
+    b_hi.c = 0.f;
+    if (band < (kExact ? kNB : p.n_bands) - 1) {
       const float y1 = p.band_ylo[band + 1];
-      g_hi = arc_solve(fmaf(y1, f1z, f1y), fmaf(y1, f2z, f2y), y1, theta_a);
+      b_hi = band_boundary(fmaf(y1, f1z, f1y), fmaf(y1, f2z, f2y), y1, inv_step, pad_s, J);
     }
-    const Arc2 ulo = arc_dilate(g_lo, kArcDilate), uhi = arc_dilate(g_hi, -kArcDilate);
-    g_lo = g_hi;  // the upper boundary of this band is the lower boundary of the next
-    return entries_from_sets(ulo, uhi, pa, inv_step, A0, A1, J, w);
+    const Runs2 runs = band_runs(b_lo, b_hi, A0, A1, J);
+    b_lo = b_hi;  // the upper boundary of this band is the lower boundary of the next
+    return finalize_runs(runs, A0, A1, J, w);
   };
-  // warp-level bookkeeping of one band: entry offset of this lane inside the warp's block of
-  // entries, reserved in s_cnt (kNB > 0) or directly in the global list (kNB == 0)
+  // warp-level bookkeeping of one band: this lane's entry offset inside the warp's block of
+  // entries; the warp's count and planned samples are parked per (band, warp) for the block scan
+  // (kNB > 0) or reserved in the global list directly (kNB == 0)
   auto book = [&](int band, const Ent3& r, unsigned long long w, bool global) -> int {
-    const unsigned m0 = __ballot_sync(0xFFFFFFFFu, r.e0 != 0u);  // entries are filled in order
+    const unsigned m0 = __ballot_sync(0xFFFFFFFFu, r.e0 != 0u);
     const unsigned m1 = __ballot_sync(0xFFFFFFFFu, r.e1 != 0u);
     const unsigned m2 = __ballot_sync(0xFFFFFFFFu, r.e2 != 0u);
     const int total = __popc(m0) + __popc(m1) + __popc(m2);
-    int wbase = 0;
-    if (lane == 0 && total) wbase = global ? atomicAdd(&b.entry_count[band], total) : atomicAdd(&s_cnt[band], total);
-    wbase = __shfl_sync(0xFFFFFFFFu, wbase, 0);
     const unsigned ws = __reduce_add_sync(0xFFFFFFFFu, (unsigned)w);  // w <= J + 128 per lane
-    if (lane == 0 && ws) atomicAdd(&s_work[band], (unsigned long long)ws);
+    int wbase = 0;
+    if (global) {
+      if (lane == 0 && total) wbase = atomicAdd(&b.entry_count[band], total);
+      wbase = __shfl_sync(0xFFFFFFFFu, wbase, 0);
+      if (lane == 0 && ws) atomicAdd(&b.band_work[band], (unsigned long long)ws);
+    } else if (lane == 0) {
+      s_wcnt[band][warp] = (uint32_t)total;
+      s_wwork[band][warp] = ws;
+    }
     return wbase + __popc(m0 & lt_mask) + __popc(m1 & lt_mask) + __popc(m2 & lt_mask);
   };
   auto emit = [&](int band, const Ent3& r, int64_t off) {
     unsigned long long* ep = b.entries + (int64_t)band * b.entry_cap + off;
+    const int o1 = r.e0 != 0u, o2 = o1 + (r.e1 != 0u);  // the slots may have gaps: packed here
     if (r.e0) ep[0] = ci | ((unsigned long long)r.e0 << 32);
-    if (r.e1) ep[1] = ci | ((unsigned long long)r.e1 << 32);
-    if (r.e2) ep[2] = ci | ((unsigned long long)r.e2 << 32);
+    if (r.e1) ep[o1] = ci | ((unsigned long long)r.e1 << 32);
+    if (r.e2) ep[o2] = ci | ((unsigned long long)r.e2 << 32);
   };
   if constexpr (kNB > 0) {
     // per-thread entries/offsets parked in shared memory (a rolled band loop keeps the code small)
-    __shared__ uint32_t s_r[kNB][3][256];
-    __shared__ int s_off[kNB][256];
-#pragma unroll 1
-    for (int band = 0; band < p.n_bands; ++band) {  // uniform
+    __shared__ uint32_t s_r[kNB][3][kPlanThreads];
+    __shared__ int s_off[kNB][kPlanThreads];
+    const int nb = kExact ? kNB : p.n_bands;
+#pragma unroll(kExact ? kNB : 1)
+    for (int band = 0; band < nb; ++band) {  // uniform
       unsigned long long w = 0;
       const Ent3 r = plan_band(band, &w);
       s_r[band][0][threadIdx.x] = r.e0;
@@ -545,23 +527,32 @@ __global__ void __launch_bounds__(256) plan_kernel(VotePlan p, VoteBuffers b, in
       s_off[band][threadIdx.x] = book(band, r, w, false);
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < p.n_bands; t += blockDim.x)
-      s_base[t] = s_cnt[t] ? atomicAdd(&b.entry_count[t], s_cnt[t]) : 0;
+    // per band: the block's entries (one global reservation) and the warps' offsets inside it
+    if (threadIdx.x < p.n_bands) {
+      const int band = threadIdx.x;
+      uint32_t tot = 0, work = 0;
+#pragma unroll
+      for (int q = 0; q < kWarps; ++q) {
+        const uint32_t c = s_wcnt[band][q];
+        s_wcnt[band][q] = tot;  // exclusive prefix
+        tot += c;
+        work += s_wwork[band][q];
+      }
+      s_base[band] = tot ? atomicAdd(&b.entry_count[band], (int)tot) : 0;
+      if (work) atomicAdd(&b.band_work[band], (unsigned long long)work);
+    }
     __syncthreads();
-#pragma unroll 1
-    for (int band = 0; band < p.n_bands; ++band)
+#pragma unroll(kExact ? kNB : 1)
+    for (int band = 0; band < nb; ++band)
       emit(band, Ent3{s_r[band][0][threadIdx.x], s_r[band][1][threadIdx.x], s_r[band][2][threadIdx.x]},
-           (int64_t)s_base[band] + s_off[band][threadIdx.x]);
+           (int64_t)s_base[band] + s_wcnt[band][warp] + s_off[band][threadIdx.x]);
   } else {
     for (int band = 0; band < p.n_bands; ++band) {  // uniform trip count: warp collectives inside
       unsigned long long w = 0;
       const Ent3 r = plan_band(band, &w);
       emit(band, r, book(band, r, w, true));
     }
-    __syncthreads();
   }
-  for (int t = threadIdx.x; t < p.n_bands; t += blockDim.x)
-    if (s_work[t]) atomicAdd(&b.band_work[t], s_work[t]);
 }
 
 // ---- K2 ------------------------------------------------------------------------------
@@ -1170,12 +1161,14 @@ __global__ void deposit_one_kernel(VotePlan p, const double* z3, const double2* 
 }  // namespace
 
 void launch_plan(const VotePlan& p, const VoteBuffers& b, int64_t n, cudaStream_t s) {
-  const int threads = 256;
+  const int threads = kPlanThreads;
   const int64_t blocks = (n + threads - 1) / threads;
-  if (p.n_bands <= 8)
-    plan_kernel<8><<<(unsigned)blocks, threads, 0, s>>>(p, b, n);
+  if (p.n_bands == 5)  // the default geometry
+    plan_kernel<5, true><<<(unsigned)blocks, threads, 0, s>>>(p, b, n);
+  else if (p.n_bands <= 8)
+    plan_kernel<8, false><<<(unsigned)blocks, threads, 0, s>>>(p, b, n);
   else
-    plan_kernel<0><<<(unsigned)blocks, threads, 0, s>>>(p, b, n);
+    plan_kernel<0, false><<<(unsigned)blocks, threads, 0, s>>>(p, b, n);
 }
 
 using VoteKernel = void (*)(VotePlan, VoteBuffers, int64_t);
