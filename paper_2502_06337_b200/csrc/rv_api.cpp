@@ -239,6 +239,7 @@ struct rv_context {
   DBuf cons_axes, cons_counts, cons_z, cons_idx;  // baseline consensus scoring
   int coop_grid = 0;
   bool coop_bar_ready = false;
+  const double* coop_part_zeroed = nullptr;
   // angles / support
   DBuf bins, raw, angle_counts, angle_sums, angle_result, sup_counts, sup_result, band_flagsA, band_flagsB,
       band_idx, band_vals, near_h, near_result;
@@ -829,12 +830,16 @@ CoopState* coop_refine_launch(rv_context* c, const ConstraintSet& cs, const doub
   const int nt = std::max(1, coop_tiles(cs.n));
   const size_t words = (size_t)(cs.n + 31) / 32 + 32;
   uint32_t* fa = c->flagsA.get<uint32_t>(words);
+  int32_t* toff = c->boffA.get<int32_t>(nt);
+  CoopState* dst = state_dst ? state_dst : c->coop_state.get<CoopState>(1);
   uint32_t* fb = c->flagsB.get<uint32_t>(words);
   int32_t* tcount = c->bcount.get<int32_t>(nt);
-  int32_t* toff = c->boffA.get<int32_t>(nt);
-  double* part = c->coop_part.get<double>((size_t)c->coop_grid * 8);
-  CoopState* dst = state_dst ? state_dst : c->coop_state.get<CoopState>(1);
-  if (!c->coop_bar_ready) {  // the kernel leaves its barrier counters at zero; clear them once
+  double* part = c->coop_part.get<double>((size_t)c->coop_grid * 16);  // one 128-byte line per block
+  if (part != c->coop_part_zeroed) {  // sequence numbers start below every launch's epoch
+    ck(cudaMemsetAsync(part, 0, sizeof(double) * 16 * (size_t)c->coop_grid, c->st), "coop lines");
+    c->coop_part_zeroed = part;
+  }
+  if (!c->coop_bar_ready) {  // launch epoch + exit counter: zeroed once, maintained by the kernel
     ck(cudaMemsetAsync(c->coop_bar.get<unsigned int>(2), 0, 2 * sizeof(unsigned int), c->st), "coop barrier");
     c->coop_bar_ready = true;
   }

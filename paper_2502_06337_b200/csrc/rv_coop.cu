@@ -1,14 +1,14 @@
 // K4': device-resident refine_loop / anneal_axis (estimator.cpp:51-69, :145-160) as ONE
 // cooperative kernel per call. Each pass is the strict classify of the constraint set (reference
-// op order, bitmask via ballot) fused with the 6 scatter sums of the same inliers. After ONE grid
-// barrier per pass, EVERY block reduces the block partials in the same fixed order and runs the
-// same short-latency 3x3 eigen-solve (axis_from_scatter_fast, rv_linalg.hpp), so all blocks
-// reach the same decision without a second barrier; block 0 publishes the state for the host.
-// No host round trip per pass.
+// op order, bitmask via ballot) fused with the 6 scatter sums of the same inliers. The blocks then
+// exchange their 8 partials through per-block 128-byte lines with release/acquire sequence numbers
+// (publish_line / load_seq: no arrival counter), EVERY block reduces all lines in the same fixed
+// order and runs the same short-latency 3x3 eigen-solve (axis_from_scatter_fast, rv_linalg.hpp,
+// warm-started from the previous pass), so all blocks reach the same decision with no second
+// exchange; block 0 publishes the state for the host. No host round trip per pass.
 //
-// Blocks own fixed contiguous tile ranges across passes, so the previous-pass flag words a block
-// compares against are its own writes: only the block partials cross blocks (read with .cg
-// after the barrier's release/acquire).
+// Blocks own fixed contiguous tile ranges across passes: their slice of z and the pass's flag
+// words stay in shared memory; only the final set is written to flags0.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -59,8 +59,8 @@ struct CoopArgs {
   uint32_t* flags1;
   int32_t* tile_count;
   int32_t* tile_offset;
-  double* block_part;       // [grid][8]
-  unsigned int* barrier;    // [2] arrival / exit counters (zero at launch; the last block to exit resets them)
+  double* block_part;       // [grid][kLine]: the blocks' partial lines (zeroed once before first use)
+  unsigned int* barrier;    // [2] launch epoch / exit counter (zeroed once; the last block out advances the epoch)
   State* state;
   // optional (refine_loop): compaction of the final set fused into the last pass
   const int32_t* kept;      // kept -> input index map (null: identity)
@@ -71,6 +71,7 @@ struct CoopArgs {
   // > 0: the block's constraint slice stays resident in shared memory after the first pass
   // (SoA, z_cap elements per coordinate); later passes classify from there
   int z_cap;
+  int fw_cap;  // flag words per block (shared memory, two slots)
 };
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -108,47 +109,68 @@ __device__ __forceinline__ void block_reduce8(double (&v)[8], double (*s_red)[kW
   }
 }
 
+// Per-pass exchange without a grid barrier: every block publishes its 8 partials and then a
+// sequence number (release) in its own 128-byte line; every block's warp 0 polls the sequence
+// numbers of all blocks (acquire) and then all blocks reduce the partials in the same fixed order.
+// One L2 round trip after the last block's release, no same-address arrival counter, and the
+// release only has to drain this block's 64 bytes (the pass's flag words stay in shared memory).
+// Sequence numbers are (launch epoch << 20) | pass; the last block to exit advances the epoch, so
+// the lines never need clearing (graph replays included).
+constexpr int kLine = 16;  // doubles per block line: 8 partials, the sequence number, padding
+__device__ __forceinline__ void publish_line(double* line, const double v[8], unsigned long long seq) {
+  for (int k = 0; k < 8; ++k) __stcg(line + k, v[k]);
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(line + 8), "l"(seq) : "memory");
+}
+__device__ __forceinline__ unsigned long long load_seq(const double* line) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(line + 8) : "memory");
+  return v;
+}
+
 __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
-  extern __shared__ double s_z[];  // [3][z_cap] when a.z_cap > 0
+  extern __shared__ double s_z[];  // [3][z_cap] z (a.z_cap > 0), then [2][fw_cap] flag words
   __shared__ double s_red[8][kWarps];
   __shared__ double s_next[4];  // next axis (3) + next e
   __shared__ int s_done;
+  __shared__ unsigned int s_epoch;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t ntiles = (a.n + kTile - 1) / kTile;
   const int64_t t_begin = ntiles * blockIdx.x / gridDim.x, t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
+  const int64_t w_begin = t_begin * (kTile / 32);
+  const int64_t w_end = min(t_end * (kTile / 32), (a.n + 31) / 32);  // this block's flag words
+  uint32_t* s_flags = reinterpret_cast<uint32_t*>(s_z + 3 * (size_t)a.z_cap);  // [2][fw_cap]
   double cls_axis[3] = {a.axis0[0], a.axis0[1], a.axis0[2]};
   if (a.axis0_dev) {
     cls_axis[0] = a.axis0_dev[0];
     cls_axis[1] = a.axis0_dev[1];
     cls_axis[2] = a.axis0_dev[2];
   }
+  if (tid == 0) s_epoch = __ldcg(a.barrier);
+  __syncthreads();
+  const unsigned long long epoch = (unsigned long long)s_epoch << 20;
   double e = a.mode == 1 ? (a.e0 > a.eps ? a.e0 : a.eps) : a.eps;
-  int slot = 0, refits = 0;
-  unsigned int bar_target = 0;
+  int slot = 0, refits = 0, pass = 0;
+  double l3 = 0.0;  // Newton warm start of the 3x3 solve across passes (thread 0)
   bool have_prev = false;
   bool first_pass = true;
   const int64_t e_begin = t_begin * kTile;
   const int64_t cap = a.z_cap;
+  double tot[8];
   for (;;) {
     // ---- classify pass over this block's tiles ----
     trace(1);
-    uint32_t* flags = slot == 0 ? a.flags0 : a.flags1;
-    const uint32_t* prev = have_prev ? (slot == 0 ? a.flags1 : a.flags0) : nullptr;
-    for (int64_t t = t_begin + tid; t < t_end; t += kThreads) a.tile_count[t] = 0;
-    __syncthreads();
+    uint32_t* flags = s_flags + (size_t)slot * a.fw_cap;
+    const uint32_t* prev = s_flags + (size_t)(slot ^ 1) * a.fw_cap;
     double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // scatter[6], diff, count
     int diff = 0, cnt = 0;
     for (int64_t t0 = t_begin; t0 < t_end; t0 += kChunk) {
       double z[kChunk][kPerTile][3];
-      uint32_t pw[kChunk][kPerTile];  // the previous pass's flag words (batched with the z loads)
 #pragma unroll
       for (int c = 0; c < kChunk; ++c)  // all loads of the chunk first
 #pragma unroll
         for (int r = 0; r < kPerTile; ++r) {
           const int64_t i = (t0 + c) * kTile + r * kThreads + tid;
           const bool ok = t0 + c < t_end && i < a.n;
-          const int64_t wq = (t0 + c) * kTile + r * kThreads + warp * 32;
-          pw[c][r] = (prev && t0 + c < t_end && wq < a.n) ? __ldcg(prev + (wq >> 5)) : 0u;
           const int64_t li = i - e_begin;  // the same thread owns element i in every pass
           if (cap > 0 && !first_pass) {
             z[c][r][0] = ok ? s_z[li] : 0.0;
@@ -180,9 +202,9 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
           const unsigned word = __ballot_sync(0xFFFFFFFFu, in);
           const int64_t w0 = (t0 + c) * kTile + r * kThreads + warp * 32;
           if (lane == 0 && w0 < a.n) {
-            flags[w0 >> 5] = word;
-            if (prev && pw[c][r] != word) diff = 1;
-            if (word) atomicAdd(a.tile_count + t0 + c, __popc(word));
+            const int64_t lw = (w0 >> 5) - w_begin;
+            if (have_prev && prev[lw] != word) diff = 1;
+            flags[lw] = word;
           }
           if (in) {
             ++cnt;
@@ -200,28 +222,42 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
     v[7] = (double)cnt;
     trace(2);
     block_reduce8(v, s_red);
-    if (tid == 0) {
-      double* bp = a.block_part + (size_t)blockIdx.x * 8;
-      for (int k = 0; k < 8; ++k) __stcg(bp + k, v[k]);
-    }
+    const unsigned long long seq = epoch | (unsigned long long)(pass + 1);
+    if (tid == 0) publish_line(a.block_part + (size_t)blockIdx.x * kLine, v, seq);
     trace(3);
-    bar_target += gridDim.x;
-    grid_barrier(a.barrier, bar_target);
-    trace(4);
-    // ---- every block: reduce all partials in the same fixed order, decide ----
-    // warp k reduces value k over all block partials (fixed order: lane-strided, then the tree)
-    if (warp < 8) {
-      double acc = 0.0;
-#pragma unroll 4
-      for (unsigned b = lane; b < gridDim.x; b += 32) acc = xa(acc, __ldcg(a.block_part + (size_t)b * 8 + warp));
-      acc = warp_sum_d(acc);
-      if (lane == 0) s_red[warp][0] = acc;
+    // ---- warp 0: wait for every block's line of this pass, reading its partials as it lands;
+    // the same fixed order in every block (lane-strided over the lines, then the tree) ----
+    if (warp == 0) {
+      const unsigned nl = (gridDim.x + 31) / 32;  // lines per lane
+      for (;;) {  // every line of this pass seen (all polls of a round issued together)
+        bool ok = true;
+        for (unsigned j = 0; j < nl; ++j) {
+          const unsigned b = lane + 32 * j;
+          if (b < gridDim.x) ok &= load_seq(a.block_part + (size_t)b * kLine) >= seq;
+        }
+        if (__all_sync(0xFFFFFFFFu, ok)) break;
+      }
+      double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (unsigned j0 = 0; j0 < nl; j0 += 4) {  // 4 lines x 8 values in flight per lane
+        double x[4][8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const unsigned b = lane + 32 * (j0 + j);
+          const bool in = j0 + j < nl && b < gridDim.x;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) x[j][k] = in ? __ldcg(a.block_part + (size_t)b * kLine + k) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[k] = xa(acc[k], x[j][k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) tot[k] = warp_sum_d(acc[k]);
     }
-    __syncthreads();
-    for (int k = 0; k < 8; ++k) v[k] = s_red[k][0];
+    trace(4);
     trace(5);
     if (tid == 0) {
-      const double* tot = v;
       const long long count = (long long)tot[7];
       const bool differs = tot[6] != 0.0;
       int done = 0, rank_deficient = 0;
@@ -233,7 +269,7 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
         if (have_prev && !differs) done = 1;  // stable
         if (!done && (refits >= 10 || count < 2)) done = 1;
         if (!done) {
-          if (axis_from_scatter_fast(tot, nxt)) {
+          if (axis_from_scatter_fast(tot, nxt, &l3)) {
             ++refits;
           } else {
             rank_deficient = 1;  // RankDeficient: keep the current axis
@@ -241,7 +277,7 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
           }
         }
       } else {  // anneal_axis (estimator.cpp:145-160)
-        if (count >= 2 && axis_from_scatter_fast(tot, nxt)) {
+        if (count >= 2 && axis_from_scatter_fast(tot, nxt, &l3)) {
           cur[0] = nxt[0];
           cur[1] = nxt[1];
           cur[2] = nxt[2];
@@ -262,7 +298,7 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
         for (int k = 0; k < 6; ++k) st->scatter[k] = tot[k];
         st->e = e_next;
         st->count = count;
-        st->slot = slot;
+        st->slot = 0;
         st->done = done;
         st->refits = refits;
         st->rank_deficient = rank_deficient;
@@ -275,90 +311,85 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
     trace(6);
     const int done = s_done;
     if (done) {
-      if (a.mode == 0 && slot == 1) {  // the final set always ends in flags0 (own tiles' words)
-        const int64_t w_lo = t_begin * (kTile / 32), w_hi = min(t_end * (kTile / 32), (a.n + 31) / 32);
-        for (int64_t w = w_lo + tid; w < w_hi; w += kThreads) a.flags0[w] = a.flags1[w];
-      }
-      trace(7);
-      if (a.mode == 0 && a.compact_out) {
-        // fused compaction: this block's offset = inliers in tiles [0, t_begin) (tile counts are
-        // final after the last barrier), then its own tiles in order
+      if (a.mode == 0) {
+        // the final set (this pass's words) into flags0; this block's position = the inliers of the
+        // blocks before it (their counts, from their lines of this pass)
+        for (int64_t w = w_begin + tid; w < w_end; w += kThreads) a.flags0[w] = flags[w - w_begin];
         __shared__ long long s_pre[kWarps];
         long long pre = 0;
-        for (int64_t t = tid; t < t_begin; t += kThreads) pre += __ldcg(a.tile_count + t);
+        for (unsigned b = tid; b < blockIdx.x; b += kThreads)
+          pre += (long long)__ldcg(a.block_part + (size_t)b * kLine + 7);
         for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xFFFFFFFFu, pre, o);
         if (lane == 0) s_pre[warp] = pre;
-        __syncthreads();  // also orders the flags0 copy above
+        __syncthreads();
         long long off = 0;
         for (int w = 0; w < kWarps; ++w) off += s_pre[w];
-        // all own flag words at once: block-wide exclusive popc scan, then one warp per word
-        const int64_t nwords = (a.n + 31) / 32;
-        const int64_t w_lo = t_begin * (kTile / 32);
-        const int64_t w_hi = min(t_end * (kTile / 32), nwords);
-        __shared__ int s_wsum[kWarps];
-        for (int64_t c0 = w_lo; c0 < w_hi; c0 += kThreads) {  // chunks of kThreads words
-          const int64_t wi = c0 + tid;
-          const uint32_t word = wi < w_hi ? a.flags0[wi] : 0u;
-          const int cnt = __popc(word);
-          int incl = cnt;
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += y;
+        trace(7);
+        if (a.compact_out) {
+          // fused compaction: all own flag words at once, block-wide exclusive popc scan, then
+          // each thread writes its own word's set bits
+          __shared__ int s_wsum[kWarps];
+          for (int64_t c0 = w_begin; c0 < w_end; c0 += kThreads) {  // chunks of kThreads words
+            const int64_t wi = c0 + tid;
+            const uint32_t word = wi < w_end ? flags[wi - w_begin] : 0u;
+            const int cw = __popc(word);
+            int incl = cw;
+            for (int o = 1; o < 32; o <<= 1) {
+              const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+              if (lane >= o) incl += y;
+            }
+            if (lane == 31) s_wsum[warp] = incl;
+            __syncthreads();
+            int wpre = 0, ctot = 0;
+            for (int w = 0; w < kWarps; ++w) {
+              wpre += w < warp ? s_wsum[w] : 0;
+              ctot += s_wsum[w];
+            }
+            uint32_t m = word;
+            long long pos = off + wpre + (incl - cw);
+            while (m) {
+              const int bit = __ffs(m) - 1;
+              m &= m - 1u;
+              const int64_t i = wi * 32 + bit;
+              a.compact_out[pos++] = a.kept ? __ldg(a.kept + i) : (int32_t)i;
+            }
+            off += ctot;
+            __syncthreads();
           }
-          if (lane == 31) s_wsum[warp] = incl;
-          __syncthreads();
-          int wpre = 0, ctot = 0;
-          for (int w = 0; w < kWarps; ++w) {
-            wpre += w < warp ? s_wsum[w] : 0;
-            ctot += s_wsum[w];
+          if (blockIdx.x == 0) {
+            for (int k = tid; k < a.n_bins; k += kThreads) a.zero_bins[k] = 0u;
+            if (tid < 2 && a.zero_counts) a.zero_counts[tid] = 0ull;
           }
-          const long long wbase_pos = off + wpre + (incl - cnt);  // first output slot of this word
-          // each thread writes its own word's set bits (independent loads across threads)
-          uint32_t m = word;
-          long long pos = wbase_pos;
-          while (m) {
-            const int bit = __ffs(m) - 1;
-            m &= m - 1u;
-            const int64_t i = wi * 32 + bit;
-            a.compact_out[pos++] = a.kept ? __ldg(a.kept + i) : (int32_t)i;
+        } else if (warp == 0) {
+          // compaction offsets of the final set (tile order): block offset + own tiles' prefix
+          long long run = off;
+          for (int64_t t0 = t_begin; t0 < t_end; t0 += 32) {
+            const int64_t t = t0 + lane;
+            int c = 0;
+            if (t < t_end)
+              for (int w = 0; w < kTile / 32; ++w) {
+                const int64_t gw = t * (kTile / 32) + w;
+                if (gw < w_end) c += __popc(flags[gw - w_begin]);
+              }
+            int x = c;
+            for (int o = 1; o < 32; o <<= 1) {
+              const int y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+              if (lane >= o) x += y;
+            }
+            if (t < t_end) a.tile_offset[t] = (int32_t)(run + x - c);
+            run += __shfl_sync(0xFFFFFFFFu, x, 31);
           }
-          off += ctot;
-          __syncthreads();
-        }
-        if (blockIdx.x == 0) {
-          for (int k = tid; k < a.n_bins; k += kThreads) a.zero_bins[k] = 0u;
-          if (tid < 2 && a.zero_counts) a.zero_counts[tid] = 0ull;
-        }
-      } else if (a.mode == 0 && blockIdx.x == 0) {  // compaction offsets of the final set (tile order)
-        __shared__ long long s_tot[kThreads];
-        const int64_t per = (ntiles + kThreads - 1) / kThreads;
-        const int64_t t0 = tid * per, t1 = t0 + per < ntiles ? t0 + per : ntiles;
-        long long acc = 0;
-        for (int64_t t = t0; t < t1; ++t) acc += __ldcg(a.tile_count + t);
-        s_tot[tid] = acc;
-        __syncthreads();
-        if (tid == 0) {
-          long long run = 0;
-          for (int k = 0; k < kThreads; ++k) {
-            const long long x = s_tot[k];
-            s_tot[k] = run;
-            run += x;
-          }
-        }
-        __syncthreads();
-        long long off = s_tot[tid];
-        for (int64_t t = t0; t < t1; ++t) {
-          a.tile_offset[t] = (int32_t)off;
-          off += __ldcg(a.tile_count + t);
         }
       }
       trace(8);
-      // exit: the last block out resets the barrier counters for the next launch
+      // exit: the last block out advances the epoch (the lines' sequence numbers of the next launch)
+      __syncthreads();
       if (tid == 0) {
         __threadfence();
         if (atomicAdd(a.barrier + 1, 1u) == gridDim.x - 1) {
-          a.barrier[0] = 0u;
           a.barrier[1] = 0u;
+          __threadfence();
+          atomicAdd(a.barrier, 1u);
         }
       }
       break;
@@ -366,6 +397,7 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
     for (int k = 0; k < 3; ++k) cls_axis[k] = s_next[k];
     e = s_next[3];
     slot ^= 1;
+    ++pass;
     have_prev = a.mode == 0;
     first_pass = false;
   }
@@ -438,13 +470,16 @@ cudaError_t launch_coop_refine(const double* zx, const double* zy, const double*
     cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(coop_refine_kernel));
     return fa.sharedSizeBytes + 1024;  // + the runtime's reserved shared memory per block
   }();
-  size_t dyn = (size_t)(3 * per_block) * sizeof(double);
+  a.fw_cap = (int)(per_block / 32);
+  const size_t flag_bytes = (size_t)2 * a.fw_cap * sizeof(uint32_t);
+  size_t dyn = (size_t)(3 * per_block) * sizeof(double) + flag_bytes;
   a.z_cap = (int)per_block;
   if (mode != 0 && mode != 1) a.z_cap = 0;
   if (dyn + static_bytes > (size_t)smem_max) {
     a.z_cap = 0;
-    dyn = 0;
+    dyn = flag_bytes;
   }
+  if (dyn + static_bytes > (size_t)smem_max) return cudaErrorInvalidValue;  // > ~200M constraints
   if (dyn > 0) {
     static std::mutex mu;
     static size_t configured[16] = {};

@@ -307,7 +307,10 @@ RV_HD bool axis_from_scatter(const double s6[6], double axis[3]) {
 // the characteristic cubic by monotone Newton from 0, eigenvector = the largest cross product of
 // two rows of M - l3 I (its exact null direction); l1, l2 from the trace and the sum of principal
 // minors. No transcendental calls: a short dependency chain for the per-pass device decision.
-RV_HD bool axis_from_scatter_fast(const double s6[6], double axis[3]) {
+// l3_hint (optional, in/out): the previous solve's smallest eigenvalue of the normalised scatter.
+// Newton then starts just below it when chi is still negative there (the same monotone iteration,
+// a few steps instead of a climb from 0 -- consecutive refine passes change the scatter little).
+RV_HD bool axis_from_scatter_fast(const double s6[6], double axis[3], double* l3_hint = nullptr) {
   double scale = 0.0;
   for (int k = 0; k < 6; ++k) scale = fabs(s6[k]) > scale ? fabs(s6[k]) : scale;
   if (!(scale > 0.0)) return false;  // all-zero scatter: rank deficient
@@ -321,6 +324,12 @@ RV_HD bool axis_from_scatter_fast(const double s6[6], double axis[3]) {
   // 0 <= l3 and chi is increasing and concave on [0, l3]: the iterates increase monotonically to
   // l3 (no overshoot), quadratically once l3 << l2 (one or two steps in the refine loop).
   double l3 = 0.0;
+  if (l3_hint && *l3_hint > 0.0) {
+    const double l0 = 0.999 * *l3_hint;
+    // below the inflection point tr/3 chi is increasing and concave up to l3: chi(l0) < 0 there
+    // means l0 < l3, the same monotone start condition as l = 0
+    if (l0 < tr / 3.0 && ((l0 - tr) * l0 + m2) * l0 - det < 0.0) l3 = l0;
+  }
   for (int it = 0; it < 32; ++it) {
     const double fl = ((l3 - tr) * l3 + m2) * l3 - det;
     const double dl = (3.0 * l3 - 2.0 * tr) * l3 + m2;
@@ -330,6 +339,7 @@ RV_HD bool axis_from_scatter_fast(const double s6[6], double axis[3]) {
     l3 = nl;
   }
   // l1 + l2 = tr - l3, l1 l2 = m2 - l3 (l1 + l2)
+  if (l3_hint) *l3_hint = l3;
   const double s = tr - l3, pm = m2 - l3 * s;
   double disc = s * s - 4.0 * pm;
   disc = disc > 0.0 ? disc : 0.0;

@@ -1,4 +1,7 @@
-python tools/guard_probe.py > gpurun_out/guard_probe.txt 2>&1
 python -m pytest tests -m gpu -q -x -rf 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
-bash tools/_ab.sh "" > gpurun_out/ab.log 2>&1
-ncu --set full --import-source on --clock-control none -k "regex:plan_kernel" -c 1 -f -o gpurun_out/plan python tools/profile_vote.py c3 1 > gpurun_out/ncu_plan.log 2>&1
+RV_NVCC_EXTRA="-DRV_COOP_TRACE" python paper_2502_06337_b200/build.py --force > /dev/null
+python tools/coop_trace.py c3 > gpurun_out/coop_trace_c3.txt 2>&1
+python tools/coop_trace.py c4 > gpurun_out/coop_trace_c4.txt 2>&1
+python paper_2502_06337_b200/build.py --force > /dev/null
+python tools/timeline.py c3 dev flush 2>/dev/null | grep -E "kernel|span" > gpurun_out/tl.txt
+python tools/timeline.py c4 dev flush 2>/dev/null | grep -E "kernel|span" | tail -3 > gpurun_out/tl4.txt
