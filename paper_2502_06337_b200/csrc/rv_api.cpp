@@ -1164,11 +1164,13 @@ PipelinedVote prep_and_vote_host(rv_context* c, const double* h_corrs, int64_t n
   ensure_tables(c, J);
   const VotePlan& p = cached_plan(c, G, cfg.extent, J);
   // chunk k+1's copy overlaps chunk k's compute (~1.4x slower per correspondence than the copy).
-  // Default 1, 2, 5, 8 sixteenths (measured best of the schedules tried): only the first 3 MB copy
-  // is exposed, and each extra chunk costs a vote-launch tail. Bounds are aligned to the
-  // preprocess tile (1024). Dev knob: RV_PIPE_CUM="0,1,3,8,16" (cumulative sixteenths).
+  // Default 1, 2, 3, 4, 6 sixteenths (measured best of 14 schedules, tools/_pipe_ab.sh: e2e 1.51
+  // ms vs 1.63 for 1, 2, 5, 8): only the first 3 MB copy is exposed, no chunk's compute waits for
+  // its copy, and the last chunk -- whose compute trails the last copy -- stays small; each extra
+  // chunk costs a vote-launch tail. Bounds are aligned to the preprocess tile (1024).
+  // Dev knob: RV_PIPE_CUM="0,1,3,6,10,16" (cumulative sixteenths).
   static const std::vector<int64_t> kCum = [] {
-    std::vector<int64_t> v{0, 1, 3, 8, 16};
+    std::vector<int64_t> v{0, 1, 3, 6, 10, 16};
     if (const char* e = std::getenv("RV_PIPE_CUM")) {
       std::vector<int64_t> w;
       for (const char* q = e; *q;) {
