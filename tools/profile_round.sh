@@ -14,3 +14,5 @@ python tools/timeline.py c3 host flush > gpurun_out/prof/timeline_c3_host.txt 2>
 python tools/gpu_check.py > gpurun_out/prof/gpu_check.log 2>&1; echo gpu_check_rc=$?
 python tools/io_bench.py > gpurun_out/prof/io_bench.json 2> gpurun_out/prof/io_bench.err; echo io_bench_rc=$?
 python -m pytest tests -m gpu -q > gpurun_out/prof/pytest_gpu.log 2>&1; echo pytest_rc=$?
+python tools/config_table.py > gpurun_out/prof/config_table.json 2> gpurun_out/prof/config_table.err; echo config_table_rc=$?
+python tools/shard_probe.py > gpurun_out/prof/shard_probe.txt 2>&1; echo shard_probe_rc=$?

@@ -17,6 +17,8 @@ fi
 [ -f gpurun_out/prof/io_bench.json ] && cp gpurun_out/prof/io_bench.json $P/io_bench_${R}.json
 [ -f gpurun_out/prof/pytest_gpu.log ] && tail -3 gpurun_out/prof/pytest_gpu.log > $P/pytest_gpu_${R}.txt
 [ -f gpurun_out/prof/gpu_check.log ] && cut -c1-600 gpurun_out/prof/gpu_check.log > $P/gpu_check_${R}.txt
+[ -f gpurun_out/prof/config_table.json ] && cp gpurun_out/prof/config_table.json $P/config_table_${R}.json && grep -v '^{' gpurun_out/prof/config_table.err > $P/config_table_${R}.txt
+[ -f gpurun_out/prof/shard_probe.txt ] && grep -v Warn gpurun_out/prof/shard_probe.txt > $P/shard_probe_${R}.txt
 python tools/summarize_profiles.py --json $P/vote_banded_${R}.ncu-rep | sed "s#\"source\": \"vote_banded_${R}.ncu-rep\"#\"source\": \"$P/vote_banded_${R}.ncu-rep\"#" > $P/vote_kernel_ncu.json
 { echo "# Round $R measurement bundle (tools/profile_round.sh on one B200; see DESIGN.md section 6)"
   echo "# launch list = ncu of 'python bench.py --steps 2 --warmup 3 --no-cpu' (device solves AND pipelined e2e"
