@@ -46,7 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     obj_dir.mkdir(exist_ok=True)
     common = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
               "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}"]
-    extra = os.environ.get("RV_NVCC_EXTRA", "").split()  # dev sweeps only (e.g. -DRV_NP=4)
+    extra = os.environ.get("RV_NVCC_EXTRA", "").split()  # dev A/B sweeps only (e.g. -DRV_BCAST_REDUX=0)
     common += extra
     jobs = []
     for src in SOURCES:

@@ -538,7 +538,8 @@ uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* 
   b.counters = c->counters.get<int32_t>(kCounterWords);
   b.entry_count = b.counters + kMaxBands + 1;
   b.stats = c->stats.get<unsigned long long>(2);
-  // enough CTAs to keep every SM busy, but not more than the work can feed (~1M pairs per CTA)
+  // enough CTAs to keep every SM busy, but not more than the work can feed (vote_ctas: one CTA per
+  // 16k planned pairs, at least one per band, at most one per SM)
   const int64_t est_pairs = n * (int64_t)p.halfJ;
   const int n_ctas = vote_ctas(c, p, est_pairs);
   b.max_slots = p.bulk ? 0 : n_ctas * p.n_bands;  // bulk: tiles are reduced into the grid directly
