@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define RV_ABI_VERSION 4
+#define RV_ABI_VERSION 5
 
 typedef enum rv_status {
   RV_OK = 0,
@@ -202,6 +202,18 @@ rv_status rv_peak_start_axis(rv_context* ctx, const uint32_t* d_grid, const rv_c
 rv_status rv_shard_classify(rv_context* ctx, const double axis[3], double epsilon, int32_t slot, int32_t compare_prev,
                             int64_t* count, double scatter[6], int32_t* differs);
 rv_status rv_axis_from_scatter(const double scatter[6], double axis[3]);
+/* refine_loop (estimator.cpp:51-69) of this shard as ONE device-resident loop, the per-pass
+ * partials exchanged between the devices of a multi-GPU solve through peer memory: every device
+ * writes its fixed-order partials (8 doubles) to line `rank` of every device's line buffer over
+ * NVLink (release at system scope) and sums all devices' lines in rank order (acquire) -- the
+ * same decision on every device, no host round trip per pass. peer_lines[q] = device q's buffer
+ * (8 x 128 bytes, zeroed before the first use, peer access enabled); epoch increases across
+ * solves and is the same on every device of one solve. n_dev = 1 needs no buffers. Leaves the
+ * final set in slot 0 (rv_shard_inliers / rv_shard_angle_hist); count = all devices' inliers,
+ * local_count = this shard's. Every device of the solve must call it concurrently. */
+rv_status rv_shard_refine(rv_context* ctx, const double axis0[3], const rv_config* cfg, int32_t n_dev, int32_t rank,
+                          double* const* peer_lines, uint64_t epoch, double axis[3], int64_t* count,
+                          int64_t* local_count, double scatter[6], int32_t* refits);
 rv_status rv_shard_inliers(rv_context* ctx, int32_t slot, int64_t offset, int32_t* dst, int64_t capacity,
                            int64_t* count);
 rv_status rv_shard_angle_hist(rv_context* ctx, const double axis[3], const rv_config* cfg, uint32_t* bins,

@@ -327,6 +327,18 @@ class Context:
                                                 C.byref(cnt), _ptr(sc, C.c_double), C.byref(diff)))
         return cnt.value, sc, bool(diff.value)
 
+    def shard_refine(self, axis0, cfg: EstimatorConfig | None = None):
+        """refine_loop of this context's shard as one device-resident loop (single device: no peer
+        exchange) -> (axis, count, local_count, scatter[6], refits); final set in slot 0."""
+        c = (cfg or EstimatorConfig()).to_c()
+        a0 = np.ascontiguousarray(axis0, dtype=np.float64)
+        ax, sc = np.zeros(3), np.zeros(6)
+        cnt, loc, rf = C.c_int64(), C.c_int64(), C.c_int32()
+        self._check(self._lib.rv_shard_refine(self.handle, _ptr(a0, C.c_double), C.byref(c), 1, 0, None, 0,
+                                              _ptr(ax, C.c_double), C.byref(cnt), C.byref(loc), _ptr(sc, C.c_double),
+                                              C.byref(rf)))
+        return ax, cnt.value, loc.value, sc, rf.value
+
     def shard_inliers(self, slot: int, offset: int, count: int) -> np.ndarray:
         out = np.zeros(max(count, 1), np.int32)
         got = C.c_int64()

@@ -825,7 +825,8 @@ struct CoopFused {  // optional work fused into the last pass of refine_loop
 };
 CoopState* coop_refine_launch(rv_context* c, const ConstraintSet& cs, const double* axis, const double* axis_dev,
                               int mode, double e0, const rv_config& cfg, uint32_t** flags, int32_t** offsets,
-                              CoopState* state_dst = nullptr, const CoopFused* fz = nullptr) {
+                              CoopState* state_dst = nullptr, const CoopFused* fz = nullptr,
+                              const CoopExchange* xch = nullptr) {
   StageScope sc(c, kRefine);
   if (c->coop_grid == 0) c->coop_grid = coop_refine_grid(c->sms);
   const int nt = std::max(1, coop_tiles(cs.n));
@@ -847,7 +848,7 @@ CoopState* coop_refine_launch(rv_context* c, const ConstraintSet& cs, const doub
   ck(launch_coop_refine(cs.zx, cs.zy, cs.zz, cs.n, mode, cfg.refine ? 1 : 0, cfg.epsilon, e0, axis, axis_dev, fa, fb,
                         tcount, toff, part, c->coop_bar.get<unsigned int>(2), dst, c->coop_grid, c->st, cs.kept,
                         fz ? fz->compact_out : nullptr, fz ? fz->zero_bins : nullptr, fz ? fz->n_bins : 0,
-                        fz ? fz->zero_counts : nullptr),
+                        fz ? fz->zero_counts : nullptr, xch),
      "coop refine launch");
   count_launch(c);
   if (flags) *flags = fa;  // refine_loop: final bitmask in flags0
@@ -2830,6 +2831,41 @@ rv_status rv_shard_classify(rv_context* c, const double axis[3], double epsilon,
     *count = r.count;
     std::memcpy(scatter, r.scatter, sizeof(double) * 6);
     *differs = r.differs ? 1 : 0;
+  });
+}
+
+rv_status rv_shard_refine(rv_context* c, const double axis0[3], const rv_config* cfg, int32_t n_dev, int32_t rank,
+                          double* const* peer_lines, uint64_t epoch, double axis[3], int64_t* count,
+                          int64_t* local_count, double scatter[6], int32_t* refits) {
+  if (!c || !axis0 || !cfg || !axis || !count || !local_count || !scatter || n_dev < 1 || n_dev > kCoopMaxDev ||
+      rank < 0 || rank >= n_dev || (n_dev > 1 && !peer_lines))
+    return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (!c->shard_corrs) fail(RV_ERR_INVALID_ARGUMENT, "no shard voted on this context");
+    CoopExchange x;
+    x.n_dev = n_dev;
+    x.rank = rank;
+    for (int q = 0; q < n_dev && n_dev > 1; ++q) x.lines[q] = peer_lines[q];
+    x.epoch = epoch;
+    uint32_t* flags = nullptr;
+    int32_t* offsets = nullptr;
+    CoopState* dst = coop_refine_launch(c, c->shard_cs, axis0, nullptr, 0, 0.0, *cfg, &flags, &offsets, nullptr,
+                                        nullptr, &x);
+    CoopState* h = reinterpret_cast<CoopState*>(c->pinned);
+    ck(cudaMemcpyAsync(h, dst, sizeof(CoopState), cudaMemcpyDeviceToHost, c->st), "coop state D2H");
+    sync(c);
+    if (h->exchange_timeout) fail(RV_ERR_CUDA, "cross-device refine: a peer device never published its partials");
+    std::memcpy(axis, h->axis, sizeof(double) * 3);
+    std::memcpy(scatter, h->scatter, sizeof(double) * 6);
+    *count = h->count;
+    *local_count = h->local_count;
+    if (refits) *refits = h->refits;
+    // the final set of this shard, for rv_shard_inliers / rv_shard_angle_hist (slot 0)
+    c->shard_cls[0].flags = flags;
+    c->shard_cls[0].offsets = offsets;
+    c->shard_cls[0].count = h->local_count;
+    c->shard_cls[1].count = -1;
   });
 }
 

@@ -26,6 +26,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kTile = 1024;                  // compaction granularity (compact_kernel): 32 flag words
 constexpr int kPerTile = kTile / kThreads;   // elements per thread per tile
 constexpr int kChunk = 2;                    // tiles whose loads are issued together
+constexpr int kMaxDev = 8;                   // devices of a cross-device exchange
 
 using State = CoopState;
 
@@ -72,6 +73,11 @@ struct CoopArgs {
   // (SoA, z_cap elements per coordinate); later passes classify from there
   int z_cap;
   int fw_cap;  // flag words per block (shared memory, two slots)
+  // cross-device exchange (a shard of a multi-GPU solve; n_dev == 1: none). xlines[q] is device
+  // q's buffer of kMaxDev lines; this device's total goes to line dev_rank of every buffer
+  int n_dev, dev_rank;
+  double* xlines[kMaxDev];
+  unsigned long long xepoch;
 };
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -151,6 +157,8 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
   double e = a.mode == 1 ? (a.e0 > a.eps ? a.e0 : a.eps) : a.eps;
   int slot = 0, refits = 0, pass = 0;
   double l3 = 0.0;  // Newton warm start of the 3x3 solve across passes (thread 0)
+  long long local_count = 0;  // this device's inliers of the last classify (warp 0)
+  int xtimeout = 0;           // cross-device exchange timed out (warp 0)
   bool have_prev = false;
   bool first_pass = true;
   const int64_t e_begin = t_begin * kTile;
@@ -254,17 +262,58 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) tot[k] = warp_sum_d(acc[k]);
+      local_count = (long long)tot[7];
+      if (a.n_dev > 1) {
+        // ---- cross-device: block 0 writes this device's total (identical in every block) to line
+        // dev_rank of every device's buffer over NVLink (data, then the sequence number with
+        // release at system scope); every block's warp 0 polls its own buffer for all devices'
+        // lines (acquire) and sums them in RANK order -- the same totals on every device
+        const unsigned long long xs = (a.xepoch << 20) | (unsigned long long)(pass + 1);
+        if (blockIdx.x == 0 && lane == 0)
+          for (int q = 0; q < a.n_dev; ++q) {
+            double* line = a.xlines[q] + (size_t)a.dev_rank * kLine;
+            for (int k = 0; k < 8; ++k) __stcg(line + k, tot[k]);
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(line + 8), "l"(xs) : "memory");
+          }
+        const double* mine = a.xlines[a.dev_rank] + (size_t)lane * kLine;
+        double xv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        unsigned long long t_start;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_start));
+        for (;;) {
+          bool ok = true;
+          if (lane < a.n_dev) {
+            unsigned long long v;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine + 8) : "memory");
+            ok = v >= xs;
+          }
+          if (__all_sync(0xFFFFFFFFu, ok)) break;
+          unsigned long long t_now;
+          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_now));
+          if (t_now - t_start > 5000000000ull) {  // a peer never arrived: fail instead of hanging
+            xtimeout = 1;
+            break;
+          }
+        }
+        if (lane < a.n_dev && !xtimeout)
+          for (int k = 0; k < 8; ++k) asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(xv[k]) : "l"(mine + k) : "memory");
+        for (int k = 0; k < 8; ++k) {
+          double g = 0.0;
+          for (int r = 0; r < a.n_dev; ++r) g = xa(g, __shfl_sync(0xFFFFFFFFu, xv[k], r));
+          tot[k] = g;
+        }
+      }
     }
     trace(4);
     trace(5);
     if (tid == 0) {
       const long long count = (long long)tot[7];
       const bool differs = tot[6] != 0.0;
-      int done = 0, rank_deficient = 0;
+      int done = xtimeout, rank_deficient = 0;  // a failed cross-device exchange stops the loop
       double cur[3] = {cls_axis[0], cls_axis[1], cls_axis[2]};  // the set just classified is current
       double nxt[3] = {cls_axis[0], cls_axis[1], cls_axis[2]};
       double e_next = e;
-      if (a.mode == 0) {  // refine_loop (estimator.cpp:51-69)
+      if (done) {
+      } else if (a.mode == 0) {  // refine_loop (estimator.cpp:51-69)
         if (!have_prev && !a.refine) done = 1;
         if (have_prev && !differs) done = 1;  // stable
         if (!done && (refits >= 10 || count < 2)) done = 1;
@@ -302,6 +351,8 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
         st->done = done;
         st->refits = refits;
         st->rank_deficient = rank_deficient;
+        st->local_count = local_count;
+        st->exchange_timeout = xtimeout;
       }
       for (int k = 0; k < 3; ++k) s_next[k] = nxt[k];
       s_next[3] = e_next;
@@ -430,8 +481,13 @@ cudaError_t launch_coop_refine(const double* zx, const double* zy, const double*
                                uint32_t* flags0, uint32_t* flags1, int32_t* tile_count, int32_t* tile_offset,
                                double* block_part, unsigned int* barrier, void* state, int grid, cudaStream_t s,
                                const int32_t* kept, int32_t* compact_out, uint32_t* zero_bins, int n_bins,
-                               unsigned long long* zero_counts) {
+                               unsigned long long* zero_counts, const CoopExchange* xch) {
   CoopArgs a;
+  a.n_dev = xch ? xch->n_dev : 1;
+  a.dev_rank = xch ? xch->rank : 0;
+  for (int q = 0; q < kMaxDev; ++q) a.xlines[q] = xch ? xch->lines[q] : nullptr;
+  a.xepoch = xch ? xch->epoch : 0ull;
+  static_assert(kMaxDev == kCoopMaxDev, "device count");
   a.zx = zx;
   a.zy = zy;
   a.zz = zz;

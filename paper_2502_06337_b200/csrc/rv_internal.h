@@ -213,6 +213,8 @@ struct CoopState {  // published by the kernel after each pass; read by the host
   int done;
   int refits;
   int rank_deficient;
+  long long local_count;  // this device's share of count (cross-device refine)
+  int exchange_timeout;   // a peer device never published its line (cross-device refine)
 };
 // Peak -> start axis on the device (estimate_from_peak, estimator.cpp:94-101): the argmax key,
 // interpolate_peak (estimator.cpp:32-47), backproject, canonicalize -- the host's op order.
@@ -226,6 +228,16 @@ struct PeakOut {
 };
 void launch_peak_axis(const unsigned long long* okey, const uint32_t* grid, int G, double E, uint32_t min_votes,
                       PeakOut* out, cudaStream_t s);
+// Cross-device exchange of a sharded refine (rv_shard_refine): this device's rank among n_dev,
+// every device's line buffer (kCoopXLineBytes each, zeroed before the first use), the solve's
+// epoch (the same on every device, increasing across solves).
+constexpr int kCoopMaxDev = 8;
+constexpr size_t kCoopXLineBytes = (size_t)kCoopMaxDev * 16 * sizeof(double);
+struct CoopExchange {
+  int n_dev = 1, rank = 0;
+  double* lines[kCoopMaxDev] = {};
+  unsigned long long epoch = 0;
+};
 int coop_refine_grid(int sms);
 int coop_tiles(int64_t n);
 size_t coop_state_bytes();
@@ -237,7 +249,7 @@ cudaError_t launch_coop_refine(const double* zx, const double* zy, const double*
                                int32_t* tile_count, int32_t* tile_offset, double* block_part, unsigned int* barrier,
                                void* state, int grid, cudaStream_t s, const int32_t* kept = nullptr,
                                int32_t* compact_out = nullptr, uint32_t* zero_bins = nullptr, int n_bins = 0,
-                               unsigned long long* zero_counts = nullptr);
+                               unsigned long long* zero_counts = nullptr, const CoopExchange* xch = nullptr);
 
 // ---- CSV ingest (rv_io.cu; io.cpp:66-101) ------------------------------------------------
 struct CsvFallback {  // a field the device left to the host's from_chars

@@ -27,6 +27,7 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <cstring>
 #include <functional>
 #include <mutex>
 #include <numbers>
@@ -174,7 +175,9 @@ struct rv_multi {
   std::vector<rv_context*> ctx;
   std::vector<cudaStream_t> streams;
   std::vector<ncclComm_t> comms;
-  std::vector<DevMem> corrs, grid, full;
+  std::vector<DevMem> corrs, grid, full, xlines;  // xlines: cross-device refine line buffers
+  bool peer_ok = false;                            // peer access between every device pair
+  uint64_t xepoch = 0;
   std::vector<int32_t> inliers;
   std::string last_error;
   int nccl_version = 0;
@@ -285,6 +288,37 @@ rv_status rv_multi_create(const int32_t* devices, int32_t n_devices, rv_multi** 
   m->corrs.resize((size_t)n_devices);
   m->grid.resize((size_t)n_devices);
   m->full.resize((size_t)n_devices);
+  m->xlines.resize((size_t)n_devices);
+  // the sharded refine exchanges its per-pass partials through peer memory (NVLink): every
+  // device needs access to every other's line buffer; without it the host steps the passes
+  m->peer_ok = n_devices <= 8;
+  for (int d = 0; d < n_devices && m->peer_ok; ++d)
+    for (int q = 0; q < n_devices && m->peer_ok; ++q) {
+      if (q == d) continue;
+      if (devices[q] == devices[d]) {  // one GPU listed twice: its kernels must not wait on each other
+        m->peer_ok = false;
+        break;
+      }
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, devices[d], devices[q]);
+      if (!can) {
+        m->peer_ok = false;
+        break;
+      }
+      cudaSetDevice(devices[d]);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(devices[q], 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) m->peer_ok = false;
+      cudaGetLastError();
+    }
+  for (int d = 0; d < n_devices && m->peer_ok; ++d) {
+    cudaSetDevice(devices[d]);
+    try {
+      void* p = m->xlines[(size_t)d].get<char>(8 * 16 * sizeof(double));
+      if (cudaMemset(p, 0, 8 * 16 * sizeof(double)) != cudaSuccess) m->peer_ok = false;
+    } catch (const MultiError&) {
+      m->peer_ok = false;
+    }
+  }
   m->pool = new DevicePool(m->devices);
   *out = m;
   return RV_OK;
@@ -301,6 +335,7 @@ void rv_multi_destroy(rv_multi* m) {
     if (d < m->corrs.size()) m->corrs[d].release();
     if (d < m->grid.size()) m->grid[d].release();
     if (d < m->full.size()) m->full[d].release();
+    if (d < m->xlines.size()) m->xlines[d].release();
   }
   for (rv_context* c : m->ctx) rv_context_destroy(c);
   for (size_t d = 0; d < m->streams.size(); ++d) {
@@ -363,7 +398,26 @@ rv_status rv_multi_estimate_single(rv_multi* m, const double* corrs, int64_t n, 
       return c;
     };
     int slot = 0;
-    int64_t count = classify(axis, slot, 0);
+    int64_t count = 0;
+    if (m->peer_ok) {
+      // device-resident refine: one cooperative loop per device, partials exchanged through
+      // peer memory each pass (rv_shard_refine); every device ends with the same axis
+      const uint64_t ep = ++m->xepoch;
+      double* lines[8] = {};
+      for (int d = 0; d < np; ++d) lines[d] = m->xlines[(size_t)d].get<double>(8 * 16);
+      std::vector<std::array<double, 3>> ax((size_t)np);
+      std::vector<int64_t> total((size_t)np);
+      run_all(m, [&](int d) {
+        return rv_shard_refine(m->ctx[(size_t)d], axis, cfg, np, d, lines, ep, ax[(size_t)d].data(),
+                               &total[(size_t)d], &cnt[(size_t)d], sc[(size_t)d].data(), nullptr);
+      });
+      count = total[0];
+      std::memcpy(axis, ax[0].data(), sizeof axis);
+      // rescue (estimator.cpp:352-368) needs every constraint: device 0 finishes
+      if (cfg->refine && (double)count < 3.0 * (cfg->epsilon * (double)n_kept))
+        return finish_on_device0(m, corrs, n, cfg, out);
+    } else {
+    count = classify(axis, slot, 0);
     if (cfg->refine) {
       for (int pass = 0; pass < 10 && count >= 2; ++pass) {
         double s6[6] = {0, 0, 0, 0, 0, 0};
@@ -382,6 +436,7 @@ rv_status rv_multi_estimate_single(rv_multi* m, const double* corrs, int64_t n, 
       }
       // rescue (estimator.cpp:352-368) needs every constraint: device 0 finishes
       if ((double)count < 3.0 * (cfg->epsilon * (double)n_kept)) return finish_on_device0(m, corrs, n, cfg, out);
+    }
     }
     // 5. build_estimate (estimator.cpp:73-92): inliers in rank order, angle vote over the shards
     m->inliers.assign((size_t)count, 0);

@@ -132,3 +132,26 @@ def test_dropin_reference_suites_through_multi():
     assert m, out[-2000:]
     cases, passed, failed, asserts, afailed = map(int, m.groups())
     assert failed == 0 and afailed == 0 and cases >= 50, out[-3000:]
+
+
+def test_shard_refine_device_resident_matches_single(ctx):
+    # rv_shard_refine (the cooperative refine_loop of a shard, whose per-pass partials go through
+    # peer memory on a multi-GPU box) with one device: the same loop, the same fixed-order sums and
+    # the same final set as the single-device solve, bit for bit
+    corrs, _, _ = synth.make_config("c3", 200_000)
+    cfg = rv.EstimatorConfig()
+    d = torch.from_numpy(corrs).cuda()
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    try:
+        grid = torch.zeros((cfg.grid, cfg.grid), dtype=torch.int32, device="cuda")
+        kept = ctx.vote_shard(d.data_ptr(), corrs.shape[0], grid.data_ptr(), cfg)
+        axis0, _, total = ctx.peak_start_axis(grid.data_ptr(), cfg)
+        assert total == kept * cfg.theta_samples
+        ax, count, local, scatter, refits = ctx.shard_refine(axis0, cfg)
+        assert count == local and refits >= 1
+        inl = ctx.shard_inliers(0, 0, count)
+        e = ctx.estimate_single_device(d.data_ptr(), corrs.shape[0], cfg)
+        assert np.array_equal(inl, e.inliers)
+        assert np.array_equal(ax, e.axis)
+    finally:
+        ctx.set_stream(None)

@@ -38,7 +38,7 @@ def test_library_is_sm100a():
 
 def test_abi_and_defaults():
     lib = _native.lib()
-    assert lib.rv_abi_version() == 4
+    assert lib.rv_abi_version() == 5
     c = _native.rv_config()
     lib.rv_config_default(c)
     d = rv.EstimatorConfig()

@@ -1,2 +1,2 @@
-python -m pytest tests -m gpu -q -x -rf 2>&1 | tail -5 > gpurun_out/pytest_gpu.log
-bash tools/_ab.sh "-DRV_ENTRY_RELOAD=0" "" "-DRV_ENTRY_RELOAD=0" "" > gpurun_out/ab.log 2>&1
+python -m pytest tests -m gpu -q -x -rf 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
+python tools/timeline.py c3 dev flush 2>/dev/null | grep -E "coop|span" > gpurun_out/tl.txt
