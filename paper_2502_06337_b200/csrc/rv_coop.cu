@@ -101,17 +101,39 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int tar
   __syncthreads();
 }
 
-// Fixed-shape block reduction of 8 per-thread values into warp 0 lane 0 (returned in v there).
+// Warp sum of 8 values per lane by transpose-reduction: each round halves the values a lane
+// carries (exchange 4, 2, 1, then two plain rounds), 9 double shuffles instead of 40. Lane l ends
+// with the warp total of value (l >> 2) & 7 (the 4 lanes of a group agree: commutative adds).
+__device__ __forceinline__ double warp_sum8(const double (&v)[8]) {
+  const int lane = threadIdx.x & 31;
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+  double a[4], b[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    a[i] = xa(h16 ? v[i + 4] : v[i], __shfl_xor_sync(0xFFFFFFFFu, h16 ? v[i] : v[i + 4], 16));
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+    b[i] = xa(h8 ? a[i + 2] : a[i], __shfl_xor_sync(0xFFFFFFFFu, h8 ? a[i] : a[i + 2], 8));
+  double c = xa(h4 ? b[1] : b[0], __shfl_xor_sync(0xFFFFFFFFu, h4 ? b[0] : b[1], 4));
+  c = xa(c, __shfl_xor_sync(0xFFFFFFFFu, c, 2));
+  return xa(c, __shfl_xor_sync(0xFFFFFFFFu, c, 1));
+}
+__device__ __forceinline__ void warp_bcast8(double r, double (&v)[8]) {  // lane 4k's r -> v[k]
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = __shfl_sync(0xFFFFFFFFu, r, 4 * k);
+}
+
+// Fixed-shape block reduction of 8 per-thread values into warp 0 (returned in v there).
 __device__ __forceinline__ void block_reduce8(double (&v)[8], double (*s_red)[kWarps]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) v[k] = warp_sum_d(v[k]);
-  if (lane == 0)
-    for (int k = 0; k < 8; ++k) s_red[k][warp] = v[k];
+  const double r = warp_sum8(v);
+  if ((lane & 3) == 0) s_red[lane >> 2][warp] = r;
   __syncthreads();
   if (warp == 0) {
+    double x[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = warp_sum_d(lane < kWarps ? s_red[k][lane] : 0.0);
+    for (int k = 0; k < 8; ++k) x[k] = lane < kWarps ? s_red[k][lane] : 0.0;
+    warp_bcast8(warp_sum8(x), v);
   }
 }
 
@@ -260,8 +282,7 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) acc[k] = xa(acc[k], x[j][k]);
       }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) tot[k] = warp_sum_d(acc[k]);
+      warp_bcast8(warp_sum8(acc), tot);
       local_count = (long long)tot[7];
       if (a.n_dev > 1) {
         // ---- cross-device: block 0 writes this device's total (identical in every block) to line
