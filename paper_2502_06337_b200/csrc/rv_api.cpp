@@ -240,6 +240,8 @@ struct rv_context {
   int coop_grid = 0;
   bool coop_bar_ready = false;
   const double* coop_part_zeroed = nullptr;
+  DBuf coop_mpart;                          // line buffer of the K-candidate cooperative refine
+  const double* coop_mpart_zeroed = nullptr;
   // angles / support
   DBuf bins, raw, angle_counts, angle_sums, angle_result, sup_counts, sup_result, band_flagsA, band_flagsB,
       band_idx, band_vals, near_h, near_result;
@@ -856,6 +858,40 @@ CoopState* coop_refine_launch(rv_context* c, const ConstraintSet& cs, const doub
   return dst;
 }
 
+// K start axes at once (launch_coop_refine_multi), in chunks of coop_multi_max(): per candidate k
+// its CoopState at (char*)states + k * stride (and the zeroed angle counts at counts + k * stride),
+// mode 0: its inlier indices at compact_out + k * compact_stride.
+void coop_refine_multi_launch(rv_context* c, const ConstraintSet& cs, const std::vector<std::array<double, 3>>& starts,
+                              const std::vector<double>& e0s, int mode, const rv_config& cfg, CoopState* states,
+                              size_t stride, unsigned long long* counts, int32_t* compact_out, size_t compact_stride,
+                              uint32_t* zero_bins, int n_bins) {
+  StageScope sc(c, kRefine);
+  if (c->coop_grid == 0) c->coop_grid = coop_refine_grid(c->sms);
+  const int km = coop_multi_max();
+  const size_t line = (size_t)8 * km + 8;
+  double* part = c->coop_mpart.get<double>((size_t)c->coop_grid * line);
+  if (part != c->coop_mpart_zeroed) {
+    ck(cudaMemsetAsync(part, 0, sizeof(double) * line * (size_t)c->coop_grid, c->st), "coop multi lines");
+    c->coop_mpart_zeroed = part;
+  }
+  if (!c->coop_bar_ready) {
+    ck(cudaMemsetAsync(c->coop_bar.get<unsigned int>(2), 0, 2 * sizeof(unsigned int), c->st), "coop barrier");
+    c->coop_bar_ready = true;
+  }
+  for (size_t k0 = 0; k0 < starts.size(); k0 += (size_t)km) {
+    const int K = (int)std::min<size_t>((size_t)km, starts.size() - k0);
+    auto* st = reinterpret_cast<CoopState*>(reinterpret_cast<char*>(states) + k0 * stride);
+    auto* cn = counts ? reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(counts) + k0 * stride) : nullptr;
+    ck(launch_coop_refine_multi(cs.zx, cs.zy, cs.zz, cs.n, mode, cfg.refine ? 1 : 0, cfg.epsilon, K,
+                                reinterpret_cast<const double(*)[3]>(starts[k0].data()), e0s.empty() ? nullptr : &e0s[k0],
+                                st, stride, cn, nullptr, 0, cs.kept, compact_out ? compact_out + k0 * compact_stride : nullptr,
+                                compact_stride, zero_bins, n_bins, part, c->coop_bar.get<unsigned int>(2), c->coop_grid,
+                                c->st),
+       "coop multi launch");
+    count_launch(c);
+  }
+}
+
 Cls coop_refine_dev(rv_context* c, const ConstraintSet& cs, double axis[3], int mode, double e0, const rv_config& cfg,
                     int* passes = nullptr) {
   Cls r;
@@ -978,22 +1014,44 @@ std::vector<std::array<double, 3>> rescue_axes_dev(rv_context* c, const uint32_t
   }
   const std::vector<Peak> ps = blurred_argmax_dev(c, grid, cfg.grid, cfg.extent, radii);
   const double cs_ = 2.0 * cfg.extent / cfg.grid;
+  std::vector<std::array<double, 3>> starts;
+  std::vector<double> e0s;
   for (size_t k = 0; k < ps.size(); ++k) {
     double b[3], start[3];
     backproject(ps[k].A, ps[k].B, b);
     canonicalize3(b, start);
-    anneal_axis_dev(c, cs, start, radii[k] * cs_, cfg);
-    out.push_back({start[0], start[1], start[2]});
+    starts.push_back({start[0], start[1], start[2]});
+    e0s.push_back(radii[k] * cs_);
   }
   // least squares over all constraints (refine_axis(constraints))
   if (cs.n >= 2) {
     const Cls all = classify_dev(c, cs, nullptr, 0.0, 0, nullptr, 1);
     double ls[3];
     if (axis_from_scatter(all.scatter, ls)) {
-      anneal_axis_dev(c, cs, ls, 0.25, cfg);
-      out.push_back({ls[0], ls[1], ls[2]});
+      starts.push_back({ls[0], ls[1], ls[2]});
+      e0s.push_back(0.25);
     }
   }
+  if (starts.empty()) return out;
+  static const bool multi_on = [] {
+    const char* e = std::getenv("RV_COOP_MULTI");
+    return !(e && e[0] == '0');
+  }();
+  if (!multi_on) {
+    for (size_t k = 0; k < starts.size(); ++k) {
+      double a[3] = {starts[k][0], starts[k][1], starts[k][2]};
+      anneal_axis_dev(c, cs, a, e0s[k], cfg);
+      out.push_back({a[0], a[1], a[2]});
+    }
+    return out;
+  }
+  // all anneals (estimator.cpp:145-160) in one cooperative launch, one read-back
+  CoopState* st = c->coop_state.get<CoopState>(starts.size());
+  coop_refine_multi_launch(c, cs, starts, e0s, 1, cfg, st, sizeof(CoopState), nullptr, nullptr, 0, nullptr, 0);
+  std::vector<CoopState> h(starts.size());
+  ck(cudaMemcpyAsync(h.data(), st, sizeof(CoopState) * starts.size(), cudaMemcpyDeviceToHost, c->st), "anneal D2H");
+  sync(c);
+  for (const CoopState& x : h) out.push_back({x.axis[0], x.axis[1], x.axis[2]});
   return out;
 }
 
@@ -1812,14 +1870,28 @@ std::vector<CandResult> evaluate_candidates(rv_context* c, const std::vector<std
   uint32_t* bins = c->bins.get<uint32_t>(cfg.angle_bins);
   double* raw = c->raw.get<double>(nn);
   double* asums = c->angle_sums.get<double>(2 * 296);
-  for (size_t k = 0; k < K; ++k) {  // queue every candidate: no read-back in between
-    CoopFused fz;
-    fz.compact_out = idx + k * nn;
-    fz.zero_bins = bins;
-    fz.n_bins = cfg.angle_bins;
-    fz.zero_counts = sums[k].counts;
-    CoopState* st = coop_refine_launch(c, cs, starts[k].data(), nullptr, 0, 0.0, cfg, nullptr, nullptr, &sums[k].st,
-                                       &fz);
+  // every candidate's refine_loop in one cooperative launch (compaction fused), then each angle
+  // vote and peak queued back to back: no read-back in between
+  static const bool multi_on = [] {
+    const char* e = std::getenv("RV_COOP_MULTI");
+    return !(e && e[0] == '0');
+  }();
+  if (multi_on)
+    coop_refine_multi_launch(c, cs, starts, {}, 0, cfg, &sums[0].st, sizeof(Summary), sums[0].counts, idx, nn, bins,
+                             cfg.angle_bins);
+  for (size_t k = 0; k < K; ++k) {
+    CoopState* st = &sums[k].st;
+    if (!multi_on) {
+      CoopFused fz;
+      fz.compact_out = idx + k * nn;
+      fz.zero_bins = bins;
+      fz.n_bins = cfg.angle_bins;
+      fz.zero_counts = sums[k].counts;
+      st = coop_refine_launch(c, cs, starts[k].data(), nullptr, 0, 0.0, cfg, nullptr, nullptr, &sums[k].st, &fz);
+    } else if (k > 0) {
+      launch_zero_i32(reinterpret_cast<int32_t*>(bins), cfg.angle_bins, c->st);  // histogram of the next vote
+      count_launch(c);
+    }
     launch_vote_angles_k(nullptr, corrs, idx + k * nn, cs.n, cfg.angle_bins, cfg.tau_deg, bins, raw, sums[k].counts,
                          c->st, st->axis, &st->count, nullptr);
     launch_peak_angle_k(bins, cfg.angle_bins, raw, cs.n, asums, sums[k].angle, c->done_ptr(), c->st, &st->count);

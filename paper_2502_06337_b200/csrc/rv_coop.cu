@@ -475,6 +475,310 @@ __global__ void __launch_bounds__(kThreads) coop_refine_kernel(CoopArgs a) {
   }
 }
 
+// ---- K candidates at once ------------------------------------------------------------------
+// refine_loop / anneal_axis of up to kMaxCand independent start axes (the rescue candidates of
+// estimator.cpp:352-368 / 452-466, the anneals of rescue_axes) in ONE cooperative launch: each
+// pass classifies the block's (shared-memory resident) constraints once per still-active
+// candidate and exchanges ALL candidates' partials in one line per block, so the latency-bound
+// per-pass exchange and decision are paid once per pass instead of once per candidate. Each
+// candidate follows exactly the single-candidate loop (the same predicate, the same fixed-order
+// sums, the same decisions); a candidate that is done is frozen with its final set.
+constexpr int kMaxCand = 8;
+struct CoopMultiArgs {
+  const double* zx;
+  const double* zy;
+  const double* zz;
+  int64_t n;
+  int mode, refine, K;
+  double eps;
+  double axis0[kMaxCand][3];
+  double e0[kMaxCand];
+  State* state;                // state of candidate k at (char*)state + k * state_stride
+  size_t state_stride;
+  unsigned long long* counts;  // zeroed [2] at (char*)counts + k * state_stride (angle vote that follows)
+  uint32_t* flags_out;         // mode 0: final bitmask of candidate k at flags_out + k * flag_stride
+  size_t flag_stride;
+  const int32_t* kept;
+  int32_t* compact_out;        // mode 0: inlier indices of candidate k at compact_out + k * compact_stride
+  size_t compact_stride;
+  uint32_t* zero_bins;
+  int n_bins;
+  double* block_part;          // [grid][line]: line = 8 K partials + the sequence number
+  unsigned int* barrier;
+  int z_cap, fw_cap;
+};
+
+__global__ void __launch_bounds__(kThreads) coop_refine_multi_kernel(CoopMultiArgs a) {
+  extern __shared__ double s_z[];  // [3][z_cap] z, then [K][2][fw_cap] flag words
+  __shared__ double s_red[8][kWarps];
+  __shared__ double s_val[kMaxCand][8];  // this block's partials of the pass
+  __shared__ double s_tot[kMaxCand][8];  // all blocks' totals of the pass
+  __shared__ double s_axis[kMaxCand][3], s_e[kMaxCand];
+  __shared__ int s_done[kMaxCand], s_fslot[kMaxCand], s_all_done;
+  __shared__ unsigned int s_epoch;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int K = a.K;
+  const size_t line = (size_t)8 * K + 8;
+  const int64_t ntiles = (a.n + kTile - 1) / kTile;
+  const int64_t t_begin = ntiles * blockIdx.x / gridDim.x, t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
+  const int64_t w_begin = t_begin * (kTile / 32);
+  const int64_t w_end = min(t_end * (kTile / 32), (a.n + 31) / 32);
+  uint32_t* s_flags = reinterpret_cast<uint32_t*>(s_z + 3 * (size_t)a.z_cap);  // [K][2][fw_cap]
+  if (tid == 0) s_epoch = __ldcg(a.barrier);
+  if (tid < K) {
+    for (int k = 0; k < 3; ++k) s_axis[tid][k] = a.axis0[tid][k];
+    s_e[tid] = a.mode == 1 ? (a.e0[tid] > a.eps ? a.e0[tid] : a.eps) : a.eps;
+    s_done[tid] = 0;
+    s_fslot[tid] = 0;
+  }
+  __syncthreads();
+  const unsigned long long epoch = (unsigned long long)s_epoch << 20;
+  int slot = 0, pass = 0;
+  bool have_prev = false, first_pass = true;
+  int refits = 0;      // thread c < K: candidate c's
+  double l3 = 0.0;     // thread c < K: candidate c's Newton warm start
+  const int64_t e_begin = t_begin * kTile;
+  const int64_t cap = a.z_cap;
+  for (;;) {
+    for (int c = 0; c < K; ++c) {
+      if (s_done[c]) continue;  // uniform
+      const double ax0 = s_axis[c][0], ax1 = s_axis[c][1], ax2 = s_axis[c][2], e = s_e[c];
+      uint32_t* flags = s_flags + ((size_t)c * 2 + slot) * a.fw_cap;
+      const uint32_t* prev = s_flags + ((size_t)c * 2 + (slot ^ 1)) * a.fw_cap;
+      double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int diff = 0, cnt = 0;
+      const bool from_global = cap == 0 || first_pass;
+      for (int64_t t0 = t_begin; t0 < t_end; t0 += kChunk) {
+        double z[kChunk][kPerTile][3];
+#pragma unroll
+        for (int cc = 0; cc < kChunk; ++cc)
+#pragma unroll
+          for (int r = 0; r < kPerTile; ++r) {
+            const int64_t i = (t0 + cc) * kTile + r * kThreads + tid;
+            const bool ok = t0 + cc < t_end && i < a.n;
+            const int64_t li = i - e_begin;  // the same thread owns element i in every pass
+            if (!from_global) {
+              z[cc][r][0] = ok ? s_z[li] : 0.0;
+              z[cc][r][1] = ok ? s_z[cap + li] : 0.0;
+              z[cc][r][2] = ok ? s_z[2 * cap + li] : 0.0;
+            } else {
+              z[cc][r][0] = ok ? a.zx[i] : 0.0;
+              z[cc][r][1] = ok ? a.zy[i] : 0.0;
+              z[cc][r][2] = ok ? a.zz[i] : 0.0;
+              if (cap > 0 && ok) {
+                s_z[li] = z[cc][r][0];
+                s_z[cap + li] = z[cc][r][1];
+                s_z[2 * cap + li] = z[cc][r][2];
+              }
+            }
+          }
+#pragma unroll
+        for (int cc = 0; cc < kChunk; ++cc) {
+          if (t0 + cc >= t_end) break;  // uniform
+#pragma unroll
+          for (int r = 0; r < kPerTile; ++r) {
+            const int64_t i = (t0 + cc) * kTile + r * kThreads + tid;
+            const double z0 = z[cc][r][0], z1 = z[cc][r][1], z2 = z[cc][r][2];
+            bool in = false;
+            if (i < a.n) {
+              const double d = xa(xa(xm(ax0, z0), xm(ax1, z1)), xm(ax2, z2));
+              in = fabs(d) < e;
+            }
+            const unsigned word = __ballot_sync(0xFFFFFFFFu, in);
+            const int64_t w0 = (t0 + cc) * kTile + r * kThreads + warp * 32;
+            if (lane == 0 && w0 < a.n) {
+              const int64_t lw = (w0 >> 5) - w_begin;
+              if (have_prev && prev[lw] != word) diff = 1;
+              flags[lw] = word;
+            }
+            if (in) {
+              ++cnt;
+              v[0] = xa(v[0], xm(z0, z0));
+              v[1] = xa(v[1], xm(z0, z1));
+              v[2] = xa(v[2], xm(z0, z2));
+              v[3] = xa(v[3], xm(z1, z1));
+              v[4] = xa(v[4], xm(z1, z2));
+              v[5] = xa(v[5], xm(z2, z2));
+            }
+          }
+        }
+      }
+      first_pass = false;  // z is now in shared memory (each thread reads back its own elements)
+      v[6] = (double)__any_sync(0xFFFFFFFFu, diff);
+      v[7] = (double)cnt;
+      block_reduce8(v, s_red);
+      if (tid == 0)
+        for (int k = 0; k < 8; ++k) s_val[c][k] = v[k];
+      __syncthreads();
+    }
+    const unsigned long long seq = epoch | (unsigned long long)(pass + 1);
+    if (tid == 0) {
+      double* ln = a.block_part + (size_t)blockIdx.x * line;
+      for (int c = 0; c < K; ++c)
+        if (!s_done[c])
+          for (int k = 0; k < 8; ++k) __stcg(ln + 8 * c + k, s_val[c][k]);
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ln + 8 * K), "l"(seq) : "memory");
+    }
+    if (warp == 0) {
+      const unsigned nl = (gridDim.x + 31) / 32;
+      for (;;) {
+        bool ok = true;
+        for (unsigned j = 0; j < nl; ++j) {
+          const unsigned b = lane + 32 * j;
+          if (b < gridDim.x) {
+            unsigned long long v;
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.block_part + (size_t)b * line + 8 * K)
+                         : "memory");
+            ok &= v >= seq;
+          }
+        }
+        if (__all_sync(0xFFFFFFFFu, ok)) break;
+      }
+      for (int c = 0; c < K; ++c) {
+        if (s_done[c]) continue;  // uniform
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (unsigned b = lane; b < gridDim.x; b += 32)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[k] = xa(acc[k], __ldcg(a.block_part + (size_t)b * line + 8 * c + k));
+        double t[8];
+        warp_bcast8(warp_sum8(acc), t);
+        if (lane == 0)
+          for (int k = 0; k < 8; ++k) s_tot[c][k] = t[k];
+      }
+      __syncwarp();
+      // lane c decides for candidate c (the single-candidate logic)
+      if (lane < K && !s_done[lane]) {
+        const int c = lane;
+        const double* tot = s_tot[c];
+        const long long count = (long long)tot[7];
+        const bool differs = tot[6] != 0.0;
+        int done = 0, rank_deficient = 0;
+        const double e = s_e[c];
+        double cur[3] = {s_axis[c][0], s_axis[c][1], s_axis[c][2]};
+        double nxt[3] = {cur[0], cur[1], cur[2]};
+        double e_next = e;
+        if (a.mode == 0) {
+          if (!have_prev && !a.refine) done = 1;
+          if (have_prev && !differs) done = 1;
+          if (!done && (refits >= 10 || count < 2)) done = 1;
+          if (!done) {
+            if (axis_from_scatter_fast(tot, nxt, &l3)) {
+              ++refits;
+            } else {
+              rank_deficient = 1;
+              done = 1;
+            }
+          }
+        } else {
+          if (count >= 2 && axis_from_scatter_fast(tot, nxt, &l3))
+            for (int k = 0; k < 3; ++k) cur[k] = nxt[k];
+          for (int k = 0; k < 3; ++k) nxt[k] = cur[k];
+          if (e <= a.eps) done = 1;
+          const double h = 0.5 * e;
+          e_next = a.eps > h ? a.eps : h;
+        }
+        if (blockIdx.x == 0) {
+          State* st = reinterpret_cast<State*>(reinterpret_cast<char*>(a.state) + (size_t)c * a.state_stride);
+          for (int k = 0; k < 3; ++k) {
+            st->axis[k] = cur[k];
+            st->next[k] = nxt[k];
+          }
+          for (int k = 0; k < 6; ++k) st->scatter[k] = tot[k];
+          st->e = e_next;
+          st->count = count;
+          st->slot = 0;
+          st->done = done;
+          st->refits = refits;
+          st->rank_deficient = rank_deficient;
+          st->local_count = count;
+          st->exchange_timeout = 0;
+        }
+        for (int k = 0; k < 3; ++k) s_axis[c][k] = nxt[k];
+        s_e[c] = e_next;
+        if (done) {
+          s_done[c] = 1;
+          s_fslot[c] = slot;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        int all = 1;
+        for (int c = 0; c < K; ++c) all &= s_done[c];
+        s_all_done = all;
+      }
+    }
+    __syncthreads();
+    if (s_all_done) break;
+    slot ^= 1;
+    ++pass;
+    have_prev = a.mode == 0;
+  }
+  if (a.mode == 0) {
+    // per candidate: final set into its flags_out, fused compaction (this block's offset = the
+    // candidate's inliers in the blocks before it, from their lines of the candidate's last pass)
+    __shared__ long long s_pre[kWarps];
+    __shared__ int s_wsum[kWarps];
+    for (int c = 0; c < K; ++c) {
+      const uint32_t* flags = s_flags + ((size_t)c * 2 + s_fslot[c]) * a.fw_cap;
+      uint32_t* fo = a.flags_out ? a.flags_out + (size_t)c * a.flag_stride : nullptr;
+      if (fo)
+        for (int64_t w = w_begin + tid; w < w_end; w += kThreads) fo[w] = flags[w - w_begin];
+      if (!a.compact_out) continue;
+      long long pre = 0;
+      for (unsigned b = tid; b < blockIdx.x; b += kThreads) pre += (long long)__ldcg(a.block_part + (size_t)b * line + 8 * c + 7);
+      for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xFFFFFFFFu, pre, o);
+      if (lane == 0) s_pre[warp] = pre;
+      __syncthreads();
+      long long off = 0;
+      for (int w = 0; w < kWarps; ++w) off += s_pre[w];
+      int32_t* out = a.compact_out + (size_t)c * a.compact_stride;
+      for (int64_t c0 = w_begin; c0 < w_end; c0 += kThreads) {
+        const int64_t wi = c0 + tid;
+        const uint32_t word = wi < w_end ? flags[wi - w_begin] : 0u;
+        const int cw = __popc(word);
+        int incl = cw;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        int wpre = 0, ctot = 0;
+        for (int w = 0; w < kWarps; ++w) {
+          wpre += w < warp ? s_wsum[w] : 0;
+          ctot += s_wsum[w];
+        }
+        uint32_t m = word;
+        long long pos = off + wpre + (incl - cw);
+        while (m) {
+          const int bit = __ffs(m) - 1;
+          m &= m - 1u;
+          const int64_t i = wi * 32 + bit;
+          out[pos++] = a.kept ? __ldg(a.kept + i) : (int32_t)i;
+        }
+        off += ctot;
+        __syncthreads();
+      }
+    }
+    if (blockIdx.x == 0) {
+      for (int k = tid; k < a.n_bins; k += kThreads) a.zero_bins[k] = 0u;
+      if (a.counts)
+        for (int c = 0; c < K; ++c)
+          if (tid < 2)
+            reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(a.counts) + (size_t)c * a.state_stride)[tid] = 0ull;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(a.barrier + 1, 1u) == gridDim.x - 1) {
+      a.barrier[1] = 0u;
+      __threadfence();
+      atomicAdd(a.barrier, 1u);
+    }
+  }
+}
+
 // estimate_from_peak on the device (single thread): see exact_peak_axis (rv_exact.cuh).
 __global__ void peak_axis_kernel(const unsigned long long* okey, const uint32_t* grid, int G, double E,
                                  uint32_t min_votes, PeakOut* out) {
@@ -574,6 +878,80 @@ cudaError_t launch_coop_refine(const double* zx, const double* zy, const double*
   // cooperative launch: guarantees co-residency of all blocks (required by the grid barrier)
   return cudaLaunchCooperativeKernel((void*)coop_refine_kernel, dim3(grid), dim3(kThreads), args, dyn, s);
 }
+
+cudaError_t launch_coop_refine_multi(const double* zx, const double* zy, const double* zz, int64_t n, int mode,
+                                     int refine, double eps, int K, const double (*axes)[3], const double* e0s,
+                                     void* state, size_t state_stride, unsigned long long* counts, uint32_t* flags_out,
+                                     size_t flag_stride, const int32_t* kept, int32_t* compact_out, size_t compact_stride,
+                                     uint32_t* zero_bins, int n_bins, double* block_part, unsigned int* barrier,
+                                     int grid, cudaStream_t s) {
+  if (K < 1 || K > kMaxCand) return cudaErrorInvalidValue;
+  CoopMultiArgs a;
+  a.zx = zx;
+  a.zy = zy;
+  a.zz = zz;
+  a.n = n;
+  a.mode = mode;
+  a.refine = refine;
+  a.K = K;
+  a.eps = eps;
+  for (int c = 0; c < kMaxCand; ++c) {
+    for (int k = 0; k < 3; ++k) a.axis0[c][k] = c < K ? axes[c][k] : 0.0;
+    a.e0[c] = c < K && e0s ? e0s[c] : 0.0;
+  }
+  a.state = static_cast<State*>(state);
+  a.state_stride = state_stride;
+  a.counts = counts;
+  a.flags_out = flags_out;
+  a.flag_stride = flag_stride;
+  a.kept = kept;
+  a.compact_out = compact_out;
+  a.compact_stride = compact_stride;
+  a.zero_bins = zero_bins;
+  a.n_bins = n_bins;
+  a.block_part = block_part;
+  a.barrier = barrier;
+  const int64_t ntiles = (n + kTile - 1) / kTile;
+  if (grid > ntiles) grid = (int)(ntiles > 0 ? ntiles : 1);
+  static int smem_max = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
+  }();
+  static const size_t static_bytes = [] {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(coop_refine_multi_kernel));
+    return fa.sharedSizeBytes + 1024;
+  }();
+  const int64_t per_block = (ntiles + grid - 1) / grid * kTile;
+  a.fw_cap = (int)(per_block / 32);
+  const size_t flag_bytes = (size_t)K * 2 * a.fw_cap * sizeof(uint32_t);
+  size_t dyn = (size_t)(3 * per_block) * sizeof(double) + flag_bytes;
+  a.z_cap = (int)per_block;
+  if (dyn + static_bytes > (size_t)smem_max) {
+    a.z_cap = 0;
+    dyn = flag_bytes;
+  }
+  if (dyn + static_bytes > (size_t)smem_max) return cudaErrorInvalidValue;
+  {
+    static std::mutex mu;
+    static size_t configured[16] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev < 0 || dev >= 16 || configured[dev] < dyn) {
+      const cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(coop_refine_multi_kernel),
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+      if (e != cudaSuccess) return e;
+      if (dev >= 0 && dev < 16) configured[dev] = dyn;
+    }
+  }
+  void* args[] = {&a};
+  return cudaLaunchCooperativeKernel((void*)coop_refine_multi_kernel, dim3(grid), dim3(kThreads), args, dyn, s);
+}
+
+int coop_multi_max() { return kMaxCand; }
 
 size_t coop_state_bytes() { return sizeof(State); }
 

@@ -238,6 +238,19 @@ struct CoopExchange {
   double* lines[kCoopMaxDev] = {};
   unsigned long long epoch = 0;
 };
+// K (<= coop_multi_max()) independent refine_loop / anneal_axis runs from their own start axes
+// in ONE cooperative launch (shared per-pass exchange). Per candidate k: CoopState at
+// (char*)state + k * state_stride, angle counts [2] zeroed at (char*)counts + k * state_stride,
+// mode 0: final bitmask at flags_out + k * flag_stride (optional), inlier indices at
+// compact_out + k * compact_stride (optional). block_part: its own buffer, grid * (8 K + 8) doubles,
+// zeroed before the first use (not shared with launch_coop_refine's lines).
+cudaError_t launch_coop_refine_multi(const double* zx, const double* zy, const double* zz, int64_t n, int mode,
+                                     int refine, double eps, int K, const double (*axes)[3], const double* e0s,
+                                     void* state, size_t state_stride, unsigned long long* counts, uint32_t* flags_out,
+                                     size_t flag_stride, const int32_t* kept, int32_t* compact_out, size_t compact_stride,
+                                     uint32_t* zero_bins, int n_bins, double* block_part, unsigned int* barrier,
+                                     int grid, cudaStream_t s);
+int coop_multi_max();
 int coop_refine_grid(int sms);
 int coop_tiles(int64_t n);
 size_t coop_state_bytes();

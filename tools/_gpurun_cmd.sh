@@ -1,6 +1,4 @@
-python -m pytest tests -m gpu -q -x -rf 2>&1 | tail -5 > gpurun_out/pytest_gpu.log
-RV_NVCC_EXTRA="-DRV_COOP_TRACE" python paper_2502_06337_b200/build.py --force > /dev/null
-python tools/coop_trace.py c3 > gpurun_out/coop_trace_c3.txt 2>&1
-python paper_2502_06337_b200/build.py --force > /dev/null
-python tools/timeline.py c3 dev flush 2>/dev/null | grep -E "coop|span" > gpurun_out/tl.txt
-python tools/timeline.py c4 dev flush 2>/dev/null | grep -E "span" > gpurun_out/tl4.txt
+python -m pytest tests -m gpu -q -x -rf 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
+python tools/fuzz_estimate.py 9 180 > gpurun_out/fuzz_est.txt 2>&1
+python tools/config_table.py > gpurun_out/ct.json 2> gpurun_out/ct_multi.txt
+RV_COOP_MULTI=0 python tools/config_table.py > gpurun_out/ct0.json 2> gpurun_out/ct_single.txt
