@@ -27,7 +27,14 @@ h.numpy()[:] = corrs
 cfg = rv.EstimatorConfig()
 
 
+multi = "multi" in sys.argv[2:]  # estimate_multi (max_models=3)
+if multi:
+    cfg = rv.EstimatorConfig(max_models=3)
+
+
 def solve():
+    if multi:
+        return ctx.estimate_multi_device(d.data_ptr(), corrs.shape[0], cfg)
     if host:
         return ctx.estimate_single(h.numpy(), cfg)
     return ctx.estimate_single_device(d.data_ptr(), corrs.shape[0], cfg)
