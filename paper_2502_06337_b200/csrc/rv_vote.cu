@@ -292,7 +292,7 @@ __device__ __forceinline__ Runs2 band_runs(const Bnd& lo_b, const Bnd& hi_b, int
 // before the wrap reads the table's 64-sample slack), so the vote's step grid never shifts.
 // Straight-line over two run slots.
 __device__ __forceinline__ void finalize_run(int lo, int hi, int prev_hi, int ub, int J, uint32_t* ea, uint32_t* eb,
-                                             int* hi_out, unsigned long long* work) {
+                                             int* hi_out, uint32_t* work) {
   lo = max(lo & ~1, prev_hi + 1);
   hi |= 1;
   int need = ((hi - lo + 64) & ~63) - (hi - lo + 1);
@@ -301,22 +301,22 @@ __device__ __forceinline__ void finalize_run(int lo, int hi, int prev_hi, int ub
   need -= up;
   lo -= min(need, lo - (prev_hi + 1));
   *hi_out = hi;
-  *work += (unsigned long long)((hi - lo + 64) & ~63);
+  *work += (uint32_t)((hi - lo + 64) & ~63);
   const int cut = lo + (((J - lo) + 63) & ~63);  // first step boundary at or after J
   const bool below = hi < J, above = lo >= J, split = !below && !above && cut <= hi;
   const int s0 = above ? lo - J : lo, h0 = above ? hi - J : (split ? cut - 1 : hi);
   *ea = (uint32_t)s0 | ((uint32_t)(h0 - s0 + 1) << 16);
   *eb = split ? ((uint32_t)(cut - J) | ((uint32_t)(hi - cut + 1) << 16)) : 0u;
 }
-__device__ __forceinline__ Ent3 finalize_runs(const Runs2& runs, int A0, int A1, int J, unsigned long long* work) {
+__device__ __forceinline__ Ent3 finalize_runs(const Runs2& runs, int A0, int A1, int J, uint32_t* work) {
   Ent3 o{0u, 0u, 0u};
   uint32_t a0, b0, a1, b1;
   int h0, h1;
-  unsigned long long w0 = 0, w1 = 0;
+  uint32_t w0 = 0, w1 = 0;
   finalize_run(runs.l0, runs.h0, A0 - 1, runs.n == 2 ? (runs.l1 & ~1) - 1 : A1, J, &a0, &b0, &h0, &w0);
   finalize_run(runs.l1, runs.h1, h0, A1, J, &a1, &b1, &h1, &w1);
   const bool one = runs.n >= 1, two = runs.n == 2;
-  *work += (one ? w0 : 0ull) + (two ? w1 : 0ull);
+  *work += (one ? w0 : 0u) + (two ? w1 : 0u);
   o.e0 = one ? a0 : 0u;
   o.e1 = two ? a1 : 0u;
   o.e2 = (one ? b0 : 0u) | (two ? b1 : 0u);
@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(VotePlan p, VoteBuff
   b_lo.olo = b_lo.ohi = b_lo.ilo = b_lo.ihi = 0;
   b_lo.c = 0.f;
   // entries of this constraint in band `band` (+ planned samples into *w)
-  auto plan_band = [&](int band, unsigned long long* w) -> Ent3 {
+  auto plan_band = [&](int band, uint32_t* w) -> Ent3 {
     Bnd b_hi;  // the last band's upper boundary: Y >= +inf, empty
     b_hi.ost = 0;
     b_hi.ist = 0;
@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(VotePlan p, VoteBuff
   // warp-level bookkeeping of one band: this lane's entry offset inside the warp's block of
   // entries; the warp's count and planned samples are parked per (band, warp) for the block scan
   // (kNB > 0) or reserved in the global list directly (kNB == 0)
-  auto book = [&](int band, const Ent3& r, unsigned long long w, bool global) -> int {
+  auto book = [&](int band, const Ent3& r, uint32_t w, bool global) -> int {
     const unsigned m0 = __ballot_sync(0xFFFFFFFFu, r.e0 != 0u);
     const unsigned m1 = __ballot_sync(0xFFFFFFFFu, r.e1 != 0u);
     const unsigned m2 = __ballot_sync(0xFFFFFFFFu, r.e2 != 0u);
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(VotePlan p, VoteBuff
     const int nb = kExact ? kNB : p.n_bands;
 #pragma unroll(kExact ? kNB : 1)
     for (int band = 0; band < nb; ++band) {  // uniform
-      unsigned long long w = 0;
+      uint32_t w = 0;
       const Ent3 r = plan_band(band, &w);
       s_r[band][0][threadIdx.x] = r.e0;
       s_r[band][1][threadIdx.x] = r.e1;
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(VotePlan p, VoteBuff
            (int64_t)s_base[band] + s_wcnt[band][warp] + s_off[band][threadIdx.x]);
   } else {
     for (int band = 0; band < p.n_bands; ++band) {  // uniform trip count: warp collectives inside
-      unsigned long long w = 0;
+      uint32_t w = 0;
       const Ent3 r = plan_band(band, &w);
       emit(band, r, book(band, r, w, true));
     }
