@@ -329,8 +329,12 @@ __global__ void __launch_bounds__(256) peak_angle_kernel(const uint32_t* bins, i
     if (d <= -kPi) d = xa(d, 2.0 * kPi);
     if (d > kPi) d = xs(d, 2.0 * kPi);
     if (fabs(d) <= window) {
-      v[0] = xa(v[0], sin(a));
-      v[1] = xa(v[1], cos(a));
+      // sincos shares the argument reduction; its results are bit-identical to sin() and cos()
+      // (checked on 16.8M angles over [-pi, pi] on the B200: tools/_bin/sincos_check)
+      double sa, ca;
+      sincos(a, &sa, &ca);
+      v[0] = xa(v[0], sa);
+      v[1] = xa(v[1], ca);
     }
   }
   for (int k = 0; k < 2; ++k)
