@@ -18,6 +18,32 @@ __device__ __forceinline__ double xdot(double a0, double a1, double a2, double b
   return xa(xa(xm(a0, b0), xm(a1, b1)), xm(a2, b2));  // Eigen 3-vector dot: (a0b0 + a1b1) + a2b2
 }
 
+// preprocess of one correspondence (estimator.cpp:264-279): optional normalisation of x and y,
+// d = y - x, dropped iff |d| < tau_z (returns false), z = d / |d| -- the reference's op order.
+__device__ __forceinline__ bool preprocess_pair(double x0, double x1, double x2, double y0, double y1, double y2,
+                                                int normalize, double tau_z, double z[3]) {
+  if (normalize) {
+    const double nx = __dsqrt_rn(xdot(x0, x1, x2, x0, x1, x2));
+    const double ny = __dsqrt_rn(xdot(y0, y1, y2, y0, y1, y2));
+    if (nx > 0.0) {
+      x0 = xd(x0, nx);
+      x1 = xd(x1, nx);
+      x2 = xd(x2, nx);
+    }
+    if (ny > 0.0) {
+      y0 = xd(y0, ny);
+      y1 = xd(y1, ny);
+      y2 = xd(y2, ny);
+    }
+  }
+  const double d0 = xs(y0, x0), d1 = xs(y1, x1), d2 = xs(y2, x2);
+  const double len = __dsqrt_rn(xdot(d0, d1, d2, d0, d1, d2));
+  z[0] = xd(d0, len);
+  z[1] = xd(d1, len);
+  z[2] = xd(d2, len);
+  return !(len < tau_z);
+}
+
 // orthonormal_basis, geom.cpp:36-43 (Gram-Schmidt from the least-aligned unit axis).
 __device__ __forceinline__ void exact_basis(double z0, double z1, double z2, double a1[3], double a2[3]) {
   const double f0 = fabs(z0), f1 = fabs(z1), f2 = fabs(z2);

@@ -65,21 +65,10 @@ __global__ void __launch_bounds__(kPrepThreads) preprocess_kernel(PrepBuffers b,
 #pragma unroll
   for (int r = 0; r < kPrepPer; ++r) {
     const int64_t i = base + r * kPrepThreads + tid;
-    double x0 = c[r][0], x1 = c[r][1], x2 = c[r][2], y0 = c[r][3], y1 = c[r][4], y2 = c[r][5];
-    if (normalize) {
-      const double nx = __dsqrt_rn(xdot(x0, x1, x2, x0, x1, x2));
-      const double ny = __dsqrt_rn(xdot(y0, y1, y2, y0, y1, y2));
-      if (nx > 0.0) { x0 = xd(x0, nx); x1 = xd(x1, nx); x2 = xd(x2, nx); }
-      if (ny > 0.0) { y0 = xd(y0, ny); y1 = xd(y1, ny); y2 = xd(y2, ny); }
-    }
-    const double d0 = xs(y0, x0), d1 = xs(y1, x1), d2 = xs(y2, x2);
-    const double len = __dsqrt_rn(xdot(d0, d1, d2, d0, d1, d2));
+    const bool kept = preprocess_pair(c[r][0], c[r][1], c[r][2], c[r][3], c[r][4], c[r][5], normalize, tau_z, zo[r]);
     const bool valid = i < lim;
-    drop[r] = valid && (len < tau_z);
-    keep[r] = valid && !drop[r];
-    zo[r][0] = xd(d0, len);
-    zo[r][1] = xd(d1, len);
-    zo[r][2] = xd(d2, len);
+    drop[r] = valid && !kept;
+    keep[r] = valid && kept;
     km[r] = __ballot_sync(0xFFFFFFFFu, keep[r]);
     if (lane == 0) s_cnt[r * kPrepWarps + warp] = __popc(km[r]);
   }
