@@ -214,6 +214,13 @@ rv_status rv_axis_from_scatter(const double scatter[6], double axis[3]);
 rv_status rv_shard_refine(rv_context* ctx, const double axis0[3], const rv_config* cfg, int32_t n_dev, int32_t rank,
                           double* const* peer_lines, uint64_t epoch, double axis[3], int64_t* count,
                           int64_t* local_count, double scatter[6], int32_t* refits);
+/* Line buffers for rv_shard_refine across PROCESSES (one rank per GPU): rv_shard_lines_export
+ * allocates this context's buffer (once, zeroed) and returns it with its CUDA IPC handle (64
+ * bytes) for the other ranks; rv_shard_lines_open maps a peer rank's buffer from its handle
+ * (closed with the context). Ranks on the same GPU must not use rv_shard_refine together (their
+ * cooperative kernels would wait on each other): host-step the passes instead. */
+rv_status rv_shard_lines_export(rv_context* ctx, void** lines, uint8_t handle[64]);
+rv_status rv_shard_lines_open(rv_context* ctx, const uint8_t handle[64], void** lines);
 rv_status rv_shard_inliers(rv_context* ctx, int32_t slot, int64_t offset, int32_t* dst, int64_t capacity,
                            int64_t* count);
 rv_status rv_shard_angle_hist(rv_context* ctx, const double axis[3], const rv_config* cfg, uint32_t* bins,

@@ -327,17 +327,34 @@ class Context:
                                                 C.byref(cnt), _ptr(sc, C.c_double), C.byref(diff)))
         return cnt.value, sc, bool(diff.value)
 
-    def shard_refine(self, axis0, cfg: EstimatorConfig | None = None):
-        """refine_loop of this context's shard as one device-resident loop (single device: no peer
-        exchange) -> (axis, count, local_count, scatter[6], refits); final set in slot 0."""
+    def shard_refine(self, axis0, cfg: EstimatorConfig | None = None, n_dev: int = 1, rank: int = 0,
+                     lines=None, epoch: int = 0):
+        """refine_loop of this context's shard as one device-resident loop; with n_dev > 1 the
+        per-pass partials are exchanged with the other devices through `lines` (every rank's line
+        buffer, rank order: rv_shard_lines_export / rv_shard_lines_open) ->
+        (axis, count, local_count, scatter[6], refits); final set in slot 0."""
         c = (cfg or EstimatorConfig()).to_c()
         a0 = np.ascontiguousarray(axis0, dtype=np.float64)
         ax, sc = np.zeros(3), np.zeros(6)
         cnt, loc, rf = C.c_int64(), C.c_int64(), C.c_int32()
-        self._check(self._lib.rv_shard_refine(self.handle, _ptr(a0, C.c_double), C.byref(c), 1, 0, None, 0,
+        arr = (C.c_void_p * max(1, n_dev))(*(lines or [])) if n_dev > 1 else None
+        self._check(self._lib.rv_shard_refine(self.handle, _ptr(a0, C.c_double), C.byref(c), n_dev, rank, arr, epoch,
                                               _ptr(ax, C.c_double), C.byref(cnt), C.byref(loc), _ptr(sc, C.c_double),
                                               C.byref(rf)))
         return ax, cnt.value, loc.value, sc, rf.value
+
+    def shard_lines_export(self) -> tuple[int, bytes]:
+        """this context's line buffer for a cross-process shard_refine -> (device pointer, IPC handle)."""
+        ptr = C.c_void_p()
+        h = C.create_string_buffer(64)
+        self._check(self._lib.rv_shard_lines_export(self.handle, C.byref(ptr), h))
+        return ptr.value, h.raw
+
+    def shard_lines_open(self, handle: bytes) -> int:
+        """map a peer rank's line buffer from its IPC handle -> device pointer (closed with the context)."""
+        ptr = C.c_void_p()
+        self._check(self._lib.rv_shard_lines_open(self.handle, C.create_string_buffer(handle, 64), C.byref(ptr)))
+        return ptr.value
 
     def shard_inliers(self, slot: int, offset: int, count: int) -> np.ndarray:
         out = np.zeros(max(count, 1), np.int32)

@@ -119,6 +119,8 @@ _SIGS = [
     ("rv_shard_refine", C.c_int,
      [C.c_void_p, c_double_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_uint64, c_double_p, c_int64_p,
       c_int64_p, c_double_p, c_int32_p]),
+    ("rv_shard_lines_export", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_char_p]),
+    ("rv_shard_lines_open", C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p)]),
     ("rv_shard_inliers", C.c_int, [C.c_void_p, C.c_int32, C.c_int64, c_int32_p, C.c_int64, c_int64_p]),
     ("rv_shard_angle_hist", C.c_int, [C.c_void_p, c_double_p, C.POINTER(rv_config), c_uint32_p, c_uint64_p]),
     ("rv_shard_angle_sums", C.c_int, [C.c_void_p, c_uint32_p, C.POINTER(rv_config), c_double_p]),

@@ -239,6 +239,8 @@ struct rv_context {
   DBuf cons_axes, cons_counts, cons_z, cons_idx;  // baseline consensus scoring
   int coop_grid = 0;
   bool coop_bar_ready = false;
+  void* xlines_own = nullptr;              // this context's line buffer for a cross-process refine
+  std::vector<void*> xlines_peers;          // peer ranks' line buffers mapped by CUDA IPC
   const double* coop_part_zeroed = nullptr;
   DBuf coop_mpart;                          // line buffer of the K-candidate cooperative refine
   const double* coop_mpart_zeroed = nullptr;
@@ -2350,6 +2352,8 @@ void rv_context_destroy(rv_context* c) {
   if (c->csv_pinned) cudaFreeHost(c->csv_pinned);
   if (c->in_pinned) cudaFreeHost(c->in_pinned);
   if (c->big_pinned) cudaFreeHost(c->big_pinned);
+  for (void* q : c->xlines_peers) cudaIpcCloseMemHandle(q);
+  if (c->xlines_own) cudaFree(c->xlines_own);
   c->copy_pool.reset();
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
@@ -2938,6 +2942,35 @@ rv_status rv_shard_refine(rv_context* c, const double axis0[3], const rv_config*
     c->shard_cls[0].offsets = offsets;
     c->shard_cls[0].count = h->local_count;
     c->shard_cls[1].count = -1;
+  });
+}
+
+rv_status rv_shard_lines_export(rv_context* c, void** lines, uint8_t handle[64]) {
+  if (!c || !lines || !handle) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (!c->xlines_own) {  // allocated once (a fixed address for the peers), zeroed
+      ck(cudaMalloc(&c->xlines_own, kCoopXLineBytes), "line buffer");
+      ck(cudaMemset(c->xlines_own, 0, kCoopXLineBytes), "line buffer");
+    }
+    cudaIpcMemHandle_t h;
+    ck(cudaIpcGetMemHandle(&h, c->xlines_own), "cudaIpcGetMemHandle");
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    std::memcpy(handle, &h, 64);
+    *lines = c->xlines_own;
+  });
+}
+
+rv_status rv_shard_lines_open(rv_context* c, const uint8_t handle[64], void** lines) {
+  if (!c || !handle || !lines) return RV_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    void* q = nullptr;
+    ck(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    c->xlines_peers.push_back(q);
+    *lines = q;
   });
 }
 

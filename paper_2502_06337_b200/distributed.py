@@ -92,6 +92,37 @@ class DeviceBackend:
     def tensor_device(self):
         return self.device
 
+    # ---- device-resident refine across the ranks (rv_shard_refine over CUDA IPC line buffers) ----
+    def peer_refine_ready(self, group=None) -> bool:
+        """Collective (first call): export this rank's line buffer, gather every rank's IPC handle and
+        GPU, map the peers' buffers. Disabled (host-stepped passes) when two ranks share a GPU --
+        their cooperative kernels would wait on each other -- or with more than 8 ranks."""
+        key = id(group)
+        cache = getattr(self, "_xready", {})
+        if key in cache:
+            return cache[key] is not None
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        ptr, handle = self.ctx.shard_lines_export()
+        uuid = str(torch.cuda.get_device_properties(self.device).uuid)
+        info = [None] * world
+        dist.all_gather_object(info, (uuid, handle), group=group)
+        lines = None
+        if world <= 8 and len({u for u, _ in info}) == world:
+            lines = [ptr if r == rank else self.ctx.shard_lines_open(info[r][1]) for r in range(world)]
+        cache[key] = lines
+        self._xready = cache
+        self._xepoch = getattr(self, "_xepoch", 0)
+        return lines is not None
+
+    def device_refine(self, axis0, cfg, group=None):
+        """refine_loop of all shards as one cooperative loop per rank, the per-pass partials exchanged
+        through peer memory; every rank returns the same (axis, total count, this shard's count)."""
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        self._xepoch += 1  # the same sequence of solves on every rank
+        ax, count, local, _, refits = self.ctx.shard_refine(axis0, cfg, world, rank, self._xready[id(group)],
+                                                           self._xepoch)
+        return ax, count, local, refits
+
 
 def all_gather_rows(shard: torch.Tensor, n_total: int, group=None) -> torch.Tensor:
     """Rank-ordered concatenation of every rank's shard (shapes are known from shard_bounds)."""
@@ -183,6 +214,20 @@ def sharded_estimate_single(shard: torch.Tensor, n_total: int, cfg, backend, gro
         return rows[:, 0].astype(np.int64), bool(rows[:, 1].any()), s6
 
     slot = 0
+    if hasattr(backend, "device_refine") and backend.peer_refine_ready(group):
+        # device-resident refine_loop: one cooperative loop per rank, partials through peer memory
+        axis, total_count, local, passes = backend.device_refine(axis, cfg, group)
+        counts = _gather_f64([float(local)], dev, group)[:, 0].astype(np.int64)
+        assert int(counts.sum()) == total_count
+        if cfg.refine and total_count < 3.0 * (cfg.epsilon * n_kept):  # rescue (estimator.cpp:352-368)
+            if stats is not None:
+                stats["mode"] = "replicated:rescue"
+            return replicated_finish(shard, n_total, grid, cfg, backend, group)
+        if stats is not None:
+            stats["mode"] = "sharded:device"
+            stats["passes"] = passes
+        return _sharded_build(shard, n_total, cfg, backend, group, axis, counts, 0, lo, world, rank, dev, stats,
+                              votes)
     counts, _, s6 = classify(axis, slot, False)
     passes = 0
     if cfg.refine:
@@ -207,6 +252,16 @@ def sharded_estimate_single(shard: torch.Tensor, n_total: int, cfg, backend, gro
             return replicated_finish(shard, n_total, grid, cfg, backend, group)
     if stats is not None:
         stats["passes"] = passes
+    return _sharded_build(shard, n_total, cfg, backend, group, axis, counts, slot, lo, world, rank, dev, stats,
+                          votes)
+
+
+def _sharded_build(shard, n_total, cfg, backend, group, axis, counts, slot, lo, world, rank, dev, stats, votes):
+    """build_estimate (estimator.cpp:73-92) over the shards: the rank-ordered concatenation of the
+    shard inlier lists is the reference's ascending list; the angle histograms are summed and
+    peak_angle's window sums around the summed peak are summed in rank order."""
+    from paper_2502_06337_b200 import RotationEstimate
+
     local = backend.inliers(slot, lo, int(counts[rank]))
     inliers = _gather_i32_varlen(local, counts, dev, group)
     bins, contrib = backend.angle_hist(axis, cfg)

@@ -87,7 +87,9 @@ def test_sharded_protocol_world1_nccl(ctx):
         d = torch.from_numpy(corrs).cuda()
         stats = {}
         e = rvd.sharded_estimate_single(d, corrs.shape[0], rv.EstimatorConfig(), rvd.DeviceBackend(ctx), stats=stats)
-        assert stats["mode"] == "sharded"
+        # one GPU per rank: the refine runs device-resident (rv_shard_refine over the ranks' line
+        # buffers exported / mapped by CUDA IPC; one rank here, so its own buffer only)
+        assert stats["mode"] == "sharded:device" and stats["passes"] >= 1
         check_golden(e, g)
     finally:
         dist.destroy_process_group()
@@ -115,6 +117,8 @@ def test_sharded_protocol_two_ranks_one_gpu(ctx):
     mp.spawn(gloo_worker, args=(2, free_port(), n, out), nprocs=2, join=True)
     for r in range(2):
         inl, rot, votes, mode, passes = out[r]
+        # two ranks on ONE GPU: their cooperative kernels must not wait on each other, so the
+        # passes are host-stepped (peer_refine_ready sees the same GPU twice)
         assert mode == "sharded" and passes >= 1
         assert np.array_equal(inl, ref.inliers) and votes == ref.axis_votes
         assert orc.rotation_error_deg(rot, ref.rotation) <= 1e-3
