@@ -9,9 +9,12 @@ SURVEY.md section 8(e): rank r owns the contiguous correspondence range [N*r/P, 
   peak     every rank finds the same peak and start axis on the summed grid
            (estimate_from_peak, estimator.cpp:94-97)
   refine   refine_loop (estimator.cpp:51-69), sharded: each pass every rank classifies its own
-           constraints and reports 8 doubles (inlier count, "set changed", the 6 scatter sums of
-           refine_axis); the partials are all-gathered and summed in rank order, and every rank
-           runs the same 3x3 solve -- identical axis and decision everywhere
+           constraints and contributes 8 doubles (inlier count, "set changed", the 6 scatter sums
+           of refine_axis), summed in rank order; every rank runs the same 3x3 solve -- identical
+           axis and decision everywhere. With one GPU per rank this is ONE device-resident loop
+           per rank (rv_shard_refine): the partials travel through peer memory (line buffers
+           shared by CUDA IPC), no host round trip per pass; otherwise (ranks sharing a GPU, the
+           CPU backend) the passes are host-stepped with an all-gather each
   estimate build_estimate (estimator.cpp:73-92): the rank-ordered concatenation of the shard
            inlier lists is the reference's ascending list; the angle histograms are summed and
            peak_angle's window sums around the summed peak are gathered and summed in rank order
