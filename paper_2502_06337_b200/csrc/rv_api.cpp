@@ -1945,11 +1945,15 @@ void materialize_candidate(rv_context* c, const uint32_t* grid, const rv_config&
                                               : 0u;
   }
   est->inliers.resize((size_t)est->dev_count);
-  if (est->dev_count > 0)
-    ck(cudaMemcpyAsync(est->inliers.data(), r.d_idx, sizeof(int32_t) * (size_t)est->dev_count,
-                       cudaMemcpyDeviceToHost, c->st),
+  if (est->dev_count > 0) {  // through the pinned inlier buffer: a pageable D2H stages at a fraction of the rate
+    int32_t* h = inlier_host_buffer(c, (size_t)est->dev_count);
+    ck(cudaMemcpyAsync(h, r.d_idx, sizeof(int32_t) * (size_t)est->dev_count, cudaMemcpyDeviceToHost, c->st),
        "inliers D2H");
-  sync(c);
+    sync(c);
+    std::memcpy(est->inliers.data(), h, sizeof(int32_t) * (size_t)est->dev_count);
+  } else {
+    sync(c);
+  }
   est->dev_count = -1;
 }
 
@@ -2009,6 +2013,21 @@ bool near_identity_dev(rv_context* c, const double* d_corrs, const ConstraintSet
 // acceptance rules (consensus floor, model_support coherence, inlier-overlap dedupe). Unlike the
 // sequential estimate_multi it does not strip inliers and re-vote, so K models cost one vote.
 // Models are returned in peak order (descending axis_votes).
+// The dedupe of estimate_multi (estimator.cpp:468-478): |inliers ∩ accepted model's inliers| as the
+// popcount of the AND of two input-index bitsets (word-parallel; the per-index lookup loop cost
+// ~50 us per accepted model at 1e5 inliers).
+std::vector<uint64_t> inlier_bits(const std::vector<int32_t>& inl, int64_t n) {
+  std::vector<uint64_t> bits((size_t)(n + 63) / 64, 0);
+  for (const int32_t i : inl) bits[(size_t)i >> 6] |= 1ull << (i & 63);
+  return bits;
+}
+int64_t bits_common(const std::vector<uint64_t>& a, const std::vector<uint64_t>& b) {
+  int64_t s = 0;
+  const size_t m = std::min(a.size(), b.size());
+  for (size_t w = 0; w < m; ++w) s += __builtin_popcountll(a[w] & b[w]);
+  return s;
+}
+
 std::vector<Estimate> estimate_multi_onepass_dev(rv_context* c, const double* d_corrs, int64_t n,
                                                  const rv_config& cfg) {
   if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
@@ -2046,17 +2065,13 @@ std::vector<Estimate> estimate_multi_onepass_dev(rv_context* c, const double* d_
         sup.coherent < std::max<int64_t>(8, (int64_t)est.inliers.size() / 5))
       continue;
     bool duplicate = false;
-    for (const auto& bits : out_bits) {  // |intersection| via the accepted model's bitset
-      int64_t common = 0;
-      for (const int32_t i : est.inliers) common += (bits[(size_t)i >> 6] >> (i & 63)) & 1u;
-      if ((double)common > cfg.dedupe_overlap * (double)est.inliers.size()) {
+    std::vector<uint64_t> bits = inlier_bits(est.inliers, n);
+    for (const auto& prev : out_bits)  // |intersection| with each accepted model's inlier set
+      if ((double)bits_common(bits, prev) > cfg.dedupe_overlap * (double)est.inliers.size()) {
         duplicate = true;
         break;
       }
-    }
     if (!duplicate) {
-      std::vector<uint64_t> bits((size_t)(n + 63) / 64, 0);
-      for (const int32_t i : est.inliers) bits[(size_t)i >> 6] |= 1ull << (i & 63);
       out_bits.push_back(std::move(bits));
       out.push_back(std::move(est));
     }
@@ -2146,20 +2161,14 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
       identity_model = true;
     }
     bool duplicate = false;
-    for (const auto& bits : out_bits) {  // |intersection| via the accepted models' inlier bitsets
-      int64_t common = 0;
-      for (const int32_t i : est.inliers) common += (bits[(size_t)i >> 6] >> (i & 63)) & 1u;
-      if ((double)common > cfg.dedupe_overlap * (double)est.inliers.size()) {
+    std::vector<uint64_t> bits = inlier_bits(est.inliers, n);
+    for (const auto& prev : out_bits)  // |intersection| with each accepted model's inlier set
+      if ((double)bits_common(bits, prev) > cfg.dedupe_overlap * (double)est.inliers.size()) {
         duplicate = true;
         break;
       }
-    }
     if (duplicate) break;
-    {
-      std::vector<uint64_t> bits((size_t)(n + 63) / 64, 0);
-      for (const int32_t i : est.inliers) bits[(size_t)i >> 6] |= 1ull << (i & 63);
-      out_bits.push_back(std::move(bits));
-    }
+    out_bits.push_back(std::move(bits));
     if (identity_model) {
       launch_strip_identity_k(d_corrs, pre.cs.kept, pre.cs.n, cfg.normalize_inputs, removed, c->st);
       count_launch(c);
