@@ -270,12 +270,14 @@ struct rv_context {
   void* pinned = nullptr;
   std::vector<std::vector<int32_t>> results;
   std::vector<int32_t> spare;       // recycled inlier vector (no page faults on the hot path)
+  std::vector<std::vector<int32_t>> spares;  // recycled inlier vectors of the multi-model calls
   bool allow_view = false;          // set by the single-solve entry points (see Estimate::view)
   const int32_t* result0_view = nullptr;  // results[0] lives in the mapped buffer (view)
   int64_t result0_view_n = 0;
   std::vector<rv_context*> pool;    // batch workers (own stream + buffers each), created lazily
   int32_t* inl_host = nullptr;      // mapped pinned buffer: the compaction writes the inlier list here
   size_t inl_cap = 0;
+  std::vector<std::vector<uint64_t>> dedupe_bits;  // estimate_multi's inlier bitsets (InlierSets)
 
   // "last block done" counters of the single-pass reductions: must start at zero; every kernel
   // that uses one resets it before exiting.
@@ -291,6 +293,7 @@ struct rv_context {
 namespace {
 
 double* pin_d(rv_context* c) { return static_cast<double*>(c->pinned); }
+constexpr size_t kPinnedScratch = 4096;  // c->pinned
 
 void sync(rv_context* c) { ck(cudaStreamSynchronize(c->st), "cudaStreamSynchronize"); }
 
@@ -301,6 +304,17 @@ cudaEvent_t take_event(rv_context* c) {
     c->event_pool.push_back(e);
   }
   return c->event_pool[c->event_used++];
+}
+
+// Read-back of a few small records (then synchronise): through the pinned scratch when they fit
+// -- a pageable D2H stages through the driver, ~10-20 us more per read-back in the multi-model loop
+template <class T>
+void read_small(rv_context* c, T* dst, const T* src, size_t count, const char* what) {
+  const size_t bytes = sizeof(T) * count;
+  void* via = bytes <= kPinnedScratch ? c->pinned : static_cast<void*>(dst);
+  ck(cudaMemcpyAsync(via, src, bytes, cudaMemcpyDeviceToHost, c->st), what);
+  sync(c);
+  if (via != dst) std::memcpy(dst, via, bytes);
 }
 
 struct StageScope {
@@ -1051,8 +1065,7 @@ std::vector<std::array<double, 3>> rescue_axes_dev(rv_context* c, const uint32_t
   CoopState* st = c->coop_state.get<CoopState>(starts.size());
   coop_refine_multi_launch(c, cs, starts, e0s, 1, cfg, st, sizeof(CoopState), nullptr, nullptr, 0, nullptr, 0);
   std::vector<CoopState> h(starts.size());
-  ck(cudaMemcpyAsync(h.data(), st, sizeof(CoopState) * starts.size(), cudaMemcpyDeviceToHost, c->st), "anneal D2H");
-  sync(c);
+  read_small(c, h.data(), st, starts.size(), "anneal D2H");
   for (const CoopState& x : h) out.push_back({x.axis[0], x.axis[1], x.axis[2]});
   return out;
 }
@@ -1900,8 +1913,7 @@ std::vector<CandResult> evaluate_candidates(rv_context* c, const std::vector<std
     count_launch(c, 2);
   }
   std::vector<Summary> hs(K);
-  ck(cudaMemcpyAsync(hs.data(), sums, sizeof(Summary) * K, cudaMemcpyDeviceToHost, c->st), "candidates D2H");
-  sync(c);
+  read_small(c, hs.data(), sums, K, "candidates D2H");
   int32_t* bc = c->sup_counts.get<int32_t>((size_t)classify_blocks(cs.n) * 2);
   for (size_t k = 0; k < K; ++k) {
     const Summary& sm = hs[k];
@@ -1926,8 +1938,7 @@ std::vector<CandResult> evaluate_candidates(rv_context* c, const std::vector<std
     count_launch(c);
   }
   std::vector<int32_t> hsup(2 * K);
-  ck(cudaMemcpyAsync(hsup.data(), sup, sizeof(int32_t) * 2 * K, cudaMemcpyDeviceToHost, c->st), "supports D2H");
-  sync(c);
+  read_small(c, hsup.data(), sup, 2 * K, "supports D2H");
   for (size_t k = 0; k < K; ++k) {
     out[k].coherent = hsup[2 * k];
     out[k].band = hsup[2 * k + 1];
@@ -1944,14 +1955,19 @@ void materialize_candidate(rv_context* c, const uint32_t* grid, const rv_config&
                                                           coord_to_cell(B, cfg.grid, cfg.extent))
                                               : 0u;
   }
-  est->inliers.resize((size_t)est->dev_count);
+  est->inliers.clear();
+  if (!c->spares.empty()) {  // a previous call's inlier vector: no page faults
+    est->inliers = std::move(c->spares.back());
+    c->spares.pop_back();
+  }
   if (est->dev_count > 0) {  // through the pinned inlier buffer: a pageable D2H stages at a fraction of the rate
     int32_t* h = inlier_host_buffer(c, (size_t)est->dev_count);
     ck(cudaMemcpyAsync(h, r.d_idx, sizeof(int32_t) * (size_t)est->dev_count, cudaMemcpyDeviceToHost, c->st),
        "inliers D2H");
     sync(c);
-    std::memcpy(est->inliers.data(), h, sizeof(int32_t) * (size_t)est->dev_count);
+    est->inliers.assign(h, h + est->dev_count);
   } else {
+    est->inliers.clear();
     sync(c);
   }
   est->dev_count = -1;
@@ -2016,17 +2032,46 @@ bool near_identity_dev(rv_context* c, const double* d_corrs, const ConstraintSet
 // The dedupe of estimate_multi (estimator.cpp:468-478): |inliers ∩ accepted model's inliers| as the
 // popcount of the AND of two input-index bitsets (word-parallel; the per-index lookup loop cost
 // ~50 us per accepted model at 1e5 inliers).
-std::vector<uint64_t> inlier_bits(const std::vector<int32_t>& inl, int64_t n) {
-  std::vector<uint64_t> bits((size_t)(n + 63) / 64, 0);
-  for (const int32_t i : inl) bits[(size_t)i >> 6] |= 1ull << (i & 63);
-  return bits;
-}
-int64_t bits_common(const std::vector<uint64_t>& a, const std::vector<uint64_t>& b) {
+// Inlier bitsets of the accepted models for the dedupe test (estimator.cpp:452-458: |common
+// inliers| > dedupe_overlap * |inliers| rejects a model), in context-owned storage reused across
+// calls -- fresh n-bit vectors per model page-faulted on every call -- and intersected a word at a
+// time with the hardware popcount.
+#if defined(__x86_64__)
+__attribute__((target("popcnt"))) int64_t common_bits_hw(const uint64_t* a, const uint64_t* b, size_t m) {
   int64_t s = 0;
-  const size_t m = std::min(a.size(), b.size());
   for (size_t w = 0; w < m; ++w) s += __builtin_popcountll(a[w] & b[w]);
   return s;
 }
+#endif
+int64_t common_bits(const uint64_t* a, const uint64_t* b, size_t m) {
+#if defined(__x86_64__)
+  static const bool hw = __builtin_cpu_supports("popcnt");
+  if (hw) return common_bits_hw(a, b, m);
+#endif
+  int64_t s = 0;
+  for (size_t w = 0; w < m; ++w) s += __builtin_popcountll(a[w] & b[w]);
+  return s;
+}
+class InlierSets {
+ public:
+  InlierSets(rv_context* c, int64_t n) : pool_(c->dedupe_bits), words_((size_t)(n + 63) / 64) {}
+  // true when the model with these inliers repeats an accepted one; otherwise it is accepted
+  bool duplicate_else_accept(const std::vector<int32_t>& inl, double overlap) {
+    if (pool_.size() <= used_) pool_.resize(used_ + 1);
+    std::vector<uint64_t>& bits = pool_[used_];
+    bits.assign(words_, 0);  // keeps its capacity: no page faults after the first call
+    for (const int32_t i : inl) bits[(size_t)i >> 6] |= 1ull << (i & 63);
+    for (size_t k = 0; k < used_; ++k)
+      if ((double)common_bits(bits.data(), pool_[k].data(), words_) > overlap * (double)inl.size()) return true;
+    ++used_;
+    return false;
+  }
+
+ private:
+  std::vector<std::vector<uint64_t>>& pool_;
+  size_t words_;
+  size_t used_ = 0;
+};
 
 std::vector<Estimate> estimate_multi_onepass_dev(rv_context* c, const double* d_corrs, int64_t n,
                                                  const rv_config& cfg) {
@@ -2046,7 +2091,7 @@ std::vector<Estimate> estimate_multi_onepass_dev(rv_context* c, const double* d_
     return {};
   }
   std::vector<Estimate> out;
-  std::vector<std::vector<uint64_t>> out_bits;  // inlier bitsets of the accepted models (dedupe)
+  InlierSets accepted(c, n);
   for (const Peak& pk : peaks) {
     double A, B, b[3], axis[3];
     interpolate_peak_dev(c, grid, cfg.grid, cfg.extent, pk, &A, &B);
@@ -2064,17 +2109,7 @@ std::vector<Estimate> estimate_multi_onepass_dev(rv_context* c, const double* d_
     if ((int64_t)est.inliers.size() < consensus_floor ||
         sup.coherent < std::max<int64_t>(8, (int64_t)est.inliers.size() / 5))
       continue;
-    bool duplicate = false;
-    std::vector<uint64_t> bits = inlier_bits(est.inliers, n);
-    for (const auto& prev : out_bits)  // |intersection| with each accepted model's inlier set
-      if ((double)bits_common(bits, prev) > cfg.dedupe_overlap * (double)est.inliers.size()) {
-        duplicate = true;
-        break;
-      }
-    if (!duplicate) {
-      out_bits.push_back(std::move(bits));
-      out.push_back(std::move(est));
-    }
+    if (!accepted.duplicate_else_accept(est.inliers, cfg.dedupe_overlap)) out.push_back(std::move(est));
   }
   return out;
 }
@@ -2089,7 +2124,7 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
   uint8_t* removed = c->removed.get<uint8_t>(pre.cs.n);
   ck(cudaMemsetAsync(removed, 0, pre.cs.n, c->st), "memset removed");
   std::vector<Estimate> out;
-  std::vector<std::vector<uint64_t>> out_bits;  // inlier bitsets of the accepted models (dedupe)
+  InlierSets accepted(c, n);
   while ((int)out.size() < cfg.max_models) {
     // residual (estimator.cpp:392-398)
     ConstraintSet sub;
@@ -2160,15 +2195,7 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
       est = std::move(ident);
       identity_model = true;
     }
-    bool duplicate = false;
-    std::vector<uint64_t> bits = inlier_bits(est.inliers, n);
-    for (const auto& prev : out_bits)  // |intersection| with each accepted model's inlier set
-      if ((double)bits_common(bits, prev) > cfg.dedupe_overlap * (double)est.inliers.size()) {
-        duplicate = true;
-        break;
-      }
-    if (duplicate) break;
-    out_bits.push_back(std::move(bits));
+    if (accepted.duplicate_else_accept(est.inliers, cfg.dedupe_overlap)) break;
     if (identity_model) {
       launch_strip_identity_k(d_corrs, pre.cs.kept, pre.cs.n, cfg.normalize_inputs, removed, c->st);
       count_launch(c);
@@ -2333,7 +2360,7 @@ rv_status rv_context_create(int32_t device, rv_context** out) {
   if (!c) return RV_ERR_OUT_OF_MEMORY;
   c->device = device;
   if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaMallocHost(&c->pinned, 4096) != cudaSuccess) {
+      cudaMallocHost(&c->pinned, kPinnedScratch) != cudaSuccess) {
     cudaGetLastError();
     delete c;
     return RV_ERR_CUDA;
@@ -2394,6 +2421,13 @@ static void clear_results(rv_context* c) {
   c->result0_view_n = 0;
 }
 
+// multi-model calls: every result vector goes back to the spare pool (at most 16 kept)
+static void recycle_all_results(rv_context* c) {
+  for (auto& v : c->results)
+    if (c->spares.size() < 16 && v.capacity() > 0) c->spares.push_back(std::move(v));
+  clear_results(c);
+}
+
 static void recycle_results(rv_context* c) {
   if (!c->results.empty() && c->results[0].capacity() > c->spare.capacity()) c->spare = std::move(c->results[0]);
   c->results.clear();
@@ -2448,7 +2482,7 @@ static rv_status multi_impl(rv_context* c, const double* d, int64_t n, const rv_
                             int32_t capacity, int32_t* n_models, bool host, bool onepass = false) {
   return guarded(c, [&] {
     cudaSetDevice(c->device);
-    clear_results(c);
+    recycle_all_results(c);
     *n_models = 0;
     if (n <= 0) fail(RV_ERR_EMPTY_INPUT, "no correspondences");
     const double* dd = host ? upload_corrs(c, d, n) : d;
