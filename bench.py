@@ -347,6 +347,15 @@ def run_device(args):
         roof["issue"] = {"bound": "instruction issue", "achieved": ach / 1e9, "peak": pk / 1e9,
                          "unit": "G warp-inst/s", "frac": ach / pk,
                          "inst_per_launch": prof["inst_executed"], "source": "ncu inst_executed x live launch time"}
+        if prof.get("lsu_wavefronts"):
+            # ... and co-bound by the L1 data pipe: one wavefront (LDS/ATOMS/LDG/LDL phase) per clock
+            # per SM; its table reads and bank-conflicted shared atomics per launch (ncu) / live time
+            ach = prof["lsu_wavefronts"] / vote_avg_s
+            pk = 1.0 * sms * clocks["sm_mhz"] * 1e6
+            roof["lsu"] = {"bound": "L1 data-pipe wavefronts", "achieved": ach / 1e9, "peak": pk / 1e9,
+                           "unit": "G wavefronts/s", "frac": ach / pk,
+                           "wavefronts_per_launch": prof["lsu_wavefronts"],
+                           "source": "ncu l1tex__data_pipe_lsu_wavefronts.sum x live launch time"}
     pre_ms = statistics.mean(s["preprocess_ms"] for s in stage)
     hbm = measured_peaks().get("hbm_gbs")
     # in-order preprocess (single solves): 48 B read + 24 B of z written per correspondence

@@ -6,11 +6,15 @@ if the shared library is missing, loading fails loudly.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from . import errors
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "librotavote_b200.so"
+# dev A/B of kernel variants only (tools/ab_vote.py): another in-tree build of the same library
+if os.environ.get("RV_LIB_PATH"):
+    LIB_PATH = Path(os.environ["RV_LIB_PATH"]).resolve()
 
 c_double_p = C.POINTER(C.c_double)
 c_int32_p = C.POINTER(C.c_int32)

@@ -13,6 +13,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
+if os.environ.get("RV_LIB_OUT"):  # dev A/B builds of kernel variants (tools/ab_vote.py)
+    LIB_DIR = Path(os.environ["RV_LIB_OUT"]).resolve()
 LIB = LIB_DIR / "librotavote_b200.so"
 INCLUDE = PKG.parent / "include"
 SOURCES = ["rv_prep.cu", "rv_vote.cu", "rv_peaks.cu", "rv_refine.cu", "rv_coop.cu", "rv_io.cu", "rv_api.cpp",
@@ -41,7 +43,7 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
-    LIB_DIR.mkdir(exist_ok=True)
+    LIB_DIR.mkdir(parents=True, exist_ok=True)
     obj_dir = LIB_DIR / "obj"
     obj_dir.mkdir(exist_ok=True)
     common = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",

@@ -429,6 +429,7 @@ VotePlan make_plan(rv_context* c, int G, double E, int J) {
     p.c_max = G - 1;
     p.W = G + 4;  // row stride: 16-byte rows for the bulk copies, rows offset by 4 banks
   }
+  p.Wf = (float)p.W;
   const size_t table_bytes = (size_t)(2 * p.halfJ + 64) * sizeof(float2);  // J samples (packed) + 64 slack
   const size_t fbq_bytes = (size_t)(kVoteThreads / 32) * kFbqCap * 4 + 32 * 4;  // + 32 lane sink words
   const size_t reserve = table_bytes + fbq_bytes + 1024;

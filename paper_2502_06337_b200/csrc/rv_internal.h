@@ -40,6 +40,7 @@ struct VotePlan {
   int r_min = 0, r_max = 0;  // stored rows [r_min, r_max]
   int c_min = 0, c_max = 0;  // stored cols
   int W = 0;                 // c_max - c_min + 1
+  float Wf = 0;              // (float)W (RV_FP_CELL vote variant)
   int n_bands = 0;
   int H_max = 0;             // rows of the tallest band
   int band_r0[kMaxBands + 1];   // band b stores rows [band_r0[b], band_r0[b+1])

@@ -46,6 +46,9 @@ constexpr float kRcMin = 1e-3f;     // |c| amplitude below which a circle is tre
 #ifndef RV_UNIFORM_STEP
 #define RV_UNIFORM_STEP 1
 #endif
+#ifndef RV_TAIL_GRAB
+#define RV_TAIL_GRAB 0
+#endif
 #ifndef RV_RED_GROUPS
 #define RV_RED_GROUPS 2
 #endif
@@ -69,6 +72,26 @@ __device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
 __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
   f32x2 r;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f32x2 fma2_rz(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rz.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 add2_rm(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 add2_rz(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("add.rz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
 
@@ -109,11 +132,33 @@ struct F32Geom {
   uint32_t W;
   uint32_t lin_off;  // non-clamp: (magic_hi + r0) * W + magic_hi + c_min
   int magic_hi, G, r0, c_min;
+  float Wf;         // RV_FP_CELL: (float)W
+  uint32_t fp_off;  // RV_FP_CELL: bits(2^23) + magic + r0 * W + c_min
 };
+// RV_FP_CELL (A/B knob, off: measured slower): the fixed-S no-clamp variants compute the
+// tile-relative cell in f32 instead of shifting and multiplying the fixed-point bits (8 instead of
+// 10 issue slots per sample pair, but 4 more FMA-pipe ops and a longer dependent chain):
+//   F = (ty + (1.5*2^23 - magic)) rounded down - 1.5*2^23 = floor(t_y), exact
+//   L = F*W + tx rounded toward zero (all terms >= 0, L < 2^23): floor(L) = row*W + floor(t_x) + magic
+//   bits(L + 2^23, toward zero) = bits(2^23) + floor(L)
+#ifndef RV_FP_CELL
+#define RV_FP_CELL 0
+#endif
+template <bool kClamp, int kS>
+struct FpCellSel : std::integral_constant<bool, RV_FP_CELL && !kClamp && kS != 0> {};
+constexpr float kBig23 = 8388608.f;   // 2^23
+constexpr float kBig15 = 12582912.f;  // 1.5 * 2^23
+template <int kS>
+__device__ __forceinline__ constexpr float fp_ky() { return kBig15 - 1.5f * (float)(1 << (23 - kS)); }
 template <bool kClamp, int kS>
 __device__ __forceinline__ uint32_t cell_of_bits(const F32Geom& g, uint32_t bx, uint32_t by, bool* flag) {
   const int S = kS ? kS : g.S;
   *flag = ((bx & g.fmask) == 0u) | ((by & g.fmask) == 0u);
+  if (FpCellSel<kClamp, kS>::value) {
+    const float F = __fadd_rn(__fadd_rd(__uint_as_float(by), fp_ky<kS>()), -kBig15);
+    const float L = __fmaf_rz(F, g.Wf, __uint_as_float(bx));
+    return __float_as_uint(__fadd_rz(L, kBig23)) - g.fp_off;
+  }
   // the column is always inside [c_min, c_min+W) (|X| <= 1 < extent, or clamped), so one
   // unsigned range test on the linear index is the band-ownership test
   if (kClamp) {
@@ -572,8 +617,21 @@ __device__ __forceinline__ void f32_cell2(const F32Geom& g, float4 ba, float2 bb
   const f32x2 R = pk2(rcp_approx(__uint_as_float(cb[0])), rcp_approx(__uint_as_float(cb[1])));
   const f32x2 CM = pk2(g.CMf, g.CMf);
   uint32_t bx[2], by[2];
-  upk2(fma2(X, R, CM), bx[0], bx[1]);
-  upk2(fma2(Y, R, CM), by[0], by[1]);
+  const f32x2 TX = fma2(X, R, CM), TY = fma2(Y, R, CM);
+  upk2(TX, bx[0], bx[1]);
+  upk2(TY, by[0], by[1]);
+  if (FpCellSel<kClamp, kS>::value) {  // cell_of_bits' f32 cell, lane-parallel
+    const f32x2 F = add2(add2_rm(TY, pk2(fp_ky<kS>(), fp_ky<kS>())), pk2(-kBig15, -kBig15));
+    const f32x2 L = fma2_rz(F, pk2(g.Wf, g.Wf), TX);
+    uint32_t lb[2];
+    upk2(add2_rz(L, pk2(kBig23, kBig23)), lb[0], lb[1]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      flag[h] = ((bx[h] & g.fmask) == 0u) | ((by[h] & g.fmask) == 0u);
+      rel[h] = lb[h] - g.fp_off;
+    }
+    return;
+  }
 #pragma unroll
   for (int h = 0; h < 2; ++h) rel[h] = cell_of_bits<kClamp, kS>(g, bx[h], by[h], &flag[h]);
 }
@@ -707,9 +765,15 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
   uint32_t* fbq_all = reinterpret_cast<uint32_t*>(tab + M + 32);
   __shared__ int s_band, s_slot;
   __shared__ ColdCtx s_cold;
+  __shared__ unsigned int s_fb;  // flagged samples of this CTA (stats)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t fbq_s = (uint32_t)__cvta_generic_to_shared(fbq_all + warp * kFbqCap);  // this warp's queue
+  // this warp's exact-path queue (shared window); recomputed in the cold path from the warp index
+  // so that it holds no register across the hot loop
+  const uint32_t fbq_s0 = (uint32_t)__cvta_generic_to_shared(fbq_all);
+  auto fbq_addr = [&]() -> uint32_t {
+    return fbq_s0 + (uint32_t)(threadIdx.x >> 5) * (uint32_t)(kFbqCap * 4);
+  };
   for (int q = tid; q < M + 32; q += blockDim.x) {
     int j0 = 2 * q, j1 = 2 * q + 1;
     j0 = j0 >= J ? j0 - J : j0;
@@ -734,6 +798,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
       }
     }
     s_band = band;
+    s_fb = 0;
     set_cold_band(s_cold, p, band);
     s_cold.zx = b.zx;
     s_cold.zy = b.zy;
@@ -754,12 +819,10 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
   for (size_t k = tid; k < p.tile_words; k += blockDim.x) tile[k] = 0u;
   __syncthreads();
   vtrace(1, s_band);
-  unsigned int my_fb = 0;
-  unsigned lt_mask = (1u << lane) - 1u;
   // per-lane table address (shared window): lane l's float4 of a step at even sample a is
   // tab_s + 8 a (tab_s = table + 16 l)
   uint32_t tab_s = (uint32_t)__cvta_generic_to_shared(tab) + 16u * (uint32_t)lane;
-  asm volatile("" : "+r"(lt_mask), "+r"(tab_s), "+r"(fbq_s));
+  asm volatile("" : "+r"(tab_s));
   // opaque to the optimizer: otherwise the shared-window base is rematerialised every step
   uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(tile);
   // deposits outside this band's rows go to tile rows >= hb (never flushed) or, beyond the tile,
@@ -793,6 +856,8 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     geo.G = G;
     geo.r0 = r0;
     geo.c_min = p.c_min;
+    geo.Wf = p.Wf;
+    geo.fp_off = 0x4B000000u + (3u << (22 - (kS ? kS : 13))) + (uint32_t)r0 * (uint32_t)W + (uint32_t)p.c_min;
     const unsigned long long* ebase = b.entries + (int64_t)band * b.entry_cap;
     const int n_ent = __reduce_max_sync(0xFFFFFFFFu, b.entry_count[band]);
     int* counter = &b.counters[1 + band];
@@ -803,11 +868,25 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     // Entries are fetched in per-warp grabs of up to 32 (lane k holds entry k); flagged samples
     // are queued per warp as (constraint, sample) and drained in batches of up to 32.
     uint32_t my_ci = 0, my_enc = 0;
-    int ne = 0, qn = 0;
+    int ne = 0, qn = 0, g0 = 0;
     float4 ba = make_float4(0.f, 0.f, 0.f, 0.f);
     float2 bb = make_float2(0.f, 0.f);
     // one step: samples a + 2 lane + {0, 1} (a = the step's even first sample, recovered from the
     // table address tp); masked steps drop samples outside [mstart, mstart + mlen)
+    // The exact path is a real call; reloading the grab and the entry's basis after it (rare)
+    // keeps them out of the call's save set, so the hot loop holds them in registers (no
+    // per-entry spill reloads through L1).
+    auto after_drain = [&](uint32_t cik) {
+      my_ci = 0;
+      my_enc = 0;
+      if (lane < ne) {
+        const unsigned long long e = __ldg(ebase + g0 + lane);
+        my_ci = (uint32_t)e;
+        my_enc = (uint32_t)(e >> 32);
+      }
+      ba = __ldg(b.basis_a + cik);
+      bb = __ldg(b.basis_b + cik);
+    };
     auto step = [&](uint32_t tpa, bool masked, uint32_t cik, int mstart, int mlen) {
       float4 t4;
       asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(t4.x), "=f"(t4.y), "=f"(t4.z), "=f"(t4.w) : "r"(tpa));
@@ -831,10 +910,14 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
         // before it would pass 32 entries (one exact-path batch = one sample per lane). Both
         // samples of the step are compacted at once (one capacity check).
         const uint32_t j = (uint32_t)((tpa - tab_s) >> 3) + 2u * lane;
+        unsigned lt_mask;
+        asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt_mask));
+        const uint32_t fbq_s = fbq_addr();
         const unsigned fm0 = __ballot_sync(0xFFFFFFFFu, flag[0]), fm1 = __ballot_sync(0xFFFFFFFFu, flag[1]);
         const int c0 = __popc(fm0), c = c0 + __popc(fm1);
         if (qn + c > 32) {
           fallback_samples<kClamp, kS>(&s_cold, geo, fbq_s, qn, tab, tile);
+          after_drain(cik);
           qn = 0;
         }
         if (c <= 32) {
@@ -845,22 +928,32 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
           if (flag[0]) sts_u2(fbq_s + 8u * (uint32_t)__popc(fm0 & lt_mask), cik, j);
           __syncwarp();
           fallback_samples<kClamp, kS>(&s_cold, geo, fbq_s, c0, tab, tile);
+          after_drain(cik);
           if (flag[1]) sts_u2(fbq_s + 8u * (uint32_t)__popc(fm1 & lt_mask), cik, j + 1u);
           qn = c - c0;
         }
-        my_fb += c;
+        if (lane == 0) red_shared((uint32_t)__cvta_generic_to_shared(&s_fb), (uint32_t)c);
         __syncwarp();
       }
     };
     // grab loop / entry loop / step loop
+#if RV_TAIL_GRAB
+    int gsz = grab;  // shrinks near the end of the band (from the last grab's position): a finer
+                     // tail, so the CTA's warps reach the band-end barrier closer together
+#else
+    const int gsz = grab;
+#endif
     for (;;) {
-      int g0 = 0;
-      if (lane == 0) g0 = atomicAdd(counter, grab);
+      g0 = 0;
+      if (lane == 0) g0 = atomicAdd(counter, gsz);
       // REDUX broadcasts (uniform-register results): everything derived from them is provably
       // warp-uniform, so the loops carry no divergence checks around their votes
       g0 = __reduce_max_sync(0xFFFFFFFFu, g0);
       if (g0 >= n_ent) break;
-      ne = min(grab, n_ent - g0);
+      ne = min(gsz, n_ent - g0);
+#if RV_TAIL_GRAB
+      gsz = max(1, min(grab, (n_ent - g0 - ne) / max(per, 1)));
+#endif
       my_ci = 0;
       my_enc = 0;
       if (lane < ne) {
@@ -907,7 +1000,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
 #endif
       }
     }
-    if (qn > 0) fallback_samples<kClamp, kS>(&s_cold, geo, fbq_s, qn, tab, tile);  // before the flush
+    if (qn > 0) fallback_samples<kClamp, kS>(&s_cold, geo, fbq_addr(), qn, tab, tile);  // before the flush
     // band exhausted for this CTA: flush the tile to a partial slot, steal the next band
     __syncthreads();
     vtrace(2, band);
@@ -990,7 +1083,8 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     }
   }
   if (p.bulk && warp == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // flushes landed
-  if (lane == 0 && my_fb) atomicAdd(&b.stats[1], (unsigned long long)my_fb);
+  __syncthreads();
+  if (tid == 0 && s_fb) atomicAdd(&b.stats[1], (unsigned long long)s_fb);
 }
 
 // Sum the partial tiles of every band into the output grid.
@@ -1175,7 +1269,9 @@ using VoteKernel = void (*)(VotePlan, VoteBuffers, int64_t);
 static VoteKernel vote_kernel_for(const VotePlan& p, int* slot) {
   // S = 13 / 12 (every grid <= 1000 at the reference extents) get a compile-time shift; other S
   // use the run-time variant
-  const int ks = p.frac_shift == 13 ? 2 : (p.frac_shift == 12 ? 1 : 0);
+  // RV_FP_CELL: the fixed-S variants need every f32 cell intermediate below 2^23
+  const bool fp_ok = !RV_FP_CELL || (double)(p.G + 1) * p.W + 3.0 * std::ldexp(1.0, 23 - p.frac_shift) < 8388608.0;
+  const int ks = !fp_ok ? 0 : p.frac_shift == 13 ? 2 : (p.frac_shift == 12 ? 1 : 0);
   const int k = (p.clamp ? 3 : 0) + ks;
   *slot = k;
   switch (k) {

@@ -21,7 +21,9 @@ RAW = ["smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_
        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum",
-       "smsp__inst_executed_op_shared_atom.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"]
+       "smsp__inst_executed_op_shared_atom.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+       "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+       "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum"]
 
 
 def launches(path):
@@ -82,7 +84,14 @@ def kernel_json(path):
             "inst_executed": val("smsp__inst_executed.sum"),
             "issue_active_pct": val("smsp__issue_active.avg.pct_of_peak_sustained_active"),
             "shared_atom_inst": val("smsp__inst_executed_op_shared_atom.sum"),
-            "shared_atom_wavefronts": val("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum")}
+            "shared_atom_wavefronts": val("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum"),
+            # the L1 data pipe (one wavefront per clock per SM): the vote's other co-binding limit
+            # (peak 1 per clock per SM: wavefronts = pct x elapsed SM cycles x SMs)
+            "lsu_wavefronts": val("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed") / 100.0
+            * val("sm__cycles_elapsed.avg") * val("device__attribute_multiprocessor_count"),
+            "lsu_wavefronts_pct": val("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+            "shared_ld_wavefronts": val("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum"),
+            "sm_cycles": val("sm__cycles_elapsed.avg")}
 
 
 def per_kernel(path):
