@@ -46,6 +46,9 @@ constexpr float kRcMin = 1e-3f;     // |c| amplitude below which a circle is tre
 #ifndef RV_UNIFORM_STEP
 #define RV_UNIFORM_STEP 1
 #endif
+#ifndef RV_GRAB_PER
+#define RV_GRAB_PER 4  // target grabs per warp and band below which grabs shrink from 32 entries
+#endif
 #ifndef RV_TAIL_GRAB
 #define RV_TAIL_GRAB 0
 #endif
@@ -863,7 +866,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     int* counter = &b.counters[1 + band];
     // grab size: 32 entries when every warp of the launch still gets several grabs, smaller for
     // small problems (otherwise a handful of warps would walk all entries while the rest idle)
-    const int per = (int)(((long long)gridDim.x * (kVoteThreads / 32) * 4) / p.n_bands);
+    const int per = (int)(((long long)gridDim.x * (kVoteThreads / 32) * RV_GRAB_PER) / p.n_bands);
     const int grab = max(1, min(32, n_ent / max(per, 1)));
     // Entries are fetched in per-warp grabs of up to 32 (lane k holds entry k); flagged samples
     // are queued per warp as (constraint, sample) and drained in batches of up to 32.

@@ -29,14 +29,33 @@ for _ in range(15):
     ctx.estimate_single_device(d.data_ptr(), corrs.shape[0], cfg)
     st = ctx.stage_times()
     vk.append(st["vote_kernel_ms"]); vs.append(st["total_ms"])
-print(json.dumps({"vote_kernel_ms": vk, "total_ms": vs}))
+ctx.enable_timing(False)
+# end to end from pinned host memory (the pipelined chunked path), CUDA events on the current stream
+h = torch.empty((corrs.shape[0], 6), dtype=torch.float64, pin_memory=True)
+h.numpy()[:] = corrs
+for _ in range(3):
+    ctx.estimate_single(h.numpy(), cfg)
+e2e = []
+for _ in range(15):
+    flush.zero_()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    ctx.estimate_single(h.numpy(), cfg)
+    b.record()
+    torch.cuda.synchronize()
+    e2e.append(a.elapsed_time(b))
+print(json.dumps({"vote_kernel_ms": vk, "total_ms": vs, "e2e_ms": e2e}))
 """
 libs = sys.argv[1:]
 rounds = int(os.environ.get("AB_ROUNDS", "3"))
-res = {l: {"vote_kernel_ms": [], "total_ms": []} for l in libs}
+res = {l: {"vote_kernel_ms": [], "total_ms": [], "e2e_ms": []} for l in libs}
 for r in range(rounds):
     for l in libs:
-        env = dict(os.environ, RV_LIB_PATH=str(Path(l) / "librotavote_b200.so"))
+        # "dir" or "dir@VAR=value@VAR2=value2": a variant library plus run-time knobs
+        parts = l.split("@")
+        env = dict(os.environ, RV_LIB_PATH=str(Path(parts[0]) / "librotavote_b200.so"))
+        env.update(kv.split("=", 1) for kv in parts[1:])
         out = subprocess.run([sys.executable, "-c", CHILD % str(ROOT)], env=env, capture_output=True, text=True)
         if out.returncode != 0:
             print(l, "FAILED", out.stderr[-2000:])
@@ -47,4 +66,5 @@ for r in range(rounds):
 for l in libs:
     v = res[l]
     if v["vote_kernel_ms"]:
-        print(f"{l:40s} vote_kernel {statistics.median(v['vote_kernel_ms']):.4f} ms  stages {statistics.median(v['total_ms']):.4f} ms  (n={len(v['vote_kernel_ms'])})")
+        print(f"{l:40s} vote_kernel {statistics.median(v['vote_kernel_ms']):.4f} ms  stages {statistics.median(v['total_ms']):.4f} ms  "
+              f"e2e {statistics.median(v['e2e_ms']):.4f} ms  (n={len(v['vote_kernel_ms'])})")

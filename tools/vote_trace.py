@@ -19,7 +19,9 @@ ctx = rv.Context(0)
 d = torch.from_numpy(corrs).cuda()
 h = torch.empty((corrs.shape[0], 6), dtype=torch.float64, pin_memory=True)
 h.numpy()[:] = corrs
-lib = C.CDLL(str(ROOT / "paper_2502_06337_b200" / "_lib" / "librotavote_b200.so"))
+from paper_2502_06337_b200 import _native  # noqa: E402
+
+lib = C.CDLL(str(_native.LIB_PATH))  # the library the context uses (RV_LIB_PATH for variants)
 buf = (C.c_ulonglong * (2 * 65536))()
 
 
