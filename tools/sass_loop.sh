@@ -20,12 +20,12 @@ for i,(a,l) in enumerate(addr):
     t=int(m.group(1),16)
     if t>=a or t not in idx: continue
     body=addr[idx[t]:i+1]
-    if sum('ATOMS.ADD RZ' in x for _,x in body)==2 and any('LDS.128' in x for _,x in body):
+    if sum(re.search(r'ATOMS\.ADD RZ, \[R', x) is not None for _,x in body)>=2 and any('LDS.128' in x for _,x in body):
         if best is None or len(body)<len(best): best=body
 if best is None:
     print("hot loop not found"); raise SystemExit
 # exclude the cold block: from the first predicated forward branch after the last ATOMS to its target
-at=[k for k,(a,x) in enumerate(best) if 'ATOMS.ADD RZ' in x][-1]
+at=[k for k,(a,x) in enumerate(best) if re.search(r'ATOMS\.ADD RZ, \[R', x)][1]
 hot=best
 for k in range(at, len(best)):
     m=re.search(r'@!?P\d+\s+BRA\s+(0x[0-9a-f]+)', best[k][1])
