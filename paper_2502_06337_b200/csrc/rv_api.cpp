@@ -1883,19 +1883,30 @@ std::vector<CandResult> evaluate_candidates(rv_context* c, const std::vector<std
   int32_t* idx = c->cand_idx.get<int32_t>(K * nn);
   int32_t* sup = c->cand_sup.get<int32_t>(2 * K);
   uint32_t* band = want_band ? c->cand_band.get<uint32_t>(K * bw) : nullptr;
-  uint32_t* bins = c->bins.get<uint32_t>(cfg.angle_bins);
-  double* raw = c->raw.get<double>(nn);
-  double* asums = c->angle_sums.get<double>(2 * 296);
-  // every candidate's refine_loop in one cooperative launch (compaction fused), then each angle
-  // vote and peak queued back to back: no read-back in between
+  // every candidate's refine_loop in one cooperative launch (compaction fused), then all K angle
+  // votes in one launch and all K peak sums in one launch (per-candidate histograms, angle lists
+  // and summary slots): no read-back in between
   static const bool multi_on = [] {
     const char* e = std::getenv("RV_COOP_MULTI");
     return !(e && e[0] == '0');
   }();
+  const bool batch = multi_on && K <= 8;  // done counters: c->done_ptr() holds 8
+  const size_t KB = batch ? K : 1;
+  uint32_t* bins = c->bins.get<uint32_t>(KB * (size_t)cfg.angle_bins);
+  double* raw = c->raw.get<double>(KB * nn);
+  double* asums = c->angle_sums.get<double>(KB * 2 * 296);
   if (multi_on)
     coop_refine_multi_launch(c, cs, starts, {}, 0, cfg, &sums[0].st, sizeof(Summary), sums[0].counts, idx, nn, bins,
                              cfg.angle_bins);
-  for (size_t k = 0; k < K; ++k) {
+  if (batch) {
+    launch_zero_i32(reinterpret_cast<int32_t*>(bins), (int)(K * (size_t)cfg.angle_bins), c->st);
+    launch_vote_angles_batch_k((int)K, corrs, idx, nn, cs.n, cfg.angle_bins, cfg.tau_deg, bins, raw, nn, sums[0].counts,
+                               sums[0].st.axis, &sums[0].st.count, sizeof(Summary), c->st);
+    launch_peak_angle_batch_k((int)K, bins, cfg.angle_bins, raw, nn, cs.n, asums, sums[0].angle, c->done_ptr(),
+                              &sums[0].st.count, sizeof(Summary), c->st);
+    count_launch(c, 3);
+  }
+  for (size_t k = 0; k < K && !batch; ++k) {
     CoopState* st = &sums[k].st;
     if (!multi_on) {
       CoopFused fz;
@@ -1915,10 +1926,14 @@ std::vector<CandResult> evaluate_candidates(rv_context* c, const std::vector<std
   }
   std::vector<Summary> hs(K);
   read_small(c, hs.data(), sums, K, "candidates D2H");
-  int32_t* bc = c->sup_counts.get<int32_t>((size_t)classify_blocks(cs.n) * 2);
+  const int SM = model_support_multi_max();
+  int32_t* bc = c->sup_counts.get<int32_t>((size_t)classify_blocks(cs.n) * 2 * SM);
+  std::vector<std::array<double, 3>> ax(K);
+  std::vector<double> an(K, 0.0);
   for (size_t k = 0; k < K; ++k) {
     const Summary& sm = hs[k];
     CandResult& r = out[k];
+    std::memcpy(ax[k].data(), sm.st.axis, sizeof(double) * 3);
     if (sm.counts[0] == 0) continue;  // angle_dev: NoVotes -> the candidate is skipped
     Estimate& e = r.est;
     std::memcpy(e.axis, sm.st.axis, sizeof e.axis);
@@ -1929,13 +1944,21 @@ std::vector<CandResult> evaluate_candidates(rv_context* c, const std::vector<std
       if (angle <= -kPiD) angle += 2.0 * kPiD;
     }
     e.angle = angle;
+    an[k] = angle;
     rodrigues3(e.axis, e.angle, e.R);
     e.dev_count = (int64_t)sm.st.count;
     r.d_idx = idx + k * nn;
     r.d_band = band ? band + k * bw : nullptr;
     r.ok = true;
-    launch_model_support_k(cs.zx, cs.zy, cs.zz, cs.kept, corrs, cs.n, e.axis, e.angle, cfg.epsilon, cfg.tau_deg,
-                           band ? band + k * bw : nullptr, bc, sup + 2 * k, c->done_ptr(), c->st);
+  }
+  // every candidate's model_support (estimator.cpp:117-137) in one pass over the constraints per
+  // batch of up to SM candidates (skipped candidates are evaluated too and ignored)
+  for (size_t k0 = 0; k0 < K; k0 += (size_t)SM) {
+    const int kb = (int)std::min<size_t>((size_t)SM, K - k0);
+    launch_model_support_multi_k(cs.zx, cs.zy, cs.zz, cs.kept, corrs, cs.n, kb,
+                                 reinterpret_cast<const double(*)[3]>(ax[k0].data()), an.data() + k0, cfg.epsilon,
+                                 cfg.tau_deg, band ? band + k0 * bw : nullptr, bw, bc, sup + 2 * k0, c->done_ptr(),
+                                 c->st);
     count_launch(c);
   }
   std::vector<int32_t> hsup(2 * K);

@@ -181,6 +181,25 @@ void launch_vote_angles_k(const double axis[3], const double* corrs, const int32
                           int32_t* idx_host = nullptr);
 void launch_peak_angle_k(const uint32_t* bins, int bin_count, const double* raw, int64_t n_raw, double* block_sums,
                          double* result, unsigned int* done, cudaStream_t s, const long long* n_dev = nullptr);
+// model_support of K <= model_support_multi_max() candidates in one pass (block_counts: nblocks *
+// 2 * model_support_multi_max() ints; result: [K][2])
+// K candidates' angle votes / peak sums in one launch each (blockIdx.y = candidate; candidate k at
+// idx + k*idx_stride, bins + k*bin_count, raw + k*raw_stride, and byte offset k*state_stride_b
+// from axis_dev / n_dev / counts / result; block_sums: K * 2 * peak_angle_blocks(n); done: K
+// counters). Per candidate identical to launch_vote_angles_k / launch_peak_angle_k.
+void launch_vote_angles_batch_k(int K, const double* corrs, const int32_t* idx, size_t idx_stride, int64_t n_idx,
+                                int bin_count, double tau, uint32_t* bins, double* raw, size_t raw_stride,
+                                unsigned long long* counts, const double* axis_dev, const long long* n_dev,
+                                size_t state_stride_b, cudaStream_t s);
+int peak_angle_blocks(int64_t n_raw);
+void launch_peak_angle_batch_k(int K, const uint32_t* bins, int bin_count, const double* raw, size_t raw_stride,
+                               int64_t n_raw, double* block_sums, double* result, unsigned int* done,
+                               const long long* n_dev, size_t state_stride_b, cudaStream_t s);
+int model_support_multi_max();
+void launch_model_support_multi_k(const double* zx, const double* zy, const double* zz, const int32_t* kept,
+                                  const double* corrs, int64_t n, int K, const double (*axes)[3], const double* angles,
+                                  double eps, double tau, uint32_t* band_flags, size_t band_stride,
+                                  int32_t* block_counts, int32_t* result, unsigned int* done, cudaStream_t s);
 void launch_model_support_k(const double* zx, const double* zy, const double* zz, const int32_t* kept,
                             const double* corrs, int64_t n, const double axis[3], double angle, double eps, double tau,
                             uint32_t* band_flags, int32_t* block_counts, int32_t* result, unsigned int* done,

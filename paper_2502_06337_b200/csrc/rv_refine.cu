@@ -250,10 +250,21 @@ struct AngArgs {
   uint32_t* bins;
   double* raw;
   unsigned long long* counts;
+  // candidate batches (blockIdx.y = candidate): per-candidate offsets; 0 for a single vote
+  size_t idx_stride, raw_stride, state_stride_b;  // elements, elements, bytes (axis_dev / n_dev / counts)
 };
 
 __global__ void __launch_bounds__(256) vote_angles_kernel(AngArgs a) {
   extern __shared__ uint32_t s_bins[];
+  if (blockIdx.y) {  // candidate y of a batch: its own list, histogram, angles, summary slot
+    const size_t y = blockIdx.y;
+    a.idx += y * a.idx_stride;
+    a.raw += y * a.raw_stride;
+    a.bins += y * (size_t)a.bins_n;
+    if (a.axis_dev) a.axis_dev = reinterpret_cast<const double*>(reinterpret_cast<const char*>(a.axis_dev) + y * a.state_stride_b);
+    if (a.n_dev) a.n_dev = reinterpret_cast<const long long*>(reinterpret_cast<const char*>(a.n_dev) + y * a.state_stride_b);
+    a.counts = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(a.counts) + y * a.state_stride_b);
+  }
   const bool use_smem = a.bins_n <= 8192;
   if (use_smem)
     for (int k = threadIdx.x; k < a.bins_n; k += blockDim.x) s_bins[k] = 0;
@@ -296,7 +307,17 @@ __global__ void __launch_bounds__(256) vote_angles_kernel(AngArgs a) {
 // 1.5 bin widths (wrapped difference) of the bin center. result: [0]=s [1]=c [2]=k [3]=center.
 __global__ void __launch_bounds__(256) peak_angle_kernel(const uint32_t* bins, int bins_n, const double* raw,
                                                         int64_t n_max, double* block_sums, double* result,
-                                                        unsigned int* done, const long long* n_dev) {
+                                                        unsigned int* done, const long long* n_dev,
+                                                        size_t raw_stride, size_t state_stride_b) {
+  if (blockIdx.y) {  // candidate y of a batch (vote_angles_kernel's layout); its own done counter
+    const size_t y = blockIdx.y;
+    bins += y * (size_t)bins_n;
+    raw += y * raw_stride;
+    block_sums += y * 2 * (size_t)gridDim.x;
+    result = reinterpret_cast<double*>(reinterpret_cast<char*>(result) + y * state_stride_b);
+    done += y;
+    if (n_dev) n_dev = reinterpret_cast<const long long*>(reinterpret_cast<const char*>(n_dev) + y * state_stride_b);
+  }
   const int64_t n = n_dev ? min(n_max, (int64_t)*n_dev) : n_max;
   __shared__ unsigned long long s_key[8];
   __shared__ double s_red[2][8];
@@ -473,6 +494,104 @@ __global__ void __launch_bounds__(kClsThreads) model_support_kernel(SupArgs a) {
     a.result[1] = (int32_t)bb;
     *a.done = 0u;
   }
+}
+
+// model_support of up to kSupMax candidates in ONE pass (the rescue / estimate_multi candidate
+// batches): each constraint's z is read once and tested against every candidate, with exactly the
+// per-candidate predicate of model_support_kernel; per-candidate integer counts (order-free), the
+// last block reduces them. Equal to K launches of model_support_kernel, bit for bit.
+constexpr int kSupMax = 8;
+struct SupMultiArgs {
+  const double* zx;
+  const double* zy;
+  const double* zz;
+  const int32_t* kept;
+  const double* corrs;
+  int64_t n;
+  int K;
+  double ax[kSupMax][3];
+  double angle[kSupMax];
+  double eps, tau;
+  uint32_t* band_flags;  // nullable: candidate k's words at band_flags + k * band_stride
+  size_t band_stride;
+  int32_t* block_counts; // [nblocks][kSupMax][2]
+  int32_t* result;       // [K][2]: coherent, band size
+  unsigned int* done;
+};
+
+__global__ void __launch_bounds__(kClsThreads) model_support_multi_kernel(SupMultiArgs a) {
+  __shared__ int s_c[kClsThreads / 32][kSupMax][2];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kClsPerBlock;
+  int coh[kSupMax], band[kSupMax];
+#pragma unroll
+  for (int k = 0; k < kSupMax; ++k) coh[k] = band[k] = 0;
+  for (int r = 0; r < kClsPerThread; ++r) {
+    const int64_t i = base + r * kClsThreads + tid;
+    const bool ok = i < a.n;
+    const double z0 = ok ? a.zx[i] : 0.0, z1 = ok ? a.zy[i] : 0.0, z2 = ok ? a.zz[i] : 0.0;
+    const int64_t w0 = base + r * kClsThreads + warp * 32;
+#pragma unroll
+    for (int k = 0; k < kSupMax; ++k) {
+      if (k >= a.K) break;  // uniform
+      bool inb = false;
+      if (ok) {
+        const double d = fabs(xdot(a.ax[k][0], a.ax[k][1], a.ax[k][2], z0, z1, z2));
+        if (d < 4.0 * a.eps) {
+          double ang;
+          if (corr_angle(a.ax[k][0], a.ax[k][1], a.ax[k][2], a.corrs + 6 * (int64_t)a.kept[i], a.tau, &ang)) {
+            if (fabs(remainder(xs(ang, a.angle[k]), 2.0 * kPi)) < 0.1) {
+              inb = true;
+              if (d < a.eps) ++coh[k];
+            }
+          }
+        }
+      }
+      band[k] += inb ? 1 : 0;
+      if (a.band_flags) {
+        const unsigned word = __ballot_sync(0xFFFFFFFFu, inb);
+        if (lane == 0 && w0 < a.n) a.band_flags[k * a.band_stride + (w0 >> 5)] = word;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kSupMax; ++k) {
+    if (k >= a.K) break;
+    int c = coh[k], b = band[k];
+    for (int o = 16; o > 0; o >>= 1) {
+      c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+      b += __shfl_xor_sync(0xFFFFFFFFu, b, o);
+    }
+    if (lane == 0) {
+      s_c[warp][k][0] = c;
+      s_c[warp][k][1] = b;
+    }
+  }
+  __syncthreads();
+  if (tid < 2 * a.K) {
+    const int k = tid >> 1, q = tid & 1;
+    int v = 0;
+    for (int w = 0; w < kClsThreads / 32; ++w) v += s_c[w][k][q];
+    a.block_counts[(size_t)blockIdx.x * (2 * kSupMax) + tid] = v;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // last block: one warp per (candidate, count) pair, integer sums (order-free)
+  for (int p = warp; p < 2 * a.K; p += kClsThreads / 32) {
+    long long v = 0;
+    for (unsigned b = lane; b < gridDim.x; b += 32) v += __ldcg(a.block_counts + (size_t)b * (2 * kSupMax) + p);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if (lane == 0) a.result[p] = (int32_t)v;
+  }
+  __syncthreads();
+  if (tid == 0) *a.done = 0u;
 }
 
 __global__ void strip_kernel(const double* zx, const double* zy, const double* zz, int64_t n, double a0, double a1,
@@ -709,17 +828,58 @@ void launch_vote_angles_k(const double axis[3], const double* corrs, const int32
   a.bins = bins;
   a.raw = raw;
   a.counts = counts;
+  a.idx_stride = a.raw_stride = a.state_stride_b = 0;
   const int64_t want = (n_idx + 255) / 256;
   const int blocks = (int)(want < 1 ? 1 : (want > 592 ? 592 : want));
   const size_t smem = bin_count <= 8192 ? (size_t)bin_count * 4 : 0;
   vote_angles_kernel<<<blocks, 256, smem, s>>>(a);
 }
 
+void launch_vote_angles_batch_k(int K, const double* corrs, const int32_t* idx, size_t idx_stride, int64_t n_idx,
+                                int bin_count, double tau, uint32_t* bins, double* raw, size_t raw_stride,
+                                unsigned long long* counts, const double* axis_dev, const long long* n_dev,
+                                size_t state_stride_b, cudaStream_t s) {
+  AngArgs a;
+  a.idx_host = nullptr;
+  a.a0 = a.a1 = a.a2 = 0.0;
+  a.axis_dev = axis_dev;
+  a.n_dev = n_dev;
+  a.tau = tau;
+  a.corrs = corrs;
+  a.idx = idx;
+  a.n = n_idx;
+  a.bins_n = bin_count;
+  a.bins = bins;
+  a.raw = raw;
+  a.counts = counts;
+  a.idx_stride = idx_stride;
+  a.raw_stride = raw_stride;
+  a.state_stride_b = state_stride_b;
+  // the same grid per candidate as launch_vote_angles_k (identical thread-to-element mapping)
+  const int64_t want = (n_idx + 255) / 256;
+  const int blocks = (int)(want < 1 ? 1 : (want > 592 ? 592 : want));
+  const size_t smem = bin_count <= 8192 ? (size_t)bin_count * 4 : 0;
+  vote_angles_kernel<<<dim3(blocks, K), 256, smem, s>>>(a);
+}
+
 void launch_peak_angle_k(const uint32_t* bins, int bin_count, const double* raw, int64_t n_raw, double* block_sums,
                          double* result, unsigned int* done, cudaStream_t s, const long long* n_dev) {
   const int64_t want = (n_raw + 255) / 256;
   const int blocks = (int)(want < 1 ? 1 : (want > 296 ? 296 : want));
-  peak_angle_kernel<<<blocks, 256, 0, s>>>(bins, bin_count, raw, n_raw, block_sums, result, done, n_dev);
+  peak_angle_kernel<<<blocks, 256, 0, s>>>(bins, bin_count, raw, n_raw, block_sums, result, done, n_dev, 0, 0);
+}
+
+int peak_angle_blocks(int64_t n_raw) {
+  const int64_t want = (n_raw + 255) / 256;
+  return (int)(want < 1 ? 1 : (want > 296 ? 296 : want));
+}
+
+void launch_peak_angle_batch_k(int K, const uint32_t* bins, int bin_count, const double* raw, size_t raw_stride,
+                               int64_t n_raw, double* block_sums, double* result, unsigned int* done,
+                               const long long* n_dev, size_t state_stride_b, cudaStream_t s) {
+  // the same grid (hence the same fixed-order sums) per candidate as launch_peak_angle_k
+  peak_angle_kernel<<<dim3(peak_angle_blocks(n_raw), K), 256, 0, s>>>(bins, bin_count, raw, n_raw, block_sums, result,
+                                                                     done, n_dev, raw_stride, state_stride_b);
 }
 
 void launch_model_support_k(const double* zx, const double* zy, const double* zz, const int32_t* kept,
@@ -744,6 +904,34 @@ void launch_model_support_k(const double* zx, const double* zy, const double* zz
   a.result = result;
   a.done = done;
   model_support_kernel<<<classify_blocks(n), kClsThreads, 0, s>>>(a);
+}
+
+int model_support_multi_max() { return kSupMax; }
+
+void launch_model_support_multi_k(const double* zx, const double* zy, const double* zz, const int32_t* kept,
+                                  const double* corrs, int64_t n, int K, const double (*axes)[3], const double* angles,
+                                  double eps, double tau, uint32_t* band_flags, size_t band_stride,
+                                  int32_t* block_counts, int32_t* result, unsigned int* done, cudaStream_t s) {
+  SupMultiArgs a;
+  a.zx = zx;
+  a.zy = zy;
+  a.zz = zz;
+  a.kept = kept;
+  a.corrs = corrs;
+  a.n = n;
+  a.K = K;
+  for (int k = 0; k < kSupMax; ++k) {
+    for (int q = 0; q < 3; ++q) a.ax[k][q] = k < K ? axes[k][q] : 0.0;
+    a.angle[k] = k < K ? angles[k] : 0.0;
+  }
+  a.eps = eps;
+  a.tau = tau;
+  a.band_flags = band_flags;
+  a.band_stride = band_stride;
+  a.block_counts = block_counts;
+  a.result = result;
+  a.done = done;
+  model_support_multi_kernel<<<classify_blocks(n), kClsThreads, 0, s>>>(a);
 }
 
 void launch_strip_k(const double* zx, const double* zy, const double* zz, int64_t n, const double axis[3], double strip,
