@@ -519,62 +519,92 @@ struct SupMultiArgs {
   unsigned int* done;
 };
 
+// Per candidate, the block first compacts its |a.z| < 4 eps constraints (ballot + warp offsets:
+// ~6% of them) into a shared list, then all threads run the expensive part -- the
+// correspondence angle (f64 cross products + atan2) and the window test -- on that dense list,
+// instead of every warp running it for its one or two band lanes. Band bits are set in a shared
+// bitmap of the block's 32 words; counts are integers (order-free).
 __global__ void __launch_bounds__(kClsThreads) model_support_multi_kernel(SupMultiArgs a) {
-  __shared__ int s_c[kClsThreads / 32][kSupMax][2];
+  __shared__ int s_list[kClsPerBlock];                 // band candidates: element (r * threads + tid)
+  __shared__ double s_d[kClsPerBlock];                 // their |a.z|
+  __shared__ uint32_t s_words[kClsPerBlock / 32];      // band bits of the block's elements
+  __shared__ int s_wcnt[kClsThreads / 32], s_n;
+  __shared__ int s_cnt[kSupMax][2];
   __shared__ bool s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t base = (int64_t)blockIdx.x * kClsPerBlock;
-  int coh[kSupMax], band[kSupMax];
+  double z[kClsPerThread][3];
 #pragma unroll
-  for (int k = 0; k < kSupMax; ++k) coh[k] = band[k] = 0;
   for (int r = 0; r < kClsPerThread; ++r) {
     const int64_t i = base + r * kClsThreads + tid;
     const bool ok = i < a.n;
-    const double z0 = ok ? a.zx[i] : 0.0, z1 = ok ? a.zy[i] : 0.0, z2 = ok ? a.zz[i] : 0.0;
-    const int64_t w0 = base + r * kClsThreads + warp * 32;
+    z[r][0] = ok ? a.zx[i] : 0.0;
+    z[r][1] = ok ? a.zy[i] : 0.0;
+    z[r][2] = ok ? a.zz[i] : 0.0;
+  }
+  if (tid < 2 * kSupMax) s_cnt[tid >> 1][tid & 1] = 0;
+  for (int k = 0; k < a.K; ++k) {  // uniform
+    const double a0 = a.ax[k][0], a1 = a.ax[k][1], a2 = a.ax[k][2];
+    // 1. compaction of the band candidates (in element order within each warp)
+    int mine = 0;
+    bool cand[kClsPerThread];
+    double dv[kClsPerThread];
 #pragma unroll
-    for (int k = 0; k < kSupMax; ++k) {
-      if (k >= a.K) break;  // uniform
-      bool inb = false;
-      if (ok) {
-        const double d = fabs(xdot(a.ax[k][0], a.ax[k][1], a.ax[k][2], z0, z1, z2));
-        if (d < 4.0 * a.eps) {
-          double ang;
-          if (corr_angle(a.ax[k][0], a.ax[k][1], a.ax[k][2], a.corrs + 6 * (int64_t)a.kept[i], a.tau, &ang)) {
-            if (fabs(remainder(xs(ang, a.angle[k]), 2.0 * kPi)) < 0.1) {
-              inb = true;
-              if (d < a.eps) ++coh[k];
-            }
-          }
-        }
+    for (int r = 0; r < kClsPerThread; ++r) {
+      const int64_t i = base + r * kClsThreads + tid;
+      dv[r] = fabs(xdot(a0, a1, a2, z[r][0], z[r][1], z[r][2]));
+      cand[r] = i < a.n && dv[r] < 4.0 * a.eps;
+      mine += cand[r] ? 1 : 0;
+    }
+    int incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_wcnt[warp] = incl;
+    if (tid < kClsPerBlock / 32) s_words[tid] = 0u;
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int w = 0; w < kClsThreads / 32; ++w) {
+      off += w < warp ? s_wcnt[w] : 0;
+      tot += s_wcnt[w];
+    }
+    int pos = off + incl - mine;
+#pragma unroll
+    for (int r = 0; r < kClsPerThread; ++r)
+      if (cand[r]) {
+        s_list[pos] = r * kClsThreads + tid;
+        s_d[pos] = dv[r];
+        ++pos;
       }
-      band[k] += inb ? 1 : 0;
-      if (a.band_flags) {
-        const unsigned word = __ballot_sync(0xFFFFFFFFu, inb);
-        if (lane == 0 && w0 < a.n) a.band_flags[k * a.band_stride + (w0 >> 5)] = word;
+    __syncthreads();
+    // 2. the angle test on the dense list
+    int coh = 0, band = 0;
+    for (int q = tid; q < tot; q += kClsThreads) {
+      const int e = s_list[q];
+      const int64_t i = base + e;
+      double ang;
+      if (corr_angle(a0, a1, a2, a.corrs + 6 * (int64_t)a.kept[i], a.tau, &ang) &&
+          fabs(remainder(xs(ang, a.angle[k]), 2.0 * kPi)) < 0.1) {
+        ++band;
+        if (s_d[q] < a.eps) ++coh;
+        if (a.band_flags) atomicOr(&s_words[e >> 5], 1u << (e & 31));
       }
     }
-  }
-#pragma unroll
-  for (int k = 0; k < kSupMax; ++k) {
-    if (k >= a.K) break;
-    int c = coh[k], b = band[k];
     for (int o = 16; o > 0; o >>= 1) {
-      c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-      b += __shfl_xor_sync(0xFFFFFFFFu, b, o);
+      coh += __shfl_xor_sync(0xFFFFFFFFu, coh, o);
+      band += __shfl_xor_sync(0xFFFFFFFFu, band, o);
     }
-    if (lane == 0) {
-      s_c[warp][k][0] = c;
-      s_c[warp][k][1] = b;
+    if (lane == 0 && (coh | band)) {
+      atomicAdd(&s_cnt[k][0], coh);
+      atomicAdd(&s_cnt[k][1], band);
     }
+    __syncthreads();
+    if (a.band_flags && tid < kClsPerBlock / 32 && base + 32 * tid < a.n)
+      a.band_flags[k * a.band_stride + (size_t)(base >> 5) + tid] = s_words[tid];
+    __syncthreads();  // s_list / s_words / s_wcnt reused by the next candidate
   }
-  __syncthreads();
-  if (tid < 2 * a.K) {
-    const int k = tid >> 1, q = tid & 1;
-    int v = 0;
-    for (int w = 0; w < kClsThreads / 32; ++w) v += s_c[w][k][q];
-    a.block_counts[(size_t)blockIdx.x * (2 * kSupMax) + tid] = v;
-  }
+  if (tid < 2 * a.K) a.block_counts[(size_t)blockIdx.x * (2 * kSupMax) + tid] = s_cnt[tid >> 1][tid & 1];
   __syncthreads();
   if (tid == 0) {
     __threadfence();
