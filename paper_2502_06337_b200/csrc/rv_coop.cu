@@ -512,6 +512,7 @@ __global__ void __launch_bounds__(kThreads) coop_refine_multi_kernel(CoopMultiAr
   extern __shared__ double s_z[];  // [3][z_cap] z, then [K][2][fw_cap] flag words
   __shared__ double s_red[8][kWarps];
   __shared__ double s_val[kMaxCand][8];  // this block's partials of the pass
+  __shared__ double s_redK[kMaxCand][8][kWarps];  // per-warp partials of every candidate
   __shared__ double s_tot[kMaxCand][8];  // all blocks' totals of the pass
   __shared__ double s_axis[kMaxCand][3], s_e[kMaxCand];
   __shared__ int s_done[kMaxCand], s_fslot[kMaxCand], s_all_done;
@@ -606,11 +607,22 @@ __global__ void __launch_bounds__(kThreads) coop_refine_multi_kernel(CoopMultiAr
       first_pass = false;  // z is now in shared memory (each thread reads back its own elements)
       v[6] = (double)__any_sync(0xFFFFFFFFu, diff);
       v[7] = (double)cnt;
-      block_reduce8(v, s_red);
-      if (tid == 0)
-        for (int k = 0; k < 8; ++k) s_val[c][k] = v[k];
-      __syncthreads();
+      // block_reduce8's first half (warp sums into this candidate's slot); the cross-warp half runs
+      // for every candidate after ONE barrier below (the same fixed order)
+      const double r8 = warp_sum8(v);
+      if ((lane & 3) == 0) s_redK[c][lane >> 2][warp] = r8;
     }
+    __syncthreads();
+    if (warp == 0)
+      for (int c = 0; c < K; ++c) {
+        if (s_done[c]) continue;  // uniform
+        double x[8], t[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = lane < kWarps ? s_redK[c][k][lane] : 0.0;
+        warp_bcast8(warp_sum8(x), t);
+        if (lane == 0)
+          for (int k = 0; k < 8; ++k) s_val[c][k] = t[k];
+      }
     const unsigned long long seq = epoch | (unsigned long long)(pass + 1);
     if (tid == 0) {
       double* ln = a.block_part + (size_t)blockIdx.x * line;
@@ -637,9 +649,20 @@ __global__ void __launch_bounds__(kThreads) coop_refine_multi_kernel(CoopMultiAr
       for (int c = 0; c < K; ++c) {
         if (s_done[c]) continue;  // uniform
         double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (unsigned b = lane; b < gridDim.x; b += 32)
+        for (unsigned j0 = 0; j0 < nl; j0 += 4) {  // 4 lines x 8 values in flight per lane (same order)
+          double x[4][8];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) acc[k] = xa(acc[k], __ldcg(a.block_part + (size_t)b * line + 8 * c + k));
+          for (int j = 0; j < 4; ++j) {
+            const unsigned b = lane + 32 * (j0 + j);
+            const bool in = j0 + j < nl && b < gridDim.x;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) x[j][k] = in ? __ldcg(a.block_part + (size_t)b * line + 8 * c + k) : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[k] = xa(acc[k], x[j][k]);
+        }
         double t[8];
         warp_bcast8(warp_sum8(acc), t);
         if (lane == 0)
