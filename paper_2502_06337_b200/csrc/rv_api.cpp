@@ -223,7 +223,6 @@ struct rv_context {
   DBuf peak_out;                         // chained solve: device Summary (peak, state, angles)
   DBuf red_keys;                         // fused argmax scratch of the tile reduction
   DBuf kept_acc;                          // in-order preprocess: kept-count accumulator + ticket
-  DBuf sort_tmp;                          // CUB radix-sort scratch (multi-model strip percentile)
   DBuf cand_sums, cand_idx, cand_sup, cand_band;  // batched rescue candidates (per-candidate slots)
   // CSV ingest (rv_io.cu)
   DBuf csv_text, csv_chunk, csv_misc, csv_dpos, csv_dline, csv_nl, csv_status, csv_row, csv_block, csv_out, csv_fb,
@@ -246,7 +245,7 @@ struct rv_context {
   const double* coop_mpart_zeroed = nullptr;
   // angles / support
   DBuf bins, raw, angle_counts, angle_sums, angle_result, sup_counts, sup_result, band_flagsA, band_flagsB,
-      band_idx, band_vals, near_h, near_result;
+      band_vals, near_h, near_result, strip_val;
   DBuf user_z;  // scratch copy of a constraint span (path functions)
   DBuf chunk_hi;                          // pipelined vote: kept count at each chunk end
   cudaStream_t copy_st = nullptr;         // H2D copies of the pipelined host path
@@ -2224,37 +2223,22 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
       launch_strip_identity_k(d_corrs, pre.cs.kept, pre.cs.n, cfg.normalize_inputs, removed, c->st);
       count_launch(c);
     } else {
-      double strip = 2.0 * cfg.epsilon;
+      const double strip = 2.0 * cfg.epsilon;
       if (sup.band > 0) {
-        // 95th-percentile band value over the band members (nth_element's q-th smallest): flag
-        // offsets, compaction, |a.z| gather and a radix sort on the device; two scalar reads
-        const int nb = classify_blocks(pre.cs.n);
-        int32_t* offs = c->boffB.get<int32_t>((size_t)nb + 1);
-        int32_t* dtot = c->misc32.get<int32_t>(8) + 6;
-        launch_flag_offsets(best_band, pre.cs.n, offs, dtot, c->st);
-        int32_t* h = reinterpret_cast<int32_t*>(c->pinned);
-        ck(cudaMemcpyAsync(h, dtot, sizeof(int32_t), cudaMemcpyDeviceToHost, c->st), "band count D2H");
-        sync(c);
-        const int64_t acc = h[0];
-        if (acc > 0) {
-          int32_t* bidx = c->band_idx.get<int32_t>((size_t)acc);
-          launch_compact_flags(best_band, pre.cs.n, nullptr, offs, bidx, c->st);
-          double* bv = c->band_vals.get<double>((size_t)acc * 2);
-          launch_gather_dot_k(pre.cs.zx, pre.cs.zy, pre.cs.zz, bidx, acc, est.axis, bv, c->st);
-          size_t tb = 0;
-          ck(sort_doubles(nullptr, &tb, bv, bv + acc, (int)acc, c->st), "sort size");
-          void* tmp = c->sort_tmp.get<uint8_t>(tb);
-          ck(sort_doubles(tmp, &tb, bv, bv + acc, (int)acc, c->st), "band sort");
-          count_launch(c, 5);
-          const size_t q = std::min<size_t>((size_t)acc - 1, ((size_t)acc * 95) / 100);
-          double* hv = reinterpret_cast<double*>(c->pinned);
-          ck(cudaMemcpyAsync(hv, bv + acc + q, sizeof(double), cudaMemcpyDeviceToHost, c->st), "band q D2H");
-          sync(c);
-          strip = std::max(strip, 1.25 * hv[0]);
-        }
+        // strip = max(2 eps, 1.25 * the 95th-percentile band value) (nth_element's q-th smallest
+        // over the winner's support band, whose size the host already has from model_support):
+        // selected and applied on the device, no read-back
+        const long long acc = (long long)sup.band;
+        const long long q = std::min(acc - 1, (acc * 95) / 100);
+        unsigned long long* keys = c->band_vals.get<unsigned long long>((size_t)acc);
+        double* sdev = c->strip_val.get<double>(1);
+        launch_band_strip_k(best_band, pre.cs.n, pre.cs.zx, pre.cs.zy, pre.cs.zz, est.axis, q, strip, keys, sdev,
+                            removed, c->st);
+        count_launch(c, 2);
+      } else {
+        launch_strip_k(pre.cs.zx, pre.cs.zy, pre.cs.zz, pre.cs.n, est.axis, strip, removed, c->st);
+        count_launch(c);
       }
-      launch_strip_k(pre.cs.zx, pre.cs.zy, pre.cs.zz, pre.cs.n, est.axis, strip, removed, c->st);
-      count_launch(c);
     }
     out.push_back(std::move(est));
   }

@@ -195,6 +195,12 @@ int peak_angle_blocks(int64_t n_raw);
 void launch_peak_angle_batch_k(int K, const uint32_t* bins, int bin_count, const double* raw, size_t raw_stride,
                                int64_t n_raw, double* block_sums, double* result, unsigned int* done,
                                const long long* n_dev, size_t state_stride_b, cudaStream_t s);
+// estimate_multi's band strip on the device (no read-back): q-th smallest |axis.z| over the set
+// bits of `band` (keys: >= band-size u64 scratch), strip = max(floor_strip, 1.25 * value) into
+// strip_dev, then the strip of every constraint with |axis.z| < strip
+void launch_band_strip_k(const uint32_t* band, int64_t n, const double* zx, const double* zy, const double* zz,
+                         const double axis[3], long long q, double floor_strip, unsigned long long* keys,
+                         double* strip_dev, uint8_t* removed, cudaStream_t s);
 int model_support_multi_max();
 void launch_model_support_multi_k(const double* zx, const double* zy, const double* zz, const int32_t* kept,
                                   const double* corrs, int64_t n, int K, const double (*axes)[3], const double* angles,
@@ -212,8 +218,6 @@ void launch_strip_k(const double* zx, const double* zy, const double* zz, int64_
                     uint8_t* removed, cudaStream_t s);
 void launch_strip_identity_k(const double* corrs, const int32_t* kept, int64_t n, int normalize, uint8_t* removed,
                              cudaStream_t s);
-void launch_gather_dot_k(const double* zx, const double* zy, const double* zz, const int32_t* idx, int64_t n,
-                         const double axis[3], double* out, cudaStream_t s);
 void launch_near_identity_k(const double* corrs, const int32_t* sub_kept, int64_t n, int normalize, uint32_t* flags,
                             int32_t* block_count, double* block_h, int32_t* block_offsets, double* result,
                             unsigned int* done, cudaStream_t s);
@@ -317,6 +321,4 @@ int csv_chunks(int64_t nbytes);
 cudaError_t launch_csv_parse(const CsvBuffers& b, cudaStream_t s, int stage);
 void launch_csv_scatter(const int64_t* idx, const double* vals, int n, double* out, cudaStream_t s);
 
-void launch_flag_offsets(const uint32_t* flags, int64_t n, int32_t* offsets, int32_t* total, cudaStream_t s);
-cudaError_t sort_doubles(void* temp, size_t* temp_bytes, const double* in, double* out, int n, cudaStream_t s);
 }  // namespace rvb

@@ -10,7 +10,6 @@
 
 #include <cstdint>
 
-#include <cub/device/device_radix_sort.cuh>
 
 #include "rv_exact.cuh"
 #include "rv_internal.h"
@@ -631,14 +630,96 @@ __global__ void strip_kernel(const double* zx, const double* zy, const double* z
   if (fabs(xdot(a0, a1, a2, zx[i], zy[i], zz[i])) < strip) removed[i] = 1;
 }
 
-// |axis.z| of listed constraints (band values for the strip percentile).
-__global__ void gather_dot_kernel(const double* zx, const double* zy, const double* zz, const int32_t* idx,
-                                  int64_t n, double a0, double a1, double a2, double* out) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const int32_t i = idx[k];
-  out[k] = fabs(xdot(a0, a1, a2, zx[i], zy[i], zz[i]));
+// estimate_multi's strip width (estimator.cpp:470-480) on the device, no host read-back: the
+// q-th smallest |axis.z| over the winning model's support band (nth_element), then
+// strip = max(2 eps, 1.25 * value). One CTA: the band members' values are gathered as u64 keys
+// (the bit patterns of non-negative doubles order like the values; output order is irrelevant to a
+// selection), then an exact radix select (11-bit digits from the top, six passes) finds the key of
+// rank q. Replaces compaction + gather + a full radix sort + two host round trips.
+constexpr int kSelThreads = 1024;
+__global__ void __launch_bounds__(kSelThreads) band_strip_kernel(const uint32_t* band, int64_t n, const double* zx,
+                                                                const double* zy, const double* zz, double a0,
+                                                                double a1, double a2, long long q, double floor_strip,
+                                                                unsigned long long* keys, double* strip_out) {
+  __shared__ unsigned int s_hist[2048];
+  __shared__ unsigned int s_wsum[kSelThreads / 32];
+  __shared__ int s_cnt, s_digit;
+  __shared__ long long s_before;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_cnt = 0;
+  __syncthreads();
+  const int64_t nw = (n + 31) / 32;
+  for (int64_t w = tid; w < nw; w += kSelThreads) {
+    uint32_t m = band[w];
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1u;
+      const int64_t i = w * 32 + bit;
+      if (i < n) {
+        const double d = fabs(xdot(a0, a1, a2, zx[i], zy[i], zz[i]));  // the band value of estimator.cpp:470-480
+        keys[atomicAdd(&s_cnt, 1)] = (unsigned long long)__double_as_longlong(d);
+      }
+    }
+  }
+  __syncthreads();
+  const int acc = s_cnt;
+  if (acc == 0) {  // (the host only launches this with a non-empty band)
+    if (tid == 0) *strip_out = floor_strip;
+    return;
+  }
+  unsigned long long prefix = 0ull, pmask = 0ull;
+  long long rank = q;
+  const int shifts[6] = {53, 42, 31, 20, 9, 0};
+  const int widths[6] = {11, 11, 11, 11, 11, 9};
+  for (int p = 0; p < 6; ++p) {
+    const int sh = shifts[p];
+    const unsigned long long dmask = (1ull << widths[p]) - 1ull;
+    for (int b = tid; b < 2048; b += kSelThreads) s_hist[b] = 0u;
+    __syncthreads();
+    for (int k = tid; k < acc; k += kSelThreads) {
+      const unsigned long long key = keys[k];
+      if ((key & pmask) == prefix) atomicAdd(&s_hist[(key >> sh) & dmask], 1u);
+    }
+    __syncthreads();
+    // exclusive scan of the 2048 bins (2 per thread), then the bin holding rank
+    const unsigned h0 = s_hist[2 * tid], h1 = s_hist[2 * tid + 1];
+    unsigned incl = h0 + h1;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    unsigned long long before = 0;
+    for (int w = 0; w < warp; ++w) before += s_wsum[w];
+    before += incl - (h0 + h1);
+    if ((long long)before <= rank && rank < (long long)(before + h0)) {
+      s_digit = 2 * tid;
+      s_before = (long long)before;
+    } else if ((long long)(before + h0) <= rank && rank < (long long)(before + h0 + h1)) {
+      s_digit = 2 * tid + 1;
+      s_before = (long long)(before + h0);
+    }
+    __syncthreads();
+    prefix |= (unsigned long long)s_digit << sh;
+    pmask |= dmask << sh;
+    rank -= s_before;
+    __syncthreads();  // s_digit / s_before / s_wsum reused by the next pass
+  }
+  if (tid == 0) {
+    const double v = __longlong_as_double((long long)prefix);
+    const double x = 1.25 * v;
+    *strip_out = floor_strip < x ? x : floor_strip;  // std::max(strip, 1.25 * v)
+  }
 }
+
+__global__ void strip_dev_kernel(const double* zx, const double* zy, const double* zz, int64_t n, double a0, double a1,
+                                 double a2, const double* strip, uint8_t* removed) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (fabs(xdot(a0, a1, a2, zx[i], zy[i], zz[i])) < *strip) removed[i] = 1;
+}
+
 
 // near_identity_model cluster test + Kabsch cross-covariance (estimator.cpp:198-249).
 struct NearArgs {
@@ -969,11 +1050,15 @@ void launch_strip_k(const double* zx, const double* zy, const double* zz, int64_
   strip_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(zx, zy, zz, n, axis[0], axis[1], axis[2], strip, removed);
 }
 
-void launch_gather_dot_k(const double* zx, const double* zy, const double* zz, const int32_t* idx, int64_t n,
-                         const double axis[3], double* out, cudaStream_t s) {
-  if (n <= 0) return;
-  gather_dot_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(zx, zy, zz, idx, n, axis[0], axis[1], axis[2], out);
+void launch_band_strip_k(const uint32_t* band, int64_t n, const double* zx, const double* zy, const double* zz,
+                         const double axis[3], long long q, double floor_strip, unsigned long long* keys,
+                         double* strip_dev, uint8_t* removed, cudaStream_t s) {
+  band_strip_kernel<<<1, kSelThreads, 0, s>>>(band, n, zx, zy, zz, axis[0], axis[1], axis[2], q, floor_strip, keys,
+                                             strip_dev);
+  strip_dev_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(zx, zy, zz, n, axis[0], axis[1], axis[2], strip_dev,
+                                                              removed);
 }
+
 
 void launch_near_identity_k(const double* corrs, const int32_t* sub_kept, int64_t n, int normalize, uint32_t* flags,
                             int32_t* block_count, double* block_h, int32_t* block_offsets, double* result,
@@ -1013,55 +1098,6 @@ void launch_strip_identity_k(const double* corrs, const int32_t* kept, int64_t n
   strip_identity_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(corrs, kept, n, normalize, removed);
 }
 
-// ---- band percentile of estimate_multi's strip width (estimator.cpp:452-466) on the device ----
-namespace {
-__global__ void flag_block_counts_kernel(const uint32_t* flags, int64_t nwords, int nb, int32_t* counts) {
-  const int bk = blockIdx.x * blockDim.x + threadIdx.x;
-  if (bk >= nb) return;
-  int acc = 0;
-  for (int w = 0; w < 32; ++w) {
-    const int64_t wi = (int64_t)bk * 32 + w;
-    if (wi < nwords) acc += __popc(flags[wi]);
-  }
-  counts[bk] = acc;
-}
 
-// exclusive scan of n ints in place by one block; the total to *total
-__global__ void __launch_bounds__(1024) scan_i32_kernel(int32_t* v, int n, int32_t* total) {
-  __shared__ int32_t s[1024];
-  const int per = (n + 1023) / 1024;
-  const int lo = threadIdx.x * per, hi = min(lo + per, n);
-  int acc = 0;
-  for (int i = lo; i < hi; ++i) acc += v[i];
-  s[threadIdx.x] = acc;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    const int x = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
-    __syncthreads();
-    s[threadIdx.x] += x;
-    __syncthreads();
-  }
-  int run = threadIdx.x ? s[threadIdx.x - 1] : 0;
-  for (int i = lo; i < hi; ++i) {
-    const int x = v[i];
-    v[i] = run;
-    run += x;
-  }
-  if (threadIdx.x == 1023) *total = s[1023];
-}
-}  // namespace
-
-// Per-1024-bit-block offsets of a flag mask (exclusive popcount scan) and the total set bits.
-void launch_flag_offsets(const uint32_t* flags, int64_t n, int32_t* offsets, int32_t* total, cudaStream_t s) {
-  const int64_t nwords = (n + 31) / 32;
-  const int nb = (int)((nwords + 31) / 32);
-  flag_block_counts_kernel<<<(nb + 255) / 256, 256, 0, s>>>(flags, nwords, nb, offsets);
-  scan_i32_kernel<<<1, 1024, 0, s>>>(offsets, nb, total);
-}
-
-// Ascending sort of n doubles (CUB radix sort); temp == nullptr queries *temp_bytes.
-cudaError_t sort_doubles(void* temp, size_t* temp_bytes, const double* in, double* out, int n, cudaStream_t s) {
-  return cub::DeviceRadixSort::SortKeys(temp, *temp_bytes, in, out, n, 0, 64, s);
-}
 }  // namespace rvb
 
