@@ -2230,11 +2230,11 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
         // selected and applied on the device, no read-back
         const long long acc = (long long)sup.band;
         const long long q = std::min(acc - 1, (acc * 95) / 100);
-        unsigned long long* keys = c->band_vals.get<unsigned long long>((size_t)acc);
+        unsigned long long* keys = c->band_vals.get<unsigned long long>((size_t)acc + 1);  // count + keys
         double* sdev = c->strip_val.get<double>(1);
         launch_band_strip_k(best_band, pre.cs.n, pre.cs.zx, pre.cs.zy, pre.cs.zz, est.axis, q, strip, keys, sdev,
                             removed, c->st);
-        count_launch(c, 2);
+        count_launch(c, 3);
       } else {
         launch_strip_k(pre.cs.zx, pre.cs.zy, pre.cs.zz, pre.cs.n, est.axis, strip, removed, c->st);
         count_launch(c);

@@ -637,38 +637,58 @@ __global__ void strip_kernel(const double* zx, const double* zy, const double* z
 // selection), then an exact radix select (11-bit digits from the top, six passes) finds the key of
 // rank q. Replaces compaction + gather + a full radix sort + two host round trips.
 constexpr int kSelThreads = 1024;
-__global__ void __launch_bounds__(kSelThreads) band_strip_kernel(const uint32_t* band, int64_t n, const double* zx,
-                                                                const double* zy, const double* zz, double a0,
-                                                                double a1, double a2, long long q, double floor_strip,
-                                                                unsigned long long* keys, double* strip_out) {
+constexpr int kSelSmem = 4096;  // keys kept in shared memory once the prefix narrows them down
+// gather: one thread per band word (the whole grid), warp-aggregated output reservation; keys[-1]
+// (a u64 slot before the keys) counts them
+__global__ void band_gather_kernel(const uint32_t* band, int64_t n, const double* zx, const double* zy,
+                                   const double* zz, double a0, double a1, double a2, unsigned long long* keys,
+                                   unsigned long long* count) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const uint32_t m0 = w < (n + 31) / 32 ? band[w] : 0u;
+  uint32_t m = m0;
+  if (w * 32 + 32 > n && w < (n + 31) / 32) m &= (n - w * 32) >= 32 ? 0xFFFFFFFFu : ((1u << (n - w * 32)) - 1u);
+  const int c = __popc(m);
+  int incl = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+  unsigned long long base = 0;
+  if (lane == 31 && tot) base = atomicAdd(count, (unsigned long long)tot);
+  base = __shfl_sync(0xFFFFFFFFu, base, 31);
+  unsigned long long pos = base + (unsigned long long)(incl - c);
+  while (m) {
+    const int bit = __ffs(m) - 1;
+    m &= m - 1u;
+    const int64_t i = w * 32 + bit;
+    const double d = fabs(xdot(a0, a1, a2, zx[i], zy[i], zz[i]));  // the band value of estimator.cpp:470-480
+    keys[pos++] = (unsigned long long)__double_as_longlong(d);
+  }
+}
+
+// select: the key of rank q by an exact radix select (11-bit digits from the top, six passes); the
+// keys still matching the prefix are moved to shared memory as soon as they fit
+__global__ void __launch_bounds__(kSelThreads) band_select_kernel(const unsigned long long* keys,
+                                                                 const unsigned long long* count, long long q,
+                                                                 double floor_strip, double* strip_out) {
   __shared__ unsigned int s_hist[2048];
+  __shared__ unsigned long long s_keys[kSelSmem];
   __shared__ unsigned int s_wsum[kSelThreads / 32];
-  __shared__ int s_cnt, s_digit;
+  __shared__ int s_digit, s_m;
   __shared__ long long s_before;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_cnt = 0;
-  __syncthreads();
-  const int64_t nw = (n + 31) / 32;
-  for (int64_t w = tid; w < nw; w += kSelThreads) {
-    uint32_t m = band[w];
-    while (m) {
-      const int bit = __ffs(m) - 1;
-      m &= m - 1u;
-      const int64_t i = w * 32 + bit;
-      if (i < n) {
-        const double d = fabs(xdot(a0, a1, a2, zx[i], zy[i], zz[i]));  // the band value of estimator.cpp:470-480
-        keys[atomicAdd(&s_cnt, 1)] = (unsigned long long)__double_as_longlong(d);
-      }
-    }
-  }
-  __syncthreads();
-  const int acc = s_cnt;
+  const long long acc = (long long)*count;
   if (acc == 0) {  // (the host only launches this with a non-empty band)
     if (tid == 0) *strip_out = floor_strip;
     return;
   }
   unsigned long long prefix = 0ull, pmask = 0ull;
   long long rank = q;
+  const unsigned long long* src = keys;  // the candidate keys of this pass
+  long long m = acc;
+  bool in_smem = false;
   const int shifts[6] = {53, 42, 31, 20, 9, 0};
   const int widths[6] = {11, 11, 11, 11, 11, 9};
   for (int p = 0; p < 6; ++p) {
@@ -676,8 +696,8 @@ __global__ void __launch_bounds__(kSelThreads) band_strip_kernel(const uint32_t*
     const unsigned long long dmask = (1ull << widths[p]) - 1ull;
     for (int b = tid; b < 2048; b += kSelThreads) s_hist[b] = 0u;
     __syncthreads();
-    for (int k = tid; k < acc; k += kSelThreads) {
-      const unsigned long long key = keys[k];
+    for (long long k = tid; k < m; k += kSelThreads) {
+      const unsigned long long key = in_smem ? s_keys[k] : src[k];
       if ((key & pmask) == prefix) atomicAdd(&s_hist[(key >> sh) & dmask], 1u);
     }
     __syncthreads();
@@ -696,15 +716,29 @@ __global__ void __launch_bounds__(kSelThreads) band_strip_kernel(const uint32_t*
     if ((long long)before <= rank && rank < (long long)(before + h0)) {
       s_digit = 2 * tid;
       s_before = (long long)before;
+      s_m = (int)h0;
     } else if ((long long)(before + h0) <= rank && rank < (long long)(before + h0 + h1)) {
       s_digit = 2 * tid + 1;
       s_before = (long long)(before + h0);
+      s_m = (int)h1;
     }
     __syncthreads();
     prefix |= (unsigned long long)s_digit << sh;
     pmask |= dmask << sh;
     rank -= s_before;
-    __syncthreads();  // s_digit / s_before / s_wsum reused by the next pass
+    const int left = s_m;  // keys matching the new prefix
+    __syncthreads();
+    if (!in_smem && left <= kSelSmem && p < 5) {  // compact them into shared memory
+      if (tid == 0) s_m = 0;
+      __syncthreads();
+      for (long long k = tid; k < m; k += kSelThreads) {
+        const unsigned long long key = src[k];
+        if ((key & pmask) == prefix) s_keys[atomicAdd(&s_m, 1)] = key;
+      }
+      __syncthreads();
+      m = left;
+      in_smem = true;
+    }
   }
   if (tid == 0) {
     const double v = __longlong_as_double((long long)prefix);
@@ -1053,8 +1087,12 @@ void launch_strip_k(const double* zx, const double* zy, const double* zz, int64_
 void launch_band_strip_k(const uint32_t* band, int64_t n, const double* zx, const double* zy, const double* zz,
                          const double axis[3], long long q, double floor_strip, unsigned long long* keys,
                          double* strip_dev, uint8_t* removed, cudaStream_t s) {
-  band_strip_kernel<<<1, kSelThreads, 0, s>>>(band, n, zx, zy, zz, axis[0], axis[1], axis[2], q, floor_strip, keys,
-                                             strip_dev);
+  // keys[0] counts, keys + 1 holds the keys
+  cudaMemsetAsync(keys, 0, sizeof(unsigned long long), s);
+  const int64_t nw = (n + 31) / 32;
+  band_gather_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, s>>>(band, n, zx, zy, zz, axis[0], axis[1], axis[2],
+                                                                 keys + 1, keys);
+  band_select_kernel<<<1, kSelThreads, 0, s>>>(keys + 1, keys, q, floor_strip, strip_dev);
   strip_dev_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(zx, zy, zz, n, axis[0], axis[1], axis[2], strip_dev,
                                                               removed);
 }
