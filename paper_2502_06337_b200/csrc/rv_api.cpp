@@ -2218,7 +2218,9 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
       est = std::move(ident);
       identity_model = true;
     }
-    if (accepted.duplicate_else_accept(est.inliers, cfg.dedupe_overlap)) break;
+    // the strip (estimator.cpp:470-480) is queued before the host's duplicate test, so the GPU runs
+    // it while the host intersects the inlier bitsets; a duplicate ends the loop and leaves the
+    // strip unused
     if (identity_model) {
       launch_strip_identity_k(d_corrs, pre.cs.kept, pre.cs.n, cfg.normalize_inputs, removed, c->st);
       count_launch(c);
@@ -2240,6 +2242,7 @@ std::vector<Estimate> estimate_multi_dev(rv_context* c, const double* d_corrs, i
         count_launch(c);
       }
     }
+    if (accepted.duplicate_else_accept(est.inliers, cfg.dedupe_overlap)) break;
     out.push_back(std::move(est));
   }
   if (out.empty()) fail(RV_ERR_NO_PEAK, "no peak produced a usable model");
