@@ -397,9 +397,15 @@ __device__ __forceinline__ void exact_global(const double a1[3], const double a2
 // kNB > 0: n_bands <= kNB, entries kept in shared memory and reserved once per (block, band)
 // (same-address global atomics were the planner's bottleneck); kExact: n_bands == kNB (the band
 // loop unrolled); kNB == 0: any band count, one reservation per (warp, band).
-constexpr int kPlanThreads = 256;
+#ifndef RV_PLAN_THREADS
+#define RV_PLAN_THREADS 256
+#endif
+constexpr int kPlanThreads = RV_PLAN_THREADS;
 template <int kNB, bool kExact>
-__global__ void __launch_bounds__(kPlanThreads) plan_kernel(VotePlan p, VoteBuffers b, int64_t n) {
+#ifndef RV_PLAN_MINB
+#define RV_PLAN_MINB 5  // minimum resident plan blocks per SM: 48 registers (A/B: 1 -> 5 saves ~6 us at C3)
+#endif
+__global__ void __launch_bounds__(kPlanThreads, RV_PLAN_MINB) plan_kernel(VotePlan p, VoteBuffers b, int64_t n) {
   constexpr int kWarps = kPlanThreads / 32;
   __shared__ uint32_t s_wcnt[kMaxBands][kWarps], s_wwork[kMaxBands][kWarps];
   __shared__ int s_base[kMaxBands];
