@@ -49,6 +49,9 @@ constexpr float kRcMin = 1e-3f;     // |c| amplitude below which a circle is tre
 #ifndef RV_GRAB_PER
 #define RV_GRAB_PER 4  // target grabs per warp and band below which grabs shrink from 32 entries
 #endif
+#ifndef RV_BAND_ENTRY_W
+#define RV_BAND_ENTRY_W 100  // per-entry cost (in samples) in the initial CTA-to-band split (A/B at C3: 0 -> 100 is -1.8% vote time)
+#endif
 #ifndef RV_TAIL_GRAB
 #define RV_TAIL_GRAB 0
 #endif
@@ -793,13 +796,17 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
 
   if (tid == 0) {  // initial band: CTAs split across bands in proportion to planned work
     unsigned long long total = 0;
-    for (int q = 0; q < p.n_bands; ++q) total += b.band_work[q];
+    // band cost = planned samples + a per-entry overhead in sample equivalents (RV_BAND_ENTRY_W)
+    auto band_cost = [&](int q) -> unsigned long long {
+      return b.band_work[q] + (unsigned long long)RV_BAND_ENTRY_W * (unsigned long long)b.entry_count[q];
+    };
+    for (int q = 0; q < p.n_bands; ++q) total += band_cost(q);
     int band = p.n_bands - 1;
     if (total > 0) {
       const double pos = ((double)blockIdx.x + 0.5) / gridDim.x * (double)total;
       double acc = 0;
       for (int q = 0; q < p.n_bands; ++q) {
-        acc += (double)b.band_work[q];
+        acc += (double)band_cost(q);
         if (pos < acc) {
           band = q;
           break;
