@@ -52,6 +52,9 @@ constexpr float kRcMin = 1e-3f;     // |c| amplitude below which a circle is tre
 #ifndef RV_BAND_ENTRY_W
 #define RV_BAND_ENTRY_W 100  // per-entry cost (in samples) in the initial CTA-to-band split (A/B at C3: 0 -> 100 is -1.8% vote time)
 #endif
+#ifndef RV_STEAL_GRAB
+#define RV_STEAL_GRAB 0  // A/B knob
+#endif
 #ifndef RV_TAIL_GRAB
 #define RV_TAIL_GRAB 0
 #endif
@@ -852,6 +855,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
   const int S = p.frac_shift;
   const uint32_t fmask = p.frac_mask;
 
+  int visit = 0;  // band visits of this CTA so far
   for (;;) {
     // REDUX broadcasts (uniform-register results): the band, its entry count and each grab offset
     // are provably warp-uniform, so the vote loops carry no divergence checks
@@ -880,7 +884,9 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     // grab size: 32 entries when every warp of the launch still gets several grabs, smaller for
     // small problems (otherwise a handful of warps would walk all entries while the rest idle)
     const int per = (int)(((long long)gridDim.x * (kVoteThreads / 32) * RV_GRAB_PER) / p.n_bands);
-    const int grab = max(1, min(32, n_ent / max(per, 1)));
+    // a stolen band (second and later visits) is near its end: small grabs, so the stealer's last
+    // grab does not become the launch's tail (RV_STEAL_GRAB; 0 = the normal size)
+    const int grab = (RV_STEAL_GRAB > 0 && visit > 0) ? RV_STEAL_GRAB : max(1, min(32, n_ent / max(per, 1)));
     // Entries are fetched in per-warp grabs of up to 32 (lane k holds entry k); flagged samples
     // are queued per warp as (constraint, sample) and drained in batches of up to 32.
     uint32_t my_ci = 0, my_enc = 0;
@@ -1069,6 +1075,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     }
     __syncthreads();
     vtrace(3, band);
+    ++visit;
     if (s_band >= 0)
       for (size_t k = tid; k < p.tile_words; k += blockDim.x) tile[k] = 0u;
     __syncthreads();
