@@ -52,12 +52,6 @@ constexpr float kRcMin = 1e-3f;     // |c| amplitude below which a circle is tre
 #ifndef RV_BAND_ENTRY_W
 #define RV_BAND_ENTRY_W 100  // per-entry cost (in samples) in the initial CTA-to-band split (A/B at C3: 0 -> 100 is -1.8% vote time)
 #endif
-#ifndef RV_STEAL_GRAB
-#define RV_STEAL_GRAB 0  // A/B knob
-#endif
-#ifndef RV_TAIL_GRAB
-#define RV_TAIL_GRAB 0
-#endif
 #ifndef RV_RED_GROUPS
 #define RV_RED_GROUPS 2
 #endif
@@ -855,7 +849,6 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
   const int S = p.frac_shift;
   const uint32_t fmask = p.frac_mask;
 
-  int visit = 0;  // band visits of this CTA so far
   for (;;) {
     // REDUX broadcasts (uniform-register results): the band, its entry count and each grab offset
     // are provably warp-uniform, so the vote loops carry no divergence checks
@@ -884,9 +877,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     // grab size: 32 entries when every warp of the launch still gets several grabs, smaller for
     // small problems (otherwise a handful of warps would walk all entries while the rest idle)
     const int per = (int)(((long long)gridDim.x * (kVoteThreads / 32) * RV_GRAB_PER) / p.n_bands);
-    // a stolen band (second and later visits) is near its end: small grabs, so the stealer's last
-    // grab does not become the launch's tail (RV_STEAL_GRAB; 0 = the normal size)
-    const int grab = (RV_STEAL_GRAB > 0 && visit > 0) ? RV_STEAL_GRAB : max(1, min(32, n_ent / max(per, 1)));
+    const int grab = max(1, min(32, n_ent / max(per, 1)));
     // Entries are fetched in per-warp grabs of up to 32 (lane k holds entry k); flagged samples
     // are queued per warp as (constraint, sample) and drained in batches of up to 32.
     uint32_t my_ci = 0, my_enc = 0;
@@ -959,12 +950,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
       }
     };
     // grab loop / entry loop / step loop
-#if RV_TAIL_GRAB
-    int gsz = grab;  // shrinks near the end of the band (from the last grab's position): a finer
-                     // tail, so the CTA's warps reach the band-end barrier closer together
-#else
     const int gsz = grab;
-#endif
     for (;;) {
       g0 = 0;
       if (lane == 0) g0 = atomicAdd(counter, gsz);
@@ -973,9 +959,6 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
       g0 = __reduce_max_sync(0xFFFFFFFFu, g0);
       if (g0 >= n_ent) break;
       ne = min(gsz, n_ent - g0);
-#if RV_TAIL_GRAB
-      gsz = max(1, min(grab, (n_ent - g0 - ne) / max(per, 1)));
-#endif
       my_ci = 0;
       my_enc = 0;
       if (lane < ne) {
@@ -1075,7 +1058,6 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_banded_kernel(VotePlan p
     }
     __syncthreads();
     vtrace(3, band);
-    ++visit;
     if (s_band >= 0)
       for (size_t k = tid; k < p.tile_words; k += blockDim.x) tile[k] = 0u;
     __syncthreads();
