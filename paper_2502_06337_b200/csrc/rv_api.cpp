@@ -517,8 +517,11 @@ void set_fused(rv_context* c, VoteBuffers& b, VoteFused* f, const VotePlan& p) {
 // CTAs of a band-tiled vote launch: one per ~16k planned pairs (a CTA's fixed cost -- clearing and
 // flushing its tile -- is a few microseconds, so even small problems spread over many SMs), at
 // least one per band, at most one per SM.
+#ifndef RV_VOTE_CTA_SHIFT
+#define RV_VOTE_CTA_SHIFT 14  // one vote CTA per 2^shift planned pairs (small problems use fewer CTAs)
+#endif
 int vote_ctas(const rv_context* c, const VotePlan& p, int64_t est_pairs) {
-  return (int)std::clamp<int64_t>(est_pairs >> 14, std::min(p.n_bands, c->sms), c->sms);
+  return (int)std::clamp<int64_t>(est_pairs >> RV_VOTE_CTA_SHIFT, std::min(p.n_bands, c->sms), c->sms);
 }
 
 uint32_t* vote(rv_context* c, const double* zx, const double* zy, const double* zz, int64_t n, int G, double E,

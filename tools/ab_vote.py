@@ -1,6 +1,6 @@
 """Dev A/B of vote-kernel variants on one B200: each argument is a library built by
 `RV_NVCC_EXTRA=... RV_LIB_OUT=_variants/<name> python paper_2502_06337_b200/build.py --force`.
-Runs C3 device solves with per-stage timers in a fresh process per (variant, round), variants
+Runs C3 (AB_CONFIG) device solves with per-stage timers in a fresh process per (variant, round), variants
 interleaved over rounds; prints the median vote-kernel time and device solve time per variant."""
 import json
 import os
@@ -11,11 +11,11 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 CHILD = r"""
-import sys, json, torch
+import os, sys, json, torch
 sys.path.insert(0, %r)
 import paper_2502_06337_b200 as rv
 from paper_2502_06337_b200 import synth
-corrs, _, _ = synth.make_config("c3")
+corrs, _, _ = synth.make_config(os.environ.get("AB_CONFIG", "c3"))
 ctx = rv.Context(0)
 d = torch.from_numpy(corrs).cuda()
 cfg = rv.EstimatorConfig()
