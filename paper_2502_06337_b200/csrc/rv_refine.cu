@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(kSelThreads) band_select_kernel(const unsigned
     return;
   }
   unsigned long long prefix = 0ull, pmask = 0ull;
-  long long rank = q;
+  long long rank = q < acc ? q : acc - 1;  // (q < acc by construction: the host's band size)
   const unsigned long long* src = keys;  // the candidate keys of this pass
   long long m = acc;
   bool in_smem = false;
