@@ -191,10 +191,15 @@ def sharded_estimate_single(shard: torch.Tensor, n_total: int, cfg, backend, gro
     dev = _comm_device(backend, group)
     lo, _ = shard_bounds(n_total, world, rank)
     grid, kept = backend.vote_shard(shard, cfg)
-    _all_reduce_(grid, group)  # int32 wrap-around == uint32 sum
-    kept_t = torch.tensor([kept], dtype=torch.int64, device=dev)
-    dist.all_reduce(kept_t, group=group)
-    n_kept = int(kept_t.item())
+    # ONE all-reduce carries the grid and the kept count (an extra int32 word: int32 wrap-around ==
+    # uint32 sum for the grid; the total kept count is < 2^31)
+    cells = grid.numel()
+    buf = torch.empty(cells + 1, dtype=torch.int32, device=grid.device)
+    buf[:cells].copy_(grid.reshape(-1))
+    buf[cells] = int(kept)
+    _all_reduce_(buf, group)
+    grid = buf[:cells].view(grid.shape)
+    n_kept = int(buf[cells].item())
     mode = "sharded"
     if stats is not None:
         stats["mode"] = mode
@@ -268,14 +273,14 @@ def _sharded_build(shard, n_total, cfg, backend, group, axis, counts, slot, lo, 
     local = backend.inliers(slot, lo, int(counts[rank]))
     inliers = _gather_i32_varlen(local, counts, dev, group)
     bins, contrib = backend.angle_hist(axis, cfg)
-    bins_t = torch.as_tensor(bins.astype(np.int64), device=dev)
+    # ONE all-reduce for the angle histogram and the contributing count (last element)
+    bins_t = torch.as_tensor(np.append(bins.astype(np.int64), np.int64(contrib)), device=dev)
     dist.all_reduce(bins_t, group=group)
-    contrib_t = torch.tensor([contrib], dtype=torch.int64, device=dev)
-    dist.all_reduce(contrib_t, group=group)
-    if int(contrib_t.item()) == 0:
+    summed = bins_t.cpu().numpy()
+    if int(summed[-1]) == 0:
         from paper_2502_06337_b200.errors import NoVotes
         raise NoVotes("no correspondence produced an angle vote")
-    hist = bins_t.cpu().numpy().astype(np.uint32)
+    hist = summed[:-1].astype(np.uint32)
     peak = int(np.argmax(hist))  # first maximum (angles.cpp:70-90)
     w = 2.0 * math.pi / cfg.angle_bins
     angle = -math.pi + (peak + 0.5) * w
