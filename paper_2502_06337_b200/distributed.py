@@ -225,8 +225,6 @@ def sharded_estimate_single(shard: torch.Tensor, n_total: int, cfg, backend, gro
     if hasattr(backend, "device_refine") and backend.peer_refine_ready(group):
         # device-resident refine_loop: one cooperative loop per rank, partials through peer memory
         axis, total_count, local, passes = backend.device_refine(axis, cfg, group)
-        counts = _gather_f64([float(local)], dev, group)[:, 0].astype(np.int64)
-        assert int(counts.sum()) == total_count
         if cfg.refine and total_count < 3.0 * (cfg.epsilon * n_kept):  # rescue (estimator.cpp:352-368)
             if stats is not None:
                 stats["mode"] = "replicated:rescue"
@@ -234,8 +232,9 @@ def sharded_estimate_single(shard: torch.Tensor, n_total: int, cfg, backend, gro
         if stats is not None:
             stats["mode"] = "sharded:device"
             stats["passes"] = passes
-        return _sharded_build(shard, n_total, cfg, backend, group, axis, counts, 0, lo, world, rank, dev, stats,
-                              votes)
+        # the shard counts ride the angle-histogram all-reduce (no separate gather)
+        return _sharded_build(shard, n_total, cfg, backend, group, axis, None, 0, lo, world, rank, dev, stats,
+                              votes, local_count=int(local), total_count=int(total_count))
     counts, _, s6 = classify(axis, slot, False)
     passes = 0
     if cfg.refine:
@@ -264,23 +263,35 @@ def sharded_estimate_single(shard: torch.Tensor, n_total: int, cfg, backend, gro
                           votes)
 
 
-def _sharded_build(shard, n_total, cfg, backend, group, axis, counts, slot, lo, world, rank, dev, stats, votes):
+def _sharded_build(shard, n_total, cfg, backend, group, axis, counts, slot, lo, world, rank, dev, stats, votes,
+                   local_count=None, total_count=None):
     """build_estimate (estimator.cpp:73-92) over the shards: the rank-ordered concatenation of the
     shard inlier lists is the reference's ascending list; the angle histograms are summed and
-    peak_angle's window sums around the summed peak are summed in rank order."""
+    peak_angle's window sums around the summed peak are summed in rank order. `counts` (every
+    shard's inlier count) may be None: then each rank's own count travels in the histogram's
+    all-reduce (one-hot slot per rank), which the inlier gather needs first."""
     from paper_2502_06337_b200 import RotationEstimate
 
-    local = backend.inliers(slot, lo, int(counts[rank]))
-    inliers = _gather_i32_varlen(local, counts, dev, group)
+    mine = int(counts[rank]) if counts is not None else int(local_count)
+    local = backend.inliers(slot, lo, mine)  # compacts this shard's inliers (the angle vote's input)
     bins, contrib = backend.angle_hist(axis, cfg)
-    # ONE all-reduce for the angle histogram and the contributing count (last element)
-    bins_t = torch.as_tensor(np.append(bins.astype(np.int64), np.int64(contrib)), device=dev)
+    # ONE all-reduce: the angle histogram, the contributing count, and the shard counts
+    extra = np.zeros(1 + world, np.int64)
+    extra[0] = contrib
+    extra[1 + rank] = mine
+    bins_t = torch.as_tensor(np.concatenate([bins.astype(np.int64), extra]), device=dev)
     dist.all_reduce(bins_t, group=group)
     summed = bins_t.cpu().numpy()
-    if int(summed[-1]) == 0:
+    nb = len(bins)
+    if counts is None:
+        counts = summed[nb + 1:].astype(np.int64)
+        if total_count is not None:
+            assert int(counts.sum()) == total_count
+    inliers = _gather_i32_varlen(local, counts, dev, group)
+    if int(summed[nb]) == 0:
         from paper_2502_06337_b200.errors import NoVotes
         raise NoVotes("no correspondence produced an angle vote")
-    hist = summed[:-1].astype(np.uint32)
+    hist = summed[:nb].astype(np.uint32)
     peak = int(np.argmax(hist))  # first maximum (angles.cpp:70-90)
     w = 2.0 * math.pi / cfg.angle_bins
     angle = -math.pi + (peak + 0.5) * w
