@@ -50,7 +50,7 @@ constexpr float kRcMin = 1e-3f;     // |c| amplitude below which a circle is tre
 #define RV_GRAB_PER 4  // target grabs per warp and band below which grabs shrink from 32 entries
 #endif
 #ifndef RV_BAND_ENTRY_W
-#define RV_BAND_ENTRY_W 100  // per-entry cost (in samples) in the initial CTA-to-band split (A/B at C3: 0 -> 100 is -1.8% vote time)
+#define RV_BAND_ENTRY_W 110  // per-entry cost (in samples) in the initial CTA-to-band split (A/B: 0 -> 110 is -1.8% vote time at C3, -0.8% at C4)
 #endif
 #ifndef RV_RED_GROUPS
 #define RV_RED_GROUPS 2
